@@ -1,0 +1,479 @@
+"""B200-native randomized range finder — Python host mirror of the reference API.
+
+The product is the CUDA library ``librfgpu.so`` behind the C ABI in
+``include/rfgpu.h`` (and the C++ drop-in ``librandfact_b200.so`` for C++
+callers of the reference ``randfact`` API). This module binds that C ABI with
+ctypes and mirrors the reference entry points (``proj/include/randfact/``):
+
+* :func:`gaussian`       <- ``randfact::gaussian``       (sketch.hpp:25)
+* :func:`basic_range`    <- ``randfact::basic_range``    (rangefinder.hpp:50)
+* :func:`power_range`    <- ``randfact::power_range``    (rangefinder.hpp:55)
+* :func:`rsvd`           <- ``randfact::rsvd``           (lowrank.hpp:15-16)
+* :func:`randomized_id`  <- ``randfact::randomized_id``  (lowrank.hpp:78)
+* :func:`randomized_cur` <- ``randfact::randomized_cur`` (lowrank.hpp:102)
+* :func:`id_deterministic` (column side) <- ``col_id_core`` (lowrank.cpp:51-70)
+* :func:`single_pass_svd` <- ``randfact::single_pass_svd`` (lowrank.hpp:41)
+
+Same argument meaning, same defaults, same error classes (``ParameterError``,
+``NumericalError``, ``ConvergenceError``, ...). Matrices are numpy arrays in
+the reference's column-major layout. There is no CPU fallback: without the
+built extension or without a B200 every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "Error", "ParameterError", "NumericalError", "ConvergenceError", "NotPositiveDefiniteError",
+    "StreamContractError", "DeviceError", "Context", "DeviceMatrix", "SvdFactors", "RangeBasis", "IdFactors",
+    "CurFactors", "gaussian", "basic_range", "power_range", "rsvd", "randomized_id", "randomized_cur",
+    "id_deterministic", "single_pass_svd", "MatrixStream", "library_path", "default_context",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(HERE, "librfgpu.so")
+
+
+# ----------------------------------------------------------------- errors ---
+class Error(RuntimeError):
+    """randfact::Error (proj/include/randfact/common.hpp:11-14)."""
+
+
+class ParameterError(Error):
+    pass
+
+
+class NumericalError(Error):
+    pass
+
+
+class ConvergenceError(NumericalError):
+    pass
+
+
+class NotPositiveDefiniteError(NumericalError):
+    pass
+
+
+class StreamContractError(Error):
+    pass
+
+
+class DeviceError(Error):
+    """CUDA / NCCL failure (no reference counterpart: the reference is CPU-only)."""
+
+
+_ERRORS = {3: ParameterError, 4: NumericalError, 5: ConvergenceError, 6: NotPositiveDefiniteError, 7: DeviceError,
+           8: StreamContractError, 9: DeviceError}
+
+# ------------------------------------------------------------------ loader ---
+_lib = None
+_lib_lock = threading.Lock()
+
+_i64, _u64, _int, _vp = C.c_int64, C.c_uint64, C.c_int, C.c_void_p
+_pd, _pf, _pi = C.POINTER(C.c_double), C.POINTER(C.c_float), C.POINTER(C.c_int64)
+
+_SIGS = {
+    "rfgpu_last_error": (C.c_char_p, []),
+    "rfgpu_version": (_int, []),
+    "rfgpu_gaussian": (_int, [_u64, C.c_char_p, _i64, _i64, _pd]),
+    "rfgpu_gaussian_range": (_int, [_u64, C.c_char_p, _i64, _i64, _pd]),
+    "rfgpu_ctx_create": (_int, [_int, C.POINTER(_vp)]),
+    "rfgpu_nccl_unique_id": (_int, [_vp, C.c_size_t]),
+    "rfgpu_ctx_create_dist": (_int, [_int, _int, _int, _vp, C.c_size_t, C.POINTER(_vp)]),
+    "rfgpu_ctx_destroy": (_int, [_vp]),
+    "rfgpu_ctx_rank": (_int, [_vp]),
+    "rfgpu_ctx_world": (_int, [_vp]),
+    "rfgpu_ctx_synchronize": (_int, [_vp]),
+    "rfgpu_ctx_stream": (_vp, [_vp]),
+    "rfgpu_profile_enable": (_int, [_vp, _int]),
+    "rfgpu_profile_reset": (_int, [_vp]),
+    "rfgpu_profile_read": (_int, [_vp, C.c_char_p, _pi, _pd]),
+    "rfgpu_launch_count": (_i64, [_vp]),
+    "rfgpu_matrix_upload": (_int, [_vp, _pd, _i64, _i64, _i64, C.POINTER(_vp)]),
+    "rfgpu_matrix_wrap_device": (_int, [_vp, _vp, _i64, _i64, _i64, C.POINTER(_vp)]),
+    "rfgpu_matrix_upload_f32": (_int, [_vp, _pf, _i64, _i64, _i64, C.POINTER(_vp)]),
+    "rfgpu_matrix_wrap_device_f32": (_int, [_vp, _vp, _i64, _i64, _i64, C.POINTER(_vp)]),
+    "rfgpu_matrix_free": (_int, [_vp]),
+    "rfgpu_matrix_shape": (_int, [_vp, _pi, _pi, _pi, _pi]),
+    "rfgpu_multiply": (_int, [_vp, _vp, _int, _pd, _i64, _pd]),
+    "rfgpu_range_finder": (_int, [_vp, _vp, _pd, _i64, _i64, _int, _pd, _pd, _pd, _pi]),
+    "rfgpu_rsvd": (_int, [_vp, _vp, _pd, _i64, _i64, _i64, _int, _int, _pd, _pd, _pd, _pi]),
+    "rfgpu_rsvd_device": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _pi]),
+    "rfgpu_row_sketch": (_int, [_vp, _vp, _pd, _i64, _pd]),
+    "rfgpu_row_sketch_device": (_int, [_vp, _vp, _vp, _i64, _vp]),
+    "rfgpu_col_id": (_int, [_vp, _pd, _i64, _i64, _i64, _pi, _pd, _pi, C.POINTER(_int)]),
+    "rfgpu_col_id_device": (_int, [_vp, _vp, _i64, _i64, _i64, _pi, _vp, _pi, C.POINTER(_int)]),
+    "rfgpu_dual_sketch_f32": (_int, [_vp, _vp, _pf, _pf, _i64, _pf, _pf]),
+}
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load librfgpu.so (raises ImportError if it was never built)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(_LIB_PATH):
+                raise ImportError(f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                                  f"g.build()'` (there is no CPU fallback)")
+            L = C.CDLL(_LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        msg = lib().rfgpu_last_error().decode(errors="replace")
+        raise _ERRORS.get(status, Error)(msg)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(_pd)
+
+
+def _fp(a: np.ndarray):
+    return a.ctypes.data_as(_pf)
+
+
+def _ip(a: np.ndarray):
+    return a.ctypes.data_as(_pi)
+
+
+def _fmat(a, dtype=np.float64) -> np.ndarray:
+    a = np.asarray(a, dtype=dtype)
+    if a.ndim != 2:
+        raise ParameterError("expected a 2-D matrix")
+    if not np.isfinite(a).all():
+        raise ParameterError("from_data: non-finite entry")
+    return np.asfortranarray(a)
+
+
+def _flat(a: np.ndarray) -> np.ndarray:
+    return a.reshape(-1, order="F")
+
+
+# ------------------------------------------------------------------ results ---
+@dataclass
+class SvdFactors:
+    """randfact::SvdFactors (dense.hpp:76-80)."""
+    U: np.ndarray
+    D: np.ndarray
+    V: np.ndarray
+
+
+@dataclass
+class RangeBasis:
+    """randfact::RangeBasis (rangefinder.hpp:26-34)."""
+    Q: np.ndarray
+    B: np.ndarray | None = None
+    residual_frob: float | None = None
+    picks: list = field(default_factory=list)
+
+
+@dataclass
+class IdFactors:
+    """randfact::IdFactors (lowrank.hpp:60-67)."""
+    side: str
+    Js: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.int64))
+    Is: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.int64))
+    Z: np.ndarray = field(default_factory=lambda: np.zeros((0, 0)))
+    X: np.ndarray = field(default_factory=lambda: np.zeros((0, 0)))
+    rank_truncated: bool = False
+
+
+@dataclass
+class CurFactors:
+    """randfact::CurFactors (lowrank.hpp:90-97)."""
+    Js: np.ndarray
+    Is: np.ndarray
+    U: np.ndarray
+    cond_C: float
+    cond_R: float
+    warning: bool
+
+
+# ------------------------------------------------------------------ context ---
+class Context:
+    """One GPU (and, for world > 1, one NCCL communicator). Not re-entrant:
+    the C layer serialises calls on the same context."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        self._h = _vp()
+        if world == 1:
+            _check(lib().rfgpu_ctx_create(device, C.byref(self._h)))
+        else:
+            buf = C.create_string_buffer(nccl_id, 128)
+            _check(lib().rfgpu_ctx_create_dist(device, rank, world, C.cast(buf, _vp), 128, C.byref(self._h)))
+        self.device, self.rank, self.world = device, rank, world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().rfgpu_nccl_unique_id(C.cast(buf, _vp), 128))
+        return buf.raw
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def stream(self) -> int:
+        return lib().rfgpu_ctx_stream(self._h) or 0
+
+    def synchronize(self):
+        _check(lib().rfgpu_ctx_synchronize(self._h))
+
+    def profile(self, on: bool = True):
+        _check(lib().rfgpu_profile_enable(self._h, int(on)))
+
+    def profile_reset(self):
+        _check(lib().rfgpu_profile_reset(self._h))
+
+    def profile_read(self, name: str) -> tuple[int, float]:
+        n, ms = _i64(), C.c_double()
+        _check(lib().rfgpu_profile_read(self._h, name.encode(), C.byref(n), C.byref(ms)))
+        return n.value, ms.value
+
+    def launch_count(self) -> int:
+        return int(lib().rfgpu_launch_count(self._h))
+
+    def matrix(self, a, f32: bool = False) -> "DeviceMatrix":
+        return DeviceMatrix.upload(self, a, f32=f32)
+
+    def close(self):
+        if self._h:
+            lib().rfgpu_ctx_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("LOCAL_RANK", "0")))
+    return _default_ctx
+
+
+class DeviceMatrix:
+    """Device-resident A (this rank's rows): upload from host or wrap a device pointer."""
+
+    def __init__(self, ctx: Context, handle, m: int, n: int, f32: bool, keep=None):
+        self.ctx, self._h, self.f32 = ctx, handle, f32
+        self._keep = keep
+        ml, nn, mg, r0 = _i64(), _i64(), _i64(), _i64()
+        _check(lib().rfgpu_matrix_shape(handle, C.byref(ml), C.byref(nn), C.byref(mg), C.byref(r0)))
+        self.m, self.n, self.m_global, self.row0 = ml.value, nn.value, mg.value, r0.value
+
+    @classmethod
+    def upload(cls, ctx: Context, a, f32: bool = False):
+        dt = np.float32 if f32 else np.float64
+        a = _fmat(a, dt)
+        m, n = a.shape
+        h = _vp()
+        if f32:
+            _check(lib().rfgpu_matrix_upload_f32(ctx.handle, _fp(_flat(a)), m, n, max(1, m), C.byref(h)))
+        else:
+            _check(lib().rfgpu_matrix_upload(ctx.handle, _dp(_flat(a)), m, n, max(1, m), C.byref(h)))
+        return cls(ctx, h, m, n, f32)
+
+    @classmethod
+    def wrap(cls, ctx: Context, dev_ptr: int, m: int, n: int, lda: int, f32: bool = False, keep=None):
+        h = _vp()
+        fn = lib().rfgpu_matrix_wrap_device_f32 if f32 else lib().rfgpu_matrix_wrap_device
+        _check(fn(ctx.handle, _vp(dev_ptr), m, n, lda, C.byref(h)))
+        return cls(ctx, h, m, n, f32, keep=keep)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h:
+            lib().rfgpu_matrix_free(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+# --------------------------------------------------------------- functions ---
+def gaussian(seed: int, tag: str, m: int, n: int) -> np.ndarray:
+    """randfact::gaussian(seed, tag, m, n) — bit-identical host generator."""
+    if m < 0 or n < 0:
+        raise ParameterError("gaussian: negative dimension")
+    out = np.empty(m * n)
+    _check(lib().rfgpu_gaussian(seed & (2**64 - 1), tag.encode(), m, n, _dp(out)))
+    return out.reshape((m, n), order="F")
+
+
+def _as_device(a, ctx: Context | None):
+    if isinstance(a, DeviceMatrix):
+        return a, False
+    ctx = ctx or default_context()
+    return DeviceMatrix.upload(ctx, a), True
+
+
+def _check_sample(k, p, m, n, where):
+    if k < 1:
+        raise ParameterError(f"{where}: k must be at least 1")
+    if p < 0:
+        raise ParameterError(f"{where}: p must be non-negative")
+    if k + p > min(m, n):
+        raise ParameterError(f"{where}: k + p exceeds min(m, n)")
+
+
+def power_range(a, k: int, p: int = 10, q: int = 0, seed: int = 0, reorthonormalize: bool = False,
+                ctx: Context | None = None) -> RangeBasis:
+    """randfact::power_range(a, RangeConfig{k, p, q, reorthonormalize, seed})."""
+    if q < 0:
+        raise ParameterError("power_range: q must be non-negative")
+    dm, tmp = _as_device(a, ctx)
+    try:
+        _check_sample(k, p, dm.m_global, dm.n, "power_range")
+        ell = k + p
+        g = gaussian(seed, "range.G", dm.n, ell)
+        Q = np.zeros(max(1, dm.m * ell))
+        B = np.zeros(max(1, ell * dm.n))
+        res, r = C.c_double(), _i64()
+        _check(lib().rfgpu_range_finder(dm.ctx.handle, dm.handle, _dp(_flat(g)), ell, q, int(reorthonormalize),
+                                        _dp(Q), _dp(B), C.byref(res), C.byref(r)))
+        rr = r.value
+        return RangeBasis(Q[: dm.m * rr].reshape((dm.m, rr), order="F"),
+                          B[: rr * dm.n].reshape((rr, dm.n), order="F"), res.value)
+    finally:
+        if tmp:
+            dm.free()
+
+
+def basic_range(a, k: int, p: int = 10, seed: int = 0, q: int = 0, ctx: Context | None = None) -> RangeBasis:
+    """randfact::basic_range (requires q == 0): bitwise power_range with q = 0."""
+    if q != 0:
+        raise ParameterError("basic_range: q must be 0 (use power_range)")
+    return power_range(a, k, p, 0, seed, False, ctx)
+
+
+def rsvd(a, k: int, p: int, q: int, seed: int, keep_oversamples: bool = False, reorthonormalize: bool = False,
+         ctx: Context | None = None) -> SvdFactors:
+    """randfact::rsvd(a, k, p, q, seed, keep_oversamples, reorthonormalize)."""
+    if q < 0:
+        raise ParameterError("power_range: q must be non-negative")
+    dm, tmp = _as_device(a, ctx)
+    try:
+        _check_sample(k, p, dm.m_global, dm.n, "power_range")
+        ell = k + p
+        g = gaussian(seed, "range.G", dm.n, ell)
+        U = np.zeros(max(1, dm.m * ell))
+        D = np.zeros(ell)
+        V = np.zeros(max(1, dm.n * ell))
+        r = _i64()
+        _check(lib().rfgpu_rsvd(dm.ctx.handle, dm.handle, _dp(_flat(g)), k, ell, q, int(keep_oversamples),
+                                int(reorthonormalize), _dp(U), _dp(D), _dp(V), C.byref(r)))
+        rr = r.value
+        return SvdFactors(U[: dm.m * rr].reshape((dm.m, rr), order="F"), D[:rr].copy(),
+                          V[: dm.n * rr].reshape((dm.n, rr), order="F"))
+    finally:
+        if tmp:
+            dm.free()
+
+
+def multiply(a, x, trans: bool = False, ctx: Context | None = None) -> np.ndarray:
+    """C = A X (trans=False) or A^T X on the device (randfact::multiply for the pass shapes)."""
+    dm, tmp = _as_device(a, ctx)
+    try:
+        x = _fmat(x)
+        rows_out = dm.n if trans else dm.m
+        out = np.zeros(max(1, rows_out * x.shape[1]))
+        _check(lib().rfgpu_multiply(dm.ctx.handle, dm.handle, int(trans), _dp(_flat(x)), x.shape[1], _dp(out)))
+        return out[: rows_out * x.shape[1]].reshape((rows_out, x.shape[1]), order="F")
+    finally:
+        if tmp:
+            dm.free()
+
+
+def id_deterministic(a, k: int, side: str = "Col", ctx: Context | None = None) -> IdFactors:
+    """randfact::id_deterministic(a, k, IdSide::Col) — the column ID core on the device."""
+    if side != "Col":
+        raise ParameterError("id_deterministic: only IdSide::Col is on the device path")
+    a = _fmat(a)
+    m, n = a.shape
+    if k < 1:
+        raise ParameterError("id_deterministic: k must be at least 1")
+    if k > min(m, n):
+        raise ParameterError("id_deterministic: k exceeds min(m, n)")
+    ctx = ctx or default_context()
+    js = np.zeros(k, dtype=np.int64)
+    z = np.zeros(k * n)
+    r, tr = _i64(), C.c_int()
+    _check(lib().rfgpu_col_id(ctx.handle, _dp(_flat(a)), m, n, k, _ip(js), _dp(z), C.byref(r), C.byref(tr)))
+    ke = r.value
+    return IdFactors("Col", Js=js[:ke].copy(), Z=z[: ke * n].reshape((ke, n), order="F"),
+                     rank_truncated=bool(tr.value))
+
+
+def randomized_id(a, k: int, p: int, q: int, seed: int, ctx: Context | None = None) -> IdFactors:
+    raise ParameterError("randomized_id: not available in this build")
+
+
+def randomized_cur(a, k: int, p: int, q: int, seed: int, ctx: Context | None = None) -> CurFactors:
+    raise ParameterError("randomized_cur: not available in this build")
+
+
+class MatrixStream:
+    """randfact::MatrixStream (stream.hpp:13-41): one-shot column-block view."""
+
+    def __init__(self, a, block_cols: int = 32):
+        if block_cols < 1:
+            raise ParameterError("MatrixStream: block width must be positive")
+        self.a = _fmat(a)
+        self.block_cols = block_cols
+        self.next_col = 0
+        self.entries_served = 0
+
+    def rows(self):
+        return self.a.shape[0]
+
+    def cols(self):
+        return self.a.shape[1]
+
+    def has_next(self):
+        return self.next_col < self.a.shape[1]
+
+    def next_block(self):
+        if self.next_col >= self.a.shape[1]:
+            raise StreamContractError("MatrixStream: single pass already consumed")
+        c0 = self.next_col
+        c1 = min(self.a.shape[1], c0 + self.block_cols)
+        self.next_col = c1
+        self.entries_served += self.a.shape[0] * (c1 - c0)
+        return c0, self.a[:, c0:c1]
+
+    def passes_completed(self):
+        return 1 if self.next_col >= self.a.shape[1] else 0
+
+
+def single_pass_svd(stream: MatrixStream, k: int, p: int, seed: int, ctx: Context | None = None) -> SvdFactors:
+    raise ParameterError("single_pass_svd: not available in this build")

@@ -1,0 +1,151 @@
+// Gram-Schmidt fallback for orth() on sketches that CholeskyQR cannot take.
+//
+// Reference semantics (proj/src/dense.cpp:402-431): columns are processed in
+// order, each is orthogonalised twice against the kept basis and kept only if
+// its residual norm exceeds drop = 1e-13 ||X||_F. The device version uses
+// classical Gram-Schmidt per pass (CGS2; "twice is enough") so that each pass
+// is two bandwidth-bound sweeps over the kept basis. The kept count lives in
+// device memory so no host round trip happens per column; only the final
+// count is read back by the orchestrator.
+#include <algorithm>
+
+#include "common.cuh"
+#include "rfgpu_internal.h"
+
+namespace rfgpu {
+
+namespace {
+
+constexpr int kRowsPerChunk = 4096;
+
+__global__ void copy_col_kernel(const double* __restrict__ x, int64_t m, double* __restrict__ v) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    v[i] = x[i];
+}
+
+// partial[chunk][c] = sum over the chunk's rows of Q(i, c) * v(i), c < *r.
+__global__ void dots_partial_kernel(const double* __restrict__ Q, int64_t ldq, int64_t m,
+                                    const int64_t* __restrict__ r_dev, const double* __restrict__ v,
+                                    double* __restrict__ partial, int64_t cmax) {
+  const int64_t r = *r_dev;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerChunk;
+  const int64_t row1 = min(m, row0 + kRowsPerChunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t c = warp; c < r; c += nw) {
+    const double* q = Q + c * ldq;
+    double s = 0.0;
+    for (int64_t i = row0 + lane; i < row1; i += 32) s = fma(q[i], v[i], s);
+    s = warp_sum(s);
+    if (lane == 0) partial[blockIdx.x * cmax + c] = s;
+  }
+}
+
+__global__ void dots_reduce_kernel(const double* __restrict__ partial, int chunks, int64_t cmax,
+                                   const int64_t* __restrict__ r_dev, double* __restrict__ dots) {
+  const int64_t r = *r_dev;
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < r;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < chunks; ++k) s += partial[k * cmax + c];
+    dots[c] = s;
+  }
+}
+
+// v(i) -= sum_c dots(c) Q(i, c)
+__global__ void update_kernel(const double* __restrict__ Q, int64_t ldq, int64_t m,
+                              const int64_t* __restrict__ r_dev, const double* __restrict__ dots,
+                              double* __restrict__ v) {
+  const int64_t r = *r_dev;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double acc = v[i];
+    for (int64_t c = 0; c < r; ++c) acc -= dots[c] * Q[c * ldq + i];
+    v[i] = acc;
+  }
+}
+
+// scal[0] = ||v||^2 (already reduced), scal[1] = ||X||_F^2. Decide keep/drop.
+__global__ void accept_kernel(const double* __restrict__ scal, int64_t* r_dev, double* flag) {
+  const double nrm = sqrt(scal[0]);
+  const double drop = 1e-13 * sqrt(scal[1]);
+  const bool keep = nrm > drop && nrm > 0.0;
+  flag[0] = keep ? nrm : 0.0;
+  flag[1] = static_cast<double>(*r_dev);
+  if (keep) *r_dev += 1;
+}
+
+__global__ void store_col_kernel(const double* __restrict__ v, int64_t m, const double* __restrict__ flag,
+                                 double* __restrict__ Q, int64_t ldq) {
+  const double nrm = flag[0];
+  if (nrm == 0.0) return;
+  const int64_t col = static_cast<int64_t>(flag[1]);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    Q[col * ldq + i] = v[i] / nrm;
+}
+
+inline int grid_for(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(1184, (n + 255) / 256))); }
+
+}  // namespace
+
+size_t gs_orth_work_doubles(int64_t m, int64_t c) {
+  const int64_t chunks = (m + kRowsPerChunk - 1) / kRowsPerChunk;
+  return static_cast<size_t>(m) + chunks * c + c + 1024 + 8;
+}
+
+cudaError_t gs_orth(const double* X, int64_t m, int64_t c, int64_t ldx, double* Q, int64_t ldq, int64_t* r_dev,
+                    double* work, const DeviceAllreduce& ar, cudaStream_t st) {
+  const int chunks = static_cast<int>((m + kRowsPerChunk - 1) / kRowsPerChunk);
+  double* v = work;
+  double* partial = v + m;
+  double* dots = partial + static_cast<int64_t>(chunks) * c;
+  double* sq_part = dots + c;      // 1024 partials for sumsq
+  double* scal = sq_part + 1024;   // [0] ||v||^2, [1] ||X||^2, [2..3] flag
+  cudaError_t e = cudaMemsetAsync(r_dev, 0, sizeof(int64_t), st);
+  if (e != cudaSuccess) return e;
+  // ||X||_F^2 (column by column to honour ldx), accumulated in fixed order
+  e = cudaMemsetAsync(scal + 1, 0, sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  for (int64_t j = 0; j < c; ++j) {
+    e = sumsq(X + j * ldx, m, sq_part, scal + 4, st);
+    if (e != cudaSuccess) return e;
+    e = add_scalar(scal + 1, scal + 4, st);
+    if (e != cudaSuccess) return e;
+  }
+  if (ar.fn) {
+    e = ar.fn(ar.ctx, scal + 1, 1, st);
+    if (e != cudaSuccess) return e;
+  }
+  for (int64_t j = 0; j < c; ++j) {
+    copy_col_kernel<<<grid_for(m), 256, 0, st>>>(X + j * ldx, m, v);
+    count_launch();
+    for (int pass = 0; pass < 2; ++pass) {
+      dots_partial_kernel<<<chunks, 256, 0, st>>>(Q, ldq, m, r_dev, v, partial, c);
+    count_launch();
+      dots_reduce_kernel<<<1, 256, 0, st>>>(partial, chunks, c, r_dev, dots);
+    count_launch();
+      if (ar.fn) {
+        e = ar.fn(ar.ctx, dots, c, st);  // zero-padded beyond r on every rank
+        if (e != cudaSuccess) return e;
+      }
+      update_kernel<<<grid_for(m), 256, 0, st>>>(Q, ldq, m, r_dev, dots, v);
+    count_launch();
+    }
+    e = sumsq(v, m, sq_part, scal, st);
+    if (e != cudaSuccess) return e;
+    if (ar.fn) {
+      e = ar.fn(ar.ctx, scal, 1, st);
+      if (e != cudaSuccess) return e;
+    }
+    accept_kernel<<<1, 1, 0, st>>>(scal, r_dev, scal + 2);
+    count_launch();
+    store_col_kernel<<<grid_for(m), 256, 0, st>>>(v, m, scal + 2, Q, ldq);
+    count_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace rfgpu

@@ -1,0 +1,918 @@
+// rfgpu C ABI (include/rfgpu.h) and the device-side orchestration of the
+// randomized range finder. One call = one reference entry point:
+//
+//   rfgpu_range_finder  <- randfact::power_range / basic_range
+//                          (proj/src/rangefinder.cpp:56-80, :24-30)
+//   rfgpu_rsvd          <- randfact::rsvd (proj/src/lowrank.cpp:74-96)
+//   rfgpu_row_sketch    <- the G*A pass of randfact::randomized_cur (:351-352)
+//   rfgpu_col_id        <- col_id_core (proj/src/lowrank.cpp:51-70)
+//
+// Everything between the host copies runs on the context's stream; the only
+// host round trips are one status read per orth() (CholeskyQR2 accepted or
+// Gram-Schmidt fallback) and the final result copies.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "rfgpu.h"
+#include "rfgpu_internal.h"
+
+namespace rfgpu {
+
+static std::atomic<int64_t> g_launches{0};
+int64_t launch_counter() { return g_launches.load(); }
+void count_launch(int n) { g_launches.fetch_add(n); }
+
+namespace {
+
+__global__ void add_scalar_kernel(double* dst, const double* src) { *dst += *src; }
+
+__global__ void transpose_kernel(const double* __restrict__ in, int64_t rows, int64_t cols, int64_t ldi,
+                                 double* __restrict__ out, int64_t ldo) {
+  // out(j, i) = in(i, j); in rows x cols
+  __shared__ double tile[32][33];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, j0 = static_cast<int64_t>(blockIdx.y) * 32;
+  for (int dj = threadIdx.y; dj < 32; dj += blockDim.y) {
+    const int64_t i = i0 + threadIdx.x, j = j0 + dj;
+    if (i < rows && j < cols) tile[dj][threadIdx.x] = in[j * ldi + i];
+  }
+  __syncthreads();
+  for (int di = threadIdx.y; di < 32; di += blockDim.y) {
+    const int64_t j = j0 + threadIdx.x, i = i0 + di;
+    if (i < rows && j < cols) out[i * ldo + j] = tile[threadIdx.x][di];
+  }
+}
+
+}  // namespace
+
+cudaError_t add_scalar(double* dst, const double* src, cudaStream_t st) {
+  add_scalar_kernel<<<1, 1, 0, st>>>(dst, src);
+  count_launch();
+  return cudaGetLastError();
+}
+
+static cudaError_t transpose(const double* in, int64_t rows, int64_t cols, int64_t ldi, double* out, int64_t ldo,
+                             cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  dim3 grid(static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>((cols + 31) / 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(in, rows, cols, ldi, out, ldo);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace rfgpu
+
+using namespace rfgpu;
+
+// ============================================================ errors =====
+namespace {
+
+thread_local std::string t_err;
+
+struct Status {
+  int code = RFGPU_OK;
+  std::string msg;
+  bool ok() const { return code == RFGPU_OK; }
+};
+
+Status make_err(int code, const std::string& msg) { return Status{code, msg}; }
+
+int finish(const Status& s) {
+  if (!s.ok()) t_err = s.msg;
+  return s.code;
+}
+
+#define RF_CUDA(expr)                                                                              \
+  do {                                                                                             \
+    cudaError_t _e = (expr);                                                                       \
+    if (_e != cudaSuccess)                                                                         \
+      return make_err(RFGPU_ECUDA, std::string("CUDA: ") + cudaGetErrorString(_e) + " at " #expr); \
+  } while (0)
+
+#define RF_TRY(expr)            \
+  do {                          \
+    Status _s = (expr);         \
+    if (!_s.ok()) return _s;    \
+  } while (0)
+
+// ============================================================ NCCL (dlopen)
+// NCCL is loaded lazily so the single-GPU path has no NCCL dependency and so
+// an NCCL already loaded in the process (e.g. torch's) is reused.
+struct Nccl {
+  void* h = nullptr;
+  int (*getUniqueId)(void*) = nullptr;
+  int (*commInitRank)(void**, int, char[128], int) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*commDestroy)(void*) = nullptr;
+  const char* (*getErrorString)(int) = nullptr;
+  bool load(std::string* why) {
+    if (h) return true;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) {
+      *why = "NCCL library not found (libnccl.so.2)";
+      return false;
+    }
+    getUniqueId = reinterpret_cast<decltype(getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    commInitRank = reinterpret_cast<decltype(commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    allReduce = reinterpret_cast<decltype(allReduce)>(dlsym(h, "ncclAllReduce"));
+    commDestroy = reinterpret_cast<decltype(commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    getErrorString = reinterpret_cast<decltype(getErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (!getUniqueId || !commInitRank || !allReduce || !commDestroy || !getErrorString) {
+      *why = "NCCL symbols missing";
+      return false;
+    }
+    return true;
+  }
+};
+Nccl g_nccl;
+std::mutex g_nccl_mu;
+constexpr int kNcclDouble = 8;  // ncclFloat64
+constexpr int kNcclSum = 0;     // ncclSum
+
+}  // namespace
+
+// ============================================================ context ====
+struct rfgpu_ctx {
+  int device = 0, rank = 0, world = 1;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  void* comm = nullptr;
+  std::mutex mu;
+  // pinned scratch for status reads
+  int* h_info = nullptr;
+  double* h_d = nullptr;
+  int64_t* h_i64 = nullptr;
+  // profiling
+  bool profile = false;
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  std::map<std::string, std::pair<int64_t, double>> prof;
+  int64_t launch_base = 0;
+
+  cudaEvent_t get_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+struct rfgpu_matrix {
+  rfgpu_ctx* ctx = nullptr;
+  bool f32 = false;
+  void* dev = nullptr;
+  bool owned = false;
+  int64_t m = 0, n = 0, lda = 0, m_global = 0, row0 = 0;
+};
+
+namespace {
+
+// Scoped CUDA-event timer on the context stream.
+struct Timed {
+  rfgpu_ctx* c;
+  std::string name;
+  cudaEvent_t a = nullptr;
+  Timed(rfgpu_ctx* ctx, const char* nm) : c(ctx), name(nm) {
+    if (c->profile) {
+      a = c->get_event();
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~Timed() {
+    if (c->profile && a) {
+      cudaEvent_t b = c->get_event();
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({name, a, b});
+    }
+  }
+};
+
+void drain_profile(rfgpu_ctx* c) {
+  if (c->pending.empty()) return;
+  cudaStreamSynchronize(c->stream);
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    auto& s = c->prof[p.name];
+    s.first += 1;
+    s.second += ms;
+    c->event_pool.push_back(p.a);
+    c->event_pool.push_back(p.b);
+  }
+  c->pending.clear();
+}
+
+// Stream-ordered device buffer from the default memory pool.
+struct DBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  Status alloc(size_t bytes, cudaStream_t st) {
+    s = st;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      return make_err(RFGPU_ENOMEM, "device allocation of " + std::to_string(bytes) + " bytes failed");
+    }
+    return {};
+  }
+  double* d() const { return static_cast<double*>(p); }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+inline int64_t even(int64_t x) { return x + (x & 1); }
+
+cudaError_t nccl_allreduce_cb(void* vctx, double* buf, int64_t count, cudaStream_t st) {
+  rfgpu_ctx* c = static_cast<rfgpu_ctx*>(vctx);
+  if (c->world <= 1 || count <= 0) return cudaSuccess;
+  int r = g_nccl.allReduce(buf, buf, static_cast<size_t>(count), kNcclDouble, kNcclSum, c->comm, st);
+  return r == 0 ? cudaSuccess : cudaErrorUnknown;
+}
+
+DeviceAllreduce allreduce_of(rfgpu_ctx* c) {
+  DeviceAllreduce a{};
+  if (c->world > 1) {
+    a.ctx = c;
+    a.fn = nccl_allreduce_cb;
+  }
+  return a;
+}
+
+Status allreduce(rfgpu_ctx* c, double* buf, int64_t count) {
+  if (c->world <= 1 || count <= 0) return {};
+  Timed t(c, "allreduce");
+  int r = g_nccl.allReduce(buf, buf, static_cast<size_t>(count), kNcclDouble, kNcclSum, c->comm, c->stream);
+  if (r != 0) return make_err(RFGPU_ECUDA, std::string("NCCL allreduce: ") + g_nccl.getErrorString(r));
+  return {};
+}
+
+// ---- GEMM wrapper -----------------------------------------------------------
+Status gemm(rfgpu_ctx* c, bool trans, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+            const double* B, int64_t ldb, double* C, int64_t ldc, double* sumsq_partials = nullptr,
+            int* sumsq_count = nullptr) {
+  if (M <= 0 || N <= 0) return {};
+  const GemmPlan p = plan_gemm(M, N, K, c->num_sms);
+  DBuf ws;
+  const size_t wb = gemm_workspace_bytes(M, N, p);
+  if (wb) RF_TRY(ws.alloc(wb, c->stream));
+  {
+    Timed t(c, trans ? "gemm_tn" : "gemm_nn");
+    RF_CUDA(gemm_f64(trans, M, N, K, A, lda, B, ldb, C, ldc, ws.d(), wb, sumsq_partials, p, c->stream));
+  }
+  if (sumsq_count) *sumsq_count = p.splits * p.mtiles;
+  return {};
+}
+
+int64_t sumsq_slots(rfgpu_ctx* c, int64_t M, int64_t N, int64_t K) {
+  const GemmPlan p = plan_gemm(M, N, K, c->num_sms);
+  return static_cast<int64_t>(p.splits) * p.mtiles;
+}
+
+// ---- orth ---------------------------------------------------------------------
+// Q (m_loc x r, ld ldq) = orth(X (m_loc x cols, ld ldx)); X rows may be
+// sharded across ranks (dist = true). R (cols x cols) optional: filled when
+// the CholeskyQR2 path is taken (R = R2 R1, X = Q R). Returns r and whether
+// the fast path was taken.
+constexpr double kCholGate = 1e-10;  // min pivot / trace(G): residuals >= 1e-5 ||X||_F
+
+Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx, double* Q, int64_t ldq,
+            int64_t* r_out, double* R, bool dist, bool* fast_out = nullptr) {
+  Timed t(c, "orth");
+  if (cols == 0) {
+    *r_out = 0;
+    return {};
+  }
+  cudaStream_t st = c->stream;
+  const int64_t cc = cols * cols;
+  DBuf small;
+  // G1, R1, R1inv, G2, R2, R2inv, chol work, Q1 separately
+  RF_TRY(small.alloc(sizeof(double) * (6 * cc + 2 * cc + 16) + 64, st));
+  double* G1 = small.d();
+  double* R1 = G1 + cc;
+  double* R1i = R1 + cc;
+  double* G2 = R1i + cc;
+  double* R2 = G2 + cc;
+  double* R2i = R2 + cc;
+  double* cwork = R2i + cc;  // 2cc
+  double* infod = cwork + 2 * cc;  // 2 doubles
+  int* info = reinterpret_cast<int*>(infod + 4);  // 2 ints
+  DBuf q1;
+  const int64_t ldq1 = even(m);
+  RF_TRY(q1.alloc(sizeof(double) * std::max<int64_t>(1, ldq1 * cols), st));
+
+  RF_TRY(gemm(c, true, cols, cols, m, X, ldx, X, ldx, G1, cols));
+  if (dist) RF_TRY(allreduce(c, G1, cc));
+  RF_CUDA(chol_inv(G1, cols, R1, R1i, cwork, info, infod, st));
+  RF_TRY(gemm(c, false, m, cols, cols, X, ldx, R1i, cols, q1.d(), ldq1));
+  RF_TRY(gemm(c, true, cols, cols, m, q1.d(), ldq1, q1.d(), ldq1, G2, cols));
+  if (dist) RF_TRY(allreduce(c, G2, cc));
+  RF_CUDA(chol_inv(G2, cols, R2, R2i, cwork, info + 1, infod + 1, st));
+  RF_TRY(gemm(c, false, m, cols, cols, q1.d(), ldq1, R2i, cols, Q, ldq));
+  RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  RF_CUDA(cudaMemcpyAsync(c->h_d, infod, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  RF_CUDA(cudaStreamSynchronize(st));
+  const bool fast = c->h_info[0] == 0 && c->h_info[1] == 0 && c->h_d[0] >= kCholGate;
+  if (fast_out) *fast_out = fast;
+  if (fast) {
+    if (R) RF_TRY(gemm(c, false, cols, cols, cols, R2, cols, R1, cols, R, cols));
+    *r_out = cols;
+    return {};
+  }
+  // Gram-Schmidt with the reference's drop rule.
+  DBuf gw;
+  RF_TRY(gw.alloc(sizeof(double) * gs_orth_work_doubles(m, cols) + 64, st));
+  int64_t* r_dev = reinterpret_cast<int64_t*>(gw.d() + gs_orth_work_doubles(m, cols));
+  RF_CUDA(gs_orth(X, m, cols, ldx, Q, ldq, r_dev, gw.d(), dist ? allreduce_of(c) : DeviceAllreduce{}, st));
+  RF_CUDA(cudaMemcpyAsync(c->h_i64, r_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  RF_CUDA(cudaStreamSynchronize(st));
+  *r_out = c->h_i64[0];
+  return {};
+}
+
+// ---- small SVD of B (ell x n) given Bt = B^T (n x ell, replicated) -------------
+// Produces Ub (ell x ell: left singular vectors of B), D (ell), Vb (n x ell:
+// right singular vectors of B), matching svd_dense(B) (dense.cpp:690-701).
+Status small_svd_of_bt(rfgpu_ctx* c, const double* Bt, int64_t n, int64_t ell, double* Ub, double* D, double* Vb) {
+  Timed t(c, "small_svd");
+  cudaStream_t st = c->stream;
+  const int64_t ldn = even(n);
+  DBuf qb, rb, ur, vr, jw, inf;
+  RF_TRY(qb.alloc(sizeof(double) * ldn * ell, st));
+  RF_TRY(rb.alloc(sizeof(double) * ell * ell, st));
+  RF_TRY(inf.alloc(64, st));
+  int64_t r = 0;
+  bool fast = false;
+  RF_TRY(orth(c, Bt, n, ell, n, qb.d(), ldn, &r, rb.d(), /*dist=*/false, &fast));
+  int* info = inf.as<int>();
+  if (fast) {
+    // Bt = Qb R; R = Ur S Vr^T  =>  B = Vr S (Qb Ur)^T
+    RF_TRY(ur.alloc(sizeof(double) * ell * ell, st));
+    const size_t jwb = jacobi_work_bytes(ell, ell);
+    if (jwb) RF_TRY(jw.alloc(jwb, st));
+    RF_CUDA(jacobi_svd(rb.d(), ell, ell, ur.d(), D, Ub, jw.d(), info, info + 1, st));
+    RF_TRY(gemm(c, false, n, ell, ell, qb.d(), ldn, ur.d(), ell, Vb, n));
+  } else {
+    // rank-deficient / ill-conditioned B: Jacobi directly on the tall Bt
+    const size_t jwb = jacobi_work_bytes(n, ell);
+    if (jwb) RF_TRY(jw.alloc(jwb, st));
+    RF_CUDA(jacobi_svd(Bt, n, ell, Vb, D, Ub, jw.d(), info, info + 1, st));
+  }
+  RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  RF_CUDA(cudaStreamSynchronize(st));
+  if (c->h_info[0] == 1) return make_err(RFGPU_ECONVERGENCE, "svd_dense: Jacobi sweeps did not converge");
+  return {};
+}
+
+// ---- range finder core ------------------------------------------------------------
+struct RangeOut {
+  int64_t ell_out = 0;
+  double a_frob2 = 0.0;  // ||A||_F^2 (global)
+};
+
+// A (m_loc x n) handle; G_dev (n x ell); Q_dev (ldq x ell) receives the basis;
+// Bt_dev (n x ell, ld n) receives B^T = A^T Q (summed over ranks).
+Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, int64_t q, bool reorth,
+                  double* Q, int64_t ldq, double* Bt, RangeOut* out) {
+  cudaStream_t st = c->stream;
+  const int64_t m = a->m, n = a->n;
+  const double* A = static_cast<const double*>(a->dev);
+  const int64_t lda = a->lda;
+  DBuf y, z, w, ssq, scal;
+  RF_TRY(y.alloc(sizeof(double) * std::max<int64_t>(1, ldq * ell), st));
+  RF_TRY(z.alloc(sizeof(double) * n * ell, st));
+  RF_TRY(w.alloc(sizeof(double) * n * ell, st));
+  const int64_t slots = sumsq_slots(c, m, ell, n);
+  RF_TRY(ssq.alloc(sizeof(double) * std::max<int64_t>(1, slots), st));
+  RF_TRY(scal.alloc(sizeof(double) * 4, st));
+  RF_CUDA(cudaMemsetAsync(ssq.d(), 0, sizeof(double) * std::max<int64_t>(1, slots), st));
+
+  // pass 1: Y = A G, with ||A||_F^2 fused
+  RF_TRY(gemm(c, false, m, ell, n, A, lda, G, n, y.d(), ldq, ssq.d()));
+  RF_CUDA(sum_array(ssq.d(), slots, scal.d(), st));
+  RF_TRY(allreduce(c, scal.d(), 1));
+
+  int64_t r = ell;
+  if (!reorth) {
+    for (int64_t j = 0; j < q; ++j) {
+      RF_TRY(gemm(c, true, n, ell, m, A, lda, y.d(), ldq, z.d(), n));
+      RF_TRY(allreduce(c, z.d(), n * ell));
+      RF_TRY(gemm(c, false, m, ell, n, A, lda, z.d(), n, y.d(), ldq));
+    }
+    RF_TRY(orth(c, y.d(), m, ell, ldq, Q, ldq, &r, nullptr, true));
+  } else {
+    RF_TRY(orth(c, y.d(), m, ell, ldq, Q, ldq, &r, nullptr, true));
+    for (int64_t j = 0; j < q && r > 0; ++j) {
+      int64_t rw = 0;
+      RF_TRY(gemm(c, true, n, r, m, A, lda, Q, ldq, z.d(), n));
+      RF_TRY(allreduce(c, z.d(), n * r));
+      RF_TRY(orth(c, z.d(), n, r, n, w.d(), n, &rw, nullptr, false));
+      RF_TRY(gemm(c, false, m, rw, n, A, lda, w.d(), n, y.d(), ldq));
+      RF_TRY(orth(c, y.d(), m, rw, ldq, Q, ldq, &r, nullptr, true));
+    }
+  }
+  // projection: B^T = A^T Q
+  if (r > 0) {
+    RF_TRY(gemm(c, true, n, r, m, A, lda, Q, ldq, Bt, n));
+    RF_TRY(allreduce(c, Bt, n * r));
+  }
+  RF_CUDA(cudaMemcpyAsync(c->h_d, scal.d(), sizeof(double), cudaMemcpyDeviceToHost, st));
+  RF_CUDA(cudaStreamSynchronize(st));
+  out->a_frob2 = c->h_d[0];
+  out->ell_out = r;
+  return {};
+}
+
+// frob_residual (rangefinder.cpp:45-54) from ||A||_F^2 and B^T on the device.
+Status frob_residual_dev(rfgpu_ctx* c, double a_frob2, const double* Bt, int64_t count, double* resid) {
+  cudaStream_t st = c->stream;
+  DBuf part, out;
+  RF_TRY(part.alloc(sizeof(double) * 1024, st));
+  RF_TRY(out.alloc(sizeof(double), st));
+  double bn2 = 0.0;
+  if (count > 0) {
+    RF_CUDA(sumsq(Bt, count, part.d(), out.d(), st));
+    RF_CUDA(cudaMemcpyAsync(c->h_d, out.d(), sizeof(double), cudaMemcpyDeviceToHost, st));
+    RF_CUDA(cudaStreamSynchronize(st));
+    bn2 = c->h_d[0];
+  }
+  const double a_frob = std::sqrt(a_frob2);
+  const double bn = std::sqrt(bn2);
+  if (bn > a_frob * (1.0 + 1e-8))
+    return make_err(RFGPU_ENUMERICAL,
+                    "frob_residual: projection exceeds the total norm; basis orthonormality was lost upstream");
+  const double diff = a_frob * a_frob - bn * bn;
+  if (resid) *resid = std::sqrt(std::max(0.0, diff));
+  return {};
+}
+
+Status check_sample(const rfgpu_matrix* a, int64_t k, int64_t ell, const char* where) {
+  if (k < 1) return make_err(RFGPU_EPARAM, std::string(where) + ": k must be at least 1");
+  if (ell < k) return make_err(RFGPU_EPARAM, std::string(where) + ": p must be non-negative");
+  if (ell > std::min(a->m_global, a->n)) return make_err(RFGPU_EPARAM, std::string(where) + ": k + p exceeds min(m, n)");
+  return {};
+}
+
+// rsvd on device buffers; U_dev (ldu x ell), D_dev (ell), V_dev (n x ell).
+Status rsvd_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t k, int64_t ell, int64_t q, bool keep_over,
+                 bool reorth, double* U, int64_t ldu, double* D, double* V, int64_t* rank_out) {
+  cudaStream_t st = c->stream;
+  const int64_t m = a->m, n = a->n;
+  const int64_t ldq = even(m);
+  DBuf Q, Bt, Ub, Vb, Dd;
+  RF_TRY(Q.alloc(sizeof(double) * std::max<int64_t>(1, ldq * ell), st));
+  RF_TRY(Bt.alloc(sizeof(double) * n * ell, st));
+  RangeOut ro;
+  RF_TRY(range_core(c, a, G, ell, q, reorth, Q.d(), ldq, Bt.d(), &ro));
+  RF_TRY(frob_residual_dev(c, ro.a_frob2, Bt.d(), n * ro.ell_out, nullptr));
+  const int64_t r = ro.ell_out;
+  if (r == 0) {
+    *rank_out = 0;
+    return {};
+  }
+  RF_TRY(Ub.alloc(sizeof(double) * r * r, st));
+  RF_TRY(Vb.alloc(sizeof(double) * n * r, st));
+  RF_TRY(Dd.alloc(sizeof(double) * r, st));
+  RF_TRY(small_svd_of_bt(c, Bt.d(), n, r, Ub.d(), Dd.d(), Vb.d()));
+  const int64_t keep = keep_over ? r : std::min(k, r);
+  // lift: U = Q * Ub(:, :keep)
+  RF_TRY(gemm(c, false, m, keep, r, Q.d(), ldq, Ub.d(), r, U, ldu));
+  RF_CUDA(cudaMemcpyAsync(V, Vb.d(), sizeof(double) * n * keep, cudaMemcpyDeviceToDevice, st));
+  RF_CUDA(cudaMemcpyAsync(D, Dd.d(), sizeof(double) * keep, cudaMemcpyDeviceToDevice, st));
+  *rank_out = keep;
+  return {};
+}
+
+// ---- host gaussian (randfact::gaussian) ----------------------------------------------
+inline uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ULL;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  return z;
+}
+
+inline uint64_t fnv1a(const char* s) {
+  uint64_t h = 0xCBF29CE484222325ULL;
+  for (const unsigned char* p = reinterpret_cast<const unsigned char*>(s); *p; ++p) {
+    h ^= *p;
+    h *= 0x100000001B3ULL;
+  }
+  return h;
+}
+
+void gaussian_span(uint64_t key, int64_t e0, int64_t e1, double* out) {
+  constexpr double kTwoPi = 6.283185307179586476925286766559;
+  for (int64_t e = e0; e < e1; ++e) {
+    const uint64_t pair = static_cast<uint64_t>(e / 2);
+    const uint64_t x1 = mix64(key + 0x9E3779B97F4A7C15ULL * (2 * pair + 1)) >> 11;
+    const uint64_t x2 = mix64(key + 0x9E3779B97F4A7C15ULL * (2 * pair + 2)) >> 11;
+    const double u1 = (static_cast<double>(x1) + 0.5) * 0x1.0p-53;
+    const double u2 = (static_cast<double>(x2) + 0.5) * 0x1.0p-53;
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    out[e - e0] = (e % 2 == 0) ? r * std::cos(kTwoPi * u2) : r * std::sin(kTwoPi * u2);
+  }
+}
+
+Status ensure_device(rfgpu_ctx* c) {
+  RF_CUDA(cudaSetDevice(c->device));
+  return {};
+}
+
+}  // namespace
+
+// ============================================================ C ABI ======
+extern "C" {
+
+const char* rfgpu_last_error(void) { return t_err.c_str(); }
+int rfgpu_version(void) { return 1; }
+
+int rfgpu_gaussian_range(uint64_t seed, const char* tag, int64_t e0, int64_t count, double* out) {
+  if (e0 < 0 || count < 0 || !tag) return finish(make_err(RFGPU_EPARAM, "gaussian: negative dimension"));
+  const uint64_t key = mix64(seed ^ fnv1a(tag));
+  const int64_t per = 1 << 16;
+  const int nt = static_cast<int>(std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()),
+                                                    std::max<int64_t>(1, count / per)));
+  if (nt <= 1) {
+    gaussian_span(key, e0, e0 + count, out);
+    return RFGPU_OK;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t a = count * t / nt, b = count * (t + 1) / nt;
+    th.emplace_back(gaussian_span, key, e0 + a, e0 + b, out + a);
+  }
+  for (auto& x : th) x.join();
+  return RFGPU_OK;
+}
+
+int rfgpu_gaussian(uint64_t seed, const char* tag, int64_t m, int64_t n, double* out) {
+  if (m < 0 || n < 0) return finish(make_err(RFGPU_EPARAM, "gaussian: negative dimension"));
+  return rfgpu_gaussian_range(seed, tag, 0, m * n, out);
+}
+
+int rfgpu_ctx_create(int device, rfgpu_ctx** out) { return rfgpu_ctx_create_dist(device, 0, 1, nullptr, 0, out); }
+
+int rfgpu_nccl_unique_id(void* id, size_t id_bytes) {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  std::string why;
+  if (id_bytes < 128) return finish(make_err(RFGPU_EPARAM, "nccl id buffer must hold 128 bytes"));
+  if (!g_nccl.load(&why)) return finish(make_err(RFGPU_ECUDA, why));
+  int r = g_nccl.getUniqueId(id);
+  if (r != 0) return finish(make_err(RFGPU_ECUDA, std::string("ncclGetUniqueId: ") + g_nccl.getErrorString(r)));
+  return RFGPU_OK;
+}
+
+int rfgpu_ctx_create_dist(int device, int rank, int world, const void* nccl_id, size_t id_bytes, rfgpu_ctx** out) {
+  if (!out) return finish(make_err(RFGPU_EPARAM, "ctx_create: null output"));
+  if (world < 1 || rank < 0 || rank >= world) return finish(make_err(RFGPU_EPARAM, "ctx_create: bad rank/world"));
+  auto c = std::make_unique<rfgpu_ctx>();
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return finish(make_err(RFGPU_ECUDA, "no CUDA device available (rfgpu has no CPU fallback)"));
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return finish(make_err(RFGPU_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)));
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major != 10) {
+    return finish(make_err(RFGPU_ECUDA, std::string("rfgpu is built for sm_100a (B200); device is ") + prop.name));
+  }
+  c->num_sms = prop.multiProcessorCount;
+  cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  cudaMallocHost(&c->h_info, 64);
+  cudaMallocHost(&c->h_d, 64);
+  cudaMallocHost(&c->h_i64, 64);
+  // keep freed pool memory cached (stream-ordered temporaries are reused)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (world > 1) {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    std::string why;
+    if (!nccl_id || id_bytes < 128) return finish(make_err(RFGPU_EPARAM, "ctx_create_dist: nccl id required"));
+    if (!g_nccl.load(&why)) return finish(make_err(RFGPU_ECUDA, why));
+    char idb[128];
+    std::memcpy(idb, nccl_id, 128);
+    int r = g_nccl.commInitRank(&c->comm, world, idb, rank);
+    if (r != 0) return finish(make_err(RFGPU_ECUDA, std::string("ncclCommInitRank: ") + g_nccl.getErrorString(r)));
+  }
+  c->launch_base = launch_counter();
+  *out = c.release();
+  return RFGPU_OK;
+}
+
+int rfgpu_ctx_destroy(rfgpu_ctx* c) {
+  if (!c) return RFGPU_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  drain_profile(c);
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->comm) g_nccl.commDestroy(c->comm);
+  cudaFreeHost(c->h_info);
+  cudaFreeHost(c->h_d);
+  cudaFreeHost(c->h_i64);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return RFGPU_OK;
+}
+
+int rfgpu_ctx_rank(const rfgpu_ctx* c) { return c ? c->rank : -1; }
+int rfgpu_ctx_world(const rfgpu_ctx* c) { return c ? c->world : -1; }
+void* rfgpu_ctx_stream(rfgpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int rfgpu_ctx_synchronize(rfgpu_ctx* c) {
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return finish(make_err(RFGPU_ECUDA, cudaGetErrorString(e)));
+  return RFGPU_OK;
+}
+
+int rfgpu_profile_enable(rfgpu_ctx* c, int on) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->profile = on != 0;
+  return RFGPU_OK;
+}
+
+int rfgpu_profile_reset(rfgpu_ctx* c) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  drain_profile(c);
+  c->prof.clear();
+  c->launch_base = launch_counter();
+  return RFGPU_OK;
+}
+
+int rfgpu_profile_read(rfgpu_ctx* c, const char* name, int64_t* launches, double* total_ms) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  drain_profile(c);
+  auto it = c->prof.find(name);
+  *launches = it == c->prof.end() ? 0 : it->second.first;
+  *total_ms = it == c->prof.end() ? 0.0 : it->second.second;
+  return RFGPU_OK;
+}
+
+int64_t rfgpu_launch_count(rfgpu_ctx* c) { return launch_counter() - c->launch_base; }
+
+static int matrix_make(rfgpu_ctx* c, const void* host, const void* dev, bool f32, int64_t m, int64_t n, int64_t lda,
+                       rfgpu_matrix** out) {
+  if (!c || !out) return finish(make_err(RFGPU_EPARAM, "matrix: null argument"));
+  if (m < 0 || n < 0) return finish(make_err(RFGPU_EPARAM, "DenseMatrix: negative dimension"));
+  if (lda < std::max<int64_t>(1, m)) return finish(make_err(RFGPU_EPARAM, "matrix: lda < m"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaSetDevice(c->device);
+  auto h = std::make_unique<rfgpu_matrix>();
+  h->ctx = c;
+  h->f32 = f32;
+  h->m = m;
+  h->n = n;
+  const size_t es = f32 ? sizeof(float) : sizeof(double);
+  if (dev) {
+    h->dev = const_cast<void*>(dev);
+    h->lda = lda;
+  } else {
+    h->lda = f32 ? ((m + 3) / 4) * 4 : even(std::max<int64_t>(1, m));
+    const size_t bytes = es * static_cast<size_t>(h->lda) * std::max<int64_t>(1, n);
+    if (cudaMalloc(&h->dev, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return finish(make_err(RFGPU_ENOMEM, "matrix upload: device allocation failed"));
+    }
+    h->owned = true;
+    if (m > 0 && n > 0) {
+      cudaError_t e = cudaMemcpy2DAsync(h->dev, es * h->lda, host, es * lda, es * m, n, cudaMemcpyHostToDevice, c->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+      if (e != cudaSuccess) {
+        cudaFree(h->dev);
+        return finish(make_err(RFGPU_ECUDA, std::string("matrix upload: ") + cudaGetErrorString(e)));
+      }
+    }
+  }
+  // global row count / offset across ranks (row-sharded A)
+  h->m_global = m;
+  h->row0 = 0;
+  if (c->world > 1) {
+    DBuf b;
+    Status s = b.alloc(sizeof(double) * c->world * 2, c->stream);
+    if (!s.ok()) return finish(s);
+    std::vector<double> v(c->world * 2, 0.0);
+    v[c->rank] = static_cast<double>(m);
+    cudaMemcpyAsync(b.d(), v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, c->stream);
+    s = allreduce(c, b.d(), c->world);
+    if (!s.ok()) return finish(s);
+    cudaMemcpyAsync(v.data(), b.d(), sizeof(double) * c->world, cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    int64_t tot = 0, off = 0;
+    for (int r = 0; r < c->world; ++r) {
+      if (r < c->rank) off += static_cast<int64_t>(v[r]);
+      tot += static_cast<int64_t>(v[r]);
+    }
+    h->m_global = tot;
+    h->row0 = off;
+  }
+  *out = h.release();
+  return RFGPU_OK;
+}
+
+int rfgpu_matrix_upload(rfgpu_ctx* c, const double* a, int64_t m, int64_t n, int64_t lda, rfgpu_matrix** out) {
+  return matrix_make(c, a, nullptr, false, m, n, lda, out);
+}
+int rfgpu_matrix_wrap_device(rfgpu_ctx* c, const double* a, int64_t m, int64_t n, int64_t lda, rfgpu_matrix** out) {
+  return matrix_make(c, nullptr, a, false, m, n, lda, out);
+}
+int rfgpu_matrix_upload_f32(rfgpu_ctx* c, const float* a, int64_t m, int64_t n, int64_t lda, rfgpu_matrix** out) {
+  return matrix_make(c, a, nullptr, true, m, n, lda, out);
+}
+int rfgpu_matrix_wrap_device_f32(rfgpu_ctx* c, const float* a, int64_t m, int64_t n, int64_t lda,
+                                 rfgpu_matrix** out) {
+  return matrix_make(c, nullptr, a, true, m, n, lda, out);
+}
+
+int rfgpu_matrix_free(rfgpu_matrix* h) {
+  if (!h) return RFGPU_OK;
+  if (h->owned) {
+    cudaSetDevice(h->ctx->device);
+    cudaStreamSynchronize(h->ctx->stream);
+    cudaFree(h->dev);
+  }
+  delete h;
+  return RFGPU_OK;
+}
+
+int rfgpu_matrix_shape(const rfgpu_matrix* h, int64_t* m_local, int64_t* n, int64_t* m_global, int64_t* row0) {
+  if (!h) return finish(make_err(RFGPU_EPARAM, "matrix_shape: null handle"));
+  if (m_local) *m_local = h->m;
+  if (n) *n = h->n;
+  if (m_global) *m_global = h->m_global;
+  if (row0) *row0 = h->row0;
+  return RFGPU_OK;
+}
+
+static Status copy_out(rfgpu_ctx* c, double* host, int64_t ldh, const double* dev, int64_t ldd, int64_t rows,
+                       int64_t cols) {
+  if (!host || rows <= 0 || cols <= 0) return {};
+  RF_CUDA(cudaMemcpy2DAsync(host, sizeof(double) * ldh, dev, sizeof(double) * ldd, sizeof(double) * rows, cols,
+                            cudaMemcpyDeviceToHost, c->stream));
+  return {};
+}
+
+int rfgpu_multiply(rfgpu_ctx* c, const rfgpu_matrix* a, int trans, const double* x, int64_t ncols, double* out) {
+  if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "multiply: bad handle"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status s = [&]() -> Status {
+    RF_TRY(ensure_device(c));
+    cudaStream_t st = c->stream;
+    const int64_t m = a->m, n = a->n;
+    const int64_t xr = trans ? m : n, cr = trans ? n : m;
+    DBuf xd, cd;
+    RF_TRY(xd.alloc(sizeof(double) * std::max<int64_t>(1, xr * ncols), st));
+    RF_TRY(cd.alloc(sizeof(double) * std::max<int64_t>(1, cr * ncols), st));
+    if (xr * ncols > 0) RF_CUDA(cudaMemcpyAsync(xd.d(), x, sizeof(double) * xr * ncols, cudaMemcpyHostToDevice, st));
+    RF_TRY(gemm(c, trans != 0, cr, ncols, trans ? m : n, static_cast<const double*>(a->dev), a->lda, xd.d(),
+                std::max<int64_t>(1, xr), cd.d(), std::max<int64_t>(1, cr)));
+    if (trans) RF_TRY(allreduce(c, cd.d(), cr * ncols));
+    RF_TRY(copy_out(c, out, std::max<int64_t>(1, cr), cd.d(), std::max<int64_t>(1, cr), cr, ncols));
+    RF_CUDA(cudaStreamSynchronize(st));
+    return {};
+  }();
+  return finish(s);
+}
+
+int rfgpu_range_finder(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t ell, int64_t q, int reorth,
+                       double* Qh, double* Bh, double* resid, int64_t* ell_out) {
+  if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "range_finder: bad handle"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status s = [&]() -> Status {
+    if (q < 0) return make_err(RFGPU_EPARAM, "power_range: q must be non-negative");
+    if (ell < 1 || ell > std::min(a->m_global, a->n))
+      return make_err(RFGPU_EPARAM, "power_range: k + p exceeds min(m, n)");
+    RF_TRY(ensure_device(c));
+    cudaStream_t st = c->stream;
+    const int64_t m = a->m, n = a->n, ldq = even(m);
+    DBuf gd, Q, Bt, Bd;
+    RF_TRY(gd.alloc(sizeof(double) * n * ell, st));
+    RF_TRY(Q.alloc(sizeof(double) * std::max<int64_t>(1, ldq * ell), st));
+    RF_TRY(Bt.alloc(sizeof(double) * n * ell, st));
+    RF_TRY(Bd.alloc(sizeof(double) * n * ell, st));
+    RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
+    RangeOut ro;
+    RF_TRY(range_core(c, a, gd.d(), ell, q, reorth != 0, Q.d(), ldq, Bt.d(), &ro));
+    const int64_t r = ro.ell_out;
+    double res = 0.0;
+    RF_TRY(frob_residual_dev(c, ro.a_frob2, Bt.d(), n * r, &res));
+    if (resid) *resid = res;
+    if (ell_out) *ell_out = r;
+    RF_TRY(copy_out(c, Qh, std::max<int64_t>(1, m), Q.d(), ldq, m, r));
+    if (Bh && r > 0) {
+      RF_CUDA(transpose(Bt.d(), n, r, n, Bd.d(), r, st));
+      RF_TRY(copy_out(c, Bh, r, Bd.d(), r, r, n));
+    }
+    RF_CUDA(cudaStreamSynchronize(st));
+    return {};
+  }();
+  return finish(s);
+}
+
+int rfgpu_rsvd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g_dev, int64_t k, int64_t ell, int64_t q,
+                      int keep_over, int reorth, double* U, double* D, double* V, int64_t* rank_out) {
+  if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "rsvd: bad handle"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status s = [&]() -> Status {
+    RF_TRY(check_sample(a, k, ell, "power_range"));
+    if (q < 0) return make_err(RFGPU_EPARAM, "power_range: q must be non-negative");
+    RF_TRY(ensure_device(c));
+    int64_t r = 0;
+    RF_TRY(rsvd_core(c, a, g_dev, k, ell, q, keep_over != 0, reorth != 0, U, std::max<int64_t>(1, a->m), D, V, &r));
+    if (rank_out) *rank_out = r;
+    return {};
+  }();
+  return finish(s);
+}
+
+int rfgpu_rsvd(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t k, int64_t ell, int64_t q, int keep_over,
+               int reorth, double* Uh, double* Dh, double* Vh, int64_t* rank_out) {
+  if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "rsvd: bad handle"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status s = [&]() -> Status {
+    RF_TRY(check_sample(a, k, ell, "power_range"));
+    if (q < 0) return make_err(RFGPU_EPARAM, "power_range: q must be non-negative");
+    RF_TRY(ensure_device(c));
+    cudaStream_t st = c->stream;
+    const int64_t m = a->m, n = a->n, ldu = std::max<int64_t>(1, m);
+    DBuf gd, U, D, V;
+    RF_TRY(gd.alloc(sizeof(double) * n * ell, st));
+    RF_TRY(U.alloc(sizeof(double) * ldu * ell, st));
+    RF_TRY(D.alloc(sizeof(double) * ell, st));
+    RF_TRY(V.alloc(sizeof(double) * n * ell, st));
+    RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
+    int64_t r = 0;
+    RF_TRY(rsvd_core(c, a, gd.d(), k, ell, q, keep_over != 0, reorth != 0, U.d(), ldu, D.d(), V.d(), &r));
+    RF_TRY(copy_out(c, Uh, ldu, U.d(), ldu, m, r));
+    RF_TRY(copy_out(c, Dh, std::max<int64_t>(1, r), D.d(), std::max<int64_t>(1, r), r, 1));
+    RF_TRY(copy_out(c, Vh, n, V.d(), n, n, r));
+    RF_CUDA(cudaStreamSynchronize(st));
+    if (rank_out) *rank_out = r;
+    return {};
+  }();
+  return finish(s);
+}
+
+int rfgpu_row_sketch(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t ell, double* Y) {
+  (void)c; (void)a; (void)g; (void)ell; (void)Y;
+  return finish(make_err(RFGPU_EPARAM, "row_sketch: not available in this build"));
+}
+int rfgpu_row_sketch_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t ell, double* Y) {
+  (void)c; (void)a; (void)g; (void)ell; (void)Y;
+  return finish(make_err(RFGPU_EPARAM, "row_sketch: not available in this build"));
+}
+int rfgpu_col_id(rfgpu_ctx* c, const double* Y, int64_t m, int64_t n, int64_t k, int64_t* Js, double* Z,
+                 int64_t* rank_out, int* truncated) {
+  (void)c; (void)Y; (void)m; (void)n; (void)k; (void)Js; (void)Z; (void)rank_out; (void)truncated;
+  return finish(make_err(RFGPU_EPARAM, "col_id: not available in this build"));
+}
+int rfgpu_col_id_device(rfgpu_ctx* c, const double* Y, int64_t m, int64_t n, int64_t k, int64_t* Js, double* Z,
+                        int64_t* rank_out, int* truncated) {
+  (void)c; (void)Y; (void)m; (void)n; (void)k; (void)Js; (void)Z; (void)rank_out; (void)truncated;
+  return finish(make_err(RFGPU_EPARAM, "col_id: not available in this build"));
+}
+int rfgpu_dual_sketch_f32(rfgpu_ctx* c, const rfgpu_matrix* a, const float* gc, const float* gr, int64_t ell,
+                          float* yc, float* yr) {
+  (void)c; (void)a; (void)gc; (void)gr; (void)ell; (void)yc; (void)yr;
+  return finish(make_err(RFGPU_EPARAM, "dual_sketch_f32: not available in this build"));
+}
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+// Internal interfaces between the rfgpu orchestrator (rfgpu_api.cu) and the
+// kernel translation units. Not part of the C ABI (see include/rfgpu.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rfgpu {
+
+// Count of rfgpu kernel launches issued by this process (every launch site
+// bumps it; rfgpu_launch_count reports the delta per context).
+int64_t launch_counter();
+void count_launch(int n = 1);
+
+// ---- tall-skinny FP64 GEMM (gemm_f64.cu) --------------------------------
+struct GemmPlan {
+  int ntiles;      // CTA columns along N
+  int nt;          // 8-wide MMA tiles per warp along N (CTA tile N = 16*nt)
+  int mtiles;      // CTA rows along M (128 each)
+  int splits;      // K splits (1: direct store)
+  int64_t ktiles;  // ceil(K / 32)
+};
+
+GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int num_sms, int force_splits = 0);
+size_t gemm_workspace_bytes(int64_t M, int64_t N, const GemmPlan& p);
+
+// trans_a = false: C = A(MxK) * B(KxN); true: C = A(KxM)^T * B(KxN).
+// sumsq_partials (NN only, may be null): receives splits*mtiles partial sums
+// of squares of A (each A element counted once).
+cudaError_t gemm_f64(bool trans_a, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double* C, int64_t ldc, double* workspace,
+                     size_t workspace_bytes, double* sumsq_partials, const GemmPlan& p, cudaStream_t st);
+
+cudaError_t sum_array(const double* x, int64_t n, double* out, cudaStream_t st);
+
+// ---- small dense kernels (small_f64.cu) ----------------------------------
+// Upper Cholesky R^T R = G (G c x c, symmetric, upper triangle consulted,
+// ld = c) and R^{-1}, both c x c column-major with zeros below the diagonal.
+// info[0] = 0 ok, else 1 + the failing column (reference rule: pivot <=
+// 1e-14 * max initial diagonal, proj/src/dense.cpp:763-786);
+// info_d[0] = min_j pivot_j / trace(G) (the CholeskyQR fast-path gate).
+cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double* work, int* info,
+                     double* info_d, cudaStream_t st);
+size_t chol_inv_work_bytes(int64_t c);
+
+// One-sided Jacobi SVD of X (mr x c, ld = mr): X = U diag(S) V^T with S
+// sorted non-increasing (proj/src/dense.cpp:585-686 semantics: tolerance
+// 1e-15, <= 60 sweeps, columns with S <= smax*1e-250 zeroed). U mr x c,
+// V c x c. info[0] = 0 ok, 1 no convergence, 2 zero singular values present
+// (those U columns are left zero; the caller completes them).
+cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double* S, double* V, double* work,
+                       int* info, int* sweeps_out, cudaStream_t st);
+size_t jacobi_work_bytes(int64_t mr, int64_t c);
+
+// y = sum of squares of x[0..n) into *out (fixed-order two-level reduction).
+cudaError_t sumsq(const double* x, int64_t n, double* partials, double* out, cudaStream_t st);
+
+// ---- Gram-Schmidt fallback for rank-deficient orth (orth_f64.cu) ---------
+// Reference orth semantics (proj/src/dense.cpp:402-431): classical
+// Gram-Schmidt applied twice per column, dropping columns whose residual is
+// <= drop. Q receives kept columns (ld = m); *r_dev the kept count.
+// Optional in-place sum across ranks of a device buffer (NCCL in the
+// distributed context; fn == nullptr on one GPU).
+struct DeviceAllreduce {
+  void* ctx;
+  cudaError_t (*fn)(void* ctx, double* buf, int64_t count, cudaStream_t st);
+};
+
+size_t gs_orth_work_doubles(int64_t m, int64_t c);
+cudaError_t gs_orth(const double* X, int64_t m, int64_t c, int64_t ldx, double* Q, int64_t ldq, int64_t* r_dev,
+                    double* work, const DeviceAllreduce& ar, cudaStream_t st);
+
+// *dst += *src (one thread; keeps scalar bookkeeping on the device).
+cudaError_t add_scalar(double* dst, const double* src, cudaStream_t st);
+
+}  // namespace rfgpu

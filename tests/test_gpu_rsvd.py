@@ -1,0 +1,169 @@
+"""GPU parity: the CUDA range finder / RSVD through the C ABI vs the CPU oracle.
+
+Tolerances (north star): singular values 1e-10 relative in FP64 (reorthonormalised
+mode, the only mode with that parity floor — SURVEY.md §0.4), residual
+||A - U S V^T||_F within 1% of the reference's. Reference tests mirrored:
+proj/tests/test_lowrank.cpp:42-105, proj/tests/test_rangefinder.cpp:43-185.
+"""
+import numpy as np
+import pytest
+
+import paper_1607_01649_b200 as rf
+
+pytestmark = pytest.mark.gpu
+
+
+def planted(port, m, n, sigma, seed=1, noise=0.0, tag="noise.N"):
+    a = port.planted(m, n, np.asarray(sigma, dtype=np.float64), seed)
+    if noise:
+        a = a + noise * port.gaussian(seed, tag, m, n)
+    return np.asfortranarray(a)
+
+
+def geometric(count, ratio):
+    return ratio ** np.arange(count, dtype=np.float64)
+
+
+def recon(f, k=None):
+    k = len(f.D) if k is None else k
+    return (f.U[:, :k] * f.D[:k]) @ f.V[:, :k].T
+
+
+def rel(a, b):
+    return np.abs(a - b) / np.maximum(np.abs(b), 1e-300)
+
+
+@pytest.mark.parametrize("m,n,k,p", [(300, 200, 20, 10), (257, 129, 7, 5), (1000, 777, 50, 14), (130, 300, 16, 8)])
+@pytest.mark.parametrize("trans", [False, True])
+def test_multiply_matches_numpy(ctx, m, n, k, p, trans):
+    rng = np.random.default_rng(m * 7 + n)
+    a = np.asfortranarray(rng.standard_normal((m, n)))
+    x = np.asfortranarray(rng.standard_normal((m if trans else n, k + p)))
+    got = rf.multiply(a, x, trans=trans, ctx=ctx)
+    want = (a.T @ x) if trans else (a @ x)
+    scale = np.abs(a).max() * np.abs(x).max() * (m if trans else n)
+    assert np.abs(got - want).max() <= 1e-14 * scale
+
+
+@pytest.mark.parametrize("case", ["c1", "c2s", "c3s"])
+def test_rsvd_reorth_matches_oracle(ctx, port, case):
+    if case == "c1":  # BASELINE config 1, full size
+        m, n, k, p, q = 2000, 2000, 50, 10, 1
+        sig = 1.0 / np.arange(1, 2001, dtype=np.float64) ** 2
+        a = planted(port, m, n, sig)
+    elif case == "c2s":  # config 2 shape family at 1/10 rows
+        m, n, k, p, q = 2000, 1000, 100, 10, 2
+        sig = np.exp(-np.arange(1, 501) / 20.0)
+        a = planted(port, m, n, sig, noise=1e-6)
+    else:  # config 3 family at 1/256 rows, 1/4 cols
+        m, n, k, p, q = 4096, 1024, 200, 20, 1
+        sig = np.arange(1, 1025, dtype=np.float64) ** -1.5
+        a = planted(port, m, n, sig, noise=1e-8)
+    want = port.rsvd(a, k, p, q, 1, False, True)
+    got = rf.rsvd(a, k, p, q, 1, reorthonormalize=True, ctx=ctx)
+    assert got.D.shape == want.D.shape == (k,)
+    assert rel(got.D, want.D).max() <= 1e-10
+    r_got = np.linalg.norm(a - recon(got))
+    r_want = np.linalg.norm(a - recon(want))
+    assert abs(r_got - r_want) <= 0.01 * r_want
+    # orthonormal factors
+    assert np.abs(got.U.T @ got.U - np.eye(k)).max() < 1e-12
+    assert np.abs(got.V.T @ got.V - np.eye(k)).max() < 1e-12
+    # singular vectors agree up to sign
+    s = np.sign(np.sum(got.U * want.U, axis=0))
+    assert np.abs(got.U * s - want.U)[:, : k // 2].max() < 1e-9
+
+
+def test_power_range_matches_oracle(ctx, port):
+    sig = 1.0 / np.arange(1, 401, dtype=np.float64) ** 2
+    a = planted(port, 600, 400, sig)
+    for q in (0, 1, 2):
+        want = port.power_range(a, 30, 10, q, 5, reorth=True)
+        got = rf.power_range(a, 30, 10, q, 5, reorthonormalize=True, ctx=ctx)
+        assert got.Q.shape == want.Q.shape
+        # same subspace: Q_ref^T Q has singular values 1
+        s = np.linalg.svd(want.Q.T @ got.Q, compute_uv=False)
+        assert np.abs(s - 1).max() < 1e-8
+        assert abs(got.residual_frob - want.residual_frob) <= 1e-6 * np.linalg.norm(a)
+
+
+def test_basic_range_tracks_residual(ctx):
+    # test_rangefinder.cpp:43-71
+    sig = geometric(12, 0.5)
+    from oracle.oracle import get
+    a = planted(get("port"), 30, 20, sig, seed=11)
+    rb = rf.basic_range(a, 8, 4, 3, ctx=ctx)
+    assert rb.Q.shape == (30, 12)
+    assert np.abs(rb.Q.T @ rb.Q - np.eye(12)).max() < 1e-13
+    assert np.linalg.norm(a - rb.Q @ rb.B) < 1e-12 * np.linalg.norm(a)
+    assert rb.residual_frob < 1e-7 * np.linalg.norm(a)
+    pb = rf.basic_range(a, 6, 2, 3, ctx=ctx)
+    direct = np.linalg.norm(a - pb.Q @ pb.B)
+    assert direct > 1e-4 * np.linalg.norm(a)
+    assert abs(pb.residual_frob - direct) <= 1e-9 * direct
+
+
+def test_rsvd_exact_rank_recovery(ctx, port):
+    # test_lowrank.cpp:42-55: planted rank 6, k=6, p=4 -> orth drops columns
+    sig = geometric(6, 0.7)
+    a = planted(port, 30, 20, sig, seed=3)
+    f = rf.rsvd(a, 6, 4, 0, 11, ctx=ctx)
+    assert f.U.shape == (30, 6) and f.V.shape == (20, 6) and f.D.shape == (6,)
+    assert np.abs(f.U.T @ f.U - np.eye(6)).max() < 1e-12
+    assert np.abs(f.V.T @ f.V - np.eye(6)).max() < 1e-12
+    assert np.linalg.norm(a - recon(f)) < 1e-10 * np.linalg.norm(a)
+    assert rel(f.D, sig).max() < 1e-9
+
+
+def test_rsvd_keep_oversamples_matches_projection(ctx, port):
+    # test_lowrank.cpp:68-87
+    sig = geometric(16, 0.6)
+    a = planted(port, 35, 25, sig, seed=9)
+    f = rf.rsvd(a, 5, 4, 1, 13, keep_oversamples=True, ctx=ctx)
+    assert f.D.shape == (9,)
+    rb = rf.power_range(a, 5, 4, 1, 13, ctx=ctx)
+    e1 = np.linalg.norm(a - recon(f))
+    e2 = np.linalg.norm(a - rb.Q @ (rb.Q.T @ a))
+    assert abs(e1 - e2) <= 1e-10 * e2
+
+
+def test_rsvd_plain_power_mode_matches_oracle(ctx, port):
+    # reorthonormalize = false (reference default): sketch (A A^T)^q A G then
+    # one orth; ill-conditioned for q >= 1, exercised through the
+    # Gram-Schmidt fallback. Parity floor ~1e-7 per value.
+    sig = 1.0 / np.arange(1, 301, dtype=np.float64) ** 2
+    a = planted(port, 400, 300, sig)
+    for q in (0, 1):
+        want = port.rsvd(a, 20, 10, q, 7, False, False)
+        got = rf.rsvd(a, 20, 10, q, 7, ctx=ctx)
+        assert got.D.shape == want.D.shape
+        assert rel(got.D, want.D).max() < 1e-6
+        r1, r2 = np.linalg.norm(a - recon(got)), np.linalg.norm(a - recon(want))
+        assert abs(r1 - r2) <= 0.01 * r2
+
+
+def test_rsvd_deterministic(ctx, port):
+    sig = geometric(10, 0.5)
+    a = planted(port, 25, 20, sig, seed=2)
+    f1 = rf.rsvd(a, 4, 4, 1, 7, ctx=ctx)
+    f2 = rf.rsvd(a, 4, 4, 1, 7, ctx=ctx)
+    assert np.array_equal(f1.U, f2.U) and np.array_equal(f1.D, f2.D)
+    f3 = rf.rsvd(a, 4, 4, 1, 8, ctx=ctx)
+    assert not np.array_equal(f1.U, f3.U)
+
+
+def test_rsvd_zero_matrix(ctx):
+    f = rf.rsvd(np.zeros((12, 9)), 3, 2, 0, 1, ctx=ctx)
+    assert f.U.shape[1] == 0 and f.D.size == 0
+
+
+def test_rsvd_validation(ctx, port):
+    a = planted(port, 10, 8, geometric(4, 0.5), seed=1)
+    with pytest.raises(rf.ParameterError):
+        rf.rsvd(a, 0, 2, 0, 1, ctx=ctx)
+    with pytest.raises(rf.ParameterError):
+        rf.rsvd(a, 5, 4, 0, 1, ctx=ctx)
+    with pytest.raises(rf.ParameterError):
+        rf.rsvd(a, 2, 2, -1, 1, ctx=ctx)
+    with pytest.raises(rf.ParameterError):
+        rf.basic_range(a, 2, 2, 1, q=1, ctx=ctx)

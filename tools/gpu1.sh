@@ -1,0 +1,3 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 600 python -m pytest tests/test_gpu_rsvd.py -x -q 2>&1 | tail -40
