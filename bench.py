@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""bench.py — RSVD time-to-rank-k on BASELINE.json config 3 (tall RSVD, FP64).
+
+Workload (BASELINE.json configs[2], the 1/2/4/8-GPU tall-matrix config the
+metric is quoted on): A = U_r diag(s) V_r^T + 1e-8 N, m = 1,048,576,
+n = 4096, r = 1024, s_j = j^-1.5, U_r / V_r orthonormal Q factors of seeded
+Gaussians, N i.i.d. Gaussian; rsvd(A, k=200, p=20, q=1, reorthonormalize=true)
+with G = gaussian(1, "range.G", n, 220) from the reference generator. A is
+row-sharded over the ranks (strong scaling: the matrix is fixed, N GPUs share
+its rows); the only collectives are NCCL allreduces of the n x l products and
+the l x l Grams. Synthetic data generated on the device (seeded torch RNG per
+64Ki-row chunk, so every N sees the same A); A (34.4 GB) is larger than L2, so
+no flush is needed between steps.
+
+`value` = device-resident time per rsvd call (A, G already in HBM; CUDA
+events on the library's stream; max over ranks). `e2e` = the same call made
+through the public C ABI with HOST buffers: upload of A from pinned memory,
+rfgpu_rsvd, and the D2H of U, D, V, all inside the timed region.
+
+--impl reference runs the reference's own CPU implementation (oracle/_ref,
+compiled from /root/reference/proj/src) on a bounded row sample of the same
+workload on all host cores and extrapolates linearly in m.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (m, n, k, p, q, r, spectrum, noise)
+    "c3": dict(m=1048576, n=4096, k=200, p=20, q=1, r=1024, spectrum="pow1.5", noise=1e-8),
+    "c2": dict(m=20000, n=10000, k=100, p=10, q=2, r=500, spectrum="exp20", noise=1e-6),
+    "c1": dict(m=2000, n=2000, k=50, p=10, q=1, r=2000, spectrum="pow2", noise=0.0),
+}
+CHUNK = 65536
+SEED = 1
+FP64_PEAK_TFLOPS = 37.1  # DMMA m8n8k4 burst, profiles/r01_fp_peaks.txt (MEASURED_PEAKS.json has no FP64 entry)
+
+
+def spectrum(kind, r):
+    j = np.arange(1, r + 1, dtype=np.float64)
+    if kind == "pow1.5":
+        return j ** -1.5
+    if kind == "exp20":
+        return np.exp(-j / 20.0)
+    if kind == "pow2":
+        return 1.0 / j ** 2
+    raise ValueError(kind)
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ----------------------------------------------------------------- GPU data ---
+def gen_shard(torch, dist, w, row0, row1, dev):
+    """A^T for rows [row0, row1) as an (n, rows) float64 tensor (= A col-major, lda = rows)."""
+    m, n, r = w["m"], w["n"], w["r"]
+    sig = torch.tensor(spectrum(w["spectrum"], r), device=dev, dtype=torch.float64)
+    g = torch.Generator(device=dev)
+    g.manual_seed(SEED * 7919 + 2)
+    V, _ = torch.linalg.qr(torch.randn(n, r, generator=g, device=dev, dtype=torch.float64))
+    rows = row1 - row0
+    U = torch.empty(rows, r, device=dev, dtype=torch.float64)
+    for c0 in range((row0 // CHUNK) * CHUNK, row1, CHUNK):
+        g.manual_seed(SEED * 1000003 + c0 // CHUNK)
+        blk = torch.randn(CHUNK, r, generator=g, device=dev, dtype=torch.float64)
+        a0, a1 = max(c0, row0), min(c0 + CHUNK, row1)
+        U[a0 - row0:a1 - row0] = blk[a0 - c0:a1 - c0]
+        del blk
+    for _ in range(2):  # CholeskyQR2 of the distributed Gaussian -> orthonormal Q factor
+        gram = U.T @ U
+        if dist is not None:
+            dist.all_reduce(gram)
+        R = torch.linalg.cholesky(gram, upper=True)
+        U = torch.linalg.solve_triangular(R, U, upper=True, left=False)
+    At = (V * sig) @ U.T  # n x rows
+    del U, V
+    if w["noise"]:
+        for c0 in range((row0 // CHUNK) * CHUNK, row1, CHUNK):
+            g.manual_seed(SEED * 2000003 + c0 // CHUNK)
+            blk = torch.randn(n, CHUNK, generator=g, device=dev, dtype=torch.float64)
+            a0, a1 = max(c0, row0), min(c0 + CHUNK, row1)
+            At[:, a0 - row0:a1 - row0].add_(blk[:, a0 - c0:a1 - c0], alpha=w["noise"])
+            del blk
+    return At.contiguous()
+
+
+# ------------------------------------------------------------------ clocks ---
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(device), "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons, pw = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------- reference ---
+def cpu_sample_matrix(w, rows):
+    """Row sample (rows x n) of the workload's distribution, built on the host."""
+    rng = np.random.default_rng(SEED)
+    n, r = w["n"], w["r"]
+    V, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    U, _ = np.linalg.qr(rng.standard_normal((rows, r)))
+    U *= np.sqrt(rows / w["m"])  # rows of an m-row orthonormal factor have this scale
+    a = (U * spectrum(w["spectrum"], r)) @ V.T
+    if w["noise"]:
+        a += w["noise"] * rng.standard_normal((rows, n))
+    return np.asfortranarray(a)
+
+
+def run_reference_rsvd(w, a_sample, threads):
+    from oracle.oracle import get
+    ref = get("reference")
+    ref.set_threads(threads)
+    t0 = time.perf_counter()
+    ref.rsvd(a_sample, w["k"], w["p"], w["q"], SEED, False, True)
+    return time.perf_counter() - t0
+
+
+def sample_rows_for(w, budget_rows):
+    return max(w["n"], min(w["m"], budget_rows))
+
+
+def reference_arm(args, w, rank, world):
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    rows = sample_rows_for(w, args.ref_rows)
+    a = cpu_sample_matrix(w, rows)
+    scale = w["m"] / rows
+    for _ in range(args.warmup):
+        run_reference_rsvd(w, a, threads)
+    times = [run_reference_rsvd(w, a, threads) * scale for _ in range(args.steps)]
+    val = statistics.mean(times)
+    sample = (f"reference rsvd(A_sample, k={w['k']}, p={w['p']}, q={w['q']}, reorth=true) on a {rows}x{w['n']} "
+              f"row sample (1/{scale:g} of config rows), time scaled x{scale:g} (linear in m)")
+    line = {
+        "metric": "rsvd_time_to_rank_k", "value": val, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (planted spectrum, seeded)", "impl": "reference",
+        "config": config_of(w, world, args),
+        "cpu_baseline": {"value": val, "unit": "s", "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_of(w, world, args):
+    return {"workload": f"{args.workload}: tall RSVD fp64 m={w['m']} n={w['n']} k={w['k']} p={w['p']} q={w['q']} "
+                        f"reorthonormalize=true", "m": w["m"], "n": w["n"], "k": w["k"], "p": w["p"], "q": w["q"],
+            "rank_planted": w["r"], "noise": w["noise"], "seed": SEED, "parallelism": f"row-shard x{world}",
+            "l2": "A (8*m*n bytes) larger than L2; no flush needed"}
+
+
+# --------------------------------------------------------------------- main ---
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="rfgpu", choices=["rfgpu", "reference"])
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-rows", type=int, default=8192, help="row sample for the CPU reference")
+    args = ap.parse_args()
+    w = WORKLOADS[args.workload]
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+
+    if args.impl == "reference":
+        return reference_arm(args, w, rank, world)
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl")
+        dist = tdist
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    import paper_1607_01649_b200 as rf
+    L = rf.lib()
+    if world > 1:
+        obj = [rf.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = rf.Context(local, rank, world, obj[0])
+    else:
+        ctx = rf.Context(local)
+
+    m, n, k, p, q = w["m"], w["n"], w["k"], w["p"], w["q"]
+    ell = k + p
+    row0, row1 = m * rank // world, m * (rank + 1) // world
+    mloc = row1 - row0
+    At = gen_shard(torch, dist, w, row0, row1, dev)
+    torch.cuda.synchronize()
+    A = rf.DeviceMatrix.wrap(ctx, At.data_ptr(), mloc, n, mloc, keep=At)
+    G = torch.from_numpy(rf.gaussian(SEED, "range.G", n, ell).reshape(-1, order="F")).to(dev)
+    Ud = torch.empty(mloc * ell, device=dev, dtype=torch.float64)
+    Dd = torch.empty(ell, device=dev, dtype=torch.float64)
+    Vd = torch.empty(n * ell, device=dev, dtype=torch.float64)
+    rank_out = C.c_int64()
+
+    def step():
+        rf._check(L.rfgpu_rsvd_device(ctx.handle, A.handle, C.c_void_p(G.data_ptr()), k, ell, q, 0, 1,
+                                      C.c_void_p(Ud.data_ptr()), C.c_void_p(Dd.data_ptr()),
+                                      C.c_void_p(Vd.data_ptr()), C.byref(rank_out)))
+
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    ctx.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ctx.profile(True)
+    ctx.profile_reset()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    ev1.synchronize()
+    clocks = sampler.stop()
+    ctx.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    launches = ctx.launch_count() // args.steps
+    prof = {nm: ctx.profile_read(nm) for nm in ("pass_nn", "pass_tn", "orth", "small_svd", "gemm_nn", "gemm_tn",
+                                                "allreduce")}
+    ctx.profile(False)
+    n_pass = prof["pass_nn"][0] + prof["pass_tn"][0]
+    pass_ms = prof["pass_nn"][1] + prof["pass_tn"][1]
+    flops_per_pass = 2.0 * mloc * n * ell
+    achieved = flops_per_pass * n_pass / (pass_ms * 1e-3) / 1e12 if pass_ms > 0 else None
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get(args.workload)
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the host-buffer C ABI (upload + rsvd + D2H) -----------
+    e2e = None
+    if not args.no_e2e:
+        try:
+            Ah = torch.empty((n, mloc), dtype=torch.float64, pin_memory=True)
+            Ah.copy_(At)
+            Gh = rf.gaussian(SEED, "range.G", n, ell)
+            Uh = torch.empty(mloc * ell, dtype=torch.float64, pin_memory=True)
+            Vh = torch.empty(n * ell, dtype=torch.float64, pin_memory=True)
+            Dh = np.zeros(ell)
+            gflat = np.asfortranarray(Gh).reshape(-1, order="F")
+
+            def e2e_step():
+                h = C.c_void_p()
+                rf._check(L.rfgpu_matrix_upload(ctx.handle, C.cast(C.c_void_p(Ah.data_ptr()), rf._pd), mloc, n, mloc,
+                                                 C.byref(h)))
+                try:
+                    rf._check(L.rfgpu_rsvd(ctx.handle, h, rf._dp(gflat), k, ell, q, 0, 1,
+                                           C.cast(C.c_void_p(Uh.data_ptr()), rf._pd), rf._dp(Dh),
+                                           C.cast(C.c_void_p(Vh.data_ptr()), rf._pd), C.byref(rank_out)))
+                finally:
+                    L.rfgpu_matrix_free(h)
+
+            e2e_step()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                e2e_step()
+            e1.record(stream)
+            e1.synchronize()
+            e2e_s = max_over_ranks(e0.elapsed_time(e1) / args.steps) / 1e3
+            kk = rank_out.value
+            e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(8 * (mloc * n + n * ell)),
+                   "d2h_bytes_per_step": int(8 * (mloc * kk + n * kk + kk))}
+            del Ah, Uh, Vh
+        except Exception as ex:  # report, never hide
+            e2e = {"value": None, "unit": "s", "error": f"{type(ex).__name__}: {ex}"}
+
+    # ---- CPU baseline (reference, bounded sample), rank 0 at N=1 ------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows = sample_rows_for(w, args.ref_rows)
+        a_s = np.asfortranarray(At[:, :rows].T.cpu().numpy())
+        threads = os.cpu_count() or 1
+        t = run_reference_rsvd(w, a_s, threads)
+        scale = m / rows
+        cpu = {"value": t * scale, "unit": "s", "cores": threads, "kind": "reference",
+               "sample": f"reference rsvd (reorth=true) on the first {rows} rows of this A ({rows}x{n}); "
+                         f"{t:.2f} s measured, scaled x{scale:g} (linear in m)"}
+
+    if rank == 0:
+        line = {
+            "metric": "rsvd_time_to_rank_k", "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (planted spectrum, seeded torch RNG on device)",
+            "config": config_of(w, world, args),
+            "sketch_tflops": achieved,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
+                         "kernel": "gemm_f64_kernel (passes over A: pass_nn + pass_tn)",
+                         "per_launch_flops": flops_per_pass, "passes_per_step": n_pass / args.steps,
+                         "pass_ms_avg": pass_ms / n_pass if n_pass else None,
+                         "peak_source": "FP64 DMMA microbenchmark profiles/r01_fp_peaks.txt (no FP64 entry in "
+                                        "MEASURED_PEAKS.json)"},
+            "phase_ms_per_step": {nm: v[1] / args.steps for nm, v in prof.items()},
+            "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    A.free()
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

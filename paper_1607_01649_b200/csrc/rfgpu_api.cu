@@ -280,17 +280,16 @@ Status allreduce(rfgpu_ctx* c, double* buf, int64_t count) {
 // ---- GEMM wrapper -----------------------------------------------------------
 Status gemm(rfgpu_ctx* c, bool trans, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
             const double* B, int64_t ldb, double* C, int64_t ldc, double* sumsq_partials = nullptr,
-            int* sumsq_count = nullptr) {
+            const char* label = nullptr) {
   if (M <= 0 || N <= 0) return {};
   const GemmPlan p = plan_gemm(M, N, K, c->num_sms);
   DBuf ws;
   const size_t wb = gemm_workspace_bytes(M, N, p);
   if (wb) RF_TRY(ws.alloc(wb, c->stream));
   {
-    Timed t(c, trans ? "gemm_tn" : "gemm_nn");
+    Timed t(c, label ? label : (trans ? "gemm_tn" : "gemm_nn"));
     RF_CUDA(gemm_f64(trans, M, N, K, A, lda, B, ldb, C, ldc, ws.d(), wb, sumsq_partials, p, c->stream));
   }
-  if (sumsq_count) *sumsq_count = p.splits * p.mtiles;
   return {};
 }
 
@@ -418,32 +417,32 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
   RF_CUDA(cudaMemsetAsync(ssq.d(), 0, sizeof(double) * std::max<int64_t>(1, slots), st));
 
   // pass 1: Y = A G, with ||A||_F^2 fused
-  RF_TRY(gemm(c, false, m, ell, n, A, lda, G, n, y.d(), ldq, ssq.d()));
+  RF_TRY(gemm(c, false, m, ell, n, A, lda, G, n, y.d(), ldq, ssq.d(), "pass_nn"));
   RF_CUDA(sum_array(ssq.d(), slots, scal.d(), st));
   RF_TRY(allreduce(c, scal.d(), 1));
 
   int64_t r = ell;
   if (!reorth) {
     for (int64_t j = 0; j < q; ++j) {
-      RF_TRY(gemm(c, true, n, ell, m, A, lda, y.d(), ldq, z.d(), n));
+      RF_TRY(gemm(c, true, n, ell, m, A, lda, y.d(), ldq, z.d(), n, nullptr, "pass_tn"));
       RF_TRY(allreduce(c, z.d(), n * ell));
-      RF_TRY(gemm(c, false, m, ell, n, A, lda, z.d(), n, y.d(), ldq));
+      RF_TRY(gemm(c, false, m, ell, n, A, lda, z.d(), n, y.d(), ldq, nullptr, "pass_nn"));
     }
     RF_TRY(orth(c, y.d(), m, ell, ldq, Q, ldq, &r, nullptr, true));
   } else {
     RF_TRY(orth(c, y.d(), m, ell, ldq, Q, ldq, &r, nullptr, true));
     for (int64_t j = 0; j < q && r > 0; ++j) {
       int64_t rw = 0;
-      RF_TRY(gemm(c, true, n, r, m, A, lda, Q, ldq, z.d(), n));
+      RF_TRY(gemm(c, true, n, r, m, A, lda, Q, ldq, z.d(), n, nullptr, "pass_tn"));
       RF_TRY(allreduce(c, z.d(), n * r));
       RF_TRY(orth(c, z.d(), n, r, n, w.d(), n, &rw, nullptr, false));
-      RF_TRY(gemm(c, false, m, rw, n, A, lda, w.d(), n, y.d(), ldq));
+      RF_TRY(gemm(c, false, m, rw, n, A, lda, w.d(), n, y.d(), ldq, nullptr, "pass_nn"));
       RF_TRY(orth(c, y.d(), m, rw, ldq, Q, ldq, &r, nullptr, true));
     }
   }
   // projection: B^T = A^T Q
   if (r > 0) {
-    RF_TRY(gemm(c, true, n, r, m, A, lda, Q, ldq, Bt, n));
+    RF_TRY(gemm(c, true, n, r, m, A, lda, Q, ldq, Bt, n, nullptr, "pass_tn"));
     RF_TRY(allreduce(c, Bt, n * r));
   }
   RF_CUDA(cudaMemcpyAsync(c->h_d, scal.d(), sizeof(double), cudaMemcpyDeviceToHost, st));
