@@ -16,6 +16,8 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -316,16 +318,16 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
   const int64_t cc = cols * cols;
   DBuf small;
   // G1, R1, R1inv, G2, R2, R2inv, chol work, Q1 separately
-  RF_TRY(small.alloc(sizeof(double) * (6 * cc + 2 * cc + 16) + 64, st));
+  RF_TRY(small.alloc(sizeof(double) * (6 * cc + 16) + chol_inv_work_bytes(cols) + 64, st));
   double* G1 = small.d();
   double* R1 = G1 + cc;
   double* R1i = R1 + cc;
   double* G2 = R1i + cc;
   double* R2 = G2 + cc;
   double* R2i = R2 + cc;
-  double* cwork = R2i + cc;  // 2cc
-  double* infod = cwork + 2 * cc;  // 2 doubles
-  int* info = reinterpret_cast<int*>(infod + 4);  // 2 ints
+  double* infod = R2i + cc;  // 2 doubles (+pad)
+  double* cwork = infod + 8;  // chol_inv_work_bytes(cols)
+  int* info = reinterpret_cast<int*>(infod + 4);  // 2 ints (inside the pad)
   DBuf q1;
   const int64_t ldq1 = even(m);
   RF_TRY(q1.alloc(sizeof(double) * std::max<int64_t>(1, ldq1 * cols), st));
@@ -379,16 +381,23 @@ Status small_svd_of_bt(rfgpu_ctx* c, const double* Bt, int64_t n, int64_t ell, d
     RF_TRY(ur.alloc(sizeof(double) * ell * ell, st));
     const size_t jwb = jacobi_work_bytes(ell, ell);
     if (jwb) RF_TRY(jw.alloc(jwb, st));
-    RF_CUDA(jacobi_svd(rb.d(), ell, ell, ur.d(), D, Ub, jw.d(), info, info + 1, st));
+    {
+      Timed tj(c, "jacobi");
+      RF_CUDA(jacobi_svd(rb.d(), ell, ell, ur.d(), D, Ub, jw.d(), info, info + 1, st));
+    }
     RF_TRY(gemm(c, false, n, ell, ell, qb.d(), ldn, ur.d(), ell, Vb, n));
   } else {
     // rank-deficient / ill-conditioned B: Jacobi directly on the tall Bt
     const size_t jwb = jacobi_work_bytes(n, ell);
     if (jwb) RF_TRY(jw.alloc(jwb, st));
+    Timed tj(c, "jacobi");
     RF_CUDA(jacobi_svd(Bt, n, ell, Vb, D, Ub, jw.d(), info, info + 1, st));
   }
   RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));
+  if (std::getenv("RFGPU_DEBUG"))
+    std::fprintf(stderr, "[rfgpu] small_svd ell=%lld fast=%d jacobi info=%d sweeps=%d\n", (long long)ell, (int)fast,
+                 c->h_info[0], c->h_info[1]);
   if (c->h_info[0] == 1) return make_err(RFGPU_ECONVERGENCE, "svd_dense: Jacobi sweeps did not converge");
   return {};
 }

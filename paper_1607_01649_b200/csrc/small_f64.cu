@@ -28,45 +28,37 @@ namespace {
 constexpr int kSmallThreads = 1024;
 
 // ------------------------------------------------------------ chol_inv ---
-// Augmented elimination on M = [G | I] (c x 2c, row-major, W = 2c): row j is
-// scaled by 1/sqrt(pivot) and eliminated from the trailing rows, so the left
-// block becomes R and the right block L^{-1} = R^{-T}.
-template <bool SMEM>
+// Packed upper-triangular storage P (column-packed: (i, j) at j(j+1)/2 + i,
+// i <= j), in shared memory when it fits (c <= 236), else in global memory.
+// Phase 1: right-looking Cholesky in the reference recurrence order
+// (dense.cpp:763-786): row j is divided by sqrt(pivot), then each trailing
+// entry (i, col), j < i <= col, subtracts R(j,i) R(j,col).
+// Phase 2: R^{-1} one warp per column: back substitution R x = e_j in axpy
+// form, x distributed over the lanes' registers (S slots per lane).
+__device__ __forceinline__ int64_t pk(int i, int j) { return static_cast<int64_t>(j) * (j + 1) / 2 + i; }
+
+template <bool SMEM, int S>
 __global__ void __launch_bounds__(kSmallThreads, 1)
     chol_inv_kernel(const double* __restrict__ G, int c, double* __restrict__ R, double* __restrict__ Rinv,
                     double* __restrict__ work, int* info, double* info_d) {
   extern __shared__ double sm[];
-  double* M = SMEM ? sm : work;
-  const int W = 2 * c;
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  __shared__ double s_floor, s_trace, s_minratio, s_cjj;
+  double* base = SMEM ? sm : work;
+  double* rowj = base;          // [c]  current pivot row of R
+  double* rdiag = base + c;     // [c]  1 / R(j,j)
+  double* P = base + 2 * c;     // packed upper triangle
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  __shared__ double s_floor, s_trace, s_minratio;
   __shared__ int s_fail;
-  __shared__ double red[32];
 
-  for (int e = tid; e < c * W; e += nthr) {
-    const int i = e / W, col = e % W;
-    double v;
-    if (col < c) {
-      const int a = min(i, col), b = max(i, col);
-      v = G[static_cast<int64_t>(b) * c + a];  // upper triangle of G (col-major)
-    } else {
-      v = (col - c == i) ? 1.0 : 0.0;
-    }
-    M[e] = v;
-  }
-  double md = 0.0, tr = 0.0;
-  for (int j = tid; j < c; j += nthr) {
-    const double g = G[static_cast<int64_t>(j) * c + j];
-    md = fmax(md, fabs(g));
-  }
-  // block max via shuffles
-  for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
-  if ((tid & 31) == 0) red[tid >> 5] = md;
-  __syncthreads();
+  for (int j = warp; j < c; j += nwarps)
+    for (int i = lane; i <= j; i += 32) P[pk(i, j)] = G[static_cast<int64_t>(j) * c + i];
   if (tid == 0) {
-    double mx = 0.0;
-    for (int w = 0; w < nthr / 32; ++w) mx = fmax(mx, red[w]);
-    for (int j = 0; j < c; ++j) tr += G[static_cast<int64_t>(j) * c + j];
+    double mx = 0.0, tr = 0.0;
+    for (int j = 0; j < c; ++j) {
+      const double g = G[static_cast<int64_t>(j) * c + j];
+      mx = fmax(mx, fabs(g));
+      tr += g;
+    }
     s_floor = 1e-14 * mx;
     s_trace = tr;
     s_minratio = INFINITY;
@@ -76,46 +68,83 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
 
   for (int j = 0; j < c; ++j) {
     if (tid == 0) {
-      const double d = M[j * W + j];
+      const double d = P[pk(j, j)];
       if (d <= s_floor || !(d > 0.0)) {
         s_fail = j + 1;
       } else {
         s_minratio = fmin(s_minratio, s_trace > 0.0 ? d / s_trace : 0.0);
-        s_cjj = sqrt(d);
+        const double cjj = sqrt(d);
+        P[pk(j, j)] = cjj;
+        rowj[j] = cjj;
+        rdiag[j] = 1.0 / cjj;
       }
     }
     __syncthreads();
     if (s_fail) break;
-    const double cjj = s_cjj;
-    // scale row j: left columns > j, right columns c..c+j
-    for (int col = j + 1 + tid; col <= c + j; col += nthr) M[j * W + col] = M[j * W + col] / cjj;
-    if (tid == 0) M[j * W + j] = cjj;
+    const double cjj = rowj[j];
+    for (int col = j + 1 + tid; col < c; col += nthr) {
+      const double v = P[pk(j, col)] / cjj;
+      P[pk(j, col)] = v;
+      rowj[col] = v;
+    }
     __syncthreads();
-    // eliminate rows i > j over columns j+1 .. c+j (left part: col >= i only)
-    const int rows = c - j - 1, width = c;
-    const int total = rows * width;
-    for (int e = tid; e < total; e += nthr) {
-      const int i = j + 1 + e / width;
-      const int col = j + 1 + e % width;
-      if (col < c && col < i) continue;
-      M[i * W + col] -= M[j * W + i] * M[j * W + col];
+    for (int col = j + 1 + warp; col < c; col += nwarps) {
+      const double rc = rowj[col];
+      double* pc = P + pk(0, col);
+      for (int i = j + 1 + lane; i <= col; i += 32) pc[i] -= rowj[i] * rc;
     }
     __syncthreads();
   }
-
   if (tid == 0) {
     info[0] = s_fail;
     info_d[0] = s_minratio;
   }
   if (s_fail) return;
-  for (int e = tid; e < c * c; e += nthr) {
-    const int col = e / c, i = e % c;  // column-major output index
-    R[e] = (i <= col) ? M[i * W + col] : 0.0;
-    Rinv[e] = (i <= col) ? M[col * W + c + i] : 0.0;  // Rinv(i, col) = Linv(col, i)
+
+  for (int j = warp; j < c; j += nwarps)
+    for (int i = lane; i < c; i += 32) R[static_cast<int64_t>(j) * c + i] = i <= j ? P[pk(i, j)] : 0.0;
+
+  // Phase 2: column j of R^{-1}: x = e_j; for i = j..0: x_i /= R(i,i);
+  // x[0:i) -= x_i R(0:i, i).
+  for (int j = warp; j < c; j += nwarps) {
+    double x[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) x[s] = (lane + 32 * s == j) ? 1.0 : 0.0;
+    for (int i = j; i >= 0; --i) {
+      const int si = i >> 5, owner = i & 31;
+      double v = 0.0;
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        if (s == si) v = x[s];
+      const double xi = __shfl_sync(0xffffffffu, v, owner) * rdiag[i];
+      const double* pc = P + pk(0, i);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int r = lane + 32 * s;
+        if (r == i) x[s] = xi;
+        else if (r < i) x[s] = fma(-xi, pc[r], x[s]);
+      }
+    }
+    double* out = Rinv + static_cast<int64_t>(j) * c;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int r = lane + 32 * s;
+      if (r < c) out[r] = r <= j ? x[s] : 0.0;
+    }
   }
 }
 
 // ----------------------------------------------------------- jacobi_svd ---
+// Round-robin parallel one-sided Jacobi. The rows of X (mr x c) and V (c x c)
+// are split over the P CTAs of a cluster; inside a CTA the 32 warps form
+// G pair-groups x H row-groups: lane k of a warp owns column pair
+// 32*g + k of the round, the warp owns a row slice. Per round:
+//   A. partial (app, aqq, apq) over the warp's rows      -> red[h][k]
+//   B. row-group reduction (fixed order), pushed to every CTA's pbuf[q][k]
+//   C. one warp per pair-group sums the P CTA partials (fixed order) and
+//      computes the rotation (reference formula, dense.cpp:624-644)
+//   D. every warp rotates its row slice of X and V.
+// Decisions are bitwise identical in all CTAs (same sums, same order).
 struct JacobiParams {
   const double* X;
   int64_t mr;  // rows of X
@@ -123,9 +152,10 @@ struct JacobiParams {
   double* U;
   double* S;
   double* V;
-  double* gX;  // global staging (mode without smem residency), [P][c][RX]
-  double* gV;  // [P][c][RV]
+  double* gX;  // global staging when X/V rows do not fit in shared memory
+  double* gV;
   int RX, RV;  // rows of X / V owned per CTA
+  int LDX, LDV;
   int* info;
   int* sweeps_out;
 };
@@ -133,18 +163,20 @@ struct JacobiParams {
 __device__ __forceinline__ void pair_of(int r, int k, int cc, int* a, int* b) {
   // circle-method round-robin on cc (even) logical positions
   const int n = cc - 1;
+  int x, y;
   if (k == 0) {
-    *a = 0;
-    *b = 1 + (r % n);
+    x = 0;
+    y = 1 + r;  // r < n
   } else {
-    *a = 1 + (r + k) % n;
-    *b = 1 + (r - k + n) % n;
+    int t = r + k;
+    if (t >= n) t -= n;
+    x = 1 + t;
+    t = r - k;
+    if (t < 0) t += n;
+    y = 1 + t;
   }
-  if (*a > *b) {
-    const int t = *a;
-    *a = *b;
-    *b = t;
-  }
+  *a = min(x, y);
+  *b = max(x, y);
 }
 
 template <bool SMEM>
@@ -153,147 +185,181 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
   const int P = static_cast<int>(cluster.num_blocks());
   const int q = static_cast<int>(cluster.block_rank());
   const int c = p.c, cc = c + (c & 1), npairs = cc / 2;
-  const int RX = p.RX, RV = p.RV;
+  const int RX = p.RX, RV = p.RV, LDX = p.LDX, LDV = p.LDV;
   const int64_t r0x = static_cast<int64_t>(q) * RX;
   const int64_t rem_x = p.mr - r0x;
   const int nrx = rem_x <= 0 ? 0 : static_cast<int>(rem_x < RX ? rem_x : RX);
   const int r0v = q * RV;
   const int nrv = max(0, min(RV, c - r0v));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int G = (npairs + 31) / 32;
+  const int H = nwarps / G;  // row groups (>= 1 since npairs <= 1024)
+  const int g = warp % G, h = warp / G;
+  const bool active = h < H;
+  const int k = g * 32 + lane;  // pair owned by this lane
+  const int rhx = (nrx + H - 1) / H, rhv = (nrv + H - 1) / H;
+  const int x0 = min(nrx, h * rhx), x1 = min(nrx, x0 + rhx);
+  const int v0 = min(nrv, h * rhv), v1 = min(nrv, v0 + rhv);
 
   extern __shared__ double sm[];
-  // layout: [X rows (c*RX)] [V rows (c*RV)] (SMEM only) | partials[2][P][npairs*3] | nrm[P][cc] | perm, cs/sn
   double* Xs;
   double* Vs;
-  double* part;
+  double* rest;
   if (SMEM) {
     Xs = sm;
-    Vs = sm + static_cast<size_t>(c) * RX;
-    part = Vs + static_cast<size_t>(c) * RV;
+    Vs = sm + static_cast<size_t>(c) * LDX;
+    rest = Vs + static_cast<size_t>(c) * LDV;
   } else {
-    Xs = p.gX + static_cast<size_t>(q) * c * RX;
-    Vs = p.gV + static_cast<size_t>(q) * c * RV;
-    part = sm;
+    Xs = p.gX + static_cast<size_t>(q) * c * LDX;
+    Vs = p.gV + static_cast<size_t>(q) * c * LDV;
+    rest = sm;
   }
-  double* nrmp = part + 2 * P * npairs * 3;        // [P][cc]
-  double* csn = nrmp + P * cc;                      // [npairs][2]
-  int* perm = reinterpret_cast<int*>(csn + 2 * npairs);  // [cc]
-  int* rotflag = perm + cc;                         // [npairs]
+  const int np3 = npairs * 3;
+  double* red = rest;                    // [H][npairs][3]
+  double* pbuf = red + H * np3;          // [2][P][npairs][3]
+  double* rot = pbuf + 2 * P * np3;      // [npairs][2]
+  double* nrmp = rot + 2 * npairs;       // [P][cc]
+  double* nrm = nrmp + P * cc;           // [cc]
+  int* perm = reinterpret_cast<int*>(nrm + cc);  // [cc]
   __shared__ int s_rotated, s_conv;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-
-  // load owned rows; V = I
   for (int e = tid; e < c * RX; e += blockDim.x) {
     const int col = e / RX, r = e % RX;
-    Xs[e] = (r < nrx) ? p.X[static_cast<int64_t>(col) * p.mr + r0x + r] : 0.0;
+    Xs[static_cast<size_t>(col) * LDX + r] = (r < nrx) ? p.X[static_cast<int64_t>(col) * p.mr + r0x + r] : 0.0;
   }
   for (int e = tid; e < c * RV; e += blockDim.x) {
     const int col = e / RV, r = e % RV;
-    Vs[e] = (r < nrv && r0v + r == col) ? 1.0 : 0.0;
+    Vs[static_cast<size_t>(col) * LDV + r] = (r < nrv && r0v + r == col) ? 1.0 : 0.0;
   }
   __syncthreads();
 
-  auto exchange_norms = [&]() {
-    // partial squared column norms over owned rows -> every CTA's nrmp[q][*]
+  // Column norms over the owned rows, exchanged across the cluster; nrm[j]
+  // receives the total in fixed rank order.
+  auto norms = [&]() {
     for (int col = warp; col < c; col += nwarps) {
       double s = 0.0;
-      const double* x = Xs + static_cast<size_t>(col) * RX;
+      const double* x = Xs + static_cast<size_t>(col) * LDX;
       for (int r = lane; r < nrx; r += 32) s = fma(x[r], x[r], s);
       s = warp_sum(s);
-      if (lane == 0) {
-        for (int d = 0; d < P; ++d) cluster.map_shared_rank(nrmp, d)[q * cc + col] = s;
-      }
+      if (lane < P) cluster.map_shared_rank(nrmp, lane)[q * cc + col] = s;
     }
     cluster.sync();
-  };
-  auto rank_sort = [&]() {
-    // stable descending sort by total norm (std::stable_sort with >)
     for (int j = tid; j < c; j += blockDim.x) {
-      double nj = 0.0;
-      for (int d = 0; d < P; ++d) nj += nrmp[d * cc + j];
+      double t = 0.0;
+      for (int d = 0; d < P; ++d) t += nrmp[d * cc + j];
+      nrm[j] = t;
+    }
+    __syncthreads();
+  };
+  auto sort_desc = [&](const double* key) {
+    for (int j = tid; j < c; j += blockDim.x) {
+      const double kj = key[j];
       int rank = 0;
       for (int i = 0; i < c; ++i) {
-        double ni = 0.0;
-        for (int d = 0; d < P; ++d) ni += nrmp[d * cc + i];
-        if (ni > nj || (ni == nj && i < j)) ++rank;
+        const double ki = key[i];
+        rank += (ki > kj || (ki == kj && i < j)) ? 1 : 0;
       }
       perm[rank] = j;
     }
-    if (tid == 0 && (c & 1)) perm[c] = -1;  // phantom
+    if (tid == 0 && (c & 1)) perm[c] = -1;  // phantom column
     __syncthreads();
   };
 
-  int sweep = 0;
+  int sweep = 0, parity = 0;
   if (tid == 0) s_conv = (c <= 1);
   __syncthreads();
-  int parity = 0;
   while (!s_conv && sweep < 60) {
-    exchange_norms();
-    rank_sort();
+    norms();
+    sort_desc(nrm);
     if (tid == 0) s_rotated = 0;
     __syncthreads();
     for (int rd = 0; rd < cc - 1; ++rd) {
-      double* pbuf = part + parity * P * npairs * 3;
-      // 1. partial inner products for every pair of this round
-      for (int k = warp; k < npairs; k += nwarps) {
+      int cp = -1, cq = -1;
+      if (active && k < npairs) {
         int a, b;
         pair_of(rd, k, cc, &a, &b);
-        const int cp = perm[a], cq = perm[b];
+        cp = perm[a];
+        cq = perm[b];
+      }
+      const bool valid = cp >= 0 && cq >= 0;
+      // A. partial inner products over this warp's rows
+      if (active && k < npairs) {
         double app = 0.0, aqq = 0.0, apq = 0.0;
-        if (cp >= 0 && cq >= 0) {
-          const double* xp = Xs + static_cast<size_t>(cp) * RX;
-          const double* xq = Xs + static_cast<size_t>(cq) * RX;
-          for (int r = lane; r < nrx; r += 32) {
+        if (valid) {
+          const double* xp = Xs + static_cast<size_t>(cp) * LDX;
+          const double* xq = Xs + static_cast<size_t>(cq) * LDX;
+          for (int r = x0; r < x1; ++r) {
             const double u = xp[r], v = xq[r];
             app = fma(u, u, app);
             aqq = fma(v, v, aqq);
             apq = fma(u, v, apq);
           }
-          app = warp_sum(app);
-          aqq = warp_sum(aqq);
-          apq = warp_sum(apq);
         }
-        if (lane < P) {
-          double* dst = cluster.map_shared_rank(pbuf, lane) + (q * npairs + k) * 3;
+        double* d = red + (h * npairs + k) * 3;
+        d[0] = app;
+        d[1] = aqq;
+        d[2] = apq;
+      }
+      __syncthreads();
+      // B. CTA partial -> every CTA of the cluster
+      double* pb = pbuf + parity * P * np3;
+      if (h == 0 && k < npairs) {
+        double app = 0.0, aqq = 0.0, apq = 0.0;
+        for (int hh = 0; hh < H; ++hh) {
+          const double* s = red + (hh * npairs + k) * 3;
+          app += s[0];
+          aqq += s[1];
+          apq += s[2];
+        }
+        for (int d = 0; d < P; ++d) {
+          double* dst = cluster.map_shared_rank(pb, d) + (q * npairs + k) * 3;
           dst[0] = app;
           dst[1] = aqq;
           dst[2] = apq;
         }
       }
-      cluster.sync();
-      // 2. identical rotation decisions in every CTA; rotate owned rows
-      for (int k = warp; k < npairs; k += nwarps) {
-        int a, b;
-        pair_of(rd, k, cc, &a, &b);
-        const int cp = perm[a], cq = perm[b];
-        if (cp < 0 || cq < 0) continue;
+      if (P > 1) cluster.sync();
+      else __syncthreads();
+      // C. rotation parameters (one lane per pair)
+      if (h == 0 && k < npairs) {
         double app = 0.0, aqq = 0.0, apq = 0.0;
         for (int d = 0; d < P; ++d) {
-          const double* s = pbuf + (d * npairs + k) * 3;
+          const double* s = pb + (d * npairs + k) * 3;
           app += s[0];
           aqq += s[1];
           apq += s[2];
         }
-        if (app == 0.0 || aqq == 0.0) continue;
-        if (fabs(apq) <= 1e-15 * sqrt(app * aqq)) continue;
-        const double zeta = (aqq - app) / (2.0 * apq);
-        const double t = (zeta < 0.0 ? -1.0 : 1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + t * t);
-        const double sn = cs * t;
-        if (lane == 0) s_rotated = 1;
-        double* xp = Xs + static_cast<size_t>(cp) * RX;
-        double* xq = Xs + static_cast<size_t>(cq) * RX;
-        for (int r = lane; r < nrx; r += 32) {
-          const double u = xp[r], v = xq[r];
-          xp[r] = cs * u - sn * v;
-          xq[r] = sn * u + cs * v;
+        double cs = 1.0, sn = 0.0;
+        bool do_rot = valid && app != 0.0 && aqq != 0.0 && !(fabs(apq) <= 1e-15 * sqrt(app * aqq));
+        if (do_rot) {
+          const double zeta = (aqq - app) / (2.0 * apq);
+          const double t = (zeta < 0.0 ? -1.0 : 1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          cs = 1.0 / sqrt(1.0 + t * t);
+          sn = cs * t;
+          s_rotated = 1;
         }
-        double* vp = Vs + static_cast<size_t>(cp) * RV;
-        double* vq = Vs + static_cast<size_t>(cq) * RV;
-        for (int r = lane; r < nrv; r += 32) {
-          const double u = vp[r], v = vq[r];
-          vp[r] = cs * u - sn * v;
-          vq[r] = sn * u + cs * v;
+        rot[2 * k] = cs;
+        rot[2 * k + 1] = do_rot ? sn : 2.0;  // 2.0 marks "skip"
+      }
+      __syncthreads();
+      // D. rotate this warp's rows of X and V
+      if (active && k < npairs && valid) {
+        const double cs = rot[2 * k], sn = rot[2 * k + 1];
+        if (sn != 2.0) {
+          double* xp = Xs + static_cast<size_t>(cp) * LDX;
+          double* xq = Xs + static_cast<size_t>(cq) * LDX;
+          for (int r = x0; r < x1; ++r) {
+            const double u = xp[r], v = xq[r];
+            xp[r] = cs * u - sn * v;
+            xq[r] = sn * u + cs * v;
+          }
+          double* vp = Vs + static_cast<size_t>(cp) * LDV;
+          double* vq = Vs + static_cast<size_t>(cq) * LDV;
+          for (int r = v0; r < v1; ++r) {
+            const double u = vp[r], v = vq[r];
+            vp[r] = cs * u - sn * v;
+            vq[r] = sn * u + cs * v;
+          }
         }
       }
       __syncthreads();
@@ -306,24 +372,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
   const bool converged = s_conv;
 
   // final singular values, stable descending order
-  exchange_norms();
-  for (int j = tid; j < c; j += blockDim.x) {
-    double nj = 0.0;
-    for (int d = 0; d < P; ++d) nj += nrmp[d * cc + j];
-    nrmp[j] = nj;  // rank-0 slot reused after the sum (all reads of slot d=0 for j done by this thread only)
-  }
+  norms();
+  double* sig = rot;  // 2*npairs >= c doubles
+  for (int j = tid; j < c; j += blockDim.x) sig[j] = sqrt(nrm[j]);
   __syncthreads();
-  // sigma_j = sqrt(total norm); use a separate array to avoid read/write races
-  double* sig = csn;  // npairs*2 >= c doubles
-  for (int j = tid; j < c; j += blockDim.x) sig[j] = sqrt(nrmp[j]);
-  __syncthreads();
-  for (int j = tid; j < c; j += blockDim.x) {
-    int rank = 0;
-    for (int i = 0; i < c; ++i)
-      if (sig[i] > sig[j] || (sig[i] == sig[j] && i < j)) ++rank;
-    perm[rank] = j;
-  }
-  __syncthreads();
+  sort_desc(sig);
   const double smax = c > 0 ? sig[perm[0]] : 0.0;
   int zero_cols = 0;
   for (int j = 0; j < c; ++j) {
@@ -332,9 +385,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
     const bool ok = s > 0.0 && s > smax * 1e-250;
     if (!ok) zero_cols = 1;
     if (q == 0 && tid == 0) p.S[j] = ok ? s : 0.0;
-    const double* x = Xs + static_cast<size_t>(src) * RX;
+    const double* x = Xs + static_cast<size_t>(src) * LDX;
     for (int r = tid; r < nrx; r += blockDim.x) p.U[static_cast<int64_t>(j) * p.mr + r0x + r] = ok ? x[r] / s : 0.0;
-    const double* v = Vs + static_cast<size_t>(src) * RV;
+    const double* v = Vs + static_cast<size_t>(src) * LDV;
     for (int r = tid; r < nrv; r += blockDim.x) p.V[static_cast<int64_t>(j) * c + r0v + r] = v[r];
   }
   if (q == 0 && tid == 0) {
@@ -355,46 +408,53 @@ __global__ void sumsq_partial_kernel(const double* __restrict__ x, int64_t n, do
 }
 
 struct JacobiLayout {
-  int P, RX, RV;
+  int P, RX, RV, LDX, LDV;
   bool smem;
   size_t bytes;
 };
 
+inline int pad_ld(int r) { return r + ((r % 2 == 0) ? 1 : 0); }  // odd leading dimension
+
 JacobiLayout jacobi_layout(int64_t mr, int64_t c) {
   const int64_t cc = c + (c & 1), npairs = cc / 2;
+  const int64_t G = (npairs + 31) / 32, H = 32 / G;
   auto extra = [&](int P) {
-    return sizeof(double) * (2 * P * npairs * 3 + P * cc + 2 * npairs) + sizeof(int) * (cc + npairs) + 64;
+    return sizeof(double) * (H * npairs * 3 + 2 * P * npairs * 3 + 2 * npairs + P * cc + cc) + sizeof(int) * cc + 64;
   };
-  constexpr size_t kMax = 220 * 1024;
+  constexpr size_t kMax = 224 * 1024;
   for (int P : {1, 2, 4, 8}) {
     const int RX = static_cast<int>((mr + P - 1) / P), RV = static_cast<int>((c + P - 1) / P);
-    const size_t b = sizeof(double) * static_cast<size_t>(c) * (RX + RV) + extra(P);
-    if (b <= kMax) return {P, RX, RV, true, b};
+    const int LDX = pad_ld(RX), LDV = pad_ld(RV);
+    const size_t b = sizeof(double) * static_cast<size_t>(c) * (LDX + LDV) + extra(P);
+    if (b <= kMax) return {P, RX, RV, LDX, LDV, true, b};
   }
   const int P = 8;
-  return {P, static_cast<int>((mr + P - 1) / P), static_cast<int>((c + P - 1) / P), false, extra(P)};
+  const int RX = static_cast<int>((mr + P - 1) / P), RV = static_cast<int>((c + P - 1) / P);
+  return {P, RX, RV, pad_ld(RX), pad_ld(RV), false, extra(P)};
 }
 
 }  // namespace
 
-size_t chol_inv_work_bytes(int64_t c) { return sizeof(double) * 2 * c * c; }
+size_t chol_inv_work_bytes(int64_t c) { return sizeof(double) * (2 * c + c * (c + 1) / 2); }
 
 cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double* work, int* info,
                      double* info_d, cudaStream_t st) {
   if (c <= 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * 2 * c * c;
-  if (smem <= 200 * 1024) {
+  if (c > 352) return cudaErrorInvalidValue;
+  const size_t smem = chol_inv_work_bytes(c);
+  const int ci = static_cast<int>(c);
+  if (smem <= 224 * 1024 && c <= 256) {
     static bool cfg = false;
     if (!cfg) {
-      cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           200 * 1024);
+      cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           224 * 1024);
       if (e != cudaSuccess) return e;
       cfg = true;
     }
-    chol_inv_kernel<true><<<1, kSmallThreads, smem, st>>>(G, static_cast<int>(c), R, Rinv, work, info, info_d);
+    chol_inv_kernel<true, 8><<<1, kSmallThreads, smem, st>>>(G, ci, R, Rinv, work, info, info_d);
     count_launch();
   } else {
-    chol_inv_kernel<false><<<1, kSmallThreads, 0, st>>>(G, static_cast<int>(c), R, Rinv, work, info, info_d);
+    chol_inv_kernel<false, 11><<<1, kSmallThreads, 0, st>>>(G, ci, R, Rinv, work, info, info_d);
     count_launch();
   }
   return cudaGetLastError();
@@ -403,7 +463,7 @@ cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double
 size_t jacobi_work_bytes(int64_t mr, int64_t c) {
   const JacobiLayout L = jacobi_layout(mr, c);
   if (L.smem) return 0;
-  return sizeof(double) * static_cast<size_t>(L.P) * c * (L.RX + L.RV);
+  return sizeof(double) * static_cast<size_t>(L.P) * c * (L.LDX + L.LDV);
 }
 
 cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double* S, double* V, double* work,
@@ -419,11 +479,13 @@ cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double
   p.V = V;
   p.RX = L.RX;
   p.RV = L.RV;
+  p.LDX = L.LDX;
+  p.LDV = L.LDV;
   p.info = info;
   p.sweeps_out = sweeps_out;
   if (!L.smem) {
     p.gX = work;
-    p.gV = work + static_cast<size_t>(L.P) * c * L.RX;
+    p.gV = work + static_cast<size_t>(L.P) * c * L.LDX;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(L.P);
