@@ -292,7 +292,7 @@ def main():
     torch.cuda.synchronize()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     launches = ctx.launch_count() // args.steps
-    prof = {nm: ctx.profile_read(nm) for nm in ("pass_nn", "pass_tn", "orth", "small_svd", "jacobi", "gemm_nn", "gemm_tn",
+    prof = {nm: ctx.profile_read(nm) for nm in ("pass_nn", "pass_tn", "orth", "small_svd", "jacobi", "gram", "trsm", "lift", "gemm_nn", "gemm_tn",
                                                 "allreduce")}
     ctx.profile(False)
     n_pass = prof["pass_nn"][0] + prof["pass_tn"][0]

@@ -282,15 +282,15 @@ Status allreduce(rfgpu_ctx* c, double* buf, int64_t count) {
 // ---- GEMM wrapper -----------------------------------------------------------
 Status gemm(rfgpu_ctx* c, bool trans, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
             const double* B, int64_t ldb, double* C, int64_t ldc, double* sumsq_partials = nullptr,
-            const char* label = nullptr) {
+            const char* label = nullptr, bool sym = false, bool tri_b = false) {
   if (M <= 0 || N <= 0) return {};
-  const GemmPlan p = plan_gemm(M, N, K, c->num_sms);
+  const GemmPlan p = plan_gemm(M, N, K, c->num_sms, 0, sym);
   DBuf ws;
   const size_t wb = gemm_workspace_bytes(M, N, p);
   if (wb) RF_TRY(ws.alloc(wb, c->stream));
   {
     Timed t(c, label ? label : (trans ? "gemm_tn" : "gemm_nn"));
-    RF_CUDA(gemm_f64(trans, M, N, K, A, lda, B, ldb, C, ldc, ws.d(), wb, sumsq_partials, p, c->stream));
+    RF_CUDA(gemm_f64(trans, M, N, K, A, lda, B, ldb, C, ldc, ws.d(), wb, sumsq_partials, p, c->stream, tri_b));
   }
   return {};
 }
@@ -301,23 +301,43 @@ int64_t sumsq_slots(rfgpu_ctx* c, int64_t M, int64_t N, int64_t K) {
 }
 
 // ---- orth ---------------------------------------------------------------------
-// Q (m_loc x r, ld ldq) = orth(X (m_loc x cols, ld ldx)); X rows may be
-// sharded across ranks (dist = true). R (cols x cols) optional: filled when
-// the CholeskyQR2 path is taken (R = R2 R1, X = Q R). Returns r and whether
-// the fast path was taken.
-constexpr double kCholGate = 1e-10;  // min pivot / trace(G): residuals >= 1e-5 ||X||_F
+// Orthonormal basis of X (m_loc x cols, ld ldx; rows sharded over ranks when
+// dist) replacing the reference MGS (dense.cpp:402-431).
+//
+// CholeskyQR2 fast path, accepted when every Cholesky pivot of the Gram is
+// >= 1e-10 trace(G) (each column keeps a residual >= 1e-5 ||X||_F, far above
+// the reference's 1e-13 drop threshold, so the reference keeps all columns
+// and CholeskyQR2 is orthonormal to working precision):
+//   G1 = X^T X, R1 = chol(G1), Q1 = X R1^{-1}, G2 = Q1^T Q1, R2 = chol(G2).
+// The basis is Q = Q1 R2^{-1}. With fold = true, Q1 and R2^{-1} are returned
+// separately (Q is never formed; consumers apply R2^{-1} on the l-sized
+// side), saving one m x l x l product per orth. Otherwise Q is formed.
+// R (optional) = R2 R1, so that X = Q R.
+//
+// Fallback (rank-deficient / ill-conditioned X): Gram-Schmidt with the
+// reference's drop rule; the basis is returned directly (folded = false).
+struct Basis {
+  double* Q = nullptr;      // m_loc x r (Q1 when folded)
+  int64_t ldq = 0;
+  int64_t r = 0;
+  double* R2inv = nullptr;  // r x r (folded only)
+  bool folded = false;
+  bool fast = false;
+};
 
-Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx, double* Q, int64_t ldq,
-            int64_t* r_out, double* R, bool dist, bool* fast_out = nullptr) {
+constexpr double kCholGate = 1e-10;  // min pivot / trace(G)
+
+Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx, Basis* out, double* R2inv_buf,
+            double* R, bool dist, bool fold) {
   Timed t(c, "orth");
-  if (cols == 0) {
-    *r_out = 0;
-    return {};
-  }
+  out->r = 0;
+  out->folded = false;
+  out->fast = false;
+  out->R2inv = nullptr;
+  if (cols == 0) return {};
   cudaStream_t st = c->stream;
   const int64_t cc = cols * cols;
   DBuf small;
-  // G1, R1, R1inv, G2, R2, R2inv, chol work, Q1 separately
   RF_TRY(small.alloc(sizeof(double) * (6 * cc + 16) + chol_inv_work_bytes(cols) + 64, st));
   double* G1 = small.d();
   double* R1 = G1 + cc;
@@ -327,37 +347,60 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
   double* R2i = R2 + cc;
   double* infod = R2i + cc;  // 2 doubles (+pad)
   double* cwork = infod + 8;  // chol_inv_work_bytes(cols)
-  int* info = reinterpret_cast<int*>(infod + 4);  // 2 ints (inside the pad)
-  DBuf q1;
-  const int64_t ldq1 = even(m);
-  RF_TRY(q1.alloc(sizeof(double) * std::max<int64_t>(1, ldq1 * cols), st));
+  int* info = reinterpret_cast<int*>(infod + 4);
+  DBuf q1buf;
+  double* Q1 = out->Q;  // folded: Q1 lands directly in the output buffer
+  int64_t ldq1 = out->ldq;
+  if (!fold) {
+    ldq1 = even(m);
+    RF_TRY(q1buf.alloc(sizeof(double) * std::max<int64_t>(1, ldq1 * cols), st));
+    Q1 = q1buf.d();
+  }
 
-  RF_TRY(gemm(c, true, cols, cols, m, X, ldx, X, ldx, G1, cols));
+  RF_TRY(gemm(c, true, cols, cols, m, X, ldx, X, ldx, G1, cols, nullptr, "gram", /*sym=*/true));
   if (dist) RF_TRY(allreduce(c, G1, cc));
   RF_CUDA(chol_inv(G1, cols, R1, R1i, cwork, info, infod, st));
-  RF_TRY(gemm(c, false, m, cols, cols, X, ldx, R1i, cols, q1.d(), ldq1));
-  RF_TRY(gemm(c, true, cols, cols, m, q1.d(), ldq1, q1.d(), ldq1, G2, cols));
+  RF_TRY(gemm(c, false, m, cols, cols, X, ldx, R1i, cols, Q1, ldq1, nullptr, "trsm", false, /*tri_b=*/true));
+  RF_TRY(gemm(c, true, cols, cols, m, Q1, ldq1, Q1, ldq1, G2, cols, nullptr, "gram", /*sym=*/true));
   if (dist) RF_TRY(allreduce(c, G2, cc));
   RF_CUDA(chol_inv(G2, cols, R2, R2i, cwork, info + 1, infod + 1, st));
-  RF_TRY(gemm(c, false, m, cols, cols, q1.d(), ldq1, R2i, cols, Q, ldq));
   RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaMemcpyAsync(c->h_d, infod, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));
   const bool fast = c->h_info[0] == 0 && c->h_info[1] == 0 && c->h_d[0] >= kCholGate;
-  if (fast_out) *fast_out = fast;
   if (fast) {
+    out->fast = true;
+    out->r = cols;
     if (R) RF_TRY(gemm(c, false, cols, cols, cols, R2, cols, R1, cols, R, cols));
-    *r_out = cols;
+    if (fold) {
+      RF_CUDA(cudaMemcpyAsync(R2inv_buf, R2i, sizeof(double) * cc, cudaMemcpyDeviceToDevice, st));
+      out->R2inv = R2inv_buf;
+      out->folded = true;
+    } else {
+      RF_TRY(gemm(c, false, m, cols, cols, Q1, ldq1, R2i, cols, out->Q, out->ldq, nullptr, "trsm", false, true));
+    }
     return {};
   }
   // Gram-Schmidt with the reference's drop rule.
   DBuf gw;
   RF_TRY(gw.alloc(sizeof(double) * gs_orth_work_doubles(m, cols) + 64, st));
   int64_t* r_dev = reinterpret_cast<int64_t*>(gw.d() + gs_orth_work_doubles(m, cols));
-  RF_CUDA(gs_orth(X, m, cols, ldx, Q, ldq, r_dev, gw.d(), dist ? allreduce_of(c) : DeviceAllreduce{}, st));
+  RF_CUDA(gs_orth(X, m, cols, ldx, out->Q, out->ldq, r_dev, gw.d(), dist ? allreduce_of(c) : DeviceAllreduce{}, st));
   RF_CUDA(cudaMemcpyAsync(c->h_i64, r_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));
-  *r_out = c->h_i64[0];
+  out->r = c->h_i64[0];
+  return {};
+}
+
+// Z (n x r) = A^T Q for a (possibly folded) basis: (A^T Q1) R2^{-1}; summed
+// over ranks. tmp: n x r scratch.
+Status pass_tn(rfgpu_ctx* c, const rfgpu_matrix* a, const Basis& b, double* Z, double* tmp) {
+  const int64_t m = a->m, n = a->n;
+  const double* A = static_cast<const double*>(a->dev);
+  double* dst = b.folded ? tmp : Z;
+  RF_TRY(gemm(c, true, n, b.r, m, A, a->lda, b.Q, b.ldq, dst, n, nullptr, "pass_tn"));
+  RF_TRY(allreduce(c, dst, n * b.r));
+  if (b.folded) RF_TRY(gemm(c, false, n, b.r, b.r, tmp, n, b.R2inv, b.r, Z, n, nullptr, nullptr, false, true));
   return {};
 }
 
@@ -368,24 +411,28 @@ Status small_svd_of_bt(rfgpu_ctx* c, const double* Bt, int64_t n, int64_t ell, d
   Timed t(c, "small_svd");
   cudaStream_t st = c->stream;
   const int64_t ldn = even(n);
-  DBuf qb, rb, ur, vr, jw, inf;
+  DBuf qb, rb, r2i, ur, ur2, jw, inf;
   RF_TRY(qb.alloc(sizeof(double) * ldn * ell, st));
   RF_TRY(rb.alloc(sizeof(double) * ell * ell, st));
+  RF_TRY(r2i.alloc(sizeof(double) * ell * ell, st));
   RF_TRY(inf.alloc(64, st));
-  int64_t r = 0;
-  bool fast = false;
-  RF_TRY(orth(c, Bt, n, ell, n, qb.d(), ldn, &r, rb.d(), /*dist=*/false, &fast));
+  Basis bq;
+  bq.Q = qb.d();
+  bq.ldq = ldn;
+  RF_TRY(orth(c, Bt, n, ell, n, &bq, r2i.d(), rb.d(), /*dist=*/false, /*fold=*/true));
   int* info = inf.as<int>();
-  if (fast) {
-    // Bt = Qb R; R = Ur S Vr^T  =>  B = Vr S (Qb Ur)^T
+  if (bq.fast) {
+    // Bt = Q1 R2^{-1} R; R = Ur S Vr^T  =>  B = Vr S (Q1 R2^{-1} Ur)^T
     RF_TRY(ur.alloc(sizeof(double) * ell * ell, st));
+    RF_TRY(ur2.alloc(sizeof(double) * ell * ell, st));
     const size_t jwb = jacobi_work_bytes(ell, ell);
     if (jwb) RF_TRY(jw.alloc(jwb, st));
     {
       Timed tj(c, "jacobi");
       RF_CUDA(jacobi_svd(rb.d(), ell, ell, ur.d(), D, Ub, jw.d(), info, info + 1, st));
     }
-    RF_TRY(gemm(c, false, n, ell, ell, qb.d(), ldn, ur.d(), ell, Vb, n));
+    RF_TRY(gemm(c, false, ell, ell, ell, bq.R2inv, ell, ur.d(), ell, ur2.d(), ell));
+    RF_TRY(gemm(c, false, n, ell, ell, bq.Q, ldn, ur2.d(), ell, Vb, n));
   } else {
     // rank-deficient / ill-conditioned B: Jacobi directly on the tall Bt
     const size_t jwb = jacobi_work_bytes(n, ell);
@@ -396,68 +443,82 @@ Status small_svd_of_bt(rfgpu_ctx* c, const double* Bt, int64_t n, int64_t ell, d
   RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));
   if (std::getenv("RFGPU_DEBUG"))
-    std::fprintf(stderr, "[rfgpu] small_svd ell=%lld fast=%d jacobi info=%d sweeps=%d\n", (long long)ell, (int)fast,
-                 c->h_info[0], c->h_info[1]);
+    std::fprintf(stderr, "[rfgpu] small_svd ell=%lld fast=%d jacobi info=%d sweeps=%d\n", (long long)ell,
+                 (int)bq.fast, c->h_info[0], c->h_info[1]);
   if (c->h_info[0] == 1) return make_err(RFGPU_ECONVERGENCE, "svd_dense: Jacobi sweeps did not converge");
   return {};
 }
 
 // ---- range finder core ------------------------------------------------------------
 struct RangeOut {
-  int64_t ell_out = 0;
+  Basis basis;           // Q (possibly folded: Q = basis.Q * basis.R2inv)
   double a_frob2 = 0.0;  // ||A||_F^2 (global)
 };
 
-// A (m_loc x n) handle; G_dev (n x ell); Q_dev (ldq x ell) receives the basis;
-// Bt_dev (n x ell, ld n) receives B^T = A^T Q (summed over ranks).
+// A (m_loc x n) handle; G (n x ell) on the device. Qbuf (ldq x ell) and
+// R2ibuf (ell x ell) receive the basis; Bt (n x ell, ld n) receives
+// B^T = A^T Q (summed over ranks). power_range, rangefinder.cpp:63-80.
 Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, int64_t q, bool reorth,
-                  double* Q, int64_t ldq, double* Bt, RangeOut* out) {
+                  double* Qbuf, int64_t ldq, double* R2ibuf, double* Bt, RangeOut* out) {
   cudaStream_t st = c->stream;
   const int64_t m = a->m, n = a->n;
   const double* A = static_cast<const double*>(a->dev);
   const int64_t lda = a->lda;
-  DBuf y, z, w, ssq, scal;
+  DBuf y, z, w, tmp, ssq, scal;
   RF_TRY(y.alloc(sizeof(double) * std::max<int64_t>(1, ldq * ell), st));
   RF_TRY(z.alloc(sizeof(double) * n * ell, st));
   RF_TRY(w.alloc(sizeof(double) * n * ell, st));
+  RF_TRY(tmp.alloc(sizeof(double) * n * ell, st));
   const int64_t slots = sumsq_slots(c, m, ell, n);
   RF_TRY(ssq.alloc(sizeof(double) * std::max<int64_t>(1, slots), st));
   RF_TRY(scal.alloc(sizeof(double) * 4, st));
   RF_CUDA(cudaMemsetAsync(ssq.d(), 0, sizeof(double) * std::max<int64_t>(1, slots), st));
 
+  Basis& Qb = out->basis;
+  Qb.Q = Qbuf;
+  Qb.ldq = ldq;
   // pass 1: Y = A G, with ||A||_F^2 fused
   RF_TRY(gemm(c, false, m, ell, n, A, lda, G, n, y.d(), ldq, ssq.d(), "pass_nn"));
   RF_CUDA(sum_array(ssq.d(), slots, scal.d(), st));
   RF_TRY(allreduce(c, scal.d(), 1));
 
-  int64_t r = ell;
   if (!reorth) {
     for (int64_t j = 0; j < q; ++j) {
       RF_TRY(gemm(c, true, n, ell, m, A, lda, y.d(), ldq, z.d(), n, nullptr, "pass_tn"));
       RF_TRY(allreduce(c, z.d(), n * ell));
       RF_TRY(gemm(c, false, m, ell, n, A, lda, z.d(), n, y.d(), ldq, nullptr, "pass_nn"));
     }
-    RF_TRY(orth(c, y.d(), m, ell, ldq, Q, ldq, &r, nullptr, true));
+    RF_TRY(orth(c, y.d(), m, ell, ldq, &Qb, R2ibuf, nullptr, true, true));
   } else {
-    RF_TRY(orth(c, y.d(), m, ell, ldq, Q, ldq, &r, nullptr, true));
-    for (int64_t j = 0; j < q && r > 0; ++j) {
-      int64_t rw = 0;
-      RF_TRY(gemm(c, true, n, r, m, A, lda, Q, ldq, z.d(), n, nullptr, "pass_tn"));
-      RF_TRY(allreduce(c, z.d(), n * r));
-      RF_TRY(orth(c, z.d(), n, r, n, w.d(), n, &rw, nullptr, false));
-      RF_TRY(gemm(c, false, m, rw, n, A, lda, w.d(), n, y.d(), ldq, nullptr, "pass_nn"));
-      RF_TRY(orth(c, y.d(), m, rw, ldq, Q, ldq, &r, nullptr, true));
+    RF_TRY(orth(c, y.d(), m, ell, ldq, &Qb, R2ibuf, nullptr, true, true));
+    for (int64_t j = 0; j < q && Qb.r > 0; ++j) {
+      RF_TRY(pass_tn(c, a, Qb, z.d(), tmp.d()));
+      Basis Wb;
+      Wb.Q = w.d();
+      Wb.ldq = n;
+      RF_TRY(orth(c, z.d(), n, Qb.r, n, &Wb, nullptr, nullptr, false, false));
+      if (Wb.r == 0) {
+        Qb.r = 0;
+        break;
+      }
+      RF_TRY(gemm(c, false, m, Wb.r, n, A, lda, w.d(), n, y.d(), ldq, nullptr, "pass_nn"));
+      RF_TRY(orth(c, y.d(), m, Wb.r, ldq, &Qb, R2ibuf, nullptr, true, true));
     }
   }
-  // projection: B^T = A^T Q
-  if (r > 0) {
-    RF_TRY(gemm(c, true, n, r, m, A, lda, Q, ldq, Bt, n, nullptr, "pass_tn"));
-    RF_TRY(allreduce(c, Bt, n * r));
-  }
+  // projection: B^T = A^T Q (finish_with_projection, rangefinder.cpp:24-30)
+  if (Qb.r > 0) RF_TRY(pass_tn(c, a, Qb, Bt, tmp.d()));
   RF_CUDA(cudaMemcpyAsync(c->h_d, scal.d(), sizeof(double), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));
   out->a_frob2 = c->h_d[0];
-  out->ell_out = r;
+  return {};
+}
+
+// Explicit Q (m x r, ld ldo) from a possibly folded basis.
+Status materialize_q(rfgpu_ctx* c, int64_t m, const Basis& b, double* Qo, int64_t ldo) {
+  if (b.r == 0 || m == 0) return {};
+  if (b.folded) return gemm(c, false, m, b.r, b.r, b.Q, b.ldq, b.R2inv, b.r, Qo, ldo, nullptr, "trsm", false, true);
+  RF_CUDA(cudaMemcpy2DAsync(Qo, sizeof(double) * ldo, b.Q, sizeof(double) * b.ldq, sizeof(double) * m, b.r,
+                            cudaMemcpyDeviceToDevice, c->stream));
   return {};
 }
 
@@ -491,30 +552,38 @@ Status check_sample(const rfgpu_matrix* a, int64_t k, int64_t ell, const char* w
   return {};
 }
 
-// rsvd on device buffers; U_dev (ldu x ell), D_dev (ell), V_dev (n x ell).
+// rsvd on device buffers; U (ldu x ell), D (ell), V (n x ell). lowrank.cpp:74-96.
 Status rsvd_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t k, int64_t ell, int64_t q, bool keep_over,
                  bool reorth, double* U, int64_t ldu, double* D, double* V, int64_t* rank_out) {
   cudaStream_t st = c->stream;
   const int64_t m = a->m, n = a->n;
   const int64_t ldq = even(m);
-  DBuf Q, Bt, Ub, Vb, Dd;
+  DBuf Q, R2i, Bt, Ub, Ub2, Vb, Dd;
   RF_TRY(Q.alloc(sizeof(double) * std::max<int64_t>(1, ldq * ell), st));
+  RF_TRY(R2i.alloc(sizeof(double) * ell * ell, st));
   RF_TRY(Bt.alloc(sizeof(double) * n * ell, st));
   RangeOut ro;
-  RF_TRY(range_core(c, a, G, ell, q, reorth, Q.d(), ldq, Bt.d(), &ro));
-  RF_TRY(frob_residual_dev(c, ro.a_frob2, Bt.d(), n * ro.ell_out, nullptr));
-  const int64_t r = ro.ell_out;
+  RF_TRY(range_core(c, a, G, ell, q, reorth, Q.d(), ldq, R2i.d(), Bt.d(), &ro));
+  const Basis& b = ro.basis;
+  const int64_t r = b.r;
+  RF_TRY(frob_residual_dev(c, ro.a_frob2, Bt.d(), n * r, nullptr));
   if (r == 0) {
     *rank_out = 0;
     return {};
   }
   RF_TRY(Ub.alloc(sizeof(double) * r * r, st));
+  RF_TRY(Ub2.alloc(sizeof(double) * r * r, st));
   RF_TRY(Vb.alloc(sizeof(double) * n * r, st));
   RF_TRY(Dd.alloc(sizeof(double) * r, st));
   RF_TRY(small_svd_of_bt(c, Bt.d(), n, r, Ub.d(), Dd.d(), Vb.d()));
   const int64_t keep = keep_over ? r : std::min(k, r);
-  // lift: U = Q * Ub(:, :keep)
-  RF_TRY(gemm(c, false, m, keep, r, Q.d(), ldq, Ub.d(), r, U, ldu));
+  // lift: U = Q Ub(:, :keep) = Q1 (R2^{-1} Ub(:, :keep))
+  const double* ub = Ub.d();
+  if (b.folded) {
+    RF_TRY(gemm(c, false, r, keep, r, b.R2inv, r, Ub.d(), r, Ub2.d(), r));
+    ub = Ub2.d();
+  }
+  RF_TRY(gemm(c, false, m, keep, r, b.Q, b.ldq, ub, r, U, ldu, nullptr, "lift"));
   RF_CUDA(cudaMemcpyAsync(V, Vb.d(), sizeof(double) * n * keep, cudaMemcpyDeviceToDevice, st));
   RF_CUDA(cudaMemcpyAsync(D, Dd.d(), sizeof(double) * keep, cudaMemcpyDeviceToDevice, st));
   *rank_out = keep;
@@ -831,20 +900,25 @@ int rfgpu_range_finder(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int
     RF_TRY(ensure_device(c));
     cudaStream_t st = c->stream;
     const int64_t m = a->m, n = a->n, ldq = even(m);
-    DBuf gd, Q, Bt, Bd;
+    DBuf gd, Q, Qx, R2i, Bt, Bd;
     RF_TRY(gd.alloc(sizeof(double) * n * ell, st));
     RF_TRY(Q.alloc(sizeof(double) * std::max<int64_t>(1, ldq * ell), st));
+    RF_TRY(Qx.alloc(sizeof(double) * std::max<int64_t>(1, ldq * ell), st));
+    RF_TRY(R2i.alloc(sizeof(double) * ell * ell, st));
     RF_TRY(Bt.alloc(sizeof(double) * n * ell, st));
     RF_TRY(Bd.alloc(sizeof(double) * n * ell, st));
     RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
     RangeOut ro;
-    RF_TRY(range_core(c, a, gd.d(), ell, q, reorth != 0, Q.d(), ldq, Bt.d(), &ro));
-    const int64_t r = ro.ell_out;
+    RF_TRY(range_core(c, a, gd.d(), ell, q, reorth != 0, Q.d(), ldq, R2i.d(), Bt.d(), &ro));
+    const int64_t r = ro.basis.r;
     double res = 0.0;
     RF_TRY(frob_residual_dev(c, ro.a_frob2, Bt.d(), n * r, &res));
     if (resid) *resid = res;
     if (ell_out) *ell_out = r;
-    RF_TRY(copy_out(c, Qh, std::max<int64_t>(1, m), Q.d(), ldq, m, r));
+    if (Qh) {
+      RF_TRY(materialize_q(c, m, ro.basis, Qx.d(), ldq));
+      RF_TRY(copy_out(c, Qh, std::max<int64_t>(1, m), Qx.d(), ldq, m, r));
+    }
     if (Bh && r > 0) {
       RF_CUDA(transpose(Bt.d(), n, r, n, Bd.d(), r, st));
       RF_TRY(copy_out(c, Bh, r, Bd.d(), r, r, n));

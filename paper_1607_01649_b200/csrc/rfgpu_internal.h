@@ -14,6 +14,8 @@ void count_launch(int n = 1);
 
 // ---- tall-skinny FP64 GEMM (gemm_f64.cu) --------------------------------
 struct GemmPlan {
+  bool sym;        // Gram-type product: only upper tiles are computed, then mirrored
+  int64_t units;   // CTA tiles per split
   int ntiles;      // CTA columns along N
   int nt;          // 8-wide MMA tiles per warp along N (CTA tile N = 16*nt)
   int mtiles;      // CTA rows along M (128 each)
@@ -21,7 +23,7 @@ struct GemmPlan {
   int64_t ktiles;  // ceil(K / 32)
 };
 
-GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int num_sms, int force_splits = 0);
+GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int num_sms, int force_splits = 0, bool sym = false);
 size_t gemm_workspace_bytes(int64_t M, int64_t N, const GemmPlan& p);
 
 // trans_a = false: C = A(MxK) * B(KxN); true: C = A(KxM)^T * B(KxN).
@@ -29,7 +31,8 @@ size_t gemm_workspace_bytes(int64_t M, int64_t N, const GemmPlan& p);
 // of squares of A (each A element counted once).
 cudaError_t gemm_f64(bool trans_a, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                      const double* B, int64_t ldb, double* C, int64_t ldc, double* workspace,
-                     size_t workspace_bytes, double* sumsq_partials, const GemmPlan& p, cudaStream_t st);
+                     size_t workspace_bytes, double* sumsq_partials, const GemmPlan& p, cudaStream_t st,
+                     bool tri_b = false);
 
 cudaError_t sum_array(const double* x, int64_t n, double* out, cudaStream_t st);
 
