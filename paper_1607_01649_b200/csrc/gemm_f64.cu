@@ -267,7 +267,7 @@ constexpr int WS_THREADS = (NCONS + 4) * 32;
 template <bool TRANS>
 constexpr int a_stage_ws() { return TRANS ? 2 * BM * 16 : BK * LDA_NN; }
 template <bool TRANS, int NT>
-constexpr int b_stage_ws() { return TRANS ? 2 * 16 * NT * 16 : 16 * NT * LDK; }
+constexpr int b_stage_ws() { return 2 * 16 * NT * 16; }  // [2 k-halves][BN][16], both modes
 template <bool TRANS, int NT>
 constexpr size_t smem_bytes_ws() {
   return sizeof(double) * STAGES * (a_stage_ws<TRANS>() + b_stage_ws<TRANS, NT>()) + 2 * STAGES * sizeof(uint64_t) +
@@ -374,8 +374,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         na = static_cast<int>(rows_m);
         bytes_a = bytes_k;
       }
-      const int nb = static_cast<int>(cols_n);
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], na * bytes_a + nb * bytes_k);
+      // B: two swizzled tensor boxes (zero-filled beyond K / N)
+      if (lane == 0)
+        mbar_arrive_expect_tx(&full[s], na * bytes_a + static_cast<uint32_t>(sizeof(double) * b_stage_ws<TRANS, NT>()));
       __syncwarp();
       double* a_st = sA + s * a_stage_ws<TRANS>();
       double* b_st = sB + s * b_stage_ws<TRANS, NT>();
@@ -383,7 +384,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         if constexpr (!TRANS) bulk_g2s(a_st + c * LDA_NN, g.A + (k0 + c) * g.lda + m0, bytes_a, &full[s]);
         else bulk_g2s(a_st + c * LDK, g.A + (m0 + c) * g.lda + k0, bytes_a, &full[s]);
       }
-      for (int c = lane; c < nb; c += 32) bulk_g2s(b_st + c * LDK, g.B + (n0 + c) * g.ldb + k0, bytes_k, &full[s]);
+      if (lane == 0) {
+        tma_load_2d(b_st, &tmB, static_cast<int>(k0), static_cast<int>(n0), &full[s]);
+        tma_load_2d(b_st + BN * 16, &tmB, static_cast<int>(k0 + 16), static_cast<int>(n0), &full[s]);
+      }
     }
     return;
   }
@@ -396,6 +400,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   double rowmask[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) rowmask[i] = (m0 + wm * 32 + i * 8 + g4 < g.M) ? 1.0 : 0.0;
+  // NN: B arrives swizzled; natural k = 4*ks + t4 -> chunk (kk >> 1) ^ (row & 7)
+  int bsw[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int kk = 4 * u + t4;
+    bsw[u] = (((kk >> 1) ^ g4) << 1) | (kk & 1);
+  }
 
   double acc[4][NT][2];
 #pragma unroll
@@ -440,7 +451,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
           else af[i] = a[mrow * LDK + ks * 4 + t4];
         }
 #pragma unroll
-        for (int j = 0; j < NT; ++j) bf[j] = b[(wn * NT * 8 + j * 8 + g4) * LDK + ks * 4 + t4];
+        for (int j = 0; j < NT; ++j) bf[j] = b[(ks >> 2) * (BN * 16) + (wn * NT * 8 + j * 8 + g4) * 16 + bsw[ks & 3]];
         if (do_sumsq) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) ss = fma(af[i] * rowmask[i], af[i], ss);
@@ -464,8 +475,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         }
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-          const double v = b[(wn * NT * 8 + j * 8 + g4) * LDK + ks * 4 + t4];
-          bf[j] = kin ? v : 0.0;
+          bf[j] = b[(ks >> 2) * (BN * 16) + (wn * NT * 8 + j * 8 + g4) * 16 + bsw[ks & 3]];
         }
         if (do_sumsq) {
 #pragma unroll
@@ -718,9 +728,10 @@ cudaError_t gemm_f64(bool trans_a, int64_t M, int64_t N, int64_t K, const double
                    (lda % 2 == 0) && (ldb % 2 == 0);
   int mode = v16 ? 1 : 0;
   CUtensorMap ta{}, tb{};
-  if (mode == 1 && trans_a) {
-    const bool ok = K < (int64_t(1) << 31) && M < (int64_t(1) << 31) && N < (int64_t(1) << 31) &&
-                    make_tmap(&ta, A, K, M, lda, BM) && make_tmap(&tb, B, K, N, ldb, 16 * p.nt);
+  if (mode == 1) {
+    const bool dims_ok = K < (int64_t(1) << 31) && M < (int64_t(1) << 31) && N < (int64_t(1) << 31);
+    bool ok = dims_ok && make_tmap(&tb, B, K, N, ldb, 16 * p.nt);
+    if (ok && trans_a) ok = make_tmap(&ta, A, K, M, lda, BM);
     if (!ok) mode = 0;
   }
   // The cp.async kernel computes every tile; the TMA kernel honours sym/tri_b.
