@@ -215,14 +215,21 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
     rest = sm;
   }
   const int np3 = npairs * 3;
-  double* red = rest;                    // [H][npairs][3]
-  double* pbuf = red + H * np3;          // [2][P][npairs][3]
-  double* rot = pbuf + 2 * P * np3;      // [npairs][2]
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(rest);  // [2] DSMEM arrival barriers (per parity)
+  double* red = rest + 2;                // [H][npairs][3]
+  double* pbuf = red + H * np3;          // [2][P][npairs][4]
+  double* rot = pbuf + 2 * P * npairs * 4;  // [npairs][2]
   double* nrmp = rot + 2 * npairs;       // [P][cc]
   double* nrm = nrmp + P * cc;           // [cc]
   int* perm = reinterpret_cast<int*>(nrm + cc);  // [cc]
   __shared__ int s_rotated, s_conv;
 
+  if (tid == 0) {
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    mbar_fence_init();
+  }
+  uint32_t rbar_uses[2] = {0u, 0u};
   for (int e = tid; e < c * RX; e += blockDim.x) {
     const int col = e / RX, r = e % RX;
     Xs[static_cast<size_t>(col) * LDX + r] = (r < nrx) ? p.X[static_cast<int64_t>(col) * p.mr + r0x + r] : 0.0;
@@ -231,7 +238,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
     const int col = e / RV, r = e % RV;
     Vs[static_cast<size_t>(col) * LDV + r] = (r < nrv && r0v + r == col) ? 1.0 : 0.0;
   }
-  __syncthreads();
+  cluster.sync();  // barriers initialised cluster-wide before any st.async
 
   // Column norms over the owned rows, exchanged across the cluster; nrm[j]
   // receives the total in fixed rank order.
@@ -300,9 +307,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
         d[1] = aqq;
         d[2] = apq;
       }
+      if (P > 1 && tid == 0) mbar_arrive_expect_tx(&rbar[parity], static_cast<uint32_t>(P * npairs * 32));
       __syncthreads();
-      // B. CTA partial -> every CTA of the cluster
-      double* pb = pbuf + parity * P * np3;
+      // B. CTA partial -> every CTA of the cluster (st.async, counted on the
+      //    receiver's mbarrier; no cluster-wide barrier per round)
+      double* pb = pbuf + parity * P * npairs * 4;
       if (h == 0 && k < npairs) {
         double app = 0.0, aqq = 0.0, apq = 0.0;
         for (int hh = 0; hh < H; ++hh) {
@@ -311,20 +320,28 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
           aqq += s[1];
           apq += s[2];
         }
-        for (int d = 0; d < P; ++d) {
-          double* dst = cluster.map_shared_rank(pb, d) + (q * npairs + k) * 3;
+        if (P > 1) {
+          const uint32_t la = smem_u32(pb + (q * npairs + k) * 4), lb = smem_u32(&rbar[parity]);
+          for (int d = 0; d < P; ++d) {
+            const uint32_t ra = mapa_u32(la, d), rb = mapa_u32(lb, d);
+            st_async_v2(ra, app, aqq, rb);
+            st_async_v2(ra + 16, apq, 0.0, rb);
+          }
+        } else {
+          double* dst = pb + k * 4;
           dst[0] = app;
           dst[1] = aqq;
           dst[2] = apq;
         }
       }
-      if (P > 1) cluster.sync();
-      else __syncthreads();
+      if (P == 1) __syncthreads();
+      else if (h == 0) mbar_wait(&rbar[parity], rbar_uses[parity] & 1u);
+      rbar_uses[parity] += 1u;
       // C. rotation parameters (one lane per pair)
       if (h == 0 && k < npairs) {
         double app = 0.0, aqq = 0.0, apq = 0.0;
         for (int d = 0; d < P; ++d) {
-          const double* s = pb + (d * npairs + k) * 3;
+          const double* s = pb + (d * npairs + k) * 4;
           app += s[0];
           aqq += s[1];
           apq += s[2];
@@ -419,7 +436,7 @@ JacobiLayout jacobi_layout(int64_t mr, int64_t c) {
   const int64_t cc = c + (c & 1), npairs = cc / 2;
   const int64_t G = (npairs + 31) / 32, H = 32 / G;
   auto extra = [&](int P) {
-    return sizeof(double) * (H * npairs * 3 + 2 * P * npairs * 3 + 2 * npairs + P * cc + cc) + sizeof(int) * cc + 64;
+    return sizeof(double) * (2 + H * npairs * 3 + 2 * P * npairs * 4 + 2 * npairs + P * cc + cc) + sizeof(int) * cc + 64;
   };
   constexpr size_t kMax = 224 * 1024;
   for (int P : {1, 2, 4, 8}) {
