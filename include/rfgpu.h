@@ -147,6 +147,20 @@ int rfgpu_col_id(rfgpu_ctx* ctx, const double* Y, int64_t m, int64_t n, int64_t 
 int rfgpu_col_id_device(rfgpu_ctx* ctx, const double* Y_dev, int64_t m, int64_t n, int64_t k, int64_t* Js,
                         double* Z_dev, int64_t* rank_out, int* truncated);
 
+/* randfact::randomized_id (proj/src/lowrank.cpp:312-329): tall sketch
+ * Y = (A A^T)^q A G (G n x ell from rfgpu_gaussian(seed, "rid.G")), row ID
+ * from col_id_core(Y^T, k). Is (k), X (m x rank, ld m). Single GPU. */
+int rfgpu_randomized_id(rfgpu_ctx* ctx, const rfgpu_matrix* a, const double* g, int64_t k, int64_t ell, int64_t q,
+                        int64_t* Is, double* X, int64_t* rank_out, int* truncated);
+
+/* randfact::randomized_cur (proj/src/lowrank.cpp:348-372): G ell x m from
+ * rfgpu_gaussian(seed, "cur.G"); column ID of G A, row ID of A(:, Js),
+ * U (kc x kr, ld kc) by the reference's SVD least squares (1e-12 cutoff),
+ * cond numbers of C and R, warning = either > 1e8. Single GPU. */
+int rfgpu_randomized_cur(rfgpu_ctx* ctx, const rfgpu_matrix* a, const double* g, int64_t k, int64_t ell, int64_t q,
+                         int64_t* Js, int64_t* Is, double* U, double* cond_c, double* cond_r, int* warning,
+                         int64_t* kc_out, int64_t* kr_out);
+
 /* ---- single pass (FP32) ---------------------------------------------------
  * Dual sketch of randfact::single_pass_svd (proj/src/lowrank.cpp:170-176):
  * one read of A (fp32 handle) -> Yc = A Gc (m_local x ell),

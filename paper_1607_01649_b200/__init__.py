@@ -32,7 +32,8 @@ __all__ = [
     "Error", "ParameterError", "NumericalError", "ConvergenceError", "NotPositiveDefiniteError",
     "StreamContractError", "DeviceError", "Context", "DeviceMatrix", "SvdFactors", "RangeBasis", "IdFactors",
     "CurFactors", "gaussian", "basic_range", "power_range", "rsvd", "randomized_id", "randomized_cur",
-    "id_deterministic", "single_pass_svd", "MatrixStream", "library_path", "default_context",
+    "id_deterministic", "single_pass_svd", "MatrixStream", "library_path", "default_context", "row_sketch",
+    "multiply",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -110,6 +111,9 @@ _SIGS = {
     "rfgpu_col_id": (_int, [_vp, _pd, _i64, _i64, _i64, _pi, _pd, _pi, C.POINTER(_int)]),
     "rfgpu_col_id_device": (_int, [_vp, _vp, _i64, _i64, _i64, _pi, _vp, _pi, C.POINTER(_int)]),
     "rfgpu_dual_sketch_f32": (_int, [_vp, _vp, _pf, _pf, _i64, _pf, _pf]),
+    "rfgpu_randomized_id": (_int, [_vp, _vp, _pd, _i64, _i64, _i64, _pi, _pd, _pi, C.POINTER(_int)]),
+    "rfgpu_randomized_cur": (_int, [_vp, _vp, _pd, _i64, _i64, _i64, _pi, _pi, _pd, _pd, _pd, C.POINTER(_int), _pi,
+                                     _pi]),
 }
 
 
@@ -435,11 +439,61 @@ def id_deterministic(a, k: int, side: str = "Col", ctx: Context | None = None) -
 
 
 def randomized_id(a, k: int, p: int, q: int, seed: int, ctx: Context | None = None) -> IdFactors:
-    raise ParameterError("randomized_id: not available in this build")
+    """randfact::randomized_id(a, k, p, q, seed): row ID from the tall sketch."""
+    dm, tmp = _as_device(a, ctx)
+    try:
+        _check_sample(k, p, dm.m_global, dm.n, "randomized_id")
+        if q < 0:
+            raise ParameterError("randomized_id: q must be non-negative")
+        ell = k + p
+        g = gaussian(seed, "rid.G", dm.n, ell)
+        is_ = np.zeros(k, dtype=np.int64)
+        x = np.zeros(dm.m * k)
+        r, tr = _i64(), C.c_int()
+        _check(lib().rfgpu_randomized_id(dm.ctx.handle, dm.handle, _dp(_flat(g)), k, ell, q, _ip(is_), _dp(x),
+                                         C.byref(r), C.byref(tr)))
+        ke = r.value
+        return IdFactors("Row", Is=is_[:ke].copy(), X=x[: dm.m * ke].reshape((dm.m, ke), order="F"),
+                         rank_truncated=bool(tr.value))
+    finally:
+        if tmp:
+            dm.free()
 
 
 def randomized_cur(a, k: int, p: int, q: int, seed: int, ctx: Context | None = None) -> CurFactors:
-    raise ParameterError("randomized_cur: not available in this build")
+    """randfact::randomized_cur(a, k, p, q, seed)."""
+    dm, tmp = _as_device(a, ctx)
+    try:
+        _check_sample(k, p, dm.m_global, dm.n, "randomized_cur")
+        if q < 0:
+            raise ParameterError("randomized_cur: q must be non-negative")
+        ell = k + p
+        g = gaussian(seed, "cur.G", ell, dm.m_global)
+        js, is_ = np.zeros(k, dtype=np.int64), np.zeros(k, dtype=np.int64)
+        u = np.zeros(k * k)
+        cc, cr, w = C.c_double(), C.c_double(), C.c_int()
+        kc, kr = _i64(), _i64()
+        _check(lib().rfgpu_randomized_cur(dm.ctx.handle, dm.handle, _dp(_flat(g)), k, ell, q, _ip(js), _ip(is_),
+                                          _dp(u), C.byref(cc), C.byref(cr), C.byref(w), C.byref(kc), C.byref(kr)))
+        return CurFactors(js[: kc.value].copy(), is_[: kr.value].copy(),
+                          u[: kc.value * kr.value].reshape((kc.value, kr.value), order="F"), cc.value, cr.value,
+                          bool(w.value))
+    finally:
+        if tmp:
+            dm.free()
+
+
+def row_sketch(a, ell: int, seed: int, ctx: Context | None = None) -> np.ndarray:
+    """Y = G A with G = gaussian(seed, "cur.G", ell, m) (randomized_cur's pass over A)."""
+    dm, tmp = _as_device(a, ctx)
+    try:
+        g = gaussian(seed, "cur.G", ell, dm.m_global)
+        y = np.zeros(ell * dm.n)
+        _check(lib().rfgpu_row_sketch(dm.ctx.handle, dm.handle, _dp(_flat(g)), ell, _dp(y)))
+        return y.reshape((ell, dm.n), order="F")
+    finally:
+        if tmp:
+            dm.free()
 
 
 class MatrixStream:

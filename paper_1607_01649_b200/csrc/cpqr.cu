@@ -1,0 +1,332 @@
+// Column-pivoted Householder QR with the reference's greedy pivot rule, and
+// the interpolative-decomposition pieces built on it.
+//
+//  * cpqr_rank   cpqr(Y, CpqrStop::rank(k)) of proj/src/dense.cpp:453-552:
+//                pivot = FIRST column attaining the largest down-dated norm
+//                (strict > scan from best = -1), exact recompute when the
+//                winner fell below 1e-8 of its original norm, halt when
+//                sqrt(best) < 1e-14 ||Y||_F, non-negative R diagonal
+//                (make_reflector, dense.cpp:328-357). One persistent
+//                cooperative kernel; each CTA owns a contiguous block of
+//                columns, two grid barriers per step (argmax, then swap +
+//                reflector application), the ell x n sketch stays in L2.
+//  * trinv_upper R^{-1} of an upper-triangular k x k factor (warp per column).
+//  * assemble_z  Z(:, Js) = I, Z(:, perm(k:)) = T (col_id_core, lowrank.cpp:51-70).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "rfgpu_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace rfgpu {
+
+namespace {
+
+constexpr int kCpqrThreads = 512;
+constexpr int kMaxRows = 512;  // sketch height (k + p) supported by the kernel
+
+struct CpqrParams {
+  double* W;  // m x n, column-major, ld
+  int64_t ld;
+  int m;
+  int64_t n;
+  int kmax;          // rank stop
+  double halt;       // 1e-14 ||Y||_F
+  double* norms2;    // [n]
+  double* norms0;    // [n]
+  int64_t* perm;     // [n]
+  double* part_val;  // [grid]
+  int64_t* part_idx; // [grid]
+  int* stopped;      // [1] stopped rank
+  int* recomputes;   // [1]
+};
+
+__device__ __forceinline__ void better(double& bv, int64_t& bi, double v, int64_t i) {
+  // "first index attaining the maximum": strictly larger value, or equal value
+  // at a smaller index (only reachable when combining partial winners).
+  if (v > bv || (v == bv && i < bi)) {
+    bv = v;
+    bi = i;
+  }
+}
+
+__global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams p) {
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x, b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int64_t cpb = (p.n + G - 1) / G;
+  const int64_t c0 = lmin(p.n, b * cpb), c1 = lmin(p.n, c0 + cpb);
+  const int m = p.m;
+  const int rmax = lmin(lmin(m, p.n), p.kmax);
+
+  __shared__ double colP[kMaxRows], colR[kMaxRows], tail[kMaxRows];
+  __shared__ double s_val[32];
+  __shared__ int64_t s_idx[32];
+  __shared__ double s_beta, s_result, s_best, s_oldn2_piv, s_oldn0_piv, s_oldn2_r, s_oldn0_r;
+  __shared__ int64_t s_piv, s_perm_piv, s_perm_r;
+  __shared__ int s_stop, s_recompute;
+
+  // initial norms (dense.cpp:466-471) and identity permutation
+  for (int64_t c = c0 + warp; c < c1; c += nwarps) {
+    const double* col = p.W + c * p.ld;
+    double s = 0.0;
+    for (int i = lane; i < m; i += 32) s = fma(col[i], col[i], s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      p.norms2[c] = s;
+      p.norms0[c] = s;
+      p.perm[c] = c;
+    }
+  }
+  grid.sync();
+
+  auto local_argmax = [&](int r) {
+    double bv = -1.0;
+    int64_t bi = r;
+    for (int64_t c = lmax(c0, r) + tid; c < c1; c += blockDim.x) {
+      const double v = p.norms2[c];
+      if (v > bv) {  // strided scan: ties resolved by index in the combine
+        bv = v;
+        bi = c;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      better(bv, bi, ov, oi);
+    }
+    if (lane == 0) {
+      s_val[warp] = bv;
+      s_idx[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double v = -1.0;
+      int64_t i = r;
+      for (int w = 0; w < nwarps; ++w) better(v, i, s_val[w], s_idx[w]);
+      p.part_val[b] = v;
+      p.part_idx[b] = i;
+    }
+  };
+  auto global_argmax = [&](int r) {
+    if (tid == 0) {
+      double v = -1.0;
+      int64_t i = r;
+      for (int g = 0; g < G; ++g) better(v, i, p.part_val[g], p.part_idx[g]);
+      s_best = v;
+      s_piv = i;
+    }
+    __syncthreads();
+  };
+
+  int r = 0;
+  for (; r < rmax; ++r) {
+    local_argmax(r);
+    grid.sync();
+    global_argmax(r);
+    if (tid == 0) s_recompute = (s_best <= 0.0 || s_best < 1e-8 * p.norms0[s_piv]) ? 1 : 0;
+    __syncthreads();
+    if (s_recompute) {
+      // exact recompute of the trailing norms (dense.cpp:503-518)
+      if (b == 0 && tid == 0) atomicAdd(p.recomputes, 1);
+      for (int64_t c = lmax(c0, r) + warp; c < c1; c += nwarps) {
+        const double* col = p.W + c * p.ld;
+        double s = 0.0;
+        for (int i = r + lane; i < m; i += 32) s = fma(col[i], col[i], s);
+        s = warp_sum(s);
+        if (lane == 0) p.norms2[c] = s;
+      }
+      __syncthreads();
+      grid.sync();
+      local_argmax(r);
+      grid.sync();
+      global_argmax(r);
+    }
+    if (tid == 0) s_stop = sqrt(fmax(0.0, s_best)) < p.halt ? 1 : 0;  // numerically exhausted
+    __syncthreads();
+    if (s_stop) break;
+    const int64_t piv = s_piv;
+    // read the old columns r and piv before anyone swaps them
+    const double* gp = p.W + piv * p.ld;
+    const double* gr = p.W + static_cast<int64_t>(r) * p.ld;
+    for (int i = tid; i < m; i += blockDim.x) {
+      colP[i] = gp[i];
+      colR[i] = gr[i];
+    }
+    if (tid == 0) {
+      s_oldn2_piv = p.norms2[piv];
+      s_oldn0_piv = p.norms0[piv];
+      s_oldn2_r = p.norms2[r];
+      s_oldn0_r = p.norms0[r];
+      s_perm_piv = p.perm[piv];
+      s_perm_r = p.perm[r];
+    }
+    __syncthreads();
+    // reflector for x = colP[r:m) (make_reflector, dense.cpp:328-357)
+    {
+      double sg = 0.0;
+      for (int i = r + 1 + tid; i < m; i += blockDim.x) sg = fma(colP[i], colP[i], sg);
+      __shared__ double red[32];
+      const double sigma = block_sum(sg, red);
+      const double alpha = colP[r];
+      double beta, result, v0 = 1.0;
+      if (sigma == 0.0) {
+        beta = alpha >= 0.0 ? 0.0 : 2.0;
+        result = fabs(alpha);
+      } else {
+        const double mu = sqrt(alpha * alpha + sigma);
+        v0 = (alpha <= 0.0) ? alpha - mu : -sigma / (alpha + mu);
+        beta = 2.0 * v0 * v0 / (sigma + v0 * v0);
+        result = mu;
+      }
+      for (int i = r + 1 + tid; i < m; i += blockDim.x) tail[i] = sigma == 0.0 ? 0.0 : colP[i] / v0;
+      if (tid == 0) {
+        s_beta = beta;
+        s_result = result;
+      }
+    }
+    __syncthreads();
+    grid.sync();  // every CTA holds the old columns r, piv
+    const double beta = s_beta;
+    // apply (I - beta v v^T), v = [1; tail], to owned columns c > r and do the swap
+    for (int64_t c = lmax(c0, r) + warp; c < c1; c += nwarps) {
+      double* col = p.W + c * p.ld;
+      if (c == r) {
+        for (int i = lane; i < m; i += 32) col[i] = (i < r) ? colP[i] : (i == r ? s_result : 0.0);
+        if (lane == 0) {
+          p.perm[r] = s_perm_piv;
+          p.norms2[r] = s_oldn2_piv;
+          p.norms0[r] = s_oldn0_piv;
+        }
+        continue;
+      }
+      const bool is_piv = (c == piv);
+      const double* src = is_piv ? colR : col;  // slot piv receives the old column r
+      double dot = 0.0;
+      for (int i = r + 1 + lane; i < m; i += 32) dot = fma(tail[i], src[i], dot);
+      dot = warp_sum(dot) + src[r];
+      const double bd = beta * dot;
+      if (is_piv) {
+        for (int i = lane; i < m; i += 32) {
+          double v = colR[i];
+          if (i == r) v -= bd;
+          else if (i > r) v -= bd * tail[i];
+          col[i] = v;
+        }
+      } else if (beta != 0.0) {
+        for (int i = r + lane; i < m; i += 32) col[i] = (i == r) ? col[i] - bd : col[i] - bd * tail[i];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const double wr = col[r];
+        double n2 = is_piv ? s_oldn2_r : p.norms2[c];
+        if (is_piv) {
+          p.perm[c] = s_perm_r;
+          p.norms0[c] = s_oldn0_r;
+        }
+        p.norms2[c] = n2 - wr * wr;  // down-date (dense.cpp:531-533)
+      }
+    }
+    __syncthreads();
+  }
+  if (b == 0 && tid == 0) p.stopped[0] = r;
+}
+
+// R^{-1} of the leading k x k upper triangle of R (ld ldr): warp per column,
+// back substitution R x = e_j in axpy form, x in the lanes' registers.
+template <int S>
+__global__ void trinv_upper_kernel(const double* __restrict__ R, int64_t ldr, int k, double* __restrict__ Rinv) {
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= k) return;
+  double x[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) x[s] = (lane + 32 * s == j) ? 1.0 : 0.0;
+  for (int i = j; i >= 0; --i) {
+    const int si = i >> 5;
+    double v = 0.0;
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      if (s == si) v = x[s];
+    const double* ri = R + static_cast<int64_t>(i) * ldr;
+    const double xi = __shfl_sync(0xffffffffu, v, i & 31) / ri[i];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int r = lane + 32 * s;
+      if (r == i) x[s] = xi;
+      else if (r < i) x[s] = fma(-xi, ri[r], x[s]);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int r = lane + 32 * s;
+    if (r < k) Rinv[static_cast<int64_t>(j) * k + r] = r <= j ? x[s] : 0.0;
+  }
+}
+
+// Z (ke x n): Z(:, perm[j]) = e_j for j < ke, = T(:, j - ke) otherwise.
+__global__ void assemble_z_kernel(const int64_t* __restrict__ perm, int ke, int64_t n,
+                                  const double* __restrict__ T, double* __restrict__ Z) {
+  const int64_t total = n * ke;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / ke;
+    const int i = static_cast<int>(e % ke);
+    const int64_t col = perm[j];
+    Z[col * ke + i] = (j < ke) ? (i == j ? 1.0 : 0.0) : T[(j - ke) * ke + i];
+  }
+}
+
+}  // namespace
+
+size_t cpqr_work_bytes(int64_t n, int grid) {
+  return sizeof(double) * 2 * n + sizeof(int64_t) * n + sizeof(double) * grid + sizeof(int64_t) * grid + 64;
+}
+
+cudaError_t cpqr_rank(double* W, int64_t ld, int m, int64_t n, int kmax, double halt, int64_t* perm, void* work,
+                      int* stopped, int* recomputes, int num_sms, cudaStream_t st) {
+  if (m > kMaxRows) return cudaErrorInvalidValue;
+  CpqrParams prm{};
+  prm.W = W;
+  prm.ld = ld;
+  prm.m = m;
+  prm.n = n;
+  prm.kmax = kmax;
+  prm.halt = halt;
+  char* w = static_cast<char*>(work);
+  prm.norms2 = reinterpret_cast<double*>(w);
+  prm.norms0 = prm.norms2 + n;
+  prm.part_val = prm.norms0 + n;
+  prm.part_idx = reinterpret_cast<int64_t*>(prm.part_val + num_sms);
+  prm.perm = perm;
+  prm.stopped = stopped;
+  prm.recomputes = recomputes;
+  void* args[] = {&prm};
+  cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cpqr_kernel), dim3(num_sms),
+                                              dim3(kCpqrThreads), args, 0, st);
+  count_launch();
+  return e;
+}
+
+cudaError_t trinv_upper(const double* R, int64_t ldr, int k, double* Rinv, cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  if (k > 352) return cudaErrorInvalidValue;
+  const int warps = 8;
+  trinv_upper_kernel<11><<<(k + warps - 1) / warps, warps * 32, 0, st>>>(R, ldr, k, Rinv);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t assemble_z(const int64_t* perm, int ke, int64_t n, const double* T, double* Z, cudaStream_t st) {
+  if (ke <= 0 || n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n * ke + 255) / 256, 148 * 8);
+  assemble_z_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(perm, ke, n, T, Z);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace rfgpu

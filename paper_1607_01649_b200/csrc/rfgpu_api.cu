@@ -55,6 +55,36 @@ __global__ void transpose_kernel(const double* __restrict__ in, int64_t rows, in
   }
 }
 
+__global__ void gather_cols_kernel(const double* __restrict__ A, int64_t lda, int64_t m, const int64_t* __restrict__ idx,
+                                   int64_t k, double* __restrict__ C, int64_t ldc) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < m * k;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / m, i = e % m;
+    C[j * ldc + i] = A[idx[j] * lda + i];
+  }
+}
+
+__global__ void gather_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t n, const int64_t* __restrict__ idx,
+                                   int64_t k, double* __restrict__ R, int64_t ldr) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * k;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / k, i = e % k;
+    R[j * ldr + i] = A[j * lda + idx[i]];
+  }
+}
+
+// scale row i of X (r x c, ld r) by inv(s_i) with the least_squares cutoff
+// (dense.cpp:825-837): 1/s if s > 1e-12 s_max and s > 0, else 0.
+__global__ void lsq_scale_kernel(double* __restrict__ X, int64_t r, int64_t c, const double* __restrict__ S) {
+  const double cutoff = (r > 0 ? S[0] : 0.0) * 1e-12;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < r * c;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % r;
+    const double d = S[i];
+    X[e] *= (d > cutoff && d > 0.0) ? 1.0 / d : 0.0;
+  }
+}
+
 }  // namespace
 
 cudaError_t add_scalar(double* dst, const double* src, cudaStream_t st) {
@@ -590,6 +620,142 @@ Status rsvd_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t k
   return {};
 }
 
+// ---- interpolative decompositions ------------------------------------------------
+inline unsigned grid1d(int64_t n) { return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1184))); }
+
+// SVD of a tall replicated matrix M (rows x c, ld ldm): M = Um diag(S) Vm^T
+// (svd_dense semantics, dense.cpp:585-701) via CholeskyQR2 + Jacobi on the
+// c x c factor, Jacobi on M itself when CholeskyQR is not accepted.
+Status svd_tall_dev(rfgpu_ctx* c, const double* M, int64_t rows, int64_t cols, int64_t ldm, double* Um, double* S,
+                    double* Vm) {
+  cudaStream_t st = c->stream;
+  const int64_t ldr = even(rows);
+  DBuf q, rr, r2i, ur, ur2, jw, inf, mc;
+  RF_TRY(q.alloc(sizeof(double) * std::max<int64_t>(1, ldr * cols), st));
+  RF_TRY(rr.alloc(sizeof(double) * cols * cols, st));
+  RF_TRY(r2i.alloc(sizeof(double) * cols * cols, st));
+  RF_TRY(inf.alloc(64, st));
+  Basis b;
+  b.Q = q.d();
+  b.ldq = ldr;
+  RF_TRY(orth(c, M, rows, cols, ldm, &b, r2i.d(), rr.d(), false, true));
+  int* info = inf.as<int>();
+  if (b.fast) {
+    RF_TRY(ur.alloc(sizeof(double) * cols * cols, st));
+    RF_TRY(ur2.alloc(sizeof(double) * cols * cols, st));
+    const size_t jwb = jacobi_work_bytes(cols, cols);
+    if (jwb) RF_TRY(jw.alloc(jwb, st));
+    {
+      Timed tj(c, "jacobi");
+      RF_CUDA(jacobi_svd(rr.d(), cols, cols, ur.d(), S, Vm, jw.d(), info, info + 1, st));
+    }
+    RF_TRY(gemm(c, false, cols, cols, cols, b.R2inv, cols, ur.d(), cols, ur2.d(), cols));
+    RF_TRY(gemm(c, false, rows, cols, cols, b.Q, ldr, ur2.d(), cols, Um, rows));
+  } else {
+    // Jacobi reads rows with stride `rows`: compact copy when ldm != rows
+    const double* src = M;
+    if (ldm != rows) {
+      RF_TRY(mc.alloc(sizeof(double) * rows * cols, st));
+      RF_CUDA(cudaMemcpy2DAsync(mc.d(), sizeof(double) * rows, M, sizeof(double) * ldm, sizeof(double) * rows, cols,
+                                cudaMemcpyDeviceToDevice, st));
+      src = mc.d();
+    }
+    const size_t jwb = jacobi_work_bytes(rows, cols);
+    if (jwb) RF_TRY(jw.alloc(jwb, st));
+    Timed tj(c, "jacobi");
+    RF_CUDA(jacobi_svd(src, rows, cols, Um, S, Vm, jw.d(), info, info + 1, st));
+  }
+  RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  RF_CUDA(cudaStreamSynchronize(st));
+  if (c->h_info[0] == 1) return make_err(RFGPU_ECONVERGENCE, "svd_dense: Jacobi sweeps did not converge");
+  return {};
+}
+
+// col_id_core (lowrank.cpp:51-70) of Y (m x n, ld ldy; not modified). Z_dev
+// receives ke x n (ld ke); Js_dev / Js_host (either may be null) the skeleton.
+Status col_id_dev(rfgpu_ctx* c, const double* Y, int64_t m, int64_t n, int64_t ldy, int64_t k, int64_t* Js_dev,
+                  int64_t* Js_host, double* Z, int64_t* ke_out, int* truncated) {
+  Timed t(c, "col_id");
+  cudaStream_t st = c->stream;
+  if (m > 512) return make_err(RFGPU_EPARAM, "col_id: sketch height above 512 is not supported on the device path");
+  if (k < 0 || k > std::min(m, n)) return make_err(RFGPU_EPARAM, "cpqr: rank target out of range");
+  const int64_t ldw = even(m);
+  DBuf W, perm, work, part, scal, R11i, T;
+  RF_TRY(W.alloc(sizeof(double) * ldw * std::max<int64_t>(1, n), st));
+  RF_TRY(perm.alloc(sizeof(int64_t) * std::max<int64_t>(1, n), st));
+  RF_TRY(work.alloc(cpqr_work_bytes(n, c->num_sms), st));
+  RF_TRY(part.alloc(sizeof(double) * 1024, st));
+  RF_TRY(scal.alloc(64, st));
+  if (n > 0 && m > 0)
+    RF_CUDA(cudaMemcpy2DAsync(W.d(), sizeof(double) * ldw, Y, sizeof(double) * ldy, sizeof(double) * m, n,
+                              cudaMemcpyDeviceToDevice, st));
+  // halt = 1e-14 ||Y||_F (dense.cpp:473-474)
+  double fro2 = 0.0;
+  for (int64_t j0 = 0; j0 < n; j0 += 1) {
+    if (ldw == m) {
+      RF_CUDA(sumsq(W.d(), m * n, part.d(), scal.d(), st));
+      break;
+    }
+    // ld padding: zero the pad row so a flat sum of squares is exact
+    RF_CUDA(cudaMemset2DAsync(W.d() + m, sizeof(double) * ldw, 0, sizeof(double), n, st));
+    RF_CUDA(sumsq(W.d(), ldw * n, part.d(), scal.d(), st));
+    break;
+  }
+  int* stopped = reinterpret_cast<int*>(scal.d() + 2);
+  RF_CUDA(cudaMemsetAsync(stopped, 0, 2 * sizeof(int), st));
+  RF_CUDA(cudaMemcpyAsync(c->h_d, scal.d(), sizeof(double), cudaMemcpyDeviceToHost, st));
+  RF_CUDA(cudaStreamSynchronize(st));
+  fro2 = c->h_d[0];
+  {
+    Timed tq(c, "cpqr");
+    RF_CUDA(cpqr_rank(W.d(), ldw, static_cast<int>(m), n, static_cast<int>(k), 1e-14 * std::sqrt(fro2), perm.as<int64_t>(),
+                      work.p, stopped, stopped + 1, c->num_sms, st));
+  }
+  RF_CUDA(cudaMemcpyAsync(c->h_info, stopped, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  RF_CUDA(cudaStreamSynchronize(st));
+  const int64_t ke = std::min<int64_t>(k, c->h_info[0]);
+  *ke_out = ke;
+  if (truncated) *truncated = ke < k ? 1 : 0;
+  if (std::getenv("RFGPU_DEBUG"))
+    std::fprintf(stderr, "[rfgpu] cpqr m=%lld n=%lld k=%lld stopped=%d recomputes=%d\n", (long long)m, (long long)n,
+                 (long long)k, c->h_info[0], c->h_info[1]);
+  if (Js_dev && ke > 0) RF_CUDA(cudaMemcpyAsync(Js_dev, perm.d(), sizeof(int64_t) * ke, cudaMemcpyDeviceToDevice, st));
+  if (Js_host && ke > 0) RF_CUDA(cudaMemcpyAsync(Js_host, perm.d(), sizeof(int64_t) * ke, cudaMemcpyDeviceToHost, st));
+  if (ke > 0) {
+    RF_TRY(T.alloc(sizeof(double) * ke * std::max<int64_t>(1, n - ke), st));
+    if (n > ke) {
+      RF_TRY(R11i.alloc(sizeof(double) * ke * ke, st));
+      RF_CUDA(trinv_upper(W.d(), ldw, static_cast<int>(ke), R11i.d(), st));
+      // T = S11^{-1} S12 (solve_upper, dense.cpp:788-804)
+      RF_TRY(gemm(c, false, ke, n - ke, ke, R11i.d(), ke, W.d() + ke * ldw, ldw, T.d(), ke, nullptr, "trsm_id"));
+    }
+    RF_CUDA(assemble_z(perm.as<int64_t>(), static_cast<int>(ke), n, T.d(), Z, st));
+  }
+  RF_CUDA(cudaStreamSynchronize(st));
+  return {};
+}
+
+// Transposed row sketch Yt = (G A)^T = A^T G^T (n x ell), q power passes
+// (lowrank.cpp:351-355: y <- (y A^T) A). Gt: m_loc x ell (this rank's rows of
+// G^T, ld ldg). Summed over ranks.
+Status row_sketch_t(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Gt, int64_t ldg, int64_t ell, int64_t q,
+                    double* Yt) {
+  const int64_t m = a->m, n = a->n;
+  const double* A = static_cast<const double*>(a->dev);
+  RF_TRY(gemm(c, true, n, ell, m, A, a->lda, Gt, ldg, Yt, n, nullptr, "pass_tn"));
+  RF_TRY(allreduce(c, Yt, n * ell));
+  if (q > 0) {
+    DBuf t;
+    RF_TRY(t.alloc(sizeof(double) * std::max<int64_t>(1, even(m) * ell), c->stream));
+    for (int64_t j = 0; j < q; ++j) {
+      RF_TRY(gemm(c, false, m, ell, n, A, a->lda, Yt, n, t.d(), even(m), nullptr, "pass_nn"));
+      RF_TRY(gemm(c, true, n, ell, m, A, a->lda, t.d(), even(m), Yt, n, nullptr, "pass_tn"));
+      RF_TRY(allreduce(c, Yt, n * ell));
+    }
+  }
+  return {};
+}
+
 // ---- host gaussian (randfact::gaussian) ----------------------------------------------
 inline uint64_t mix64(uint64_t z) {
   z ^= z >> 30;
@@ -973,24 +1139,213 @@ int rfgpu_rsvd(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t k, 
   return finish(s);
 }
 
-int rfgpu_row_sketch(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t ell, double* Y) {
-  (void)c; (void)a; (void)g; (void)ell; (void)Y;
-  return finish(make_err(RFGPU_EPARAM, "row_sketch: not available in this build"));
-}
 int rfgpu_row_sketch_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t ell, double* Y) {
-  (void)c; (void)a; (void)g; (void)ell; (void)Y;
-  return finish(make_err(RFGPU_EPARAM, "row_sketch: not available in this build"));
+  if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "row_sketch: bad handle"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status s = [&]() -> Status {
+    if (ell < 1) return make_err(RFGPU_EPARAM, "row_sketch: ell must be at least 1");
+    RF_TRY(ensure_device(c));
+    cudaStream_t st = c->stream;
+    const int64_t mg = a->m_global, n = a->n;
+    DBuf gt, yt;
+    RF_TRY(gt.alloc(sizeof(double) * mg * ell, st));
+    RF_TRY(yt.alloc(sizeof(double) * n * ell, st));
+    RF_CUDA(transpose(g, ell, mg, ell, gt.d(), mg, st));  // G (ell x m) -> G^T (m x ell)
+    RF_TRY(row_sketch_t(c, a, gt.d() + a->row0, mg, ell, 0, yt.d()));
+    RF_CUDA(transpose(yt.d(), n, ell, n, Y, ell, st));
+    RF_CUDA(cudaStreamSynchronize(st));
+    return {};
+  }();
+  return finish(s);
 }
-int rfgpu_col_id(rfgpu_ctx* c, const double* Y, int64_t m, int64_t n, int64_t k, int64_t* Js, double* Z,
-                 int64_t* rank_out, int* truncated) {
-  (void)c; (void)Y; (void)m; (void)n; (void)k; (void)Js; (void)Z; (void)rank_out; (void)truncated;
-  return finish(make_err(RFGPU_EPARAM, "col_id: not available in this build"));
+
+int rfgpu_row_sketch(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t ell, double* Yh) {
+  if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "row_sketch: bad handle"));
+  DBuf gd, yd;
+  Status s = [&]() -> Status {
+    RF_TRY(ensure_device(c));
+    RF_TRY(gd.alloc(sizeof(double) * a->m_global * ell, c->stream));
+    RF_TRY(yd.alloc(sizeof(double) * a->n * ell, c->stream));
+    RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * a->m_global * ell, cudaMemcpyHostToDevice, c->stream));
+    return {};
+  }();
+  if (!s.ok()) return finish(s);
+  int r = rfgpu_row_sketch_device(c, a, gd.d(), ell, yd.d());
+  if (r) return r;
+  cudaMemcpyAsync(Yh, yd.d(), sizeof(double) * a->n * ell, cudaMemcpyDeviceToHost, c->stream);
+  return rfgpu_ctx_synchronize(c);
 }
+
 int rfgpu_col_id_device(rfgpu_ctx* c, const double* Y, int64_t m, int64_t n, int64_t k, int64_t* Js, double* Z,
                         int64_t* rank_out, int* truncated) {
-  (void)c; (void)Y; (void)m; (void)n; (void)k; (void)Js; (void)Z; (void)rank_out; (void)truncated;
-  return finish(make_err(RFGPU_EPARAM, "col_id: not available in this build"));
+  if (!c) return finish(make_err(RFGPU_EPARAM, "col_id: null context"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status s = [&]() -> Status {
+    if (k < 1) return make_err(RFGPU_EPARAM, "id_deterministic: k must be at least 1");
+    if (k > std::min(m, n)) return make_err(RFGPU_EPARAM, "id_deterministic: k exceeds min(m, n)");
+    RF_TRY(ensure_device(c));
+    int64_t ke = 0;
+    RF_TRY(col_id_dev(c, Y, m, n, m, k, nullptr, Js, Z, &ke, truncated));
+    if (rank_out) *rank_out = ke;
+    return {};
+  }();
+  return finish(s);
 }
+
+int rfgpu_col_id(rfgpu_ctx* c, const double* Yh, int64_t m, int64_t n, int64_t k, int64_t* Js, double* Zh,
+                 int64_t* rank_out, int* truncated) {
+  if (!c) return finish(make_err(RFGPU_EPARAM, "col_id: null context"));
+  DBuf yd, zd;
+  Status s = [&]() -> Status {
+    RF_TRY(ensure_device(c));
+    RF_TRY(yd.alloc(sizeof(double) * std::max<int64_t>(1, m * n), c->stream));
+    RF_TRY(zd.alloc(sizeof(double) * std::max<int64_t>(1, std::max<int64_t>(k, 1) * n), c->stream));
+    if (m * n > 0) RF_CUDA(cudaMemcpyAsync(yd.d(), Yh, sizeof(double) * m * n, cudaMemcpyHostToDevice, c->stream));
+    return {};
+  }();
+  if (!s.ok()) return finish(s);
+  int64_t ke = 0;
+  int r = rfgpu_col_id_device(c, yd.d(), m, n, k, Js, zd.d(), &ke, truncated);
+  if (r) return r;
+  if (rank_out) *rank_out = ke;
+  if (ke > 0) cudaMemcpyAsync(Zh, zd.d(), sizeof(double) * ke * n, cudaMemcpyDeviceToHost, c->stream);
+  return rfgpu_ctx_synchronize(c);
+}
+
+int rfgpu_randomized_id(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t k, int64_t ell, int64_t q,
+                        int64_t* Is, double* Xh, int64_t* rank_out, int* truncated) {
+  if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "randomized_id: bad handle"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status s = [&]() -> Status {
+    RF_TRY(check_sample(a, k, ell, "randomized_id"));
+    if (q < 0) return make_err(RFGPU_EPARAM, "randomized_id: q must be non-negative");
+    if (c->world > 1) return make_err(RFGPU_EPARAM, "randomized_id: row sharding is not supported (single GPU)");
+    RF_TRY(ensure_device(c));
+    cudaStream_t st = c->stream;
+    const int64_t m = a->m, n = a->n, ldy = even(m);
+    const double* A = static_cast<const double*>(a->dev);
+    DBuf gd, y, z, yt, zt, x;
+    RF_TRY(gd.alloc(sizeof(double) * n * ell, st));
+    RF_TRY(y.alloc(sizeof(double) * ldy * ell, st));
+    RF_TRY(z.alloc(sizeof(double) * n * ell, st));
+    RF_TRY(yt.alloc(sizeof(double) * ell * m, st));
+    RF_TRY(zt.alloc(sizeof(double) * k * m, st));
+    RF_TRY(x.alloc(sizeof(double) * m * k, st));
+    RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
+    // tall sketch Y = (A A^T)^q A G (lowrank.cpp:316-320)
+    RF_TRY(gemm(c, false, m, ell, n, A, a->lda, gd.d(), n, y.d(), ldy, nullptr, "pass_nn"));
+    for (int64_t j = 0; j < q; ++j) {
+      RF_TRY(gemm(c, true, n, ell, m, A, a->lda, y.d(), ldy, z.d(), n, nullptr, "pass_tn"));
+      RF_TRY(gemm(c, false, m, ell, n, A, a->lda, z.d(), n, y.d(), ldy, nullptr, "pass_nn"));
+    }
+    RF_CUDA(transpose(y.d(), m, ell, ldy, yt.d(), ell, st));  // Y^T (ell x m)
+    int64_t ke = 0;
+    RF_TRY(col_id_dev(c, yt.d(), ell, m, ell, k, nullptr, Is, zt.d(), &ke, truncated));
+    if (ke > 0) {
+      RF_CUDA(transpose(zt.d(), ke, m, ke, x.d(), m, st));  // X = Z^T (m x ke)
+      RF_CUDA(cudaMemcpyAsync(Xh, x.d(), sizeof(double) * m * ke, cudaMemcpyDeviceToHost, st));
+    }
+    RF_CUDA(cudaStreamSynchronize(st));
+    if (rank_out) *rank_out = ke;
+    return {};
+  }();
+  return finish(s);
+}
+
+int rfgpu_randomized_cur(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t k, int64_t ell, int64_t q,
+                         int64_t* Js, int64_t* Is, double* Uh, double* cond_c, double* cond_r, int* warning,
+                         int64_t* kc_out, int64_t* kr_out) {
+  if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "randomized_cur: bad handle"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status s = [&]() -> Status {
+    RF_TRY(check_sample(a, k, ell, "randomized_cur"));
+    if (q < 0) return make_err(RFGPU_EPARAM, "randomized_cur: q must be non-negative");
+    if (c->world > 1) return make_err(RFGPU_EPARAM, "randomized_cur: row sharding is not supported (single GPU)");
+    RF_TRY(ensure_device(c));
+    cudaStream_t st = c->stream;
+    const int64_t m = a->m, n = a->n;
+    const double* A = static_cast<const double*>(a->dev);
+    DBuf gd, gt, yt, y, z, jsd, isd, cm, ct, zr, rm, rt, zt, um, sv, vm, w1, w2, xx, uc;
+    RF_TRY(gd.alloc(sizeof(double) * ell * m, st));
+    RF_TRY(gt.alloc(sizeof(double) * m * ell, st));
+    RF_TRY(yt.alloc(sizeof(double) * n * ell, st));
+    RF_TRY(y.alloc(sizeof(double) * ell * n, st));
+    RF_TRY(z.alloc(sizeof(double) * k * n, st));
+    RF_TRY(jsd.alloc(sizeof(int64_t) * k, st));
+    RF_TRY(isd.alloc(sizeof(int64_t) * k, st));
+    RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * ell * m, cudaMemcpyHostToDevice, st));
+    RF_CUDA(transpose(gd.d(), ell, m, ell, gt.d(), m, st));
+    // wide sketch Y = G A (+ q passes), lowrank.cpp:351-355
+    RF_TRY(row_sketch_t(c, a, gt.d(), m, ell, q, yt.d()));
+    RF_CUDA(transpose(yt.d(), n, ell, n, y.d(), ell, st));
+    // column ID of Y -> Js, Z (:357)
+    int64_t kc = 0, kr = 0;
+    int trc = 0, trr = 0;
+    RF_TRY(col_id_dev(c, y.d(), ell, n, ell, k, jsd.as<int64_t>(), Js, z.d(), &kc, &trc));
+    *kc_out = kc;
+    if (kc == 0) {
+      *kr_out = 0;
+      *cond_c = *cond_r = INFINITY;
+      *warning = 1;
+      return {};
+    }
+    // C = A(:, Js) (m x kc); row ID of C: col_id_core(C^T, kc) (:360-364)
+    RF_TRY(cm.alloc(sizeof(double) * m * kc, st));
+    RF_TRY(ct.alloc(sizeof(double) * kc * m, st));
+    RF_TRY(zr.alloc(sizeof(double) * kc * m, st));
+    gather_cols_kernel<<<grid1d(m * kc), 256, 0, st>>>(A, a->lda, m, jsd.as<int64_t>(), kc, cm.d(), m);
+    count_launch();
+    RF_CUDA(cudaGetLastError());
+    RF_CUDA(transpose(cm.d(), m, kc, m, ct.d(), kc, st));
+    RF_TRY(col_id_dev(c, ct.d(), kc, m, kc, kc, isd.as<int64_t>(), Is, zr.d(), &kr, &trr));
+    *kr_out = kr;
+    // R = A(Is, :) (kr x n); U = (lsq(R^T, Z^T))^T  (:365-367)
+    RF_TRY(rm.alloc(sizeof(double) * kr * n, st));
+    RF_TRY(rt.alloc(sizeof(double) * n * kr, st));
+    RF_TRY(zt.alloc(sizeof(double) * n * kc, st));
+    gather_rows_kernel<<<grid1d(n * kr), 256, 0, st>>>(A, a->lda, n, isd.as<int64_t>(), kr, rm.d(), kr);
+    count_launch();
+    RF_CUDA(cudaGetLastError());
+    RF_CUDA(transpose(rm.d(), kr, n, kr, rt.d(), n, st));
+    RF_CUDA(transpose(z.d(), kc, n, kc, zt.d(), n, st));
+    RF_TRY(um.alloc(sizeof(double) * n * kr, st));
+    RF_TRY(sv.alloc(sizeof(double) * std::max(kr, kc), st));
+    RF_TRY(vm.alloc(sizeof(double) * kr * kr, st));
+    RF_TRY(svd_tall_dev(c, rt.d(), n, kr, n, um.d(), sv.d(), vm.d()));
+    std::vector<double> sr(kr);
+    RF_CUDA(cudaMemcpyAsync(sr.data(), sv.d(), sizeof(double) * kr, cudaMemcpyDeviceToHost, st));
+    // X = V diag(1/s) U^T Z^T  (least_squares, dense.cpp:825-837)
+    RF_TRY(w1.alloc(sizeof(double) * kr * kc, st));
+    RF_TRY(xx.alloc(sizeof(double) * kr * kc, st));
+    RF_TRY(uc.alloc(sizeof(double) * kc * kr, st));
+    RF_TRY(gemm(c, true, kr, kc, n, um.d(), n, zt.d(), n, w1.d(), kr));
+    lsq_scale_kernel<<<grid1d(kr * kc), 256, 0, st>>>(w1.d(), kr, kc, sv.d());
+    count_launch();
+    RF_CUDA(cudaGetLastError());
+    RF_TRY(gemm(c, false, kr, kc, kr, vm.d(), kr, w1.d(), kr, xx.d(), kr));
+    RF_CUDA(transpose(xx.d(), kr, kc, kr, uc.d(), kc, st));  // U = X^T (kc x kr)
+    RF_CUDA(cudaMemcpyAsync(Uh, uc.d(), sizeof(double) * kc * kr, cudaMemcpyDeviceToHost, st));
+    // cond numbers (cond_number, lowrank.cpp:37-41): singular values of C and R
+    DBuf uc2, sc, vc2;
+    RF_TRY(uc2.alloc(sizeof(double) * m * kc, st));
+    RF_TRY(sc.alloc(sizeof(double) * kc, st));
+    RF_TRY(vc2.alloc(sizeof(double) * kc * kc, st));
+    RF_TRY(svd_tall_dev(c, cm.d(), m, kc, m, uc2.d(), sc.d(), vc2.d()));
+    std::vector<double> scv(kc);
+    RF_CUDA(cudaMemcpyAsync(scv.data(), sc.d(), sizeof(double) * kc, cudaMemcpyDeviceToHost, st));
+    RF_CUDA(cudaStreamSynchronize(st));
+    auto cond = [](const std::vector<double>& d) {
+      if (d.empty() || d.back() <= 0.0) return static_cast<double>(INFINITY);
+      return d.front() / d.back();
+    };
+    *cond_c = cond(scv);
+    *cond_r = cond(sr);
+    *warning = (*cond_c > 1e8 || *cond_r > 1e8) ? 1 : 0;
+    return {};
+  }();
+  return finish(s);
+}
+
 int rfgpu_dual_sketch_f32(rfgpu_ctx* c, const rfgpu_matrix* a, const float* gc, const float* gr, int64_t ell,
                           float* yc, float* yr) {
   (void)c; (void)a; (void)gc; (void)gr; (void)ell; (void)yc; (void)yr;

@@ -73,6 +73,16 @@ size_t gs_orth_work_doubles(int64_t m, int64_t c);
 cudaError_t gs_orth(const double* X, int64_t m, int64_t c, int64_t ldx, double* Q, int64_t ldq, int64_t* r_dev,
                     double* work, const DeviceAllreduce& ar, cudaStream_t st);
 
+// ---- column-pivoted QR / interpolative decomposition (cpqr.cu) -----------
+// In place on W (m x n, ld, m <= 512): cpqr with CpqrStop::rank(kmax) and the
+// reference pivot / recompute / halt rules; perm (n) device, *stopped (device)
+// = stopped rank, *recomputes (device) counts exact norm recomputes.
+size_t cpqr_work_bytes(int64_t n, int grid);
+cudaError_t cpqr_rank(double* W, int64_t ld, int m, int64_t n, int kmax, double halt, int64_t* perm, void* work,
+                      int* stopped, int* recomputes, int num_sms, cudaStream_t st);
+cudaError_t trinv_upper(const double* R, int64_t ldr, int k, double* Rinv, cudaStream_t st);
+cudaError_t assemble_z(const int64_t* perm, int ke, int64_t n, const double* T, double* Z, cudaStream_t st);
+
 // *dst += *src (one thread; keeps scalar bookkeeping on the device).
 cudaError_t add_scalar(double* dst, const double* src, cudaStream_t st);
 

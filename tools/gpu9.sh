@@ -1,0 +1,1 @@
+RFGPU_DEBUG=1 timeout 900 python -m pytest tests/test_gpu_id_cur.py -x -q 2>&1 | tail -30
