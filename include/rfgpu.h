@@ -168,6 +168,24 @@ int rfgpu_randomized_cur(rfgpu_ctx* ctx, const rfgpu_matrix* a, const double* g,
 int rfgpu_dual_sketch_f32(rfgpu_ctx* ctx, const rfgpu_matrix* a32, const float* gc, const float* gr, int64_t ell,
                           float* yc, float* yr);
 
+/* ---- single pass (randfact::single_pass_svd, proj/src/lowrank.cpp:160-220)
+ * Streaming form (MatrixStream, proj/include/randfact/stream.hpp:13-41):
+ * begin with Gc = gaussian(seed, "spsvd.Gc", n, ell) and
+ * Gr = gaussian(seed, "spsvd.Gr", m, ell); push every column block once, in
+ * order (ESTREAM otherwise); finish solves the core on the device and frees
+ * the state (U m x r, D r, V n x r, r = min(k, ell)). */
+typedef struct rfgpu_single_pass rfgpu_single_pass;
+int rfgpu_single_pass_begin(rfgpu_ctx* ctx, int64_t m, int64_t n, int64_t ell, const double* gc, const double* gr,
+                            rfgpu_single_pass** out);
+int rfgpu_single_pass_push(rfgpu_single_pass* sp, int64_t col0, const double* block, int64_t ncols);
+int rfgpu_single_pass_finish(rfgpu_single_pass* sp, int64_t k, double* U, double* D, double* V, int64_t* rank_out);
+int rfgpu_single_pass_abort(rfgpu_single_pass* sp);
+/* One-shot on a device-resident A (fp64 or fp32 handle; an fp32 matrix is
+ * widened chunk by chunk, every entry read once). Gc, Gr, U, D, V device. */
+int rfgpu_single_pass_svd_device(rfgpu_ctx* ctx, const rfgpu_matrix* a, const double* gc_dev, const double* gr_dev,
+                                 int64_t k, int64_t ell, double* U_dev, double* D_dev, double* V_dev,
+                                 int64_t* rank_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -111,6 +111,11 @@ _SIGS = {
     "rfgpu_col_id": (_int, [_vp, _pd, _i64, _i64, _i64, _pi, _pd, _pi, C.POINTER(_int)]),
     "rfgpu_col_id_device": (_int, [_vp, _vp, _i64, _i64, _i64, _pi, _vp, _pi, C.POINTER(_int)]),
     "rfgpu_dual_sketch_f32": (_int, [_vp, _vp, _pf, _pf, _i64, _pf, _pf]),
+    "rfgpu_single_pass_begin": (_int, [_vp, _i64, _i64, _i64, _pd, _pd, C.POINTER(_vp)]),
+    "rfgpu_single_pass_push": (_int, [_vp, _i64, _pd, _i64]),
+    "rfgpu_single_pass_finish": (_int, [_vp, _i64, _pd, _pd, _pd, _pi]),
+    "rfgpu_single_pass_abort": (_int, [_vp]),
+    "rfgpu_single_pass_svd_device": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _pi]),
     "rfgpu_randomized_id": (_int, [_vp, _vp, _pd, _i64, _i64, _i64, _pi, _pd, _pi, C.POINTER(_int)]),
     "rfgpu_randomized_cur": (_int, [_vp, _vp, _pd, _i64, _i64, _i64, _pi, _pi, _pd, _pd, _pd, C.POINTER(_int), _pi,
                                      _pi]),
@@ -530,4 +535,28 @@ class MatrixStream:
 
 
 def single_pass_svd(stream: MatrixStream, k: int, p: int, seed: int, ctx: Context | None = None) -> SvdFactors:
-    raise ParameterError("single_pass_svd: not available in this build")
+    """randfact::single_pass_svd(stream, k, p, seed): one traversal of the stream;
+    every block is pushed to the device once (Yc += A_blk Gc_blk, Yr_blk = A_blk^T Gr)
+    and the core is solved on the device."""
+    m, n = stream.rows(), stream.cols()
+    _check_sample(k, p, m, n, "single_pass_svd")
+    ctx = ctx or default_context()
+    ell = k + p
+    gc = gaussian(seed, "spsvd.Gc", n, ell)
+    gr = gaussian(seed, "spsvd.Gr", m, ell)
+    h = _vp()
+    _check(lib().rfgpu_single_pass_begin(ctx.handle, m, n, ell, _dp(_flat(gc)), _dp(_flat(gr)), C.byref(h)))
+    try:
+        while stream.has_next():
+            c0, blk = stream.next_block()
+            blk = np.asfortranarray(blk)
+            _check(lib().rfgpu_single_pass_push(h, c0, _dp(_flat(blk)), blk.shape[1]))
+    except BaseException:
+        lib().rfgpu_single_pass_abort(h)
+        raise
+    kk = min(k, ell)
+    U, D, V = np.zeros(m * kk), np.zeros(kk), np.zeros(n * kk)
+    r = _i64()
+    _check(lib().rfgpu_single_pass_finish(h, k, _dp(U), _dp(D), _dp(V), C.byref(r)))
+    rr = r.value
+    return SvdFactors(U[: m * rr].reshape((m, rr), order="F"), D[:rr].copy(), V[: n * rr].reshape((n, rr), order="F"))

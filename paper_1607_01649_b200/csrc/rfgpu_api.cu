@@ -85,6 +85,37 @@ __global__ void lsq_scale_kernel(double* __restrict__ X, int64_t r, int64_t c, c
   }
 }
 
+__global__ void add_inplace_kernel(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] += x[i];
+}
+
+// X(i, j) /= (a_i^2 + b_j^2): the Sylvester solve in the eigenbases.
+__global__ void sylvester_scale_kernel(double* __restrict__ X, int64_t k, const double* __restrict__ a,
+                                       const double* __restrict__ b) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < k * k;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % k, j = e / k;
+    X[e] /= (a[i] * a[i] + b[j] * b[j]);
+  }
+}
+
+__global__ void f32_to_f64_kernel(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
+                                  double* __restrict__ y, int64_t ldy) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < rows * cols;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    y[j * ldy + i] = static_cast<double>(x[j * ldx + i]);
+  }
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = static_cast<float>(x[i]);
+}
+
 }  // namespace
 
 cudaError_t add_scalar(double* dst, const double* src, cudaStream_t st) {
@@ -756,6 +787,95 @@ Status row_sketch_t(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Gt, int64
   return {};
 }
 
+// ---- single pass (lowrank.cpp:160-220) ------------------------------------------
+// Core of single_pass_svd from the two sketches, all on the device:
+// dominant_left(Yc, k), dominant_left(Yr, k) (:178-179), the small products
+// P = Gr^T Qc, E = Yr^T Qr, W = Qr^T Gc, F = Qc^T Yc (:184-187), the core C
+// from the normal equations of the reference's stacked least squares
+// (P^T P C + C W W^T = P^T E + F W^T) solved in the
+// eigenbases of P^T P and W W^T (right singular vectors of P and W^T), then
+// svd(C) and the lift U = Qc Uc, V = Qr Vc (:214-218).
+Status single_pass_core(rfgpu_ctx* c, const double* Yc, int64_t m, const double* Yr, int64_t n, const double* Gc,
+                        const double* Gr, int64_t k, int64_t ell, double* U, int64_t ldu, double* D, double* V,
+                        int64_t* rank_out) {
+  Timed t(c, "single_pass_core");
+  cudaStream_t st = c->stream;
+  const int64_t kk = std::min(k, ell);
+  DBuf uc, sc, vc, ur, sr, vr, P, E, W, F, Wt, up, sp, vp, uw, sw, vw, rhs, tmp, tmp2, cm, cu, cs, cv, den;
+  RF_TRY(uc.alloc(sizeof(double) * m * ell, st));
+  RF_TRY(sc.alloc(sizeof(double) * ell, st));
+  RF_TRY(vc.alloc(sizeof(double) * ell * ell, st));
+  RF_TRY(ur.alloc(sizeof(double) * n * ell, st));
+  RF_TRY(sr.alloc(sizeof(double) * ell, st));
+  RF_TRY(vr.alloc(sizeof(double) * ell * ell, st));
+  RF_TRY(svd_tall_dev(c, Yc, m, ell, m, uc.d(), sc.d(), vc.d()));  // Qc = uc(:, :kk)
+  RF_TRY(svd_tall_dev(c, Yr, n, ell, n, ur.d(), sr.d(), vr.d()));  // Qr = ur(:, :kk)
+  RF_TRY(P.alloc(sizeof(double) * ell * kk, st));
+  RF_TRY(E.alloc(sizeof(double) * ell * kk, st));
+  RF_TRY(W.alloc(sizeof(double) * kk * ell, st));
+  RF_TRY(F.alloc(sizeof(double) * kk * ell, st));
+  RF_TRY(Wt.alloc(sizeof(double) * ell * kk, st));
+  RF_TRY(gemm(c, true, ell, kk, m, Gr, m, uc.d(), m, P.d(), ell));   // P = Gr^T Qc
+  RF_TRY(gemm(c, true, ell, kk, n, Yr, n, ur.d(), n, E.d(), ell));   // E = Yr^T Qr
+  RF_TRY(gemm(c, true, kk, ell, n, ur.d(), n, Gc, n, W.d(), kk));    // W = Qr^T Gc
+  RF_TRY(gemm(c, true, kk, ell, m, uc.d(), m, Yc, m, F.d(), kk));    // F = Qc^T Yc
+  RF_CUDA(transpose(W.d(), kk, ell, kk, Wt.d(), ell, st));
+  // P = Up Sp Vp^T  =>  P^T P = Vp Sp^2 Vp^T;  W^T = Uw Sw Vw^T => W W^T = Vw Sw^2 Vw^T
+  RF_TRY(up.alloc(sizeof(double) * ell * kk, st));
+  RF_TRY(sp.alloc(sizeof(double) * kk, st));
+  RF_TRY(vp.alloc(sizeof(double) * kk * kk, st));
+  RF_TRY(uw.alloc(sizeof(double) * ell * kk, st));
+  RF_TRY(sw.alloc(sizeof(double) * kk, st));
+  RF_TRY(vw.alloc(sizeof(double) * kk * kk, st));
+  RF_TRY(svd_tall_dev(c, P.d(), ell, kk, ell, up.d(), sp.d(), vp.d()));
+  RF_TRY(svd_tall_dev(c, Wt.d(), ell, kk, ell, uw.d(), sw.d(), vw.d()));
+  // RHS = P^T E + F W^T
+  RF_TRY(rhs.alloc(sizeof(double) * kk * kk, st));
+  RF_TRY(tmp.alloc(sizeof(double) * kk * kk, st));
+  RF_TRY(tmp2.alloc(sizeof(double) * kk * kk, st));
+  RF_TRY(gemm(c, true, kk, kk, ell, P.d(), ell, E.d(), ell, rhs.d(), kk));
+  RF_TRY(gemm(c, false, kk, kk, ell, F.d(), kk, Wt.d(), ell, tmp.d(), kk));
+  add_inplace_kernel<<<grid1d(kk * kk), 256, 0, st>>>(rhs.d(), tmp.d(), kk * kk);
+  count_launch();
+  // Ct = Vp^T RHS Vw ./ (sp_i^2 + sw_j^2);  C = Vp Ct Vw^T
+  RF_TRY(gemm(c, true, kk, kk, kk, vp.d(), kk, rhs.d(), kk, tmp.d(), kk));
+  RF_TRY(gemm(c, false, kk, kk, kk, tmp.d(), kk, vw.d(), kk, tmp2.d(), kk));
+  sylvester_scale_kernel<<<grid1d(kk * kk), 256, 0, st>>>(tmp2.d(), kk, sp.d(), sw.d());
+  count_launch();
+  RF_CUDA(transpose(vw.d(), kk, kk, kk, tmp.d(), kk, st));  // Vw^T
+  RF_TRY(cm.alloc(sizeof(double) * kk * kk, st));
+  DBuf tmp3;
+  RF_TRY(tmp3.alloc(sizeof(double) * kk * kk, st));
+  RF_TRY(gemm(c, false, kk, kk, kk, vp.d(), kk, tmp2.d(), kk, tmp3.d(), kk));
+  RF_TRY(gemm(c, false, kk, kk, kk, tmp3.d(), kk, tmp.d(), kk, cm.d(), kk));
+  // svd(C) and the lift
+  RF_TRY(cu.alloc(sizeof(double) * kk * kk, st));
+  RF_TRY(cv.alloc(sizeof(double) * kk * kk, st));
+  RF_TRY(svd_tall_dev(c, cm.d(), kk, kk, kk, cu.d(), D, cv.d()));
+  RF_TRY(gemm(c, false, m, kk, kk, uc.d(), m, cu.d(), kk, U, ldu, nullptr, "lift"));
+  RF_TRY(gemm(c, false, n, kk, kk, ur.d(), n, cv.d(), kk, V, n, nullptr, "lift"));
+  *rank_out = kk;
+  return {};
+}
+
+// Dual sketch of the single pass (lowrank.cpp:170-176) for a resident column
+// block A(:, c0:c0+b) (m x b, ld lda): Yc += A_blk Gc(c0:c0+b, :), Yr(c0:c0+b, :)
+// = A_blk^T Gr. Both products run on the block while it is in HBM; the block
+// is consumed from the stream exactly once.
+Status dual_sketch_block(rfgpu_ctx* c, const double* Ablk, int64_t m, int64_t b, int64_t lda, int64_t c0, int64_t n,
+                         const double* Gc, const double* Gr, int64_t ell, double* Yc, double* Yr, double* scratch,
+                         bool first) {
+  cudaStream_t st = c->stream;
+  RF_TRY(gemm(c, false, m, ell, b, Ablk, lda, Gc + c0, n, first ? Yc : scratch, m, nullptr, "sketch_nn"));
+  if (!first) {
+    add_inplace_kernel<<<grid1d(m * ell), 256, 0, st>>>(Yc, scratch, m * ell);
+    count_launch();
+    RF_CUDA(cudaGetLastError());
+  }
+  RF_TRY(gemm(c, true, b, ell, m, Ablk, lda, Gr, m, Yr + c0, n, nullptr, "sketch_tn"));
+  return {};
+}
+
 // ---- host gaussian (randfact::gaussian) ----------------------------------------------
 inline uint64_t mix64(uint64_t z) {
   z ^= z >> 30;
@@ -1348,8 +1468,223 @@ int rfgpu_randomized_cur(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, i
 
 int rfgpu_dual_sketch_f32(rfgpu_ctx* c, const rfgpu_matrix* a, const float* gc, const float* gr, int64_t ell,
                           float* yc, float* yr) {
-  (void)c; (void)a; (void)gc; (void)gr; (void)ell; (void)yc; (void)yr;
-  return finish(make_err(RFGPU_EPARAM, "dual_sketch_f32: not available in this build"));
+  if (!c || !a || !a->f32) return finish(make_err(RFGPU_EPARAM, "dual_sketch_f32: needs an fp32 handle"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status st = [&]() -> Status {
+    RF_TRY(ensure_device(c));
+    cudaStream_t s = c->stream;
+    const int64_t m = a->m, n = a->n, ldc = even(m);
+    const int64_t chunk = std::max<int64_t>(256, std::min<int64_t>(n, (int64_t(1) << 28) / std::max<int64_t>(1, m)));
+    DBuf g32, gcd, grd, ycd, yrd, scratch, conv, out32;
+    RF_TRY(g32.alloc(sizeof(float) * std::max(m, n) * ell, s));
+    RF_TRY(gcd.alloc(sizeof(double) * n * ell, s));
+    RF_TRY(grd.alloc(sizeof(double) * m * ell, s));
+    RF_TRY(ycd.alloc(sizeof(double) * m * ell, s));
+    RF_TRY(yrd.alloc(sizeof(double) * n * ell, s));
+    RF_TRY(scratch.alloc(sizeof(double) * m * ell, s));
+    RF_TRY(conv.alloc(sizeof(double) * ldc * chunk, s));
+    RF_TRY(out32.alloc(sizeof(float) * std::max(m, n) * ell, s));
+    RF_CUDA(cudaMemcpyAsync(g32.p, gc, sizeof(float) * n * ell, cudaMemcpyHostToDevice, s));
+    f32_to_f64_kernel<<<grid1d(n * ell), 256, 0, s>>>(g32.as<float>(), n, ell, n, gcd.d(), n);
+    RF_CUDA(cudaMemcpyAsync(g32.p, gr, sizeof(float) * m * ell, cudaMemcpyHostToDevice, s));
+    f32_to_f64_kernel<<<grid1d(m * ell), 256, 0, s>>>(g32.as<float>(), m, ell, m, grd.d(), m);
+    count_launch(2);
+    bool first = true;
+    for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+      const int64_t b = std::min(chunk, n - c0);
+      f32_to_f64_kernel<<<grid1d(m * b), 256, 0, s>>>(static_cast<const float*>(a->dev) + c0 * a->lda, m, b, a->lda,
+                                                      conv.d(), ldc);
+      count_launch();
+      RF_TRY(dual_sketch_block(c, conv.d(), m, b, ldc, c0, n, gcd.d(), grd.d(), ell, ycd.d(), yrd.d(), scratch.d(),
+                               first));
+      first = false;
+    }
+    f64_to_f32_kernel<<<grid1d(m * ell), 256, 0, s>>>(ycd.d(), m * ell, out32.as<float>());
+    count_launch();
+    RF_CUDA(cudaMemcpyAsync(yc, out32.p, sizeof(float) * m * ell, cudaMemcpyDeviceToHost, s));
+    RF_CUDA(cudaStreamSynchronize(s));
+    f64_to_f32_kernel<<<grid1d(n * ell), 256, 0, s>>>(yrd.d(), n * ell, out32.as<float>());
+    count_launch();
+    RF_CUDA(cudaMemcpyAsync(yr, out32.p, sizeof(float) * n * ell, cudaMemcpyDeviceToHost, s));
+    RF_CUDA(cudaStreamSynchronize(s));
+    return {};
+  }();
+  return finish(st);
+}
+
+}  // extern "C"
+
+struct rfgpu_single_pass {
+  rfgpu_ctx* ctx = nullptr;
+  int64_t m = 0, n = 0, ell = 0, chunk = 0;
+  double* gc = nullptr;  // device n x ell
+  double* gr = nullptr;  // device m x ell
+  double* yc = nullptr;  // device m x ell
+  double* yr = nullptr;  // device n x ell
+  double* scratch = nullptr;  // m x ell
+  double* stage_d = nullptr;  // device m x chunk
+  double* stage_h = nullptr;  // pinned m x chunk
+  int64_t staged = 0, stage_c0 = 0, next_col = 0;
+  bool first = true;
+};
+
+namespace {
+Status sp_flush(rfgpu_single_pass* s) {
+  if (s->staged == 0) return {};
+  rfgpu_ctx* c = s->ctx;
+  RF_CUDA(cudaMemcpyAsync(s->stage_d, s->stage_h, sizeof(double) * s->m * s->staged, cudaMemcpyHostToDevice, c->stream));
+  RF_TRY(dual_sketch_block(c, s->stage_d, s->m, s->staged, s->m, s->stage_c0, s->n, s->gc, s->gr, s->ell, s->yc, s->yr,
+                           s->scratch, s->first));
+  RF_CUDA(cudaStreamSynchronize(c->stream));  // stage_h is reused by the next push
+  s->first = false;
+  s->stage_c0 += s->staged;
+  s->staged = 0;
+  return {};
+}
+
+void sp_free(rfgpu_single_pass* s) {
+  if (!s) return;
+  cudaSetDevice(s->ctx->device);
+  cudaStreamSynchronize(s->ctx->stream);
+  for (double* p : {s->gc, s->gr, s->yc, s->yr, s->scratch, s->stage_d})
+    if (p) cudaFree(p);
+  if (s->stage_h) cudaFreeHost(s->stage_h);
+  delete s;
+}
+}  // namespace
+
+extern "C" {
+
+int rfgpu_single_pass_begin(rfgpu_ctx* c, int64_t m, int64_t n, int64_t ell, const double* gc, const double* gr,
+                            rfgpu_single_pass** out) {
+  if (!c || !out) return finish(make_err(RFGPU_EPARAM, "single_pass: null argument"));
+  if (c->world > 1) return finish(make_err(RFGPU_EPARAM, "single_pass: row sharding is not supported (single GPU)"));
+  if (m < 1 || n < 1 || ell < 1) return finish(make_err(RFGPU_EPARAM, "single_pass_svd: bad dimensions"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  auto s = new rfgpu_single_pass();
+  s->ctx = c;
+  s->m = m;
+  s->n = n;
+  s->ell = ell;
+  // device staging chunk: ~1 GiB of columns, at least 256
+  s->chunk = std::max<int64_t>(256, std::min<int64_t>(n, (int64_t(1) << 27) / std::max<int64_t>(1, m)));
+  cudaSetDevice(c->device);
+  bool ok = cudaMalloc(&s->gc, sizeof(double) * n * ell) == cudaSuccess &&
+            cudaMalloc(&s->gr, sizeof(double) * m * ell) == cudaSuccess &&
+            cudaMalloc(&s->yc, sizeof(double) * m * ell) == cudaSuccess &&
+            cudaMalloc(&s->yr, sizeof(double) * n * ell) == cudaSuccess &&
+            cudaMalloc(&s->scratch, sizeof(double) * m * ell) == cudaSuccess &&
+            cudaMalloc(&s->stage_d, sizeof(double) * m * s->chunk) == cudaSuccess &&
+            cudaMallocHost(&s->stage_h, sizeof(double) * m * s->chunk) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    sp_free(s);
+    return finish(make_err(RFGPU_ENOMEM, "single_pass: device allocation failed"));
+  }
+  cudaMemcpy(s->gc, gc, sizeof(double) * n * ell, cudaMemcpyHostToDevice);
+  cudaMemcpy(s->gr, gr, sizeof(double) * m * ell, cudaMemcpyHostToDevice);
+  *out = s;
+  return RFGPU_OK;
+}
+
+int rfgpu_single_pass_push(rfgpu_single_pass* s, int64_t col0, const double* blk, int64_t b) {
+  if (!s) return finish(make_err(RFGPU_EPARAM, "single_pass: null state"));
+  rfgpu_ctx* c = s->ctx;
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status st = [&]() -> Status {
+    if (col0 != s->next_col || b < 0 || col0 + b > s->n)
+      return make_err(RFGPU_ESTREAM, "single_pass: blocks must arrive once, in column order");
+    RF_TRY(ensure_device(c));
+    int64_t done = 0;
+    while (done < b) {
+      const int64_t take = std::min(b - done, s->chunk - s->staged);
+      std::memcpy(s->stage_h + s->m * s->staged, blk + s->m * done, sizeof(double) * s->m * take);
+      s->staged += take;
+      done += take;
+      if (s->staged == s->chunk) RF_TRY(sp_flush(s));
+    }
+    s->next_col += b;
+    return {};
+  }();
+  return finish(st);
+}
+
+int rfgpu_single_pass_finish(rfgpu_single_pass* s, int64_t k, double* Uh, double* Dh, double* Vh, int64_t* rank_out) {
+  if (!s) return finish(make_err(RFGPU_EPARAM, "single_pass: null state"));
+  rfgpu_ctx* c = s->ctx;
+  Status st;
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    st = [&]() -> Status {
+      if (s->next_col != s->n) return make_err(RFGPU_ESTREAM, "single_pass: stream not fully consumed");
+      RF_TRY(ensure_device(c));
+      RF_TRY(sp_flush(s));
+      const int64_t m = s->m, n = s->n, kk = std::min(k, s->ell);
+      DBuf U, D, V;
+      RF_TRY(U.alloc(sizeof(double) * m * kk, c->stream));
+      RF_TRY(D.alloc(sizeof(double) * kk, c->stream));
+      RF_TRY(V.alloc(sizeof(double) * n * kk, c->stream));
+      int64_t r = 0;
+      RF_TRY(single_pass_core(c, s->yc, m, s->yr, n, s->gc, s->gr, k, s->ell, U.d(), m, D.d(), V.d(), &r));
+      RF_TRY(copy_out(c, Uh, m, U.d(), m, m, r));
+      RF_TRY(copy_out(c, Dh, r, D.d(), r, r, 1));
+      RF_TRY(copy_out(c, Vh, n, V.d(), n, n, r));
+      RF_CUDA(cudaStreamSynchronize(c->stream));
+      if (rank_out) *rank_out = r;
+      return {};
+    }();
+  }
+  sp_free(s);
+  return finish(st);
+}
+
+int rfgpu_single_pass_abort(rfgpu_single_pass* s) {
+  sp_free(s);
+  return RFGPU_OK;
+}
+
+int rfgpu_single_pass_svd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* gc, const double* gr, int64_t k,
+                                 int64_t ell, double* U, double* D, double* V, int64_t* rank_out) {
+  if (!c || !a) return finish(make_err(RFGPU_EPARAM, "single_pass_svd: bad handle"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status st = [&]() -> Status {
+    RF_TRY(check_sample(a, k, ell, "single_pass_svd"));
+    if (c->world > 1) return make_err(RFGPU_EPARAM, "single_pass: row sharding is not supported (single GPU)");
+    RF_TRY(ensure_device(c));
+    cudaStream_t s = c->stream;
+    const int64_t m = a->m, n = a->n;
+    DBuf yc, yr, scratch, conv;
+    RF_TRY(yc.alloc(sizeof(double) * m * ell, s));
+    RF_TRY(yr.alloc(sizeof(double) * n * ell, s));
+    RF_TRY(scratch.alloc(sizeof(double) * m * ell, s));
+    {
+      Timed t(c, "dual_sketch");
+      if (!a->f32) {
+        RF_TRY(dual_sketch_block(c, static_cast<const double*>(a->dev), m, n, a->lda, 0, n, gc, gr, ell, yc.d(), yr.d(),
+                                 scratch.d(), true));
+      } else {
+        // fp32 matrix: widened to fp64 one column chunk at a time (each entry read once)
+        const int64_t chunk = std::max<int64_t>(256, std::min<int64_t>(n, (int64_t(1) << 28) / std::max<int64_t>(1, m)));
+        const int64_t ldc = even(m);
+        RF_TRY(conv.alloc(sizeof(double) * ldc * chunk, s));
+        bool first = true;
+        for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+          const int64_t b = std::min(chunk, n - c0);
+          f32_to_f64_kernel<<<grid1d(m * b), 256, 0, s>>>(static_cast<const float*>(a->dev) + c0 * a->lda, m, b, a->lda,
+                                                          conv.d(), ldc);
+          count_launch();
+          RF_CUDA(cudaGetLastError());
+          RF_TRY(dual_sketch_block(c, conv.d(), m, b, ldc, c0, n, gc, gr, ell, yc.d(), yr.d(), scratch.d(), first));
+          first = false;
+        }
+      }
+    }
+    int64_t r = 0;
+    RF_TRY(single_pass_core(c, yc.d(), m, yr.d(), n, gc, gr, k, ell, U, m, D, V, &r));
+    if (rank_out) *rank_out = r;
+    return {};
+  }();
+  return finish(st);
 }
 
 }  // extern "C"

@@ -270,9 +270,35 @@ CurFactors randomized_cur(const DenseMatrix& a, idx k, idx p, idx q, std::uint64
 }
 
 SvdFactors single_pass_svd(MatrixStream& stream, idx k, idx p, std::uint64_t seed) {
-  check_sample(k, p, stream.rows(), stream.cols(), "single_pass_svd");
-  (void)seed;
-  throw ParameterError("single_pass_svd: device path not available in this build");
+  // lowrank.cpp:160-220: every block of the stream is consumed once and
+  // pushed to the device, where both sketches and the core solve live.
+  const idx m = stream.rows(), n = stream.cols();
+  check_sample(k, p, m, n, "single_pass_svd");
+  const idx ell = k + p;
+  const DenseMatrix gc = gaussian(seed, "spsvd.Gc", n, ell);
+  const DenseMatrix gr = gaussian(seed, "spsvd.Gr", m, ell);
+  std::lock_guard<std::mutex> lk(g_mu);
+  rfgpu_single_pass* sp = nullptr;
+  check(rfgpu_single_pass_begin(ctx(), m, n, ell, gc.data.data(), gr.data.data(), &sp));
+  try {
+    while (stream.has_next()) {
+      const MatrixStream::Block blk = stream.next_block();
+      check(rfgpu_single_pass_push(sp, blk.col0, blk.block.data.data(), blk.block.cols));
+    }
+  } catch (...) {
+    rfgpu_single_pass_abort(sp);
+    throw;
+  }
+  const idx kk = std::min(k, ell);
+  std::vector<double> u(static_cast<std::size_t>(m * kk)), d(static_cast<std::size_t>(kk)),
+      v(static_cast<std::size_t>(n * kk));
+  int64_t r = 0;
+  check(rfgpu_single_pass_finish(sp, k, u.data(), d.data(), v.data(), &r));
+  SvdFactors out;
+  out.U = make(m, r, u.data());
+  out.V = make(n, r, v.data());
+  out.D.assign(d.begin(), d.begin() + r);
+  return out;
 }
 
 namespace b200 {

@@ -167,3 +167,46 @@ def test_rsvd_validation(ctx, port):
         rf.rsvd(a, 2, 2, -1, 1, ctx=ctx)
     with pytest.raises(rf.ParameterError):
         rf.basic_range(a, 2, 2, 1, q=1, ctx=ctx)
+
+
+# ----------------------------------------------------------- single pass ---
+def test_single_pass_matches_reference_small_k(ctx, ref):
+    # the reference's own stacked least squares is feasible at small k
+    a = ref.planted(300, 250, np.exp(-np.arange(1, 101) / 10.0), 1)
+    want = ref.single_pass_svd(a, 10, 10, 3, block=32)
+    s = rf.MatrixStream(a, 32)
+    got = rf.single_pass_svd(s, 10, 10, 3, ctx=ctx)
+    assert s.passes_completed() == 1 and s.entries_served == 300 * 250
+    assert rel(got.D, want.D).max() < 1e-10
+    r1, r2 = np.linalg.norm(a - recon(got)), np.linalg.norm(a - recon(want))
+    assert abs(r1 - r2) <= 0.01 * r2
+
+
+def test_single_pass_matches_restated_oracle(ctx, port):
+    # config-4 family at reduced size: r = 200, s_j = exp(-j/10), noise 1e-4
+    m, n, k, p = 1500, 1200, 60, 10
+    a = planted(port, m, n, np.exp(-np.arange(1, 201) / 10.0), seed=1, noise=1e-4)
+    want = port.single_pass_svd(a, k, p, 1, block=64)
+    got = rf.single_pass_svd(rf.MatrixStream(a, 64), k, p, 1, ctx=ctx)
+    assert got.D.shape == want.D.shape == (k,)
+    assert rel(got.D, want.D).max() < 1e-8
+    assert np.abs(got.U.T @ got.U - np.eye(k)).max() < 1e-10
+
+
+def test_single_pass_exact_rank(ctx, port):
+    # test_lowrank.cpp:144-160
+    sig = 0.5 ** np.arange(5.0)
+    a = planted(port, 35, 25, sig, seed=6)
+    s = rf.MatrixStream(a, 6)
+    f = rf.single_pass_svd(s, 5, 5, 29, ctx=ctx)
+    assert s.passes_completed() == 1 and s.entries_served == 35 * 25
+    assert rel(f.D, sig).max() < 1e-7
+    assert np.linalg.norm(a - recon(f)) < 1e-7 * np.linalg.norm(a)
+
+
+def test_single_pass_stream_contract(ctx, port):
+    a = planted(port, 20, 16, geometric(4, 0.5), seed=2)
+    s = rf.MatrixStream(a, 7)
+    rf.single_pass_svd(s, 3, 2, 1, ctx=ctx)
+    with pytest.raises(rf.StreamContractError):
+        s.next_block()
