@@ -39,10 +39,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (m, n, k, p, q, r, spectrum, noise)
-    "c3": dict(m=1048576, n=4096, k=200, p=20, q=1, r=1024, spectrum="pow1.5", noise=1e-8),
-    "c2": dict(m=20000, n=10000, k=100, p=10, q=2, r=500, spectrum="exp20", noise=1e-6),
-    "c1": dict(m=2000, n=2000, k=50, p=10, q=1, r=2000, spectrum="pow2", noise=0.0),
+    # BASELINE.json configs: rsvd (configs 1-3), single pass (4), column ID / CUR (5)
+    "c3": dict(kind="rsvd", m=1048576, n=4096, k=200, p=20, q=1, r=1024, spectrum="pow1.5", noise=1e-8),
+    "c2": dict(kind="rsvd", m=20000, n=10000, k=100, p=10, q=2, r=500, spectrum="exp20", noise=1e-6),
+    "c1": dict(kind="rsvd", m=2000, n=2000, k=50, p=10, q=1, r=2000, spectrum="pow2", noise=0.0),
+    "c4": dict(kind="single_pass", m=65536, n=65536, k=300, p=30, q=0, r=2000, spectrum="exp100", noise=1e-4,
+               f32=True),
+    "c5": dict(kind="cur", m=32768, n=32768, k=300, p=20, q=0, r=1000, spectrum="decade6", noise=0.0),
 }
 CHUNK = 65536
 SEED = 1
@@ -57,6 +60,10 @@ def spectrum(kind, r):
         return np.exp(-j / 20.0)
     if kind == "pow2":
         return 1.0 / j ** 2
+    if kind == "exp100":
+        return np.exp(-j / 100.0)
+    if kind == "decade6":
+        return 10.0 ** (-6.0 * (j - 1) / (r - 1))
     raise ValueError(kind)
 
 
@@ -92,12 +99,17 @@ def gen_shard(torch, dist, w, row0, row1, dev):
     At = (V * sig) @ U.T  # n x rows
     del U, V
     if w["noise"]:
-        for c0 in range((row0 // CHUNK) * CHUNK, row1, CHUNK):
-            g.manual_seed(SEED * 2000003 + c0 // CHUNK)
-            blk = torch.randn(n, CHUNK, generator=g, device=dev, dtype=torch.float64)
-            a0, a1 = max(c0, row0), min(c0 + CHUNK, row1)
+        nch = max(1024, min(CHUNK, (1 << 28) // n))  # noise rows per draw (<= 2 GiB)
+        for c0 in range((row0 // nch) * nch, row1, nch):
+            g.manual_seed(SEED * 2000003 + c0 // nch)
+            blk = torch.randn(n, nch, generator=g, device=dev, dtype=torch.float64)
+            a0, a1 = max(c0, row0), min(c0 + nch, row1)
             At[:, a0 - row0:a1 - row0].add_(blk[:, a0 - c0:a1 - c0], alpha=w["noise"])
             del blk
+    if w.get("f32"):
+        At32 = At.float()
+        del At
+        return At32.contiguous()
     return At.contiguous()
 
 
@@ -198,8 +210,10 @@ def reference_arm(args, w, rank, world):
 
 
 def config_of(w, world, args):
-    return {"workload": f"{args.workload}: tall RSVD fp64 m={w['m']} n={w['n']} k={w['k']} p={w['p']} q={w['q']} "
-                        f"reorthonormalize=true", "m": w["m"], "n": w["n"], "k": w["k"], "p": w["p"], "q": w["q"],
+    desc = {"rsvd": f"RSVD fp64 m={w['m']} n={w['n']} k={w['k']} p={w['p']} q={w['q']} reorthonormalize=true",
+            "cur": f"column ID (row sketch G A + CPQR + Z) fp64 m={w['m']} n={w['n']} k={w['k']} p={w['p']}",
+            "single_pass": f"single-pass SVD, fp32 A (fp64 arithmetic) m={w['m']} n={w['n']} k={w['k']} p={w['p']}"}
+    return {"workload": f"{args.workload}: " + desc[w["kind"]], "m": w["m"], "n": w["n"], "k": w["k"], "p": w["p"], "q": w["q"],
             "rank_planted": w["r"], "noise": w["noise"], "seed": SEED, "parallelism": f"row-shard x{world}",
             "l2": "A (8*m*n bytes) larger than L2; no flush needed"}
 
@@ -247,17 +261,44 @@ def main():
     mloc = row1 - row0
     At = gen_shard(torch, dist, w, row0, row1, dev)
     torch.cuda.synchronize()
-    A = rf.DeviceMatrix.wrap(ctx, At.data_ptr(), mloc, n, mloc, keep=At)
-    G = torch.from_numpy(rf.gaussian(SEED, "range.G", n, ell).reshape(-1, order="F")).to(dev)
+    kind = w["kind"]
+    A = rf.DeviceMatrix.wrap(ctx, At.data_ptr(), mloc, n, mloc, f32=bool(w.get("f32")), keep=At)
     Ud = torch.empty(mloc * ell, device=dev, dtype=torch.float64)
     Dd = torch.empty(ell, device=dev, dtype=torch.float64)
     Vd = torch.empty(n * ell, device=dev, dtype=torch.float64)
     rank_out = C.c_int64()
+    trunc = C.c_int()
 
-    def step():
-        rf._check(L.rfgpu_rsvd_device(ctx.handle, A.handle, C.c_void_p(G.data_ptr()), k, ell, q, 0, 1,
-                                      C.c_void_p(Ud.data_ptr()), C.c_void_p(Dd.data_ptr()),
-                                      C.c_void_p(Vd.data_ptr()), C.byref(rank_out)))
+    def dev_gauss(tag, r, c):
+        return torch.from_numpy(rf.gaussian(SEED, tag, r, c).reshape(-1, order="F")).to(dev)
+
+    if kind == "rsvd":
+        G = dev_gauss("range.G", n, ell)
+
+        def step():
+            rf._check(L.rfgpu_rsvd_device(ctx.handle, A.handle, C.c_void_p(G.data_ptr()), k, ell, q, 0, 1,
+                                          C.c_void_p(Ud.data_ptr()), C.c_void_p(Dd.data_ptr()),
+                                          C.c_void_p(Vd.data_ptr()), C.byref(rank_out)))
+    elif kind == "cur":
+        G = dev_gauss("cur.G", ell, m)
+        Yd = torch.empty(ell * n, device=dev, dtype=torch.float64)
+        Zd = torch.empty(k * n, device=dev, dtype=torch.float64)
+        Js = np.zeros(k, dtype=np.int64)
+
+        def step():
+            rf._check(L.rfgpu_row_sketch_device(ctx.handle, A.handle, C.c_void_p(G.data_ptr()), ell,
+                                                C.c_void_p(Yd.data_ptr())))
+            rf._check(L.rfgpu_col_id_device(ctx.handle, C.c_void_p(Yd.data_ptr()), ell, n, k, rf._ip(Js),
+                                            C.c_void_p(Zd.data_ptr()), C.byref(rank_out), C.byref(trunc)))
+    else:
+        Gc = dev_gauss("spsvd.Gc", n, ell)
+        Gr = dev_gauss("spsvd.Gr", m, ell)
+
+        def step():
+            rf._check(L.rfgpu_single_pass_svd_device(ctx.handle, A.handle, C.c_void_p(Gc.data_ptr()),
+                                                     C.c_void_p(Gr.data_ptr()), k, ell, C.c_void_p(Ud.data_ptr()),
+                                                     C.c_void_p(Dd.data_ptr()), C.c_void_p(Vd.data_ptr()),
+                                                     C.byref(rank_out)))
 
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
 
@@ -292,13 +333,18 @@ def main():
     torch.cuda.synchronize()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     launches = ctx.launch_count() // args.steps
-    prof = {nm: ctx.profile_read(nm) for nm in ("pass_nn", "pass_tn", "orth", "small_svd", "jacobi", "gram", "trsm", "lift", "gemm_nn", "gemm_tn",
-                                                "allreduce")}
+    prof = {nm: ctx.profile_read(nm) for nm in ("pass_nn", "pass_tn", "sketch_nn", "sketch_tn", "orth", "small_svd",
+                                                "jacobi", "gram", "trsm", "lift", "col_id", "cpqr", "trsm_id",
+                                                "single_pass_core", "gemm_nn", "gemm_tn", "allreduce")}
     ctx.profile(False)
-    n_pass = prof["pass_nn"][0] + prof["pass_tn"][0]
-    pass_ms = prof["pass_nn"][1] + prof["pass_tn"][1]
+    pass_names = ("sketch_nn", "sketch_tn") if kind == "single_pass" else ("pass_nn", "pass_tn")
+    n_pass = sum(prof[nm][0] for nm in pass_names)
+    pass_ms = sum(prof[nm][1] for nm in pass_names)
+    # algorithmic flops of the passes over A (ell unpadded): 2 m n ell per pass;
+    # the single pass computes both sketches (4 m n ell) from one read of A
     flops_per_pass = 2.0 * mloc * n * ell
-    achieved = flops_per_pass * n_pass / (pass_ms * 1e-3) / 1e12 if pass_ms > 0 else None
+    passes_alg = {"rsvd": n_pass / args.steps, "cur": 1.0, "single_pass": 2.0}[kind]
+    achieved = flops_per_pass * passes_alg * args.steps / (pass_ms * 1e-3) / 1e12 if pass_ms > 0 else None
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tr_path):
@@ -309,7 +355,7 @@ def main():
 
     # ---- e2e through the host-buffer C ABI (upload + rsvd + D2H) -----------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and kind == "rsvd":
         try:
             Ah = torch.empty((n, mloc), dtype=torch.float64, pin_memory=True)
             Ah.copy_(At)
@@ -348,7 +394,7 @@ def main():
 
     # ---- CPU baseline (reference, bounded sample), rank 0 at N=1 ------------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and kind == "rsvd":
         rows = sample_rows_for(w, args.ref_rows)
         a_s = np.asfortranarray(At[:, :rows].T.cpu().numpy())
         threads = os.cpu_count() or 1
@@ -360,15 +406,19 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "rsvd_time_to_rank_k", "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "metric": {"rsvd": "rsvd_time_to_rank_k", "cur": "column_id_time",
+                       "single_pass": "single_pass_svd_time"}[kind],
+            "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (planted spectrum, seeded torch RNG on device)",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (planted spectrum, seeded torch RNG on device)" + (", A stored fp32" if w.get("f32") else ""),
             "config": config_of(w, world, args),
             "sketch_tflops": achieved,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
-                         "kernel": "gemm_f64_kernel (passes over A: pass_nn + pass_tn)",
-                         "per_launch_flops": flops_per_pass, "passes_per_step": n_pass / args.steps,
+                         "kernel": f"gemm_f64_tma_kernel (passes over A: {' + '.join(pass_names)})",
+                         "per_pass_flops": flops_per_pass, "passes_per_step": passes_alg,
+                         "launches_per_step": n_pass / args.steps,
                          "pass_ms_avg": pass_ms / n_pass if n_pass else None,
                          "peak_source": "FP64 DMMA microbenchmark profiles/r01_fp_peaks.txt (no FP64 entry in "
                                         "MEASURED_PEAKS.json)"},

@@ -168,6 +168,13 @@ int rfgpu_randomized_cur(rfgpu_ctx* ctx, const rfgpu_matrix* a, const double* g,
 int rfgpu_dual_sketch_f32(rfgpu_ctx* ctx, const rfgpu_matrix* a32, const float* gc, const float* gr, int64_t ell,
                           float* yc, float* yr);
 
+/* randfact::svd_dense for tall input (proj/src/dense.cpp:585-701 semantics:
+ * D non-increasing, U columns normalised): CholeskyQR2 + one-sided Jacobi on
+ * the cols x cols factor (cluster of up to 16 CTAs), or Jacobi on M when
+ * CholeskyQR is not accepted. rows >= cols; *sweeps = Jacobi sweeps used. */
+int rfgpu_svd(rfgpu_ctx* ctx, const double* M, int64_t rows, int64_t cols, double* U, double* S, double* V,
+              int* sweeps);
+
 /* ---- single pass (randfact::single_pass_svd, proj/src/lowrank.cpp:160-220)
  * Streaming form (MatrixStream, proj/include/randfact/stream.hpp:13-41):
  * begin with Gc = gaussian(seed, "spsvd.Gc", n, ell) and

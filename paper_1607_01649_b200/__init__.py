@@ -33,7 +33,7 @@ __all__ = [
     "StreamContractError", "DeviceError", "Context", "DeviceMatrix", "SvdFactors", "RangeBasis", "IdFactors",
     "CurFactors", "gaussian", "basic_range", "power_range", "rsvd", "randomized_id", "randomized_cur",
     "id_deterministic", "single_pass_svd", "MatrixStream", "library_path", "default_context", "row_sketch",
-    "multiply",
+    "multiply", "svd_dense",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -116,6 +116,7 @@ _SIGS = {
     "rfgpu_single_pass_finish": (_int, [_vp, _i64, _pd, _pd, _pd, _pi]),
     "rfgpu_single_pass_abort": (_int, [_vp]),
     "rfgpu_single_pass_svd_device": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _pi]),
+    "rfgpu_svd": (_int, [_vp, _pd, _i64, _i64, _pd, _pd, _pd, C.POINTER(_int)]),
     "rfgpu_randomized_id": (_int, [_vp, _vp, _pd, _i64, _i64, _i64, _pi, _pd, _pi, C.POINTER(_int)]),
     "rfgpu_randomized_cur": (_int, [_vp, _vp, _pd, _i64, _i64, _i64, _pi, _pi, _pd, _pd, _pd, C.POINTER(_int), _pi,
                                      _pi]),
@@ -421,6 +422,21 @@ def multiply(a, x, trans: bool = False, ctx: Context | None = None) -> np.ndarra
     finally:
         if tmp:
             dm.free()
+
+
+def svd_dense(a, ctx: Context | None = None) -> SvdFactors:
+    """randfact::svd_dense (dense.hpp:117) on the device: thin SVD, D non-increasing."""
+    a = _fmat(a)
+    m, n = a.shape
+    wide = m < n
+    x = np.asfortranarray(a.T) if wide else a
+    r, c = x.shape
+    ctx = ctx or default_context()
+    U, S, V = np.zeros(r * c), np.zeros(c), np.zeros(c * c)
+    sw = C.c_int()
+    _check(lib().rfgpu_svd(ctx.handle, _dp(_flat(x)), r, c, _dp(U), _dp(S), _dp(V), C.byref(sw)))
+    U, V = U.reshape((r, c), order="F"), V.reshape((c, c), order="F")
+    return SvdFactors(V, S, U) if wide else SvdFactors(U, S, V)
 
 
 def id_deterministic(a, k: int, side: str = "Col", ctx: Context | None = None) -> IdFactors:

@@ -135,3 +135,11 @@ namespace rfgpu {
 __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t lmax(int64_t a, int64_t b) { return a > b ? a : b; }
 }  // namespace rfgpu
+
+namespace rfgpu {
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t rbar) {
+  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(raddr),
+               "l"(__double_as_longlong(a)), "r"(rbar)
+               : "memory");
+}
+}  // namespace rfgpu

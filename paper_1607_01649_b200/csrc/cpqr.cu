@@ -113,12 +113,21 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
     }
   };
   auto global_argmax = [&](int r) {
-    if (tid == 0) {
+    // warp 0 combines the per-CTA winners (parallel loads, shuffle tree; the
+    // index tie-break makes the result independent of the combine order)
+    if (warp == 0) {
       double v = -1.0;
       int64_t i = r;
-      for (int g = 0; g < G; ++g) better(v, i, p.part_val[g], p.part_idx[g]);
-      s_best = v;
-      s_piv = i;
+      for (int g = lane; g < G; g += 32) better(v, i, __ldcg(p.part_val + g), __ldcg(p.part_idx + g));
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, i, o);
+        better(v, i, ov, oi);
+      }
+      if (lane == 0) {
+        s_best = v;
+        s_piv = i;
+      }
     }
     __syncthreads();
   };
@@ -193,7 +202,7 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
     grid.sync();  // every CTA holds the old columns r, piv
     const double beta = s_beta;
     // apply (I - beta v v^T), v = [1; tail], to owned columns c > r and do the swap
-    for (int64_t c = lmax(c0, r) + warp; c < c1; c += nwarps) {
+    auto slow_column = [&](int64_t c) {
       double* col = p.W + c * p.ld;
       if (c == r) {
         for (int i = lane; i < m; i += 32) col[i] = (i < r) ? colP[i] : (i == r ? s_result : 0.0);
@@ -202,7 +211,7 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
           p.norms2[r] = s_oldn2_piv;
           p.norms0[r] = s_oldn0_piv;
         }
-        continue;
+        return;
       }
       const bool is_piv = (c == piv);
       const double* src = is_piv ? colR : col;  // slot piv receives the old column r
@@ -223,12 +232,76 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
       __syncwarp();
       if (lane == 0) {
         const double wr = col[r];
-        double n2 = is_piv ? s_oldn2_r : p.norms2[c];
+        const double n2 = is_piv ? s_oldn2_r : p.norms2[c];
         if (is_piv) {
           p.perm[c] = s_perm_r;
           p.norms0[c] = s_oldn0_r;
         }
         p.norms2[c] = n2 - wr * wr;  // down-date (dense.cpp:531-533)
+      }
+    };
+    // Ordinary columns: two per warp, rows cached in registers (one L2 round
+    // trip per column), reflector applied in place, norm down-dated by the
+    // lane that owns row r.
+    constexpr int S = kMaxRows / 32;
+    const int sr = r >> 5, lr = r & 31;
+    const int64_t cstart = lmax(c0, r);
+    for (int64_t cb = cstart + 2 * warp; cb < c1; cb += 2 * nwarps) {
+      const int64_t ca = cb, cc2 = cb + 1;
+      const bool two = cc2 < c1;
+      if (ca == r || ca == piv || (two && (cc2 == r || cc2 == piv))) {
+        slow_column(ca);
+        if (two) slow_column(cc2);
+        continue;
+      }
+      double* pa = p.W + ca * p.ld;
+      double* pb = p.W + (two ? cc2 : ca) * p.ld;
+      double xa[S], xb[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        const bool in = i >= r && i < m;
+        xa[s] = in ? pa[i] : 0.0;
+        xb[s] = in ? pb[i] : 0.0;
+      }
+      double da = 0.0, db = 0.0, ra = 0.0, rb = 0.0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        if (i > r && i < m) {
+          const double t = tail[i];
+          da = fma(t, xa[s], da);
+          db = fma(t, xb[s], db);
+        }
+        if (s == sr) {
+          ra = xa[s];
+          rb = xb[s];
+        }
+      }
+      da = warp_sum(da) + __shfl_sync(0xffffffffu, ra, lr);
+      db = warp_sum(db) + __shfl_sync(0xffffffffu, rb, lr);
+      const double bda = beta * da, bdb = beta * db;
+      double wa = 0.0, wb = 0.0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        if (i < r || i >= m) continue;
+        double va = xa[s], vb = xb[s];
+        if (beta != 0.0) {
+          const double t = (i == r) ? 1.0 : tail[i];
+          va = (i == r) ? va - bda : va - bda * t;
+          vb = (i == r) ? vb - bdb : vb - bdb * t;
+          pa[i] = va;
+          if (two) pb[i] = vb;
+        }
+        if (i == r) {
+          wa = va;
+          wb = vb;
+        }
+      }
+      if (lane == lr) {
+        p.norms2[ca] -= wa * wa;
+        if (two) p.norms2[cc2] -= wb * wb;
       }
     }
     __syncthreads();

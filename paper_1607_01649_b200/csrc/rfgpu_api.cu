@@ -1687,4 +1687,31 @@ int rfgpu_single_pass_svd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const doub
   return finish(st);
 }
 
+
+int rfgpu_svd(rfgpu_ctx* c, const double* Mh, int64_t rows, int64_t cols, double* Uh, double* Sh, double* Vh,
+              int* sweeps) {
+  if (!c) return finish(make_err(RFGPU_EPARAM, "svd: null context"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status st = [&]() -> Status {
+    if (rows < cols) return make_err(RFGPU_EPARAM, "svd: device path expects rows >= cols (transpose wide input)");
+    if (cols < 1 || cols > 2048) return make_err(RFGPU_EPARAM, "svd: 1 <= cols <= 2048");
+    RF_TRY(ensure_device(c));
+    cudaStream_t s = c->stream;
+    DBuf M, U, S, V;
+    RF_TRY(M.alloc(sizeof(double) * rows * cols, s));
+    RF_TRY(U.alloc(sizeof(double) * rows * cols, s));
+    RF_TRY(S.alloc(sizeof(double) * cols, s));
+    RF_TRY(V.alloc(sizeof(double) * cols * cols, s));
+    RF_CUDA(cudaMemcpyAsync(M.d(), Mh, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, s));
+    RF_TRY(svd_tall_dev(c, M.d(), rows, cols, rows, U.d(), S.d(), V.d()));
+    if (sweeps) *sweeps = c->h_info[1];
+    RF_TRY(copy_out(c, Uh, rows, U.d(), rows, rows, cols));
+    RF_TRY(copy_out(c, Sh, cols, S.d(), cols, cols, 1));
+    RF_TRY(copy_out(c, Vh, cols, V.d(), cols, cols, cols));
+    RF_CUDA(cudaStreamSynchronize(s));
+    return {};
+  }();
+  return finish(st);
+}
+
 }  // extern "C"

@@ -200,6 +200,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
   const int rhx = (nrx + H - 1) / H, rhv = (nrv + H - 1) / H;
   const int x0 = min(nrx, h * rhx), x1 = min(nrx, x0 + rhx);
   const int v0 = min(nrv, h * rhv), v1 = min(nrv, v0 + rhv);
+  const int npo = (npairs + P - 1) / P;            // pairs per owner CTA
+  const int owned = (npairs - q + P - 1) / P;      // pairs owned by this CTA (k % P == q)
 
   extern __shared__ double sm[];
   double* Xs;
@@ -215,21 +217,21 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
     rest = sm;
   }
   const int np3 = npairs * 3;
-  uint64_t* rbar = reinterpret_cast<uint64_t*>(rest);  // [2] DSMEM arrival barriers (per parity)
-  double* red = rest + 2;                // [H][npairs][3]
-  double* pbuf = red + H * np3;          // [2][P][npairs][4]
-  double* rot = pbuf + 2 * P * npairs * 4;  // [npairs][2]
-  double* nrmp = rot + 2 * npairs;       // [P][cc]
-  double* nrm = nrmp + P * cc;           // [cc]
-  int* perm = reinterpret_cast<int*>(nrm + cc);  // [cc]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rest);  // [0..1] partial inbox, [2..3] params
+  double* params = rest + 4;                           // [2][npairs][2] (cs, sn; sn = 2 => skip)
+  double* inbox = params + 4 * npairs;                 // [2][P][npo][3]
+  double* red = inbox + 2 * P * npo * 3;               // [H][npairs][3], aliased by nrmp [P][cc]
+  const int red_sz = max(H * np3, P * cc);
+  double* nrmp = red;
+  double* nrm = red + red_sz;                          // [cc]
+  int* perm = reinterpret_cast<int*>(nrm + cc);        // [cc]
   __shared__ int s_rotated, s_conv;
 
   if (tid == 0) {
-    mbar_init(&rbar[0], 1);
-    mbar_init(&rbar[1], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
     mbar_fence_init();
   }
-  uint32_t rbar_uses[2] = {0u, 0u};
+  uint32_t uses[2] = {0u, 0u};
   for (int e = tid; e < c * RX; e += blockDim.x) {
     const int col = e / RX, r = e % RX;
     Xs[static_cast<size_t>(col) * LDX + r] = (r < nrx) ? p.X[static_cast<int64_t>(col) * p.mr + r0x + r] : 0.0;
@@ -289,6 +291,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
         cq = perm[b];
       }
       const bool valid = cp >= 0 && cq >= 0;
+      if (P > 1 && tid == 0) {
+        mbar_arrive_expect_tx(&bars[parity], static_cast<uint32_t>(P * owned * 24));
+        mbar_arrive_expect_tx(&bars[2 + parity], static_cast<uint32_t>(npairs * 16));
+      }
       // A. partial inner products over this warp's rows
       if (active && k < npairs) {
         double app = 0.0, aqq = 0.0, apq = 0.0;
@@ -307,11 +313,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
         d[1] = aqq;
         d[2] = apq;
       }
-      if (P > 1 && tid == 0) mbar_arrive_expect_tx(&rbar[parity], static_cast<uint32_t>(P * npairs * 32));
       __syncthreads();
-      // B. CTA partial -> every CTA of the cluster (st.async, counted on the
-      //    receiver's mbarrier; no cluster-wide barrier per round)
-      double* pb = pbuf + parity * P * npairs * 4;
+      // B. CTA partial -> the pair's owner CTA (k mod P)
+      double* ib = inbox + parity * P * npo * 3;
+      double* pr = params + parity * npairs * 2;
       if (h == 0 && k < npairs) {
         double app = 0.0, aqq = 0.0, apq = 0.0;
         for (int hh = 0; hh < H; ++hh) {
@@ -320,49 +325,53 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
           aqq += s[1];
           apq += s[2];
         }
+        double* slot = ib + (q * npo + k / P) * 3;
         if (P > 1) {
-          const uint32_t la = smem_u32(pb + (q * npairs + k) * 4), lb = smem_u32(&rbar[parity]);
-          for (int d = 0; d < P; ++d) {
-            const uint32_t ra = mapa_u32(la, d), rb = mapa_u32(lb, d);
-            st_async_v2(ra, app, aqq, rb);
-            st_async_v2(ra + 16, apq, 0.0, rb);
-          }
+          const uint32_t o = static_cast<uint32_t>(k % P);
+          const uint32_t ra = mapa_u32(smem_u32(slot), o), rb = mapa_u32(smem_u32(&bars[parity]), o);
+          st_async_f64(ra, app, rb);
+          st_async_f64(ra + 8, aqq, rb);
+          st_async_f64(ra + 16, apq, rb);
         } else {
-          double* dst = pb + k * 4;
-          dst[0] = app;
-          dst[1] = aqq;
-          dst[2] = apq;
+          slot[0] = app;
+          slot[1] = aqq;
+          slot[2] = apq;
         }
       }
       if (P == 1) __syncthreads();
-      else if (h == 0) mbar_wait(&rbar[parity], rbar_uses[parity] & 1u);
-      rbar_uses[parity] += 1u;
-      // C. rotation parameters (one lane per pair)
-      if (h == 0 && k < npairs) {
+      else if (h == 0) mbar_wait(&bars[parity], uses[parity] & 1u);
+      // C. owners: rotation parameters (reference formula), broadcast to all
+      if (h == 0 && k < npairs && k % P == q) {
         double app = 0.0, aqq = 0.0, apq = 0.0;
         for (int d = 0; d < P; ++d) {
-          const double* s = pb + (d * npairs + k) * 4;
+          const double* s = ib + (d * npo + k / P) * 3;
           app += s[0];
           aqq += s[1];
           apq += s[2];
         }
-        double cs = 1.0, sn = 0.0;
-        bool do_rot = valid && app != 0.0 && aqq != 0.0 && !(fabs(apq) <= 1e-15 * sqrt(app * aqq));
-        if (do_rot) {
+        double cs = 1.0, sn = 2.0;
+        if (valid && app != 0.0 && aqq != 0.0 && !(fabs(apq) <= 1e-15 * sqrt(app * aqq))) {
           const double zeta = (aqq - app) / (2.0 * apq);
           const double t = (zeta < 0.0 ? -1.0 : 1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           cs = 1.0 / sqrt(1.0 + t * t);
           sn = cs * t;
-          s_rotated = 1;
         }
-        rot[2 * k] = cs;
-        rot[2 * k + 1] = do_rot ? sn : 2.0;  // 2.0 marks "skip"
+        if (P > 1) {
+          const uint32_t la = smem_u32(pr + 2 * k), lb = smem_u32(&bars[2 + parity]);
+          for (int d = 0; d < P; ++d) st_async_v2(mapa_u32(la, d), cs, sn, mapa_u32(lb, d));
+        } else {
+          pr[2 * k] = cs;
+          pr[2 * k + 1] = sn;
+        }
       }
-      __syncthreads();
+      if (P == 1) __syncthreads();
+      else if (active) mbar_wait(&bars[2 + parity], uses[parity] & 1u);
+      uses[parity] += 1u;
       // D. rotate this warp's rows of X and V
       if (active && k < npairs && valid) {
-        const double cs = rot[2 * k], sn = rot[2 * k + 1];
+        const double cs = pr[2 * k], sn = pr[2 * k + 1];
         if (sn != 2.0) {
+          if (h == 0) s_rotated = 1;
           double* xp = Xs + static_cast<size_t>(cp) * LDX;
           double* xq = Xs + static_cast<size_t>(cq) * LDX;
           for (int r = x0; r < x1; ++r) {
@@ -390,7 +399,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
 
   // final singular values, stable descending order
   norms();
-  double* sig = rot;  // 2*npairs >= c doubles
+  double* sig = red + P * cc;  // free after norms(): red_sz >= P*cc, use params-sized scratch instead
+  sig = params;                // 4*npairs >= c doubles
   for (int j = tid; j < c; j += blockDim.x) sig[j] = sqrt(nrm[j]);
   __syncthreads();
   sort_desc(sig);
@@ -436,10 +446,12 @@ JacobiLayout jacobi_layout(int64_t mr, int64_t c) {
   const int64_t cc = c + (c & 1), npairs = cc / 2;
   const int64_t G = (npairs + 31) / 32, H = 32 / G;
   auto extra = [&](int P) {
-    return sizeof(double) * (2 + H * npairs * 3 + 2 * P * npairs * 4 + 2 * npairs + P * cc + cc) + sizeof(int) * cc + 64;
+    const int64_t npo = (npairs + P - 1) / P;
+    return sizeof(double) * (4 + 4 * npairs + 2 * P * npo * 3 + std::max<int64_t>(H * npairs * 3, P * cc) + cc) +
+           sizeof(int) * cc + 64;
   };
   constexpr size_t kMax = 224 * 1024;
-  for (int P : {1, 2, 4, 8}) {
+  for (int P : {1, 2, 4, 8, 16}) {
     const int RX = static_cast<int>((mr + P - 1) / P), RV = static_cast<int>((c + P - 1) / P);
     const int LDX = pad_ld(RX), LDV = pad_ld(RV);
     const size_t b = sizeof(double) * static_cast<size_t>(c) * (LDX + LDV) + extra(P);
@@ -522,6 +534,8 @@ cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double
     if (L.bytes > c1) {
       e = cudaFuncSetAttribute(jacobi_svd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(L.bytes));
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(jacobi_svd_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
       c1 = L.bytes;
     }

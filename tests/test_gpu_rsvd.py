@@ -210,3 +210,18 @@ def test_single_pass_stream_contract(ctx, port):
     rf.single_pass_svd(s, 3, 2, 1, ctx=ctx)
     with pytest.raises(rf.StreamContractError):
         s.next_block()
+
+
+@pytest.mark.parametrize("m,n", [(60, 60), (500, 110), (220, 220), (2000, 300), (330, 330), (5000, 64)])
+def test_svd_dense_matches_oracle(ctx, port, m, n):
+    rng = np.random.default_rng(m + n)
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    s = np.arange(1, n + 1, dtype=np.float64) ** -1.5
+    a = np.asfortranarray((u * s) @ v.T)
+    want = port.svd(a)
+    got = rf.svd_dense(a, ctx=ctx)
+    assert rel(got.D, want.D).max() < 1e-12
+    assert np.abs(got.U.T @ got.U - np.eye(n)).max() < 1e-12
+    assert np.abs(got.V.T @ got.V - np.eye(n)).max() < 1e-12
+    assert np.linalg.norm(a - (got.U * got.D) @ got.V.T) < 1e-13 * np.linalg.norm(a) * np.sqrt(n)
