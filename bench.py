@@ -349,7 +349,8 @@ def main():
     tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get(args.workload)
+            t = json.load(open(tr_path)).get(args.workload)
+            traffic = t.get("traffic_bytes") if isinstance(t, dict) else t
         except Exception:
             traffic = None
 

@@ -34,26 +34,35 @@ struct CpqrParams {
   int64_t ld;
   int m;
   int64_t n;
-  int kmax;          // rank stop
-  double halt;       // 1e-14 ||Y||_F
-  double* norms2;    // [n]
-  double* norms0;    // [n]
-  int64_t* perm;     // [n]
-  double* part_val;  // [grid]
-  int64_t* part_idx; // [grid]
-  int* stopped;      // [1] stopped rank
-  int* recomputes;   // [1]
+  int kmax;           // rank stop
+  double halt;        // 1e-14 ||Y||_F
+  double* norms2;     // [n]
+  double* norms0;     // [n]
+  int64_t* perm;      // [n]
+  // per-step staging (double-buffered by step parity): every CTA publishes
+  // its local winner (value, index, perm, norm0, the column itself); the
+  // owner of slot r publishes column r. Readers never touch W columns that
+  // their owners are rewriting in the same phase.
+  double* part_val;   // [2][grid]
+  int64_t* part_idx;  // [2][grid]
+  int64_t* part_perm; // [2][grid]
+  double* part_n0;    // [2][grid]
+  double* stage_col;  // [2][grid][m]
+  double* stage_r;    // [2][m + 4]: column r, then perm, norms2, norms0
+  int* stopped;       // [1] stopped rank
+  int* recomputes;    // [1]
 };
 
 __device__ __forceinline__ void better(double& bv, int64_t& bi, double v, int64_t i) {
   // "first index attaining the maximum": strictly larger value, or equal value
-  // at a smaller index (only reachable when combining partial winners).
+  // at a smaller index (a total order, so the combine order does not matter).
   if (v > bv || (v == bv && i < bi)) {
     bv = v;
     bi = i;
   }
 }
 
+template <int S>
 __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams p) {
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x, b = blockIdx.x;
@@ -61,35 +70,25 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
   const int64_t cpb = (p.n + G - 1) / G;
   const int64_t c0 = lmin(p.n, b * cpb), c1 = lmin(p.n, c0 + cpb);
   const int m = p.m;
-  const int rmax = lmin(lmin(m, p.n), p.kmax);
+  const int rmax = static_cast<int>(lmin(lmin(m, p.n), p.kmax));
 
   __shared__ double colP[kMaxRows], colR[kMaxRows], tail[kMaxRows];
   __shared__ double s_val[32];
   __shared__ int64_t s_idx[32];
-  __shared__ double s_beta, s_result, s_best, s_oldn2_piv, s_oldn0_piv, s_oldn2_r, s_oldn0_r;
+  __shared__ double s_beta, s_result, s_best, s_n2r, s_n0r, s_n0p;
   __shared__ int64_t s_piv, s_perm_piv, s_perm_r;
   __shared__ int s_stop, s_recompute;
 
-  // initial norms (dense.cpp:466-471) and identity permutation
-  for (int64_t c = c0 + warp; c < c1; c += nwarps) {
-    const double* col = p.W + c * p.ld;
-    double s = 0.0;
-    for (int i = lane; i < m; i += 32) s = fma(col[i], col[i], s);
-    s = warp_sum(s);
-    if (lane == 0) {
-      p.norms2[c] = s;
-      p.norms0[c] = s;
-      p.perm[c] = c;
-    }
-  }
-  grid.sync();
+  auto owner = [&](int64_t c) { return static_cast<int>(c / cpb); };
 
-  auto local_argmax = [&](int r) {
+  // Local winner over owned columns c >= r; published with a copy of the
+  // winning column into buffer `buf`. Slot r's owner also stages column r.
+  auto publish = [&](int r, int buf) {
     double bv = -1.0;
     int64_t bi = r;
     for (int64_t c = lmax(c0, r) + tid; c < c1; c += blockDim.x) {
       const double v = p.norms2[c];
-      if (v > bv) {  // strided scan: ties resolved by index in the combine
+      if (v > bv) {
         bv = v;
         bi = c;
       }
@@ -104,21 +103,50 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
       s_idx[warp] = bi;
     }
     __syncthreads();
-    if (tid == 0) {
-      double v = -1.0;
-      int64_t i = r;
-      for (int w = 0; w < nwarps; ++w) better(v, i, s_val[w], s_idx[w]);
-      p.part_val[b] = v;
-      p.part_idx[b] = i;
-    }
-  };
-  auto global_argmax = [&](int r) {
-    // warp 0 combines the per-CTA winners (parallel loads, shuffle tree; the
-    // index tie-break makes the result independent of the combine order)
     if (warp == 0) {
       double v = -1.0;
       int64_t i = r;
-      for (int g = lane; g < G; g += 32) better(v, i, __ldcg(p.part_val + g), __ldcg(p.part_idx + g));
+      for (int w = lane; w < nwarps; w += 32) better(v, i, s_val[w], s_idx[w]);
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, i, o);
+        better(v, i, ov, oi);
+      }
+      if (lane == 0) {
+        s_val[0] = v;
+        s_idx[0] = i;
+      }
+    }
+    __syncthreads();
+    const int64_t wi = s_idx[0];
+    if (tid == 0) {
+      p.part_val[buf * G + b] = s_val[0];
+      p.part_idx[buf * G + b] = wi;
+      const bool mine = wi >= c0 && wi < c1;
+      p.part_perm[buf * G + b] = mine ? p.perm[wi] : -1;
+      p.part_n0[buf * G + b] = mine ? p.norms0[wi] : 0.0;
+    }
+    if (wi >= c0 && wi < c1) {
+      const double* src = p.W + wi * p.ld;
+      double* dst = p.stage_col + (static_cast<int64_t>(buf) * G + b) * m;
+      for (int i = tid; i < m; i += blockDim.x) dst[i] = src[i];
+    }
+    if (r < p.n && r >= c0 && r < c1) {
+      const double* src = p.W + static_cast<int64_t>(r) * p.ld;
+      double* dst = p.stage_r + static_cast<int64_t>(buf) * (m + 4);
+      for (int i = tid; i < m; i += blockDim.x) dst[i] = src[i];
+      if (tid == 0) {
+        dst[m] = static_cast<double>(p.perm[r]);
+        dst[m + 1] = p.norms2[r];
+        dst[m + 2] = p.norms0[r];
+      }
+    }
+  };
+  auto global_winner = [&](int r, int buf) {
+    if (warp == 0) {
+      double v = -1.0;
+      int64_t i = r;
+      for (int g = lane; g < G; g += 32) better(v, i, __ldcg(p.part_val + buf * G + g), __ldcg(p.part_idx + buf * G + g));
       for (int o = 16; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, v, o);
         const int64_t oi = __shfl_xor_sync(0xffffffffu, i, o);
@@ -127,21 +155,41 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
       if (lane == 0) {
         s_best = v;
         s_piv = i;
+        const int w = owner(i);
+        s_n0p = __ldcg(p.part_n0 + buf * G + w);
+        s_perm_piv = __ldcg(p.part_perm + buf * G + w);
       }
     }
     __syncthreads();
   };
 
+  // initial norms (dense.cpp:466-471) and identity permutation
+  for (int64_t c = c0 + warp; c < c1; c += nwarps) {
+    const double* col = p.W + c * p.ld;
+    double s = 0.0;
+    for (int i = lane; i < m; i += 32) s = fma(col[i], col[i], s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      p.norms2[c] = s;
+      p.norms0[c] = s;
+      p.perm[c] = c;
+    }
+  }
+  __syncthreads();
+  if (rmax > 0) publish(0, 0);
+  grid.sync();
+
+  constexpr int SMAX = S;
   int r = 0;
   for (; r < rmax; ++r) {
-    local_argmax(r);
-    grid.sync();
-    global_argmax(r);
-    if (tid == 0) s_recompute = (s_best <= 0.0 || s_best < 1e-8 * p.norms0[s_piv]) ? 1 : 0;
+    const int buf = r & 1;
+    global_winner(r, buf);
+    if (tid == 0) s_recompute = (s_best <= 0.0 || s_best < 1e-8 * s_n0p) ? 1 : 0;
     __syncthreads();
     if (s_recompute) {
       // exact recompute of the trailing norms (dense.cpp:503-518)
       if (b == 0 && tid == 0) atomicAdd(p.recomputes, 1);
+      grid.sync();  // everyone has read the stale winners
       for (int64_t c = lmax(c0, r) + warp; c < c1; c += nwarps) {
         const double* col = p.W + c * p.ld;
         double s = 0.0;
@@ -150,29 +198,26 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
         if (lane == 0) p.norms2[c] = s;
       }
       __syncthreads();
+      publish(r, buf);
       grid.sync();
-      local_argmax(r);
-      grid.sync();
-      global_argmax(r);
+      global_winner(r, buf);
     }
     if (tid == 0) s_stop = sqrt(fmax(0.0, s_best)) < p.halt ? 1 : 0;  // numerically exhausted
     __syncthreads();
     if (s_stop) break;
     const int64_t piv = s_piv;
-    // read the old columns r and piv before anyone swaps them
-    const double* gp = p.W + piv * p.ld;
-    const double* gr = p.W + static_cast<int64_t>(r) * p.ld;
-    for (int i = tid; i < m; i += blockDim.x) {
-      colP[i] = gp[i];
-      colR[i] = gr[i];
-    }
-    if (tid == 0) {
-      s_oldn2_piv = p.norms2[piv];
-      s_oldn0_piv = p.norms0[piv];
-      s_oldn2_r = p.norms2[r];
-      s_oldn0_r = p.norms0[r];
-      s_perm_piv = p.perm[piv];
-      s_perm_r = p.perm[r];
+    {
+      const double* sp = p.stage_col + (static_cast<int64_t>(buf) * G + owner(piv)) * m;
+      const double* sr = p.stage_r + static_cast<int64_t>(buf) * (m + 4);
+      for (int i = tid; i < m; i += blockDim.x) {
+        colP[i] = __ldcg(sp + i);
+        colR[i] = __ldcg(sr + i);
+      }
+      if (tid == 0) {
+        s_perm_r = static_cast<int64_t>(__ldcg(sr + m));
+        s_n2r = __ldcg(sr + m + 1);
+        s_n0r = __ldcg(sr + m + 2);
+      }
     }
     __syncthreads();
     // reflector for x = colP[r:m) (make_reflector, dense.cpp:328-357)
@@ -199,66 +244,72 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
       }
     }
     __syncthreads();
-    grid.sync();  // every CTA holds the old columns r, piv
     const double beta = s_beta;
-    // apply (I - beta v v^T), v = [1; tail], to owned columns c > r and do the swap
+    // apply (I - beta v v^T), v = [1; tail], to owned columns c >= r with the swap
     auto slow_column = [&](int64_t c) {
       double* col = p.W + c * p.ld;
       if (c == r) {
         for (int i = lane; i < m; i += 32) col[i] = (i < r) ? colP[i] : (i == r ? s_result : 0.0);
         if (lane == 0) {
           p.perm[r] = s_perm_piv;
-          p.norms2[r] = s_oldn2_piv;
-          p.norms0[r] = s_oldn0_piv;
+          p.norms2[r] = s_best;
+          p.norms0[r] = s_n0p;
         }
         return;
       }
-      const bool is_piv = (c == piv);
-      const double* src = is_piv ? colR : col;  // slot piv receives the old column r
+      // c == piv: slot piv receives the old column r
       double dot = 0.0;
-      for (int i = r + 1 + lane; i < m; i += 32) dot = fma(tail[i], src[i], dot);
-      dot = warp_sum(dot) + src[r];
+      for (int i = r + 1 + lane; i < m; i += 32) dot = fma(tail[i], colR[i], dot);
+      dot = warp_sum(dot) + colR[r];
       const double bd = beta * dot;
-      if (is_piv) {
-        for (int i = lane; i < m; i += 32) {
-          double v = colR[i];
+      for (int i = lane; i < m; i += 32) {
+        double v = colR[i];
+        if (beta != 0.0) {
           if (i == r) v -= bd;
           else if (i > r) v -= bd * tail[i];
-          col[i] = v;
         }
-      } else if (beta != 0.0) {
-        for (int i = r + lane; i < m; i += 32) col[i] = (i == r) ? col[i] - bd : col[i] - bd * tail[i];
+        col[i] = v;
       }
       __syncwarp();
       if (lane == 0) {
         const double wr = col[r];
-        const double n2 = is_piv ? s_oldn2_r : p.norms2[c];
-        if (is_piv) {
-          p.perm[c] = s_perm_r;
-          p.norms0[c] = s_oldn0_r;
-        }
-        p.norms2[c] = n2 - wr * wr;  // down-date (dense.cpp:531-533)
+        p.perm[c] = s_perm_r;
+        p.norms0[c] = s_n0r;
+        p.norms2[c] = s_n2r - wr * wr;  // down-date (dense.cpp:531-533)
       }
     };
-    // Ordinary columns: two per warp, rows cached in registers (one L2 round
-    // trip per column), reflector applied in place, norm down-dated by the
-    // lane that owns row r.
-    constexpr int S = kMaxRows / 32;
     const int sr = r >> 5, lr = r & 31;
     const int64_t cstart = lmax(c0, r);
     for (int64_t cb = cstart + 2 * warp; cb < c1; cb += 2 * nwarps) {
       const int64_t ca = cb, cc2 = cb + 1;
       const bool two = cc2 < c1;
       if (ca == r || ca == piv || (two && (cc2 == r || cc2 == piv))) {
-        slow_column(ca);
-        if (two) slow_column(cc2);
+        for (int t2 = 0; t2 < (two ? 2 : 1); ++t2) {
+          const int64_t c = ca + t2;
+          if (c == r || c == piv) {
+            slow_column(c);
+            continue;
+          }
+          double* col = p.W + c * p.ld;  // ordinary column next to a special one
+          double dot = 0.0;
+          for (int i = r + 1 + lane; i < m; i += 32) dot = fma(tail[i], col[i], dot);
+          dot = warp_sum(dot) + col[r];
+          const double bd = beta * dot;
+          if (beta != 0.0)
+            for (int i = r + lane; i < m; i += 32) col[i] = (i == r) ? col[i] - bd : col[i] - bd * tail[i];
+          __syncwarp();
+          if (lane == 0) {
+            const double wr = col[r];
+            p.norms2[c] -= wr * wr;
+          }
+        }
         continue;
       }
       double* pa = p.W + ca * p.ld;
       double* pb = p.W + (two ? cc2 : ca) * p.ld;
-      double xa[S], xb[S];
+      double xa[SMAX], xb[SMAX];
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
+      for (int s = 0; s < SMAX; ++s) {
         const int i = lane + 32 * s;
         const bool in = i >= r && i < m;
         xa[s] = in ? pa[i] : 0.0;
@@ -266,7 +317,7 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
       }
       double da = 0.0, db = 0.0, ra = 0.0, rb = 0.0;
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
+      for (int s = 0; s < SMAX; ++s) {
         const int i = lane + 32 * s;
         if (i > r && i < m) {
           const double t = tail[i];
@@ -283,7 +334,7 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
       const double bda = beta * da, bdb = beta * db;
       double wa = 0.0, wb = 0.0;
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
+      for (int s = 0; s < SMAX; ++s) {
         const int i = lane + 32 * s;
         if (i < r || i >= m) continue;
         double va = xa[s], vb = xb[s];
@@ -305,6 +356,8 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
       }
     }
     __syncthreads();
+    if (r + 1 < rmax) publish(r + 1, buf ^ 1);
+    grid.sync();
   }
   if (b == 0 && tid == 0) p.stopped[0] = r;
 }
@@ -356,13 +409,16 @@ __global__ void assemble_z_kernel(const int64_t* __restrict__ perm, int ke, int6
 
 }  // namespace
 
-size_t cpqr_work_bytes(int64_t n, int grid) {
-  return sizeof(double) * 2 * n + sizeof(int64_t) * n + sizeof(double) * grid + sizeof(int64_t) * grid + 64;
+size_t cpqr_work_bytes(int64_t n, int grid, int m) {
+  return sizeof(double) * 2 * n + sizeof(int64_t) * n +
+         2 * static_cast<size_t>(grid) * (sizeof(double) * 2 + sizeof(int64_t) * 2) +
+         sizeof(double) * (2 * static_cast<size_t>(grid) * m + 2 * (m + 4)) + 256;
 }
 
 cudaError_t cpqr_rank(double* W, int64_t ld, int m, int64_t n, int kmax, double halt, int64_t* perm, void* work,
                       int* stopped, int* recomputes, int num_sms, cudaStream_t st) {
   if (m > kMaxRows) return cudaErrorInvalidValue;
+  const int G = num_sms;
   CpqrParams prm{};
   prm.W = W;
   prm.ld = ld;
@@ -370,17 +426,25 @@ cudaError_t cpqr_rank(double* W, int64_t ld, int m, int64_t n, int kmax, double 
   prm.n = n;
   prm.kmax = kmax;
   prm.halt = halt;
-  char* w = static_cast<char*>(work);
-  prm.norms2 = reinterpret_cast<double*>(w);
+  double* w = static_cast<double*>(work);
+  prm.norms2 = w;
   prm.norms0 = prm.norms2 + n;
   prm.part_val = prm.norms0 + n;
-  prm.part_idx = reinterpret_cast<int64_t*>(prm.part_val + num_sms);
+  prm.part_n0 = prm.part_val + 2 * G;
+  prm.stage_col = prm.part_n0 + 2 * G;
+  prm.stage_r = prm.stage_col + 2 * static_cast<int64_t>(G) * m;
+  prm.part_idx = reinterpret_cast<int64_t*>(prm.stage_r + 2 * (m + 4));
+  prm.part_perm = prm.part_idx + 2 * G;
   prm.perm = perm;
   prm.stopped = stopped;
   prm.recomputes = recomputes;
   void* args[] = {&prm};
-  cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cpqr_kernel), dim3(num_sms),
-                                              dim3(kCpqrThreads), args, 0, st);
+  void* fn;
+  if (m <= 128) fn = reinterpret_cast<void*>(cpqr_kernel<4>);
+  else if (m <= 256) fn = reinterpret_cast<void*>(cpqr_kernel<8>);
+  else if (m <= 384) fn = reinterpret_cast<void*>(cpqr_kernel<12>);
+  else fn = reinterpret_cast<void*>(cpqr_kernel<16>);
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kCpqrThreads), args, 0, st);
   count_launch();
   return e;
 }

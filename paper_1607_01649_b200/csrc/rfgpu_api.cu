@@ -714,7 +714,7 @@ Status col_id_dev(rfgpu_ctx* c, const double* Y, int64_t m, int64_t n, int64_t l
   DBuf W, perm, work, part, scal, R11i, T;
   RF_TRY(W.alloc(sizeof(double) * ldw * std::max<int64_t>(1, n), st));
   RF_TRY(perm.alloc(sizeof(int64_t) * std::max<int64_t>(1, n), st));
-  RF_TRY(work.alloc(cpqr_work_bytes(n, c->num_sms), st));
+  RF_TRY(work.alloc(cpqr_work_bytes(n, c->num_sms, static_cast<int>(m)), st));
   RF_TRY(part.alloc(sizeof(double) * 1024, st));
   RF_TRY(scal.alloc(64, st));
   if (n > 0 && m > 0)

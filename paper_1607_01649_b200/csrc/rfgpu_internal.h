@@ -77,7 +77,7 @@ cudaError_t gs_orth(const double* X, int64_t m, int64_t c, int64_t ldx, double* 
 // In place on W (m x n, ld, m <= 512): cpqr with CpqrStop::rank(kmax) and the
 // reference pivot / recompute / halt rules; perm (n) device, *stopped (device)
 // = stopped rank, *recomputes (device) counts exact norm recomputes.
-size_t cpqr_work_bytes(int64_t n, int grid);
+size_t cpqr_work_bytes(int64_t n, int grid, int m);
 cudaError_t cpqr_rank(double* W, int64_t ld, int m, int64_t n, int kmax, double halt, int64_t* perm, void* work,
                       int* stopped, int* recomputes, int num_sms, cudaStream_t st);
 cudaError_t trinv_upper(const double* R, int64_t ldr, int k, double* Rinv, cudaStream_t st);
