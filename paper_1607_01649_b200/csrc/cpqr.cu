@@ -26,7 +26,7 @@ namespace rfgpu {
 
 namespace {
 
-constexpr int kCpqrThreads = 512;
+constexpr int kCpqrThreads = 384;
 constexpr int kMaxRows = 512;  // sketch height (k + p) supported by the kernel
 
 struct CpqrParams {
@@ -278,14 +278,26 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
         p.norms2[c] = s_n2r - wr * wr;  // down-date (dense.cpp:531-533)
       }
     };
-    const int sr = r >> 5, lr = r & 31;
+    const int lr = r & 31;
+    // Reflector in registers: t[s] = v_i for row i = lane + 32 s (v_r = 1,
+    // rows above r zero), so the dot and the update are plain FMAs.
+    double t[SMAX];
+#pragma unroll
+    for (int s = 0; s < SMAX; ++s) {
+      const int i = lane + 32 * s;
+      t[s] = (i < r || i >= m) ? 0.0 : (i == r ? 1.0 : tail[i]);
+    }
+    const int sfirst = r >> 5;  // slots entirely above row r are skipped (warp-uniform)
     const int64_t cstart = lmax(c0, r);
-    for (int64_t cb = cstart + 2 * warp; cb < c1; cb += 2 * nwarps) {
-      const int64_t ca = cb, cc2 = cb + 1;
-      const bool two = cc2 < c1;
-      if (ca == r || ca == piv || (two && (cc2 == r || cc2 == piv))) {
-        for (int t2 = 0; t2 < (two ? 2 : 1); ++t2) {
-          const int64_t c = ca + t2;
+    constexpr int NC = SMAX <= 8 ? 4 : (SMAX <= 12 ? 3 : 2);  // columns per warp in flight
+    for (int64_t cb = cstart + NC * warp; cb < c1; cb += NC * nwarps) {
+      bool special = false;
+#pragma unroll
+      for (int u = 0; u < NC; ++u) special |= (cb + u < c1) && (cb + u == r || cb + u == piv);
+      if (special) {
+        for (int u = 0; u < NC; ++u) {
+          const int64_t c = cb + u;
+          if (c >= c1) break;
           if (c == r || c == piv) {
             slow_column(c);
             continue;
@@ -305,54 +317,59 @@ __global__ void __launch_bounds__(kCpqrThreads, 1) cpqr_kernel(const CpqrParams 
         }
         continue;
       }
-      double* pa = p.W + ca * p.ld;
-      double* pb = p.W + (two ? cc2 : ca) * p.ld;
-      double xa[SMAX], xb[SMAX];
+      double x[NC][SMAX];
+      double* pc[NC];
+      bool live[NC];
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        live[u] = cb + u < c1;
+        pc[u] = p.W + (live[u] ? cb + u : cb) * p.ld;
+      }
 #pragma unroll
       for (int s = 0; s < SMAX; ++s) {
         const int i = lane + 32 * s;
-        const bool in = i >= r && i < m;
-        xa[s] = in ? pa[i] : 0.0;
-        xb[s] = in ? pb[i] : 0.0;
+        const bool in = s >= sfirst && i >= r && i < m;
+#pragma unroll
+        for (int u = 0; u < NC; ++u) x[u][s] = in ? pc[u][i] : 0.0;
       }
-      double da = 0.0, db = 0.0, ra = 0.0, rb = 0.0;
+      double d[NC], xr[NC], n2[NC];
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        d[u] = 0.0;
+        xr[u] = 0.0;
+        n2[u] = (lane == lr && live[u]) ? p.norms2[cb + u] : 0.0;  // prefetched with the column loads
+      }
 #pragma unroll
       for (int s = 0; s < SMAX; ++s) {
-        const int i = lane + 32 * s;
-        if (i > r && i < m) {
-          const double t = tail[i];
-          da = fma(t, xa[s], da);
-          db = fma(t, xb[s], db);
-        }
-        if (s == sr) {
-          ra = xa[s];
-          rb = xb[s];
-        }
-      }
-      da = warp_sum(da) + __shfl_sync(0xffffffffu, ra, lr);
-      db = warp_sum(db) + __shfl_sync(0xffffffffu, rb, lr);
-      const double bda = beta * da, bdb = beta * db;
-      double wa = 0.0, wb = 0.0;
+        if (s < sfirst) continue;
 #pragma unroll
-      for (int s = 0; s < SMAX; ++s) {
-        const int i = lane + 32 * s;
-        if (i < r || i >= m) continue;
-        double va = xa[s], vb = xb[s];
-        if (beta != 0.0) {
-          const double t = (i == r) ? 1.0 : tail[i];
-          va = (i == r) ? va - bda : va - bda * t;
-          vb = (i == r) ? vb - bdb : vb - bdb * t;
-          pa[i] = va;
-          if (two) pb[i] = vb;
-        }
-        if (i == r) {
-          wa = va;
-          wb = vb;
+        for (int u = 0; u < NC; ++u) d[u] = fma(t[s], x[u][s], d[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < NC; ++u) d[u] = warp_sum(d[u]) * beta;
+      if (beta != 0.0) {
+#pragma unroll
+        for (int s = 0; s < SMAX; ++s) {
+          if (s < sfirst) continue;
+          const int i = lane + 32 * s;
+          const bool in = i >= r && i < m;
+#pragma unroll
+          for (int u = 0; u < NC; ++u) {
+            x[u][s] = fma(-d[u], t[s], x[u][s]);
+            if (in && live[u]) pc[u][i] = x[u][s];
+          }
         }
       }
+      // down-date with the new row-r entries (owned by lane r & 31, slot r >> 5)
+#pragma unroll
+      for (int s = 0; s < SMAX; ++s)
+        if (s == sfirst)
+#pragma unroll
+          for (int u = 0; u < NC; ++u) xr[u] = x[u][s];
       if (lane == lr) {
-        p.norms2[ca] -= wa * wa;
-        if (two) p.norms2[cc2] -= wb * wb;
+#pragma unroll
+        for (int u = 0; u < NC; ++u)
+          if (live[u]) p.norms2[cb + u] = n2[u] - xr[u] * xr[u];
       }
     }
     __syncthreads();
