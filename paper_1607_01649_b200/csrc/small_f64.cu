@@ -104,34 +104,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   for (int j = warp; j < c; j += nwarps)
     for (int i = lane; i < c; i += 32) R[static_cast<int64_t>(j) * c + i] = i <= j ? P[pk(i, j)] : 0.0;
 
-  // Phase 2: column j of R^{-1}: x = e_j; for i = j..0: x_i /= R(i,i);
-  // x[0:i) -= x_i R(0:i, i).
-  for (int j = warp; j < c; j += nwarps) {
-    double x[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) x[s] = (lane + 32 * s == j) ? 1.0 : 0.0;
-    for (int i = j; i >= 0; --i) {
-      const int si = i >> 5, owner = i & 31;
-      double v = 0.0;
-#pragma unroll
-      for (int s = 0; s < S; ++s)
-        if (s == si) v = x[s];
-      const double xi = __shfl_sync(0xffffffffu, v, owner) * rdiag[i];
-      const double* pc = P + pk(0, i);
-#pragma unroll
-      for (int s = 0; s < S; ++s) {
-        const int r = lane + 32 * s;
-        if (r == i) x[s] = xi;
-        else if (r < i) x[s] = fma(-xi, pc[r], x[s]);
-      }
-    }
-    double* out = Rinv + static_cast<int64_t>(j) * c;
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int r = lane + 32 * s;
-      if (r < c) out[r] = r <= j ? x[s] : 0.0;
-    }
-  }
+  // R^{-1} is formed by trinv_upper (many CTAs, one warp per column).
+  (void)Rinv;
 }
 
 // ----------------------------------------------------------- jacobi_svd ---
@@ -486,7 +460,9 @@ cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double
     chol_inv_kernel<false, 11><<<1, kSmallThreads, 0, st>>>(G, ci, R, Rinv, work, info, info_d);
     count_launch();
   }
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return trinv_upper(R, c, ci, Rinv, st);
 }
 
 size_t jacobi_work_bytes(int64_t mr, int64_t c) {
