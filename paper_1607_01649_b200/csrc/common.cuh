@@ -143,3 +143,17 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t 
                : "memory");
 }
 }  // namespace rfgpu
+
+namespace rfgpu {
+// Bulk copy (TMA engine) from this CTA's shared memory into a cluster CTA's
+// shared memory; completion counted as transaction bytes on that CTA's
+// mbarrier. Addresses from mapa_u32; bytes % 16 == 0.
+__device__ __forceinline__ void bulk_s2s_cluster(uint32_t dst, const void* src, uint32_t bytes, uint32_t rbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   dst),
+               "r"(smem_u32(src)), "r"(bytes), "r"(rbar)
+               : "memory");
+}
+// Make this thread's generic-proxy shared-memory writes visible to the async proxy.
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+}  // namespace rfgpu

@@ -668,24 +668,22 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int num_sms, int force_split
   if (force_splits > 0) {
     best = static_cast<int>(std::min<int64_t>(force_splits, std::max<int64_t>(1, p.ktiles)));
   } else if (units < 12 * num_sms && p.ktiles > 1) {
-    // Smallest split count whose last wave is >= 90% full, keeping >= 4
-    // K-tiles per split; else the best-filling one.
-    double best_eff = -1.0;
+    // Split-K count with the fullest last wave, keeping >= 4 K-tiles per
+    // split (deterministic fixed-order reduction afterwards). Among counts
+    // within 1% of the best wave efficiency, the smallest wins.
     const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(p.ktiles / 4, 256));
-    for (int64_t s = 1; s <= max_s; ++s) {
+    auto eff_of = [&](int64_t s) {
       const int64_t work = units * s;
       const int64_t waves = (work + num_sms - 1) / num_sms;
-      const double eff = static_cast<double>(work) / static_cast<double>(waves * num_sms);
-      if (eff >= 0.9) {
+      return static_cast<double>(work) / static_cast<double>(waves * num_sms) - 0.002 * (waves - 1);
+    };
+    double best_eff = -1.0;
+    for (int64_t s = 1; s <= max_s; ++s) best_eff = std::max(best_eff, eff_of(s));
+    for (int64_t s = 1; s <= max_s; ++s)
+      if (eff_of(s) >= best_eff - 0.01) {
         best = static_cast<int>(s);
-        best_eff = eff;
         break;
       }
-      if (eff > best_eff + 1e-9) {
-        best_eff = eff;
-        best = static_cast<int>(s);
-      }
-    }
   }
   p.splits = best;
   return p;

@@ -698,6 +698,9 @@ Status svd_tall_dev(rfgpu_ctx* c, const double* M, int64_t rows, int64_t cols, i
   }
   RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));
+  if (std::getenv("RFGPU_DEBUG"))
+    std::fprintf(stderr, "[rfgpu] svd_tall %lldx%lld fast=%d jacobi info=%d sweeps=%d\n", (long long)rows,
+                 (long long)cols, (int)b.fast, c->h_info[0], c->h_info[1]);
   if (c->h_info[0] == 1) return make_err(RFGPU_ECONVERGENCE, "svd_dense: Jacobi sweeps did not converge");
   return {};
 }

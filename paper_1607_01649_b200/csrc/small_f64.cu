@@ -15,6 +15,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "rfgpu_internal.h"
@@ -128,8 +130,11 @@ struct JacobiParams {
   double* V;
   double* gX;  // global staging when X/V rows do not fit in shared memory
   double* gV;
+  double* gS;  // per-CTA staging for the physical column permutation of each sweep
   int RX, RV;  // rows of X / V owned per CTA
   int LDX, LDV;
+  int bcast;  // 1: every CTA receives every partial (one hop); 0: owner CTA per pair (two hops, less smem)
+  long long* trace;  // optional: clock64 at the phase boundaries of sweep 0 (CTA 0, thread 0)
   int* info;
   int* sweeps_out;
 };
@@ -174,8 +179,17 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
   const int rhx = (nrx + H - 1) / H, rhv = (nrv + H - 1) / H;
   const int x0 = min(nrx, h * rhx), x1 = min(nrx, x0 + rhx);
   const int v0 = min(nrv, h * rhv), v1 = min(nrv, v0 + rhv);
-  const int npo = (npairs + P - 1) / P;            // pairs per owner CTA
-  const int owned = (npairs - q + P - 1) / P;      // pairs owned by this CTA (k % P == q)
+  const bool bc = p.bcast != 0 || P == 1;
+  // Exchange layout. Partials are staged per destination in `outb` and shipped
+  // with ONE bulk shared->shared copy per destination CTA per round (TMA
+  // engine, transaction bytes on the receiver's mbarrier).
+  //   bc (one hop): every CTA receives every pair's partial; params computed
+  //                 locally.  block = npairs partials.
+  //   owner:        pair k's partials go to CTA k % P (block = its owned pairs),
+  //                 which broadcasts (cs, sn) back as one bulk copy.
+  const int npo = bc ? npairs : (npairs + P - 1) / P;  // pairs per destination block
+  const int blk3 = (npo * 3 + 1) & ~1;                 // doubles per partial block (16B multiple)
+  auto owned_by = [&](int d) { return bc ? npairs : (npairs - d + P - 1) / P; };
 
   extern __shared__ double sm[];
   double* Xs;
@@ -192,9 +206,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
   }
   const int np3 = npairs * 3;
   uint64_t* bars = reinterpret_cast<uint64_t*>(rest);  // [0..1] partial inbox, [2..3] params
-  double* params = rest + 4;                           // [2][npairs][2] (cs, sn; sn = 2 => skip)
-  double* inbox = params + 4 * npairs;                 // [2][P][npo][3]
-  double* red = inbox + 2 * P * npo * 3;               // [H][npairs][3], aliased by nrmp [P][cc]
+  double* params = rest + 4;                           // [2][P][npo][2] by owner (bc: [2][npairs][2])
+  // staging buffers are double-buffered by round parity: a bulk copy of
+  // round r is known to have landed everywhere only after round r+1's waits
+  double* pout = params + 4 * P * npo;                 // [2][npo][2] this owner's params (owner mode)
+  double* outb = pout + 4 * npo;                       // [2][P][blk3] staged partials per destination
+  double* inbox = outb + 2 * P * blk3;                 // [2][P][blk3]
+  double* red = inbox + 2 * P * blk3;                  // [H][npairs][3], aliased by nrmp [P][cc]
   const int red_sz = max(H * np3, P * cc);
   double* nrmp = red;
   double* nrm = red + red_sz;                          // [cc]
@@ -205,7 +223,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
     for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
     mbar_fence_init();
   }
-  uint32_t uses[2] = {0u, 0u};
+  uint32_t uses0 = 0u, uses1 = 0u;
   for (int e = tid; e < c * RX; e += blockDim.x) {
     const int col = e / RX, r = e % RX;
     Xs[static_cast<size_t>(col) * LDX + r] = (r < nrx) ? p.X[static_cast<int64_t>(col) * p.mr + r0x + r] : 0.0;
@@ -214,7 +232,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
     const int col = e / RV, r = e % RV;
     Vs[static_cast<size_t>(col) * LDV + r] = (r < nrv && r0v + r == col) ? 1.0 : 0.0;
   }
-  cluster.sync();  // barriers initialised cluster-wide before any st.async
+  cluster.sync();  // barriers initialised cluster-wide before any remote copy
 
   // Column norms over the owned rows, exchanged across the cluster; nrm[j]
   // receives the total in fixed rank order.
@@ -247,28 +265,70 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
     if (tid == 0 && (c & 1)) perm[c] = -1;  // phantom column
     __syncthreads();
   };
+  // Physically reorder the columns of X and V by perm (through global
+  // staging), so that a round's pairs are consecutive columns: lanes then hit
+  // distinct shared-memory banks (odd leading dimensions).
+  auto permute_cols = [&]() {
+    double* sx = p.gS + static_cast<size_t>(q) * c * (LDX + LDV);
+    double* sv = sx + static_cast<size_t>(c) * LDX;
+    for (int e = tid; e < c * LDX; e += blockDim.x) sx[e] = Xs[e];
+    for (int e = tid; e < c * LDV; e += blockDim.x) sv[e] = Vs[e];
+    __syncthreads();
+    for (int e = tid; e < c * nrx; e += blockDim.x) {
+      const int col = e / nrx, r = e - col * nrx;
+      Xs[static_cast<size_t>(col) * LDX + r] = sx[static_cast<size_t>(perm[col]) * LDX + r];
+    }
+    for (int e = tid; e < c * nrv; e += blockDim.x) {
+      const int col = e / nrv, r = e - col * nrv;
+      Vs[static_cast<size_t>(col) * LDV + r] = sv[static_cast<size_t>(perm[col]) * LDV + r];
+    }
+    __syncthreads();
+  };
 
+  const int kd = bc ? 0 : k % P;   // destination block of pair k
+  const int kl = bc ? k : k / P;   // slot of pair k inside its block
   int sweep = 0, parity = 0;
+#ifdef RFGPU_JACOBI_TRACE
+  long long tacc[14] = {0}, tlast = 0;  // per-slot clocks of sweep 0, CTA 0, thread 0
+#endif
   if (tid == 0) s_conv = (c <= 1);
   __syncthreads();
   while (!s_conv && sweep < 60) {
     norms();
     sort_desc(nrm);
+    permute_cols();
     if (tid == 0) s_rotated = 0;
     __syncthreads();
+#ifdef RFGPU_JACOBI_TRACE
+    const bool tracing = p.trace && sweep == 0 && q == 0 && tid == 0;
+#define RF_TRACE(slot)                                                     \
+  if (tracing) {                                                           \
+    const long long now = clock64();                                       \
+    if (rd >= 1 && rd < 31 && (slot) > 0) tacc[(slot)] += now - tlast;     \
+    if ((slot) == 0 && rd >= 2 && rd < 32) tacc[0] += now - tlast;         \
+    tlast = now;                                                           \
+  }
+#else
+#define RF_TRACE(slot)
+#endif
     for (int rd = 0; rd < cc - 1; ++rd) {
+      RF_TRACE(0)
       int cp = -1, cq = -1;
       if (active && k < npairs) {
         int a, b;
         pair_of(rd, k, cc, &a, &b);
-        cp = perm[a];
-        cq = perm[b];
+        cp = a < c ? a : -1;
+        cq = b < c ? b : -1;
       }
       const bool valid = cp >= 0 && cq >= 0;
-      if (P > 1 && tid == 0) {
-        mbar_arrive_expect_tx(&bars[parity], static_cast<uint32_t>(P * owned * 24));
-        mbar_arrive_expect_tx(&bars[2 + parity], static_cast<uint32_t>(npairs * 16));
+      const uint32_t ph = (parity ? uses1 : uses0) & 1u;
+      if (P > 1 && tid == blockDim.x - 32) {  // a lane off the reduction warps' critical path
+        uint32_t bytes = 0;  // partial blocks from every CTA
+        for (int d = 0; d < P; ++d) bytes += static_cast<uint32_t>(((owned_by(q) * 3 + 1) & ~1) * 8);
+        mbar_arrive_expect_tx(&bars[parity], bytes);
+        if (!bc) mbar_arrive_expect_tx(&bars[2 + parity], static_cast<uint32_t>(npairs * 16));
       }
+      RF_TRACE(1)
       // A. partial inner products over this warp's rows
       if (active && k < npairs) {
         double app = 0.0, aqq = 0.0, apq = 0.0;
@@ -282,43 +342,50 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
             apq = fma(u, v, apq);
           }
         }
+        RF_TRACE(2)
         double* d = red + (h * npairs + k) * 3;
         d[0] = app;
         d[1] = aqq;
         d[2] = apq;
       }
+      RF_TRACE(3)
       __syncthreads();
-      // B. CTA partial -> the pair's owner CTA (k mod P)
-      double* ib = inbox + parity * P * npo * 3;
-      double* pr = params + parity * npairs * 2;
+      RF_TRACE(4)
+      // B. CTA partial (fixed row-group order), staged per destination block
+      double* ib = inbox + parity * P * blk3;
+      double* pr = params + parity * 2 * P * npo;
       if (h == 0 && k < npairs) {
         double app = 0.0, aqq = 0.0, apq = 0.0;
+#pragma unroll 4
         for (int hh = 0; hh < H; ++hh) {
           const double* s = red + (hh * npairs + k) * 3;
           app += s[0];
           aqq += s[1];
           apq += s[2];
         }
-        double* slot = ib + (q * npo + k / P) * 3;
-        if (P > 1) {
-          const uint32_t o = static_cast<uint32_t>(k % P);
-          const uint32_t ra = mapa_u32(smem_u32(slot), o), rb = mapa_u32(smem_u32(&bars[parity]), o);
-          st_async_f64(ra, app, rb);
-          st_async_f64(ra + 8, aqq, rb);
-          st_async_f64(ra + 16, apq, rb);
-        } else {
-          slot[0] = app;
-          slot[1] = aqq;
-          slot[2] = apq;
-        }
+        double* slot = (P > 1 ? outb + (parity * P + kd) * blk3 : ib) + kl * 3;
+        slot[0] = app;
+        slot[1] = aqq;
+        slot[2] = apq;
+        if (P > 1) fence_proxy_async_smem();
       }
-      if (P == 1) __syncthreads();
-      else if (h == 0) mbar_wait(&bars[parity], uses[parity] & 1u);
-      // C. owners: rotation parameters (reference formula), broadcast to all
-      if (h == 0 && k < npairs && k % P == q) {
+      RF_TRACE(5)
+      __syncthreads();
+      RF_TRACE(6)
+      if (P > 1 && tid < P) {  // lane d ships block d to CTA d (bc: the same full block to all)
+        const int dd = tid;
+        const double* src = outb + (parity * P + (bc ? 0 : dd)) * blk3;
+        const uint32_t bytes = static_cast<uint32_t>(((owned_by(dd) * 3 + 1) & ~1) * 8);
+        bulk_s2s_cluster(mapa_u32(smem_u32(ib + q * blk3), dd), src, bytes, mapa_u32(smem_u32(&bars[parity]), dd));
+      }
+      RF_TRACE(7)
+      if (P > 1 && h == 0) mbar_wait(&bars[parity], ph);
+      RF_TRACE(8)
+      // C. rotation parameters (reference formula, dense.cpp:624-644)
+      if (h == 0 && k < npairs && (bc || kd == q)) {
         double app = 0.0, aqq = 0.0, apq = 0.0;
         for (int d = 0; d < P; ++d) {
-          const double* s = ib + (d * npo + k / P) * 3;
+          const double* s = ib + d * blk3 + kl * 3;
           app += s[0];
           aqq += s[1];
           apq += s[2];
@@ -327,23 +394,32 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
         if (valid && app != 0.0 && aqq != 0.0 && !(fabs(apq) <= 1e-15 * sqrt(app * aqq))) {
           const double zeta = (aqq - app) / (2.0 * apq);
           const double t = (zeta < 0.0 ? -1.0 : 1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          cs = 1.0 / sqrt(1.0 + t * t);
+          cs = rsqrt(1.0 + t * t);
           sn = cs * t;
         }
-        if (P > 1) {
-          const uint32_t la = smem_u32(pr + 2 * k), lb = smem_u32(&bars[2 + parity]);
-          for (int d = 0; d < P; ++d) st_async_v2(mapa_u32(la, d), cs, sn, mapa_u32(lb, d));
-        } else {
-          pr[2 * k] = cs;
-          pr[2 * k + 1] = sn;
-        }
+        double* dst = bc ? pr + 2 * k : pout + parity * 2 * npo + 2 * kl;
+        dst[0] = cs;
+        dst[1] = sn;
+        if (!bc) fence_proxy_async_smem();
       }
-      if (P == 1) __syncthreads();
-      else if (active) mbar_wait(&bars[2 + parity], uses[parity] & 1u);
-      uses[parity] += 1u;
+      RF_TRACE(9)
+      __syncthreads();
+      RF_TRACE(10)
+      if (!bc) {
+        if (tid < P) {
+          const uint32_t bytes = static_cast<uint32_t>(owned_by(q) * 16);
+          bulk_s2s_cluster(mapa_u32(smem_u32(pr + q * 2 * npo), tid), pout + parity * 2 * npo, bytes,
+                           mapa_u32(smem_u32(&bars[2 + parity]), tid));
+        }
+        if (active) mbar_wait(&bars[2 + parity], ph);
+      }
+      if (parity) ++uses1;
+      else ++uses0;
+      RF_TRACE(11)
       // D. rotate this warp's rows of X and V
       if (active && k < npairs && valid) {
-        const double cs = pr[2 * k], sn = pr[2 * k + 1];
+        const double* prm = bc ? pr + 2 * k : pr + kd * 2 * npo + 2 * kl;
+        const double cs = prm[0], sn = prm[1];
         if (sn != 2.0) {
           if (h == 0) s_rotated = 1;
           double* xp = Xs + static_cast<size_t>(cp) * LDX;
@@ -362,9 +438,15 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
           }
         }
       }
+      RF_TRACE(12)
       __syncthreads();
+      RF_TRACE(13)
       parity ^= 1;
     }
+#ifdef RFGPU_JACOBI_TRACE
+    if (tracing)
+      for (int i = 0; i < 14; ++i) p.trace[i] = tacc[i];
+#endif
     ++sweep;
     if (tid == 0) s_conv = !s_rotated;
     __syncthreads();
@@ -373,8 +455,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
 
   // final singular values, stable descending order
   norms();
-  double* sig = red + P * cc;  // free after norms(): red_sz >= P*cc, use params-sized scratch instead
-  sig = params;                // 4*npairs >= c doubles
+  double* sig = params;  // 4 * P * npo >= 2 * npairs >= c doubles
   for (int j = tid; j < c; j += blockDim.x) sig[j] = sqrt(nrm[j]);
   __syncthreads();
   sort_desc(sig);
@@ -409,8 +490,9 @@ __global__ void sumsq_partial_kernel(const double* __restrict__ x, int64_t n, do
 }
 
 struct JacobiLayout {
-  int P, RX, RV, LDX, LDV;
+  int P, RX, RV, LDX, LDV, threads;
   bool smem;
+  bool bcast;
   size_t bytes;
 };
 
@@ -418,22 +500,44 @@ inline int pad_ld(int r) { return r + ((r % 2 == 0) ? 1 : 0); }  // odd leading 
 
 JacobiLayout jacobi_layout(int64_t mr, int64_t c) {
   const int64_t cc = c + (c & 1), npairs = cc / 2;
-  const int64_t G = (npairs + 31) / 32, H = 32 / G;
-  auto extra = [&](int P) {
-    const int64_t npo = (npairs + P - 1) / P;
-    return sizeof(double) * (4 + 4 * npairs + 2 * P * npo * 3 + std::max<int64_t>(H * npairs * 3, P * cc) + cc) +
+  const int64_t G = (npairs + 31) / 32;
+  // Row groups per pair: enough warps to keep ~8 rows each. More groups make
+  // the rows/warp loop shorter but the serial per-pair reduction over groups
+  // longer; both sit on every round's critical path.
+  static const int rpw = [] {
+    const char* e = std::getenv("RFGPU_JACOBI_RPW");
+    return e ? std::max(1, std::atoi(e)) : 8;
+  }();
+  auto groups = [&](int64_t rows) { return std::max<int64_t>(1, std::min<int64_t>(32 / G, (rows + rpw - 1) / rpw)); };
+  auto extra = [&](int P, bool bcast) {
+    const int64_t H = groups((mr + P - 1) / P);
+    const int64_t npo = bcast ? npairs : (npairs + P - 1) / P;
+    const int64_t blk3 = (npo * 3 + 1) & ~int64_t(1);
+    return sizeof(double) * (4 + 4 * P * npo + 4 * npo + 4 * P * blk3 + std::max<int64_t>(H * npairs * 3, P * cc) +
+                             cc) +
            sizeof(int) * cc + 64;
   };
   constexpr size_t kMax = 224 * 1024;
-  for (int P : {1, 2, 4, 8, 16}) {
-    const int RX = static_cast<int>((mr + P - 1) / P), RV = static_cast<int>((c + P - 1) / P);
-    const int LDX = pad_ld(RX), LDV = pad_ld(RV);
-    const size_t b = sizeof(double) * static_cast<size_t>(c) * (LDX + LDV) + extra(P);
-    if (b <= kMax) return {P, RX, RV, LDX, LDV, true, b};
+  // Smallest cluster that leaves at most `target` rows of X per CTA: the
+  // per-round shared-memory traffic of a CTA is proportional to its rows.
+  static const int target = [] {
+    const char* e = std::getenv("RFGPU_JACOBI_ROWS");
+    return e ? std::max(1, std::atoi(e)) : 16;
+  }();
+  int P0 = 1;
+  while (P0 < 16 && (mr + P0 - 1) / P0 > target) P0 *= 2;
+  for (bool bcast : {true, false}) {
+    for (int P : {1, 2, 4, 8, 16}) {
+      if (P < P0) continue;
+      const int RX = static_cast<int>((mr + P - 1) / P), RV = static_cast<int>((c + P - 1) / P);
+      const int LDX = pad_ld(RX), LDV = pad_ld(RV);
+      const size_t b = sizeof(double) * static_cast<size_t>(c) * (LDX + LDV) + extra(P, bcast);
+      if (b <= kMax) return {P, RX, RV, LDX, LDV, static_cast<int>(32 * G * groups(RX)), true, bcast, b};
+    }
   }
   const int P = 8;
   const int RX = static_cast<int>((mr + P - 1) / P), RV = static_cast<int>((c + P - 1) / P);
-  return {P, RX, RV, pad_ld(RX), pad_ld(RV), false, extra(P)};
+  return {P, RX, RV, pad_ld(RX), pad_ld(RV), static_cast<int>(32 * G * groups(RX)), false, false, extra(P, false)};
 }
 
 }  // namespace
@@ -467,8 +571,8 @@ cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double
 
 size_t jacobi_work_bytes(int64_t mr, int64_t c) {
   const JacobiLayout L = jacobi_layout(mr, c);
-  if (L.smem) return 0;
-  return sizeof(double) * static_cast<size_t>(L.P) * c * (L.LDX + L.LDV);
+  const size_t stage = sizeof(double) * static_cast<size_t>(L.P) * c * (L.LDX + L.LDV);
+  return L.smem ? stage : 2 * stage;
 }
 
 cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double* S, double* V, double* work,
@@ -486,15 +590,23 @@ cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double
   p.RV = L.RV;
   p.LDX = L.LDX;
   p.LDV = L.LDV;
+  p.bcast = L.bcast ? 1 : 0;
   p.info = info;
   p.sweeps_out = sweeps_out;
+#ifdef RFGPU_JACOBI_TRACE
+  static long long* trace_buf = nullptr;
+  if (!trace_buf) cudaMalloc(&trace_buf, sizeof(long long) * 16);
+  p.trace = trace_buf;
+#endif
+  const size_t stage = static_cast<size_t>(L.P) * c * (L.LDX + L.LDV);
+  p.gS = work;
   if (!L.smem) {
-    p.gX = work;
-    p.gV = work + static_cast<size_t>(L.P) * c * L.LDX;
+    p.gX = work + stage;
+    p.gV = p.gX + static_cast<size_t>(L.P) * c * L.LDX;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(L.P);
-  cfg.blockDim = dim3(kSmallThreads);
+  cfg.blockDim = dim3(L.threads);
   cfg.dynamicSmemBytes = L.bytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -529,6 +641,17 @@ cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double
     count_launch();
   }
   if (e != cudaSuccess) return e;
+#ifdef RFGPU_JACOBI_TRACE
+  {
+    long long h[14];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "[rfgpu] jacobi c=%lld P=%d bcast=%d slots (clk/round):", static_cast<long long>(c), L.P,
+                 static_cast<int>(L.bcast));
+    for (int k = 1; k < 14; ++k) std::fprintf(stderr, " %d:%.0f", k, static_cast<double>(h[k]) / 30);
+    std::fprintf(stderr, " next:%.0f\n", static_cast<double>(h[0]) / 30);
+  }
+#endif
   return cudaGetLastError();
 }
 
