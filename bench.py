@@ -14,8 +14,10 @@ no flush is needed between steps.
 
 `value` = device-resident time per rsvd call (A, G already in HBM; CUDA
 events on the library's stream; max over ranks). `e2e` = the same call made
-through the public C ABI with HOST buffers: upload of A from pinned memory,
-rfgpu_rsvd, and the D2H of U, D, V, all inside the timed region.
+through the public C ABI with HOST buffers (rfgpu_rsvd_host, the call the
+drop-in rsvd(const DenseMatrix&) makes): A streamed from pinned memory in row
+panels overlapped with the first pass, and the D2H of U, D, V, all inside the
+timed region.
 
 --impl reference runs the reference's own CPU implementation (oracle/_ref,
 compiled from /root/reference/proj/src) on a bounded row sample of the same
@@ -367,15 +369,11 @@ def main():
             gflat = np.asfortranarray(Gh).reshape(-1, order="F")
 
             def e2e_step():
-                h = C.c_void_p()
-                rf._check(L.rfgpu_matrix_upload(ctx.handle, C.cast(C.c_void_p(Ah.data_ptr()), rf._pd), mloc, n, mloc,
-                                                 C.byref(h)))
-                try:
-                    rf._check(L.rfgpu_rsvd(ctx.handle, h, rf._dp(gflat), k, ell, q, 0, 1,
-                                           C.cast(C.c_void_p(Uh.data_ptr()), rf._pd), rf._dp(Dh),
-                                           C.cast(C.c_void_p(Vh.data_ptr()), rf._pd), C.byref(rank_out)))
-                finally:
-                    L.rfgpu_matrix_free(h)
+                # the drop-in call: host A in (streamed behind pass 1), host U, D, V out
+                rf._check(L.rfgpu_rsvd_host(ctx.handle, C.cast(C.c_void_p(Ah.data_ptr()), rf._pd), mloc, n, mloc,
+                                            rf._dp(gflat), k, ell, q, 0, 1,
+                                            C.cast(C.c_void_p(Uh.data_ptr()), rf._pd), rf._dp(Dh),
+                                            C.cast(C.c_void_p(Vh.data_ptr()), rf._pd), C.byref(rank_out)))
 
             e2e_step()
             barrier()

@@ -123,6 +123,16 @@ int rfgpu_range_finder(rfgpu_ctx* ctx, const rfgpu_matrix* a, const double* g, i
 int rfgpu_rsvd(rfgpu_ctx* ctx, const rfgpu_matrix* a, const double* g, int64_t k, int64_t ell, int64_t q,
                int keep_oversamples, int reorth, double* U, double* D, double* V, int64_t* rank_out);
 
+/* Host-matrix variant: the value-semantics drop-in rsvd(const DenseMatrix& a,
+ * ...) (lowrank.hpp:15-16). A (m_local x n, column-major, leading dim lda) is
+ * read from host memory: it is copied into a device buffer cached on the
+ * context in row panels whose H2D copies overlap the first pass (pinned host
+ * memory gives full copy bandwidth; pageable works, slower). The caller's
+ * buffer is no longer read once the call returns. Outputs as rfgpu_rsvd. */
+int rfgpu_rsvd_host(rfgpu_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda, const double* g, int64_t k,
+                    int64_t ell, int64_t q, int keep_oversamples, int reorth, double* U, double* D, double* V,
+                    int64_t* rank_out);
+
 /* Device-pointer variant (inputs and outputs in device memory; no host
  * copies): the path bench.py times for the device-resident metric. */
 int rfgpu_rsvd_device(rfgpu_ctx* ctx, const rfgpu_matrix* a, const double* g_dev, int64_t k, int64_t ell,

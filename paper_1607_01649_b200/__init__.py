@@ -105,6 +105,7 @@ _SIGS = {
     "rfgpu_multiply": (_int, [_vp, _vp, _int, _pd, _i64, _pd]),
     "rfgpu_range_finder": (_int, [_vp, _vp, _pd, _i64, _i64, _int, _pd, _pd, _pd, _pi]),
     "rfgpu_rsvd": (_int, [_vp, _vp, _pd, _i64, _i64, _i64, _int, _int, _pd, _pd, _pd, _pi]),
+    "rfgpu_rsvd_host": (_int, [_vp, _pd, _i64, _i64, _i64, _pd, _i64, _i64, _i64, _int, _int, _pd, _pd, _pd, _pi]),
     "rfgpu_rsvd_device": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _pi]),
     "rfgpu_row_sketch": (_int, [_vp, _vp, _pd, _i64, _pd]),
     "rfgpu_row_sketch_device": (_int, [_vp, _vp, _vp, _i64, _vp]),
@@ -391,6 +392,25 @@ def rsvd(a, k: int, p: int, q: int, seed: int, keep_oversamples: bool = False, r
     """randfact::rsvd(a, k, p, q, seed, keep_oversamples, reorthonormalize)."""
     if q < 0:
         raise ParameterError("power_range: q must be non-negative")
+    if not isinstance(a, DeviceMatrix):
+        # host matrix: one call that streams A in behind the first pass
+        if k < 1 or p < 0:
+            _check_sample(k, p, k + max(p, 0), k + max(p, 0), "power_range")
+        ctx = ctx or default_context()
+        a = _fmat(a)
+        m, n = a.shape
+        ell = k + p
+        g = gaussian(seed, "range.G", n, ell)
+        U = np.zeros(max(1, m * ell))
+        D = np.zeros(ell)
+        V = np.zeros(max(1, n * ell))
+        r = _i64()
+        _check(lib().rfgpu_rsvd_host(ctx.handle, _dp(_flat(a)), m, n, max(1, m), _dp(_flat(g)), k, ell, q,
+                                     int(keep_oversamples), int(reorthonormalize), _dp(U), _dp(D), _dp(V),
+                                     C.byref(r)))
+        rr = r.value
+        return SvdFactors(U[: m * rr].reshape((m, rr), order="F"), D[:rr].copy(),
+                          V[: n * rr].reshape((n, rr), order="F"))
     dm, tmp = _as_device(a, ctx)
     try:
         _check_sample(k, p, dm.m_global, dm.n, "power_range")

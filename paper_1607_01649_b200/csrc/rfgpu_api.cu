@@ -228,6 +228,12 @@ struct rfgpu_ctx {
   std::vector<cudaEvent_t> event_pool;
   std::map<std::string, std::pair<int64_t, double>> prof;
   int64_t launch_base = 0;
+  // host-input calls (rfgpu_rsvd_host): H2D copy stream and a reusable
+  // device buffer for A, so repeated drop-in calls neither re-allocate nor
+  // serialise the upload in front of the first pass
+  cudaStream_t copy_stream = nullptr;
+  void* a_cache = nullptr;
+  size_t a_cache_bytes = 0;
 
   cudaEvent_t get_event() {
     if (!event_pool.empty()) {
@@ -247,6 +253,11 @@ struct rfgpu_matrix {
   void* dev = nullptr;
   bool owned = false;
   int64_t m = 0, n = 0, lda = 0, m_global = 0, row0 = 0;
+  // Host rows not yet on the device (rfgpu_rsvd_host): the first pass of the
+  // range finder uploads them in row panels on ctx->copy_stream and consumes
+  // each panel as soon as it lands. Cleared once the upload is issued.
+  mutable const double* src = nullptr;
+  mutable int64_t src_ld = 0;
 };
 
 namespace {
@@ -359,6 +370,70 @@ Status gemm(rfgpu_ctx* c, bool trans, int64_t M, int64_t N, int64_t K, const dou
 int64_t sumsq_slots(rfgpu_ctx* c, int64_t M, int64_t N, int64_t K) {
   const GemmPlan p = plan_gemm(M, N, K, c->num_sms);
   return static_cast<int64_t>(p.splits) * p.mtiles;
+}
+
+// Row panels for streaming a host A in behind the first pass: large enough to
+// keep every SM busy on a panel's product (>= 32768 rows), few enough that
+// the per-panel launch and event costs vanish; the last panel's product is
+// the only compute not hidden under the copy.
+std::vector<std::pair<int64_t, int64_t>> upload_panels(int64_t m) {
+  int64_t np = m >= (int64_t{1} << 19) ? 16 : (m >= (int64_t{1} << 16) ? 4 : 1);
+  const int64_t step = ((m + np - 1) / np + 255) / 256 * 256;
+  std::vector<std::pair<int64_t, int64_t>> out;
+  for (int64_t r = 0; r < m; r += step) out.emplace_back(r, std::min(m, r + step));
+  if (out.empty()) out.emplace_back(0, 0);
+  return out;
+}
+
+int64_t pass1_slots(rfgpu_ctx* c, const rfgpu_matrix* a, int64_t ell) {
+  if (!a->src) return sumsq_slots(c, a->m, ell, a->n);
+  int64_t s = 0;
+  for (auto& pr : upload_panels(a->m)) s += sumsq_slots(c, pr.second - pr.first, ell, a->n);
+  return s;
+}
+
+// Y = A G with ||A||_F^2 partials fused (pass 1). For a handle whose rows are
+// still on the host, panel i+1's H2D copy runs on the copy stream while panel
+// i's product runs on the compute stream.
+Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, double* Y, int64_t ldy,
+             double* ssq) {
+  const int64_t m = a->m, n = a->n, lda = a->lda;
+  const double* A = static_cast<const double*>(a->dev);
+  if (!a->src) return gemm(c, false, m, ell, n, A, lda, G, n, Y, ldy, ssq, "pass_nn");
+  cudaStream_t st = c->stream, cs = c->copy_stream;
+  const auto panels = upload_panels(m);
+  std::vector<cudaEvent_t> ev(panels.size());
+  for (auto& e : ev) RF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  auto copy = [&](size_t i) -> Status {
+    const int64_t r0 = panels[i].first, rows = panels[i].second - r0;
+    if (rows > 0 && n > 0)
+      RF_CUDA(cudaMemcpy2DAsync(const_cast<double*>(A) + r0, sizeof(double) * lda, a->src + r0,
+                                sizeof(double) * a->src_ld, sizeof(double) * rows, n, cudaMemcpyHostToDevice, cs));
+    RF_CUDA(cudaEventRecord(ev[i], cs));
+    return {};
+  };
+  // the device buffer may still be read by the previous call's tail
+  cudaEvent_t ready;
+  RF_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  RF_CUDA(cudaEventRecord(ready, st));
+  RF_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+  Status s = copy(0);
+  int64_t off = 0;
+  for (size_t i = 0; i < panels.size() && s.ok(); ++i) {
+    if (i + 1 < panels.size()) s = copy(i + 1);
+    if (!s.ok()) break;
+    const int64_t r0 = panels[i].first, rows = panels[i].second - r0;
+    if (cudaStreamWaitEvent(st, ev[i], 0) != cudaSuccess) {
+      s = make_err(RFGPU_ECUDA, "pass 1: stream wait failed");
+      break;
+    }
+    s = gemm(c, false, rows, ell, n, A + r0, lda, G, n, Y + r0, ldy, ssq + off, "pass_nn");
+    off += sumsq_slots(c, rows, ell, n);
+  }
+  a->src = nullptr;  // issued: every later consumer is ordered after the waits above
+  cudaEventDestroy(ready);
+  for (auto& e : ev) cudaEventDestroy(e);  // destruction is deferred until the events complete
+  return s;
 }
 
 // ---- orth ---------------------------------------------------------------------
@@ -530,7 +605,7 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
   RF_TRY(z.alloc(sizeof(double) * n * ell, st));
   RF_TRY(w.alloc(sizeof(double) * n * ell, st));
   RF_TRY(tmp.alloc(sizeof(double) * n * ell, st));
-  const int64_t slots = sumsq_slots(c, m, ell, n);
+  const int64_t slots = pass1_slots(c, a, ell);
   RF_TRY(ssq.alloc(sizeof(double) * std::max<int64_t>(1, slots), st));
   RF_TRY(scal.alloc(sizeof(double) * 4, st));
   RF_CUDA(cudaMemsetAsync(ssq.d(), 0, sizeof(double) * std::max<int64_t>(1, slots), st));
@@ -538,8 +613,8 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
   Basis& Qb = out->basis;
   Qb.Q = Qbuf;
   Qb.ldq = ldq;
-  // pass 1: Y = A G, with ||A||_F^2 fused
-  RF_TRY(gemm(c, false, m, ell, n, A, lda, G, n, y.d(), ldq, ssq.d(), "pass_nn"));
+  // pass 1: Y = A G, with ||A||_F^2 fused (streams a host A in by panels)
+  RF_TRY(pass1(c, a, G, ell, y.d(), ldq, ssq.d()));
   RF_CUDA(sum_array(ssq.d(), slots, scal.d(), st));
   RF_TRY(allreduce(c, scal.d(), 1));
 
@@ -916,6 +991,29 @@ Status ensure_device(rfgpu_ctx* c) {
   return {};
 }
 
+// Global row count and this rank's row offset for a row-sharded A.
+Status global_rows(rfgpu_ctx* c, rfgpu_matrix* h) {
+  h->m_global = h->m;
+  h->row0 = 0;
+  if (c->world <= 1) return {};
+  DBuf b;
+  RF_TRY(b.alloc(sizeof(double) * c->world * 2, c->stream));
+  std::vector<double> v(c->world * 2, 0.0);
+  v[c->rank] = static_cast<double>(h->m);
+  RF_CUDA(cudaMemcpyAsync(b.d(), v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, c->stream));
+  RF_TRY(allreduce(c, b.d(), c->world));
+  RF_CUDA(cudaMemcpyAsync(v.data(), b.d(), sizeof(double) * c->world, cudaMemcpyDeviceToHost, c->stream));
+  RF_CUDA(cudaStreamSynchronize(c->stream));
+  int64_t tot = 0, off = 0;
+  for (int r = 0; r < c->world; ++r) {
+    if (r < c->rank) off += static_cast<int64_t>(v[r]);
+    tot += static_cast<int64_t>(v[r]);
+  }
+  h->m_global = tot;
+  h->row0 = off;
+  return {};
+}
+
 }  // namespace
 
 // ============================================================ C ABI ======
@@ -1015,6 +1113,11 @@ int rfgpu_ctx_destroy(rfgpu_ctx* c) {
   cudaFreeHost(c->h_info);
   cudaFreeHost(c->h_d);
   cudaFreeHost(c->h_i64);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
+  if (c->a_cache) cudaFree(c->a_cache);
   cudaStreamDestroy(c->stream);
   delete c;
   return RFGPU_OK;
@@ -1088,28 +1191,8 @@ static int matrix_make(rfgpu_ctx* c, const void* host, const void* dev, bool f32
       }
     }
   }
-  // global row count / offset across ranks (row-sharded A)
-  h->m_global = m;
-  h->row0 = 0;
-  if (c->world > 1) {
-    DBuf b;
-    Status s = b.alloc(sizeof(double) * c->world * 2, c->stream);
-    if (!s.ok()) return finish(s);
-    std::vector<double> v(c->world * 2, 0.0);
-    v[c->rank] = static_cast<double>(m);
-    cudaMemcpyAsync(b.d(), v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, c->stream);
-    s = allreduce(c, b.d(), c->world);
-    if (!s.ok()) return finish(s);
-    cudaMemcpyAsync(v.data(), b.d(), sizeof(double) * c->world, cudaMemcpyDeviceToHost, c->stream);
-    cudaStreamSynchronize(c->stream);
-    int64_t tot = 0, off = 0;
-    for (int r = 0; r < c->world; ++r) {
-      if (r < c->rank) off += static_cast<int64_t>(v[r]);
-      tot += static_cast<int64_t>(v[r]);
-    }
-    h->m_global = tot;
-    h->row0 = off;
-  }
+  Status s = global_rows(c, h.get());
+  if (!s.ok()) return finish(s);
   *out = h.release();
   return RFGPU_OK;
 }
@@ -1252,6 +1335,68 @@ int rfgpu_rsvd(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t k, 
     RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
     int64_t r = 0;
     RF_TRY(rsvd_core(c, a, gd.d(), k, ell, q, keep_over != 0, reorth != 0, U.d(), ldu, D.d(), V.d(), &r));
+    RF_TRY(copy_out(c, Uh, ldu, U.d(), ldu, m, r));
+    RF_TRY(copy_out(c, Dh, std::max<int64_t>(1, r), D.d(), std::max<int64_t>(1, r), r, 1));
+    RF_TRY(copy_out(c, Vh, n, V.d(), n, n, r));
+    RF_CUDA(cudaStreamSynchronize(st));
+    if (rank_out) *rank_out = r;
+    return {};
+  }();
+  return finish(s);
+}
+
+// rsvd straight from host memory: the value-semantics drop-in call
+// (randfact::rsvd(const DenseMatrix&, ...), lowrank.hpp:15-16). A is copied
+// into a device buffer cached on the context, in row panels that overlap the
+// first pass; U, D, V come back to host buffers.
+int rfgpu_rsvd_host(rfgpu_ctx* c, const double* a, int64_t m, int64_t n, int64_t lda, const double* g, int64_t k,
+                    int64_t ell, int64_t q, int keep_over, int reorth, double* Uh, double* Dh, double* Vh,
+                    int64_t* rank_out) {
+  if (!c) return finish(make_err(RFGPU_EPARAM, "rsvd: null context"));
+  if (m < 0 || n < 0) return finish(make_err(RFGPU_EPARAM, "DenseMatrix: negative dimension"));
+  if (lda < std::max<int64_t>(1, m) || (!a && m * n > 0)) return finish(make_err(RFGPU_EPARAM, "rsvd: bad host matrix"));
+  std::lock_guard<std::mutex> lk(c->mu);
+  Status s = [&]() -> Status {
+    RF_TRY(ensure_device(c));
+    rfgpu_matrix h;
+    h.ctx = c;
+    h.m = m;
+    h.n = n;
+    h.m_global = m;
+    RF_TRY(global_rows(c, &h));
+    RF_TRY(check_sample(&h, k, ell, "power_range"));
+    if (q < 0) return make_err(RFGPU_EPARAM, "power_range: q must be non-negative");
+    if (!c->copy_stream) RF_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    h.lda = even(std::max<int64_t>(1, m));
+    const size_t bytes = sizeof(double) * static_cast<size_t>(h.lda) * std::max<int64_t>(1, n);
+    if (c->a_cache_bytes < bytes) {
+      RF_CUDA(cudaStreamSynchronize(c->stream));
+      if (c->a_cache) cudaFree(c->a_cache);
+      c->a_cache = nullptr;
+      c->a_cache_bytes = 0;
+      if (cudaMalloc(&c->a_cache, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return make_err(RFGPU_ENOMEM, "matrix upload: device allocation failed");
+      }
+      c->a_cache_bytes = bytes;
+    }
+    h.dev = c->a_cache;
+    h.src = a;
+    h.src_ld = lda;
+    cudaStream_t st = c->stream;
+    const int64_t ldu = std::max<int64_t>(1, m);
+    DBuf gd, U, D, V;
+    RF_TRY(gd.alloc(sizeof(double) * n * ell, st));
+    RF_TRY(U.alloc(sizeof(double) * ldu * ell, st));
+    RF_TRY(D.alloc(sizeof(double) * ell, st));
+    RF_TRY(V.alloc(sizeof(double) * n * ell, st));
+    RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
+    int64_t r = 0;
+    Status cs = rsvd_core(c, &h, gd.d(), k, ell, q, keep_over != 0, reorth != 0, U.d(), ldu, D.d(), V.d(), &r);
+    if (!cs.ok()) {
+      cudaStreamSynchronize(c->copy_stream);  // never leave a copy from the caller's buffer in flight
+      return cs;
+    }
     RF_TRY(copy_out(c, Uh, ldu, U.d(), ldu, m, r));
     RF_TRY(copy_out(c, Dh, std::max<int64_t>(1, r), D.d(), std::max<int64_t>(1, r), r, 1));
     RF_TRY(copy_out(c, Vh, n, V.d(), n, n, r));

@@ -162,13 +162,13 @@ SvdFactors rsvd(const DenseMatrix& a, idx k, idx p, idx q, std::uint64_t seed, b
   const idx ell = k + p;
   const DenseMatrix g = gaussian(seed, "range.G", a.cols, ell);
   std::lock_guard<std::mutex> lk(g_mu);
-  DeviceA da(a);
   std::vector<double> u(static_cast<std::size_t>(std::max<idx>(1, a.rows * ell)));
   std::vector<double> d(static_cast<std::size_t>(ell));
   std::vector<double> v(static_cast<std::size_t>(std::max<idx>(1, a.cols * ell)));
   int64_t r = 0;
-  check(rfgpu_rsvd(ctx(), da.h, g.data.data(), k, ell, q, keep_oversamples ? 1 : 0, reorthonormalize ? 1 : 0, u.data(),
-                   d.data(), v.data(), &r));
+  // A streams in from the caller's DenseMatrix behind the first pass
+  check(rfgpu_rsvd_host(ctx(), a.data.data(), a.rows, a.cols, std::max<idx>(1, a.rows), g.data.data(), k, ell, q,
+                        keep_oversamples ? 1 : 0, reorthonormalize ? 1 : 0, u.data(), d.data(), v.data(), &r));
   SvdFactors out;
   out.U = make(a.rows, r, u.data());
   out.V = make(a.cols, r, v.data());

@@ -152,6 +152,35 @@ def test_rsvd_deterministic(ctx, port):
     assert not np.array_equal(f1.U, f3.U)
 
 
+@pytest.mark.parametrize("m", [70000, 600000])
+def test_rsvd_host_streamed_matches_device_path(ctx, m):
+    """rfgpu_rsvd_host streams A in row panels behind pass 1 (4 / 16 panels
+    here); the factors must match the device-resident call and the cached
+    device buffer must be reusable across calls of different sizes."""
+    n, k, p = 96, 10, 6
+    rng = np.random.default_rng(m)
+    u, _ = np.linalg.qr(rng.standard_normal((m, 40)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, 40)))
+    a = np.asfortranarray((u * 0.8 ** np.arange(40)) @ v.T)
+    host = rf.rsvd(a, k, p, 1, 3, reorthonormalize=True, ctx=ctx)
+    dm = ctx.matrix(a)
+    try:
+        dev = rf.rsvd(dm, k, p, 1, 3, reorthonormalize=True, ctx=ctx)
+    finally:
+        dm.free()
+    assert rel(host.D, dev.D).max() < 1e-12
+    assert np.abs(np.abs(host.U) - np.abs(dev.U)).max() < 1e-9
+    assert np.abs(np.abs(host.V) - np.abs(dev.V)).max() < 1e-9
+    a5 = np.asfortranarray(a[:5000])
+    small = rf.rsvd(a5, k, p, 1, 3, reorthonormalize=True, ctx=ctx)  # reuses the larger cached buffer
+    dm = ctx.matrix(a5)
+    try:
+        want = rf.rsvd(dm, k, p, 1, 3, reorthonormalize=True, ctx=ctx)
+    finally:
+        dm.free()
+    assert np.array_equal(small.D, want.D) and np.array_equal(small.U, want.U)
+
+
 def test_rsvd_zero_matrix(ctx):
     f = rf.rsvd(np.zeros((12, 9)), 3, 2, 0, 1, ctx=ctx)
     assert f.U.shape[1] == 0 and f.D.size == 0
