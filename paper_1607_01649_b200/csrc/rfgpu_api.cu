@@ -64,12 +64,16 @@ __global__ void gather_cols_kernel(const double* __restrict__ A, int64_t lda, in
   }
 }
 
+// R(i, :) = A(idx[i] - row0, :) for global row indices owned by this shard
+// (rows row0 .. row0 + m_loc - 1), zero otherwise: summed over ranks this
+// assembles A(idx, :) of the row-sharded A.
 __global__ void gather_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t n, const int64_t* __restrict__ idx,
-                                   int64_t k, double* __restrict__ R, int64_t ldr) {
+                                   int64_t k, double* __restrict__ R, int64_t ldr, int64_t row0, int64_t m_loc) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * k;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t j = e / k, i = e % k;
-    R[j * ldr + i] = A[j * lda + idx[i]];
+    const int64_t r = idx[i] - row0;
+    R[j * ldr + i] = (r >= 0 && r < m_loc) ? A[j * lda + r] : 0.0;
   }
 }
 
@@ -733,7 +737,7 @@ inline unsigned grid1d(int64_t n) { return static_cast<unsigned>(std::max<int64_
 // (svd_dense semantics, dense.cpp:585-701) via CholeskyQR2 + Jacobi on the
 // c x c factor, Jacobi on M itself when CholeskyQR is not accepted.
 Status svd_tall_dev(rfgpu_ctx* c, const double* M, int64_t rows, int64_t cols, int64_t ldm, double* Um, double* S,
-                    double* Vm) {
+                    double* Vm, bool dist = false) {
   cudaStream_t st = c->stream;
   const int64_t ldr = even(rows);
   DBuf q, rr, r2i, ur, ur2, jw, inf, mc;
@@ -744,9 +748,31 @@ Status svd_tall_dev(rfgpu_ctx* c, const double* M, int64_t rows, int64_t cols, i
   Basis b;
   b.Q = q.d();
   b.ldq = ldr;
-  RF_TRY(orth(c, M, rows, cols, ldm, &b, r2i.d(), rr.d(), false, true));
+  RF_TRY(orth(c, M, rows, cols, ldm, &b, r2i.d(), rr.d(), dist, true));
   int* info = inf.as<int>();
-  if (b.fast) {
+  if (dist && !b.fast) {
+    // Row-sharded M, rank-deficient / ill-conditioned: the Gram-Schmidt basis
+    // Q (rows x r) spans M's columns up to the reference drop rule, so
+    // M = Q R with R = Q^T M (summed over ranks); SVD of the replicated R.
+    const int64_t r = b.r;
+    DBuf rq;
+    RF_TRY(rq.alloc(sizeof(double) * std::max<int64_t>(1, r * cols), st));
+    RF_TRY(ur.alloc(sizeof(double) * std::max<int64_t>(1, r * cols), st));
+    if (r > 0) {
+      RF_TRY(gemm(c, true, r, cols, rows, b.Q, b.ldq, M, ldm, rq.d(), r));
+      RF_TRY(allreduce(c, rq.d(), r * cols));
+      const size_t jwb = jacobi_work_bytes(r, cols);
+      if (jwb) RF_TRY(jw.alloc(jwb, st));
+      Timed tj(c, "jacobi");
+      RF_CUDA(jacobi_svd(rq.d(), r, cols, ur.d(), S, Vm, jw.d(), info, info + 1, st));
+    }
+    RF_CUDA(cudaMemsetAsync(Um, 0, sizeof(double) * rows * cols, st));
+    if (r > 0) RF_TRY(gemm(c, false, rows, cols, r, b.Q, b.ldq, ur.d(), r, Um, rows));
+    if (r == 0) {
+      RF_CUDA(cudaMemsetAsync(S, 0, sizeof(double) * cols, st));
+      return {};
+    }
+  } else if (b.fast) {
     RF_TRY(ur.alloc(sizeof(double) * cols * cols, st));
     RF_TRY(ur2.alloc(sizeof(double) * cols * cols, st));
     const size_t jwb = jacobi_work_bytes(cols, cols);
@@ -873,9 +899,13 @@ Status row_sketch_t(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Gt, int64
 // (P^T P C + C W W^T = P^T E + F W^T) solved in the
 // eigenbases of P^T P and W W^T (right singular vectors of P and W^T), then
 // svd(C) and the lift U = Qc Uc, V = Qr Vc (:214-218).
+//
+// Row-sharded A (dist): Yc, Gr (ld ldgr) and U hold this rank's rows; Yr
+// (already summed) is replicated; the two products over m (P, F) are summed
+// over ranks and the tall SVD of Yc runs on the sharded rows.
 Status single_pass_core(rfgpu_ctx* c, const double* Yc, int64_t m, const double* Yr, int64_t n, const double* Gc,
-                        const double* Gr, int64_t k, int64_t ell, double* U, int64_t ldu, double* D, double* V,
-                        int64_t* rank_out) {
+                        const double* Gr, int64_t ldgr, int64_t k, int64_t ell, double* U, int64_t ldu, double* D,
+                        double* V, int64_t* rank_out, bool dist = false) {
   Timed t(c, "single_pass_core");
   cudaStream_t st = c->stream;
   const int64_t kk = std::min(k, ell);
@@ -886,17 +916,19 @@ Status single_pass_core(rfgpu_ctx* c, const double* Yc, int64_t m, const double*
   RF_TRY(ur.alloc(sizeof(double) * n * ell, st));
   RF_TRY(sr.alloc(sizeof(double) * ell, st));
   RF_TRY(vr.alloc(sizeof(double) * ell * ell, st));
-  RF_TRY(svd_tall_dev(c, Yc, m, ell, m, uc.d(), sc.d(), vc.d()));  // Qc = uc(:, :kk)
+  RF_TRY(svd_tall_dev(c, Yc, m, ell, m, uc.d(), sc.d(), vc.d(), dist));  // Qc = uc(:, :kk)
   RF_TRY(svd_tall_dev(c, Yr, n, ell, n, ur.d(), sr.d(), vr.d()));  // Qr = ur(:, :kk)
   RF_TRY(P.alloc(sizeof(double) * ell * kk, st));
   RF_TRY(E.alloc(sizeof(double) * ell * kk, st));
   RF_TRY(W.alloc(sizeof(double) * kk * ell, st));
   RF_TRY(F.alloc(sizeof(double) * kk * ell, st));
   RF_TRY(Wt.alloc(sizeof(double) * ell * kk, st));
-  RF_TRY(gemm(c, true, ell, kk, m, Gr, m, uc.d(), m, P.d(), ell));   // P = Gr^T Qc
+  RF_TRY(gemm(c, true, ell, kk, m, Gr, ldgr, uc.d(), m, P.d(), ell));   // P = Gr^T Qc
+  if (dist) RF_TRY(allreduce(c, P.d(), ell * kk));
   RF_TRY(gemm(c, true, ell, kk, n, Yr, n, ur.d(), n, E.d(), ell));   // E = Yr^T Qr
   RF_TRY(gemm(c, true, kk, ell, n, ur.d(), n, Gc, n, W.d(), kk));    // W = Qr^T Gc
   RF_TRY(gemm(c, true, kk, ell, m, uc.d(), m, Yc, m, F.d(), kk));    // F = Qc^T Yc
+  if (dist) RF_TRY(allreduce(c, F.d(), kk * ell));
   RF_CUDA(transpose(W.d(), kk, ell, kk, Wt.d(), ell, st));
   // P = Up Sp Vp^T  =>  P^T P = Vp Sp^2 Vp^T;  W^T = Uw Sw Vw^T => W W^T = Vw Sw^2 Vw^T
   RF_TRY(up.alloc(sizeof(double) * ell * kk, st));
@@ -941,8 +973,8 @@ Status single_pass_core(rfgpu_ctx* c, const double* Yc, int64_t m, const double*
 // = A_blk^T Gr. Both products run on the block while it is in HBM; the block
 // is consumed from the stream exactly once.
 Status dual_sketch_block(rfgpu_ctx* c, const double* Ablk, int64_t m, int64_t b, int64_t lda, int64_t c0, int64_t n,
-                         const double* Gc, const double* Gr, int64_t ell, double* Yc, double* Yr, double* scratch,
-                         bool first) {
+                         const double* Gc, const double* Gr, int64_t ldgr, int64_t ell, double* Yc, double* Yr,
+                         double* scratch, bool first) {
   cudaStream_t st = c->stream;
   RF_TRY(gemm(c, false, m, ell, b, Ablk, lda, Gc + c0, n, first ? Yc : scratch, m, nullptr, "sketch_nn"));
   if (!first) {
@@ -950,7 +982,7 @@ Status dual_sketch_block(rfgpu_ctx* c, const double* Ablk, int64_t m, int64_t b,
     count_launch();
     RF_CUDA(cudaGetLastError());
   }
-  RF_TRY(gemm(c, true, b, ell, m, Ablk, lda, Gr, m, Yr + c0, n, nullptr, "sketch_tn"));
+  RF_TRY(gemm(c, true, b, ell, m, Ablk, lda, Gr, ldgr, Yr + c0, n, nullptr, "sketch_tn"));
   return {};
 }
 
@@ -1487,30 +1519,36 @@ int rfgpu_randomized_id(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, in
   Status s = [&]() -> Status {
     RF_TRY(check_sample(a, k, ell, "randomized_id"));
     if (q < 0) return make_err(RFGPU_EPARAM, "randomized_id: q must be non-negative");
-    if (c->world > 1) return make_err(RFGPU_EPARAM, "randomized_id: row sharding is not supported (single GPU)");
     RF_TRY(ensure_device(c));
     cudaStream_t st = c->stream;
-    const int64_t m = a->m, n = a->n, ldy = even(m);
+    // Row-sharded A (world > 1): Y stays row-local, A^T Y is summed over
+    // ranks, and Y^T (ell x m_global) is assembled on every rank (zero-padded
+    // columns + allreduce) for the replicated CPQR; Is are global row
+    // indices, X holds this rank's rows.
+    const int64_t m = a->m, mg = a->m_global, n = a->n, ldy = even(m);
     const double* A = static_cast<const double*>(a->dev);
     DBuf gd, y, z, yt, zt, x;
     RF_TRY(gd.alloc(sizeof(double) * n * ell, st));
     RF_TRY(y.alloc(sizeof(double) * ldy * ell, st));
     RF_TRY(z.alloc(sizeof(double) * n * ell, st));
-    RF_TRY(yt.alloc(sizeof(double) * ell * m, st));
-    RF_TRY(zt.alloc(sizeof(double) * k * m, st));
+    RF_TRY(yt.alloc(sizeof(double) * ell * mg, st));
+    RF_TRY(zt.alloc(sizeof(double) * k * mg, st));
     RF_TRY(x.alloc(sizeof(double) * m * k, st));
     RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
     // tall sketch Y = (A A^T)^q A G (lowrank.cpp:316-320)
     RF_TRY(gemm(c, false, m, ell, n, A, a->lda, gd.d(), n, y.d(), ldy, nullptr, "pass_nn"));
     for (int64_t j = 0; j < q; ++j) {
       RF_TRY(gemm(c, true, n, ell, m, A, a->lda, y.d(), ldy, z.d(), n, nullptr, "pass_tn"));
+      RF_TRY(allreduce(c, z.d(), n * ell));
       RF_TRY(gemm(c, false, m, ell, n, A, a->lda, z.d(), n, y.d(), ldy, nullptr, "pass_nn"));
     }
-    RF_CUDA(transpose(y.d(), m, ell, ldy, yt.d(), ell, st));  // Y^T (ell x m)
+    if (c->world > 1) RF_CUDA(cudaMemsetAsync(yt.d(), 0, sizeof(double) * ell * mg, st));
+    RF_CUDA(transpose(y.d(), m, ell, ldy, yt.d() + a->row0 * ell, ell, st));  // Y^T (ell x m), this rank's columns
+    RF_TRY(allreduce(c, yt.d(), ell * mg));
     int64_t ke = 0;
-    RF_TRY(col_id_dev(c, yt.d(), ell, m, ell, k, nullptr, Is, zt.d(), &ke, truncated));
+    RF_TRY(col_id_dev(c, yt.d(), ell, mg, ell, k, nullptr, Is, zt.d(), &ke, truncated));
     if (ke > 0) {
-      RF_CUDA(transpose(zt.d(), ke, m, ke, x.d(), m, st));  // X = Z^T (m x ke)
+      RF_CUDA(transpose(zt.d() + a->row0 * ke, ke, m, ke, x.d(), m, st));  // X = Z^T, this rank's rows
       RF_CUDA(cudaMemcpyAsync(Xh, x.d(), sizeof(double) * m * ke, cudaMemcpyDeviceToHost, st));
     }
     RF_CUDA(cudaStreamSynchronize(st));
@@ -1528,23 +1566,26 @@ int rfgpu_randomized_cur(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, i
   Status s = [&]() -> Status {
     RF_TRY(check_sample(a, k, ell, "randomized_cur"));
     if (q < 0) return make_err(RFGPU_EPARAM, "randomized_cur: q must be non-negative");
-    if (c->world > 1) return make_err(RFGPU_EPARAM, "randomized_cur: row sharding is not supported (single GPU)");
     RF_TRY(ensure_device(c));
     cudaStream_t st = c->stream;
-    const int64_t m = a->m, n = a->n;
+    // Row-sharded A (world > 1): the wide sketch is summed over ranks inside
+    // row_sketch_t; C = A(:, Js) is assembled on every rank (zero-padded
+    // rows + allreduce), R = A(Is, :) likewise; every later step is
+    // replicated and deterministic, so all ranks return the same Js, Is, U.
+    const int64_t m = a->m, mg = a->m_global, n = a->n;
     const double* A = static_cast<const double*>(a->dev);
     DBuf gd, gt, yt, y, z, jsd, isd, cm, ct, zr, rm, rt, zt, um, sv, vm, w1, w2, xx, uc;
-    RF_TRY(gd.alloc(sizeof(double) * ell * m, st));
-    RF_TRY(gt.alloc(sizeof(double) * m * ell, st));
+    RF_TRY(gd.alloc(sizeof(double) * ell * mg, st));
+    RF_TRY(gt.alloc(sizeof(double) * mg * ell, st));
     RF_TRY(yt.alloc(sizeof(double) * n * ell, st));
     RF_TRY(y.alloc(sizeof(double) * ell * n, st));
     RF_TRY(z.alloc(sizeof(double) * k * n, st));
     RF_TRY(jsd.alloc(sizeof(int64_t) * k, st));
     RF_TRY(isd.alloc(sizeof(int64_t) * k, st));
-    RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * ell * m, cudaMemcpyHostToDevice, st));
-    RF_CUDA(transpose(gd.d(), ell, m, ell, gt.d(), m, st));
+    RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * ell * mg, cudaMemcpyHostToDevice, st));
+    RF_CUDA(transpose(gd.d(), ell, mg, ell, gt.d(), mg, st));
     // wide sketch Y = G A (+ q passes), lowrank.cpp:351-355
-    RF_TRY(row_sketch_t(c, a, gt.d(), m, ell, q, yt.d()));
+    RF_TRY(row_sketch_t(c, a, gt.d() + a->row0, mg, ell, q, yt.d()));
     RF_CUDA(transpose(yt.d(), n, ell, n, y.d(), ell, st));
     // column ID of Y -> Js, Z (:357)
     int64_t kc = 0, kr = 0;
@@ -1558,22 +1599,25 @@ int rfgpu_randomized_cur(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, i
       return {};
     }
     // C = A(:, Js) (m x kc); row ID of C: col_id_core(C^T, kc) (:360-364)
-    RF_TRY(cm.alloc(sizeof(double) * m * kc, st));
-    RF_TRY(ct.alloc(sizeof(double) * kc * m, st));
-    RF_TRY(zr.alloc(sizeof(double) * kc * m, st));
-    gather_cols_kernel<<<grid1d(m * kc), 256, 0, st>>>(A, a->lda, m, jsd.as<int64_t>(), kc, cm.d(), m);
+    RF_TRY(cm.alloc(sizeof(double) * mg * kc, st));
+    RF_TRY(ct.alloc(sizeof(double) * kc * mg, st));
+    RF_TRY(zr.alloc(sizeof(double) * kc * mg, st));
+    if (c->world > 1) RF_CUDA(cudaMemsetAsync(cm.d(), 0, sizeof(double) * mg * kc, st));
+    gather_cols_kernel<<<grid1d(m * kc), 256, 0, st>>>(A, a->lda, m, jsd.as<int64_t>(), kc, cm.d() + a->row0, mg);
     count_launch();
     RF_CUDA(cudaGetLastError());
-    RF_CUDA(transpose(cm.d(), m, kc, m, ct.d(), kc, st));
-    RF_TRY(col_id_dev(c, ct.d(), kc, m, kc, kc, isd.as<int64_t>(), Is, zr.d(), &kr, &trr));
+    RF_TRY(allreduce(c, cm.d(), mg * kc));  // all rows of C on every rank
+    RF_CUDA(transpose(cm.d(), mg, kc, mg, ct.d(), kc, st));
+    RF_TRY(col_id_dev(c, ct.d(), kc, mg, kc, kc, isd.as<int64_t>(), Is, zr.d(), &kr, &trr));
     *kr_out = kr;
     // R = A(Is, :) (kr x n); U = (lsq(R^T, Z^T))^T  (:365-367)
     RF_TRY(rm.alloc(sizeof(double) * kr * n, st));
     RF_TRY(rt.alloc(sizeof(double) * n * kr, st));
     RF_TRY(zt.alloc(sizeof(double) * n * kc, st));
-    gather_rows_kernel<<<grid1d(n * kr), 256, 0, st>>>(A, a->lda, n, isd.as<int64_t>(), kr, rm.d(), kr);
+    gather_rows_kernel<<<grid1d(n * kr), 256, 0, st>>>(A, a->lda, n, isd.as<int64_t>(), kr, rm.d(), kr, a->row0, m);
     count_launch();
     RF_CUDA(cudaGetLastError());
+    RF_TRY(allreduce(c, rm.d(), kr * n));  // rows Is live on their owning ranks
     RF_CUDA(transpose(rm.d(), kr, n, kr, rt.d(), n, st));
     RF_CUDA(transpose(z.d(), kc, n, kc, zt.d(), n, st));
     RF_TRY(um.alloc(sizeof(double) * n * kr, st));
@@ -1595,10 +1639,10 @@ int rfgpu_randomized_cur(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, i
     RF_CUDA(cudaMemcpyAsync(Uh, uc.d(), sizeof(double) * kc * kr, cudaMemcpyDeviceToHost, st));
     // cond numbers (cond_number, lowrank.cpp:37-41): singular values of C and R
     DBuf uc2, sc, vc2;
-    RF_TRY(uc2.alloc(sizeof(double) * m * kc, st));
+    RF_TRY(uc2.alloc(sizeof(double) * mg * kc, st));
     RF_TRY(sc.alloc(sizeof(double) * kc, st));
     RF_TRY(vc2.alloc(sizeof(double) * kc * kc, st));
-    RF_TRY(svd_tall_dev(c, cm.d(), m, kc, m, uc2.d(), sc.d(), vc2.d()));
+    RF_TRY(svd_tall_dev(c, cm.d(), mg, kc, mg, uc2.d(), sc.d(), vc2.d()));
     std::vector<double> scv(kc);
     RF_CUDA(cudaMemcpyAsync(scv.data(), sc.d(), sizeof(double) * kc, cudaMemcpyDeviceToHost, st));
     RF_CUDA(cudaStreamSynchronize(st));
@@ -1643,7 +1687,7 @@ int rfgpu_dual_sketch_f32(rfgpu_ctx* c, const rfgpu_matrix* a, const float* gc, 
       f32_to_f64_kernel<<<grid1d(m * b), 256, 0, s>>>(static_cast<const float*>(a->dev) + c0 * a->lda, m, b, a->lda,
                                                       conv.d(), ldc);
       count_launch();
-      RF_TRY(dual_sketch_block(c, conv.d(), m, b, ldc, c0, n, gcd.d(), grd.d(), ell, ycd.d(), yrd.d(), scratch.d(),
+      RF_TRY(dual_sketch_block(c, conv.d(), m, b, ldc, c0, n, gcd.d(), grd.d(), m, ell, ycd.d(), yrd.d(), scratch.d(),
                                first));
       first = false;
     }
@@ -1681,7 +1725,7 @@ Status sp_flush(rfgpu_single_pass* s) {
   if (s->staged == 0) return {};
   rfgpu_ctx* c = s->ctx;
   RF_CUDA(cudaMemcpyAsync(s->stage_d, s->stage_h, sizeof(double) * s->m * s->staged, cudaMemcpyHostToDevice, c->stream));
-  RF_TRY(dual_sketch_block(c, s->stage_d, s->m, s->staged, s->m, s->stage_c0, s->n, s->gc, s->gr, s->ell, s->yc, s->yr,
+  RF_TRY(dual_sketch_block(c, s->stage_d, s->m, s->staged, s->m, s->stage_c0, s->n, s->gc, s->gr, s->m, s->ell, s->yc, s->yr,
                            s->scratch, s->first));
   RF_CUDA(cudaStreamSynchronize(c->stream));  // stage_h is reused by the next push
   s->first = false;
@@ -1706,9 +1750,17 @@ extern "C" {
 int rfgpu_single_pass_begin(rfgpu_ctx* c, int64_t m, int64_t n, int64_t ell, const double* gc, const double* gr,
                             rfgpu_single_pass** out) {
   if (!c || !out) return finish(make_err(RFGPU_EPARAM, "single_pass: null argument"));
-  if (c->world > 1) return finish(make_err(RFGPU_EPARAM, "single_pass: row sharding is not supported (single GPU)"));
   if (m < 1 || n < 1 || ell < 1) return finish(make_err(RFGPU_EPARAM, "single_pass_svd: bad dimensions"));
   std::lock_guard<std::mutex> lk(c->mu);
+  // Row-sharded stream (world > 1): every rank streams the column blocks of
+  // ITS rows (m = local rows) and passes the FULL m_global x ell Gr.
+  rfgpu_matrix shape;
+  shape.m = m;
+  {
+    cudaSetDevice(c->device);
+    Status gs = global_rows(c, &shape);
+    if (!gs.ok()) return finish(gs);
+  }
   auto s = new rfgpu_single_pass();
   s->ctx = c;
   s->m = m;
@@ -1730,7 +1782,8 @@ int rfgpu_single_pass_begin(rfgpu_ctx* c, int64_t m, int64_t n, int64_t ell, con
     return finish(make_err(RFGPU_ENOMEM, "single_pass: device allocation failed"));
   }
   cudaMemcpy(s->gc, gc, sizeof(double) * n * ell, cudaMemcpyHostToDevice);
-  cudaMemcpy(s->gr, gr, sizeof(double) * m * ell, cudaMemcpyHostToDevice);
+  cudaMemcpy2D(s->gr, sizeof(double) * m, gr + shape.row0, sizeof(double) * shape.m_global, sizeof(double) * m, ell,
+               cudaMemcpyHostToDevice);
   *out = s;
   return RFGPU_OK;
 }
@@ -1773,7 +1826,9 @@ int rfgpu_single_pass_finish(rfgpu_single_pass* s, int64_t k, double* Uh, double
       RF_TRY(D.alloc(sizeof(double) * kk, c->stream));
       RF_TRY(V.alloc(sizeof(double) * n * kk, c->stream));
       int64_t r = 0;
-      RF_TRY(single_pass_core(c, s->yc, m, s->yr, n, s->gc, s->gr, k, s->ell, U.d(), m, D.d(), V.d(), &r));
+      if (c->world > 1) RF_TRY(allreduce(c, s->yr, n * s->ell));  // Yr = sum over row shards of A^T Gr
+      RF_TRY(single_pass_core(c, s->yc, m, s->yr, n, s->gc, s->gr, m, k, s->ell, U.d(), m, D.d(), V.d(), &r,
+                              c->world > 1));
       RF_TRY(copy_out(c, Uh, m, U.d(), m, m, r));
       RF_TRY(copy_out(c, Dh, r, D.d(), r, r, 1));
       RF_TRY(copy_out(c, Vh, n, V.d(), n, n, r));
@@ -1797,10 +1852,11 @@ int rfgpu_single_pass_svd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const doub
   std::lock_guard<std::mutex> lk(c->mu);
   Status st = [&]() -> Status {
     RF_TRY(check_sample(a, k, ell, "single_pass_svd"));
-    if (c->world > 1) return make_err(RFGPU_EPARAM, "single_pass: row sharding is not supported (single GPU)");
     RF_TRY(ensure_device(c));
     cudaStream_t s = c->stream;
-    const int64_t m = a->m, n = a->n;
+    // row-sharded A: gr is the FULL m_global x ell Gr; this rank uses its rows
+    const int64_t m = a->m, n = a->n, ldgr = a->m_global;
+    gr += a->row0;
     DBuf yc, yr, scratch, conv;
     RF_TRY(yc.alloc(sizeof(double) * m * ell, s));
     RF_TRY(yr.alloc(sizeof(double) * n * ell, s));
@@ -1808,7 +1864,7 @@ int rfgpu_single_pass_svd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const doub
     {
       Timed t(c, "dual_sketch");
       if (!a->f32) {
-        RF_TRY(dual_sketch_block(c, static_cast<const double*>(a->dev), m, n, a->lda, 0, n, gc, gr, ell, yc.d(), yr.d(),
+        RF_TRY(dual_sketch_block(c, static_cast<const double*>(a->dev), m, n, a->lda, 0, n, gc, gr, ldgr, ell, yc.d(), yr.d(),
                                  scratch.d(), true));
       } else {
         // fp32 matrix: widened to fp64 one column chunk at a time (each entry read once)
@@ -1822,13 +1878,14 @@ int rfgpu_single_pass_svd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const doub
                                                           conv.d(), ldc);
           count_launch();
           RF_CUDA(cudaGetLastError());
-          RF_TRY(dual_sketch_block(c, conv.d(), m, b, ldc, c0, n, gc, gr, ell, yc.d(), yr.d(), scratch.d(), first));
+          RF_TRY(dual_sketch_block(c, conv.d(), m, b, ldc, c0, n, gc, gr, ldgr, ell, yc.d(), yr.d(), scratch.d(), first));
           first = false;
         }
       }
     }
+    RF_TRY(allreduce(c, yr.d(), n * ell));  // Yr = sum over row shards of A^T Gr
     int64_t r = 0;
-    RF_TRY(single_pass_core(c, yc.d(), m, yr.d(), n, gc, gr, k, ell, U, m, D, V, &r));
+    RF_TRY(single_pass_core(c, yc.d(), m, yr.d(), n, gc, gr, ldgr, k, ell, U, m, D, V, &r, c->world > 1));
     if (rank_out) *rank_out = r;
     return {};
   }();
