@@ -333,14 +333,36 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
       if (active && k < npairs) {
         double app = 0.0, aqq = 0.0, apq = 0.0;
         if (valid) {
-          const double* xp = Xs + static_cast<size_t>(cp) * LDX;
-          const double* xq = Xs + static_cast<size_t>(cq) * LDX;
-          for (int r = x0; r < x1; ++r) {
+          const double* __restrict__ xp = Xs + static_cast<size_t>(cp) * LDX;
+          const double* __restrict__ xq = Xs + static_cast<size_t>(cq) * LDX;
+          // 4 rows in flight: the loads of a group issue back to back
+          double bpp = 0.0, bqq = 0.0, bpq = 0.0;
+          int r = x0;
+          for (; r + 4 <= x1; r += 4) {
+            const double u0 = xp[r], u1 = xp[r + 1], u2 = xp[r + 2], u3 = xp[r + 3];
+            const double v0 = xq[r], v1 = xq[r + 1], v2 = xq[r + 2], v3 = xq[r + 3];
+            app = fma(u0, u0, app);
+            aqq = fma(v0, v0, aqq);
+            apq = fma(u0, v0, apq);
+            bpp = fma(u1, u1, bpp);
+            bqq = fma(v1, v1, bqq);
+            bpq = fma(u1, v1, bpq);
+            app = fma(u2, u2, app);
+            aqq = fma(v2, v2, aqq);
+            apq = fma(u2, v2, apq);
+            bpp = fma(u3, u3, bpp);
+            bqq = fma(v3, v3, bqq);
+            bpq = fma(u3, v3, bpq);
+          }
+          for (; r < x1; ++r) {
             const double u = xp[r], v = xq[r];
             app = fma(u, u, app);
             aqq = fma(v, v, aqq);
             apq = fma(u, v, apq);
           }
+          app += bpp;
+          aqq += bqq;
+          apq += bpq;
         }
         RF_TRACE(2)
         double* d = red + (h * npairs + k) * 3;
@@ -422,20 +444,29 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
         const double cs = prm[0], sn = prm[1];
         if (sn != 2.0) {
           if (h == 0) s_rotated = 1;
-          double* xp = Xs + static_cast<size_t>(cp) * LDX;
-          double* xq = Xs + static_cast<size_t>(cq) * LDX;
-          for (int r = x0; r < x1; ++r) {
-            const double u = xp[r], v = xq[r];
-            xp[r] = cs * u - sn * v;
-            xq[r] = sn * u + cs * v;
-          }
-          double* vp = Vs + static_cast<size_t>(cp) * LDV;
-          double* vq = Vs + static_cast<size_t>(cq) * LDV;
-          for (int r = v0; r < v1; ++r) {
-            const double u = vp[r], v = vq[r];
-            vp[r] = cs * u - sn * v;
-            vq[r] = sn * u + cs * v;
-          }
+          // columns cp != cq never alias: 4 rows of loads in flight per group
+          auto rotate = [&](double* __restrict__ a, double* __restrict__ b, int r0, int r1) {
+            int r = r0;
+            for (; r + 4 <= r1; r += 4) {
+              const double u0 = a[r], u1 = a[r + 1], u2 = a[r + 2], u3 = a[r + 3];
+              const double w0 = b[r], w1 = b[r + 1], w2 = b[r + 2], w3 = b[r + 3];
+              a[r] = cs * u0 - sn * w0;
+              a[r + 1] = cs * u1 - sn * w1;
+              a[r + 2] = cs * u2 - sn * w2;
+              a[r + 3] = cs * u3 - sn * w3;
+              b[r] = sn * u0 + cs * w0;
+              b[r + 1] = sn * u1 + cs * w1;
+              b[r + 2] = sn * u2 + cs * w2;
+              b[r + 3] = sn * u3 + cs * w3;
+            }
+            for (; r < r1; ++r) {
+              const double u = a[r], w = b[r];
+              a[r] = cs * u - sn * w;
+              b[r] = sn * u + cs * w;
+            }
+          };
+          rotate(Xs + static_cast<size_t>(cp) * LDX, Xs + static_cast<size_t>(cq) * LDX, x0, x1);
+          rotate(Vs + static_cast<size_t>(cp) * LDV, Vs + static_cast<size_t>(cq) * LDV, v0, v1);
         }
       }
       RF_TRACE(12)
@@ -522,7 +553,7 @@ JacobiLayout jacobi_layout(int64_t mr, int64_t c) {
   // per-round shared-memory traffic of a CTA is proportional to its rows.
   static const int target = [] {
     const char* e = std::getenv("RFGPU_JACOBI_ROWS");
-    return e ? std::max(1, std::atoi(e)) : 16;
+    return e ? std::max(1, std::atoi(e)) : 32;
   }();
   int P0 = 1;
   while (P0 < 16 && (mr + P0 - 1) / P0 > target) P0 *= 2;
