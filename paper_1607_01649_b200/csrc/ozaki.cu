@@ -1,0 +1,557 @@
+// FP64 passes over A on the INT8 tensor cores (tcgen05.mma kind::i8, TMEM
+// accumulators): Ozaki-scheme splitting of both operands into kS = 8 signed
+// 7-bit digits, exact int32 digit products on the tensor cores, recombined in
+// FP64 in the epilogue.
+//
+// Why: B200's FP64 pipe (DMMA) peaks at 37 TF/s, its INT8 tensor cores at
+// 4.5 POPS. A pass over A (Y = A X, Z = A^T Q: proj/src/dense.cpp:102-126 on
+// the reference's hot path, rangefinder.cpp:68-78, lowrank.cpp:92) needs
+// 2 m n l flops; as 36 int8 digit products it still runs ~2x faster than
+// DMMA (tools/microbench/ozk.cu).
+//
+// Numerics. Row i of A is scaled by 2^-e_i (|A(i,:)| < 2^e_i, exact), every
+// column c of the thin operand by 2^-f_c; a scaled value x in (-1, 1) is
+// x = sum_{s<8} d_s 128^-(s+1) + r, d_s = trunc(128 * remainder) in
+// [-127, 127], |r| < 2^-56 (each step exact in FP64). The product keeps the
+// digit pairs with s + t <= 7 (36 of 64), grouped by g = s + t into 8 int32
+// TMEM accumulators (8 x 64 columns = all 512; exact: 8 * K * 127^2 < 2^31
+// for K <= 16384, the split size), and sums sum_g 2^-7(g+2) acc_g in FP64
+// (one rounding per group), then scales by 2^(e_i + f_c). Per term the
+// result is within ~10 * 2^-56 = 1.4e-16 of the exact product, relative to
+// max|A(i,:)| max|X(:,c)|: FP64-class (7 digits, 28 products, measured
+// 2e-13 on rsvd singular values, was too coarse for the reference's
+// down-dated residual on exact-rank inputs).
+// For A^T Q the row scale of A moves onto Q: sum_i A'(i,j) (Q(i,c) 2^e_i).
+//
+// Layouts:
+//   NN digits of A: [kS][m_pad][n_pad]  (row-major: K = n contiguous)
+//   (64-byte swizzled TMA tiles; both GEMM operands K-major)
+//   TN digits of A: [kS][n_pad][m_pad]  (column-major: K = m contiguous)
+//   thin operand digits: [kS][l_pad][K_pad]
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+
+#include "common.cuh"
+#include "rfgpu_internal.h"
+
+namespace rfgpu {
+namespace {
+
+constexpr int kS = 8;          // digits per operand
+constexpr int OBM = 128;       // tile rows (TMEM lanes)
+constexpr int OBN = 64;        // tile columns per accumulator group
+constexpr int OBK = 64;        // K bytes per pipeline stage (64B swizzle)
+constexpr int kStages = 2;
+constexpr int kTmemCols = 512;  // kS * OBN
+constexpr int64_t kSplitK = 16384;
+constexpr int kThreads = 192;   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr size_t kStageBytes = static_cast<size_t>(kS) * (OBM + OBN) * OBK;
+constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 + 256;
+
+__host__ __device__ inline int64_t roundup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// ---- operand preparation ---------------------------------------------------------
+// Exponent e with |v| < 2^e for v = max |.| (0 for an all-zero vector).
+__device__ __forceinline__ int bound_exp(double mx) { return mx > 0.0 ? ilogb(mx) + 1 : 0; }
+
+// Row exponents of A rows [r0, r1) and sum-of-squares partials (one per CTA).
+__global__ void row_stats_kernel(const double* __restrict__ A, int64_t r0, int64_t r1, int64_t n, int64_t lda,
+                                 int* __restrict__ rowexp, double* __restrict__ ssq_part) {
+  __shared__ double red[32];
+  const int64_t i = r0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  double mx = 0.0, s0 = 0.0, s1 = 0.0;
+  if (i < r1) {
+    const double* a = A + i;
+    int64_t j = 0;
+    for (; j + 2 <= n; j += 2) {
+      const double v0 = a[j * lda], v1 = a[(j + 1) * lda];
+      mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
+      s0 = fma(v0, v0, s0);
+      s1 = fma(v1, v1, s1);
+    }
+    for (; j < n; ++j) {
+      const double v = a[j * lda];
+      mx = fmax(mx, fabs(v));
+      s0 = fma(v, v, s0);
+    }
+    rowexp[i] = bound_exp(mx);
+  }
+  const double s = block_sum(s0 + s1, red);
+  if (threadIdx.x == 0 && ssq_part) ssq_part[blockIdx.x] = s;
+}
+
+// Digits of x in (-1, 1): d[s] = trunc(128 * rem).
+__device__ __forceinline__ void digits(double x, int8_t* d) {
+#pragma unroll
+  for (int s = 0; s < kS; ++s) {
+    x *= 128.0;
+    const double t = trunc(x);
+    d[s] = static_cast<int8_t>(static_cast<int>(t));
+    x -= t;
+  }
+}
+
+// A rows [r0, r1) (64-row blocks) x all n_pad columns (64-column blocks):
+// digits of A(i, j) 2^-e_i into both the NN (row-major) and TN
+// (column-major) layouts; padding rows/columns get zero digits.
+__global__ void __launch_bounds__(256) slice_a_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                                                      int64_t r0, const int* __restrict__ rowexp, int8_t* __restrict__ nn,
+                                                      int8_t* __restrict__ tn, int64_t m_pad, int64_t n_pad) {
+  __shared__ int8_t dg[kS][64][68];  // [s][col][row] (+4 pad)
+  const int64_t i0 = r0 + static_cast<int64_t>(blockIdx.y) * 64, j0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int tid = threadIdx.x;
+  // each thread: 16 elements (rows rr, col jj), reading A coalesced over rows
+  for (int e = tid; e < 64 * 64; e += 256) {
+    const int rr = e & 63, jj = e >> 6;
+    const int64_t i = i0 + rr, j = j0 + jj;
+    int8_t d[kS];
+    if (i < m && j < n) {
+      const double v = ldexp(A[j * lda + i], -rowexp[i]);
+      digits(v, d);
+    } else {
+#pragma unroll
+      for (int s = 0; s < kS; ++s) d[s] = 0;
+    }
+#pragma unroll
+    for (int s = 0; s < kS; ++s) dg[s][jj][rr] = d[s];
+  }
+  __syncthreads();
+  // TN: [s][j][i], contiguous over i: 4 bytes per thread
+  for (int e = tid; e < kS * 64 * 16; e += 256) {
+    const int q = e & 15, jj = (e >> 4) & 63, s = e >> 10;
+    const int64_t j = j0 + jj;
+    if (j < n_pad) {
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(&dg[s][jj][q * 4]);
+      *reinterpret_cast<uint32_t*>(tn + (static_cast<int64_t>(s) * n_pad + j) * m_pad + i0 + q * 4) = w;
+    }
+  }
+  // NN: [s][i][j], contiguous over j
+  for (int e = tid; e < kS * 64 * 16; e += 256) {
+    const int q = e & 15, rr = (e >> 4) & 63, s = e >> 10;
+    const int64_t i = i0 + rr;
+    uint32_t w = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) w |= static_cast<uint32_t>(static_cast<uint8_t>(dg[s][q * 4 + b][rr])) << (8 * b);
+    if (i < m_pad) *reinterpret_cast<uint32_t*>(nn + (static_cast<int64_t>(s) * m_pad + i) * n_pad + j0 + q * 4) = w;
+  }
+}
+
+// Thin operand R (K x N, col-major ld), optionally pre-scaled by 2^rowexp[i]:
+// per-column exponent f_c of max |R(i,c) 2^e_i|.
+__global__ void col_exp_kernel(const double* __restrict__ R, int64_t K, int64_t ldr, const int* __restrict__ rowexp,
+                               int* __restrict__ colexp) {
+  __shared__ double red[32];
+  const int64_t c = blockIdx.x;
+  double mx = 0.0;
+  for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
+    double v = fabs(R[c * ldr + i]);
+    if (rowexp) v = ldexp(v, rowexp[i]);
+    mx = fmax(mx, v);
+  }
+  // block max
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) colexp[c] = bound_exp(v);
+  }
+}
+
+// Digits of R(i,c) 2^(e_i - f_c) into [kS][N_pad][K_pad] (4 rows per thread).
+__global__ void slice_r_kernel(const double* __restrict__ R, int64_t K, int64_t N, int64_t ldr,
+                               const int* __restrict__ rowexp, const int* __restrict__ colexp, int8_t* __restrict__ out,
+                               int64_t K_pad, int64_t N_pad) {
+  const int64_t quads = K_pad / 4;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < quads * N_pad;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / quads, i0 = (e - c * quads) * 4;
+    uint32_t w[kS] = {};
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t i = i0 + b;
+      int8_t d[kS];
+      if (i < K && c < N) {
+        const double v = ldexp(R[c * ldr + i], (rowexp ? rowexp[i] : 0) - colexp[c]);
+        digits(v, d);
+      } else {
+#pragma unroll
+        for (int s = 0; s < kS; ++s) d[s] = 0;
+      }
+#pragma unroll
+      for (int s = 0; s < kS; ++s) w[s] |= static_cast<uint32_t>(static_cast<uint8_t>(d[s])) << (8 * b);
+    }
+#pragma unroll
+    for (int s = 0; s < kS; ++s)
+      *reinterpret_cast<uint32_t*>(out + (static_cast<int64_t>(s) * N_pad + c) * K_pad + i0) = w[s];
+  }
+}
+
+// ---- the digit GEMM -------------------------------------------------------------
+struct OzParams {
+  int64_t L_rows;   // rows per digit plane of L (multiple of 128)
+  int64_t R_rows;   // rows per digit plane of R (multiple of 64)
+  int64_t kb_per_split;  // K blocks (64 B) per split
+  int64_t kb_total;
+  int ntn, mtn, splits;
+  int64_t row0;      // first L row handled by this launch (panelled pass 1)
+  double* C;         // output (col-major, ldc) or split workspace
+  int64_t ldc;
+  int64_t M_real, N_real;  // valid output extent
+  int64_t c_row0;    // output row offset (row of C for L row row0)
+  const int* rowexp;  // optional 2^e_row output scale (indexed by L row)
+  const int* colexp;  // 2^f_col output scale
+  int ws_mode;        // 1: C is [split][N_real][M_real]
+};
+
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t umma_desc(const void* p) {
+  uint64_t d = 0;
+  d |= (static_cast<uint64_t>(smem_u32(p)) >> 4) & 0x3FFF;  // start address
+  d |= static_cast<uint64_t>(1) << 16;                       // LBO (unused: swizzled K-major)
+  d |= static_cast<uint64_t>((8 * OBK) >> 4) << 32;          // SBO: 8 rows x 64 B
+  d |= static_cast<uint64_t>(1) << 46;                       // sm100 descriptor version
+  d |= static_cast<uint64_t>(4) << 61;                       // SWIZZLE_64B
+  return d;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmL,
+                                                                  const __grid_constant__ CUtensorMap tmR,
+                                                                  const OzParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int ASZ = kS * OBM * OBK, BSZ = kS * OBN * OBK;
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + kStages * ASZ;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * BSZ);
+  uint64_t* empty = full + kStages;
+  uint64_t* done = empty + kStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // n-tile fastest: the CTAs sharing an L tile run together (L2 reuse)
+  const int64_t bid = blockIdx.x;
+  const int nt = static_cast<int>(bid % p.ntn);
+  const int64_t rest = bid / p.ntn;
+  const int mt = static_cast<int>(rest % p.mtn);
+  const int split = static_cast<int>(rest / p.mtn);
+  const int64_t lrow0 = p.row0 + static_cast<int64_t>(mt) * OBM;
+  const int64_t ncol0 = static_cast<int64_t>(nt) * OBN;
+  const int64_t kb0 = split * p.kb_per_split;
+  const int64_t kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+  const int nk = static_cast<int>(kb1 - kb0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    mbar_fence_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % kStages;
+      const uint32_t ph = (kb / kStages) & 1;
+      mbar_wait(&empty[st], ph ^ 1);
+      mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(ASZ + BSZ));
+      const int kx = static_cast<int>((kb0 + kb) * OBK);
+#pragma unroll
+      for (int s = 0; s < kS; ++s) {
+        tma2d(sA + st * ASZ + s * OBM * OBK, &tmL, &full[st], kx, static_cast<int>(s * p.L_rows + lrow0));
+        tma2d(sB + st * BSZ + s * OBN * OBK, &tmR, &full[st], kx, static_cast<int>(s * p.R_rows + ncol0));
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(OBN >> 3) << 17) |
+                               (static_cast<uint32_t>(OBM >> 4) << 24);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % kStages;
+      const uint32_t ph = (kb / kStages) & 1;
+      mbar_wait(&full[st], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int kk = 0; kk < OBK / 32; ++kk) {
+#pragma unroll
+        for (int s = 0; s < kS; ++s) {
+#pragma unroll
+          for (int t = 0; t + s < kS; ++t) {
+            const uint64_t da = umma_desc(sA + st * ASZ + s * OBM * OBK + kk * 32);
+            const uint64_t db = umma_desc(sB + st * BSZ + t * OBN * OBK + kk * 32);
+            // group g = s + t starts at (s = 0) of the first K step
+            const uint32_t accum = (kb == 0 && kk == 0 && s == 0) ? 0u : 1u;
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (s + t) * OBN),
+                "l"(da), "l"(db), "r"(idesc), "r"(accum));
+          }
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&empty[st]))
+                   : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(done))
+                 : "memory");
+  } else if (warp >= 2) {
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;  // TMEM lane quarter of this warp
+    const int64_t lrow = lrow0 + q * 32 + lane;
+    const int64_t orow = p.c_row0 + (lrow - p.row0);
+    const int rex = (p.rowexp && nk > 0) ? p.rowexp[lrow] : 0;
+    const bool row_ok = orow < p.M_real + p.c_row0 && lrow - p.row0 < p.M_real;
+    for (int c = 0; c < OBN; c += 16) {
+      double acc[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+      if (nk > 0) {
+#pragma unroll
+        for (int g = kS - 1; g >= 0; --g) {
+          uint32_t r[16];
+          const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + g * OBN + c;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+              : "r"(ta));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          const double sc = ldexp(1.0, -7 * (g + 2));
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = fma(static_cast<double>(static_cast<int32_t>(r[j])), sc, acc[j]);
+        }
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int64_t col = ncol0 + c + j;
+          if (col < p.N_real) {
+            const double v = ldexp(acc[j], rex + p.colexp[col]);
+            if (p.ws_mode)
+              p.C[(static_cast<int64_t>(split) * p.N_real + col) * p.M_real + (lrow - p.row0)] = v;
+            else
+              p.C[col * p.ldc + orow] = v;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+__global__ void reduce_ws_kernel(const double* __restrict__ part, int64_t M, int64_t N, int S, double* __restrict__ C,
+                                 int64_t ldc) {
+  const int64_t total = M * N;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n = e / M, m = e - n * M;
+    double s = 0.0;
+    for (int k = 0; k < S; ++k) s += part[k * total + e];
+    C[n * ldc + m] = s;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// int8 digit planes: rows x K bytes (row-major), box 64 B x box_rows.
+bool digit_tmap(CUtensorMap* tm, const int8_t* base, int64_t rows, int64_t K, int box_rows) {
+  auto fn = tmap_encoder();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(K)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(OBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t launch_digit_gemm(const int8_t* L, int64_t L_rows, const int8_t* R, int64_t R_rows, int64_t K_pad,
+                              int64_t row0, int64_t rows, int64_t N_real, int splits, const OzParams& base,
+                              cudaStream_t st) {
+  static bool cfg = false;
+  if (!cfg) {
+    cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmemBytes));
+    if (e != cudaSuccess) return e;
+    cfg = true;
+  }
+  CUtensorMap tl, tr;
+  if (!digit_tmap(&tl, L, kS * L_rows, K_pad, OBM) || !digit_tmap(&tr, R, kS * R_rows, K_pad, OBN))
+    return cudaErrorInvalidValue;
+  OzParams p = base;
+  p.L_rows = L_rows;
+  p.R_rows = R_rows;
+  p.kb_total = K_pad / OBK;
+  p.splits = splits;
+  p.kb_per_split = (p.kb_total + splits - 1) / splits;
+  p.ntn = static_cast<int>(R_rows / OBN);
+  p.mtn = static_cast<int>((rows + OBM - 1) / OBM);
+  p.row0 = row0;
+  p.M_real = rows;
+  p.N_real = N_real;
+  const int64_t grid = static_cast<int64_t>(p.ntn) * p.mtn * splits;
+  if (grid <= 0) return cudaSuccess;
+  ozaki_gemm_kernel<<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(tl, tr, p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool ozaki_enabled(int64_t m, int64_t n) {
+  const char* e = std::getenv("RFGPU_OZAKI");
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return true;
+  return m * n >= (int64_t(1) << 26);  // large passes only: the digit planes cost 14 m n bytes
+}
+
+OzakiA ozaki_layout(int64_t m, int64_t n) {
+  OzakiA a{};
+  a.m = m;
+  a.n = n;
+  a.m_pad = roundup(std::max<int64_t>(m, 1), OBM);
+  a.n_pad = roundup(std::max<int64_t>(n, 1), OBM);
+  return a;
+}
+
+size_t ozaki_a_bytes(int64_t m, int64_t n) {
+  const OzakiA a = ozaki_layout(m, n);
+  return 2 * static_cast<size_t>(kS) * a.m_pad * a.n_pad + sizeof(int) * a.m_pad + 256;
+}
+
+int64_t ozaki_ssq_slots(int64_t rows) { return (rows + 255) / 256; }
+
+cudaError_t ozaki_prepare_a(const double* A, int64_t m, int64_t n, int64_t lda, int64_t r0, int64_t r1, void* work,
+                            OzakiA* out, double* ssq_part, cudaStream_t st) {
+  *out = ozaki_layout(m, n);
+  int8_t* base = static_cast<int8_t*>(work);
+  out->nn = base;
+  out->tn = base + static_cast<size_t>(kS) * out->m_pad * out->n_pad;
+  out->rowexp = reinterpret_cast<int*>(out->tn + static_cast<size_t>(kS) * out->m_pad * out->n_pad);
+  if (r0 == 0 && r1 == m) {
+    // padding rows: exponent 0 (their digits are zero)
+    if (out->m_pad > m) {
+      cudaError_t e = cudaMemsetAsync(out->rowexp + m, 0, sizeof(int) * (out->m_pad - m), st);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  const int64_t rows = r1 - r0;
+  if (rows > 0) {
+    row_stats_kernel<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, st>>>(A, r0, r1, n, lda, out->rowexp, ssq_part);
+    count_launch();
+  }
+  // slice 64-row blocks covering [r0, r1) (the last panel also covers the padding rows)
+  const int64_t b0 = r0 / 64, b1 = (r1 == m ? out->m_pad : r1) / 64;
+  if (b1 > b0) {
+    dim3 grid(static_cast<unsigned>(out->n_pad / 64), static_cast<unsigned>(b1 - b0));
+    slice_a_kernel<<<grid, 256, 0, st>>>(A, m, n, lda, b0 * 64, out->rowexp, out->nn, out->tn, out->m_pad, out->n_pad);
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
+size_t ozaki_nn_work_bytes(const OzakiA& a, int64_t rows, int64_t ell) {
+  const int64_t lp = roundup(ell, OBN);
+  const int splits = static_cast<int>((a.n_pad + kSplitK - 1) / kSplitK);
+  return static_cast<size_t>(kS) * lp * a.n_pad + sizeof(int) * lp + 256 +
+         (splits > 1 ? sizeof(double) * static_cast<size_t>(splits) * rows * ell : 0);
+}
+
+cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, int64_t ldx, int64_t ell, double* Y,
+                     int64_t ldy, void* work, cudaStream_t st) {
+  const int64_t lp = roundup(ell, OBN), rows = r1 - r0;
+  int8_t* xd = static_cast<int8_t*>(work);
+  int* colexp = reinterpret_cast<int*>(xd + static_cast<size_t>(kS) * lp * a.n_pad);
+  double* ws = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(colexp) + ((sizeof(int) * lp + 255) / 256) * 256);
+  col_exp_kernel<<<static_cast<unsigned>(ell), 256, 0, st>>>(X, a.n, ldx, nullptr, colexp);
+  slice_r_kernel<<<1184, 256, 0, st>>>(X, a.n, ell, ldx, nullptr, colexp, xd, a.n_pad, lp);
+  count_launch(2);
+  // K = n beyond kSplitK would overflow the int32 group sums: split K
+  const int splits = static_cast<int>((a.n_pad + kSplitK - 1) / kSplitK);
+  OzParams p{};
+  p.C = splits > 1 ? ws : Y + r0;
+  p.ldc = ldy;
+  p.c_row0 = 0;
+  p.rowexp = a.rowexp;
+  p.colexp = colexp;
+  p.ws_mode = splits > 1 ? 1 : 0;
+  cudaError_t e = launch_digit_gemm(a.nn, a.m_pad, xd, lp, a.n_pad, r0, rows, ell, splits, p, st);
+  if (e != cudaSuccess || splits == 1) return e;
+  const int64_t total = rows * ell;
+  reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(
+      ws, rows, ell, splits, Y + r0, ldy);
+  count_launch();
+  return cudaGetLastError();
+}
+
+size_t ozaki_tn_work_bytes(const OzakiA& a, int64_t ell) {
+  const int64_t lp = roundup(ell, OBN);
+  const int splits = static_cast<int>((a.m_pad + kSplitK - 1) / kSplitK);
+  return static_cast<size_t>(kS) * lp * a.m_pad + sizeof(int) * lp + 256 +
+         sizeof(double) * static_cast<size_t>(splits) * a.n * ell;
+}
+
+cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell, double* Z, int64_t ldz, void* work,
+                     cudaStream_t st) {
+  const int64_t lp = roundup(ell, OBN);
+  int8_t* qd = static_cast<int8_t*>(work);
+  int* colexp = reinterpret_cast<int*>(qd + static_cast<size_t>(kS) * lp * a.m_pad);
+  double* ws = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(colexp) + ((sizeof(int) * lp + 255) / 256) * 256);
+  // Q rows carry A's row scale: sum_i A'(i,j) (Q(i,c) 2^e_i)
+  col_exp_kernel<<<static_cast<unsigned>(ell), 256, 0, st>>>(Q, a.m, ldq, a.rowexp, colexp);
+  slice_r_kernel<<<1184, 256, 0, st>>>(Q, a.m, ell, ldq, a.rowexp, colexp, qd, a.m_pad, lp);
+  count_launch(2);
+  const int splits = static_cast<int>((a.m_pad + kSplitK - 1) / kSplitK);
+  OzParams p{};
+  p.C = splits > 1 ? ws : Z;
+  p.ldc = ldz;
+  p.c_row0 = 0;
+  p.rowexp = nullptr;
+  p.colexp = colexp;
+  p.ws_mode = splits > 1 ? 1 : 0;
+  cudaError_t e = launch_digit_gemm(a.tn, a.n_pad, qd, lp, a.m_pad, 0, a.n, ell, splits, p, st);
+  if (e != cudaSuccess || splits == 1) return e;
+  const int64_t total = a.n * ell;
+  reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(
+      ws, a.n, ell, splits, Z, ldz);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace rfgpu

@@ -389,21 +389,78 @@ std::vector<std::pair<int64_t, int64_t>> upload_panels(int64_t m) {
   return out;
 }
 
-int64_t pass1_slots(rfgpu_ctx* c, const rfgpu_matrix* a, int64_t ell) {
-  if (!a->src) return sumsq_slots(c, a->m, ell, a->n);
+// FP64 passes on the INT8 tensor cores (ozaki.cu) for one call: the digit
+// planes of A are built once (inside pass 1) and serve every later pass.
+struct OzPasses {
+  bool on = false;
+  OzakiA a{};
+  DBuf planes, work;
+  Status init(rfgpu_ctx* c, const rfgpu_matrix* m, int64_t ell) {
+    on = !m->f32 && ozaki_enabled(m->m, m->n) && m->m > 0 && m->n > 0;
+    if (!on) return {};
+    const OzakiA lay = ozaki_layout(m->m, m->n);
+    RF_TRY(planes.alloc(ozaki_a_bytes(m->m, m->n), c->stream));
+    RF_TRY(work.alloc(std::max(ozaki_nn_work_bytes(lay, m->m, ell), ozaki_tn_work_bytes(lay, ell)), c->stream));
+    return {};
+  }
+};
+
+int64_t pass1_slots(rfgpu_ctx* c, const rfgpu_matrix* a, int64_t ell, const OzPasses& oz) {
+  auto slots = [&](int64_t rows) { return oz.on ? ozaki_ssq_slots(rows) : sumsq_slots(c, rows, ell, a->n); };
+  if (!a->src) return slots(a->m);
   int64_t s = 0;
-  for (auto& pr : upload_panels(a->m)) s += sumsq_slots(c, pr.second - pr.first, ell, a->n);
+  for (auto& pr : upload_panels(a->m)) s += slots(pr.second - pr.first);
   return s;
+}
+
+// One pass-1 block: rows [r0, r1) of Y = A G (+ ||A||_F^2 partials at ssq).
+Status pass1_rows(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, double* Y, int64_t ldy,
+                  double* ssq, int64_t r0, int64_t r1, OzPasses& oz) {
+  const double* A = static_cast<const double*>(a->dev);
+  if (oz.on) {
+    {
+      Timed t(c, "ozaki_slice");
+      RF_CUDA(ozaki_prepare_a(A, a->m, a->n, a->lda, r0, r1, oz.planes.p, &oz.a, ssq, c->stream));
+    }
+    Timed t(c, "pass_nn");
+    RF_CUDA(ozaki_nn(oz.a, r0, r1, G, a->n, ell, Y, ldy, oz.work.p, c->stream));
+    return {};
+  }
+  return gemm(c, false, r1 - r0, ell, a->n, A + r0, a->lda, G, a->n, Y + r0, ldy, ssq, "pass_nn");
+}
+
+// Y = A X for the later passes (X n x cols).
+Status pass_nn(rfgpu_ctx* c, const rfgpu_matrix* a, const double* X, int64_t cols, double* Y, int64_t ldy,
+               OzPasses* oz) {
+  if (oz && oz->on) {
+    Timed t(c, "pass_nn");
+    RF_CUDA(ozaki_nn(oz->a, 0, a->m, X, a->n, cols, Y, ldy, oz->work.p, c->stream));
+    return {};
+  }
+  return gemm(c, false, a->m, cols, a->n, static_cast<const double*>(a->dev), a->lda, X, a->n, Y, ldy, nullptr,
+              "pass_nn");
+}
+
+// Z = A^T Y (Y m x cols), not summed over ranks.
+Status pass_tn_raw(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Y, int64_t ldy, int64_t cols, double* Z,
+                   OzPasses* oz) {
+  if (oz && oz->on) {
+    Timed t(c, "pass_tn");
+    RF_CUDA(ozaki_tn(oz->a, Y, ldy, cols, Z, a->n, oz->work.p, c->stream));
+    return {};
+  }
+  return gemm(c, true, a->n, cols, a->m, static_cast<const double*>(a->dev), a->lda, Y, ldy, Z, a->n, nullptr,
+              "pass_tn");
 }
 
 // Y = A G with ||A||_F^2 partials fused (pass 1). For a handle whose rows are
 // still on the host, panel i+1's H2D copy runs on the copy stream while panel
 // i's product runs on the compute stream.
 Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, double* Y, int64_t ldy,
-             double* ssq) {
+             double* ssq, OzPasses& oz) {
   const int64_t m = a->m, n = a->n, lda = a->lda;
   const double* A = static_cast<const double*>(a->dev);
-  if (!a->src) return gemm(c, false, m, ell, n, A, lda, G, n, Y, ldy, ssq, "pass_nn");
+  if (!a->src) return pass1_rows(c, a, G, ell, Y, ldy, ssq, 0, m, oz);
   cudaStream_t st = c->stream, cs = c->copy_stream;
   const auto panels = upload_panels(m);
   std::vector<cudaEvent_t> ev(panels.size());
@@ -431,8 +488,8 @@ Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, 
       s = make_err(RFGPU_ECUDA, "pass 1: stream wait failed");
       break;
     }
-    s = gemm(c, false, rows, ell, n, A + r0, lda, G, n, Y + r0, ldy, ssq + off, "pass_nn");
-    off += sumsq_slots(c, rows, ell, n);
+    s = pass1_rows(c, a, G, ell, Y, ldy, ssq + off, r0, r0 + rows, oz);
+    off += oz.on ? ozaki_ssq_slots(rows) : sumsq_slots(c, rows, ell, n);
   }
   a->src = nullptr;  // issued: every later consumer is ordered after the waits above
   cudaEventDestroy(ready);
@@ -534,11 +591,10 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
 
 // Z (n x r) = A^T Q for a (possibly folded) basis: (A^T Q1) R2^{-1}; summed
 // over ranks. tmp: n x r scratch.
-Status pass_tn(rfgpu_ctx* c, const rfgpu_matrix* a, const Basis& b, double* Z, double* tmp) {
-  const int64_t m = a->m, n = a->n;
-  const double* A = static_cast<const double*>(a->dev);
+Status pass_tn(rfgpu_ctx* c, const rfgpu_matrix* a, const Basis& b, double* Z, double* tmp, OzPasses* oz = nullptr) {
+  const int64_t n = a->n;
   double* dst = b.folded ? tmp : Z;
-  RF_TRY(gemm(c, true, n, b.r, m, A, a->lda, b.Q, b.ldq, dst, n, nullptr, "pass_tn"));
+  RF_TRY(pass_tn_raw(c, a, b.Q, b.ldq, b.r, dst, oz));
   RF_TRY(allreduce(c, dst, n * b.r));
   if (b.folded) RF_TRY(gemm(c, false, n, b.r, b.r, tmp, n, b.R2inv, b.r, Z, n, nullptr, nullptr, false, true));
   return {};
@@ -602,14 +658,14 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
                   double* Qbuf, int64_t ldq, double* R2ibuf, double* Bt, RangeOut* out) {
   cudaStream_t st = c->stream;
   const int64_t m = a->m, n = a->n;
-  const double* A = static_cast<const double*>(a->dev);
-  const int64_t lda = a->lda;
   DBuf y, z, w, tmp, ssq, scal;
   RF_TRY(y.alloc(sizeof(double) * std::max<int64_t>(1, ldq * ell), st));
   RF_TRY(z.alloc(sizeof(double) * n * ell, st));
   RF_TRY(w.alloc(sizeof(double) * n * ell, st));
   RF_TRY(tmp.alloc(sizeof(double) * n * ell, st));
-  const int64_t slots = pass1_slots(c, a, ell);
+  OzPasses oz;
+  RF_TRY(oz.init(c, a, ell));
+  const int64_t slots = pass1_slots(c, a, ell, oz);
   RF_TRY(ssq.alloc(sizeof(double) * std::max<int64_t>(1, slots), st));
   RF_TRY(scal.alloc(sizeof(double) * 4, st));
   RF_CUDA(cudaMemsetAsync(ssq.d(), 0, sizeof(double) * std::max<int64_t>(1, slots), st));
@@ -618,21 +674,21 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
   Qb.Q = Qbuf;
   Qb.ldq = ldq;
   // pass 1: Y = A G, with ||A||_F^2 fused (streams a host A in by panels)
-  RF_TRY(pass1(c, a, G, ell, y.d(), ldq, ssq.d()));
+  RF_TRY(pass1(c, a, G, ell, y.d(), ldq, ssq.d(), oz));
   RF_CUDA(sum_array(ssq.d(), slots, scal.d(), st));
   RF_TRY(allreduce(c, scal.d(), 1));
 
   if (!reorth) {
     for (int64_t j = 0; j < q; ++j) {
-      RF_TRY(gemm(c, true, n, ell, m, A, lda, y.d(), ldq, z.d(), n, nullptr, "pass_tn"));
+      RF_TRY(pass_tn_raw(c, a, y.d(), ldq, ell, z.d(), &oz));
       RF_TRY(allreduce(c, z.d(), n * ell));
-      RF_TRY(gemm(c, false, m, ell, n, A, lda, z.d(), n, y.d(), ldq, nullptr, "pass_nn"));
+      RF_TRY(pass_nn(c, a, z.d(), ell, y.d(), ldq, &oz));
     }
     RF_TRY(orth(c, y.d(), m, ell, ldq, &Qb, R2ibuf, nullptr, true, true));
   } else {
     RF_TRY(orth(c, y.d(), m, ell, ldq, &Qb, R2ibuf, nullptr, true, true));
     for (int64_t j = 0; j < q && Qb.r > 0; ++j) {
-      RF_TRY(pass_tn(c, a, Qb, z.d(), tmp.d()));
+      RF_TRY(pass_tn(c, a, Qb, z.d(), tmp.d(), &oz));
       Basis Wb;
       Wb.Q = w.d();
       Wb.ldq = n;
@@ -641,12 +697,12 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
         Qb.r = 0;
         break;
       }
-      RF_TRY(gemm(c, false, m, Wb.r, n, A, lda, w.d(), n, y.d(), ldq, nullptr, "pass_nn"));
+      RF_TRY(pass_nn(c, a, w.d(), Wb.r, y.d(), ldq, &oz));
       RF_TRY(orth(c, y.d(), m, Wb.r, ldq, &Qb, R2ibuf, nullptr, true, true));
     }
   }
   // projection: B^T = A^T Q (finish_with_projection, rangefinder.cpp:24-30)
-  if (Qb.r > 0) RF_TRY(pass_tn(c, a, Qb, Bt, tmp.d()));
+  if (Qb.r > 0) RF_TRY(pass_tn(c, a, Qb, Bt, tmp.d(), &oz));
   RF_CUDA(cudaMemcpyAsync(c->h_d, scal.d(), sizeof(double), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));
   out->a_frob2 = c->h_d[0];

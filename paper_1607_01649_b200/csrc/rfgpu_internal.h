@@ -36,6 +36,32 @@ cudaError_t gemm_f64(bool trans_a, int64_t M, int64_t N, int64_t K, const double
 
 cudaError_t sum_array(const double* x, int64_t n, double* out, cudaStream_t st);
 
+// ---- FP64 passes on the INT8 tensor cores (ozaki.cu) -----------------------
+// Digit planes of A (m x n, FP64) for Y = A X and Z = A^T Q (Ozaki scheme,
+// 8 signed 7-bit digits per operand, tcgen05 kind::i8, FP64 recombination).
+struct OzakiA {
+  int8_t* nn;   // [8][m_pad][n_pad] row-scaled digits, row-major
+  int8_t* tn;   // [8][n_pad][m_pad] the same digits, column-major
+  int* rowexp;  // m_pad row exponents (|A(i,:)| < 2^rowexp[i])
+  int64_t m, n, m_pad, n_pad;
+};
+bool ozaki_enabled(int64_t m, int64_t n);  // RFGPU_OZAKI=0/1 overrides the size rule
+OzakiA ozaki_layout(int64_t m, int64_t n);  // shapes only (no buffers)
+size_t ozaki_a_bytes(int64_t m, int64_t n);
+int64_t ozaki_ssq_slots(int64_t rows);
+// Rows [r0, r1) of A (whole 256-row blocks except at m): row exponents,
+// ||A||_F^2 partials (ozaki_ssq_slots(r1 - r0) of them) and digit planes.
+cudaError_t ozaki_prepare_a(const double* A, int64_t m, int64_t n, int64_t lda, int64_t r0, int64_t r1, void* work,
+                            OzakiA* out, double* ssq_part, cudaStream_t st);
+size_t ozaki_nn_work_bytes(const OzakiA& a, int64_t rows, int64_t ell);
+// Y(r0:r1, 0:ell) = A(r0:r1, :) X  (X n x ell, col-major)
+cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, int64_t ldx, int64_t ell, double* Y,
+                     int64_t ldy, void* work, cudaStream_t st);
+size_t ozaki_tn_work_bytes(const OzakiA& a, int64_t ell);
+// Z (n x ell) = A^T Q  (Q m x ell, col-major)
+cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell, double* Z, int64_t ldz, void* work,
+                     cudaStream_t st);
+
 // ---- small dense kernels (small_f64.cu) ----------------------------------
 // Upper Cholesky R^T R = G (G c x c, symmetric, upper triangle consulted,
 // ld = c) and R^{-1}, both c x c column-major with zeros below the diagonal.
