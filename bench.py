@@ -52,6 +52,8 @@ WORKLOADS = {
 CHUNK = 65536
 SEED = 1
 FP64_PEAK_TFLOPS = 37.1  # DMMA m8n8k4 burst, profiles/r01_fp_peaks.txt (MEASURED_PEAKS.json has no FP64 entry)
+INT8_PEAK_TOPS = 4594.7  # tcgen05 kind::i8 dense burst, tools/microbench/i8peak.cu -> profiles/r01_i8_peak.txt
+OZAKI_PRODUCTS = 36      # int8 digit products per FP64 product (8 digits, groups s + t <= 7; csrc/ozaki.cu)
 
 
 def spectrum(kind, r):
@@ -335,7 +337,7 @@ def main():
     torch.cuda.synchronize()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     launches = ctx.launch_count() // args.steps
-    prof = {nm: ctx.profile_read(nm) for nm in ("pass_nn", "pass_tn", "sketch_nn", "sketch_tn", "orth", "small_svd",
+    prof = {nm: ctx.profile_read(nm) for nm in ("pass_nn", "pass_tn", "ozaki_slice", "sketch_nn", "sketch_tn", "orth", "small_svd",
                                                 "jacobi", "gram", "trsm", "lift", "col_id", "cpqr", "trsm_id",
                                                 "single_pass_core", "gemm_nn", "gemm_tn", "allreduce")}
     ctx.profile(False)
@@ -347,6 +349,7 @@ def main():
     flops_per_pass = 2.0 * mloc * n * ell
     passes_alg = {"rsvd": n_pass / args.steps, "cur": 1.0, "single_pass": 2.0}[kind]
     achieved = flops_per_pass * passes_alg * args.steps / (pass_ms * 1e-3) / 1e12 if pass_ms > 0 else None
+    ozaki = prof["ozaki_slice"][0] > 0  # the FP64 passes ran as int8 digit products on tcgen05
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tr_path):
@@ -413,14 +416,24 @@ def main():
             "data": "synthetic (planted spectrum, seeded torch RNG on device)" + (", A stored fp32" if w.get("f32") else ""),
             "config": config_of(w, world, args),
             "sketch_tflops": achieved,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
-                         "kernel": f"gemm_f64_tma_kernel (passes over A: {' + '.join(pass_names)})",
-                         "per_pass_flops": flops_per_pass, "passes_per_step": passes_alg,
-                         "launches_per_step": n_pass / args.steps,
-                         "pass_ms_avg": pass_ms / n_pass if n_pass else None,
-                         "peak_source": "FP64 DMMA microbenchmark profiles/r01_fp_peaks.txt (no FP64 entry in "
-                                        "MEASURED_PEAKS.json)"},
+            "roofline": ({"bound": "tensor", "achieved": achieved * OZAKI_PRODUCTS, "peak": INT8_PEAK_TOPS,
+                          "unit": "TOPS", "frac": achieved * OZAKI_PRODUCTS / INT8_PEAK_TOPS, "traffic": traffic,
+                          "kernel": f"ozaki_gemm_kernel (tcgen05 kind::i8; passes over A: {' + '.join(pass_names)})",
+                          "algorithmic_ops_per_pass": flops_per_pass * OZAKI_PRODUCTS,
+                          "fp64_equivalent_tflops": achieved, "fp64_dmma_peak_tflops": FP64_PEAK_TFLOPS,
+                          "passes_per_step": passes_alg, "launches_per_step": n_pass / args.steps,
+                          "pass_ms_avg": pass_ms / n_pass if n_pass else None,
+                          "peak_source": "INT8 tcgen05 dense microbenchmark profiles/r01_i8_peak.txt (MEASURED_PEAKS.json "
+                                         "has bf16 only; int8 nominal = 2x bf16)"}
+                         if ozaki and achieved else
+                         {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                          "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
+                          "kernel": f"gemm_f64_tma_kernel (passes over A: {' + '.join(pass_names)})",
+                          "per_pass_flops": flops_per_pass, "passes_per_step": passes_alg,
+                          "launches_per_step": n_pass / args.steps,
+                          "pass_ms_avg": pass_ms / n_pass if n_pass else None,
+                          "peak_source": "FP64 DMMA microbenchmark profiles/r01_fp_peaks.txt (no FP64 entry in "
+                                         "MEASURED_PEAKS.json)"}),
             "phase_ms_per_step": {nm: v[1] / args.steps for nm, v in prof.items()},
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
         }

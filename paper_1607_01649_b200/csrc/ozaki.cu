@@ -24,9 +24,9 @@
 // For A^T Q the row scale of A moves onto Q: sum_i A'(i,j) (Q(i,c) 2^e_i).
 //
 // Layouts:
-//   NN digits of A: [kS][m_pad][n_pad]  (row-major: K = n contiguous)
-//   (64-byte swizzled TMA tiles; both GEMM operands K-major)
-//   TN digits of A: [kS][n_pad][m_pad]  (column-major: K = m contiguous)
+//   digits of A: [kS][n_pad][m_pad] (column-major, like A). Y = A X reads them
+//     M-major (TMA box 128 rows x 64 columns, 128B swizzle), A^T Q K-major
+//     (box 64 rows x 128 columns, 64B swizzle): one copy serves both passes.
 //   thin operand digits: [kS][l_pad][K_pad]
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -96,48 +96,32 @@ __device__ __forceinline__ void digits(double x, int8_t* d) {
   }
 }
 
-// A rows [r0, r1) (64-row blocks) x all n_pad columns (64-column blocks):
-// digits of A(i, j) 2^-e_i into both the NN (row-major) and TN
-// (column-major) layouts; padding rows/columns get zero digits.
+// Digits of A(i, j) 2^-e_i for rows [r0, r1) (r0 a multiple of 4) into the
+// column-major planes [kS][n_pad][m_pad]; padding rows / columns get zero
+// digits. One thread: 4 consecutive rows of one column (32 B read, kS x 4 B
+// written), a warp 128 rows: fully coalesced both ways.
 __global__ void __launch_bounds__(256) slice_a_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
-                                                      int64_t r0, const int* __restrict__ rowexp, int8_t* __restrict__ nn,
+                                                      int64_t r0, int64_t r1, const int* __restrict__ rowexp,
                                                       int8_t* __restrict__ tn, int64_t m_pad, int64_t n_pad) {
-  __shared__ int8_t dg[kS][64][68];  // [s][col][row] (+4 pad)
-  const int64_t i0 = r0 + static_cast<int64_t>(blockIdx.y) * 64, j0 = static_cast<int64_t>(blockIdx.x) * 64;
-  const int tid = threadIdx.x;
-  // each thread: 16 elements (rows rr, col jj), reading A coalesced over rows
-  for (int e = tid; e < 64 * 64; e += 256) {
-    const int rr = e & 63, jj = e >> 6;
-    const int64_t i = i0 + rr, j = j0 + jj;
-    int8_t d[kS];
-    if (i < m && j < n) {
-      const double v = ldexp(A[j * lda + i], -rowexp[i]);
-      digits(v, d);
-    } else {
+  const int64_t quads = (r1 - r0 + 3) / 4;
+  const int64_t total = quads * n_pad;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / quads, i0 = r0 + (e - j * quads) * 4;
+    uint32_t w[kS] = {};
 #pragma unroll
-      for (int s = 0; s < kS; ++s) d[s] = 0;
+    for (int b = 0; b < 4; ++b) {
+      const int64_t i = i0 + b;
+      if (i < m && j < n) {
+        int8_t d[kS];
+        digits(ldexp(A[j * lda + i], -rowexp[i]), d);
+#pragma unroll
+        for (int s = 0; s < kS; ++s) w[s] |= static_cast<uint32_t>(static_cast<uint8_t>(d[s])) << (8 * b);
+      }
     }
 #pragma unroll
-    for (int s = 0; s < kS; ++s) dg[s][jj][rr] = d[s];
-  }
-  __syncthreads();
-  // TN: [s][j][i], contiguous over i: 4 bytes per thread
-  for (int e = tid; e < kS * 64 * 16; e += 256) {
-    const int q = e & 15, jj = (e >> 4) & 63, s = e >> 10;
-    const int64_t j = j0 + jj;
-    if (j < n_pad) {
-      const uint32_t w = *reinterpret_cast<const uint32_t*>(&dg[s][jj][q * 4]);
-      *reinterpret_cast<uint32_t*>(tn + (static_cast<int64_t>(s) * n_pad + j) * m_pad + i0 + q * 4) = w;
-    }
-  }
-  // NN: [s][i][j], contiguous over j
-  for (int e = tid; e < kS * 64 * 16; e += 256) {
-    const int q = e & 15, rr = (e >> 4) & 63, s = e >> 10;
-    const int64_t i = i0 + rr;
-    uint32_t w = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) w |= static_cast<uint32_t>(static_cast<uint8_t>(dg[s][q * 4 + b][rr])) << (8 * b);
-    if (i < m_pad) *reinterpret_cast<uint32_t*>(nn + (static_cast<int64_t>(s) * m_pad + i) * n_pad + j0 + q * 4) = w;
+    for (int s = 0; s < kS; ++s)
+      *reinterpret_cast<uint32_t*>(tn + (static_cast<int64_t>(s) * n_pad + j) * m_pad + i0) = w[s];
   }
 }
 
@@ -208,6 +192,7 @@ struct OzParams {
   const int* rowexp;  // optional 2^e_row output scale (indexed by L row)
   const int* colexp;  // 2^f_col output scale
   int ws_mode;        // 1: C is [split][N_real][M_real]
+  int cl;             // cluster size along N tiles: the A tile is TMA-multicast to all of them
 };
 
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
@@ -218,6 +203,18 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t
       : "memory");
 }
 
+// Same tile into every CTA of the cluster in ctaMask (same smem offsets; each
+// destination's mbarrier at `bar`'s offset receives the bytes).
+__device__ __forceinline__ void tma2d_mc(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1,
+                                         uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, "
+      "{%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+// K-major operand tile: rows of 64 K-bytes, 64B swizzle (8-row atoms, SBO 512 B).
 __device__ __forceinline__ uint64_t umma_desc(const void* p) {
   uint64_t d = 0;
   d |= (static_cast<uint64_t>(smem_u32(p)) >> 4) & 0x3FFF;  // start address
@@ -228,6 +225,21 @@ __device__ __forceinline__ uint64_t umma_desc(const void* p) {
   return d;
 }
 
+// MN-major operand tile: K rows of 128 M-bytes, 128B swizzle (atoms of 8
+// K-rows x 128 B, SBO 1024 B; a single atom along M).
+__device__ __forceinline__ uint64_t umma_desc_mn(const void* p) {
+  uint64_t d = 0;
+  d |= (static_cast<uint64_t>(smem_u32(p)) >> 4) & 0x3FFF;
+  d |= static_cast<uint64_t>((OBK * OBM) >> 4) << 16;        // LBO: next M atom (unused, M = 128)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;               // SBO: 8 K-rows x 128 B
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;                       // SWIZZLE_128B
+  return d;
+}
+
+// L_MN: the L digit planes are read M-major (column-major A digits serving
+// Y = A X), else K-major (A^T Q).
+template <bool L_MN>
 __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmL,
                                                                   const __grid_constant__ CUtensorMap tmR,
                                                                   const OzParams p) {
@@ -252,10 +264,13 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
   const int64_t kb0 = split * p.kb_per_split;
   const int64_t kb1 = min(p.kb_total, kb0 + p.kb_per_split);
   const int nk = static_cast<int>(kb1 - kb0);
+  const int cl = p.cl;
+  const int crank = nt % cl;  // rank in the cluster (clusters span consecutive n-tiles)
+  const uint16_t cmask = static_cast<uint16_t>((1u << cl) - 1u);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], cl);  // every CTA of the cluster must release the (shared) A stage
     }
     mbar_init(done, 1);
     mbar_fence_init();
@@ -266,7 +281,11 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (cl > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
 
@@ -279,13 +298,28 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
       const int kx = static_cast<int>((kb0 + kb) * OBK);
 #pragma unroll
       for (int s = 0; s < kS; ++s) {
-        tma2d(sA + st * ASZ + s * OBM * OBK, &tmL, &full[st], kx, static_cast<int>(s * p.L_rows + lrow0));
+        // A planes round-robin over the cluster, multicast to all of it
+        // K-major L: box {64 K-bytes, 128 rows} at (k, plane row); M-major L
+        // (planes [kS][K_rows][M]): box {128 M-bytes, 64 K-rows} at (m, plane k)
+        const int lc0 = L_MN ? static_cast<int>(lrow0) : kx;
+        const int lc1 = L_MN ? static_cast<int>(s * p.L_rows + (kb0 + kb) * OBK) : static_cast<int>(s * p.L_rows + lrow0);
+        if (cl == 1)
+          tma2d(sA + st * ASZ + s * OBM * OBK, &tmL, &full[st], lc0, lc1);
+        else if (s % cl == crank)
+          tma2d_mc(sA + st * ASZ + s * OBM * OBK, &tmL, &full[st], lc0, lc1, cmask);
         tma2d(sB + st * BSZ + s * OBN * OBK, &tmR, &full[st], kx, static_cast<int>(s * p.R_rows + ncol0));
       }
     }
   } else if (warp == 1 && lane == 0) {
-    constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(OBN >> 3) << 17) |
-                               (static_cast<uint32_t>(OBM >> 4) << 24);
+    // For a fixed A digit s the groups g = s + t of consecutive t are
+    // consecutive 64-column TMEM blocks, and the B digit planes are
+    // consecutive 64-row blocks in shared memory: one MMA with N = 64 x (up to
+    // 4 digits of B) covers them. 12 MMAs per K step instead of 36, each A
+    // tile read from shared memory once per 4 B digits.
+    auto idesc_n = [](int n) {
+      return (2u << 4) | (1u << 7) | (1u << 10) | (L_MN ? (1u << 15) : 0u) | (static_cast<uint32_t>(n >> 3) << 17) |
+             (static_cast<uint32_t>(OBM >> 4) << 24);
+    };
     for (int kb = 0; kb < nk; ++kb) {
       const int st = kb % kStages;
       const uint32_t ph = (kb / kStages) & 1;
@@ -296,21 +330,31 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
 #pragma unroll
         for (int s = 0; s < kS; ++s) {
 #pragma unroll
-          for (int t = 0; t + s < kS; ++t) {
-            const uint64_t da = umma_desc(sA + st * ASZ + s * OBM * OBK + kk * 32);
-            const uint64_t db = umma_desc(sB + st * BSZ + t * OBN * OBK + kk * 32);
-            // group g = s + t starts at (s = 0) of the first K step
+          for (int t0 = 0; t0 < kS - s; t0 += 4) {
+            const int cnt = (kS - s - t0) < 4 ? (kS - s - t0) : 4;
+            // M-major: K advances by 32 K-rows = 4 swizzle atoms
+            const uint64_t da = L_MN ? umma_desc_mn(sA + st * ASZ + s * OBM * OBK + kk * 32 * OBM)
+                                     : umma_desc(sA + st * ASZ + s * OBM * OBK + kk * 32);
+            const uint64_t db = umma_desc(sB + st * BSZ + t0 * OBN * OBK + kk * 32);
+            // groups s + t0 .. s + t0 + cnt - 1; every group is first written by s = 0
             const uint32_t accum = (kb == 0 && kk == 0 && s == 0) ? 0u : 1u;
             asm volatile(
                 "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (s + t) * OBN),
-                "l"(da), "l"(db), "r"(idesc), "r"(accum));
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (s + t0) * OBN),
+                "l"(da), "l"(db), "r"(idesc_n(OBN * cnt)), "r"(accum));
           }
         }
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(&empty[st]))
-                   : "memory");
+      if (cl == 1)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&empty[st]))
+                     : "memory");
+      else  // release this stage in every CTA of the cluster
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(&empty[st])),
+            "h"(cmask)
+            : "memory");
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(done))
                  : "memory");
@@ -358,7 +402,11 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  // no CTA may leave while cluster peers can still write into its shared memory
+  if (cl > 1)
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  else
+    __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
@@ -388,31 +436,41 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
-// int8 digit planes: rows x K bytes (row-major), box 64 B x box_rows.
-bool digit_tmap(CUtensorMap* tm, const int8_t* base, int64_t rows, int64_t K, int box_rows) {
+// int8 digit planes: rows x inner bytes (row-major); box {box_inner, box_rows}.
+bool digit_tmap(CUtensorMap* tm, const int8_t* base, int64_t rows, int64_t inner, int box_inner, int box_rows,
+                CUtensorMapSwizzle sw) {
   auto fn = tmap_encoder();
   if (!fn) return false;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(K)};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(OBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t es[2] = {1, 1};
   return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-cudaError_t launch_digit_gemm(const int8_t* L, int64_t L_rows, const int8_t* R, int64_t R_rows, int64_t K_pad,
-                              int64_t row0, int64_t rows, int64_t N_real, int splits, const OzParams& base,
-                              cudaStream_t st) {
+// multicast: share each A tile across the CTAs of its N tiles (cluster).
+// Measured at config 3: it pays for the split-K A^T Q pass (31.1 vs 39.1 ms)
+// and costs the NN pass (30.3 vs 25.3 ms: four CTAs in lock step through a
+// 2-stage ring), so the caller chooses.
+// L_mn: L planes are [kS][K_pad][L_M] (M contiguous, L_rows = K_pad rows per
+// plane, L_M = M extent), else [kS][L_rows][K_pad].
+cudaError_t launch_digit_gemm(const int8_t* L, int64_t L_rows, bool L_mn, int64_t L_M, const int8_t* R, int64_t R_rows,
+                              int64_t K_pad, int64_t row0, int64_t rows, int64_t N_real, int splits,
+                              const OzParams& base, bool multicast, cudaStream_t st) {
   static bool cfg = false;
   if (!cfg) {
-    cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemBytes));
-    if (e != cudaSuccess) return e;
+    for (auto fn : {ozaki_gemm_kernel<true>, ozaki_gemm_kernel<false>}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+      if (e != cudaSuccess) return e;
+    }
     cfg = true;
   }
   CUtensorMap tl, tr;
-  if (!digit_tmap(&tl, L, kS * L_rows, K_pad, OBM) || !digit_tmap(&tr, R, kS * R_rows, K_pad, OBN))
+  const bool okl = L_mn ? digit_tmap(&tl, L, kS * L_rows, L_M, OBM, OBK, CU_TENSOR_MAP_SWIZZLE_128B)
+                        : digit_tmap(&tl, L, kS * L_rows, K_pad, OBK, OBM, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (!okl || !digit_tmap(&tr, R, kS * R_rows, K_pad, OBK, OBN, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
   OzParams p = base;
   p.L_rows = L_rows;
@@ -427,8 +485,29 @@ cudaError_t launch_digit_gemm(const int8_t* L, int64_t L_rows, const int8_t* R, 
   p.N_real = N_real;
   const int64_t grid = static_cast<int64_t>(p.ntn) * p.mtn * splits;
   if (grid <= 0) return cudaSuccess;
-  ozaki_gemm_kernel<<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(tl, tr, p);
+  p.cl = 1;
+  if (multicast)
+    for (int c : {8, 7, 6, 5, 4, 3, 2})
+      if (p.ntn % c == 0) {
+        p.cl = c;
+        break;
+      }
+  cudaLaunchConfig_t cfgl{};
+  cfgl.gridDim = dim3(static_cast<unsigned>(grid));
+  cfgl.blockDim = dim3(kThreads);
+  cfgl.dynamicSmemBytes = kSmemBytes;
+  cfgl.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(p.cl);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfgl.attrs = attr;
+  cfgl.numAttrs = 1;
+  cudaError_t e = L_mn ? cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<true>, tl, tr, p)
+                       : cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<false>, tl, tr, p);
   count_launch();
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -452,7 +531,7 @@ OzakiA ozaki_layout(int64_t m, int64_t n) {
 
 size_t ozaki_a_bytes(int64_t m, int64_t n) {
   const OzakiA a = ozaki_layout(m, n);
-  return 2 * static_cast<size_t>(kS) * a.m_pad * a.n_pad + sizeof(int) * a.m_pad + 256;
+  return static_cast<size_t>(kS) * a.m_pad * a.n_pad + sizeof(int) * a.m_pad + 256;
 }
 
 int64_t ozaki_ssq_slots(int64_t rows) { return (rows + 255) / 256; }
@@ -460,27 +539,23 @@ int64_t ozaki_ssq_slots(int64_t rows) { return (rows + 255) / 256; }
 cudaError_t ozaki_prepare_a(const double* A, int64_t m, int64_t n, int64_t lda, int64_t r0, int64_t r1, void* work,
                             OzakiA* out, double* ssq_part, cudaStream_t st) {
   *out = ozaki_layout(m, n);
-  int8_t* base = static_cast<int8_t*>(work);
-  out->nn = base;
-  out->tn = base + static_cast<size_t>(kS) * out->m_pad * out->n_pad;
+  out->tn = static_cast<int8_t*>(work);
   out->rowexp = reinterpret_cast<int*>(out->tn + static_cast<size_t>(kS) * out->m_pad * out->n_pad);
-  if (r0 == 0 && r1 == m) {
-    // padding rows: exponent 0 (their digits are zero)
-    if (out->m_pad > m) {
-      cudaError_t e = cudaMemsetAsync(out->rowexp + m, 0, sizeof(int) * (out->m_pad - m), st);
-      if (e != cudaSuccess) return e;
-    }
+  if (r1 == m && out->m_pad > m) {  // padding rows: exponent 0 (their digits are zero)
+    cudaError_t e = cudaMemsetAsync(out->rowexp + m, 0, sizeof(int) * (out->m_pad - m), st);
+    if (e != cudaSuccess) return e;
   }
   const int64_t rows = r1 - r0;
   if (rows > 0) {
     row_stats_kernel<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, st>>>(A, r0, r1, n, lda, out->rowexp, ssq_part);
     count_launch();
   }
-  // slice 64-row blocks covering [r0, r1) (the last panel also covers the padding rows)
-  const int64_t b0 = r0 / 64, b1 = (r1 == m ? out->m_pad : r1) / 64;
-  if (b1 > b0) {
-    dim3 grid(static_cast<unsigned>(out->n_pad / 64), static_cast<unsigned>(b1 - b0));
-    slice_a_kernel<<<grid, 256, 0, st>>>(A, m, n, lda, b0 * 64, out->rowexp, out->nn, out->tn, out->m_pad, out->n_pad);
+  // rows [r0, r1) (the last panel also covers the padding rows up to m_pad)
+  const int64_t s1 = r1 == m ? out->m_pad : r1;
+  if (s1 > r0) {
+    const int64_t work_items = (s1 - r0 + 3) / 4 * out->n_pad;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((work_items + 255) / 256, 148 * 32));
+    slice_a_kernel<<<blocks, 256, 0, st>>>(A, m, n, lda, r0, s1, out->rowexp, out->tn, out->m_pad, out->n_pad);
     count_launch();
   }
   return cudaGetLastError();
@@ -511,7 +586,7 @@ cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, i
   p.rowexp = a.rowexp;
   p.colexp = colexp;
   p.ws_mode = splits > 1 ? 1 : 0;
-  cudaError_t e = launch_digit_gemm(a.nn, a.m_pad, xd, lp, a.n_pad, r0, rows, ell, splits, p, st);
+  cudaError_t e = launch_digit_gemm(a.tn, a.n_pad, true, a.m_pad, xd, lp, a.n_pad, r0, rows, ell, splits, p, false, st);
   if (e != cudaSuccess || splits == 1) return e;
   const int64_t total = rows * ell;
   reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(
@@ -545,7 +620,7 @@ cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell,
   p.rowexp = nullptr;
   p.colexp = colexp;
   p.ws_mode = splits > 1 ? 1 : 0;
-  cudaError_t e = launch_digit_gemm(a.tn, a.n_pad, qd, lp, a.m_pad, 0, a.n, ell, splits, p, st);
+  cudaError_t e = launch_digit_gemm(a.tn, a.n_pad, false, 0, qd, lp, a.m_pad, 0, a.n, ell, splits, p, true, st);
   if (e != cudaSuccess || splits == 1) return e;
   const int64_t total = a.n * ell;
   reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(

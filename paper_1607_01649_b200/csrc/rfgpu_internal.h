@@ -40,8 +40,7 @@ cudaError_t sum_array(const double* x, int64_t n, double* out, cudaStream_t st);
 // Digit planes of A (m x n, FP64) for Y = A X and Z = A^T Q (Ozaki scheme,
 // 8 signed 7-bit digits per operand, tcgen05 kind::i8, FP64 recombination).
 struct OzakiA {
-  int8_t* nn;   // [8][m_pad][n_pad] row-scaled digits, row-major
-  int8_t* tn;   // [8][n_pad][m_pad] the same digits, column-major
+  int8_t* tn;   // [8][n_pad][m_pad] row-scaled digits, column-major (read M-major by Y = A X, K-major by A^T Q)
   int* rowexp;  // m_pad row exponents (|A(i,:)| < 2^rowexp[i])
   int64_t m, n, m_pad, n_pad;
 };
