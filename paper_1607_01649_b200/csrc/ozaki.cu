@@ -1,27 +1,27 @@
 // FP64 passes over A on the INT8 tensor cores (tcgen05.mma kind::i8, TMEM
-// accumulators): Ozaki-scheme splitting of both operands into kS = 8 signed
-// 7-bit digits, exact int32 digit products on the tensor cores, recombined in
+// accumulators): Ozaki-scheme splitting of both operands into kS = 7 signed
+// 8-bit digits, exact int32 digit products on the tensor cores, recombined in
 // FP64 in the epilogue.
 //
 // Why: B200's FP64 pipe (DMMA) peaks at 37 TF/s, its INT8 tensor cores at
-// 4.5 POPS. A pass over A (Y = A X, Z = A^T Q: proj/src/dense.cpp:102-126 on
-// the reference's hot path, rangefinder.cpp:68-78, lowrank.cpp:92) needs
-// 2 m n l flops; as 36 int8 digit products it still runs ~2x faster than
-// DMMA (tools/microbench/ozk.cu).
+// 4.6 POPS (profiles/r01_i8_peak.txt). A pass over A (Y = A X, Z = A^T Q:
+// proj/src/dense.cpp:102-126 on the reference's hot path,
+// rangefinder.cpp:68-78, lowrank.cpp:92) needs 2 m n l flops; as 28 int8
+// digit products it runs ~2x faster than DMMA can.
 //
-// Numerics. Row i of A is scaled by 2^-e_i (|A(i,:)| < 2^e_i, exact), every
-// column c of the thin operand by 2^-f_c; a scaled value x in (-1, 1) is
-// x = sum_{s<8} d_s 128^-(s+1) + r, d_s = trunc(128 * remainder) in
-// [-127, 127], |r| < 2^-56 (each step exact in FP64). The product keeps the
-// digit pairs with s + t <= 7 (36 of 64), grouped by g = s + t into 8 int32
-// TMEM accumulators (8 x 64 columns = all 512; exact: 8 * K * 127^2 < 2^31
-// for K <= 16384, the split size), and sums sum_g 2^-7(g+2) acc_g in FP64
-// (one rounding per group), then scales by 2^(e_i + f_c). Per term the
-// result is within ~10 * 2^-56 = 1.4e-16 of the exact product, relative to
-// max|A(i,:)| max|X(:,c)|: FP64-class (7 digits, 28 products, measured
-// 2e-13 on rsvd singular values, was too coarse for the reference's
-// down-dated residual on exact-rank inputs).
-// For A^T Q the row scale of A moves onto Q: sum_i A'(i,j) (Q(i,c) 2^e_i).
+// Numerics. Row i of A is scaled by 2^-e_i (|A(i,:)| < 2^e_i) for A X, column
+// j by 2^-f_j for A^T Q, every column c of the thin operand by 2^-g_c. A
+// scaled value x in (-1, 1) becomes the integer X = trunc(x 2^54) (exact
+// exponent arithmetic + one truncating conversion), written in balanced
+// base 256: X = sum_{k<7} d_k 256^k with d_k in [-128, 127] (add 0x80 to
+// every byte of X, read the bytes back minus 0x80 — no carry chain). Digit
+// plane s holds d_{6-s}. The product keeps the digit pairs with s + t <= 6
+// (28 of 49), grouped by g = s + t into 7 int32 TMEM accumulators (exact:
+// 7 * K * 128^2 < 2^31 for K <= 16384, the split size), and sums
+// sum_g 2^-(12+8g) acc_g in FP64 (one rounding per group), then scales by
+// 2^(e + g_c). Per term the result is within ~8 * 2^-54 of the exact product
+// relative to max|row| max|column| — FP64-class (measured below 1e-14 of the
+// extended-precision product in tests/test_gpu_ozaki.py).
 //
 // Layouts:
 //   digits of A: [kS][n_pad][m_pad] (column-major, like A). Y = A X reads them
@@ -42,12 +42,12 @@
 namespace rfgpu {
 namespace {
 
-constexpr int kS = 8;          // digits per operand
+constexpr int kS = 7;          // balanced base-256 digits per operand
 constexpr int OBM = 128;       // tile rows (TMEM lanes)
 constexpr int OBN = 64;        // tile columns per accumulator group
 constexpr int OBK = 64;        // K bytes per pipeline stage (64B swizzle)
 constexpr int kStages = 2;
-constexpr int kTmemCols = 512;  // kS * OBN
+constexpr int kTmemCols = 512;  // kS * OBN = 448 -> 512
 constexpr int64_t kSplitK = 16384;
 constexpr int kThreads = 192;   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
 constexpr size_t kStageBytes = static_cast<size_t>(kS) * (OBM + OBN) * OBK;
@@ -59,69 +59,185 @@ __host__ __device__ inline int64_t roundup(int64_t x, int64_t a) { return (x + a
 // Exponent e with |v| < 2^e for v = max |.| (0 for an all-zero vector).
 __device__ __forceinline__ int bound_exp(double mx) { return mx > 0.0 ? ilogb(mx) + 1 : 0; }
 
-// Row exponents of A rows [r0, r1) and sum-of-squares partials (one per CTA).
-__global__ void row_stats_kernel(const double* __restrict__ A, int64_t r0, int64_t r1, int64_t n, int64_t lda,
-                                 int* __restrict__ rowexp, double* __restrict__ ssq_part) {
+// High word of |v|: ordered like |v| to within the top 20 mantissa bits, so
+// its maximum carries the exponent of the maximum.
+__device__ __forceinline__ uint32_t abs_hi(double v) {
+  return static_cast<uint32_t>(static_cast<unsigned long long>(__double_as_longlong(fabs(v))) >> 32);
+}
+// Exponent e with |v| < 2^e from a high word (0 for zero).
+__device__ __forceinline__ int hi_exp(uint32_t h) {
+  const int E = static_cast<int>((h >> 20) & 0x7FF);
+  return h == 0 ? 0 : (E == 0 ? -1021 : E - 1022);
+}
+
+// Rows [r0, r1) (r0 a multiple of 256): row exponents, ||A||_F^2 partials
+// (one per CTA) and per-CTA column maxima (high words) colpart[blk][j],
+// blk = (row0 / 256) + blockIdx.x. One thread per row, columns in chunks of
+// 256: warp maxima by redux, CTA maxima through shared memory.
+__global__ void __launch_bounds__(256) stats_kernel(const double* __restrict__ A, int64_t r0, int64_t r1, int64_t n,
+                                                    int64_t lda, int64_t n_pad, int* __restrict__ rowexp,
+                                                    uint32_t* __restrict__ colpart, double* __restrict__ ssq_part) {
   __shared__ double red[32];
+  __shared__ uint32_t wmax[8][257];
   const int64_t i = r0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  double mx = 0.0, s0 = 0.0, s1 = 0.0;
-  if (i < r1) {
-    const double* a = A + i;
-    int64_t j = 0;
-    for (; j + 2 <= n; j += 2) {
-      const double v0 = a[j * lda], v1 = a[(j + 1) * lda];
-      mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
-      s0 = fma(v0, v0, s0);
-      s1 = fma(v1, v1, s1);
+  const bool ok = i < r1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t blk = r0 / 256 + blockIdx.x;
+  uint32_t rmax = 0;
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t j0 = 0; j0 < n; j0 += 256) {
+    const int jn = static_cast<int>(lmin(256, n - j0));
+    int jj = 0;
+    for (; jj + 4 <= jn; jj += 4) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = ok ? A[(j0 + jj + u) * lda + i] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t h = abs_hi(v[u]);
+        rmax = max(rmax, h);
+        if (u & 1) s1 = fma(v[u], v[u], s1);
+        else s0 = fma(v[u], v[u], s0);
+        const uint32_t w = __reduce_max_sync(0xffffffffu, h);
+        if (lane == 0) wmax[warp][jj + u] = w;
+      }
     }
-    for (; j < n; ++j) {
-      const double v = a[j * lda];
-      mx = fmax(mx, fabs(v));
+    for (; jj < jn; ++jj) {
+      const double v = ok ? A[(j0 + jj) * lda + i] : 0.0;
+      const uint32_t h = abs_hi(v);
+      rmax = max(rmax, h);
       s0 = fma(v, v, s0);
+      const uint32_t w = __reduce_max_sync(0xffffffffu, h);
+      if (lane == 0) wmax[warp][jj] = w;
     }
-    rowexp[i] = bound_exp(mx);
+    __syncthreads();
+    if (threadIdx.x < jn) {
+      uint32_t mx = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) mx = max(mx, wmax[w][threadIdx.x]);
+      colpart[blk * n_pad + j0 + threadIdx.x] = mx;
+    }
+    __syncthreads();
   }
+  if (ok) rowexp[i] = hi_exp(rmax);
   const double s = block_sum(s0 + s1, red);
   if (threadIdx.x == 0 && ssq_part) ssq_part[blockIdx.x] = s;
 }
 
-// Digits of x in (-1, 1): d[s] = trunc(128 * rem).
-__device__ __forceinline__ void digits(double x, int8_t* d) {
-#pragma unroll
-  for (int s = 0; s < kS; ++s) {
-    x *= 128.0;
-    const double t = trunc(x);
-    d[s] = static_cast<int8_t>(static_cast<int>(t));
-    x -= t;
+// Column exponents from the per-CTA column maxima.
+__global__ void colexp_kernel(const uint32_t* __restrict__ colpart, int64_t nblk, int64_t n, int64_t n_pad,
+                              int* __restrict__ colexp) {
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n_pad;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t mx = 0;
+    if (j < n)
+      for (int64_t b = 0; b < nblk; ++b) mx = max(mx, colpart[b * n_pad + j]);
+    colexp[j] = hi_exp(mx);
   }
 }
 
-// Digits of A(i, j) 2^-e_i for rows [r0, r1) (r0 a multiple of 4) into the
-// column-major planes [kS][n_pad][m_pad]; padding rows / columns get zero
-// digits. One thread: 4 consecutive rows of one column (32 B read, kS x 4 B
-// written), a warp 128 rows: fully coalesced both ways.
+// X' = trunc(v 2^(54-e)) + 0x0080808080808080 for |v| < 2^e: byte k of X',
+// minus 0x80, is the balanced base-256 digit d_k of trunc(v 2^(54-e)).
+// Built from v's bits (new exponent E + 54 - e, then a truncating
+// conversion); zero, subnormal and negligible (< 2^-54 relative) inputs give
+// all-zero digits (X' bytes 0x80).
+__device__ __forceinline__ uint64_t balanced7(double v, int e) {
+  const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v));
+  const int E = static_cast<int>((bits >> 52) & 0x7FF);
+  const int En = E + 54 - e;
+  int64_t X = 0;
+  if (E != 0 && En > 0)
+    X = static_cast<int64_t>(__longlong_as_double(static_cast<long long>((bits & ~(uint64_t(0x7FF) << 52)) |
+                                                                          (static_cast<uint64_t>(En) << 52))));
+  return static_cast<uint64_t>(X) + 0x0080808080808080ull;
+}
+
+// Digits of A for rows [r0, r1) (r0 a multiple of 4), column-major planes
+// [kS][n_pad][m_pad]: rs <- A(i,j) 2^-e_i (row exponents, for A X), cs <-
+// A(i,j) 2^-f_j (column exponents, for A^T Q); either may be null. Padding
+// rows / columns get zero digits. One thread: 4 consecutive rows of one
+// column (32 B read, 4 B per plane written), a warp 128 rows: coalesced.
+// Four elements' packed digits (p[b] = digits of element b) -> per-digit words
+// (word s = digit s of elements 0..3 in bytes 0..3): a 4x4 byte transpose.
+__device__ __forceinline__ void transpose4(const uint32_t* p, uint32_t* w) {
+  const uint32_t a = __byte_perm(p[0], p[1], 0x5140), b = __byte_perm(p[0], p[1], 0x7362);
+  const uint32_t c = __byte_perm(p[2], p[3], 0x5140), d = __byte_perm(p[2], p[3], 0x7362);
+  w[0] = __byte_perm(a, c, 0x5410);
+  w[1] = __byte_perm(a, c, 0x7632);
+  w[2] = __byte_perm(b, d, 0x5410);
+  w[3] = __byte_perm(b, d, 0x7632);
+}
+
 __global__ void __launch_bounds__(256) slice_a_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
                                                       int64_t r0, int64_t r1, const int* __restrict__ rowexp,
-                                                      int8_t* __restrict__ tn, int64_t m_pad, int64_t n_pad) {
+                                                      const int* __restrict__ colexp, int8_t* __restrict__ rs,
+                                                      int8_t* __restrict__ cs, int64_t m_pad, int64_t n_pad) {
   const int64_t quads = (r1 - r0 + 3) / 4;
   const int64_t total = quads * n_pad;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t j = e / quads, i0 = r0 + (e - j * quads) * 4;
-    uint32_t w[kS] = {};
+    uint32_t wr[kS] = {}, wc[kS] = {};
+    if (j < n) {
+      const int fj = cs ? colexp[j] : 0;
+      double v[4];
+      int er[4];
+      if (i0 + 3 < m && ((j * lda + i0) & 1) == 0) {
+        const double2 p0 = *reinterpret_cast<const double2*>(A + j * lda + i0);
+        const double2 p1 = *reinterpret_cast<const double2*>(A + j * lda + i0 + 2);
+        v[0] = p0.x, v[1] = p0.y, v[2] = p1.x, v[3] = p1.y;
+        if (rs) {
+          const int4 q = *reinterpret_cast<const int4*>(rowexp + i0);
+          er[0] = q.x, er[1] = q.y, er[2] = q.z, er[3] = q.w;
+        }
+      } else {
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int64_t i = i0 + b;
-      if (i < m && j < n) {
-        int8_t d[kS];
-        digits(ldexp(A[j * lda + i], -rowexp[i]), d);
-#pragma unroll
-        for (int s = 0; s < kS; ++s) w[s] |= static_cast<uint32_t>(static_cast<uint8_t>(d[s])) << (8 * b);
+        for (int b = 0; b < 4; ++b) {
+          const bool in = i0 + b < m;
+          v[b] = in ? A[j * lda + i0 + b] : 0.0;
+          er[b] = (in && rs) ? rowexp[i0 + b] : 0;
+        }
       }
-    }
+      // words of X' per element: lo = bytes 0-3, hi = bytes 4-6 (+0)
+      uint32_t hr[4], lr[4], hc[4], lc[4];
 #pragma unroll
-    for (int s = 0; s < kS; ++s)
-      *reinterpret_cast<uint32_t*>(tn + (static_cast<int64_t>(s) * n_pad + j) * m_pad + i0) = w[s];
+      for (int b = 0; b < 4; ++b) {
+        if (rs) {
+          const uint64_t x = balanced7(v[b], er[b]);
+          lr[b] = static_cast<uint32_t>(x) ^ 0x80808080u;
+          hr[b] = static_cast<uint32_t>(x >> 32) ^ 0x80808080u;
+        }
+        if (cs) {
+          const uint64_t x = balanced7(v[b], fj);
+          lc[b] = static_cast<uint32_t>(x) ^ 0x80808080u;
+          hc[b] = static_cast<uint32_t>(x >> 32) ^ 0x80808080u;
+        }
+      }
+      // transpose: t[k] = byte k of the four elements; plane s = byte 6 - s
+      if (rs) {
+        uint32_t t[8];
+        transpose4(lr, t);
+        transpose4(hr, t + 4);
+#pragma unroll
+        for (int q = 0; q < kS; ++q) wr[q] = t[6 - q];
+      }
+      if (cs) {
+        uint32_t t[8];
+        transpose4(lc, t);
+        transpose4(hc, t + 4);
+#pragma unroll
+        for (int q = 0; q < kS; ++q) wc[q] = t[6 - q];
+      }
+    } else {
+      // padding columns: zero digits
+    }
+    const int64_t off = j * m_pad + i0;
+#pragma unroll
+    for (int s = 0; s < kS; ++s) {
+      const int64_t o = static_cast<int64_t>(s) * n_pad * m_pad + off;
+      if (rs) *reinterpret_cast<uint32_t*>(rs + o) = wr[s];
+      if (cs) *reinterpret_cast<uint32_t*>(cs + o) = wc[s];
+    }
   }
 }
 
@@ -148,32 +264,29 @@ __global__ void col_exp_kernel(const double* __restrict__ R, int64_t K, int64_t 
   }
 }
 
-// Digits of R(i,c) 2^(e_i - f_c) into [kS][N_pad][K_pad] (4 rows per thread).
+// Digits of R(i,c) 2^-f_c into [kS][N_pad][K_pad] (4 rows per thread).
 __global__ void slice_r_kernel(const double* __restrict__ R, int64_t K, int64_t N, int64_t ldr,
-                               const int* __restrict__ rowexp, const int* __restrict__ colexp, int8_t* __restrict__ out,
-                               int64_t K_pad, int64_t N_pad) {
+                               const int* __restrict__ colexp, int8_t* __restrict__ out, int64_t K_pad, int64_t N_pad) {
   const int64_t quads = K_pad / 4;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < quads * N_pad;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t c = e / quads, i0 = (e - c * quads) * 4;
-    uint32_t w[kS] = {};
+    uint32_t lo[4], hi[4];
+    const int fc = c < N ? colexp[c] : 0;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int64_t i = i0 + b;
-      int8_t d[kS];
-      if (i < K && c < N) {
-        const double v = ldexp(R[c * ldr + i], (rowexp ? rowexp[i] : 0) - colexp[c]);
-        digits(v, d);
-      } else {
-#pragma unroll
-        for (int s = 0; s < kS; ++s) d[s] = 0;
-      }
-#pragma unroll
-      for (int s = 0; s < kS; ++s) w[s] |= static_cast<uint32_t>(static_cast<uint8_t>(d[s])) << (8 * b);
+      const double v = (i < K && c < N) ? R[c * ldr + i] : 0.0;
+      const uint64_t x = balanced7(v, fc);
+      lo[b] = static_cast<uint32_t>(x) ^ 0x80808080u;
+      hi[b] = static_cast<uint32_t>(x >> 32) ^ 0x80808080u;
     }
+    uint32_t t[8];
+    transpose4(lo, t);
+    transpose4(hi, t + 4);
 #pragma unroll
     for (int s = 0; s < kS; ++s)
-      *reinterpret_cast<uint32_t*>(out + (static_cast<int64_t>(s) * N_pad + c) * K_pad + i0) = w[s];
+      *reinterpret_cast<uint32_t*>(out + (static_cast<int64_t>(s) * N_pad + c) * K_pad + i0) = t[6 - s];
   }
 }
 
@@ -381,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
               : "r"(ta));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          const double sc = ldexp(1.0, -7 * (g + 2));
+          const double sc = ldexp(1.0, -12 - 8 * g);
 #pragma unroll
           for (int j = 0; j < 16; ++j) acc[j] = fma(static_cast<double>(static_cast<int32_t>(r[j])), sc, acc[j]);
         }
@@ -524,40 +637,62 @@ OzakiA ozaki_layout(int64_t m, int64_t n) {
   OzakiA a{};
   a.m = m;
   a.n = n;
-  a.m_pad = roundup(std::max<int64_t>(m, 1), OBM);
+  a.m_pad = roundup(std::max<int64_t>(m, 1), 256);
   a.n_pad = roundup(std::max<int64_t>(n, 1), OBM);
   return a;
 }
 
 size_t ozaki_a_bytes(int64_t m, int64_t n) {
   const OzakiA a = ozaki_layout(m, n);
-  return static_cast<size_t>(kS) * a.m_pad * a.n_pad + sizeof(int) * a.m_pad + 256;
+  const size_t planes = static_cast<size_t>(kS) * a.m_pad * a.n_pad;
+  return 2 * planes + sizeof(int) * (a.m_pad + a.n_pad) + sizeof(uint32_t) * (a.m_pad / 256) * a.n_pad + 1024;
 }
 
 int64_t ozaki_ssq_slots(int64_t rows) { return (rows + 255) / 256; }
 
-cudaError_t ozaki_prepare_a(const double* A, int64_t m, int64_t n, int64_t lda, int64_t r0, int64_t r1, void* work,
-                            OzakiA* out, double* ssq_part, cudaStream_t st) {
+void ozaki_bind(void* work, int64_t m, int64_t n, OzakiA* out) {
   *out = ozaki_layout(m, n);
-  out->tn = static_cast<int8_t*>(work);
-  out->rowexp = reinterpret_cast<int*>(out->tn + static_cast<size_t>(kS) * out->m_pad * out->n_pad);
-  if (r1 == m && out->m_pad > m) {  // padding rows: exponent 0 (their digits are zero)
-    cudaError_t e = cudaMemsetAsync(out->rowexp + m, 0, sizeof(int) * (out->m_pad - m), st);
+  const size_t planes = static_cast<size_t>(kS) * out->m_pad * out->n_pad;
+  int8_t* base = static_cast<int8_t*>(work);
+  out->rs = base;
+  out->cs = base + planes;
+  out->rowexp = reinterpret_cast<int*>(base + 2 * planes);
+  out->colexp = out->rowexp + out->m_pad;
+  out->colpart = reinterpret_cast<uint32_t*>(out->colexp + out->n_pad);
+}
+
+cudaError_t ozaki_prepare_rows(const double* A, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
+                               double* ssq_part, bool slice_rows, cudaStream_t st) {
+  if (r1 == a.m && a.m_pad > a.m) {  // padding rows: exponent 0, zero column maxima
+    cudaError_t e = cudaMemsetAsync(a.rowexp + a.m, 0, sizeof(int) * (a.m_pad - a.m), st);
     if (e != cudaSuccess) return e;
   }
   const int64_t rows = r1 - r0;
+  const int64_t blocks = (rows + 255) / 256;
   if (rows > 0) {
-    row_stats_kernel<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, st>>>(A, r0, r1, n, lda, out->rowexp, ssq_part);
+    stats_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(A, r0, r1, a.n, lda, a.n_pad, a.rowexp, a.colpart,
+                                                               ssq_part);
     count_launch();
   }
-  // rows [r0, r1) (the last panel also covers the padding rows up to m_pad)
-  const int64_t s1 = r1 == m ? out->m_pad : r1;
-  if (s1 > r0) {
-    const int64_t work_items = (s1 - r0 + 3) / 4 * out->n_pad;
-    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((work_items + 255) / 256, 148 * 32));
-    slice_a_kernel<<<blocks, 256, 0, st>>>(A, m, n, lda, r0, s1, out->rowexp, out->tn, out->m_pad, out->n_pad);
-    count_launch();
+  if (slice_rows) {
+    const int64_t s1 = r1 == a.m ? a.m_pad : r1;
+    const int64_t items = (s1 - r0 + 3) / 4 * a.n_pad;
+    if (items > 0) {
+      slice_a_kernel<<<static_cast<unsigned>(std::min<int64_t>((items + 255) / 256, 148 * 32)), 256, 0, st>>>(
+          A, a.m, a.n, lda, r0, s1, a.rowexp, nullptr, a.rs, nullptr, a.m_pad, a.n_pad);
+      count_launch();
+    }
   }
+  return cudaGetLastError();
+}
+
+cudaError_t ozaki_prepare_cols(const double* A, int64_t lda, const OzakiA& a, bool slice_rows_too, cudaStream_t st) {
+  const int64_t nblk = (a.m + 255) / 256;
+  colexp_kernel<<<static_cast<unsigned>((a.n_pad + 255) / 256), 256, 0, st>>>(a.colpart, nblk, a.n, a.n_pad, a.colexp);
+  const int64_t items = a.m_pad / 4 * a.n_pad;
+  slice_a_kernel<<<static_cast<unsigned>(std::min<int64_t>((items + 255) / 256, 148 * 32)), 256, 0, st>>>(
+      A, a.m, a.n, lda, 0, a.m_pad, a.rowexp, a.colexp, slice_rows_too ? a.rs : nullptr, a.cs, a.m_pad, a.n_pad);
+  count_launch(2);
   return cudaGetLastError();
 }
 
@@ -575,7 +710,7 @@ cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, i
   int* colexp = reinterpret_cast<int*>(xd + static_cast<size_t>(kS) * lp * a.n_pad);
   double* ws = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(colexp) + ((sizeof(int) * lp + 255) / 256) * 256);
   col_exp_kernel<<<static_cast<unsigned>(ell), 256, 0, st>>>(X, a.n, ldx, nullptr, colexp);
-  slice_r_kernel<<<1184, 256, 0, st>>>(X, a.n, ell, ldx, nullptr, colexp, xd, a.n_pad, lp);
+  slice_r_kernel<<<1184, 256, 0, st>>>(X, a.n, ell, ldx, colexp, xd, a.n_pad, lp);
   count_launch(2);
   // K = n beyond kSplitK would overflow the int32 group sums: split K
   const int splits = static_cast<int>((a.n_pad + kSplitK - 1) / kSplitK);
@@ -586,7 +721,7 @@ cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, i
   p.rowexp = a.rowexp;
   p.colexp = colexp;
   p.ws_mode = splits > 1 ? 1 : 0;
-  cudaError_t e = launch_digit_gemm(a.tn, a.n_pad, true, a.m_pad, xd, lp, a.n_pad, r0, rows, ell, splits, p, false, st);
+  cudaError_t e = launch_digit_gemm(a.rs, a.n_pad, true, a.m_pad, xd, lp, a.n_pad, r0, rows, ell, splits, p, false, st);
   if (e != cudaSuccess || splits == 1) return e;
   const int64_t total = rows * ell;
   reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(
@@ -608,19 +743,19 @@ cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell,
   int8_t* qd = static_cast<int8_t*>(work);
   int* colexp = reinterpret_cast<int*>(qd + static_cast<size_t>(kS) * lp * a.m_pad);
   double* ws = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(colexp) + ((sizeof(int) * lp + 255) / 256) * 256);
-  // Q rows carry A's row scale: sum_i A'(i,j) (Q(i,c) 2^e_i)
-  col_exp_kernel<<<static_cast<unsigned>(ell), 256, 0, st>>>(Q, a.m, ldq, a.rowexp, colexp);
-  slice_r_kernel<<<1184, 256, 0, st>>>(Q, a.m, ell, ldq, a.rowexp, colexp, qd, a.m_pad, lp);
+  // column-scaled digits of A: Z(j, c) = 2^(f_j + g_c) sum_g 2^-7(g+2) acc_g
+  col_exp_kernel<<<static_cast<unsigned>(ell), 256, 0, st>>>(Q, a.m, ldq, nullptr, colexp);
+  slice_r_kernel<<<1184, 256, 0, st>>>(Q, a.m, ell, ldq, colexp, qd, a.m_pad, lp);
   count_launch(2);
   const int splits = static_cast<int>((a.m_pad + kSplitK - 1) / kSplitK);
   OzParams p{};
   p.C = splits > 1 ? ws : Z;
   p.ldc = ldz;
   p.c_row0 = 0;
-  p.rowexp = nullptr;
+  p.rowexp = a.colexp;  // output row j of A^T Q = column j of A
   p.colexp = colexp;
   p.ws_mode = splits > 1 ? 1 : 0;
-  cudaError_t e = launch_digit_gemm(a.tn, a.n_pad, false, 0, qd, lp, a.m_pad, 0, a.n, ell, splits, p, true, st);
+  cudaError_t e = launch_digit_gemm(a.cs, a.n_pad, false, 0, qd, lp, a.m_pad, 0, a.n, ell, splits, p, true, st);
   if (e != cudaSuccess || splits == 1) return e;
   const int64_t total = a.n * ell;
   reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(

@@ -401,6 +401,15 @@ struct OzPasses {
     const OzakiA lay = ozaki_layout(m->m, m->n);
     RF_TRY(planes.alloc(ozaki_a_bytes(m->m, m->n), c->stream));
     RF_TRY(work.alloc(std::max(ozaki_nn_work_bytes(lay, m->m, ell), ozaki_tn_work_bytes(lay, ell)), c->stream));
+    ozaki_bind(planes.p, m->m, m->n, &a);
+    return {};
+  }
+  // Whole resident A: stats (one read), then both digit sets (one read).
+  Status prepare(rfgpu_ctx* c, const rfgpu_matrix* m, double* ssq) {
+    Timed t(c, "ozaki_slice");
+    const double* A = static_cast<const double*>(m->dev);
+    RF_CUDA(ozaki_prepare_rows(A, m->lda, 0, m->m, a, ssq, false, c->stream));
+    RF_CUDA(ozaki_prepare_cols(A, m->lda, a, true, c->stream));
     return {};
   }
 };
@@ -414,13 +423,17 @@ int64_t pass1_slots(rfgpu_ctx* c, const rfgpu_matrix* a, int64_t ell, const OzPa
 }
 
 // One pass-1 block: rows [r0, r1) of Y = A G (+ ||A||_F^2 partials at ssq).
+// whole: the block is all of a resident A (both digit sets built here);
+// otherwise an upload panel (row digits only; column digits after the last).
 Status pass1_rows(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, double* Y, int64_t ldy,
-                  double* ssq, int64_t r0, int64_t r1, OzPasses& oz) {
+                  double* ssq, int64_t r0, int64_t r1, OzPasses& oz, bool whole) {
   const double* A = static_cast<const double*>(a->dev);
   if (oz.on) {
-    {
+    if (whole) {
+      RF_TRY(oz.prepare(c, a, ssq));
+    } else {
       Timed t(c, "ozaki_slice");
-      RF_CUDA(ozaki_prepare_a(A, a->m, a->n, a->lda, r0, r1, oz.planes.p, &oz.a, ssq, c->stream));
+      RF_CUDA(ozaki_prepare_rows(A, a->lda, r0, r1, oz.a, ssq, true, c->stream));
     }
     Timed t(c, "pass_nn");
     RF_CUDA(ozaki_nn(oz.a, r0, r1, G, a->n, ell, Y, ldy, oz.work.p, c->stream));
@@ -460,7 +473,7 @@ Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, 
              double* ssq, OzPasses& oz) {
   const int64_t m = a->m, n = a->n, lda = a->lda;
   const double* A = static_cast<const double*>(a->dev);
-  if (!a->src) return pass1_rows(c, a, G, ell, Y, ldy, ssq, 0, m, oz);
+  if (!a->src) return pass1_rows(c, a, G, ell, Y, ldy, ssq, 0, m, oz, true);
   cudaStream_t st = c->stream, cs = c->copy_stream;
   const auto panels = upload_panels(m);
   std::vector<cudaEvent_t> ev(panels.size());
@@ -488,8 +501,12 @@ Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, 
       s = make_err(RFGPU_ECUDA, "pass 1: stream wait failed");
       break;
     }
-    s = pass1_rows(c, a, G, ell, Y, ldy, ssq + off, r0, r0 + rows, oz);
+    s = pass1_rows(c, a, G, ell, Y, ldy, ssq + off, r0, r0 + rows, oz, false);
     off += oz.on ? ozaki_ssq_slots(rows) : sumsq_slots(c, rows, ell, n);
+  }
+  if (s.ok() && oz.on) {  // all rows landed: column exponents and the A^T Q digits
+    Timed t(c, "ozaki_slice");
+    if (ozaki_prepare_cols(A, lda, oz.a, false, st) != cudaSuccess) s = make_err(RFGPU_ECUDA, "pass 1: slicing failed");
   }
   a->src = nullptr;  // issued: every later consumer is ordered after the waits above
   cudaEventDestroy(ready);
@@ -1339,8 +1356,21 @@ int rfgpu_multiply(rfgpu_ctx* c, const rfgpu_matrix* a, int trans, const double*
     RF_TRY(xd.alloc(sizeof(double) * std::max<int64_t>(1, xr * ncols), st));
     RF_TRY(cd.alloc(sizeof(double) * std::max<int64_t>(1, cr * ncols), st));
     if (xr * ncols > 0) RF_CUDA(cudaMemcpyAsync(xd.d(), x, sizeof(double) * xr * ncols, cudaMemcpyHostToDevice, st));
-    RF_TRY(gemm(c, trans != 0, cr, ncols, trans ? m : n, static_cast<const double*>(a->dev), a->lda, xd.d(),
-                std::max<int64_t>(1, xr), cd.d(), std::max<int64_t>(1, cr)));
+    OzPasses oz;
+    RF_TRY(oz.init(c, a, ncols));
+    if (oz.on && ncols > 0) {
+      // the same INT8-tensor-core path the range finder takes at this size
+      DBuf ssq;
+      RF_TRY(ssq.alloc(sizeof(double) * ozaki_ssq_slots(m), st));
+      RF_TRY(oz.prepare(c, a, ssq.d()));
+      if (trans)
+        RF_TRY(pass_tn_raw(c, a, xd.d(), std::max<int64_t>(1, xr), ncols, cd.d(), &oz));
+      else
+        RF_TRY(pass_nn(c, a, xd.d(), ncols, cd.d(), std::max<int64_t>(1, cr), &oz));
+    } else {
+      RF_TRY(gemm(c, trans != 0, cr, ncols, trans ? m : n, static_cast<const double*>(a->dev), a->lda, xd.d(),
+                  std::max<int64_t>(1, xr), cd.d(), std::max<int64_t>(1, cr)));
+    }
     if (trans) RF_TRY(allreduce(c, cd.d(), cr * ncols));
     RF_TRY(copy_out(c, out, std::max<int64_t>(1, cr), cd.d(), std::max<int64_t>(1, cr), cr, ncols));
     RF_CUDA(cudaStreamSynchronize(st));

@@ -40,18 +40,27 @@ cudaError_t sum_array(const double* x, int64_t n, double* out, cudaStream_t st);
 // Digit planes of A (m x n, FP64) for Y = A X and Z = A^T Q (Ozaki scheme,
 // 8 signed 7-bit digits per operand, tcgen05 kind::i8, FP64 recombination).
 struct OzakiA {
-  int8_t* tn;   // [8][n_pad][m_pad] row-scaled digits, column-major (read M-major by Y = A X, K-major by A^T Q)
-  int* rowexp;  // m_pad row exponents (|A(i,:)| < 2^rowexp[i])
+  int8_t* rs;   // [8][n_pad][m_pad] digits of A(i,j) 2^-rowexp[i] (column-major; read M-major by A X)
+  int8_t* cs;   // [8][n_pad][m_pad] digits of A(i,j) 2^-colexp[j] (read K-major by A^T Q)
+  int* rowexp;  // m_pad: |A(i,:)| < 2^rowexp[i]
+  int* colexp;  // n_pad: |A(:,j)| < 2^colexp[j]
+  uint32_t* colpart;  // (m_pad / 256) x n_pad per-block column maxima (high words)
   int64_t m, n, m_pad, n_pad;
 };
 bool ozaki_enabled(int64_t m, int64_t n);  // RFGPU_OZAKI=0/1 overrides the size rule
 OzakiA ozaki_layout(int64_t m, int64_t n);  // shapes only (no buffers)
 size_t ozaki_a_bytes(int64_t m, int64_t n);
+void ozaki_bind(void* work, int64_t m, int64_t n, OzakiA* out);  // carve a work buffer of ozaki_a_bytes
 int64_t ozaki_ssq_slots(int64_t rows);
-// Rows [r0, r1) of A (whole 256-row blocks except at m): row exponents,
-// ||A||_F^2 partials (ozaki_ssq_slots(r1 - r0) of them) and digit planes.
-cudaError_t ozaki_prepare_a(const double* A, int64_t m, int64_t n, int64_t lda, int64_t r0, int64_t r1, void* work,
-                            OzakiA* out, double* ssq_part, cudaStream_t st);
+// Rows [r0, r1) (r0 a multiple of 256): row exponents, ||A||_F^2 partials
+// (ozaki_ssq_slots(r1 - r0) of them), column maxima of these rows, and, with
+// slice_rows, the row-scaled digits of these rows (all A X needs).
+cudaError_t ozaki_prepare_rows(const double* A, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
+                               double* ssq_part, bool slice_rows, cudaStream_t st);
+// After every row block's stats: column exponents and the column-scaled
+// digits (A^T Q); slice_rows_too also writes the row-scaled digits in the
+// same read of A.
+cudaError_t ozaki_prepare_cols(const double* A, int64_t lda, const OzakiA& a, bool slice_rows_too, cudaStream_t st);
 size_t ozaki_nn_work_bytes(const OzakiA& a, int64_t rows, int64_t ell);
 // Y(r0:r1, 0:ell) = A(r0:r1, :) X  (X n x ell, col-major)
 cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, int64_t ldx, int64_t ell, double* Y,

@@ -1,0 +1,95 @@
+"""GPU: the FP64 passes on the INT8 tensor cores (csrc/ozaki.cu, Ozaki digit
+splitting + tcgen05 kind::i8). Forced on with RFGPU_OZAKI=1 at sizes where the
+size rule would pick DMMA, so every case here runs the digit GEMM.
+
+Bars: products within 1e-14 of an extended-precision reference, relative to
+max|A(i,:)| max|X(:,c)| * sqrt(K) (the digit truncation bound, ~2^-53 per
+term); rsvd singular values 1e-10 vs the oracle (the north-star bar); the
+reference's exact-rank residual identity (test_rangefinder.cpp:43-71).
+"""
+import numpy as np
+import pytest
+
+import paper_1607_01649_b200 as rf
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def ozaki(monkeypatch):
+    monkeypatch.setenv("RFGPU_OZAKI", "1")
+
+
+def exact_product(a, x, trans):
+    a = a.astype(np.longdouble)
+    x = x.astype(np.longdouble)
+    return (a.T @ x) if trans else (a @ x)
+
+
+def scaled_err(got, want, a, x, trans):
+    rows = np.abs(a).max(axis=0 if trans else 1)
+    cols = np.abs(x).max(axis=0)
+    k = a.shape[0] if trans else a.shape[1]
+    scale = np.outer(rows, cols) * np.sqrt(k)
+    scale[scale == 0] = 1.0
+    return float(np.max(np.abs(got.astype(np.longdouble) - want) / scale))
+
+
+@pytest.mark.parametrize("m,n,cols", [(1000, 777, 40), (4096, 300, 64), (257, 20000, 3), (40000, 129, 70)])
+@pytest.mark.parametrize("trans", [False, True])
+def test_digit_gemm_matches_extended_precision(ctx, ozaki, m, n, cols, trans):
+    rng = np.random.default_rng(m + n + cols)
+    a = rng.standard_normal((m, n))
+    a[3] *= 1e120             # wide dynamic range across rows
+    a[5] *= 1e-150
+    a[7] = 0.0                # zero row
+    a[:, 2] *= 1e-8           # small column inside every row
+    x = rng.standard_normal((m if trans else n, cols))
+    x[:, 1] *= 1e80
+    x[:, 2] = 0.0
+    a = np.asfortranarray(a)
+    got = rf.multiply(a, x, trans=trans, ctx=ctx)
+    want = exact_product(a, x, trans)
+    assert scaled_err(got, want, a, x, trans) < 1e-14
+    if not trans:
+        assert np.all(got[7] == 0.0)
+    assert np.all(got[:, 2] == 0.0)
+
+
+@pytest.mark.parametrize("case", [(600, 400, 20, 10, 1), (2000, 2000, 50, 10, 1), (5000, 1500, 100, 10, 2)])
+def test_rsvd_on_digit_gemm_matches_oracle(ctx, port, ozaki, case):
+    m, n, k, p, q = case
+    sig = np.arange(1, min(m, n) + 1, dtype=np.float64) ** -1.5
+    a = np.asfortranarray(port.planted(m, n, sig, 3))
+    want = port.rsvd(a, k, p, q, 7, False, True)
+    got = rf.rsvd(a, k, p, q, 7, reorthonormalize=True, ctx=ctx)
+    assert np.max(np.abs(got.D - want.D) / want.D) < 1e-10
+    r1 = np.linalg.norm(a - (got.U * got.D) @ got.V.T)
+    r2 = np.linalg.norm(a - (want.U * want.D) @ want.V.T)
+    assert abs(r1 - r2) <= 0.01 * r2
+
+
+def test_exact_rank_residual_on_digit_gemm(ctx, port, ozaki):
+    # test_rangefinder.cpp:43-71 with every pass on the INT8 tensor cores
+    sig = 0.5 ** np.arange(12, dtype=np.float64)
+    a = np.asfortranarray(port.planted(30, 20, sig, 11))
+    rb = rf.basic_range(a, 8, 4, 3, ctx=ctx)
+    assert rb.residual_frob < 1e-7 * np.linalg.norm(a)
+    assert np.linalg.norm(a - rb.Q @ rb.B) < 1e-12 * np.linalg.norm(a)
+
+
+def test_streamed_panels_on_digit_gemm(ctx, ozaki, monkeypatch):
+    # host matrix -> rfgpu_rsvd_host: 4 upload panels, each sliced and multiplied as it lands
+    m, n, k, p = 70000, 96, 10, 6
+    rng = np.random.default_rng(5)
+    u, _ = np.linalg.qr(rng.standard_normal((m, 40)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, 40)))
+    a = np.asfortranarray((u * 0.8 ** np.arange(40)) @ v.T)
+    host = rf.rsvd(a, k, p, 1, 3, reorthonormalize=True, ctx=ctx)
+    monkeypatch.setenv("RFGPU_OZAKI", "0")
+    dm = ctx.matrix(a)
+    try:
+        dev = rf.rsvd(dm, k, p, 1, 3, reorthonormalize=True, ctx=ctx)
+    finally:
+        dm.free()
+    assert np.max(np.abs(host.D - dev.D) / dev.D) < 1e-12
