@@ -599,6 +599,11 @@ cudaError_t launch_digit_gemm(const int8_t* L, int64_t L_rows, bool L_mn, int64_
   const int64_t grid = static_cast<int64_t>(p.ntn) * p.mtn * splits;
   if (grid <= 0) return cudaSuccess;
   p.cl = 1;
+  static const int mc_env = [] {
+    const char* e = std::getenv("RFGPU_OZAKI_MC");  // experiments: 0 never, 1 always, unset: caller's choice
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  if (mc_env >= 0) multicast = mc_env == 1;
   if (multicast)
     for (int c : {8, 7, 6, 5, 4, 3, 2})
       if (p.ntn % c == 0) {
