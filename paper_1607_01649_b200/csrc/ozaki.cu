@@ -70,23 +70,27 @@ __device__ __forceinline__ int hi_exp(uint32_t h) {
   return h == 0 ? 0 : (E == 0 ? -1021 : E - 1022);
 }
 
-// Rows [r0, r1) (r0 a multiple of 256): row exponents, ||A||_F^2 partials
-// (one per CTA) and per-CTA column maxima (high words) colpart[blk][j],
-// blk = (row0 / 256) + blockIdx.x. One thread per row, columns in chunks of
-// 256: warp maxima by redux, CTA maxima through shared memory.
+// Rows [r0, r1) (r0 a multiple of 256) x one column chunk per blockIdx.y:
+// row maxima (high words, atomicMax into rowhi), ||A||_F^2 partials (one per
+// CTA) and per-CTA column maxima colpart[blk][j], blk = r0 / 256 +
+// blockIdx.x. One thread per row, columns in sub-chunks of 256: warp maxima
+// by redux, CTA maxima through shared memory. The column chunks keep the grid
+// at >= 4 CTAs per SM for short (square) matrices.
 __global__ void __launch_bounds__(256) stats_kernel(const double* __restrict__ A, int64_t r0, int64_t r1, int64_t n,
-                                                    int64_t lda, int64_t n_pad, int* __restrict__ rowexp,
-                                                    uint32_t* __restrict__ colpart, double* __restrict__ ssq_part) {
+                                                    int64_t lda, int64_t n_pad, int64_t chunk,
+                                                    uint32_t* __restrict__ rowhi, uint32_t* __restrict__ colpart,
+                                                    double* __restrict__ ssq_part) {
   __shared__ double red[32];
   __shared__ uint32_t wmax[8][257];
   const int64_t i = r0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool ok = i < r1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t blk = r0 / 256 + blockIdx.x;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.y) * chunk, c1 = lmin(n, c0 + chunk);
   uint32_t rmax = 0;
   double s0 = 0.0, s1 = 0.0;
-  for (int64_t j0 = 0; j0 < n; j0 += 256) {
-    const int jn = static_cast<int>(lmin(256, n - j0));
+  for (int64_t j0 = c0; j0 < c1; j0 += 256) {
+    const int jn = static_cast<int>(lmin(256, c1 - j0));
     int jj = 0;
     for (; jj + 4 <= jn; jj += 4) {
       double v[4];
@@ -119,9 +123,18 @@ __global__ void __launch_bounds__(256) stats_kernel(const double* __restrict__ A
     }
     __syncthreads();
   }
-  if (ok) rowexp[i] = hi_exp(rmax);
+  if (ok) {
+    if (gridDim.y == 1) rowhi[i] = rmax;
+    else atomicMax(&rowhi[i], rmax);
+  }
   const double s = block_sum(s0 + s1, red);
-  if (threadIdx.x == 0 && ssq_part) ssq_part[blockIdx.x] = s;
+  if (threadIdx.x == 0 && ssq_part) ssq_part[static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x] = s;
+}
+
+__global__ void rowexp_kernel(const uint32_t* __restrict__ rowhi, int64_t r0, int64_t r1, int* __restrict__ rowexp) {
+  for (int64_t i = r0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < r1;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    rowexp[i] = hi_exp(rowhi[i]);
 }
 
 // Column exponents from the per-CTA column maxima.
@@ -650,10 +663,18 @@ OzakiA ozaki_layout(int64_t m, int64_t n) {
 size_t ozaki_a_bytes(int64_t m, int64_t n) {
   const OzakiA a = ozaki_layout(m, n);
   const size_t planes = static_cast<size_t>(kS) * a.m_pad * a.n_pad;
-  return 2 * planes + sizeof(int) * (a.m_pad + a.n_pad) + sizeof(uint32_t) * (a.m_pad / 256) * a.n_pad + 1024;
+  return 2 * planes + sizeof(int) * (2 * a.m_pad + a.n_pad) + sizeof(uint32_t) * (a.m_pad / 256) * a.n_pad + 1024;
 }
 
-int64_t ozaki_ssq_slots(int64_t rows) { return (rows + 255) / 256; }
+namespace {
+// Column chunks of the stats pass: >= 4 CTAs per SM in total.
+int64_t stats_chunks(int64_t rows, int64_t n) {
+  const int64_t rb = std::max<int64_t>(1, (rows + 255) / 256), cb = std::max<int64_t>(1, (n + 255) / 256);
+  return std::max<int64_t>(1, std::min<int64_t>(cb, (592 + rb - 1) / rb));
+}
+}  // namespace
+
+int64_t ozaki_ssq_slots(int64_t rows, int64_t n) { return ((rows + 255) / 256) * stats_chunks(rows, n); }
 
 void ozaki_bind(void* work, int64_t m, int64_t n, OzakiA* out) {
   *out = ozaki_layout(m, n);
@@ -663,7 +684,8 @@ void ozaki_bind(void* work, int64_t m, int64_t n, OzakiA* out) {
   out->cs = base + planes;
   out->rowexp = reinterpret_cast<int*>(base + 2 * planes);
   out->colexp = out->rowexp + out->m_pad;
-  out->colpart = reinterpret_cast<uint32_t*>(out->colexp + out->n_pad);
+  out->rowhi = reinterpret_cast<uint32_t*>(out->colexp + out->n_pad);
+  out->colpart = out->rowhi + out->m_pad;
 }
 
 cudaError_t ozaki_prepare_rows(const double* A, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
@@ -675,9 +697,18 @@ cudaError_t ozaki_prepare_rows(const double* A, int64_t lda, int64_t r0, int64_t
   const int64_t rows = r1 - r0;
   const int64_t blocks = (rows + 255) / 256;
   if (rows > 0) {
-    stats_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(A, r0, r1, a.n, lda, a.n_pad, a.rowexp, a.colpart,
-                                                               ssq_part);
-    count_launch();
+    const int64_t chunks = stats_chunks(rows, a.n);
+    const int64_t chunk = ((a.n + chunks - 1) / chunks + 255) / 256 * 256;
+    uint32_t* rowhi = reinterpret_cast<uint32_t*>(a.rowhi);
+    if (chunks > 1) {
+      cudaError_t e = cudaMemsetAsync(rowhi + r0, 0, sizeof(uint32_t) * rows, st);
+      if (e != cudaSuccess) return e;
+    }
+    dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>((a.n + chunk - 1) / chunk));
+    stats_kernel<<<grid, 256, 0, st>>>(A, r0, r1, a.n, lda, a.n_pad, chunk, rowhi, a.colpart, ssq_part);
+    rowexp_kernel<<<static_cast<unsigned>(std::min<int64_t>((rows + 255) / 256, 1184)), 256, 0, st>>>(rowhi, r0, r1,
+                                                                                                       a.rowexp);
+    count_launch(2);
   }
   if (slice_rows) {
     const int64_t s1 = r1 == a.m ? a.m_pad : r1;

@@ -404,18 +404,19 @@ struct OzPasses {
     ozaki_bind(planes.p, m->m, m->n, &a);
     return {};
   }
-  // Whole resident A: stats (one read), then both digit sets (one read).
-  Status prepare(rfgpu_ctx* c, const rfgpu_matrix* m, double* ssq) {
+  // Whole resident A: stats (one read), then the digit sets (one read):
+  // row-scaled (A X) only when `rows`, column-scaled (A^T Q) always.
+  Status prepare(rfgpu_ctx* c, const rfgpu_matrix* m, double* ssq, bool rows = true) {
     Timed t(c, "ozaki_slice");
     const double* A = static_cast<const double*>(m->dev);
     RF_CUDA(ozaki_prepare_rows(A, m->lda, 0, m->m, a, ssq, false, c->stream));
-    RF_CUDA(ozaki_prepare_cols(A, m->lda, a, true, c->stream));
+    RF_CUDA(ozaki_prepare_cols(A, m->lda, a, rows, c->stream));
     return {};
   }
 };
 
 int64_t pass1_slots(rfgpu_ctx* c, const rfgpu_matrix* a, int64_t ell, const OzPasses& oz) {
-  auto slots = [&](int64_t rows) { return oz.on ? ozaki_ssq_slots(rows) : sumsq_slots(c, rows, ell, a->n); };
+  auto slots = [&](int64_t rows) { return oz.on ? ozaki_ssq_slots(rows, a->n) : sumsq_slots(c, rows, ell, a->n); };
   if (!a->src) return slots(a->m);
   int64_t s = 0;
   for (auto& pr : upload_panels(a->m)) s += slots(pr.second - pr.first);
@@ -502,7 +503,7 @@ Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, 
       break;
     }
     s = pass1_rows(c, a, G, ell, Y, ldy, ssq + off, r0, r0 + rows, oz, false);
-    off += oz.on ? ozaki_ssq_slots(rows) : sumsq_slots(c, rows, ell, n);
+    off += oz.on ? ozaki_ssq_slots(rows, a->n) : sumsq_slots(c, rows, ell, n);
   }
   if (s.ok() && oz.on) {  // all rows landed: column exponents and the A^T Q digits
     Timed t(c, "ozaki_slice");
@@ -949,15 +950,21 @@ Status col_id_dev(rfgpu_ctx* c, const double* Y, int64_t m, int64_t n, int64_t l
 Status row_sketch_t(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Gt, int64_t ldg, int64_t ell, int64_t q,
                     double* Yt) {
   const int64_t m = a->m, n = a->n;
-  const double* A = static_cast<const double*>(a->dev);
-  RF_TRY(gemm(c, true, n, ell, m, A, a->lda, Gt, ldg, Yt, n, nullptr, "pass_tn"));
+  OzPasses oz;  // the passes over A on the INT8 tensor cores at pass sizes
+  RF_TRY(oz.init(c, a, ell));
+  if (oz.on) {
+    DBuf ssq;
+    RF_TRY(ssq.alloc(sizeof(double) * ozaki_ssq_slots(m, n), c->stream));
+    RF_TRY(oz.prepare(c, a, ssq.d(), q > 0));
+  }
+  RF_TRY(pass_tn_raw(c, a, Gt, ldg, ell, Yt, &oz));
   RF_TRY(allreduce(c, Yt, n * ell));
   if (q > 0) {
     DBuf t;
     RF_TRY(t.alloc(sizeof(double) * std::max<int64_t>(1, even(m) * ell), c->stream));
     for (int64_t j = 0; j < q; ++j) {
-      RF_TRY(gemm(c, false, m, ell, n, A, a->lda, Yt, n, t.d(), even(m), nullptr, "pass_nn"));
-      RF_TRY(gemm(c, true, n, ell, m, A, a->lda, t.d(), even(m), Yt, n, nullptr, "pass_tn"));
+      RF_TRY(pass_nn(c, a, Yt, ell, t.d(), even(m), &oz));
+      RF_TRY(pass_tn_raw(c, a, t.d(), even(m), ell, Yt, &oz));
       RF_TRY(allreduce(c, Yt, n * ell));
     }
   }
@@ -1361,7 +1368,7 @@ int rfgpu_multiply(rfgpu_ctx* c, const rfgpu_matrix* a, int trans, const double*
     if (oz.on && ncols > 0) {
       // the same INT8-tensor-core path the range finder takes at this size
       DBuf ssq;
-      RF_TRY(ssq.alloc(sizeof(double) * ozaki_ssq_slots(m), st));
+      RF_TRY(ssq.alloc(sizeof(double) * ozaki_ssq_slots(m, n), st));
       RF_TRY(oz.prepare(c, a, ssq.d()));
       if (trans)
         RF_TRY(pass_tn_raw(c, a, xd.d(), std::max<int64_t>(1, xr), ncols, cd.d(), &oz));
@@ -1612,7 +1619,6 @@ int rfgpu_randomized_id(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, in
     // columns + allreduce) for the replicated CPQR; Is are global row
     // indices, X holds this rank's rows.
     const int64_t m = a->m, mg = a->m_global, n = a->n, ldy = even(m);
-    const double* A = static_cast<const double*>(a->dev);
     DBuf gd, y, z, yt, zt, x;
     RF_TRY(gd.alloc(sizeof(double) * n * ell, st));
     RF_TRY(y.alloc(sizeof(double) * ldy * ell, st));
@@ -1622,11 +1628,18 @@ int rfgpu_randomized_id(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, in
     RF_TRY(x.alloc(sizeof(double) * m * k, st));
     RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
     // tall sketch Y = (A A^T)^q A G (lowrank.cpp:316-320)
-    RF_TRY(gemm(c, false, m, ell, n, A, a->lda, gd.d(), n, y.d(), ldy, nullptr, "pass_nn"));
+    OzPasses oz;  // the passes over A on the INT8 tensor cores at pass sizes
+    RF_TRY(oz.init(c, a, ell));
+    if (oz.on) {
+      DBuf ssq;
+      RF_TRY(ssq.alloc(sizeof(double) * ozaki_ssq_slots(m, n), st));
+      RF_TRY(oz.prepare(c, a, ssq.d(), true));
+    }
+    RF_TRY(pass_nn(c, a, gd.d(), ell, y.d(), ldy, &oz));
     for (int64_t j = 0; j < q; ++j) {
-      RF_TRY(gemm(c, true, n, ell, m, A, a->lda, y.d(), ldy, z.d(), n, nullptr, "pass_tn"));
+      RF_TRY(pass_tn_raw(c, a, y.d(), ldy, ell, z.d(), &oz));
       RF_TRY(allreduce(c, z.d(), n * ell));
-      RF_TRY(gemm(c, false, m, ell, n, A, a->lda, z.d(), n, y.d(), ldy, nullptr, "pass_nn"));
+      RF_TRY(pass_nn(c, a, z.d(), ell, y.d(), ldy, &oz));
     }
     if (c->world > 1) RF_CUDA(cudaMemsetAsync(yt.d(), 0, sizeof(double) * ell * mg, st));
     RF_CUDA(transpose(y.d(), m, ell, ldy, yt.d() + a->row0 * ell, ell, st));  // Y^T (ell x m), this rank's columns

@@ -44,6 +44,7 @@ struct OzakiA {
   int8_t* cs;   // [8][n_pad][m_pad] digits of A(i,j) 2^-colexp[j] (read K-major by A^T Q)
   int* rowexp;  // m_pad: |A(i,:)| < 2^rowexp[i]
   int* colexp;  // n_pad: |A(:,j)| < 2^colexp[j]
+  uint32_t* rowhi;    // m_pad row maxima (high words of |A(i,:)|)
   uint32_t* colpart;  // (m_pad / 256) x n_pad per-block column maxima (high words)
   int64_t m, n, m_pad, n_pad;
 };
@@ -51,9 +52,9 @@ bool ozaki_enabled(int64_t m, int64_t n);  // RFGPU_OZAKI=0/1 overrides the size
 OzakiA ozaki_layout(int64_t m, int64_t n);  // shapes only (no buffers)
 size_t ozaki_a_bytes(int64_t m, int64_t n);
 void ozaki_bind(void* work, int64_t m, int64_t n, OzakiA* out);  // carve a work buffer of ozaki_a_bytes
-int64_t ozaki_ssq_slots(int64_t rows);
+int64_t ozaki_ssq_slots(int64_t rows, int64_t n);  // ||A||_F^2 partials of a row block
 // Rows [r0, r1) (r0 a multiple of 256): row exponents, ||A||_F^2 partials
-// (ozaki_ssq_slots(r1 - r0) of them), column maxima of these rows, and, with
+// (ozaki_ssq_slots(r1 - r0, n) of them), column maxima of these rows, and, with
 // slice_rows, the row-scaled digits of these rows (all A X needs).
 cudaError_t ozaki_prepare_rows(const double* A, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
                                double* ssq_part, bool slice_rows, cudaStream_t st);
