@@ -21,7 +21,8 @@ from collections import defaultdict
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OURS = ("gemm_f64", "jacobi_svd", "chol_inv", "trinv_upper", "cpqr", "reduce_splits", "symmetrize", "sumsq",
         "sum_array", "transpose", "gather_", "lsq_scale", "gs_", "add_inplace", "sylvester", "f32_to_f64",
-        "scale_", "copy_", "fill_", "rfgpu")
+        "scale_", "copy_", "fill_", "ozaki_gemm", "stats_kernel", "slice_a_kernel", "slice_r_kernel", "colexp_kernel",
+        "col_exp_kernel", "rowexp_kernel", "reduce_ws_kernel", "rfgpu")
 
 
 def ours(name):
@@ -64,6 +65,7 @@ def launches(rnd, wl, steps_total):
 
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__registers_per_thread",
            "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
            "sm__cycles_elapsed.avg.per_second"]
@@ -82,6 +84,8 @@ def ncu_full(rnd, wl):
                 i = hdr.index(m)
                 d[m] = f"{r[i]} {units[i]}".strip()
         out.append(d)
+        if "gemm" not in d["kernel"]:
+            continue
         try:
             t = float(r[hdr.index("dram__bytes_read.sum")].replace(",", "")) * (1e9 if "Gbyte" in units[hdr.index("dram__bytes_read.sum")] else 1)
             wb = float(r[hdr.index("dram__bytes_write.sum")].replace(",", "")) * (1e9 if "Gbyte" in units[hdr.index("dram__bytes_write.sum")] else 1)
@@ -94,9 +98,17 @@ def ncu_full(rnd, wl):
         for d in out:
             f.write(json.dumps(d) + "\n")
     if best:
-        json.dump({"kernel": best[2], "traffic_bytes": best[1], "source": f"ncu --set full, profiles/{rnd}_ncu_top_kernels_{wl}.jsonl",
-                   "note": "dram__bytes_read.sum + dram__bytes_write.sum of the longest captured pass launch"},
-                  open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+        path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        try:
+            cur = json.load(open(path))
+            if not isinstance(cur, dict) or "kernel" in cur:
+                cur = {}
+        except Exception:
+            cur = {}
+        cur[wl] = {"kernel": best[2], "traffic_bytes": best[1],
+                   "source": f"ncu --set full, profiles/{rnd}_ncu_top_kernels_{wl}.jsonl",
+                   "note": "dram__bytes_read.sum + dram__bytes_write.sum of the longest captured pass launch"}
+        json.dump(cur, open(path, "w"), indent=1)
     for d in out:
         print(d)
 
