@@ -53,7 +53,8 @@ CHUNK = 65536
 SEED = 1
 FP64_PEAK_TFLOPS = 37.1  # DMMA m8n8k4 burst, profiles/r01_fp_peaks.txt (MEASURED_PEAKS.json has no FP64 entry)
 INT8_PEAK_TOPS = 4594.7  # tcgen05 kind::i8 dense burst, tools/microbench/i8peak.cu -> profiles/r01_i8_peak.txt
-OZAKI_PRODUCTS = 36      # int8 digit products per FP64 product (8 digits, groups s + t <= 7; csrc/ozaki.cu)
+OZAKI_PRODUCTS = 28      # int8 digit products per FP64 product (7 digits, s + t <= 6; csrc/ozaki.cu)
+OZAKI_PRODUCTS_F32 = 10  # FP32 data: 4 digits, s + t <= 3
 
 
 def spectrum(kind, r):
@@ -342,6 +343,8 @@ def main():
                                                 "single_pass_core", "gemm_nn", "gemm_tn", "allreduce")}
     ctx.profile(False)
     pass_names = ("sketch_nn", "sketch_tn") if kind == "single_pass" else ("pass_nn", "pass_tn")
+    if kind == "single_pass" and prof["sketch_nn"][0] == 0:  # the dual sketch ran on the digit path
+        pass_names = ("pass_nn", "pass_tn")
     n_pass = sum(prof[nm][0] for nm in pass_names)
     pass_ms = sum(prof[nm][1] for nm in pass_names)
     # algorithmic flops of the passes over A (ell unpadded): 2 m n ell per pass;
@@ -350,6 +353,7 @@ def main():
     passes_alg = {"rsvd": n_pass / args.steps, "cur": 1.0, "single_pass": 2.0}[kind]
     achieved = flops_per_pass * passes_alg * args.steps / (pass_ms * 1e-3) / 1e12 if pass_ms > 0 else None
     ozaki = prof["ozaki_slice"][0] > 0  # the FP64 passes ran as int8 digit products on tcgen05
+    products = OZAKI_PRODUCTS_F32 if w.get("f32") else OZAKI_PRODUCTS
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tr_path):
@@ -416,10 +420,10 @@ def main():
             "data": "synthetic (planted spectrum, seeded torch RNG on device)" + (", A stored fp32" if w.get("f32") else ""),
             "config": config_of(w, world, args),
             "sketch_tflops": achieved,
-            "roofline": ({"bound": "tensor", "achieved": achieved * OZAKI_PRODUCTS, "peak": INT8_PEAK_TOPS,
-                          "unit": "TOPS", "frac": achieved * OZAKI_PRODUCTS / INT8_PEAK_TOPS, "traffic": traffic,
+            "roofline": ({"bound": "tensor", "achieved": achieved * products, "peak": INT8_PEAK_TOPS,
+                          "unit": "TOPS", "frac": achieved * products / INT8_PEAK_TOPS, "traffic": traffic,
                           "kernel": f"ozaki_gemm_kernel (tcgen05 kind::i8; passes over A: {' + '.join(pass_names)})",
-                          "algorithmic_ops_per_pass": flops_per_pass * OZAKI_PRODUCTS,
+                          "algorithmic_ops_per_pass": flops_per_pass * products,
                           "fp64_equivalent_tflops": achieved, "fp64_dmma_peak_tflops": FP64_PEAK_TFLOPS,
                           "passes_per_step": passes_alg, "launches_per_step": n_pass / args.steps,
                           "pass_ms_avg": pass_ms / n_pass if n_pass else None,

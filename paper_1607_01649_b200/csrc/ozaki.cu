@@ -42,16 +42,22 @@
 namespace rfgpu {
 namespace {
 
-constexpr int kS = 7;          // balanced base-256 digits per operand
+// balanced base-256 digits per operand: 7 for FP64 data, 4 for FP32 (template S)
 constexpr int OBM = 128;       // tile rows (TMEM lanes)
 constexpr int OBN = 64;        // tile columns per accumulator group
 constexpr int OBK = 64;        // K bytes per pipeline stage (64B swizzle)
-constexpr int kStages = 2;
-constexpr int kTmemCols = 512;  // kS * OBN = 448 -> 512
-constexpr int64_t kSplitK = 16384;
+constexpr int64_t kSplitK = 16384;  // int32 safety: S * K * 128^2 < 2^31
 constexpr int kThreads = 192;   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
-constexpr size_t kStageBytes = static_cast<size_t>(kS) * (OBM + OBN) * OBK;
-constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 + 256;
+
+// Per digit count S: S accumulator groups of OBN TMEM columns; as many
+// 2-digit-plane... stages as fit in shared memory.
+template <int S>
+struct Dig {
+  static constexpr size_t stage_bytes = static_cast<size_t>(S) * (OBM + OBN) * OBK;
+  static constexpr int stages = S <= 4 ? 4 : 2;
+  static constexpr int tmem_cols = S * OBN <= 256 ? 256 : 512;
+  static constexpr size_t smem = stages * stage_bytes + 1024 + 256;
+};
 
 __host__ __device__ inline int64_t roundup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -76,7 +82,8 @@ __device__ __forceinline__ int hi_exp(uint32_t h) {
 // blockIdx.x. One thread per row, columns in sub-chunks of 256: warp maxima
 // by redux, CTA maxima through shared memory. The column chunks keep the grid
 // at >= 4 CTAs per SM for short (square) matrices.
-__global__ void __launch_bounds__(256) stats_kernel(const double* __restrict__ A, int64_t r0, int64_t r1, int64_t n,
+template <class T>
+__global__ void __launch_bounds__(256) stats_kernel(const T* __restrict__ A, int64_t r0, int64_t r1, int64_t n,
                                                     int64_t lda, int64_t n_pad, int64_t chunk,
                                                     uint32_t* __restrict__ rowhi, uint32_t* __restrict__ colpart,
                                                     double* __restrict__ ssq_part) {
@@ -95,7 +102,7 @@ __global__ void __launch_bounds__(256) stats_kernel(const double* __restrict__ A
     for (; jj + 4 <= jn; jj += 4) {
       double v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = ok ? A[(j0 + jj + u) * lda + i] : 0.0;
+      for (int u = 0; u < 4; ++u) v[u] = ok ? static_cast<double>(A[(j0 + jj + u) * lda + i]) : 0.0;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const uint32_t h = abs_hi(v[u]);
@@ -107,7 +114,7 @@ __global__ void __launch_bounds__(256) stats_kernel(const double* __restrict__ A
       }
     }
     for (; jj < jn; ++jj) {
-      const double v = ok ? A[(j0 + jj) * lda + i] : 0.0;
+      const double v = ok ? static_cast<double>(A[(j0 + jj) * lda + i]) : 0.0;
       const uint32_t h = abs_hi(v);
       rmax = max(rmax, h);
       s0 = fma(v, v, s0);
@@ -149,20 +156,24 @@ __global__ void colexp_kernel(const uint32_t* __restrict__ colpart, int64_t nblk
   }
 }
 
-// X' = trunc(v 2^(54-e)) + 0x0080808080808080 for |v| < 2^e: byte k of X',
-// minus 0x80, is the balanced base-256 digit d_k of trunc(v 2^(54-e)).
-// Built from v's bits (new exponent E + 54 - e, then a truncating
-// conversion); zero, subnormal and negligible (< 2^-54 relative) inputs give
-// all-zero digits (X' bytes 0x80).
-__device__ __forceinline__ uint64_t balanced7(double v, int e) {
+// S digits: X' = trunc(v 2^(8S-2-e)) + (0x80 in each of the S low bytes) for
+// |v| < 2^e; byte k of X', minus 0x80, is the balanced base-256 digit d_k of
+// trunc(v 2^(8S-2-e)) (|X| < 2^(8S-2) keeps the top byte in range). Built
+// from v's bits (new exponent E + 8S-2 - e, then a truncating conversion);
+// zero, subnormal and negligible (< 2^-(8S-2) relative) inputs give all-zero
+// digits (X' bytes 0x80).
+template <int S>
+__device__ __forceinline__ uint64_t balanced(double v, int e) {
+  constexpr uint64_t bias = S == 7 ? 0x0080808080808080ull : 0x0000000080808080ull;
+  static_assert(S == 7 || S == 4, "digit counts: 7 (FP64) or 4 (FP32)");
   const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v));
   const int E = static_cast<int>((bits >> 52) & 0x7FF);
-  const int En = E + 54 - e;
+  const int En = E + (8 * S - 2) - e;
   int64_t X = 0;
   if (E != 0 && En > 0)
     X = static_cast<int64_t>(__longlong_as_double(static_cast<long long>((bits & ~(uint64_t(0x7FF) << 52)) |
                                                                           (static_cast<uint64_t>(En) << 52))));
-  return static_cast<uint64_t>(X) + 0x0080808080808080ull;
+  return static_cast<uint64_t>(X) + bias;
 }
 
 // Digits of A for rows [r0, r1) (r0 a multiple of 4), column-major planes
@@ -181,7 +192,8 @@ __device__ __forceinline__ void transpose4(const uint32_t* p, uint32_t* w) {
   w[3] = __byte_perm(b, d, 0x7632);
 }
 
-__global__ void __launch_bounds__(256) slice_a_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+template <class T, int S>
+__global__ void __launch_bounds__(256) slice_a_kernel(const T* __restrict__ A, int64_t m, int64_t n, int64_t lda,
                                                       int64_t r0, int64_t r1, const int* __restrict__ rowexp,
                                                       const int* __restrict__ colexp, int8_t* __restrict__ rs,
                                                       int8_t* __restrict__ cs, int64_t m_pad, int64_t n_pad) {
@@ -190,12 +202,12 @@ __global__ void __launch_bounds__(256) slice_a_kernel(const double* __restrict__
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t j = e / quads, i0 = r0 + (e - j * quads) * 4;
-    uint32_t wr[kS] = {}, wc[kS] = {};
+    uint32_t wr[S] = {}, wc[S] = {};
     if (j < n) {
       const int fj = cs ? colexp[j] : 0;
       double v[4];
       int er[4];
-      if (i0 + 3 < m && ((j * lda + i0) & 1) == 0) {
+      if (i0 + 3 < m && sizeof(T) == 8 && ((j * lda + i0) & 1) == 0) {
         const double2 p0 = *reinterpret_cast<const double2*>(A + j * lda + i0);
         const double2 p1 = *reinterpret_cast<const double2*>(A + j * lda + i0 + 2);
         v[0] = p0.x, v[1] = p0.y, v[2] = p1.x, v[3] = p1.y;
@@ -207,7 +219,7 @@ __global__ void __launch_bounds__(256) slice_a_kernel(const double* __restrict__
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const bool in = i0 + b < m;
-          v[b] = in ? A[j * lda + i0 + b] : 0.0;
+          v[b] = in ? static_cast<double>(A[j * lda + i0 + b]) : 0.0;
           er[b] = (in && rs) ? rowexp[i0 + b] : 0;
         }
       }
@@ -216,12 +228,12 @@ __global__ void __launch_bounds__(256) slice_a_kernel(const double* __restrict__
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         if (rs) {
-          const uint64_t x = balanced7(v[b], er[b]);
+          const uint64_t x = balanced<S>(v[b], er[b]);
           lr[b] = static_cast<uint32_t>(x) ^ 0x80808080u;
           hr[b] = static_cast<uint32_t>(x >> 32) ^ 0x80808080u;
         }
         if (cs) {
-          const uint64_t x = balanced7(v[b], fj);
+          const uint64_t x = balanced<S>(v[b], fj);
           lc[b] = static_cast<uint32_t>(x) ^ 0x80808080u;
           hc[b] = static_cast<uint32_t>(x >> 32) ^ 0x80808080u;
         }
@@ -232,21 +244,21 @@ __global__ void __launch_bounds__(256) slice_a_kernel(const double* __restrict__
         transpose4(lr, t);
         transpose4(hr, t + 4);
 #pragma unroll
-        for (int q = 0; q < kS; ++q) wr[q] = t[6 - q];
+        for (int q = 0; q < S; ++q) wr[q] = t[S - 1 - q];
       }
       if (cs) {
         uint32_t t[8];
         transpose4(lc, t);
         transpose4(hc, t + 4);
 #pragma unroll
-        for (int q = 0; q < kS; ++q) wc[q] = t[6 - q];
+        for (int q = 0; q < S; ++q) wc[q] = t[S - 1 - q];
       }
     } else {
       // padding columns: zero digits
     }
     const int64_t off = j * m_pad + i0;
 #pragma unroll
-    for (int s = 0; s < kS; ++s) {
+    for (int s = 0; s < S; ++s) {
       const int64_t o = static_cast<int64_t>(s) * n_pad * m_pad + off;
       if (rs) *reinterpret_cast<uint32_t*>(rs + o) = wr[s];
       if (cs) *reinterpret_cast<uint32_t*>(cs + o) = wc[s];
@@ -278,6 +290,7 @@ __global__ void col_exp_kernel(const double* __restrict__ R, int64_t K, int64_t 
 }
 
 // Digits of R(i,c) 2^-f_c into [kS][N_pad][K_pad] (4 rows per thread).
+template <int S>
 __global__ void slice_r_kernel(const double* __restrict__ R, int64_t K, int64_t N, int64_t ldr,
                                const int* __restrict__ colexp, int8_t* __restrict__ out, int64_t K_pad, int64_t N_pad) {
   const int64_t quads = K_pad / 4;
@@ -290,7 +303,7 @@ __global__ void slice_r_kernel(const double* __restrict__ R, int64_t K, int64_t 
     for (int b = 0; b < 4; ++b) {
       const int64_t i = i0 + b;
       const double v = (i < K && c < N) ? R[c * ldr + i] : 0.0;
-      const uint64_t x = balanced7(v, fc);
+      const uint64_t x = balanced<S>(v, fc);
       lo[b] = static_cast<uint32_t>(x) ^ 0x80808080u;
       hi[b] = static_cast<uint32_t>(x >> 32) ^ 0x80808080u;
     }
@@ -298,8 +311,8 @@ __global__ void slice_r_kernel(const double* __restrict__ R, int64_t K, int64_t 
     transpose4(lo, t);
     transpose4(hi, t + 4);
 #pragma unroll
-    for (int s = 0; s < kS; ++s)
-      *reinterpret_cast<uint32_t*>(out + (static_cast<int64_t>(s) * N_pad + c) * K_pad + i0) = t[6 - s];
+    for (int s = 0; s < S; ++s)
+      *reinterpret_cast<uint32_t*>(out + (static_cast<int64_t>(s) * N_pad + c) * K_pad + i0) = t[S - 1 - s];
   }
 }
 
@@ -365,12 +378,13 @@ __device__ __forceinline__ uint64_t umma_desc_mn(const void* p) {
 
 // L_MN: the L digit planes are read M-major (column-major A digits serving
 // Y = A X), else K-major (A^T Q).
-template <bool L_MN>
+template <bool L_MN, int S>
 __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmL,
                                                                   const __grid_constant__ CUtensorMap tmR,
                                                                   const OzParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kS = S, kStages = Dig<S>::stages, kTmemCols = Dig<S>::tmem_cols;
   constexpr int ASZ = kS * OBM * OBK, BSZ = kS * OBN * OBK;
   uint8_t* sA = smem;
   uint8_t* sB = sA + kStages * ASZ;
@@ -582,12 +596,15 @@ bool digit_tmap(CUtensorMap* tm, const int8_t* base, int64_t rows, int64_t inner
 // 2-stage ring), so the caller chooses.
 // L_mn: L planes are [kS][K_pad][L_M] (M contiguous, L_rows = K_pad rows per
 // plane, L_M = M extent), else [kS][L_rows][K_pad].
-cudaError_t launch_digit_gemm(const int8_t* L, int64_t L_rows, bool L_mn, int64_t L_M, const int8_t* R, int64_t R_rows,
-                              int64_t K_pad, int64_t row0, int64_t rows, int64_t N_real, int splits,
-                              const OzParams& base, bool multicast, cudaStream_t st) {
+template <int S>
+cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int64_t L_M, const int8_t* R,
+                                int64_t R_rows, int64_t K_pad, int64_t row0, int64_t rows, int64_t N_real, int splits,
+                                const OzParams& base, bool multicast, cudaStream_t st) {
+  constexpr int kS = S;
+  constexpr size_t kSmemBytes = Dig<S>::smem;
   static bool cfg = false;
   if (!cfg) {
-    for (auto fn : {ozaki_gemm_kernel<true>, ozaki_gemm_kernel<false>}) {
+    for (auto fn : {ozaki_gemm_kernel<true, S>, ozaki_gemm_kernel<false, S>}) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
       if (e != cudaSuccess) return e;
     }
@@ -635,11 +652,40 @@ cudaError_t launch_digit_gemm(const int8_t* L, int64_t L_rows, bool L_mn, int64_
   attr[0].val.clusterDim.z = 1;
   cfgl.attrs = attr;
   cfgl.numAttrs = 1;
-  cudaError_t e = L_mn ? cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<true>, tl, tr, p)
-                       : cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<false>, tl, tr, p);
+  cudaError_t e = L_mn ? cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<true, S>, tl, tr, p)
+                       : cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<false, S>, tl, tr, p);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+cudaError_t launch_digit_gemm(int S, const int8_t* L, int64_t L_rows, bool L_mn, int64_t L_M, const int8_t* R,
+                              int64_t R_rows, int64_t K_pad, int64_t row0, int64_t rows, int64_t N_real, int splits,
+                              const OzParams& base, bool multicast, cudaStream_t st) {
+  return S == 4 ? launch_digit_gemm_s<4>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
+                                         multicast, st)
+                : launch_digit_gemm_s<7>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
+                                         multicast, st);
+}
+
+void slice_r(int S, const double* R, int64_t K, int64_t N, int64_t ldr, const int* colexp, int8_t* out, int64_t K_pad,
+             int64_t N_pad, cudaStream_t st) {
+  if (S == 4)
+    slice_r_kernel<4><<<1184, 256, 0, st>>>(R, K, N, ldr, colexp, out, K_pad, N_pad);
+  else
+    slice_r_kernel<7><<<1184, 256, 0, st>>>(R, K, N, ldr, colexp, out, K_pad, N_pad);
+}
+
+template <class T>
+void slice_a(int S, const T* A, int64_t m, int64_t n, int64_t lda, int64_t r0, int64_t r1, const int* rowexp,
+             const int* colexp, int8_t* rs, int8_t* cs, int64_t m_pad, int64_t n_pad, cudaStream_t st) {
+  const int64_t items = (r1 - r0 + 3) / 4 * n_pad;
+  if (items <= 0) return;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((items + 255) / 256, 148 * 32));
+  if (S == 4)
+    slice_a_kernel<T, 4><<<blocks, 256, 0, st>>>(A, m, n, lda, r0, r1, rowexp, colexp, rs, cs, m_pad, n_pad);
+  else
+    slice_a_kernel<T, 7><<<blocks, 256, 0, st>>>(A, m, n, lda, r0, r1, rowexp, colexp, rs, cs, m_pad, n_pad);
 }
 
 }  // namespace
@@ -651,18 +697,19 @@ bool ozaki_enabled(int64_t m, int64_t n) {
   return m * n >= (int64_t(1) << 26);  // large passes only: the digit planes cost 14 m n bytes
 }
 
-OzakiA ozaki_layout(int64_t m, int64_t n) {
+OzakiA ozaki_layout(int64_t m, int64_t n, int digits) {
   OzakiA a{};
   a.m = m;
   a.n = n;
+  a.digits = digits;
   a.m_pad = roundup(std::max<int64_t>(m, 1), 256);
   a.n_pad = roundup(std::max<int64_t>(n, 1), OBM);
   return a;
 }
 
-size_t ozaki_a_bytes(int64_t m, int64_t n) {
-  const OzakiA a = ozaki_layout(m, n);
-  const size_t planes = static_cast<size_t>(kS) * a.m_pad * a.n_pad;
+size_t ozaki_a_bytes(int64_t m, int64_t n, int digits) {
+  const OzakiA a = ozaki_layout(m, n, digits);
+  const size_t planes = static_cast<size_t>(digits) * a.m_pad * a.n_pad;
   return 2 * planes + sizeof(int) * (2 * a.m_pad + a.n_pad) + sizeof(uint32_t) * (a.m_pad / 256) * a.n_pad + 1024;
 }
 
@@ -676,9 +723,9 @@ int64_t stats_chunks(int64_t rows, int64_t n) {
 
 int64_t ozaki_ssq_slots(int64_t rows, int64_t n) { return ((rows + 255) / 256) * stats_chunks(rows, n); }
 
-void ozaki_bind(void* work, int64_t m, int64_t n, OzakiA* out) {
-  *out = ozaki_layout(m, n);
-  const size_t planes = static_cast<size_t>(kS) * out->m_pad * out->n_pad;
+void ozaki_bind(void* work, int64_t m, int64_t n, int digits, OzakiA* out) {
+  *out = ozaki_layout(m, n, digits);
+  const size_t planes = static_cast<size_t>(digits) * out->m_pad * out->n_pad;
   int8_t* base = static_cast<int8_t*>(work);
   out->rs = base;
   out->cs = base + planes;
@@ -688,8 +735,9 @@ void ozaki_bind(void* work, int64_t m, int64_t n, OzakiA* out) {
   out->colpart = out->rowhi + out->m_pad;
 }
 
-cudaError_t ozaki_prepare_rows(const double* A, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
-                               double* ssq_part, bool slice_rows, cudaStream_t st) {
+template <class T>
+cudaError_t prepare_rows_t(const T* A, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a, double* ssq_part,
+                           bool slice_rows, cudaStream_t st) {
   if (r1 == a.m && a.m_pad > a.m) {  // padding rows: exponent 0, zero column maxima
     cudaError_t e = cudaMemsetAsync(a.rowexp + a.m, 0, sizeof(int) * (a.m_pad - a.m), st);
     if (e != cudaSuccess) return e;
@@ -705,37 +753,45 @@ cudaError_t ozaki_prepare_rows(const double* A, int64_t lda, int64_t r0, int64_t
       if (e != cudaSuccess) return e;
     }
     dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>((a.n + chunk - 1) / chunk));
-    stats_kernel<<<grid, 256, 0, st>>>(A, r0, r1, a.n, lda, a.n_pad, chunk, rowhi, a.colpart, ssq_part);
+    stats_kernel<T><<<grid, 256, 0, st>>>(A, r0, r1, a.n, lda, a.n_pad, chunk, rowhi, a.colpart, ssq_part);
     rowexp_kernel<<<static_cast<unsigned>(std::min<int64_t>((rows + 255) / 256, 1184)), 256, 0, st>>>(rowhi, r0, r1,
                                                                                                        a.rowexp);
     count_launch(2);
   }
   if (slice_rows) {
     const int64_t s1 = r1 == a.m ? a.m_pad : r1;
-    const int64_t items = (s1 - r0 + 3) / 4 * a.n_pad;
-    if (items > 0) {
-      slice_a_kernel<<<static_cast<unsigned>(std::min<int64_t>((items + 255) / 256, 148 * 32)), 256, 0, st>>>(
-          A, a.m, a.n, lda, r0, s1, a.rowexp, nullptr, a.rs, nullptr, a.m_pad, a.n_pad);
-      count_launch();
-    }
+    slice_a<T>(a.digits, A, a.m, a.n, lda, r0, s1, a.rowexp, nullptr, a.rs, nullptr, a.m_pad, a.n_pad, st);
+    count_launch();
   }
   return cudaGetLastError();
 }
 
-cudaError_t ozaki_prepare_cols(const double* A, int64_t lda, const OzakiA& a, bool slice_rows_too, cudaStream_t st) {
+template <class T>
+cudaError_t prepare_cols_t(const T* A, int64_t lda, const OzakiA& a, bool slice_rows_too, cudaStream_t st) {
   const int64_t nblk = (a.m + 255) / 256;
   colexp_kernel<<<static_cast<unsigned>((a.n_pad + 255) / 256), 256, 0, st>>>(a.colpart, nblk, a.n, a.n_pad, a.colexp);
-  const int64_t items = a.m_pad / 4 * a.n_pad;
-  slice_a_kernel<<<static_cast<unsigned>(std::min<int64_t>((items + 255) / 256, 148 * 32)), 256, 0, st>>>(
-      A, a.m, a.n, lda, 0, a.m_pad, a.rowexp, a.colexp, slice_rows_too ? a.rs : nullptr, a.cs, a.m_pad, a.n_pad);
+  slice_a<T>(a.digits, A, a.m, a.n, lda, 0, a.m_pad, a.rowexp, a.colexp, slice_rows_too ? a.rs : nullptr, a.cs,
+             a.m_pad, a.n_pad, st);
   count_launch(2);
   return cudaGetLastError();
+}
+
+cudaError_t ozaki_prepare_rows(const void* A, bool f32, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
+                               double* ssq_part, bool slice_rows, cudaStream_t st) {
+  return f32 ? prepare_rows_t(static_cast<const float*>(A), lda, r0, r1, a, ssq_part, slice_rows, st)
+             : prepare_rows_t(static_cast<const double*>(A), lda, r0, r1, a, ssq_part, slice_rows, st);
+}
+
+cudaError_t ozaki_prepare_cols(const void* A, bool f32, int64_t lda, const OzakiA& a, bool slice_rows_too,
+                               cudaStream_t st) {
+  return f32 ? prepare_cols_t(static_cast<const float*>(A), lda, a, slice_rows_too, st)
+             : prepare_cols_t(static_cast<const double*>(A), lda, a, slice_rows_too, st);
 }
 
 size_t ozaki_nn_work_bytes(const OzakiA& a, int64_t rows, int64_t ell) {
   const int64_t lp = roundup(ell, OBN);
   const int splits = static_cast<int>((a.n_pad + kSplitK - 1) / kSplitK);
-  return static_cast<size_t>(kS) * lp * a.n_pad + sizeof(int) * lp + 256 +
+  return static_cast<size_t>(a.digits) * lp * a.n_pad + sizeof(int) * lp + 256 +
          (splits > 1 ? sizeof(double) * static_cast<size_t>(splits) * rows * ell : 0);
 }
 
@@ -743,10 +799,10 @@ cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, i
                      int64_t ldy, void* work, cudaStream_t st) {
   const int64_t lp = roundup(ell, OBN), rows = r1 - r0;
   int8_t* xd = static_cast<int8_t*>(work);
-  int* colexp = reinterpret_cast<int*>(xd + static_cast<size_t>(kS) * lp * a.n_pad);
+  int* colexp = reinterpret_cast<int*>(xd + static_cast<size_t>(a.digits) * lp * a.n_pad);
   double* ws = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(colexp) + ((sizeof(int) * lp + 255) / 256) * 256);
   col_exp_kernel<<<static_cast<unsigned>(ell), 256, 0, st>>>(X, a.n, ldx, nullptr, colexp);
-  slice_r_kernel<<<1184, 256, 0, st>>>(X, a.n, ell, ldx, colexp, xd, a.n_pad, lp);
+  slice_r(a.digits, X, a.n, ell, ldx, colexp, xd, a.n_pad, lp, st);
   count_launch(2);
   // K = n beyond kSplitK would overflow the int32 group sums: split K
   const int splits = static_cast<int>((a.n_pad + kSplitK - 1) / kSplitK);
@@ -757,7 +813,8 @@ cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, i
   p.rowexp = a.rowexp;
   p.colexp = colexp;
   p.ws_mode = splits > 1 ? 1 : 0;
-  cudaError_t e = launch_digit_gemm(a.rs, a.n_pad, true, a.m_pad, xd, lp, a.n_pad, r0, rows, ell, splits, p, false, st);
+  cudaError_t e =
+      launch_digit_gemm(a.digits, a.rs, a.n_pad, true, a.m_pad, xd, lp, a.n_pad, r0, rows, ell, splits, p, false, st);
   if (e != cudaSuccess || splits == 1) return e;
   const int64_t total = rows * ell;
   reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(
@@ -769,7 +826,7 @@ cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, i
 size_t ozaki_tn_work_bytes(const OzakiA& a, int64_t ell) {
   const int64_t lp = roundup(ell, OBN);
   const int splits = static_cast<int>((a.m_pad + kSplitK - 1) / kSplitK);
-  return static_cast<size_t>(kS) * lp * a.m_pad + sizeof(int) * lp + 256 +
+  return static_cast<size_t>(a.digits) * lp * a.m_pad + sizeof(int) * lp + 256 +
          sizeof(double) * static_cast<size_t>(splits) * a.n * ell;
 }
 
@@ -777,11 +834,11 @@ cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell,
                      cudaStream_t st) {
   const int64_t lp = roundup(ell, OBN);
   int8_t* qd = static_cast<int8_t*>(work);
-  int* colexp = reinterpret_cast<int*>(qd + static_cast<size_t>(kS) * lp * a.m_pad);
+  int* colexp = reinterpret_cast<int*>(qd + static_cast<size_t>(a.digits) * lp * a.m_pad);
   double* ws = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(colexp) + ((sizeof(int) * lp + 255) / 256) * 256);
-  // column-scaled digits of A: Z(j, c) = 2^(f_j + g_c) sum_g 2^-7(g+2) acc_g
+  // column-scaled digits of A: Z(j, c) = 2^(f_j + g_c) sum_g 2^-(12+8g) acc_g
   col_exp_kernel<<<static_cast<unsigned>(ell), 256, 0, st>>>(Q, a.m, ldq, nullptr, colexp);
-  slice_r_kernel<<<1184, 256, 0, st>>>(Q, a.m, ell, ldq, colexp, qd, a.m_pad, lp);
+  slice_r(a.digits, Q, a.m, ell, ldq, colexp, qd, a.m_pad, lp, st);
   count_launch(2);
   const int splits = static_cast<int>((a.m_pad + kSplitK - 1) / kSplitK);
   OzParams p{};
@@ -791,7 +848,8 @@ cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell,
   p.rowexp = a.colexp;  // output row j of A^T Q = column j of A
   p.colexp = colexp;
   p.ws_mode = splits > 1 ? 1 : 0;
-  cudaError_t e = launch_digit_gemm(a.cs, a.n_pad, false, 0, qd, lp, a.m_pad, 0, a.n, ell, splits, p, true, st);
+  cudaError_t e =
+      launch_digit_gemm(a.digits, a.cs, a.n_pad, false, 0, qd, lp, a.m_pad, 0, a.n, ell, splits, p, true, st);
   if (e != cudaSuccess || splits == 1) return e;
   const int64_t total = a.n * ell;
   reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(

@@ -396,21 +396,21 @@ struct OzPasses {
   OzakiA a{};
   DBuf planes, work;
   Status init(rfgpu_ctx* c, const rfgpu_matrix* m, int64_t ell) {
-    on = !m->f32 && ozaki_enabled(m->m, m->n) && m->m > 0 && m->n > 0;
+    on = ozaki_enabled(m->m, m->n) && m->m > 0 && m->n > 0;
     if (!on) return {};
-    const OzakiA lay = ozaki_layout(m->m, m->n);
-    RF_TRY(planes.alloc(ozaki_a_bytes(m->m, m->n), c->stream));
+    const int digits = m->f32 ? 4 : 7;  // FP32 data: 4 digits (30 bits) per element
+    const OzakiA lay = ozaki_layout(m->m, m->n, digits);
+    RF_TRY(planes.alloc(ozaki_a_bytes(m->m, m->n, digits), c->stream));
     RF_TRY(work.alloc(std::max(ozaki_nn_work_bytes(lay, m->m, ell), ozaki_tn_work_bytes(lay, ell)), c->stream));
-    ozaki_bind(planes.p, m->m, m->n, &a);
+    ozaki_bind(planes.p, m->m, m->n, digits, &a);
     return {};
   }
   // Whole resident A: stats (one read), then the digit sets (one read):
   // row-scaled (A X) only when `rows`, column-scaled (A^T Q) always.
   Status prepare(rfgpu_ctx* c, const rfgpu_matrix* m, double* ssq, bool rows = true) {
     Timed t(c, "ozaki_slice");
-    const double* A = static_cast<const double*>(m->dev);
-    RF_CUDA(ozaki_prepare_rows(A, m->lda, 0, m->m, a, ssq, false, c->stream));
-    RF_CUDA(ozaki_prepare_cols(A, m->lda, a, rows, c->stream));
+    RF_CUDA(ozaki_prepare_rows(m->dev, m->f32, m->lda, 0, m->m, a, ssq, false, c->stream));
+    RF_CUDA(ozaki_prepare_cols(m->dev, m->f32, m->lda, a, rows, c->stream));
     return {};
   }
 };
@@ -434,7 +434,7 @@ Status pass1_rows(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
       RF_TRY(oz.prepare(c, a, ssq));
     } else {
       Timed t(c, "ozaki_slice");
-      RF_CUDA(ozaki_prepare_rows(A, a->lda, r0, r1, oz.a, ssq, true, c->stream));
+      RF_CUDA(ozaki_prepare_rows(A, false, a->lda, r0, r1, oz.a, ssq, true, c->stream));
     }
     Timed t(c, "pass_nn");
     RF_CUDA(ozaki_nn(oz.a, r0, r1, G, a->n, ell, Y, ldy, oz.work.p, c->stream));
@@ -507,7 +507,8 @@ Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, 
   }
   if (s.ok() && oz.on) {  // all rows landed: column exponents and the A^T Q digits
     Timed t(c, "ozaki_slice");
-    if (ozaki_prepare_cols(A, lda, oz.a, false, st) != cudaSuccess) s = make_err(RFGPU_ECUDA, "pass 1: slicing failed");
+    if (ozaki_prepare_cols(A, false, lda, oz.a, false, st) != cudaSuccess)
+      s = make_err(RFGPU_ECUDA, "pass 1: slicing failed");
   }
   a->src = nullptr;  // issued: every later consumer is ordered after the waits above
   cudaEventDestroy(ready);
@@ -1960,7 +1961,18 @@ int rfgpu_single_pass_svd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const doub
     RF_TRY(yc.alloc(sizeof(double) * m * ell, s));
     RF_TRY(yr.alloc(sizeof(double) * n * ell, s));
     RF_TRY(scratch.alloc(sizeof(double) * m * ell, s));
+    bool on_digits = false;
     {
+      OzPasses oz;  // both sketches on the INT8 tensor cores at pass sizes (FP32 data: 4 digits)
+      RF_TRY(oz.init(c, a, ell));
+      if (oz.on) {
+        RF_TRY(oz.prepare(c, a, nullptr, true));
+        RF_TRY(pass_nn(c, a, gc, ell, yc.d(), m, &oz));                       // Yc = A Gc
+        RF_TRY(pass_tn_raw(c, a, gr, ldgr, ell, yr.d(), &oz));                // Yr = A^T Gr
+        on_digits = true;
+      }
+    }  // digit planes released before the core
+    if (!on_digits) {
       Timed t(c, "dual_sketch");
       if (!a->f32) {
         RF_TRY(dual_sketch_block(c, static_cast<const double*>(a->dev), m, n, a->lda, 0, n, gc, gr, ldgr, ell, yc.d(), yr.d(),

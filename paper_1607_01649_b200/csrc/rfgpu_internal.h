@@ -47,21 +47,23 @@ struct OzakiA {
   uint32_t* rowhi;    // m_pad row maxima (high words of |A(i,:)|)
   uint32_t* colpart;  // (m_pad / 256) x n_pad per-block column maxima (high words)
   int64_t m, n, m_pad, n_pad;
+  int digits;   // 7 (FP64 A) or 4 (FP32 A)
 };
 bool ozaki_enabled(int64_t m, int64_t n);  // RFGPU_OZAKI=0/1 overrides the size rule
-OzakiA ozaki_layout(int64_t m, int64_t n);  // shapes only (no buffers)
-size_t ozaki_a_bytes(int64_t m, int64_t n);
-void ozaki_bind(void* work, int64_t m, int64_t n, OzakiA* out);  // carve a work buffer of ozaki_a_bytes
+OzakiA ozaki_layout(int64_t m, int64_t n, int digits);  // shapes only (no buffers)
+size_t ozaki_a_bytes(int64_t m, int64_t n, int digits);
+void ozaki_bind(void* work, int64_t m, int64_t n, int digits, OzakiA* out);  // carve ozaki_a_bytes
 int64_t ozaki_ssq_slots(int64_t rows, int64_t n);  // ||A||_F^2 partials of a row block
 // Rows [r0, r1) (r0 a multiple of 256): row exponents, ||A||_F^2 partials
 // (ozaki_ssq_slots(r1 - r0, n) of them), column maxima of these rows, and, with
 // slice_rows, the row-scaled digits of these rows (all A X needs).
-cudaError_t ozaki_prepare_rows(const double* A, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
+cudaError_t ozaki_prepare_rows(const void* A, bool f32, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
                                double* ssq_part, bool slice_rows, cudaStream_t st);
 // After every row block's stats: column exponents and the column-scaled
 // digits (A^T Q); slice_rows_too also writes the row-scaled digits in the
 // same read of A.
-cudaError_t ozaki_prepare_cols(const double* A, int64_t lda, const OzakiA& a, bool slice_rows_too, cudaStream_t st);
+cudaError_t ozaki_prepare_cols(const void* A, bool f32, int64_t lda, const OzakiA& a, bool slice_rows_too,
+                               cudaStream_t st);
 size_t ozaki_nn_work_bytes(const OzakiA& a, int64_t rows, int64_t ell);
 // Y(r0:r1, 0:ell) = A(r0:r1, :) X  (X n x ell, col-major)
 cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, int64_t ldx, int64_t ell, double* Y,
