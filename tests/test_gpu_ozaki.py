@@ -15,6 +15,13 @@ import paper_1607_01649_b200 as rf
 pytestmark = pytest.mark.gpu
 
 
+def planted(port, m, n, sigma, seed=1, noise=0.0):
+    a = port.planted(m, n, np.asarray(sigma, dtype=np.float64), seed)
+    if noise:
+        a = a + noise * port.gaussian(seed, "noise.N", m, n)
+    return np.asfortranarray(a)
+
+
 @pytest.fixture
 def ozaki(monkeypatch):
     monkeypatch.setenv("RFGPU_OZAKI", "1")
@@ -93,3 +100,38 @@ def test_streamed_panels_on_digit_gemm(ctx, ozaki, monkeypatch):
     finally:
         dm.free()
     assert np.max(np.abs(host.D - dev.D) / dev.D) < 1e-12
+
+
+@pytest.mark.parametrize("f32", [False, True])
+def test_single_pass_device_on_digit_gemm(ctx, port, ozaki, f32):
+    """rfgpu_single_pass_svd_device with both sketches on the digit path:
+    FP64 data (7 digits) within 1e-8 of the restated oracle, FP32 data (4
+    digits, 10 products) within the FP32 bar 1e-4 of the oracle run on the
+    same rounded data."""
+    import ctypes as C
+    import torch
+    m, n, k, p = 1500, 1200, 60, 10
+    ell = k + p
+    a = planted(port, m, n, np.exp(-np.arange(1, 201) / 10.0), seed=1, noise=1e-4)
+    if f32:
+        a = np.asfortranarray(a.astype(np.float32).astype(np.float64))
+    want = port.single_pass_svd(a, k, p, 1, block=64)
+    dev = torch.device("cuda")
+    At = torch.from_numpy(np.ascontiguousarray(a.T)).to(dev)  # column-major A as rows of A^T
+    if f32:
+        At = At.float()
+    dm = rf.DeviceMatrix.wrap(ctx, At.data_ptr(), m, n, m, f32=f32, keep=At)
+    gc = torch.from_numpy(np.asfortranarray(rf.gaussian(1, "spsvd.Gc", n, ell)).reshape(-1, order="F")).to(dev)
+    gr = torch.from_numpy(np.asfortranarray(rf.gaussian(1, "spsvd.Gr", m, ell)).reshape(-1, order="F")).to(dev)
+    U = torch.empty(m * ell, device=dev, dtype=torch.float64)
+    D = torch.empty(ell, device=dev, dtype=torch.float64)
+    V = torch.empty(n * ell, device=dev, dtype=torch.float64)
+    r = C.c_int64()
+    rf._check(rf.lib().rfgpu_single_pass_svd_device(ctx.handle, dm.handle, C.c_void_p(gc.data_ptr()),
+                                                      C.c_void_p(gr.data_ptr()), k, ell, C.c_void_p(U.data_ptr()),
+                                                      C.c_void_p(D.data_ptr()), C.c_void_p(V.data_ptr()), C.byref(r)))
+    torch.cuda.synchronize()
+    got = D.cpu().numpy()[: r.value]
+    tol = 1e-4 if f32 else 1e-8
+    assert r.value == k
+    assert np.max(np.abs(got - want.D) / want.D) < tol
