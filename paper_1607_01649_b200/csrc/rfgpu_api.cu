@@ -972,6 +972,69 @@ Status row_sketch_t(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Gt, int64
   return {};
 }
 
+// Two tall SVDs of the same width (svd_tall_dev semantics each): both
+// orthonormalised, then their l x l Jacobi SVDs in ONE launch (one cluster
+// each), so the two latency-bound round sequences run side by side.
+struct TallSvd {
+  const double* M;
+  int64_t rows, ldm;
+  double* U;
+  double* S;
+  double* V;
+  bool dist;
+};
+
+Status svd_tall_pair(rfgpu_ctx* c, const TallSvd& x, const TallSvd& y, int64_t cols) {
+  cudaStream_t st = c->stream;
+  struct Side {
+    DBuf q, rr, r2i, ur, ur2, jw, inf;
+    Basis b;
+    int64_t ldr = 0;
+  };
+  Side sd[2];
+  const TallSvd* t[2] = {&x, &y};
+  for (int i = 0; i < 2; ++i) {
+    sd[i].ldr = even(t[i]->rows);
+    RF_TRY(sd[i].q.alloc(sizeof(double) * std::max<int64_t>(1, sd[i].ldr * cols), st));
+    RF_TRY(sd[i].rr.alloc(sizeof(double) * cols * cols, st));
+    RF_TRY(sd[i].r2i.alloc(sizeof(double) * cols * cols, st));
+    RF_TRY(sd[i].inf.alloc(64, st));
+    sd[i].b.Q = sd[i].q.d();
+    sd[i].b.ldq = sd[i].ldr;
+    RF_TRY(orth(c, t[i]->M, t[i]->rows, cols, t[i]->ldm, &sd[i].b, sd[i].r2i.d(), sd[i].rr.d(), t[i]->dist, true));
+  }
+  if (!sd[0].b.fast || !sd[1].b.fast) {  // rank-deficient side: one at a time
+    RF_TRY(svd_tall_dev(c, x.M, x.rows, cols, x.ldm, x.U, x.S, x.V, x.dist));
+    return svd_tall_dev(c, y.M, y.rows, cols, y.ldm, y.U, y.S, y.V, y.dist);
+  }
+  JacobiProblem pj[2];
+  for (int i = 0; i < 2; ++i) {
+    RF_TRY(sd[i].ur.alloc(sizeof(double) * cols * cols, st));
+    RF_TRY(sd[i].ur2.alloc(sizeof(double) * cols * cols, st));
+    const size_t jwb = jacobi_work_bytes(cols, cols);
+    RF_TRY(sd[i].jw.alloc(std::max<size_t>(jwb, 16), st));
+    int* info = sd[i].inf.as<int>();
+    pj[i] = JacobiProblem{sd[i].rr.d(), sd[i].ur.d(), t[i]->S, t[i]->V, sd[i].jw.d(), info, info + 1};
+  }
+  {
+    Timed tj(c, "jacobi");
+    RF_CUDA(jacobi_svd_pair(pj[0], pj[1], cols, cols, st));
+  }
+  for (int i = 0; i < 2; ++i) {
+    RF_TRY(gemm(c, false, cols, cols, cols, sd[i].b.R2inv, cols, sd[i].ur.d(), cols, sd[i].ur2.d(), cols));
+    RF_TRY(gemm(c, false, t[i]->rows, cols, cols, sd[i].b.Q, sd[i].ldr, sd[i].ur2.d(), cols, t[i]->U, t[i]->rows));
+  }
+  int h[4];
+  for (int i = 0; i < 2; ++i)
+    RF_CUDA(cudaMemcpyAsync(h + 2 * i, sd[i].inf.d(), 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  RF_CUDA(cudaStreamSynchronize(st));
+  if (std::getenv("RFGPU_DEBUG"))
+    std::fprintf(stderr, "[rfgpu] svd_tall pair %lldx%lld + %lldx%lld jacobi info=%d/%d sweeps=%d/%d\n",
+                 (long long)x.rows, (long long)cols, (long long)y.rows, (long long)cols, h[0], h[2], h[1], h[3]);
+  if (h[0] == 1 || h[2] == 1) return make_err(RFGPU_ECONVERGENCE, "svd_dense: Jacobi sweeps did not converge");
+  return {};
+}
+
 // ---- single pass (lowrank.cpp:160-220) ------------------------------------------
 // Core of single_pass_svd from the two sketches, all on the device:
 // dominant_left(Yc, k), dominant_left(Yr, k) (:178-179), the small products
@@ -997,8 +1060,9 @@ Status single_pass_core(rfgpu_ctx* c, const double* Yc, int64_t m, const double*
   RF_TRY(ur.alloc(sizeof(double) * n * ell, st));
   RF_TRY(sr.alloc(sizeof(double) * ell, st));
   RF_TRY(vr.alloc(sizeof(double) * ell * ell, st));
-  RF_TRY(svd_tall_dev(c, Yc, m, ell, m, uc.d(), sc.d(), vc.d(), dist));  // Qc = uc(:, :kk)
-  RF_TRY(svd_tall_dev(c, Yr, n, ell, n, ur.d(), sr.d(), vr.d()));  // Qr = ur(:, :kk)
+  // Qc = uc(:, :kk), Qr = ur(:, :kk): the two dominant_left SVDs side by side
+  RF_TRY(svd_tall_pair(c, TallSvd{Yc, m, m, uc.d(), sc.d(), vc.d(), dist}, TallSvd{Yr, n, n, ur.d(), sr.d(), vr.d(), false},
+                       ell));
   RF_TRY(P.alloc(sizeof(double) * ell * kk, st));
   RF_TRY(E.alloc(sizeof(double) * ell * kk, st));
   RF_TRY(W.alloc(sizeof(double) * kk * ell, st));
@@ -1018,8 +1082,8 @@ Status single_pass_core(rfgpu_ctx* c, const double* Yc, int64_t m, const double*
   RF_TRY(uw.alloc(sizeof(double) * ell * kk, st));
   RF_TRY(sw.alloc(sizeof(double) * kk, st));
   RF_TRY(vw.alloc(sizeof(double) * kk * kk, st));
-  RF_TRY(svd_tall_dev(c, P.d(), ell, kk, ell, up.d(), sp.d(), vp.d()));
-  RF_TRY(svd_tall_dev(c, Wt.d(), ell, kk, ell, uw.d(), sw.d(), vw.d()));
+  RF_TRY(svd_tall_pair(c, TallSvd{P.d(), ell, ell, up.d(), sp.d(), vp.d(), false},
+                       TallSvd{Wt.d(), ell, ell, uw.d(), sw.d(), vw.d(), false}, kk));
   // RHS = P^T E + F W^T
   RF_TRY(rhs.alloc(sizeof(double) * kk * kk, st));
   RF_TRY(tmp.alloc(sizeof(double) * kk * kk, st));

@@ -91,6 +91,17 @@ size_t chol_inv_work_bytes(int64_t c);
 cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double* S, double* V, double* work,
                        int* info, int* sweeps_out, cudaStream_t st);
 size_t jacobi_work_bytes(int64_t mr, int64_t c);
+// Two independent same-shape problems in one launch (one cluster each).
+struct JacobiProblem {
+  const double* X;
+  double* U;
+  double* S;
+  double* V;
+  double* work;  // jacobi_work_bytes(mr, c)
+  int* info;
+  int* sweeps;
+};
+cudaError_t jacobi_svd_pair(const JacobiProblem& a, const JacobiProblem& b, int64_t mr, int64_t c, cudaStream_t st);
 
 // y = sum of squares of x[0..n) into *out (fixed-order two-level reduction).
 cudaError_t sumsq(const double* x, int64_t n, double* partials, double* out, cudaStream_t st);

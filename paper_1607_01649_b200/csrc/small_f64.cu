@@ -159,9 +159,13 @@ __device__ __forceinline__ void pair_of(int r, int k, int cc, int* a, int* b) {
 }
 
 template <bool SMEM>
-__global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const JacobiParams p) {
+// Two independent problems of the same shape may share a launch: cluster 0
+// solves p0, cluster 1 solves p1 (the single-pass core's Yc / Yr and P / W^T
+// pairs), so their latency-bound rounds overlap.
+__global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const JacobiParams p0, const JacobiParams p1) {
   cg::cluster_group cluster = cg::this_cluster();
   const int P = static_cast<int>(cluster.num_blocks());
+  const JacobiParams& p = (static_cast<int>(blockIdx.x) / P == 0) ? p0 : p1;
   const int q = static_cast<int>(cluster.block_rank());
   const int c = p.c, cc = c + (c & 1), npairs = cc / 2;
   const int RX = p.RX, RV = p.RV, LDX = p.LDX, LDV = p.LDV;
@@ -606,37 +610,43 @@ size_t jacobi_work_bytes(int64_t mr, int64_t c) {
   return L.smem ? stage : 2 * stage;
 }
 
-cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double* S, double* V, double* work,
-                       int* info, int* sweeps_out, cudaStream_t st) {
+namespace {
+// One launch for 1 or 2 same-shape problems (one cluster each).
+cudaError_t jacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64_t c, cudaStream_t st) {
   if (c <= 0 || mr <= 0) return cudaSuccess;
   const JacobiLayout L = jacobi_layout(mr, c);
-  JacobiParams p{};
-  p.X = X;
-  p.mr = mr;
-  p.c = static_cast<int>(c);
-  p.U = U;
-  p.S = S;
-  p.V = V;
-  p.RX = L.RX;
-  p.RV = L.RV;
-  p.LDX = L.LDX;
-  p.LDV = L.LDV;
-  p.bcast = L.bcast ? 1 : 0;
-  p.info = info;
-  p.sweeps_out = sweeps_out;
+  JacobiParams ps[2];
+  for (int i = 0; i < count; ++i) {
+    JacobiParams& p = ps[i];
+    p = JacobiParams{};
+    p.X = pr[i].X;
+    p.mr = mr;
+    p.c = static_cast<int>(c);
+    p.U = pr[i].U;
+    p.S = pr[i].S;
+    p.V = pr[i].V;
+    p.RX = L.RX;
+    p.RV = L.RV;
+    p.LDX = L.LDX;
+    p.LDV = L.LDV;
+    p.bcast = L.bcast ? 1 : 0;
+    p.info = pr[i].info;
+    p.sweeps_out = pr[i].sweeps;
 #ifdef RFGPU_JACOBI_TRACE
-  static long long* trace_buf = nullptr;
-  if (!trace_buf) cudaMalloc(&trace_buf, sizeof(long long) * 16);
-  p.trace = trace_buf;
+    static long long* trace_buf = nullptr;
+    if (!trace_buf) cudaMalloc(&trace_buf, sizeof(long long) * 16);
+    p.trace = trace_buf;
 #endif
-  const size_t stage = static_cast<size_t>(L.P) * c * (L.LDX + L.LDV);
-  p.gS = work;
-  if (!L.smem) {
-    p.gX = work + stage;
-    p.gV = p.gX + static_cast<size_t>(L.P) * c * L.LDX;
+    const size_t stage = static_cast<size_t>(L.P) * c * (L.LDX + L.LDV);
+    p.gS = pr[i].work;
+    if (!L.smem) {
+      p.gX = pr[i].work + stage;
+      p.gV = p.gX + static_cast<size_t>(L.P) * c * L.LDX;
+    }
   }
+  if (count == 1) ps[1] = ps[0];
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(L.P);
+  cfg.gridDim = dim3(L.P * count);
   cfg.blockDim = dim3(L.threads);
   cfg.dynamicSmemBytes = L.bytes;
   cfg.stream = st;
@@ -658,7 +668,7 @@ cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double
       if (e != cudaSuccess) return e;
       c1 = L.bytes;
     }
-    e = cudaLaunchKernelEx(&cfg, jacobi_svd_kernel<true>, p);
+    e = cudaLaunchKernelEx(&cfg, jacobi_svd_kernel<true>, ps[0], ps[1]);
     count_launch();
   } else {
     static size_t c2 = 0;
@@ -668,7 +678,7 @@ cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double
       if (e != cudaSuccess) return e;
       c2 = L.bytes;
     }
-    e = cudaLaunchKernelEx(&cfg, jacobi_svd_kernel<false>, p);
+    e = cudaLaunchKernelEx(&cfg, jacobi_svd_kernel<false>, ps[0], ps[1]);
     count_launch();
   }
   if (e != cudaSuccess) return e;
@@ -676,7 +686,7 @@ cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double
   {
     long long h[14];
     cudaStreamSynchronize(st);
-    cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaMemcpy(h, ps[0].trace, sizeof(h), cudaMemcpyDeviceToHost);
     std::fprintf(stderr, "[rfgpu] jacobi c=%lld P=%d bcast=%d slots (clk/round):", static_cast<long long>(c), L.P,
                  static_cast<int>(L.bcast));
     for (int k = 1; k < 14; ++k) std::fprintf(stderr, " %d:%.0f", k, static_cast<double>(h[k]) / 30);
@@ -684,6 +694,18 @@ cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double
   }
 #endif
   return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double* S, double* V, double* work,
+                       int* info, int* sweeps_out, cudaStream_t st) {
+  const JacobiProblem p{X, U, S, V, work, info, sweeps_out};
+  return jacobi_launch(&p, 1, mr, c, st);
+}
+
+cudaError_t jacobi_svd_pair(const JacobiProblem& a, const JacobiProblem& b, int64_t mr, int64_t c, cudaStream_t st) {
+  const JacobiProblem p[2] = {a, b};
+  return jacobi_launch(p, 2, mr, c, st);
 }
 
 cudaError_t sumsq(const double* x, int64_t n, double* partials, double* out, cudaStream_t st) {
