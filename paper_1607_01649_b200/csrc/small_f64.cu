@@ -579,6 +579,185 @@ JacobiLayout jacobi_layout(int64_t mr, int64_t c) {
 
 size_t chol_inv_work_bytes(int64_t c) { return sizeof(double) * (2 * c + c * (c + 1) / 2); }
 
+namespace {
+// ---- blocked Cholesky for l > 256 (the packed triangle no longer fits in
+// one CTA's shared memory): right-looking with kCB-wide panels, R doubling as
+// the working copy of G (32-wide panels). Per panel: the diagonal block is factored in shared
+// memory by one CTA (reference pivot rule, dense.cpp:763-786) and inverted;
+// the block row R(k, k1:) = R_kk^-T G(k, k1:) and the trailing update
+// G(k1:, k1:) -= R(k, k1:)^T R(k, k1:) run over many CTAs.
+constexpr int kCB = 32;
+
+__global__ void cholb_prep(const double* __restrict__ G, int c, double* __restrict__ R, double* __restrict__ stat,
+                           int* info, double* info_d) {
+  const int64_t cc = static_cast<int64_t>(c) * c;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < cc;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / c, i = e - j * c;
+    R[e] = i <= j ? G[e] : 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double mx = 0.0, tr = 0.0;
+    for (int j = 0; j < c; ++j) {
+      const double g = G[static_cast<int64_t>(j) * c + j];
+      mx = fmax(mx, fabs(g));
+      tr += g;
+    }
+    stat[0] = 1e-14 * mx;
+    stat[1] = tr;
+    info[0] = 0;
+    info_d[0] = INFINITY;
+  }
+}
+
+__global__ void __launch_bounds__(256) cholb_diag(double* __restrict__ R, int c, int k0, int k1,
+                                                  const double* __restrict__ stat, double* __restrict__ Dinv, int* info,
+                                                  double* info_d) {
+  if (info[0]) return;
+  __shared__ double A[kCB][kCB + 1];  // A[col][row]
+  __shared__ double X[kCB][kCB + 1];  // inverse, X[col][row]
+  __shared__ int s_fail;
+  __shared__ double s_min;
+  const int b = k1 - k0, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < b * b; e += blockDim.x) {
+    const int j = e / b, i = e - j * b;
+    A[j][i] = i <= j ? R[static_cast<int64_t>(k0 + j) * c + k0 + i] : 0.0;
+  }
+  if (tid == 0) {
+    s_fail = 0;
+    s_min = info_d[0];
+  }
+  __syncthreads();
+  const double floor = stat[0], trace = stat[1];
+  for (int j = 0; j < b; ++j) {
+    if (tid == 0) {
+      const double d = A[j][j];
+      if (d <= floor || !(d > 0.0)) {
+        s_fail = k0 + j + 1;
+      } else {
+        s_min = fmin(s_min, trace > 0.0 ? d / trace : 0.0);
+        A[j][j] = sqrt(d);
+      }
+    }
+    __syncthreads();
+    if (s_fail) break;
+    const double cjj = A[j][j];
+    for (int col = j + 1 + tid; col < b; col += blockDim.x) A[col][j] /= cjj;
+    __syncthreads();
+    for (int col = j + 1 + warp; col < b; col += 8) {
+      const double rc = A[col][j];
+      for (int i = j + 1 + lane; i <= col; i += 32) A[col][i] -= A[i][j] * rc;
+    }
+    __syncthreads();
+  }
+  if (s_fail) {
+    if (tid == 0) {
+      info[0] = s_fail;
+      info_d[0] = s_min;
+    }
+    return;
+  }
+  // R_kk^{-1} (upper), one warp per column: R x = e_j by back substitution
+  for (int j = warp; j < b; j += 8) {
+    for (int i = lane; i < b; i += 32) X[j][i] = 0.0;
+    __syncwarp();
+    if (lane == 0) {
+      for (int i = j; i >= 0; --i) {
+        double t = (i == j) ? 1.0 : 0.0;
+        for (int k = i + 1; k <= j; ++k) t -= A[k][i] * X[j][k];
+        X[j][i] = t / A[i][i];
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int e = tid; e < b * b; e += blockDim.x) {
+    const int j = e / b, i = e - j * b;
+    R[static_cast<int64_t>(k0 + j) * c + k0 + i] = i <= j ? A[j][i] : 0.0;
+    Dinv[j * kCB + i] = X[j][i];
+  }
+  if (tid == 0) info_d[0] = s_min;
+}
+
+// R(k0:k1, j) = R_kk^-T W(k0:k1, j) for 32 columns j per CTA.
+__global__ void __launch_bounds__(256) cholb_panel(double* __restrict__ R, int c, int k0, int k1,
+                                                   const double* __restrict__ Dinv, const int* info) {
+  if (info[0]) return;
+  __shared__ double D[kCB][kCB + 1];   // D[col][row] = Dinv
+  __shared__ double W[32][kCB + 1];    // W[col][row]
+  const int b = k1 - k0, tid = threadIdx.x;
+  const int j0 = k1 + blockIdx.x * 32, nj = min(32, c - j0);
+  for (int e = tid; e < b * b; e += blockDim.x) {
+    const int j = e / b, i = e - j * b;
+    D[j][i] = Dinv[j * kCB + i];
+  }
+  for (int e = tid; e < b * nj; e += blockDim.x) {
+    const int jj = e / b, i = e - jj * b;
+    W[jj][i] = R[static_cast<int64_t>(j0 + jj) * c + k0 + i];
+  }
+  __syncthreads();
+  for (int e = tid; e < b * nj; e += blockDim.x) {
+    const int jj = e / b, i = e - jj * b;
+    // (Dinv^T W)(i, jj) = sum_t Dinv(t, i) W(t, jj), Dinv upper: t <= i
+    double acc = 0.0;
+    for (int t = 0; t <= i; ++t) acc = fma(D[i][t], W[jj][t], acc);
+    R[static_cast<int64_t>(j0 + jj) * c + k0 + i] = acc;
+  }
+}
+
+// W(i, j) -= sum_t R(t, i) R(t, j), t in the panel, for k1 <= i <= j: 32 x 32 tiles.
+__global__ void __launch_bounds__(256) cholb_update(double* __restrict__ R, int c, int k0, int k1, int ntile,
+                                                    const int* info) {
+  if (info[0]) return;
+  // upper-triangular tile index -> (ti, tj), ti <= tj
+  int t = blockIdx.x, ti = 0;
+  while (t >= ntile - ti) {
+    t -= ntile - ti;
+    ++ti;
+  }
+  const int tj = ti + t;
+  __shared__ double Xi[32][kCB + 1], Xj[32][kCB + 1];  // [col][t]
+  const int b = k1 - k0, tid = threadIdx.x;
+  const int i0 = k1 + ti * 32, j0 = k1 + tj * 32;
+  const int ni = min(32, c - i0), nj = min(32, c - j0);
+  for (int e = tid; e < b * 32; e += blockDim.x) {
+    const int col = e / b, r = e - col * b;
+    Xi[col][r] = col < ni ? R[static_cast<int64_t>(i0 + col) * c + k0 + r] : 0.0;
+    Xj[col][r] = col < nj ? R[static_cast<int64_t>(j0 + col) * c + k0 + r] : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < 32 * 32; e += blockDim.x) {
+    const int jj = e >> 5, ii = e & 31;
+    const int i = i0 + ii, j = j0 + jj;
+    if (ii < ni && jj < nj && i <= j) {
+      double acc = 0.0;
+      for (int r = 0; r < b; ++r) acc = fma(Xi[ii][r], Xj[jj][r], acc);
+      R[static_cast<int64_t>(j) * c + i] -= acc;
+    }
+  }
+}
+
+cudaError_t chol_blocked(const double* G, int c, double* R, double* work, int* info, double* info_d, cudaStream_t st) {
+  double* stat = work;          // floor, trace
+  double* Dinv = work + 16;     // kCB x kCB
+  cholb_prep<<<static_cast<unsigned>(std::min<int64_t>((static_cast<int64_t>(c) * c + 255) / 256, 592)), 256, 0, st>>>(
+      G, c, R, stat, info, info_d);
+  count_launch();
+  for (int k0 = 0; k0 < c; k0 += kCB) {
+    const int k1 = std::min(c, k0 + kCB);
+    cholb_diag<<<1, 256, 0, st>>>(R, c, k0, k1, stat, Dinv, info, info_d);
+    count_launch();
+    if (k1 < c) {
+      cholb_panel<<<static_cast<unsigned>((c - k1 + 31) / 32), 256, 0, st>>>(R, c, k0, k1, Dinv, info);
+      const int ntile = (c - k1 + 31) / 32;
+      cholb_update<<<static_cast<unsigned>(ntile * (ntile + 1) / 2), 256, 0, st>>>(R, c, k0, k1, ntile, info);
+      count_launch(2);
+    }
+  }
+  return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double* work, int* info,
                      double* info_d, cudaStream_t st) {
   if (c <= 0) return cudaSuccess;
@@ -596,8 +775,8 @@ cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double
     chol_inv_kernel<true, 8><<<1, kSmallThreads, smem, st>>>(G, ci, R, Rinv, work, info, info_d);
     count_launch();
   } else {
-    chol_inv_kernel<false, 11><<<1, kSmallThreads, 0, st>>>(G, ci, R, Rinv, work, info, info_d);
-    count_launch();
+    cudaError_t e = chol_blocked(G, ci, R, work, info, info_d, st);
+    if (e != cudaSuccess) return e;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
