@@ -400,8 +400,14 @@ struct OzPasses {
     if (!on) return {};
     const int digits = m->f32 ? 4 : 7;  // FP32 data: 4 digits (30 bits) per element
     const OzakiA lay = ozaki_layout(m->m, m->n, digits);
-    RF_TRY(planes.alloc(ozaki_a_bytes(m->m, m->n, digits), c->stream));
-    RF_TRY(work.alloc(std::max(ozaki_nn_work_bytes(lay, m->m, ell), ozaki_tn_work_bytes(lay, ell)), c->stream));
+    // The digit planes take 2 x digits bytes per element of A: when HBM cannot
+    // hold them next to A, the passes stay on the FP64 tensor pipe (DMMA).
+    if (!planes.alloc(ozaki_a_bytes(m->m, m->n, digits), c->stream).ok() ||
+        !work.alloc(std::max(ozaki_nn_work_bytes(lay, m->m, ell), ozaki_tn_work_bytes(lay, ell)), c->stream).ok()) {
+      on = false;
+      if (std::getenv("RFGPU_DEBUG")) std::fprintf(stderr, "[rfgpu] digit planes do not fit: DMMA passes\n");
+      return {};
+    }
     ozaki_bind(planes.p, m->m, m->n, digits, &a);
     return {};
   }
