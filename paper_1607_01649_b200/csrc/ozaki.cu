@@ -32,6 +32,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -45,16 +46,25 @@ namespace {
 // balanced base-256 digits per operand: 7 for FP64 data, 4 for FP32 (template S)
 constexpr int OBM = 128;       // tile rows (TMEM lanes)
 constexpr int OBN = 64;        // tile columns per accumulator group
-constexpr int OBK = 64;        // K bytes per pipeline stage (64B swizzle)
+// K bytes per pipeline stage: BK = 64 (64B-swizzled K-major rows, 2 stages
+// of 86 KB for 7 digits) or 32 (32B swizzle, 5 stages of 43 KB: more bytes in
+// flight per SM at the same shared-memory footprint).
 constexpr int64_t kSplitK = 16384;  // int32 safety: S * K * 128^2 < 2^31
-constexpr int kThreads = 192;   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr int kThreads = 192;
+// One digit set serves both passes when the non-zero columns' exponents span
+// at most this many bits (ozaki_col_exponents): A^T Q on the row-scaled
+// digits then loses at most kSharedSpread + 2 bits against column-scaled
+// digits (see ozaki_tn).
+constexpr int kSharedSpread = 2;
+constexpr int kDefaultBK = 64;  // stage depth (see Dig); RFGPU_OZAKI_BK overrides   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
 
 // Per digit count S: S accumulator groups of OBN TMEM columns; as many
 // 2-digit-plane... stages as fit in shared memory.
-template <int S>
+template <int S, int BK>
 struct Dig {
-  static constexpr size_t stage_bytes = static_cast<size_t>(S) * (OBM + OBN) * OBK;
-  static constexpr int stages = S <= 4 ? 4 : 2;
+  static constexpr size_t stage_bytes = static_cast<size_t>(S) * (OBM + OBN) * BK;
+  static constexpr int fit = static_cast<int>((225 * 1024 - 2048) / stage_bytes);
+  static constexpr int stages = fit > 8 ? 8 : fit;
   static constexpr int tmem_cols = S * OBN <= 256 ? 256 : 512;
   static constexpr size_t smem = stages * stage_bytes + 1024 + 256;
 };
@@ -62,9 +72,6 @@ struct Dig {
 __host__ __device__ inline int64_t roundup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 // ---- operand preparation ---------------------------------------------------------
-// Exponent e with |v| < 2^e for v = max |.| (0 for an all-zero vector).
-__device__ __forceinline__ int bound_exp(double mx) { return mx > 0.0 ? ilogb(mx) + 1 : 0; }
-
 // High word of |v|: ordered like |v| to within the top 20 mantissa bits, so
 // its maximum carries the exponent of the maximum.
 __device__ __forceinline__ uint32_t abs_hi(double v) {
@@ -144,15 +151,28 @@ __global__ void rowexp_kernel(const uint32_t* __restrict__ rowhi, int64_t r0, in
     rowexp[i] = hi_exp(rowhi[i]);
 }
 
-// Column exponents from the per-CTA column maxima.
+// Column exponents from the per-CTA column maxima; ext[0] = max and ext[1] =
+// -min exponent over the non-zero columns (both pre-set very negative).
 __global__ void colexp_kernel(const uint32_t* __restrict__ colpart, int64_t nblk, int64_t n, int64_t n_pad,
-                              int* __restrict__ colexp) {
+                              int* __restrict__ colexp, int* __restrict__ ext) {
+  int emax = INT_MIN, nmin = INT_MIN;
   for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n_pad;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     uint32_t mx = 0;
     if (j < n)
       for (int64_t b = 0; b < nblk; ++b) mx = max(mx, colpart[b * n_pad + j]);
-    colexp[j] = hi_exp(mx);
+    const int e = hi_exp(mx);
+    colexp[j] = e;
+    if (mx != 0) {
+      emax = max(emax, e);
+      nmin = max(nmin, -e);
+    }
+  }
+  emax = __reduce_max_sync(0xffffffffu, emax);
+  nmin = __reduce_max_sync(0xffffffffu, nmin);
+  if ((threadIdx.x & 31) == 0 && emax != INT_MIN) {
+    atomicMax(&ext[0], emax);
+    atomicMax(&ext[1], nmin);
   }
 }
 
@@ -266,33 +286,46 @@ __global__ void __launch_bounds__(256) slice_a_kernel(const T* __restrict__ A, i
   }
 }
 
-// Thin operand R (K x N, col-major ld), optionally pre-scaled by 2^rowexp[i]:
-// per-column exponent f_c of max |R(i,c) 2^e_i|.
-__global__ void col_exp_kernel(const double* __restrict__ R, int64_t K, int64_t ldr, const int* __restrict__ rowexp,
-                               int* __restrict__ colexp) {
-  __shared__ double red[32];
+// Thin operand R (K x N, col-major ld), optionally pre-scaled by
+// 2^(rowexp[i] - shift): per-column exponent f_c of max |R(i,c) 2^(e_i - shift)|.
+// Grid (N, row chunks): each CTA reduces one chunk of one column and folds its
+// exponent into colexp[c] (pre-set very negative; colexp_fix_kernel maps
+// all-zero columns to 0).
+__device__ __forceinline__ double thin_val(const double* __restrict__ R, int64_t c, int64_t ldr, int64_t i,
+                                          const int* __restrict__ rowexp, int shift) {
+  const double v = R[c * ldr + i];
+  return rowexp ? ldexp(v, rowexp[i] - shift) : v;
+}
+
+__global__ void __launch_bounds__(256) col_exp_kernel(const double* __restrict__ R, int64_t K, int64_t ldr,
+                                                      const int* __restrict__ rowexp, int shift, int64_t chunk,
+                                                      int* __restrict__ colexp) {
+  __shared__ uint32_t red[8];
   const int64_t c = blockIdx.x;
-  double mx = 0.0;
-  for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
-    double v = fabs(R[c * ldr + i]);
-    if (rowexp) v = ldexp(v, rowexp[i]);
-    mx = fmax(mx, v);
-  }
-  // block max
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int64_t i0 = static_cast<int64_t>(blockIdx.y) * chunk, i1 = lmin(K, i0 + chunk);
+  uint32_t mx = 0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) mx = max(mx, abs_hi(thin_val(R, c, ldr, i, rowexp, shift)));
+  mx = __reduce_max_sync(0xffffffffu, mx);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (threadIdx.x == 0) colexp[c] = bound_exp(v);
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) mx = max(mx, red[w]);
+    if (mx) atomicMax(&colexp[c], hi_exp(mx));
   }
 }
 
-// Digits of R(i,c) 2^-f_c into [kS][N_pad][K_pad] (4 rows per thread).
+__global__ void colexp_fix_kernel(int* __restrict__ colexp, int64_t N) {
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < N;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (colexp[c] < -100000) colexp[c] = 0;
+}
+
+// Digits of R(i,c) 2^(e_i - shift) 2^-f_c (row factor only with rowexp) into
+// [kS][N_pad][K_pad] (4 rows per thread).
 template <int S>
 __global__ void slice_r_kernel(const double* __restrict__ R, int64_t K, int64_t N, int64_t ldr,
-                               const int* __restrict__ colexp, int8_t* __restrict__ out, int64_t K_pad, int64_t N_pad) {
+                               const int* __restrict__ rowexp, int shift, const int* __restrict__ colexp,
+                               int8_t* __restrict__ out, int64_t K_pad, int64_t N_pad) {
   const int64_t quads = K_pad / 4;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < quads * N_pad;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -302,7 +335,7 @@ __global__ void slice_r_kernel(const double* __restrict__ R, int64_t K, int64_t 
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int64_t i = i0 + b;
-      const double v = (i < K && c < N) ? R[c * ldr + i] : 0.0;
+      const double v = (i < K && c < N) ? thin_val(R, c, ldr, i, rowexp, shift) : 0.0;
       const uint64_t x = balanced<S>(v, fc);
       lo[b] = static_cast<uint32_t>(x) ^ 0x80808080u;
       hi[b] = static_cast<uint32_t>(x >> 32) ^ 0x80808080u;
@@ -330,6 +363,7 @@ struct OzParams {
   int64_t c_row0;    // output row offset (row of C for L row row0)
   const int* rowexp;  // optional 2^e_row output scale (indexed by L row)
   const int* colexp;  // 2^f_col output scale
+  int cshift;         // extra output exponent (the thin operand's row pre-scaling shift)
   int ws_mode;        // 1: C is [split][N_real][M_real]
   int cl;             // cluster size along N tiles: the A tile is TMA-multicast to all of them
 };
@@ -353,23 +387,25 @@ __device__ __forceinline__ void tma2d_mc(void* dst, const CUtensorMap* tm, uint6
       : "memory");
 }
 
-// K-major operand tile: rows of 64 K-bytes, 64B swizzle (8-row atoms, SBO 512 B).
+// K-major operand tile: rows of BK K-bytes, BK-byte swizzle (8-row atoms, SBO 8 BK).
+template <int BK>
 __device__ __forceinline__ uint64_t umma_desc(const void* p) {
   uint64_t d = 0;
   d |= (static_cast<uint64_t>(smem_u32(p)) >> 4) & 0x3FFF;  // start address
   d |= static_cast<uint64_t>(1) << 16;                       // LBO (unused: swizzled K-major)
-  d |= static_cast<uint64_t>((8 * OBK) >> 4) << 32;          // SBO: 8 rows x 64 B
+  d |= static_cast<uint64_t>((8 * BK) >> 4) << 32;           // SBO: 8 rows x BK bytes
   d |= static_cast<uint64_t>(1) << 46;                       // sm100 descriptor version
-  d |= static_cast<uint64_t>(4) << 61;                       // SWIZZLE_64B
+  d |= static_cast<uint64_t>(BK == 64 ? 4 : 6) << 61;        // SWIZZLE_64B / SWIZZLE_32B
   return d;
 }
 
 // MN-major operand tile: K rows of 128 M-bytes, 128B swizzle (atoms of 8
 // K-rows x 128 B, SBO 1024 B; a single atom along M).
+template <int BK>
 __device__ __forceinline__ uint64_t umma_desc_mn(const void* p) {
   uint64_t d = 0;
   d |= (static_cast<uint64_t>(smem_u32(p)) >> 4) & 0x3FFF;
-  d |= static_cast<uint64_t>((OBK * OBM) >> 4) << 16;        // LBO: next M atom (unused, M = 128)
+  d |= static_cast<uint64_t>((BK * OBM) >> 4) << 16;         // LBO: next M atom (unused, M = 128)
   d |= static_cast<uint64_t>(1024 >> 4) << 32;               // SBO: 8 K-rows x 128 B
   d |= static_cast<uint64_t>(1) << 46;
   d |= static_cast<uint64_t>(2) << 61;                       // SWIZZLE_128B
@@ -378,14 +414,14 @@ __device__ __forceinline__ uint64_t umma_desc_mn(const void* p) {
 
 // L_MN: the L digit planes are read M-major (column-major A digits serving
 // Y = A X), else K-major (A^T Q).
-template <bool L_MN, int S>
+template <bool L_MN, int S, int BK>
 __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmL,
                                                                   const __grid_constant__ CUtensorMap tmR,
                                                                   const OzParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int kS = S, kStages = Dig<S>::stages, kTmemCols = Dig<S>::tmem_cols;
-  constexpr int ASZ = kS * OBM * OBK, BSZ = kS * OBN * OBK;
+  constexpr int kS = S, kStages = Dig<S, BK>::stages, kTmemCols = Dig<S, BK>::tmem_cols;
+  constexpr int ASZ = kS * OBM * BK, BSZ = kS * OBN * BK;
   uint8_t* sA = smem;
   uint8_t* sB = sA + kStages * ASZ;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * BSZ);
@@ -435,19 +471,19 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
       const uint32_t ph = (kb / kStages) & 1;
       mbar_wait(&empty[st], ph ^ 1);
       mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(ASZ + BSZ));
-      const int kx = static_cast<int>((kb0 + kb) * OBK);
+      const int kx = static_cast<int>((kb0 + kb) * BK);
 #pragma unroll
       for (int s = 0; s < kS; ++s) {
         // A planes round-robin over the cluster, multicast to all of it
         // K-major L: box {64 K-bytes, 128 rows} at (k, plane row); M-major L
         // (planes [kS][K_rows][M]): box {128 M-bytes, 64 K-rows} at (m, plane k)
         const int lc0 = L_MN ? static_cast<int>(lrow0) : kx;
-        const int lc1 = L_MN ? static_cast<int>(s * p.L_rows + (kb0 + kb) * OBK) : static_cast<int>(s * p.L_rows + lrow0);
+        const int lc1 = L_MN ? static_cast<int>(s * p.L_rows + (kb0 + kb) * BK) : static_cast<int>(s * p.L_rows + lrow0);
         if (cl == 1)
-          tma2d(sA + st * ASZ + s * OBM * OBK, &tmL, &full[st], lc0, lc1);
+          tma2d(sA + st * ASZ + s * OBM * BK, &tmL, &full[st], lc0, lc1);
         else if (s % cl == crank)
-          tma2d_mc(sA + st * ASZ + s * OBM * OBK, &tmL, &full[st], lc0, lc1, cmask);
-        tma2d(sB + st * BSZ + s * OBN * OBK, &tmR, &full[st], kx, static_cast<int>(s * p.R_rows + ncol0));
+          tma2d_mc(sA + st * ASZ + s * OBM * BK, &tmL, &full[st], lc0, lc1, cmask);
+        tma2d(sB + st * BSZ + s * OBN * BK, &tmR, &full[st], kx, static_cast<int>(s * p.R_rows + ncol0));
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -466,16 +502,16 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
       mbar_wait(&full[st], ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int kk = 0; kk < OBK / 32; ++kk) {
+      for (int kk = 0; kk < BK / 32; ++kk) {
 #pragma unroll
         for (int s = 0; s < kS; ++s) {
 #pragma unroll
           for (int t0 = 0; t0 < kS - s; t0 += 4) {
             const int cnt = (kS - s - t0) < 4 ? (kS - s - t0) : 4;
             // M-major: K advances by 32 K-rows = 4 swizzle atoms
-            const uint64_t da = L_MN ? umma_desc_mn(sA + st * ASZ + s * OBM * OBK + kk * 32 * OBM)
-                                     : umma_desc(sA + st * ASZ + s * OBM * OBK + kk * 32);
-            const uint64_t db = umma_desc(sB + st * BSZ + t0 * OBN * OBK + kk * 32);
+            const uint64_t da = L_MN ? umma_desc_mn<BK>(sA + st * ASZ + s * OBM * BK + kk * 32 * OBM)
+                                     : umma_desc<BK>(sA + st * ASZ + s * OBM * BK + kk * 32);
+            const uint64_t db = umma_desc<BK>(sB + st * BSZ + t0 * OBN * BK + kk * 32);
             // groups s + t0 .. s + t0 + cnt - 1; every group is first written by s = 0
             const uint32_t accum = (kb == 0 && kk == 0 && s == 0) ? 0u : 1u;
             asm volatile(
@@ -531,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
         for (int j = 0; j < 16; ++j) {
           const int64_t col = ncol0 + c + j;
           if (col < p.N_real) {
-            const double v = ldexp(acc[j], rex + p.colexp[col]);
+            const double v = ldexp(acc[j], rex + p.colexp[col] + p.cshift);
             if (p.ws_mode)
               p.C[(static_cast<int64_t>(split) * p.N_real + col) * p.M_real + (lrow - p.row0)] = v;
             else
@@ -596,29 +632,29 @@ bool digit_tmap(CUtensorMap* tm, const int8_t* base, int64_t rows, int64_t inner
 // 2-stage ring), so the caller chooses.
 // L_mn: L planes are [kS][K_pad][L_M] (M contiguous, L_rows = K_pad rows per
 // plane, L_M = M extent), else [kS][L_rows][K_pad].
-template <int S>
+template <int S, int BK>
 cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int64_t L_M, const int8_t* R,
                                 int64_t R_rows, int64_t K_pad, int64_t row0, int64_t rows, int64_t N_real, int splits,
                                 const OzParams& base, bool multicast, cudaStream_t st) {
   constexpr int kS = S;
-  constexpr size_t kSmemBytes = Dig<S>::smem;
+  constexpr size_t kSmemBytes = Dig<S, BK>::smem;
+  constexpr CUtensorMapSwizzle kSwK = BK == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
   static bool cfg = false;
   if (!cfg) {
-    for (auto fn : {ozaki_gemm_kernel<true, S>, ozaki_gemm_kernel<false, S>}) {
+    for (auto fn : {ozaki_gemm_kernel<true, S, BK>, ozaki_gemm_kernel<false, S, BK>}) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
       if (e != cudaSuccess) return e;
     }
     cfg = true;
   }
   CUtensorMap tl, tr;
-  const bool okl = L_mn ? digit_tmap(&tl, L, kS * L_rows, L_M, OBM, OBK, CU_TENSOR_MAP_SWIZZLE_128B)
-                        : digit_tmap(&tl, L, kS * L_rows, K_pad, OBK, OBM, CU_TENSOR_MAP_SWIZZLE_64B);
-  if (!okl || !digit_tmap(&tr, R, kS * R_rows, K_pad, OBK, OBN, CU_TENSOR_MAP_SWIZZLE_64B))
-    return cudaErrorInvalidValue;
+  const bool okl = L_mn ? digit_tmap(&tl, L, kS * L_rows, L_M, OBM, BK, CU_TENSOR_MAP_SWIZZLE_128B)
+                        : digit_tmap(&tl, L, kS * L_rows, K_pad, BK, OBM, kSwK);
+  if (!okl || !digit_tmap(&tr, R, kS * R_rows, K_pad, BK, OBN, kSwK)) return cudaErrorInvalidValue;
   OzParams p = base;
   p.L_rows = L_rows;
   p.R_rows = R_rows;
-  p.kb_total = K_pad / OBK;
+  p.kb_total = K_pad / BK;
   p.splits = splits;
   p.kb_per_split = (p.kb_total + splits - 1) / splits;
   p.ntn = static_cast<int>(R_rows / OBN);
@@ -629,11 +665,8 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   const int64_t grid = static_cast<int64_t>(p.ntn) * p.mtn * splits;
   if (grid <= 0) return cudaSuccess;
   p.cl = 1;
-  static const int mc_env = [] {
-    const char* e = std::getenv("RFGPU_OZAKI_MC");  // experiments: 0 never, 1 always, unset: caller's choice
-    return e ? (e[0] == '1' ? 1 : 0) : -1;
-  }();
-  if (mc_env >= 0) multicast = mc_env == 1;
+  const char* mc_env = std::getenv("RFGPU_OZAKI_MC");  // experiments: 0 never, 1 always, unset: caller's choice
+  if (mc_env) multicast = mc_env[0] == '1';
   if (multicast)
     for (int c : {8, 7, 6, 5, 4, 3, 2})
       if (p.ntn % c == 0) {
@@ -652,28 +685,52 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   attr[0].val.clusterDim.z = 1;
   cfgl.attrs = attr;
   cfgl.numAttrs = 1;
-  cudaError_t e = L_mn ? cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<true, S>, tl, tr, p)
-                       : cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<false, S>, tl, tr, p);
+  cudaError_t e = L_mn ? cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<true, S, BK>, tl, tr, p)
+                       : cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<false, S, BK>, tl, tr, p);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
+// Stage depth: RFGPU_OZAKI_BK=32 (5 x 43 KB stages for 7 digits) or 64 (2 x 86 KB).
+int stage_bk() {
+  const char* e = std::getenv("RFGPU_OZAKI_BK");
+  if (e) return std::atoi(e) == 32 ? 32 : 64;
+  return kDefaultBK;
+}
+
 cudaError_t launch_digit_gemm(int S, const int8_t* L, int64_t L_rows, bool L_mn, int64_t L_M, const int8_t* R,
                               int64_t R_rows, int64_t K_pad, int64_t row0, int64_t rows, int64_t N_real, int splits,
                               const OzParams& base, bool multicast, cudaStream_t st) {
-  return S == 4 ? launch_digit_gemm_s<4>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
-                                         multicast, st)
-                : launch_digit_gemm_s<7>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
-                                         multicast, st);
+  const bool b32 = stage_bk() == 32;
+  if (S == 4)
+    return b32 ? launch_digit_gemm_s<4, 32>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
+                                            multicast, st)
+               : launch_digit_gemm_s<4, 64>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
+                                            multicast, st);
+  return b32 ? launch_digit_gemm_s<7, 32>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
+                                          multicast, st)
+             : launch_digit_gemm_s<7, 64>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
+                                          multicast, st);
 }
 
-void slice_r(int S, const double* R, int64_t K, int64_t N, int64_t ldr, const int* colexp, int8_t* out, int64_t K_pad,
-             int64_t N_pad, cudaStream_t st) {
+// Column exponents (many CTAs per column) + digits of the thin operand R
+// (K x N), rows optionally pre-scaled by 2^(rowexp[i] - shift).
+cudaError_t slice_thin(int S, const double* R, int64_t K, int64_t N, int64_t ldr, const int* rowexp, int shift,
+                       int* colexp, int8_t* out, int64_t K_pad, int64_t N_pad, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(colexp, 0x80, sizeof(int) * N, st);  // very negative
+  if (e != cudaSuccess) return e;
+  const int64_t chunk = 16384;
+  if (N > 0 && K > 0)
+    col_exp_kernel<<<dim3(static_cast<unsigned>(N), static_cast<unsigned>((K + chunk - 1) / chunk)), 256, 0, st>>>(
+        R, K, ldr, rowexp, shift, chunk, colexp);
+  colexp_fix_kernel<<<static_cast<unsigned>(std::max<int64_t>(1, (N + 255) / 256)), 256, 0, st>>>(colexp, N);
   if (S == 4)
-    slice_r_kernel<4><<<1184, 256, 0, st>>>(R, K, N, ldr, colexp, out, K_pad, N_pad);
+    slice_r_kernel<4><<<1184, 256, 0, st>>>(R, K, N, ldr, rowexp, shift, colexp, out, K_pad, N_pad);
   else
-    slice_r_kernel<7><<<1184, 256, 0, st>>>(R, K, N, ldr, colexp, out, K_pad, N_pad);
+    slice_r_kernel<7><<<1184, 256, 0, st>>>(R, K, N, ldr, rowexp, shift, colexp, out, K_pad, N_pad);
+  count_launch(3);
+  return cudaGetLastError();
 }
 
 template <class T>
@@ -707,10 +764,15 @@ OzakiA ozaki_layout(int64_t m, int64_t n, int digits) {
   return a;
 }
 
+size_t ozaki_set_bytes(int64_t m, int64_t n, int digits) {
+  const OzakiA a = ozaki_layout(m, n, digits);
+  return static_cast<size_t>(digits) * a.m_pad * a.n_pad;
+}
+
 size_t ozaki_a_bytes(int64_t m, int64_t n, int digits) {
   const OzakiA a = ozaki_layout(m, n, digits);
-  const size_t planes = static_cast<size_t>(digits) * a.m_pad * a.n_pad;
-  return 2 * planes + sizeof(int) * (2 * a.m_pad + a.n_pad) + sizeof(uint32_t) * (a.m_pad / 256) * a.n_pad + 1024;
+  return ozaki_set_bytes(m, n, digits) + sizeof(int) * (2 * a.m_pad + a.n_pad + 8) +
+         sizeof(uint32_t) * (a.m_pad / 256) * a.n_pad + 1024;
 }
 
 namespace {
@@ -725,13 +787,14 @@ int64_t ozaki_ssq_slots(int64_t rows, int64_t n) { return ((rows + 255) / 256) *
 
 void ozaki_bind(void* work, int64_t m, int64_t n, int digits, OzakiA* out) {
   *out = ozaki_layout(m, n, digits);
-  const size_t planes = static_cast<size_t>(digits) * out->m_pad * out->n_pad;
+  const size_t planes = ozaki_set_bytes(m, n, digits);
   int8_t* base = static_cast<int8_t*>(work);
   out->rs = base;
-  out->cs = base + planes;
-  out->rowexp = reinterpret_cast<int*>(base + 2 * planes);
+  out->cs = nullptr;  // bound by the caller once ozaki_decide says the column-scaled set is needed
+  out->rowexp = reinterpret_cast<int*>(base + planes);
   out->colexp = out->rowexp + out->m_pad;
-  out->rowhi = reinterpret_cast<uint32_t*>(out->colexp + out->n_pad);
+  out->ext = out->colexp + out->n_pad;
+  out->rowhi = reinterpret_cast<uint32_t*>(out->ext + 8);
   out->colpart = out->rowhi + out->m_pad;
 }
 
@@ -766,26 +829,45 @@ cudaError_t prepare_rows_t(const T* A, int64_t lda, int64_t r0, int64_t r1, cons
   return cudaGetLastError();
 }
 
-template <class T>
-cudaError_t prepare_cols_t(const T* A, int64_t lda, const OzakiA& a, bool slice_rows_too, cudaStream_t st) {
-  const int64_t nblk = (a.m + 255) / 256;
-  colexp_kernel<<<static_cast<unsigned>((a.n_pad + 255) / 256), 256, 0, st>>>(a.colpart, nblk, a.n, a.n_pad, a.colexp);
-  slice_a<T>(a.digits, A, a.m, a.n, lda, 0, a.m_pad, a.rowexp, a.colexp, slice_rows_too ? a.rs : nullptr, a.cs,
-             a.m_pad, a.n_pad, st);
-  count_launch(2);
-  return cudaGetLastError();
-}
-
 cudaError_t ozaki_prepare_rows(const void* A, bool f32, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
                                double* ssq_part, bool slice_rows, cudaStream_t st) {
   return f32 ? prepare_rows_t(static_cast<const float*>(A), lda, r0, r1, a, ssq_part, slice_rows, st)
              : prepare_rows_t(static_cast<const double*>(A), lda, r0, r1, a, ssq_part, slice_rows, st);
 }
 
-cudaError_t ozaki_prepare_cols(const void* A, bool f32, int64_t lda, const OzakiA& a, bool slice_rows_too,
-                               cudaStream_t st) {
-  return f32 ? prepare_cols_t(static_cast<const float*>(A), lda, a, slice_rows_too, st)
-             : prepare_cols_t(static_cast<const double*>(A), lda, a, slice_rows_too, st);
+cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext) {
+  cudaError_t e = cudaMemsetAsync(a->ext, 0x80, 2 * sizeof(int), st);  // very negative
+  if (e != cudaSuccess) return e;
+  const int64_t nblk = (a->m + 255) / 256;
+  colexp_kernel<<<static_cast<unsigned>((a->n_pad + 255) / 256), 256, 0, st>>>(a->colpart, nblk, a->n, a->n_pad,
+                                                                                a->colexp, a->ext);
+  count_launch();
+  if ((e = cudaMemcpyAsync(h_ext, a->ext, 2 * sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  const bool any = h_ext[0] > -100000;  // some non-zero column
+  a->emax = any ? h_ext[0] : 0;
+  const int spread = any ? h_ext[0] + h_ext[1] : 0;
+  const char* v = std::getenv("RFGPU_OZAKI_SHARED");  // experiments / tests: 0 never, 1 always
+  const int force = v ? (v[0] == '1' ? 1 : 0) : -1;
+  a->shared = force >= 0 ? force == 1 : spread <= kSharedSpread;
+  return cudaGetLastError();
+}
+
+template <class T>
+void slice_sets_t(const T* A, int64_t lda, const OzakiA& a, bool rows, bool cols, cudaStream_t st) {
+  slice_a<T>(a.digits, A, a.m, a.n, lda, 0, a.m_pad, a.rowexp, a.colexp, rows ? a.rs : nullptr,
+             cols ? a.cs : nullptr, a.m_pad, a.n_pad, st);
+  count_launch();
+}
+
+cudaError_t ozaki_slice_sets(const void* A, bool f32, int64_t lda, const OzakiA& a, bool rows, bool cols,
+                             cudaStream_t st) {
+  if (!rows && !cols) return cudaSuccess;
+  if (f32)
+    slice_sets_t(static_cast<const float*>(A), lda, a, rows, cols, st);
+  else
+    slice_sets_t(static_cast<const double*>(A), lda, a, rows, cols, st);
+  return cudaGetLastError();
 }
 
 size_t ozaki_nn_work_bytes(const OzakiA& a, int64_t rows, int64_t ell) {
@@ -801,9 +883,8 @@ cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, i
   int8_t* xd = static_cast<int8_t*>(work);
   int* colexp = reinterpret_cast<int*>(xd + static_cast<size_t>(a.digits) * lp * a.n_pad);
   double* ws = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(colexp) + ((sizeof(int) * lp + 255) / 256) * 256);
-  col_exp_kernel<<<static_cast<unsigned>(ell), 256, 0, st>>>(X, a.n, ldx, nullptr, colexp);
-  slice_r(a.digits, X, a.n, ell, ldx, colexp, xd, a.n_pad, lp, st);
-  count_launch(2);
+  cudaError_t e = slice_thin(a.digits, X, a.n, ell, ldx, nullptr, 0, colexp, xd, a.n_pad, lp, st);
+  if (e != cudaSuccess) return e;
   // K = n beyond kSplitK would overflow the int32 group sums: split K
   const int splits = static_cast<int>((a.n_pad + kSplitK - 1) / kSplitK);
   OzParams p{};
@@ -813,8 +894,7 @@ cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, i
   p.rowexp = a.rowexp;
   p.colexp = colexp;
   p.ws_mode = splits > 1 ? 1 : 0;
-  cudaError_t e =
-      launch_digit_gemm(a.digits, a.rs, a.n_pad, true, a.m_pad, xd, lp, a.n_pad, r0, rows, ell, splits, p, false, st);
+  e = launch_digit_gemm(a.digits, a.rs, a.n_pad, true, a.m_pad, xd, lp, a.n_pad, r0, rows, ell, splits, p, false, st);
   if (e != cudaSuccess || splits == 1) return e;
   const int64_t total = rows * ell;
   reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(
@@ -836,20 +916,28 @@ cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell,
   int8_t* qd = static_cast<int8_t*>(work);
   int* colexp = reinterpret_cast<int*>(qd + static_cast<size_t>(a.digits) * lp * a.m_pad);
   double* ws = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(colexp) + ((sizeof(int) * lp + 255) / 256) * 256);
-  // column-scaled digits of A: Z(j, c) = 2^(f_j + g_c) sum_g 2^-(12+8g) acc_g
-  col_exp_kernel<<<static_cast<unsigned>(ell), 256, 0, st>>>(Q, a.m, ldq, nullptr, colexp);
-  slice_r(a.digits, Q, a.m, ell, ldq, colexp, qd, a.m_pad, lp, st);
-  count_launch(2);
+  // Two ways to scale the summation index i (rows of A):
+  //  * column-scaled digits of A (a.cs): Z(j, c) = 2^(f_j + g_c) sum_g 2^-(12+8g) acc_g;
+  //  * shared (a.shared, one digit set for both passes): the row-scaled digits
+  //    a'(i, j) = A(i, j) 2^-e_i with the row factors moved onto Q:
+  //    Q'(i, c) = Q(i, c) 2^(e_i - emax) (exact, <= |Q|), sliced per column with
+  //    2^-g_c; Z(j, c) = 2^(emax + g_c) sum_g 2^-(12+8g) acc_g. The truncation
+  //    error per term is <= 2^-54 2^(emax) max|Q(:, c)| (x2), i.e. at most
+  //    2^(emax - f_j + 2) times the column-scaled bound: ozaki_col_exponents
+  //    only picks it when every non-zero column has f_j >= emax - kSharedSpread.
+  cudaError_t e = a.shared ? slice_thin(a.digits, Q, a.m, ell, ldq, a.rowexp, a.emax, colexp, qd, a.m_pad, lp, st)
+                           : slice_thin(a.digits, Q, a.m, ell, ldq, nullptr, 0, colexp, qd, a.m_pad, lp, st);
+  if (e != cudaSuccess) return e;
   const int splits = static_cast<int>((a.m_pad + kSplitK - 1) / kSplitK);
   OzParams p{};
   p.C = splits > 1 ? ws : Z;
   p.ldc = ldz;
   p.c_row0 = 0;
-  p.rowexp = a.colexp;  // output row j of A^T Q = column j of A
+  p.rowexp = a.shared ? nullptr : a.colexp;  // output row j of A^T Q = column j of A
   p.colexp = colexp;
+  p.cshift = a.shared ? a.emax : 0;
   p.ws_mode = splits > 1 ? 1 : 0;
-  cudaError_t e =
-      launch_digit_gemm(a.digits, a.cs, a.n_pad, false, 0, qd, lp, a.m_pad, 0, a.n, ell, splits, p, true, st);
+  e = launch_digit_gemm(a.digits, a.shared ? a.rs : a.cs, a.n_pad, false, 0, qd, lp, a.m_pad, 0, a.n, ell, splits, p, true, st);
   if (e != cudaSuccess || splits == 1) return e;
   const int64_t total = a.n * ell;
   reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(

@@ -393,15 +393,16 @@ std::vector<std::pair<int64_t, int64_t>> upload_panels(int64_t m) {
 // planes of A are built once (inside pass 1) and serve every later pass.
 struct OzPasses {
   bool on = false;
+  bool tn = true;  // A^T Q on the digits (false: the column-scaled set did not fit; DMMA)
   OzakiA a{};
-  DBuf planes, work;
+  DBuf planes, cplanes, work;
   Status init(rfgpu_ctx* c, const rfgpu_matrix* m, int64_t ell) {
     on = ozaki_enabled(m->m, m->n) && m->m > 0 && m->n > 0;
     if (!on) return {};
     const int digits = m->f32 ? 4 : 7;  // FP32 data: 4 digits (30 bits) per element
     const OzakiA lay = ozaki_layout(m->m, m->n, digits);
-    // The digit planes take 2 x digits bytes per element of A: when HBM cannot
-    // hold them next to A, the passes stay on the FP64 tensor pipe (DMMA).
+    // One digit set takes `digits` bytes per element of A: when HBM cannot
+    // hold it next to A, the passes stay on the FP64 tensor pipe (DMMA).
     if (!planes.alloc(ozaki_a_bytes(m->m, m->n, digits), c->stream).ok() ||
         !work.alloc(std::max(ozaki_nn_work_bytes(lay, m->m, ell), ozaki_tn_work_bytes(lay, ell)), c->stream).ok()) {
       on = false;
@@ -411,12 +412,31 @@ struct OzPasses {
     ozaki_bind(planes.p, m->m, m->n, digits, &a);
     return {};
   }
-  // Whole resident A: stats (one read), then the digit sets (one read):
-  // row-scaled (A X) only when `rows`, column-scaled (A^T Q) always.
+  // After every row's stats: column exponents; one shared digit set when the
+  // column scales allow it (ozaki.cu kSharedSpread), else a second,
+  // column-scaled set for A^T Q (on DMMA if that set does not fit).
+  Status columns(rfgpu_ctx* c, const rfgpu_matrix* m) {
+    RF_CUDA(ozaki_col_exponents(&a, c->stream, c->h_info));
+    if (!a.shared) {
+      if (cplanes.alloc(ozaki_set_bytes(m->m, m->n, a.digits), c->stream).ok()) {
+        a.cs = cplanes.as<int8_t>();
+      } else {
+        tn = false;
+        if (std::getenv("RFGPU_DEBUG")) std::fprintf(stderr, "[rfgpu] column-scaled digits do not fit: DMMA A^T Q\n");
+      }
+    }
+    if (std::getenv("RFGPU_DEBUG"))
+      std::fprintf(stderr, "[rfgpu] digit sets: %s (column exponents %d..%d)\n", a.shared ? "shared" : "two",
+                   -c->h_info[1], c->h_info[0]);
+    return {};
+  }
+  // Whole resident A: stats (one read), then the digit set(s) (one read):
+  // row-scaled when `rows` (A X) or shared, column-scaled when not shared.
   Status prepare(rfgpu_ctx* c, const rfgpu_matrix* m, double* ssq, bool rows = true) {
     Timed t(c, "ozaki_slice");
     RF_CUDA(ozaki_prepare_rows(m->dev, m->f32, m->lda, 0, m->m, a, ssq, false, c->stream));
-    RF_CUDA(ozaki_prepare_cols(m->dev, m->f32, m->lda, a, rows, c->stream));
+    RF_TRY(columns(c, m));
+    RF_CUDA(ozaki_slice_sets(m->dev, m->f32, m->lda, a, rows || a.shared, tn && !a.shared, c->stream));
     return {};
   }
 };
@@ -464,7 +484,7 @@ Status pass_nn(rfgpu_ctx* c, const rfgpu_matrix* a, const double* X, int64_t col
 // Z = A^T Y (Y m x cols), not summed over ranks.
 Status pass_tn_raw(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Y, int64_t ldy, int64_t cols, double* Z,
                    OzPasses* oz) {
-  if (oz && oz->on) {
+  if (oz && oz->on && oz->tn) {
     Timed t(c, "pass_tn");
     RF_CUDA(ozaki_tn(oz->a, Y, ldy, cols, Z, a->n, oz->work.p, c->stream));
     return {};
@@ -511,9 +531,10 @@ Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, 
     s = pass1_rows(c, a, G, ell, Y, ldy, ssq + off, r0, r0 + rows, oz, false);
     off += oz.on ? ozaki_ssq_slots(rows, a->n) : sumsq_slots(c, rows, ell, n);
   }
-  if (s.ok() && oz.on) {  // all rows landed: column exponents and the A^T Q digits
+  if (s.ok() && oz.on) {  // all rows landed: column exponents, and the A^T Q digits unless shared
     Timed t(c, "ozaki_slice");
-    if (ozaki_prepare_cols(A, false, lda, oz.a, false, st) != cudaSuccess)
+    s = oz.columns(c, a);
+    if (s.ok() && ozaki_slice_sets(A, false, lda, oz.a, false, oz.tn && !oz.a.shared, st) != cudaSuccess)
       s = make_err(RFGPU_ECUDA, "pass 1: slicing failed");
   }
   a->src = nullptr;  // issued: every later consumer is ordered after the waits above

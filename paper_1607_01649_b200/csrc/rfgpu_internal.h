@@ -37,21 +37,27 @@ cudaError_t gemm_f64(bool trans_a, int64_t M, int64_t N, int64_t K, const double
 cudaError_t sum_array(const double* x, int64_t n, double* out, cudaStream_t st);
 
 // ---- FP64 passes on the INT8 tensor cores (ozaki.cu) -----------------------
-// Digit planes of A (m x n, FP64) for Y = A X and Z = A^T Q (Ozaki scheme,
-// 8 signed 7-bit digits per operand, tcgen05 kind::i8, FP64 recombination).
+// Digit planes of A (m x n, FP64 or FP32) for Y = A X and Z = A^T Q (Ozaki
+// scheme, 7 (FP64) / 4 (FP32) balanced 8-bit digits per operand, tcgen05
+// kind::i8, FP64 recombination).
 struct OzakiA {
-  int8_t* rs;   // [8][n_pad][m_pad] digits of A(i,j) 2^-rowexp[i] (column-major; read M-major by A X)
-  int8_t* cs;   // [8][n_pad][m_pad] digits of A(i,j) 2^-colexp[j] (read K-major by A^T Q)
+  int8_t* rs;   // [digits][n_pad][m_pad] digits of A(i,j) 2^-rowexp[i] (column-major; A X reads them
+                // M-major; A^T Q reads them K-major when `shared`)
+  int8_t* cs;   // [digits][n_pad][m_pad] digits of A(i,j) 2^-colexp[j] (A^T Q when !shared; caller-bound)
   int* rowexp;  // m_pad: |A(i,:)| < 2^rowexp[i]
   int* colexp;  // n_pad: |A(:,j)| < 2^colexp[j]
+  int* ext;     // 2 (+pad): max column exponent, -min column exponent (non-zero columns)
   uint32_t* rowhi;    // m_pad row maxima (high words of |A(i,:)|)
   uint32_t* colpart;  // (m_pad / 256) x n_pad per-block column maxima (high words)
   int64_t m, n, m_pad, n_pad;
   int digits;   // 7 (FP64 A) or 4 (FP32 A)
+  bool shared;  // one digit set (rs) serves both passes (ozaki_col_exponents decides)
+  int emax;     // max column exponent (shared mode's thin-operand shift)
 };
 bool ozaki_enabled(int64_t m, int64_t n);  // RFGPU_OZAKI=0/1 overrides the size rule
 OzakiA ozaki_layout(int64_t m, int64_t n, int digits);  // shapes only (no buffers)
-size_t ozaki_a_bytes(int64_t m, int64_t n, int digits);
+size_t ozaki_set_bytes(int64_t m, int64_t n, int digits);  // one digit set (rs or cs)
+size_t ozaki_a_bytes(int64_t m, int64_t n, int digits);    // rs + exponents + maxima (not cs)
 void ozaki_bind(void* work, int64_t m, int64_t n, int digits, OzakiA* out);  // carve ozaki_a_bytes
 int64_t ozaki_ssq_slots(int64_t rows, int64_t n);  // ||A||_F^2 partials of a row block
 // Rows [r0, r1) (r0 a multiple of 256): row exponents, ||A||_F^2 partials
@@ -59,11 +65,13 @@ int64_t ozaki_ssq_slots(int64_t rows, int64_t n);  // ||A||_F^2 partials of a ro
 // slice_rows, the row-scaled digits of these rows (all A X needs).
 cudaError_t ozaki_prepare_rows(const void* A, bool f32, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
                                double* ssq_part, bool slice_rows, cudaStream_t st);
-// After every row block's stats: column exponents and the column-scaled
-// digits (A^T Q); slice_rows_too also writes the row-scaled digits in the
-// same read of A.
-cudaError_t ozaki_prepare_cols(const void* A, bool f32, int64_t lda, const OzakiA& a, bool slice_rows_too,
-                               cudaStream_t st);
+// After every row block's stats: column exponents, and the choice between one
+// shared digit set and a second, column-scaled set for A^T Q (synchronises
+// the stream; h_ext: 2 pinned ints).
+cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext);
+// One read of A writing the row-scaled (rows) and / or column-scaled (cols) digits.
+cudaError_t ozaki_slice_sets(const void* A, bool f32, int64_t lda, const OzakiA& a, bool rows, bool cols,
+                             cudaStream_t st);
 size_t ozaki_nn_work_bytes(const OzakiA& a, int64_t rows, int64_t ell);
 // Y(r0:r1, 0:ell) = A(r0:r1, :) X  (X n x ell, col-major)
 cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, int64_t ldx, int64_t ell, double* Y,

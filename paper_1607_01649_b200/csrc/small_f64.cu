@@ -30,84 +30,110 @@ namespace {
 constexpr int kSmallThreads = 1024;
 
 // ------------------------------------------------------------ chol_inv ---
-// Packed upper-triangular storage P (column-packed: (i, j) at j(j+1)/2 + i,
-// i <= j), in shared memory when it fits (c <= 236), else in global memory.
-// Phase 1: right-looking Cholesky in the reference recurrence order
-// (dense.cpp:763-786): row j is divided by sqrt(pivot), then each trailing
-// entry (i, col), j < i <= col, subtracts R(j,i) R(j,col).
-// Phase 2: R^{-1} one warp per column: back substitution R x = e_j in axpy
-// form, x distributed over the lanes' registers (S slots per lane).
+// One CTA, the packed upper triangle P (column-packed: (i, j) at
+// j(j+1)/2 + i, i <= j) in shared memory (c <= 236).
+// Phase 1: outer-product Cholesky on the UNSCALED rows: step j subtracts
+// P(j,i) P(j,col) / P(j,j) from every trailing entry (i, col), j < i <= col.
+// Row j is final after step j - 1 and only rows > j are written in step j,
+// so one barrier per step suffices; afterwards R(j, :) = P(j, :) / sqrt(P(j,j)).
+// The pivot test is the reference rule (pivot <= 1e-14 max initial diagonal,
+// proj/src/dense.cpp:763-786) plus the CholeskyQR gate statistic
+// min_j pivot_j / trace(G).
+// Phase 2: R^{-1}, one warp per column: back substitution R x = e_j in axpy
+// form from shared memory, x distributed over the lanes' registers (S slots).
 __device__ __forceinline__ int64_t pk(int i, int j) { return static_cast<int64_t>(j) * (j + 1) / 2 + i; }
 
-template <bool SMEM, int S>
+template <int S>
 __global__ void __launch_bounds__(kSmallThreads, 1)
     chol_inv_kernel(const double* __restrict__ G, int c, double* __restrict__ R, double* __restrict__ Rinv,
-                    double* __restrict__ work, int* info, double* info_d) {
+                    int* info, double* info_d) {
   extern __shared__ double sm[];
-  double* base = SMEM ? sm : work;
-  double* rowj = base;          // [c]  current pivot row of R
-  double* rdiag = base + c;     // [c]  1 / R(j,j)
-  double* P = base + 2 * c;     // packed upper triangle
-  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  double* rs = sm;          // [c] sqrt of the pivots
+  double* P = sm + c;       // packed upper triangle
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   __shared__ double s_floor, s_trace, s_minratio;
   __shared__ int s_fail;
 
   for (int j = warp; j < c; j += nwarps)
     for (int i = lane; i <= j; i += 32) P[pk(i, j)] = G[static_cast<int64_t>(j) * c + i];
-  if (tid == 0) {
+  if (warp == 0) {
     double mx = 0.0, tr = 0.0;
-    for (int j = 0; j < c; ++j) {
+    for (int j = lane; j < c; j += 32) {
       const double g = G[static_cast<int64_t>(j) * c + j];
       mx = fmax(mx, fabs(g));
       tr += g;
     }
-    s_floor = 1e-14 * mx;
-    s_trace = tr;
-    s_minratio = INFINITY;
-    s_fail = 0;
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    }
+    if (lane == 0) {
+      s_floor = 1e-14 * mx;
+      s_trace = tr;
+      s_minratio = INFINITY;
+      s_fail = 0;
+    }
   }
   __syncthreads();
-
+  const double floor = s_floor, trace = s_trace;
+  int fail = 0;
   for (int j = 0; j < c; ++j) {
-    if (tid == 0) {
-      const double d = P[pk(j, j)];
-      if (d <= s_floor || !(d > 0.0)) {
-        s_fail = j + 1;
-      } else {
-        s_minratio = fmin(s_minratio, s_trace > 0.0 ? d / s_trace : 0.0);
-        const double cjj = sqrt(d);
-        P[pk(j, j)] = cjj;
-        rowj[j] = cjj;
-        rdiag[j] = 1.0 / cjj;
-      }
+    const double d = P[pk(j, j)];
+    if (d <= floor || !(d > 0.0)) {  // every thread sees the same pivot
+      fail = j + 1;
+      break;
     }
-    __syncthreads();
-    if (s_fail) break;
-    const double cjj = rowj[j];
-    for (int col = j + 1 + tid; col < c; col += nthr) {
-      const double v = P[pk(j, col)] / cjj;
-      P[pk(j, col)] = v;
-      rowj[col] = v;
-    }
-    __syncthreads();
+    if (tid == 0) s_minratio = fmin(s_minratio, trace > 0.0 ? d / trace : 0.0);
+    const double* pj = P + pk(0, 0);
     for (int col = j + 1 + warp; col < c; col += nwarps) {
-      const double rc = rowj[col];
       double* pc = P + pk(0, col);
-      for (int i = j + 1 + lane; i <= col; i += 32) pc[i] -= rowj[i] * rc;
+      const double f = pc[j] / d;
+      for (int i = j + 1 + lane; i <= col; i += 32) pc[i] = fma(-pj[pk(j, i)], f, pc[i]);
     }
     __syncthreads();
   }
   if (tid == 0) {
-    info[0] = s_fail;
+    info[0] = fail;
     info_d[0] = s_minratio;
   }
-  if (s_fail) return;
-
+  if (fail) return;
+  for (int j = tid; j < c; j += blockDim.x) rs[j] = sqrt(P[pk(j, j)]);
+  __syncthreads();
+  for (int col = warp; col < c; col += nwarps)
+    for (int i = lane; i <= col; i += 32) P[pk(i, col)] = i == col ? rs[col] : P[pk(i, col)] / rs[i];
+  __syncthreads();
   for (int j = warp; j < c; j += nwarps)
     for (int i = lane; i < c; i += 32) R[static_cast<int64_t>(j) * c + i] = i <= j ? P[pk(i, j)] : 0.0;
 
-  // R^{-1} is formed by trinv_upper (many CTAs, one warp per column).
-  (void)Rinv;
+  // R^{-1}: columns dealt in a zig-zag so every warp gets a similar total length
+  for (int t = 0;; ++t) {
+    const int j = (t & 1) ? 32 * t + (nwarps - 1 - warp) : 32 * t + warp;
+    if (32 * t >= c) break;
+    if (j >= c) continue;
+    double x[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) x[s] = (lane + 32 * s == j) ? 1.0 : 0.0;
+    for (int i = j; i >= 0; --i) {
+      const int si = i >> 5;
+      double v = 0.0;
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        if (s == si) v = x[s];
+      const double* pi = P + pk(0, i);  // column i of R
+      const double xi = __shfl_sync(0xffffffffu, v, i & 31) / pi[i];
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int r = lane + 32 * s;
+        if (r == i) x[s] = xi;
+        else if (r < i) x[s] = fma(-xi, pi[r], x[s]);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int r = lane + 32 * s;
+      if (r < c) Rinv[static_cast<int64_t>(j) * c + r] = r <= j ? x[s] : 0.0;
+    }
+  }
 }
 
 // ----------------------------------------------------------- jacobi_svd ---
@@ -578,6 +604,9 @@ JacobiLayout jacobi_layout(int64_t mr, int64_t c) {
 }  // namespace
 
 size_t chol_inv_work_bytes(int64_t c) { return sizeof(double) * (2 * c + c * (c + 1) / 2); }
+namespace {
+size_t chol_smem_bytes(int64_t c) { return sizeof(double) * (c + c * (c + 1) / 2); }
+}  // namespace
 
 namespace {
 // ---- blocked Cholesky for l > 256 (the packed triangle no longer fits in
@@ -762,23 +791,21 @@ cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double
                      double* info_d, cudaStream_t st) {
   if (c <= 0) return cudaSuccess;
   if (c > 352) return cudaErrorInvalidValue;
-  const size_t smem = chol_inv_work_bytes(c);
+  const size_t smem = chol_smem_bytes(c);
   const int ci = static_cast<int>(c);
   if (smem <= 224 * 1024 && c <= 256) {
     static bool cfg = false;
     if (!cfg) {
-      cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            224 * 1024);
       if (e != cudaSuccess) return e;
       cfg = true;
     }
-    chol_inv_kernel<true, 8><<<1, kSmallThreads, smem, st>>>(G, ci, R, Rinv, work, info, info_d);
+    chol_inv_kernel<8><<<1, kSmallThreads, smem, st>>>(G, ci, R, Rinv, info, info_d);
     count_launch();
-  } else {
-    cudaError_t e = chol_blocked(G, ci, R, work, info, info_d, st);
-    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
   }
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = chol_blocked(G, ci, R, work, info, info_d, st);
   if (e != cudaSuccess) return e;
   return trinv_upper(R, c, ci, Rinv, st);
 }

@@ -63,6 +63,47 @@ def test_digit_gemm_matches_extended_precision(ctx, ozaki, m, n, cols, trans):
     assert np.all(got[:, 2] == 0.0)
 
 
+@pytest.mark.parametrize("shared", ["0", "1", None])
+@pytest.mark.parametrize("m,n,cols", [(1000, 777, 40), (40000, 129, 70)])
+@pytest.mark.parametrize("trans", [False, True])
+def test_digit_gemm_one_or_two_digit_sets(ctx, ozaki, monkeypatch, shared, m, n, cols, trans):
+    """Columns of comparable scale (exponents within 2 bits): A^T Q may run on
+    the row-scaled digits with the row factors moved onto Q (one digit set for
+    both passes). Forced either way (RFGPU_OZAKI_SHARED) and by the size rule,
+    the products stay within the column-scaled bar."""
+    if shared is None:
+        monkeypatch.delenv("RFGPU_OZAKI_SHARED", raising=False)
+    else:
+        monkeypatch.setenv("RFGPU_OZAKI_SHARED", shared)
+    rng = np.random.default_rng(m + cols)
+    a = rng.standard_normal((m, n))
+    a[3] *= 8.0              # a dominant row keeps every column maximum in one binade
+    a[5] *= 1e-150           # tiny row
+    a[7] = 0.0               # zero row
+    x = rng.standard_normal((m if trans else n, cols))
+    x[:, 1] *= 1e80
+    x[:, 2] = 0.0
+    a = np.asfortranarray(a)
+    got = rf.multiply(a, x, trans=trans, ctx=ctx)
+    want = exact_product(a, x, trans)
+    assert scaled_err(got, want, a, x, trans) < 1e-14
+    assert np.all(got[:, 2] == 0.0)
+
+
+def test_graded_columns_keep_two_digit_sets(ctx, ozaki, monkeypatch):
+    """A column 2^-30 below the others: the size rule must keep the
+    column-scaled set for A^T Q (the shared set would lose ~30 bits there)."""
+    monkeypatch.delenv("RFGPU_OZAKI_SHARED", raising=False)
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((3000, 300))
+    a[:, 4] *= 2.0 ** -30
+    q = rng.standard_normal((3000, 16))
+    a = np.asfortranarray(a)
+    got = rf.multiply(a, q, trans=True, ctx=ctx)
+    want = exact_product(a, q, True)
+    assert scaled_err(got, want, a, q, True) < 1e-14
+
+
 @pytest.mark.parametrize("case", [(600, 400, 20, 10, 1), (2000, 2000, 50, 10, 1), (5000, 1500, 100, 10, 2)])
 def test_rsvd_on_digit_gemm_matches_oracle(ctx, port, ozaki, case):
     m, n, k, p, q = case
