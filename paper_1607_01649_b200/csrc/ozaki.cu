@@ -56,7 +56,8 @@ constexpr int kThreads = 192;
 // digits then loses at most kSharedSpread + 2 bits against column-scaled
 // digits (see ozaki_tn).
 constexpr int kSharedSpread = 2;
-constexpr int kDefaultBK = 64;  // stage depth (see Dig); RFGPU_OZAKI_BK overrides   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr int kDefaultBK = 64;  // stage depth (see Dig); RFGPU_OZAKI_BK overrides
+constexpr bool kDefaultPersist = true;  // persistent digit GEMM grid; RFGPU_OZAKI_PERSIST overrides   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
 
 // Per digit count S: S accumulator groups of OBN TMEM columns; as many
 // 2-digit-plane... stages as fit in shared memory.
@@ -366,6 +367,7 @@ struct OzParams {
   int cshift;         // extra output exponent (the thin operand's row pre-scaling shift)
   int ws_mode;        // 1: C is [split][N_real][M_real]
   int cl;             // cluster size along N tiles: the A tile is TMA-multicast to all of them
+  int64_t ngroups;    // tile groups (all tiles / cl); the grid may be smaller (persistent)
 };
 
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
@@ -414,6 +416,33 @@ __device__ __forceinline__ uint64_t umma_desc_mn(const void* p) {
 
 // L_MN: the L digit planes are read M-major (column-major A digits serving
 // Y = A X), else K-major (A^T Q).
+//
+// Persistent over tile groups (one group = the cl CTAs of a cluster, each one
+// (m, n, split) tile): cluster c takes groups c, c + #clusters, ... The TMA
+// producer runs straight on into the next tile's K blocks while the epilogue
+// drains the previous tile, and the MMA issuer waits only for the epilogue to
+// release TMEM (tfree). With one group per cluster (grid = all tiles) this is
+// the plain one-tile-per-CTA kernel.
+struct TileCoord {
+  int64_t lrow0, ncol0, kb0;
+  int nk, split;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(const OzParams& p, int64_t tile) {
+  // n-tile fastest: the CTAs sharing an L tile run together (L2 reuse)
+  TileCoord t;
+  const int nt = static_cast<int>(tile % p.ntn);
+  const int64_t rest = tile / p.ntn;
+  const int mt = static_cast<int>(rest % p.mtn);
+  t.split = static_cast<int>(rest / p.mtn);
+  t.lrow0 = p.row0 + static_cast<int64_t>(mt) * OBM;
+  t.ncol0 = static_cast<int64_t>(nt) * OBN;
+  t.kb0 = t.split * p.kb_per_split;
+  const int64_t kb1 = min(p.kb_total, t.kb0 + p.kb_per_split);
+  t.nk = static_cast<int>(kb1 - t.kb0);
+  return t;
+}
+
 template <bool L_MN, int S, int BK>
 __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmL,
                                                                   const __grid_constant__ CUtensorMap tmR,
@@ -427,21 +456,12 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * BSZ);
   uint64_t* empty = full + kStages;
   uint64_t* done = empty + kStages;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tfree = done + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfree + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // n-tile fastest: the CTAs sharing an L tile run together (L2 reuse)
-  const int64_t bid = blockIdx.x;
-  const int nt = static_cast<int>(bid % p.ntn);
-  const int64_t rest = bid / p.ntn;
-  const int mt = static_cast<int>(rest % p.mtn);
-  const int split = static_cast<int>(rest / p.mtn);
-  const int64_t lrow0 = p.row0 + static_cast<int64_t>(mt) * OBM;
-  const int64_t ncol0 = static_cast<int64_t>(nt) * OBN;
-  const int64_t kb0 = split * p.kb_per_split;
-  const int64_t kb1 = min(p.kb_total, kb0 + p.kb_per_split);
-  const int nk = static_cast<int>(kb1 - kb0);
   const int cl = p.cl;
-  const int crank = nt % cl;  // rank in the cluster (clusters span consecutive n-tiles)
+  const int crank = static_cast<int>(blockIdx.x % cl);  // rank in the cluster (consecutive n-tiles)
+  const int64_t cid = blockIdx.x / cl, ncl = gridDim.x / cl;
   const uint16_t cmask = static_cast<uint16_t>((1u << cl) - 1u);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -449,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
       mbar_init(&empty[s], cl);  // every CTA of the cluster must release the (shared) A stage
     }
     mbar_init(done, 1);
+    mbar_init(tfree, 4);  // the four epilogue warps
     mbar_fence_init();
   }
   if (warp == 1) {
@@ -466,112 +487,138 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
   const uint32_t tmem = *tslot;
 
   if (warp == 0 && lane == 0) {
-    for (int kb = 0; kb < nk; ++kb) {
-      const int st = kb % kStages;
-      const uint32_t ph = (kb / kStages) & 1;
-      mbar_wait(&empty[st], ph ^ 1);
-      mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(ASZ + BSZ));
-      const int kx = static_cast<int>((kb0 + kb) * BK);
+    uint32_t it = 0;  // K blocks issued over all of this CTA's tiles
+    for (int64_t g = cid; g < p.ngroups; g += ncl) {
+      const TileCoord tc = tile_coord(p, g * cl + crank);
+      for (int kb = 0; kb < tc.nk; ++kb, ++it) {
+        const int st = static_cast<int>(it % kStages);
+        const uint32_t ph = (it / kStages) & 1;
+        mbar_wait(&empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(ASZ + BSZ));
+        const int kx = static_cast<int>((tc.kb0 + kb) * BK);
 #pragma unroll
-      for (int s = 0; s < kS; ++s) {
-        // A planes round-robin over the cluster, multicast to all of it
-        // K-major L: box {64 K-bytes, 128 rows} at (k, plane row); M-major L
-        // (planes [kS][K_rows][M]): box {128 M-bytes, 64 K-rows} at (m, plane k)
-        const int lc0 = L_MN ? static_cast<int>(lrow0) : kx;
-        const int lc1 = L_MN ? static_cast<int>(s * p.L_rows + (kb0 + kb) * BK) : static_cast<int>(s * p.L_rows + lrow0);
-        if (cl == 1)
-          tma2d(sA + st * ASZ + s * OBM * BK, &tmL, &full[st], lc0, lc1);
-        else if (s % cl == crank)
-          tma2d_mc(sA + st * ASZ + s * OBM * BK, &tmL, &full[st], lc0, lc1, cmask);
-        tma2d(sB + st * BSZ + s * OBN * BK, &tmR, &full[st], kx, static_cast<int>(s * p.R_rows + ncol0));
+        for (int s = 0; s < kS; ++s) {
+          // A planes round-robin over the cluster, multicast to all of it
+          // K-major L: box {BK K-bytes, 128 rows} at (k, plane row); M-major L
+          // (planes [kS][K_rows][M]): box {128 M-bytes, BK K-rows} at (m, plane k)
+          const int lc0 = L_MN ? static_cast<int>(tc.lrow0) : kx;
+          const int lc1 = L_MN ? static_cast<int>(s * p.L_rows + (tc.kb0 + kb) * BK)
+                               : static_cast<int>(s * p.L_rows + tc.lrow0);
+          if (cl == 1)
+            tma2d(sA + st * ASZ + s * OBM * BK, &tmL, &full[st], lc0, lc1);
+          else if (s % cl == crank)
+            tma2d_mc(sA + st * ASZ + s * OBM * BK, &tmL, &full[st], lc0, lc1, cmask);
+          tma2d(sB + st * BSZ + s * OBN * BK, &tmR, &full[st], kx, static_cast<int>(s * p.R_rows + tc.ncol0));
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
     // For a fixed A digit s the groups g = s + t of consecutive t are
     // consecutive 64-column TMEM blocks, and the B digit planes are
     // consecutive 64-row blocks in shared memory: one MMA with N = 64 x (up to
-    // 4 digits of B) covers them. 12 MMAs per K step instead of 36, each A
-    // tile read from shared memory once per 4 B digits.
+    // 4 digits of B) covers them. 10 MMAs per 32 K-bytes instead of 28, each
+    // A tile read from shared memory once per 4 B digits.
     auto idesc_n = [](int n) {
       return (2u << 4) | (1u << 7) | (1u << 10) | (L_MN ? (1u << 15) : 0u) | (static_cast<uint32_t>(n >> 3) << 17) |
              (static_cast<uint32_t>(OBM >> 4) << 24);
     };
-    for (int kb = 0; kb < nk; ++kb) {
-      const int st = kb % kStages;
-      const uint32_t ph = (kb / kStages) & 1;
-      mbar_wait(&full[st], ph);
+    uint32_t it = 0, tt = 0;
+    for (int64_t g = cid; g < p.ngroups; g += ncl, ++tt) {
+      const TileCoord tc = tile_coord(p, g * cl + crank);
+      mbar_wait(tfree, (tt & 1) ^ 1);  // the epilogue has drained the previous tile
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int kb = 0; kb < tc.nk; ++kb, ++it) {
+        const int st = static_cast<int>(it % kStages);
+        const uint32_t ph = (it / kStages) & 1;
+        mbar_wait(&full[st], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int kk = 0; kk < BK / 32; ++kk) {
+        for (int kk = 0; kk < BK / 32; ++kk) {
 #pragma unroll
-        for (int s = 0; s < kS; ++s) {
+          for (int s = 0; s < kS; ++s) {
 #pragma unroll
-          for (int t0 = 0; t0 < kS - s; t0 += 4) {
-            const int cnt = (kS - s - t0) < 4 ? (kS - s - t0) : 4;
-            // M-major: K advances by 32 K-rows = 4 swizzle atoms
-            const uint64_t da = L_MN ? umma_desc_mn<BK>(sA + st * ASZ + s * OBM * BK + kk * 32 * OBM)
-                                     : umma_desc<BK>(sA + st * ASZ + s * OBM * BK + kk * 32);
-            const uint64_t db = umma_desc<BK>(sB + st * BSZ + t0 * OBN * BK + kk * 32);
-            // groups s + t0 .. s + t0 + cnt - 1; every group is first written by s = 0
-            const uint32_t accum = (kb == 0 && kk == 0 && s == 0) ? 0u : 1u;
-            asm volatile(
-                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (s + t0) * OBN),
-                "l"(da), "l"(db), "r"(idesc_n(OBN * cnt)), "r"(accum));
+            for (int t0 = 0; t0 < kS - s; t0 += 4) {
+              const int cnt = (kS - s - t0) < 4 ? (kS - s - t0) : 4;
+              // M-major: K advances by 32 K-rows = 4 swizzle atoms
+              const uint64_t da = L_MN ? umma_desc_mn<BK>(sA + st * ASZ + s * OBM * BK + kk * 32 * OBM)
+                                       : umma_desc<BK>(sA + st * ASZ + s * OBM * BK + kk * 32);
+              const uint64_t db = umma_desc<BK>(sB + st * BSZ + t0 * OBN * BK + kk * 32);
+              // groups s + t0 .. s + t0 + cnt - 1; every group is first written by s = 0
+              const uint32_t accum = (kb == 0 && kk == 0 && s == 0) ? 0u : 1u;
+              asm volatile(
+                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (s + t0) * OBN),
+                  "l"(da), "l"(db), "r"(idesc_n(OBN * cnt)), "r"(accum));
+            }
           }
         }
-      }
-      if (cl == 1)
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         smem_u32(&empty[st]))
-                     : "memory");
-      else  // release this stage in every CTA of the cluster
-        asm volatile(
-            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                smem_u32(&empty[st])),
-            "h"(cmask)
-            : "memory");
-    }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(done))
-                 : "memory");
-  } else if (warp >= 2) {
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int q = warp & 3;  // TMEM lane quarter of this warp
-    const int64_t lrow = lrow0 + q * 32 + lane;
-    const int64_t orow = p.c_row0 + (lrow - p.row0);
-    const int rex = (p.rowexp && nk > 0) ? p.rowexp[lrow] : 0;
-    const bool row_ok = orow < p.M_real + p.c_row0 && lrow - p.row0 < p.M_real;
-    for (int c = 0; c < OBN; c += 16) {
-      double acc[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = 0.0;
-      if (nk > 0) {
-#pragma unroll
-        for (int g = kS - 1; g >= 0; --g) {
-          uint32_t r[16];
-          const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + g * OBN + c;
+        if (cl == 1)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&empty[st]))
+                       : "memory");
+        else  // release this stage in every CTA of the cluster
           asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-              : "r"(ta));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          const double sc = ldexp(1.0, -12 - 8 * g);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] = fma(static_cast<double>(static_cast<int32_t>(r[j])), sc, acc[j]);
-        }
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  smem_u32(&empty[st])),
+              "h"(cmask)
+              : "memory");
       }
-      if (row_ok) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(done))
+                   : "memory");
+    }
+  } else if (warp >= 2) {
+    const int q = warp & 3;  // TMEM lane quarter of this warp
+    uint32_t tt = 0;
+    for (int64_t g = cid; g < p.ngroups; g += ncl, ++tt) {
+      const TileCoord tc = tile_coord(p, g * cl + crank);
+      mbar_wait(done, tt & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t lrow = tc.lrow0 + q * 32 + lane;
+      const int64_t orow = p.c_row0 + (lrow - p.row0);
+      const int rex = (p.rowexp && tc.nk > 0) ? p.rowexp[lrow] : 0;
+      const bool row_ok = orow < p.M_real + p.c_row0 && lrow - p.row0 < p.M_real;
+      for (int c = 0; c < OBN; c += 16) {
+        uint32_t r[kS][16];
+        if (tc.nk > 0) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int64_t col = ncol0 + c + j;
-          if (col < p.N_real) {
-            const double v = ldexp(acc[j], rex + p.colexp[col] + p.cshift);
-            if (p.ws_mode)
-              p.C[(static_cast<int64_t>(split) * p.N_real + col) * p.M_real + (lrow - p.row0)] = v;
-            else
-              p.C[col * p.ldc + orow] = v;
+          for (int gg = 0; gg < kS; ++gg) {
+            const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + gg * OBN + c;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(r[gg][0]), "=r"(r[gg][1]), "=r"(r[gg][2]), "=r"(r[gg][3]), "=r"(r[gg][4]), "=r"(r[gg][5]),
+                  "=r"(r[gg][6]), "=r"(r[gg][7]), "=r"(r[gg][8]), "=r"(r[gg][9]), "=r"(r[gg][10]), "=r"(r[gg][11]),
+                  "=r"(r[gg][12]), "=r"(r[gg][13]), "=r"(r[gg][14]), "=r"(r[gg][15])
+                : "r"(ta));
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
+        if (c + 16 == OBN) {  // every TMEM column of this tile is in registers: release it
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tfree);
+        }
+        double acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+        if (tc.nk > 0) {
+#pragma unroll
+          for (int gg = kS - 1; gg >= 0; --gg) {
+            const double sc = ldexp(1.0, -12 - 8 * gg);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = fma(static_cast<double>(static_cast<int32_t>(r[gg][j])), sc, acc[j]);
+          }
+        }
+        if (row_ok) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int64_t col = tc.ncol0 + c + j;
+            if (col < p.N_real) {
+              const double v = ldexp(acc[j], rex + p.colexp[col] + p.cshift);
+              if (p.ws_mode)
+                p.C[(static_cast<int64_t>(tc.split) * p.N_real + col) * p.M_real + (lrow - p.row0)] = v;
+              else
+                p.C[col * p.ldc + orow] = v;
+            }
           }
         }
       }
@@ -632,6 +679,12 @@ bool digit_tmap(CUtensorMap* tm, const int8_t* base, int64_t rows, int64_t inner
 // 2-stage ring), so the caller chooses.
 // L_mn: L planes are [kS][K_pad][L_M] (M contiguous, L_rows = K_pad rows per
 // plane, L_M = M extent), else [kS][L_rows][K_pad].
+// RFGPU_OZAKI_PERSIST=0: one CTA per tile; otherwise the persistent grid.
+bool persistent() {
+  const char* e = std::getenv("RFGPU_OZAKI_PERSIST");
+  return e ? e[0] != '0' : kDefaultPersist;
+}
+
 template <int S, int BK>
 cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int64_t L_M, const int8_t* R,
                                 int64_t R_rows, int64_t K_pad, int64_t row0, int64_t rows, int64_t N_real, int splits,
@@ -673,6 +726,7 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
         p.cl = c;
         break;
       }
+  p.ngroups = grid / p.cl;
   cudaLaunchConfig_t cfgl{};
   cfgl.gridDim = dim3(static_cast<unsigned>(grid));
   cfgl.blockDim = dim3(kThreads);
@@ -685,12 +739,22 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   attr[0].val.clusterDim.z = 1;
   cfgl.attrs = attr;
   cfgl.numAttrs = 1;
+  if (persistent()) {  // one resident cluster per slot, looping over the tile groups
+    int nclusters = 0;
+    auto kfn = L_mn ? ozaki_gemm_kernel<true, S, BK> : ozaki_gemm_kernel<false, S, BK>;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &cfgl) != cudaSuccess || nclusters <= 0) {
+      cudaGetLastError();
+      nclusters = 148 / p.cl;
+    }
+    if (nclusters < p.ngroups) cfgl.gridDim = dim3(static_cast<unsigned>(nclusters * p.cl));
+  }
   cudaError_t e = L_mn ? cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<true, S, BK>, tl, tr, p)
                        : cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<false, S, BK>, tl, tr, p);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
+
 
 // Stage depth: RFGPU_OZAKI_BK=32 (5 x 43 KB stages for 7 digits) or 64 (2 x 86 KB).
 int stage_bk() {
