@@ -57,7 +57,7 @@ constexpr int kThreads = 192;
 // digits (see ozaki_tn).
 constexpr int kSharedSpread = 2;
 constexpr int kDefaultBK = 64;  // stage depth (see Dig); RFGPU_OZAKI_BK overrides
-constexpr bool kDefaultPersist = true;  // persistent digit GEMM grid; RFGPU_OZAKI_PERSIST overrides   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr bool kDefaultPersist = false;  // persistent digit GEMM grid (measured no faster); RFGPU_OZAKI_PERSIST=1 enables   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
 
 // Per digit count S: S accumulator groups of OBN TMEM columns; as many
 // 2-digit-plane... stages as fit in shared memory.
@@ -285,125 +285,6 @@ __global__ void __launch_bounds__(256) slice_a_kernel(const T* __restrict__ A, i
       if (cs) *reinterpret_cast<uint32_t*>(cs + o) = wc[s];
     }
   }
-}
-
-// Fused stats + row-scaled digits for rows [r0, r1) of an FP64 A (r0 a
-// multiple of 256, lda even, n <= kFusedMaxN): one CTA per 256 rows, taken as
-// 32 sub-blocks of 8 rows. Per sub-block every thread reads 8 consecutive rows
-// of its columns (64 B per column) for the row / column maxima and ||A||_F^2,
-// the CTA reduces the 8 row exponents, and the threads read the same 8 rows
-// again — from L2: with one CTA per SM the 8 x n sub-blocks of all SMs stay
-// resident (the digit stores are streamed, evict-first) — to write the digit
-// planes, one 8-byte store per plane and column. A is read from HBM once
-// instead of twice (stats_kernel + slice_a_kernel).
-constexpr int kFusedThreads = 512;
-constexpr int64_t kFusedMaxN = 8192;
-constexpr size_t kFusedSmem = 120 * 1024;  // also keeps one CTA per SM (the L2 working set)
-
-template <int S>
-__global__ void __launch_bounds__(kFusedThreads, 1)
-    stats_slice_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda, int64_t r0, int64_t r1,
-                       int64_t s1, int64_t m_pad, int64_t n_pad, uint32_t* __restrict__ rowhi,
-                       int* __restrict__ rowexp, uint32_t* __restrict__ colpart, double* __restrict__ ssq_part,
-                       int8_t* __restrict__ rs) {
-  extern __shared__ uint32_t colmax[];  // [n]
-  __shared__ uint32_t s_rmax[8];
-  __shared__ int s_rexp[8];
-  __shared__ double red[kFusedThreads / 32];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int64_t rb0 = r0 + static_cast<int64_t>(blockIdx.x) * 256;
-  const int64_t blk = rb0 / 256;
-  const int64_t rend = lmin(rb0 + 256, s1);  // s1 >= r1: padding rows get zero digits
-  for (int64_t j = tid; j < n; j += kFusedThreads) colmax[j] = 0;
-  double ss0 = 0.0, ss1 = 0.0;
-  for (int64_t i0 = rb0; i0 < rend; i0 += 8) {
-    if (tid < 8) s_rmax[tid] = 0;
-    __syncthreads();
-    const bool full8 = i0 + 8 <= m;
-    uint32_t rm[8] = {};
-    for (int64_t j = tid; j < n; j += kFusedThreads) {
-      const double* col = A + j * lda + i0;
-      double v[8];
-      if (full8) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double2 t = reinterpret_cast<const double2*>(col)[u];
-          v[2 * u] = t.x, v[2 * u + 1] = t.y;
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = i0 + u < m ? col[u] : 0.0;
-      }
-      uint32_t cm = 0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t h = abs_hi(v[u]);
-        rm[u] = max(rm[u], h);
-        cm = max(cm, h);
-        if (u & 1) ss1 = fma(v[u], v[u], ss1);
-        else ss0 = fma(v[u], v[u], ss0);
-      }
-      colmax[j] = max(colmax[j], cm);  // column j belongs to this thread
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint32_t w = __reduce_max_sync(0xffffffffu, rm[u]);
-      if (lane == 0 && w) atomicMax(&s_rmax[u], w);
-    }
-    __syncthreads();
-    if (tid < 8) {
-      const int64_t i = i0 + tid;
-      const int e = hi_exp(s_rmax[tid]);
-      s_rexp[tid] = e;
-      if (i < r1) {
-        rowhi[i] = s_rmax[tid];
-        rowexp[i] = e;
-      }
-    }
-    __syncthreads();
-    int er[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) er[u] = s_rexp[u];
-    for (int64_t j = tid; j < n_pad; j += kFusedThreads) {
-      uint32_t lo[8], hi[8];
-      if (j < n) {
-        const double* col = A + j * lda + i0;
-        double v[8];
-        if (full8) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double2 t = __ldcs(reinterpret_cast<const double2*>(col) + u);  // last use
-            v[2 * u] = t.x, v[2 * u + 1] = t.y;
-          }
-        } else {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = i0 + u < m ? col[u] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint64_t x = balanced<S>(v[u], er[u]);
-          lo[u] = static_cast<uint32_t>(x) ^ 0x80808080u;
-          hi[u] = static_cast<uint32_t>(x >> 32) ^ 0x80808080u;
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) lo[u] = hi[u] = 0u;
-      }
-      uint32_t ta[8], tb[8];  // ta[k] / tb[k]: byte k of elements 0-3 / 4-7
-      transpose4(lo, ta);
-      transpose4(hi, ta + 4);
-      transpose4(lo + 4, tb);
-      transpose4(hi + 4, tb + 4);
-      int8_t* dst = rs + j * m_pad + i0;
-#pragma unroll
-      for (int s = 0; s < S; ++s)
-        __stcs(reinterpret_cast<uint2*>(dst + static_cast<int64_t>(s) * n_pad * m_pad), make_uint2(ta[S - 1 - s], tb[S - 1 - s]));
-    }
-    __syncthreads();
-  }
-  for (int64_t j = tid; j < n_pad; j += kFusedThreads) colpart[blk * n_pad + j] = j < n ? colmax[j] : 0u;
-  const double ssum = block_sum(ss0 + ss1, red);
-  if (tid == 0 && ssq_part) ssq_part[blockIdx.x] = ssum;
 }
 
 // Thin operand R (K x N, col-major ld), optionally pre-scaled by
@@ -983,8 +864,7 @@ void ozaki_bind(void* work, int64_t m, int64_t n, int digits, OzakiA* out) {
 
 template <class T>
 cudaError_t prepare_rows_t(const T* A, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a, double* ssq_part,
-                           int slice_rows, bool* sliced, cudaStream_t st) {
-  if (sliced) *sliced = false;
+                           bool slice_rows, cudaStream_t st) {
   if (r1 == a.m && a.m_pad > a.m) {  // padding rows: exponent 0, zero column maxima
     cudaError_t e = cudaMemsetAsync(a.rowexp + a.m, 0, sizeof(int) * (a.m_pad - a.m), st);
     if (e != cudaSuccess) return e;
@@ -992,28 +872,6 @@ cudaError_t prepare_rows_t(const T* A, int64_t lda, int64_t r0, int64_t r1, cons
   const int64_t rows = r1 - r0;
   const int64_t blocks = (rows + 255) / 256;
   const int64_t s1 = r1 == a.m ? a.m_pad : r1;
-  const char* fe = std::getenv("RFGPU_OZAKI_FUSED");
-  if (sizeof(T) == 8 && slice_rows != 0 && rows > 0 && a.n <= kFusedMaxN && a.digits == 7 && (lda & 1) == 0 &&
-      (reinterpret_cast<uintptr_t>(A) & 15) == 0 && !(fe && fe[0] == '0')) {
-    static bool cfg = false;
-    if (!cfg) {
-      cudaError_t e = cudaFuncSetAttribute(stats_slice_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(kFusedSmem));
-      if (e != cudaSuccess) return e;
-      cfg = true;
-    }
-    const int64_t chunks = stats_chunks(rows, a.n);  // the slot count callers allocated (one used per block)
-    if (ssq_part && chunks > 1) {
-      cudaError_t e = cudaMemsetAsync(ssq_part, 0, sizeof(double) * blocks * chunks, st);
-      if (e != cudaSuccess) return e;
-    }
-    stats_slice_kernel<7><<<static_cast<unsigned>((s1 - r0 + 255) / 256), kFusedThreads, kFusedSmem, st>>>(
-        reinterpret_cast<const double*>(A), a.m, a.n, lda, r0, r1, s1, a.m_pad, a.n_pad, a.rowhi, a.rowexp, a.colpart,
-        ssq_part, a.rs);
-    count_launch();
-    if (sliced) *sliced = true;
-    return cudaGetLastError();
-  }
   if (rows > 0) {
     const int64_t chunks = stats_chunks(rows, a.n);
     const int64_t chunk = ((a.n + chunks - 1) / chunks + 255) / 256 * 256;
@@ -1028,18 +886,17 @@ cudaError_t prepare_rows_t(const T* A, int64_t lda, int64_t r0, int64_t r1, cons
                                                                                                        a.rowexp);
     count_launch(2);
   }
-  if (slice_rows == 1) {
+  if (slice_rows) {
     slice_a<T>(a.digits, A, a.m, a.n, lda, r0, s1, a.rowexp, nullptr, a.rs, nullptr, a.m_pad, a.n_pad, st);
     count_launch();
-    if (sliced) *sliced = true;
   }
   return cudaGetLastError();
 }
 
 cudaError_t ozaki_prepare_rows(const void* A, bool f32, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
-                               double* ssq_part, int slice_rows, bool* sliced, cudaStream_t st) {
-  return f32 ? prepare_rows_t(static_cast<const float*>(A), lda, r0, r1, a, ssq_part, slice_rows, sliced, st)
-             : prepare_rows_t(static_cast<const double*>(A), lda, r0, r1, a, ssq_part, slice_rows, sliced, st);
+                               double* ssq_part, bool slice_rows, cudaStream_t st) {
+  return f32 ? prepare_rows_t(static_cast<const float*>(A), lda, r0, r1, a, ssq_part, slice_rows, st)
+             : prepare_rows_t(static_cast<const double*>(A), lda, r0, r1, a, ssq_part, slice_rows, st);
 }
 
 cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext) {

@@ -434,11 +434,9 @@ struct OzPasses {
   // row-scaled when `rows` (A X) or shared, column-scaled when not shared.
   Status prepare(rfgpu_ctx* c, const rfgpu_matrix* m, double* ssq, bool rows = true) {
     Timed t(c, "ozaki_slice");
-    bool have_rows = false;  // row-scaled digits written in the stats read (fused path)
-    RF_CUDA(ozaki_prepare_rows(m->dev, m->f32, m->lda, 0, m->m, a, ssq, 2, &have_rows, c->stream));
+    RF_CUDA(ozaki_prepare_rows(m->dev, m->f32, m->lda, 0, m->m, a, ssq, false, c->stream));
     RF_TRY(columns(c, m));
-    RF_CUDA(ozaki_slice_sets(m->dev, m->f32, m->lda, a, (rows || a.shared) && !have_rows, tn && !a.shared,
-                             c->stream));
+    RF_CUDA(ozaki_slice_sets(m->dev, m->f32, m->lda, a, rows || a.shared, tn && !a.shared, c->stream));
     return {};
   }
 };
@@ -462,7 +460,7 @@ Status pass1_rows(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
       RF_TRY(oz.prepare(c, a, ssq));
     } else {
       Timed t(c, "ozaki_slice");
-      RF_CUDA(ozaki_prepare_rows(A, false, a->lda, r0, r1, oz.a, ssq, 1, nullptr, c->stream));
+      RF_CUDA(ozaki_prepare_rows(A, false, a->lda, r0, r1, oz.a, ssq, true, c->stream));
     }
     Timed t(c, "pass_nn");
     RF_CUDA(ozaki_nn(oz.a, r0, r1, G, a->n, ell, Y, ldy, oz.work.p, c->stream));

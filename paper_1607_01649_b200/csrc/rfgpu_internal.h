@@ -61,12 +61,10 @@ size_t ozaki_a_bytes(int64_t m, int64_t n, int digits);    // rs + exponents + m
 void ozaki_bind(void* work, int64_t m, int64_t n, int digits, OzakiA* out);  // carve ozaki_a_bytes
 int64_t ozaki_ssq_slots(int64_t rows, int64_t n);  // ||A||_F^2 partials of a row block
 // Rows [r0, r1) (r0 a multiple of 256): row exponents, ||A||_F^2 partials
-// (ozaki_ssq_slots(r1 - r0, n) of them), column maxima of these rows, and the
-// row-scaled digits of these rows (all A X needs): slice_rows = 1 always,
-// 2 only when they come in the same read of A (fused stats + slicing), 0 never.
-// *sliced (optional) tells whether they were written.
+// (ozaki_ssq_slots(r1 - r0, n) of them), column maxima of these rows, and, with
+// slice_rows, the row-scaled digits of these rows (all A X needs).
 cudaError_t ozaki_prepare_rows(const void* A, bool f32, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
-                               double* ssq_part, int slice_rows, bool* sliced, cudaStream_t st);
+                               double* ssq_part, bool slice_rows, cudaStream_t st);
 // After every row block's stats: column exponents, and the choice between one
 // shared digit set and a second, column-scaled set for A^T Q (synchronises
 // the stream; h_ext: 2 pinned ints).
