@@ -368,6 +368,7 @@ struct OzParams {
   int ws_mode;        // 1: C is [split][N_real][M_real]
   int cl;             // cluster size along N tiles: the A tile is TMA-multicast to all of them
   int64_t ngroups;    // tile groups (all tiles / cl); the grid may be smaller (persistent)
+  int last_w;         // width of the last n-tile (multiple of 16, <= OBN): l's padding is not multiplied
 };
 
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
@@ -426,6 +427,7 @@ __device__ __forceinline__ uint64_t umma_desc_mn(const void* p) {
 struct TileCoord {
   int64_t lrow0, ncol0, kb0;
   int nk, split;
+  int w;  // tile width: OBN, or p.last_w for the last n-tile (l not a multiple of 64)
 };
 
 __device__ __forceinline__ TileCoord tile_coord(const OzParams& p, int64_t tile) {
@@ -437,6 +439,7 @@ __device__ __forceinline__ TileCoord tile_coord(const OzParams& p, int64_t tile)
   t.split = static_cast<int>(rest / p.mtn);
   t.lrow0 = p.row0 + static_cast<int64_t>(mt) * OBM;
   t.ncol0 = static_cast<int64_t>(nt) * OBN;
+  t.w = nt == p.ntn - 1 ? p.last_w : OBN;
   t.kb0 = t.split * p.kb_per_split;
   const int64_t kb1 = min(p.kb_total, t.kb0 + p.kb_per_split);
   t.nk = static_cast<int>(kb1 - t.kb0);
@@ -446,6 +449,7 @@ __device__ __forceinline__ TileCoord tile_coord(const OzParams& p, int64_t tile)
 template <bool L_MN, int S, int BK>
 __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmL,
                                                                   const __grid_constant__ CUtensorMap tmR,
+                                                                  const __grid_constant__ CUtensorMap tmR2,
                                                                   const OzParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -494,7 +498,8 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
         const int st = static_cast<int>(it % kStages);
         const uint32_t ph = (it / kStages) & 1;
         mbar_wait(&empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(ASZ + BSZ));
+        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(ASZ + kS * tc.w * BK));
+        const CUtensorMap* tr = tc.w == OBN ? &tmR : &tmR2;  // the narrow last tile: box of w rows
         const int kx = static_cast<int>((tc.kb0 + kb) * BK);
 #pragma unroll
         for (int s = 0; s < kS; ++s) {
@@ -508,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
             tma2d(sA + st * ASZ + s * OBM * BK, &tmL, &full[st], lc0, lc1);
           else if (s % cl == crank)
             tma2d_mc(sA + st * ASZ + s * OBM * BK, &tmL, &full[st], lc0, lc1, cmask);
-          tma2d(sB + st * BSZ + s * OBN * BK, &tmR, &full[st], kx, static_cast<int>(s * p.R_rows + tc.ncol0));
+          tma2d(sB + st * BSZ + s * tc.w * BK, tr, &full[st], kx, static_cast<int>(s * p.R_rows + tc.ncol0));
         }
       }
     }
@@ -542,13 +547,13 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
               // M-major: K advances by 32 K-rows = 4 swizzle atoms
               const uint64_t da = L_MN ? umma_desc_mn<BK>(sA + st * ASZ + s * OBM * BK + kk * 32 * OBM)
                                        : umma_desc<BK>(sA + st * ASZ + s * OBM * BK + kk * 32);
-              const uint64_t db = umma_desc<BK>(sB + st * BSZ + t0 * OBN * BK + kk * 32);
+              const uint64_t db = umma_desc<BK>(sB + st * BSZ + t0 * tc.w * BK + kk * 32);
               // groups s + t0 .. s + t0 + cnt - 1; every group is first written by s = 0
               const uint32_t accum = (kb == 0 && kk == 0 && s == 0) ? 0u : 1u;
               asm volatile(
                   "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (s + t0) * OBN),
-                  "l"(da), "l"(db), "r"(idesc_n(OBN * cnt)), "r"(accum));
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (s + t0) * tc.w),
+                  "l"(da), "l"(db), "r"(idesc_n(tc.w * cnt)), "r"(accum));
             }
           }
         }
@@ -577,12 +582,12 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
       const int64_t orow = p.c_row0 + (lrow - p.row0);
       const int rex = (p.rowexp && tc.nk > 0) ? p.rowexp[lrow] : 0;
       const bool row_ok = orow < p.M_real + p.c_row0 && lrow - p.row0 < p.M_real;
-      for (int c = 0; c < OBN; c += 16) {
+      for (int c = 0; c < tc.w; c += 16) {
         uint32_t r[kS][16];
         if (tc.nk > 0) {
 #pragma unroll
           for (int gg = 0; gg < kS; ++gg) {
-            const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + gg * OBN + c;
+            const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + gg * tc.w + c;
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                 : "=r"(r[gg][0]), "=r"(r[gg][1]), "=r"(r[gg][2]), "=r"(r[gg][3]), "=r"(r[gg][4]), "=r"(r[gg][5]),
@@ -592,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         }
-        if (c + 16 == OBN) {  // every TMEM column of this tile is in registers: release it
+        if (c + 16 == tc.w) {  // every TMEM column of this tile is in registers: release it
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(tfree);
@@ -704,13 +709,21 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   const bool okl = L_mn ? digit_tmap(&tl, L, kS * L_rows, L_M, OBM, BK, CU_TENSOR_MAP_SWIZZLE_128B)
                         : digit_tmap(&tl, L, kS * L_rows, K_pad, BK, OBM, kSwK);
   if (!okl || !digit_tmap(&tr, R, kS * R_rows, K_pad, BK, OBN, kSwK)) return cudaErrorInvalidValue;
+  // the last n-tile spans only roundup(N_real - 64 (ntn - 1), 16) columns
+  const int ntn = static_cast<int>(R_rows / OBN);
+  int last_w = static_cast<int>(roundup(std::max<int64_t>(1, N_real - static_cast<int64_t>(ntn - 1) * OBN), 16));
+  const char* nw = std::getenv("RFGPU_OZAKI_NARROW");  // experiments: 0 pads the last tile to 64 columns
+  if (last_w > OBN || (nw && nw[0] == '0')) last_w = OBN;
+  CUtensorMap tr2 = tr;
+  if (last_w < OBN && !digit_tmap(&tr2, R, kS * R_rows, K_pad, BK, last_w, kSwK)) return cudaErrorInvalidValue;
   OzParams p = base;
   p.L_rows = L_rows;
   p.R_rows = R_rows;
   p.kb_total = K_pad / BK;
   p.splits = splits;
   p.kb_per_split = (p.kb_total + splits - 1) / splits;
-  p.ntn = static_cast<int>(R_rows / OBN);
+  p.ntn = ntn;
+  p.last_w = last_w;
   p.mtn = static_cast<int>((rows + OBM - 1) / OBM);
   p.row0 = row0;
   p.M_real = rows;
@@ -748,8 +761,8 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
     }
     if (nclusters < p.ngroups) cfgl.gridDim = dim3(static_cast<unsigned>(nclusters * p.cl));
   }
-  cudaError_t e = L_mn ? cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<true, S, BK>, tl, tr, p)
-                       : cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<false, S, BK>, tl, tr, p);
+  cudaError_t e = L_mn ? cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<true, S, BK>, tl, tr, tr2, p)
+                       : cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<false, S, BK>, tl, tr, tr2, p);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
