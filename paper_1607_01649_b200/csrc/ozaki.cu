@@ -50,6 +50,13 @@ constexpr int OBN = 64;        // tile columns per accumulator group
 // of 86 KB for 7 digits) or 32 (32B swizzle, 5 stages of 43 KB: more bytes in
 // flight per SM at the same shared-memory footprint).
 constexpr int64_t kSplitK = 16384;  // int32 safety: S * K * 128^2 < 2^31
+// K per split of the A^T Q pass (<= kSplitK, a multiple of 256): RFGPU_OZAKI_TNK overrides.
+int64_t tn_split_k() {
+  const char* e = std::getenv("RFGPU_OZAKI_TNK");
+  int64_t k = e ? std::atoll(e) : kSplitK;
+  k = std::max<int64_t>(256, std::min<int64_t>(kSplitK, k));
+  return k / 256 * 256;
+}
 constexpr int kThreads = 192;
 // One digit set serves both passes when the non-zero columns' exponents span
 // at most this many bits (ozaki_col_exponents): A^T Q on the row-scaled
@@ -283,6 +290,99 @@ __global__ void __launch_bounds__(256) slice_a_kernel(const T* __restrict__ A, i
       const int64_t o = static_cast<int64_t>(s) * n_pad * m_pad + off;
       if (rs) *reinterpret_cast<uint32_t*>(rs + o) = wr[s];
       if (cs) *reinterpret_cast<uint32_t*>(cs + o) = wc[s];
+    }
+  }
+}
+
+// Digits of A for rows [0, m_pad) with the column-scaled set ROW-major:
+// cs planes [kS][m_pad][n_pad] (row i contiguous over j), so that A^T Q reads
+// them M-major with a 128B swizzle exactly like A X reads rs (K-major 64-byte
+// rows of A's columns were measured ~30% slower on the tensor cores). rs
+// (optional) is written column-major as in slice_a_kernel.
+// Tile: 128 rows x 64 columns per CTA (column tile fastest, so neighbouring
+// CTAs complete each other's 128-byte row segments in L2). Warp w reads
+// columns w, w + 8, ... with 4 consecutive rows per lane (1 KB per column per
+// warp), writes rs directly and stages the column-scaled words (4 rows of one
+// column per word) in shared memory; then each lane byte-transposes 4 words
+// (4 columns x 4 rows) and writes 4 rows x 4 bytes (16 lanes: 64 B of a row).
+constexpr int kSliceTRows = 128, kSliceTCols = 64;
+
+template <class T, int S>
+__global__ void __launch_bounds__(256) slice_at_kernel(const T* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                                                       const int* __restrict__ rowexp, const int* __restrict__ colexp,
+                                                       int8_t* __restrict__ rs, int8_t* __restrict__ cs,
+                                                       int64_t m_pad, int64_t n_pad) {
+  extern __shared__ uint32_t W[];  // [S][kSliceTCols][33]
+  const int64_t ntc = n_pad / kSliceTCols;
+  const int64_t jt = blockIdx.x % ntc, it = blockIdx.x / ntc;
+  const int64_t i0 = it * kSliceTRows, j0 = jt * kSliceTCols;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ib = i0 + 4 * lane;
+  int er[4] = {0, 0, 0, 0};
+  if (rs)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) er[b] = ib + b < m ? rowexp[ib + b] : 0;
+  for (int cc = warp; cc < kSliceTCols; cc += 8) {
+    const int64_t j = j0 + cc;
+    uint32_t wr[S], wc[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) wr[q] = wc[q] = 0u;
+    if (j < n) {
+      const int fj = colexp[j];
+      double v[4];
+      if (ib + 3 < m && sizeof(T) == 8 && ((j * lda + ib) & 1) == 0) {
+        const double2 p0 = *reinterpret_cast<const double2*>(A + j * lda + ib);
+        const double2 p1 = *reinterpret_cast<const double2*>(A + j * lda + ib + 2);
+        v[0] = p0.x, v[1] = p0.y, v[2] = p1.x, v[3] = p1.y;
+      } else {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) v[b] = ib + b < m ? static_cast<double>(A[j * lda + ib + b]) : 0.0;
+      }
+      uint32_t lc[4], hc[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint64_t x = balanced<S>(v[b], fj);
+        lc[b] = static_cast<uint32_t>(x) ^ 0x80808080u;
+        hc[b] = static_cast<uint32_t>(x >> 32) ^ 0x80808080u;
+      }
+      uint32_t t[8];
+      transpose4(lc, t);
+      transpose4(hc, t + 4);
+#pragma unroll
+      for (int q = 0; q < S; ++q) wc[q] = t[S - 1 - q];
+      if (rs) {
+        uint32_t lr[4], hr[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint64_t x = balanced<S>(v[b], er[b]);
+          lr[b] = static_cast<uint32_t>(x) ^ 0x80808080u;
+          hr[b] = static_cast<uint32_t>(x >> 32) ^ 0x80808080u;
+        }
+        transpose4(lr, t);
+        transpose4(hr, t + 4);
+#pragma unroll
+        for (int q = 0; q < S; ++q) wr[q] = t[S - 1 - q];
+      }
+    }
+    if (rs)
+#pragma unroll
+      for (int q = 0; q < S; ++q)
+        *reinterpret_cast<uint32_t*>(rs + static_cast<int64_t>(q) * n_pad * m_pad + j * m_pad + ib) = wr[q];
+#pragma unroll
+    for (int q = 0; q < S; ++q) W[(q * kSliceTCols + cc) * 33 + lane] = wc[q];
+  }
+  __syncthreads();
+  const int cq = threadIdx.x & 15;  // column quad: columns 4 cq .. 4 cq + 3 of the tile
+  for (int rg = threadIdx.x >> 4; rg < kSliceTRows / 4; rg += 16) {
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      uint32_t in[4], out[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) in[c] = W[(q * kSliceTCols + 4 * cq + c) * 33 + rg];
+      transpose4(in, out);  // out[u]: row 4 rg + u, columns 4 cq .. 4 cq + 3
+      int8_t* dst = cs + static_cast<int64_t>(q) * m_pad * n_pad + (i0 + 4 * rg) * n_pad + j0 + 4 * cq;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) *reinterpret_cast<uint32_t*>(dst + u * n_pad) = out[u];
     }
   }
 }
@@ -846,6 +946,11 @@ size_t ozaki_set_bytes(int64_t m, int64_t n, int digits) {
   return static_cast<size_t>(digits) * a.m_pad * a.n_pad;
 }
 
+bool ozaki_cs_rowmajor() {
+  const char* e = std::getenv("RFGPU_OZAKI_TNMN");  // experiments: 0 keeps the column-major cs (K-major A^T Q)
+  return !(e && e[0] == '0');
+}
+
 size_t ozaki_a_bytes(int64_t m, int64_t n, int digits) {
   const OzakiA a = ozaki_layout(m, n, digits);
   return ozaki_set_bytes(m, n, digits) + sizeof(int) * (2 * a.m_pad + a.n_pad + 8) +
@@ -931,20 +1036,39 @@ cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext) {
 }
 
 template <class T>
-void slice_sets_t(const T* A, int64_t lda, const OzakiA& a, bool rows, bool cols, cudaStream_t st) {
+cudaError_t slice_sets_t(const T* A, int64_t lda, const OzakiA& a, bool rows, bool cols, cudaStream_t st) {
+  if (cols && a.cs_rowmajor) {
+    const size_t smem = sizeof(uint32_t) * a.digits * kSliceTCols * 33;
+    static bool cfg = false;
+    if (!cfg) {
+      for (auto fn : {slice_at_kernel<T, 7>, slice_at_kernel<T, 4>}) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(sizeof(uint32_t) * 7 * kSliceTCols * 33));
+        if (e != cudaSuccess) return e;
+      }
+      cfg = true;
+    }
+    const unsigned grid = static_cast<unsigned>((a.m_pad / kSliceTRows) * (a.n_pad / kSliceTCols));
+    if (a.digits == 4)
+      slice_at_kernel<T, 4><<<grid, 256, smem, st>>>(A, a.m, a.n, lda, a.rowexp, a.colexp, rows ? a.rs : nullptr, a.cs,
+                                                     a.m_pad, a.n_pad);
+    else
+      slice_at_kernel<T, 7><<<grid, 256, smem, st>>>(A, a.m, a.n, lda, a.rowexp, a.colexp, rows ? a.rs : nullptr, a.cs,
+                                                     a.m_pad, a.n_pad);
+    count_launch();
+    return cudaGetLastError();
+  }
   slice_a<T>(a.digits, A, a.m, a.n, lda, 0, a.m_pad, a.rowexp, a.colexp, rows ? a.rs : nullptr,
              cols ? a.cs : nullptr, a.m_pad, a.n_pad, st);
   count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t ozaki_slice_sets(const void* A, bool f32, int64_t lda, const OzakiA& a, bool rows, bool cols,
                              cudaStream_t st) {
   if (!rows && !cols) return cudaSuccess;
-  if (f32)
-    slice_sets_t(static_cast<const float*>(A), lda, a, rows, cols, st);
-  else
-    slice_sets_t(static_cast<const double*>(A), lda, a, rows, cols, st);
-  return cudaGetLastError();
+  return f32 ? slice_sets_t(static_cast<const float*>(A), lda, a, rows, cols, st)
+             : slice_sets_t(static_cast<const double*>(A), lda, a, rows, cols, st);
 }
 
 size_t ozaki_nn_work_bytes(const OzakiA& a, int64_t rows, int64_t ell) {
@@ -982,7 +1106,7 @@ cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, i
 
 size_t ozaki_tn_work_bytes(const OzakiA& a, int64_t ell) {
   const int64_t lp = roundup(ell, OBN);
-  const int splits = static_cast<int>((a.m_pad + kSplitK - 1) / kSplitK);
+  const int splits = static_cast<int>((a.m_pad + tn_split_k() - 1) / tn_split_k());
   return static_cast<size_t>(a.digits) * lp * a.m_pad + sizeof(int) * lp + 256 +
          sizeof(double) * static_cast<size_t>(splits) * a.n * ell;
 }
@@ -1005,7 +1129,7 @@ cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell,
   cudaError_t e = a.shared ? slice_thin(a.digits, Q, a.m, ell, ldq, a.rowexp, a.emax, colexp, qd, a.m_pad, lp, st)
                            : slice_thin(a.digits, Q, a.m, ell, ldq, nullptr, 0, colexp, qd, a.m_pad, lp, st);
   if (e != cudaSuccess) return e;
-  const int splits = static_cast<int>((a.m_pad + kSplitK - 1) / kSplitK);
+  const int splits = static_cast<int>((a.m_pad + tn_split_k() - 1) / tn_split_k());
   OzParams p{};
   p.C = splits > 1 ? ws : Z;
   p.ldc = ldz;
@@ -1014,7 +1138,13 @@ cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell,
   p.colexp = colexp;
   p.cshift = a.shared ? a.emax : 0;
   p.ws_mode = splits > 1 ? 1 : 0;
-  e = launch_digit_gemm(a.digits, a.shared ? a.rs : a.cs, a.n_pad, false, 0, qd, lp, a.m_pad, 0, a.n, ell, splits, p, true, st);
+  // row-major cs: M-major L tiles (planes [kS][m_pad][n_pad]), like A X. Measured at config 3:
+  // 21.9 ms per pass without multicast, 25.9 with the 4-CTA A multicast, 26.6 for the K-major
+  // column-major set (which needs the multicast: 37 ms without).
+  if (!a.shared && a.cs_rowmajor)
+    e = launch_digit_gemm(a.digits, a.cs, a.m_pad, true, a.n_pad, qd, lp, a.m_pad, 0, a.n, ell, splits, p, false, st);
+  else
+    e = launch_digit_gemm(a.digits, a.shared ? a.rs : a.cs, a.n_pad, false, 0, qd, lp, a.m_pad, 0, a.n, ell, splits, p, true, st);
   if (e != cudaSuccess || splits == 1) return e;
   const int64_t total = a.n * ell;
   reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(

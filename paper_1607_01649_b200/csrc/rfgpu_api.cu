@@ -410,6 +410,7 @@ struct OzPasses {
       return {};
     }
     ozaki_bind(planes.p, m->m, m->n, digits, &a);
+    a.cs_rowmajor = ozaki_cs_rowmajor();
     return {};
   }
   // After every row's stats: column exponents; one shared digit set when the

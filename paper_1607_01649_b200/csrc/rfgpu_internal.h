@@ -43,7 +43,8 @@ cudaError_t sum_array(const double* x, int64_t n, double* out, cudaStream_t st);
 struct OzakiA {
   int8_t* rs;   // [digits][n_pad][m_pad] digits of A(i,j) 2^-rowexp[i] (column-major; A X reads them
                 // M-major; A^T Q reads them K-major when `shared`)
-  int8_t* cs;   // [digits][n_pad][m_pad] digits of A(i,j) 2^-colexp[j] (A^T Q when !shared; caller-bound)
+  int8_t* cs;   // digits of A(i,j) 2^-colexp[j] (A^T Q when !shared; caller-bound): [digits][m_pad][n_pad]
+                // (row-major, read M-major) when cs_rowmajor, else [digits][n_pad][m_pad] (read K-major)
   int* rowexp;  // m_pad: |A(i,:)| < 2^rowexp[i]
   int* colexp;  // n_pad: |A(:,j)| < 2^colexp[j]
   int* ext;     // 2 (+pad): max column exponent, -min column exponent (non-zero columns)
@@ -53,7 +54,9 @@ struct OzakiA {
   int digits;   // 7 (FP64 A) or 4 (FP32 A)
   bool shared;  // one digit set (rs) serves both passes (ozaki_col_exponents decides)
   int emax;     // max column exponent (shared mode's thin-operand shift)
+  bool cs_rowmajor;
 };
+bool ozaki_cs_rowmajor();  // layout of the column-scaled set (RFGPU_OZAKI_TNMN=0: column-major)
 bool ozaki_enabled(int64_t m, int64_t n);  // RFGPU_OZAKI=0/1 overrides the size rule
 OzakiA ozaki_layout(int64_t m, int64_t n, int digits);  // shapes only (no buffers)
 size_t ozaki_set_bytes(int64_t m, int64_t n, int digits);  // one digit set (rs or cs)
