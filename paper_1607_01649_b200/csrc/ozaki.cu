@@ -58,10 +58,12 @@ int64_t tn_split_k() {
   return k / 256 * 256;
 }
 constexpr int kThreads = 192;
-// One digit set serves both passes when the non-zero columns' exponents span
-// at most this many bits (ozaki_col_exponents): A^T Q on the row-scaled
+// One digit set may serve both passes when the non-zero columns' exponents
+// span at most this many bits (ozaki_col_exponents): A^T Q on the row-scaled
 // digits then loses at most kSharedSpread + 2 bits against column-scaled
-// digits (see ozaki_tn).
+// digits (see ozaki_tn). Used only when the second set does not fit in HBM:
+// the row-major column-scaled set makes A^T Q ~20% faster than the shared
+// set read K-major.
 constexpr int kSharedSpread = 2;
 constexpr int kDefaultBK = 64;  // stage depth (see Dig); RFGPU_OZAKI_BK overrides
 constexpr bool kDefaultPersist = false;  // persistent digit GEMM grid (measured no faster); RFGPU_OZAKI_PERSIST=1 enables   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
@@ -1029,9 +1031,9 @@ cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext) {
   const bool any = h_ext[0] > -100000;  // some non-zero column
   a->emax = any ? h_ext[0] : 0;
   const int spread = any ? h_ext[0] + h_ext[1] : 0;
+  a->shared_ok = spread <= kSharedSpread;
   const char* v = std::getenv("RFGPU_OZAKI_SHARED");  // experiments / tests: 0 never, 1 always
-  const int force = v ? (v[0] == '1' ? 1 : 0) : -1;
-  a->shared = force >= 0 ? force == 1 : spread <= kSharedSpread;
+  a->shared = v && v[0] == '1';
   return cudaGetLastError();
 }
 

@@ -413,14 +413,17 @@ struct OzPasses {
     a.cs_rowmajor = ozaki_cs_rowmajor();
     return {};
   }
-  // After every row's stats: column exponents; one shared digit set when the
-  // column scales allow it (ozaki.cu kSharedSpread), else a second,
-  // column-scaled set for A^T Q (on DMMA if that set does not fit).
+  // After every row's stats: column exponents and a second, column-scaled
+  // (row-major) digit set for A^T Q; if it does not fit, the row-scaled set
+  // serves A^T Q when the column scales allow it (ozaki.cu kSharedSpread),
+  // else A^T Q stays on DMMA.
   Status columns(rfgpu_ctx* c, const rfgpu_matrix* m) {
     RF_CUDA(ozaki_col_exponents(&a, c->stream, c->h_info));
     if (!a.shared) {
       if (cplanes.alloc(ozaki_set_bytes(m->m, m->n, a.digits), c->stream).ok()) {
         a.cs = cplanes.as<int8_t>();
+      } else if (a.shared_ok) {  // no room for the second set: the row-scaled set serves A^T Q
+        a.shared = true;
       } else {
         tn = false;
         if (std::getenv("RFGPU_DEBUG")) std::fprintf(stderr, "[rfgpu] column-scaled digits do not fit: DMMA A^T Q\n");

@@ -52,7 +52,8 @@ struct OzakiA {
   uint32_t* colpart;  // (m_pad / 256) x n_pad per-block column maxima (high words)
   int64_t m, n, m_pad, n_pad;
   int digits;   // 7 (FP64 A) or 4 (FP32 A)
-  bool shared;  // one digit set (rs) serves both passes (ozaki_col_exponents decides)
+  bool shared;     // one digit set (rs) serves both passes
+  bool shared_ok;  // the column scales allow it (ozaki_col_exponents)
   int emax;     // max column exponent (shared mode's thin-operand shift)
   bool cs_rowmajor;
 };
@@ -68,9 +69,9 @@ int64_t ozaki_ssq_slots(int64_t rows, int64_t n);  // ||A||_F^2 partials of a ro
 // slice_rows, the row-scaled digits of these rows (all A X needs).
 cudaError_t ozaki_prepare_rows(const void* A, bool f32, int64_t lda, int64_t r0, int64_t r1, const OzakiA& a,
                                double* ssq_part, bool slice_rows, cudaStream_t st);
-// After every row block's stats: column exponents, and the choice between one
-// shared digit set and a second, column-scaled set for A^T Q (synchronises
-// the stream; h_ext: 2 pinned ints).
+// After every row block's stats: column exponents and whether one shared
+// digit set could serve A^T Q too (shared_ok; shared is set only when forced
+// by RFGPU_OZAKI_SHARED=1). Synchronises the stream; h_ext: 2 pinned ints.
 cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext);
 // One read of A writing the row-scaled (rows) and / or column-scaled (cols) digits.
 cudaError_t ozaki_slice_sets(const void* A, bool f32, int64_t lda, const OzakiA& a, bool rows, bool cols,

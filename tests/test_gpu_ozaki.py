@@ -69,8 +69,9 @@ def test_digit_gemm_matches_extended_precision(ctx, ozaki, m, n, cols, trans):
 def test_digit_gemm_one_or_two_digit_sets(ctx, ozaki, monkeypatch, shared, m, n, cols, trans):
     """Columns of comparable scale (exponents within 2 bits): A^T Q may run on
     the row-scaled digits with the row factors moved onto Q (one digit set for
-    both passes). Forced either way (RFGPU_OZAKI_SHARED) and by the size rule,
-    the products stay within the column-scaled bar."""
+    both passes; the library does so when the second set does not fit in HBM).
+    Forced on (RFGPU_OZAKI_SHARED=1), off, and by default (row-major second
+    set), the products stay within the column-scaled bar."""
     if shared is None:
         monkeypatch.delenv("RFGPU_OZAKI_SHARED", raising=False)
     else:
@@ -91,8 +92,9 @@ def test_digit_gemm_one_or_two_digit_sets(ctx, ozaki, monkeypatch, shared, m, n,
 
 
 def test_graded_columns_keep_two_digit_sets(ctx, ozaki, monkeypatch):
-    """A column 2^-30 below the others: the size rule must keep the
-    column-scaled set for A^T Q (the shared set would lose ~30 bits there)."""
+    """A column 2^-30 below the others: A^T Q must use the column-scaled set
+    (the shared set would lose ~30 bits there; it is only a fallback for
+    column exponents within 2 bits)."""
     monkeypatch.delenv("RFGPU_OZAKI_SHARED", raising=False)
     rng = np.random.default_rng(9)
     a = rng.standard_normal((3000, 300))
