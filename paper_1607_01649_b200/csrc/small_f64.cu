@@ -41,7 +41,6 @@ constexpr int kSmallThreads = 1024;
 // The pivot test is the reference rule (pivot <= 1e-14 max initial diagonal,
 // proj/src/dense.cpp:763-786) plus the CholeskyQR gate statistic
 // min_j pivot_j / trace(G). rdiag receives 1 / R(j,j) for trinv_smem_kernel.
-__device__ __forceinline__ int64_t pk(int i, int j) { return static_cast<int64_t>(j) * (j + 1) / 2 + i; }
 
 __global__ void __launch_bounds__(kSmallThreads, 1)
     chol_kernel(const double* __restrict__ G, int c, double* __restrict__ R, double* __restrict__ rdiag, int* info,
