@@ -161,28 +161,33 @@ __global__ void rowexp_kernel(const uint32_t* __restrict__ rowhi, int64_t r0, in
     rowexp[i] = hi_exp(rowhi[i]);
 }
 
-// Column exponents from the per-CTA column maxima; ext[0] = max and ext[1] =
+// Column exponents from the per-block column maxima; ext[0] = max and ext[1] =
 // -min exponent over the non-zero columns (both pre-set very negative).
-__global__ void colexp_kernel(const uint32_t* __restrict__ colpart, int64_t nblk, int64_t n, int64_t n_pad,
-                              int* __restrict__ colexp, int* __restrict__ ext) {
-  int emax = INT_MIN, nmin = INT_MIN;
-  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n_pad;
-       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    uint32_t mx = 0;
-    if (j < n)
-      for (int64_t b = 0; b < nblk; ++b) mx = max(mx, colpart[b * n_pad + j]);
-    const int e = hi_exp(mx);
-    colexp[j] = e;
+// Block (32, 32): 32 columns, the row blocks strided over threadIdx.y (each
+// warp reads 128 contiguous bytes per row block), then a shared-memory max.
+__global__ void __launch_bounds__(1024) colexp_kernel(const uint32_t* __restrict__ colpart, int64_t nblk, int64_t n,
+                                                      int64_t n_pad, int* __restrict__ colexp, int* __restrict__ ext) {
+  __shared__ uint32_t red[32][33];
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
+  uint32_t mx = 0;
+  if (j < n)
+    for (int64_t b = threadIdx.y; b < nblk; b += 32) mx = max(mx, colpart[b * n_pad + j]);
+  red[threadIdx.y][threadIdx.x] = mx;
+  __syncthreads();
+  if (threadIdx.y == 0) {
+    for (int y = 1; y < 32; ++y) mx = max(mx, red[y][threadIdx.x]);
+    if (j < n_pad) colexp[j] = hi_exp(mx);
+    int emax = INT_MIN, nmin = INT_MIN;
     if (mx != 0) {
-      emax = max(emax, e);
-      nmin = max(nmin, -e);
+      emax = hi_exp(mx);
+      nmin = -emax;
     }
-  }
-  emax = __reduce_max_sync(0xffffffffu, emax);
-  nmin = __reduce_max_sync(0xffffffffu, nmin);
-  if ((threadIdx.x & 31) == 0 && emax != INT_MIN) {
-    atomicMax(&ext[0], emax);
-    atomicMax(&ext[1], nmin);
+    emax = __reduce_max_sync(0xffffffffu, emax);
+    nmin = __reduce_max_sync(0xffffffffu, nmin);
+    if (threadIdx.x == 0 && emax != INT_MIN) {
+      atomicMax(&ext[0], emax);
+      atomicMax(&ext[1], nmin);
+    }
   }
 }
 
@@ -1023,8 +1028,8 @@ cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext) {
   cudaError_t e = cudaMemsetAsync(a->ext, 0x80, 2 * sizeof(int), st);  // very negative
   if (e != cudaSuccess) return e;
   const int64_t nblk = (a->m + 255) / 256;
-  colexp_kernel<<<static_cast<unsigned>((a->n_pad + 255) / 256), 256, 0, st>>>(a->colpart, nblk, a->n, a->n_pad,
-                                                                                a->colexp, a->ext);
+  colexp_kernel<<<static_cast<unsigned>((a->n_pad + 31) / 32), dim3(32, 32), 0, st>>>(a->colpart, nblk, a->n,
+                                                                                      a->n_pad, a->colexp, a->ext);
   count_launch();
   if ((e = cudaMemcpyAsync(h_ext, a->ext, 2 * sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
