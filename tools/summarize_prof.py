@@ -22,7 +22,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OURS = ("gemm_f64", "jacobi_svd", "chol_inv", "trinv_upper", "cpqr", "reduce_splits", "symmetrize", "sumsq",
         "sum_array", "transpose", "gather_", "lsq_scale", "gs_", "add_inplace", "sylvester", "f32_to_f64",
         "scale_", "copy_", "fill_", "ozaki_gemm", "stats_kernel", "slice_a_kernel", "slice_r_kernel", "colexp_kernel",
-        "col_exp_kernel", "rowexp_kernel", "reduce_ws_kernel", "rfgpu")
+        "col_exp_kernel", "rowexp_kernel", "reduce_ws_kernel", "chol_kernel", "trinv_smem", "slice_at_kernel",
+        "colexp_fix", "cholb_", "rfgpu")
 
 
 def ours(name):
@@ -68,7 +69,10 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__registers_per_thread",
            "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
-           "sm__cycles_elapsed.avg.per_second"]
+           "sm__cycles_elapsed.avg.per_second", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+           "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_elapsed",
+           "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+           "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
 
 
 def ncu_full(rnd, wl):
