@@ -79,5 +79,15 @@ int main() {
   const double ops = 2.0 * 128 * 256 * 32 * 4.0 * iters * sms;
   printf("int8 tcgen05 dense peak: %.1f TOPS (%d SMs, %.3f ms, err=%s)\n", ops / best / 1e9, sms, best,
          cudaGetErrorString(cudaGetLastError()));
+  // sustained: back to back for ~4 s (the power cap settles), like MEASURED_PEAKS.json's bf16_tflops_sustained
+  const int reps = static_cast<int>(4000.0f / best) + 1;
+  cudaEventRecord(a);
+  for (int r = 0; r < reps; ++r) peak<<<sms, 128, smem>>>(iters, sink);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float total;
+  cudaEventElapsedTime(&total, a, b);
+  printf("int8 tcgen05 dense sustained: %.1f TOPS (%d launches back to back, %.1f ms, err=%s)\n",
+         ops * reps / total / 1e9, reps, total, cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
