@@ -329,22 +329,30 @@ __global__ void __launch_bounds__(256) slice_at_kernel(const T* __restrict__ A, 
   if (rs)
 #pragma unroll
     for (int b = 0; b < 4; ++b) er[b] = ib + b < m ? rowexp[ib + b] : 0;
+  // 4 rows of column j0 + cc (zeros outside A); the next column's loads are
+  // issued before the current one is processed (two columns in flight per warp)
+  auto load4 = [&](int cc, double* v) {
+    const int64_t j = j0 + cc;
+    if (j < n && ib + 3 < m && sizeof(T) == 8 && ((j * lda + ib) & 1) == 0) {
+      const double2 p0 = *reinterpret_cast<const double2*>(A + j * lda + ib);
+      const double2 p1 = *reinterpret_cast<const double2*>(A + j * lda + ib + 2);
+      v[0] = p0.x, v[1] = p0.y, v[2] = p1.x, v[3] = p1.y;
+    } else {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) v[b] = (j < n && ib + b < m) ? static_cast<double>(A[j * lda + ib + b]) : 0.0;
+    }
+  };
+  double vn[4];
+  load4(warp, vn);
   for (int cc = warp; cc < kSliceTCols; cc += 8) {
     const int64_t j = j0 + cc;
+    double v[4] = {vn[0], vn[1], vn[2], vn[3]};
+    if (cc + 8 < kSliceTCols) load4(cc + 8, vn);
     uint32_t wr[S], wc[S];
 #pragma unroll
     for (int q = 0; q < S; ++q) wr[q] = wc[q] = 0u;
     if (j < n) {
       const int fj = colexp[j];
-      double v[4];
-      if (ib + 3 < m && sizeof(T) == 8 && ((j * lda + ib) & 1) == 0) {
-        const double2 p0 = *reinterpret_cast<const double2*>(A + j * lda + ib);
-        const double2 p1 = *reinterpret_cast<const double2*>(A + j * lda + ib + 2);
-        v[0] = p0.x, v[1] = p0.y, v[2] = p1.x, v[3] = p1.y;
-      } else {
-#pragma unroll
-        for (int b = 0; b < 4; ++b) v[b] = ib + b < m ? static_cast<double>(A[j * lda + ib + b]) : 0.0;
-      }
       uint32_t lc[4], hc[4];
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
@@ -1119,7 +1127,7 @@ size_t ozaki_tn_work_bytes(const OzakiA& a, int64_t ell) {
 }
 
 cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell, double* Z, int64_t ldz, void* work,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool presliced) {
   const int64_t lp = roundup(ell, OBN);
   int8_t* qd = static_cast<int8_t*>(work);
   int* colexp = reinterpret_cast<int*>(qd + static_cast<size_t>(a.digits) * lp * a.m_pad);
@@ -1133,8 +1141,12 @@ cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell,
   //    error per term is <= 2^-54 2^(emax) max|Q(:, c)| (x2), i.e. at most
   //    2^(emax - f_j + 2) times the column-scaled bound: ozaki_col_exponents
   //    only picks it when every non-zero column has f_j >= emax - kSharedSpread.
-  cudaError_t e = a.shared ? slice_thin(a.digits, Q, a.m, ell, ldq, a.rowexp, a.emax, colexp, qd, a.m_pad, lp, st)
-                           : slice_thin(a.digits, Q, a.m, ell, ldq, nullptr, 0, colexp, qd, a.m_pad, lp, st);
+  // presliced: ozaki_slice_thin already left Q's column-scaled digits in work (orth's digit Gram)
+  cudaError_t e = cudaSuccess;
+  if (a.shared)
+    e = slice_thin(a.digits, Q, a.m, ell, ldq, a.rowexp, a.emax, colexp, qd, a.m_pad, lp, st);
+  else if (!presliced)
+    e = slice_thin(a.digits, Q, a.m, ell, ldq, nullptr, 0, colexp, qd, a.m_pad, lp, st);
   if (e != cudaSuccess) return e;
   const int splits = static_cast<int>((a.m_pad + tn_split_k() - 1) / tn_split_k());
   OzParams p{};
@@ -1156,6 +1168,43 @@ cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell,
   const int64_t total = a.n * ell;
   reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(
       ws, a.n, ell, splits, Z, ldz);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---- Gram matrices of tall thin matrices on the digit path -------------------------
+// Column-scaled digits of R (K x ell, K = a.m rows) into `work` in ozaki_tn's
+// layout (digits [7][lp][m_pad], then the column exponents), so that a
+// following ozaki_tn(..., presliced = true) of the same R reuses them.
+cudaError_t ozaki_slice_thin(const OzakiA& a, const double* R, int64_t ldr, int64_t ell, void* work, cudaStream_t st) {
+  const int64_t lp = roundup(ell, OBN);
+  int8_t* qd = static_cast<int8_t*>(work);
+  int* colexp = reinterpret_cast<int*>(qd + static_cast<size_t>(a.digits) * lp * a.m_pad);
+  return slice_thin(a.digits, R, a.m, ell, ldr, nullptr, 0, colexp, qd, a.m_pad, lp, st);
+}
+
+// G (ell x ell, ld ldg) = R^T R from the digits ozaki_slice_thin left in work:
+// both operands K-major ([7][lp][m_pad]), split K in fixed order through the
+// ozaki_tn workspace. G(i, j) = 2^(g_i + g_j) sum_g 2^-(12+8g) acc_g; the full
+// square is computed (the Cholesky reads the upper triangle).
+cudaError_t ozaki_gram_thin(const OzakiA& a, int64_t ell, void* work, double* G, int64_t ldg, cudaStream_t st) {
+  const int64_t lp = roundup(ell, OBN);
+  int8_t* qd = static_cast<int8_t*>(work);
+  int* colexp = reinterpret_cast<int*>(qd + static_cast<size_t>(a.digits) * lp * a.m_pad);
+  double* ws = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(colexp) + ((sizeof(int) * lp + 255) / 256) * 256);
+  const int splits = static_cast<int>((a.m_pad + kSplitK - 1) / kSplitK);
+  OzParams p{};
+  p.C = splits > 1 ? ws : G;
+  p.ldc = ldg;
+  p.c_row0 = 0;
+  p.rowexp = colexp;
+  p.colexp = colexp;
+  p.ws_mode = splits > 1 ? 1 : 0;
+  cudaError_t e = launch_digit_gemm(a.digits, qd, lp, false, 0, qd, lp, a.m_pad, 0, ell, ell, splits, p, true, st);
+  if (e != cudaSuccess || splits == 1) return e;
+  const int64_t total = ell * ell;
+  reduce_ws_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(
+      ws, ell, ell, splits, G, ldg);
   count_launch();
   return cudaGetLastError();
 }

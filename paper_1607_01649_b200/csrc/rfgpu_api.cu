@@ -394,6 +394,10 @@ std::vector<std::pair<int64_t, int64_t>> upload_panels(int64_t m) {
 struct OzPasses {
   bool on = false;
   bool tn = true;  // A^T Q on the digits (false: the column-scaled set did not fit; DMMA)
+  // the thin matrix whose column-scaled digits are in `work` (orth's digit Gram
+  // of Q1), reused by the A^T Q1 pass that follows
+  const double* thin_src = nullptr;
+  int64_t thin_cols = 0;
   OzakiA a{};
   DBuf planes, cplanes, work;
   Status init(rfgpu_ctx* c, const rfgpu_matrix* m, int64_t ell) {
@@ -478,6 +482,7 @@ Status pass_nn(rfgpu_ctx* c, const rfgpu_matrix* a, const double* X, int64_t col
                OzPasses* oz) {
   if (oz && oz->on) {
     Timed t(c, "pass_nn");
+    oz->thin_src = nullptr;  // the thin digits of X overwrite the work buffer
     RF_CUDA(ozaki_nn(oz->a, 0, a->m, X, a->n, cols, Y, ldy, oz->work.p, c->stream));
     return {};
   }
@@ -490,7 +495,9 @@ Status pass_tn_raw(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Y, int64_t
                    OzPasses* oz) {
   if (oz && oz->on && oz->tn) {
     Timed t(c, "pass_tn");
-    RF_CUDA(ozaki_tn(oz->a, Y, ldy, cols, Z, a->n, oz->work.p, c->stream));
+    const bool pre = oz->thin_src == Y && oz->thin_cols == cols && !oz->a.shared;
+    oz->thin_src = nullptr;
+    RF_CUDA(ozaki_tn(oz->a, Y, ldy, cols, Z, a->n, oz->work.p, c->stream, pre));
     return {};
   }
   return gemm(c, true, a->n, cols, a->m, static_cast<const double*>(a->dev), a->lda, Y, ldy, Z, a->n, nullptr,
@@ -574,8 +581,14 @@ struct Basis {
 
 constexpr double kCholGate = 1e-10;  // min pivot / trace(G)
 
+// RFGPU_DIGIT_GRAM=0 keeps the tall orth Grams on DMMA.
+bool digit_grams() {
+  const char* e = std::getenv("RFGPU_DIGIT_GRAM");
+  return !(e && e[0] == '0');
+}
+
 Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx, Basis* out, double* R2inv_buf,
-            double* R, bool dist, bool fold) {
+            double* R, bool dist, bool fold, OzPasses* oz = nullptr) {
   Timed t(c, "orth");
   out->r = 0;
   out->folded = false;
@@ -604,14 +617,27 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
     Q1 = q1buf.d();
   }
 
-  RF_TRY(gemm(c, true, cols, cols, m, X, ldx, X, ldx, G1, cols, nullptr, "gram", /*sym=*/true));
+  // Tall orth over A's rows with the passes on the digit path: both Grams on
+  // the INT8 tensor cores too (column-scaled digits of X, then of Q1; Q1's
+  // digits stay in the work buffer for the A^T Q1 pass that follows).
+  const bool dig = oz && oz->on && oz->tn && !oz->a.shared && m == oz->a.m && fold && digit_grams();
+  auto gram = [&](const double* M, int64_t ldm, double* G) -> Status {
+    if (!dig) return gemm(c, true, cols, cols, m, M, ldm, M, ldm, G, cols, nullptr, "gram", /*sym=*/true);
+    Timed tg(c, "gram");
+    RF_CUDA(ozaki_slice_thin(oz->a, M, ldm, cols, oz->work.p, st));
+    RF_CUDA(ozaki_gram_thin(oz->a, cols, oz->work.p, G, cols, st));
+    oz->thin_src = M;
+    oz->thin_cols = cols;
+    return {};
+  };
+  RF_TRY(gram(X, ldx, G1));
   if (dist) RF_TRY(allreduce(c, G1, cc));
   {
     Timed tc(c, "chol");
     RF_CUDA(chol_inv(G1, cols, R1, R1i, cwork, info, infod, st));
   }
   RF_TRY(gemm(c, false, m, cols, cols, X, ldx, R1i, cols, Q1, ldq1, nullptr, "trsm", false, /*tri_b=*/true));
-  RF_TRY(gemm(c, true, cols, cols, m, Q1, ldq1, Q1, ldq1, G2, cols, nullptr, "gram", /*sym=*/true));
+  RF_TRY(gram(Q1, ldq1, G2));
   if (dist) RF_TRY(allreduce(c, G2, cc));
   {
     Timed tc(c, "chol");
@@ -634,7 +660,8 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
     }
     return {};
   }
-  // Gram-Schmidt with the reference's drop rule.
+  // Gram-Schmidt with the reference's drop rule (its basis replaces Q1 in out->Q).
+  if (oz) oz->thin_src = nullptr;
   DBuf gw;
   RF_TRY(gw.alloc(sizeof(double) * gs_orth_work_doubles(m, cols) + 64, st));
   int64_t* r_dev = reinterpret_cast<int64_t*>(gw.d() + gs_orth_work_doubles(m, cols));
@@ -740,9 +767,9 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
       RF_TRY(allreduce(c, z.d(), n * ell));
       RF_TRY(pass_nn(c, a, z.d(), ell, y.d(), ldq, &oz));
     }
-    RF_TRY(orth(c, y.d(), m, ell, ldq, &Qb, R2ibuf, nullptr, true, true));
+    RF_TRY(orth(c, y.d(), m, ell, ldq, &Qb, R2ibuf, nullptr, true, true, &oz));
   } else {
-    RF_TRY(orth(c, y.d(), m, ell, ldq, &Qb, R2ibuf, nullptr, true, true));
+    RF_TRY(orth(c, y.d(), m, ell, ldq, &Qb, R2ibuf, nullptr, true, true, &oz));
     for (int64_t j = 0; j < q && Qb.r > 0; ++j) {
       RF_TRY(pass_tn(c, a, Qb, z.d(), tmp.d(), &oz));
       Basis Wb;
@@ -754,7 +781,7 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
         break;
       }
       RF_TRY(pass_nn(c, a, w.d(), Wb.r, y.d(), ldq, &oz));
-      RF_TRY(orth(c, y.d(), m, Wb.r, ldq, &Qb, R2ibuf, nullptr, true, true));
+      RF_TRY(orth(c, y.d(), m, Wb.r, ldq, &Qb, R2ibuf, nullptr, true, true, &oz));
     }
   }
   // projection: B^T = A^T Q (finish_with_projection, rangefinder.cpp:24-30)

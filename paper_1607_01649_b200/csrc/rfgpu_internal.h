@@ -81,9 +81,13 @@ size_t ozaki_nn_work_bytes(const OzakiA& a, int64_t rows, int64_t ell);
 cudaError_t ozaki_nn(const OzakiA& a, int64_t r0, int64_t r1, const double* X, int64_t ldx, int64_t ell, double* Y,
                      int64_t ldy, void* work, cudaStream_t st);
 size_t ozaki_tn_work_bytes(const OzakiA& a, int64_t ell);
-// Z (n x ell) = A^T Q  (Q m x ell, col-major)
+// Z (n x ell) = A^T Q  (Q m x ell, col-major); presliced: Q's digits are already in work (ozaki_slice_thin)
 cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell, double* Z, int64_t ldz, void* work,
-                     cudaStream_t st);
+                     cudaStream_t st, bool presliced = false);
+// Gram of a tall R (a.m x ell) on the digit path: slice R into work (the
+// layout ozaki_tn reads), then G = R^T R (ell x ell).
+cudaError_t ozaki_slice_thin(const OzakiA& a, const double* R, int64_t ldr, int64_t ell, void* work, cudaStream_t st);
+cudaError_t ozaki_gram_thin(const OzakiA& a, int64_t ell, void* work, double* G, int64_t ldg, cudaStream_t st);
 
 // ---- small dense kernels (small_f64.cu) ----------------------------------
 // Upper Cholesky R^T R = G (G c x c, symmetric, upper triangle consulted,
