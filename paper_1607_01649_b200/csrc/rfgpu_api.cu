@@ -407,13 +407,20 @@ struct OzPasses {
     const OzakiA lay = ozaki_layout(m->m, m->n, digits);
     // One digit set takes `digits` bytes per element of A: when HBM cannot
     // hold it next to A, the passes stay on the FP64 tensor pipe (DMMA).
-    if (!planes.alloc(ozaki_a_bytes(m->m, m->n, digits), c->stream).ok() ||
-        !work.alloc(std::max(ozaki_nn_work_bytes(lay, m->m, ell), ozaki_tn_work_bytes(lay, ell)), c->stream).ok()) {
+    // Both digit sets in one allocation when they fit (the same size every
+    // call, so the stream-ordered pool reuses it); else the row-scaled set
+    // alone and columns() decides how A^T Q runs.
+    const size_t base = (ozaki_a_bytes(m->m, m->n, digits) + 4095) / 4096 * 4096;
+    const size_t set = ozaki_set_bytes(m->m, m->n, digits);
+    const size_t wbytes = std::max(ozaki_nn_work_bytes(lay, m->m, ell), ozaki_tn_work_bytes(lay, ell));
+    const bool both = planes.alloc(base + set, c->stream).ok();
+    if ((!both && !planes.alloc(base, c->stream).ok()) || !work.alloc(wbytes, c->stream).ok()) {
       on = false;
       if (std::getenv("RFGPU_DEBUG")) std::fprintf(stderr, "[rfgpu] digit planes do not fit: DMMA passes\n");
       return {};
     }
     ozaki_bind(planes.p, m->m, m->n, digits, &a);
+    if (both) a.cs = static_cast<int8_t*>(planes.p) + base;
     a.cs_rowmajor = ozaki_cs_rowmajor();
     return {};
   }
@@ -423,7 +430,7 @@ struct OzPasses {
   // else A^T Q stays on DMMA.
   Status columns(rfgpu_ctx* c, const rfgpu_matrix* m) {
     RF_CUDA(ozaki_col_exponents(&a, c->stream, c->h_info));
-    if (!a.shared) {
+    if (!a.shared && !a.cs) {
       if (cplanes.alloc(ozaki_set_bytes(m->m, m->n, a.digits), c->stream).ok()) {
         a.cs = cplanes.as<int8_t>();
       } else if (a.shared_ok) {  // no room for the second set: the row-scaled set serves A^T Q

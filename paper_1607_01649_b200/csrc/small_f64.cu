@@ -568,6 +568,187 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
   cluster.sync();  // keep DSMEM alive until every CTA is done with remote writes
 }
 
+// ------------------------------------------------------ block Jacobi (BOSJ) ---
+// One-sided block Jacobi for the small (l x l) factors, l <= ~440: the c
+// columns are cut into nb = 2P blocks of kBJB, and the P CTAs of a cluster
+// run the circle-method tournament over blocks. In a block round CTA q loads
+// its two blocks (X and V columns, all rows) from the global working copies
+// into shared memory, runs one full inner sweep over those 2 kBJB columns
+// (2 kBJB - 1 rounds of kBJB disjoint pairs, 64 threads per pair; reference
+// rotation formula and skip tolerance, dense.cpp:624-644), and writes them
+// back; a cluster barrier separates block rounds. Every column pair meets
+// once per block sweep, all of a round's work is CTA-local, and there are
+// nb - 1 cluster barriers per sweep instead of c - 1 exchanges.
+// Converged when a block sweep applies no rotation; <= 60 sweeps. The final
+// columns are sorted by norm (stable, descending) exactly as jacobi_svd_kernel.
+constexpr int kBJB = 16;
+constexpr int kBJThreads = 32 * kBJB;  // one warp per pair: warp-local sums, one barrier per inner round
+
+struct BJParams {
+  const double* X;  // mr x c input
+  int mr, c, nb;
+  double* U;
+  double* S;
+  double* V;
+  double* Xg;  // mr x (nb kBJB) working copy
+  double* Vg;  // c x (nb kBJB)
+  int* info;
+  int* sweeps_out;
+};
+
+__global__ void __launch_bounds__(kBJThreads, 1) bjacobi_kernel(const BJParams p0, const BJParams p1) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int P = static_cast<int>(cluster.num_blocks());
+  const BJParams& p = (static_cast<int>(blockIdx.x) / P == 0) ? p0 : p1;
+  const int q = static_cast<int>(cluster.block_rank());
+  const int mr = p.mr, c = p.c, nb = p.nb, W = nb * kBJB;
+  const int LX = mr | 1, LV = c | 1;
+  extern __shared__ double sm[];
+  double* Xs = sm;                    // [2 kBJB][LX]
+  double* Vs = Xs + 2 * kBJB * LX;    // [2 kBJB][LV]
+  __shared__ int s_tot[3];            // rotations per sweep (CTA 0's copy is the cluster total), by sweep % 3
+  __shared__ int s_rot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  for (int j = q; j < W; j += P) {
+    for (int i = tid; i < mr; i += kBJThreads) p.Xg[static_cast<int64_t>(j) * mr + i] = j < c ? p.X[static_cast<int64_t>(j) * mr + i] : 0.0;
+    for (int i = tid; i < c; i += kBJThreads) p.Vg[static_cast<int64_t>(j) * c + i] = (i == j) ? 1.0 : 0.0;
+  }
+  if (tid == 0) s_tot[0] = s_tot[1] = s_tot[2] = 0;
+  cluster.sync();
+
+  int sweep = 0;
+  bool conv = c <= 1;
+  while (!conv && sweep < 60) {
+    if (q == 0 && tid == 0) s_tot[(sweep + 1) % 3] = 0;  // read two sweeps ago: every CTA is past it
+    if (tid == 0) s_rot = 0;
+    for (int r = 0; r < nb - 1; ++r) {
+      int bi, bj;
+      pair_of(r, q, nb, &bi, &bj);
+      auto gcol = [&](int t) { return t < kBJB ? bi * kBJB + t : bj * kBJB + t - kBJB; };
+      for (int e = tid; e < 2 * kBJB * mr; e += kBJThreads) {
+        const int t = e / mr, i = e - t * mr;
+        Xs[t * LX + i] = p.Xg[static_cast<int64_t>(gcol(t)) * mr + i];
+      }
+      for (int e = tid; e < 2 * kBJB * c; e += kBJThreads) {
+        const int t = e / c, i = e - t * c;
+        Vs[t * LV + i] = p.Vg[static_cast<int64_t>(gcol(t)) * c + i];
+      }
+      __syncthreads();
+      for (int ir = 0; ir < 2 * kBJB - 1; ++ir) {
+        int u, v;
+        pair_of(ir, warp, 2 * kBJB, &u, &v);
+        double* xu = Xs + u * LX;
+        double* xv = Xs + v * LX;
+        double app = 0.0, aqq = 0.0, apq = 0.0;
+        for (int i = lane; i < mr; i += 32) {
+          const double a = xu[i], b = xv[i];
+          app = fma(a, a, app);
+          aqq = fma(b, b, aqq);
+          apq = fma(a, b, apq);
+        }
+        app = warp_sum(app);
+        aqq = warp_sum(aqq);
+        apq = warp_sum(apq);
+        if (app != 0.0 && aqq != 0.0 && !(fabs(apq) <= 1e-15 * sqrt(app * aqq))) {
+          const double zeta = (aqq - app) / (2.0 * apq);
+          const double t = (zeta < 0.0 ? -1.0 : 1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = rsqrt(1.0 + t * t), sn = cs * t;
+          for (int i = lane; i < mr; i += 32) {
+            const double a = xu[i], b = xv[i];
+            xu[i] = cs * a - sn * b;
+            xv[i] = sn * a + cs * b;
+          }
+          double* vu = Vs + u * LV;
+          double* vv = Vs + v * LV;
+          for (int i = lane; i < c; i += 32) {
+            const double a = vu[i], b = vv[i];
+            vu[i] = cs * a - sn * b;
+            vv[i] = sn * a + cs * b;
+          }
+          if (lane == 0) s_rot = 1;
+        }
+        __syncthreads();
+      }
+      for (int e = tid; e < 2 * kBJB * mr; e += kBJThreads) {
+        const int t = e / mr, i = e - t * mr;
+        p.Xg[static_cast<int64_t>(gcol(t)) * mr + i] = Xs[t * LX + i];
+      }
+      for (int e = tid; e < 2 * kBJB * c; e += kBJThreads) {
+        const int t = e / c, i = e - t * c;
+        p.Vg[static_cast<int64_t>(gcol(t)) * c + i] = Vs[t * LV + i];
+      }
+      cluster.sync();  // block round done everywhere: the working copies are consistent
+    }
+    if (tid == 0 && s_rot) atomicAdd(cluster.map_shared_rank(&s_tot[sweep % 3], 0), 1);
+    cluster.sync();
+    conv = *cluster.map_shared_rank(&s_tot[sweep % 3], 0) == 0;
+    ++sweep;
+  }
+
+  // final singular values (column norms), stable descending order; CTA 0
+  if (q == 0) {
+    double* nrm = Xs;                             // [W] (shared memory is free now)
+    int* perm = reinterpret_cast<int*>(Xs + W);   // [c]
+    for (int j = warp; j < c; j += kBJThreads / 32) {
+      const double* x = p.Xg + static_cast<int64_t>(j) * mr;
+      double s2 = 0.0;
+      for (int i = lane; i < mr; i += 32) s2 = fma(x[i], x[i], s2);
+      s2 = warp_sum(s2);
+      if (lane == 0) nrm[j] = sqrt(s2);
+    }
+    __syncthreads();
+    for (int j = tid; j < c; j += kBJThreads) {
+      const double kj = nrm[j];
+      int rank = 0;
+      for (int i = 0; i < c; ++i) {
+        const double ki = nrm[i];
+        rank += (ki > kj || (ki == kj && i < j)) ? 1 : 0;
+      }
+      perm[rank] = j;
+    }
+    __syncthreads();
+    const double smax = c > 0 ? nrm[perm[0]] : 0.0;
+    int zero_cols = 0;
+    for (int j = 0; j < c; ++j) {
+      const int src = perm[j];
+      const double sv = nrm[src];
+      const bool ok = sv > 0.0 && sv > smax * 1e-250;
+      if (!ok) zero_cols = 1;
+      if (tid == 0) p.S[j] = ok ? sv : 0.0;
+      const double* x = p.Xg + static_cast<int64_t>(src) * mr;
+      for (int i = tid; i < mr; i += kBJThreads) p.U[static_cast<int64_t>(j) * mr + i] = ok ? x[i] / sv : 0.0;
+      const double* vv = p.Vg + static_cast<int64_t>(src) * c;
+      for (int i = tid; i < c; i += kBJThreads) p.V[static_cast<int64_t>(j) * c + i] = vv[i];
+    }
+    if (tid == 0) {
+      p.info[0] = conv ? (zero_cols ? 2 : 0) : 1;
+      if (p.sweeps_out) p.sweeps_out[0] = sweep;
+    }
+  }
+  cluster.sync();
+}
+
+// Block Jacobi applies when the two blocks' rows fit in shared memory and the
+// tournament fits one cluster (<= 16 CTAs); RFGPU_JACOBI_BLOCK=0 disables it.
+struct BJLayout {
+  bool ok;
+  int P, nb;
+  size_t smem, work;  // bytes
+};
+BJLayout bj_layout(int64_t mr, int64_t c) {
+  BJLayout L{};
+  const char* e = std::getenv("RFGPU_JACOBI_BLOCK");
+  if ((e && e[0] == '0') || c < 2 * kBJB || mr > 1024) return L;
+  const int64_t blocks = (c + kBJB - 1) / kBJB;
+  L.nb = static_cast<int>(blocks + (blocks & 1));
+  L.P = L.nb / 2;
+  L.smem = sizeof(double) * 2 * kBJB * ((mr | 1) + (c | 1)) + 256;
+  L.work = sizeof(double) * static_cast<size_t>(L.nb) * kBJB * (mr + c);
+  L.ok = L.P <= 16 && L.smem <= 220 * 1024 && L.nb * kBJB >= c + 0;
+  return L;
+}
+
 __global__ void sumsq_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
   __shared__ double red[32];
   double s = 0.0;
@@ -844,13 +1025,51 @@ cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double
 size_t jacobi_work_bytes(int64_t mr, int64_t c) {
   const JacobiLayout L = jacobi_layout(mr, c);
   const size_t stage = sizeof(double) * static_cast<size_t>(L.P) * c * (L.LDX + L.LDV);
-  return L.smem ? stage : 2 * stage;
+  const BJLayout B = bj_layout(mr, c);
+  return std::max(L.smem ? stage : 2 * stage, B.ok ? B.work : size_t(0));
 }
 
 namespace {
 // One launch for 1 or 2 same-shape problems (one cluster each).
+cudaError_t bjacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64_t c, const BJLayout& B,
+                           cudaStream_t st) {
+  BJParams ps[2];
+  for (int i = 0; i < count; ++i) {
+    ps[i] = BJParams{pr[i].X, static_cast<int>(mr), static_cast<int>(c), B.nb, pr[i].U, pr[i].S, pr[i].V,
+                     pr[i].work, pr[i].work + static_cast<size_t>(B.nb) * kBJB * mr, pr[i].info, pr[i].sweeps};
+  }
+  if (count == 1) ps[1] = ps[0];
+  static size_t cfg_bytes = 0;
+  if (B.smem > cfg_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(bjacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(B.smem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(bjacobi_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    cfg_bytes = B.smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(B.P * count);
+  cfg.blockDim = dim3(kBJThreads);
+  cfg.dynamicSmemBytes = B.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = B.P;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, bjacobi_kernel, ps[0], ps[1]);
+  count_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 cudaError_t jacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64_t c, cudaStream_t st) {
   if (c <= 0 || mr <= 0) return cudaSuccess;
+  const BJLayout B = bj_layout(mr, c);
+  if (B.ok) return bjacobi_launch(pr, count, mr, c, B, st);
   const JacobiLayout L = jacobi_layout(mr, c);
   JacobiParams ps[2];
   for (int i = 0; i < count; ++i) {
