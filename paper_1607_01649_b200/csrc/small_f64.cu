@@ -581,8 +581,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
 // nb - 1 cluster barriers per sweep instead of c - 1 exchanges.
 // Converged when a block sweep applies no rotation; <= 60 sweeps. The final
 // columns are sorted by norm (stable, descending) exactly as jacobi_svd_kernel.
-constexpr int kBJB = 16;
-constexpr int kBJThreads = 32 * kBJB;  // one warp per pair: warp-local sums, one barrier per inner round
+// Block width B = 8 (more CTAs, fewer pairs per CTA per inner round) when the
+// tournament fits a 16-CTA cluster, else 12, else 16; one warp per pair (32 B
+// threads). Measured at l = 220: B = 8 7.5 ms, B = 16 9.0 ms, the per-column
+// cluster kernel 11.4 ms (9-10 sweeps each).
 
 struct BJParams {
   const double* X;  // mr x c input
@@ -596,12 +598,14 @@ struct BJParams {
   int* sweeps_out;
 };
 
-__global__ void __launch_bounds__(kBJThreads, 1) bjacobi_kernel(const BJParams p0, const BJParams p1) {
+template <int kBJB>
+__global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0, const BJParams p1) {
+  constexpr int kBJThreads = 32 * kBJB;
   cg::cluster_group cluster = cg::this_cluster();
   const int P = static_cast<int>(cluster.num_blocks());
   const BJParams& p = (static_cast<int>(blockIdx.x) / P == 0) ? p0 : p1;
   const int q = static_cast<int>(cluster.block_rank());
-  const int mr = p.mr, c = p.c, nb = p.nb, W = nb * kBJB;
+  const int mr = p.mr, c = p.c, nb = p.nb, W = nb * kBJB;  // W columns incl. zero padding
   const int LX = mr | 1, LV = c | 1;
   extern __shared__ double sm[];
   double* Xs = sm;                    // [2 kBJB][LX]
@@ -733,19 +737,25 @@ __global__ void __launch_bounds__(kBJThreads, 1) bjacobi_kernel(const BJParams p
 // tournament fits one cluster (<= 16 CTAs); RFGPU_JACOBI_BLOCK=0 disables it.
 struct BJLayout {
   bool ok;
-  int P, nb;
+  int B, P, nb;
   size_t smem, work;  // bytes
 };
 BJLayout bj_layout(int64_t mr, int64_t c) {
   BJLayout L{};
   const char* e = std::getenv("RFGPU_JACOBI_BLOCK");
-  if ((e && e[0] == '0') || c < 2 * kBJB || mr > 1024) return L;
-  const int64_t blocks = (c + kBJB - 1) / kBJB;
-  L.nb = static_cast<int>(blocks + (blocks & 1));
-  L.P = L.nb / 2;
-  L.smem = sizeof(double) * 2 * kBJB * ((mr | 1) + (c | 1)) + 256;
-  L.work = sizeof(double) * static_cast<size_t>(L.nb) * kBJB * (mr + c);
-  L.ok = L.P <= 16 && L.smem <= 220 * 1024 && L.nb * kBJB >= c + 0;
+  if ((e && e[0] == '0') || c < 32 || mr > 1024) return L;
+  for (int B : {8, 12, 16}) {
+    if (e && std::atoi(e) > 1 && std::atoi(e) != B) continue;  // RFGPU_JACOBI_BLOCK=8/16 pins the width
+    const int64_t blocks = (c + B - 1) / B;
+    L.B = B;
+    L.nb = static_cast<int>(blocks + (blocks & 1));
+    L.P = L.nb / 2;
+    L.smem = sizeof(double) * 2 * B * ((mr | 1) + (c | 1)) + 256;
+    L.work = sizeof(double) * static_cast<size_t>(L.nb) * B * (mr + c);
+    L.ok = L.P <= 16 && L.smem <= 220 * 1024;
+    if (L.ok) return L;
+  }
+  L.ok = false;
   return L;
 }
 
@@ -1036,21 +1046,23 @@ cudaError_t bjacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64
   BJParams ps[2];
   for (int i = 0; i < count; ++i) {
     ps[i] = BJParams{pr[i].X, static_cast<int>(mr), static_cast<int>(c), B.nb, pr[i].U, pr[i].S, pr[i].V,
-                     pr[i].work, pr[i].work + static_cast<size_t>(B.nb) * kBJB * mr, pr[i].info, pr[i].sweeps};
+                     pr[i].work, pr[i].work + static_cast<size_t>(B.nb) * B.B * mr, pr[i].info, pr[i].sweeps};
   }
   if (count == 1) ps[1] = ps[0];
-  static size_t cfg_bytes = 0;
-  if (B.smem > cfg_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(bjacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(B.smem));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(bjacobi_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-    cfg_bytes = B.smem;
+  static bool cfg_done = false;
+  if (!cfg_done) {
+    for (const void* fn : {reinterpret_cast<const void*>(bjacobi_kernel<8>), reinterpret_cast<const void*>(bjacobi_kernel<12>),
+                           reinterpret_cast<const void*>(bjacobi_kernel<16>)}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    cfg_done = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(B.P * count);
-  cfg.blockDim = dim3(kBJThreads);
+  cfg.blockDim = dim3(32 * B.B);
   cfg.dynamicSmemBytes = B.smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1060,7 +1072,9 @@ cudaError_t bjacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, bjacobi_kernel, ps[0], ps[1]);
+  cudaError_t e = B.B == 8    ? cudaLaunchKernelEx(&cfg, bjacobi_kernel<8>, ps[0], ps[1])
+                  : B.B == 12 ? cudaLaunchKernelEx(&cfg, bjacobi_kernel<12>, ps[0], ps[1])
+                              : cudaLaunchKernelEx(&cfg, bjacobi_kernel<16>, ps[0], ps[1]);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
