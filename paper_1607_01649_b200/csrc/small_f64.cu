@@ -877,27 +877,29 @@ __global__ void __launch_bounds__(256) cholb_diag(double* __restrict__ R, int c,
   }
   __syncthreads();
   const double floor = stat[0], trace = stat[1];
-  for (int j = 0; j < b; ++j) {
-    if (tid == 0) {
+  // factor the diagonal block with warp 0 alone (warp-synchronous steps):
+  // lane r owns row r of each trailing column
+  if (warp == 0) {
+    for (int j = 0; j < b; ++j) {
       const double d = A[j][j];
-      if (d <= floor || !(d > 0.0)) {
-        s_fail = k0 + j + 1;
-      } else {
-        s_min = fmin(s_min, trace > 0.0 ? d / trace : 0.0);
-        A[j][j] = sqrt(d);
+      if (d <= floor || !(d > 0.0)) {  // every lane sees the same pivot
+        if (lane == 0) s_fail = k0 + j + 1;
+        break;
       }
+      if (lane == 0) s_min = fmin(s_min, trace > 0.0 ? d / trace : 0.0);
+      const double cjj = sqrt(d);
+      __syncwarp();
+      if (lane == j) A[j][j] = cjj;
+      if (lane > j && lane < b) A[lane][j] /= cjj;  // row j of R: column `lane`
+      __syncwarp();
+      for (int col = j + 1; col < b; ++col) {
+        const double rc = A[col][j];
+        if (lane > j && lane <= col) A[col][lane] = fma(-A[lane][j], rc, A[col][lane]);
+      }
+      __syncwarp();
     }
-    __syncthreads();
-    if (s_fail) break;
-    const double cjj = A[j][j];
-    for (int col = j + 1 + tid; col < b; col += blockDim.x) A[col][j] /= cjj;
-    __syncthreads();
-    for (int col = j + 1 + warp; col < b; col += 8) {
-      const double rc = A[col][j];
-      for (int i = j + 1 + lane; i <= col; i += 32) A[col][i] -= A[i][j] * rc;
-    }
-    __syncthreads();
   }
+  __syncthreads();
   if (s_fail) {
     if (tid == 0) {
       info[0] = s_fail;
@@ -905,18 +907,16 @@ __global__ void __launch_bounds__(256) cholb_diag(double* __restrict__ R, int c,
     }
     return;
   }
-  // R_kk^{-1} (upper), one warp per column: R x = e_j by back substitution
+  // R_kk^{-1} (upper), one warp per column j: back substitution with x over
+  // the lanes (lane r holds x_r), one shuffle per step
   for (int j = warp; j < b; j += 8) {
-    for (int i = lane; i < b; i += 32) X[j][i] = 0.0;
-    __syncwarp();
-    if (lane == 0) {
-      for (int i = j; i >= 0; --i) {
-        double t = (i == j) ? 1.0 : 0.0;
-        for (int k = i + 1; k <= j; ++k) t -= A[k][i] * X[j][k];
-        X[j][i] = t / A[i][i];
-      }
+    double x = (lane == j) ? 1.0 : 0.0;
+    for (int i = j; i >= 0; --i) {
+      const double xi = __shfl_sync(0xffffffffu, x, i) / A[i][i];
+      if (lane == i) x = xi;
+      else if (lane < i) x = fma(-xi, A[i][lane], x);
     }
-    __syncwarp();
+    X[j][lane] = lane <= j ? x : 0.0;
   }
   __syncthreads();
   for (int e = tid; e < b * b; e += blockDim.x) {

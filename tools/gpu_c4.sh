@@ -1,7 +1,9 @@
 set -x
 mkdir -p gpurun_out
-for w in c4 c3 c5; do
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/pytest_gpu.log
+for w in c4 c3; do
   RFGPU_DEBUG=1 timeout 600 python bench.py --workload $w --steps 3 --no-e2e --no-cpu-baseline > gpurun_out/exp_$w.json 2> gpurun_out/exp_$w.err; echo "$w exit $?"
   python -c "import json; d=json.loads(open('gpurun_out/exp_$w.json').read().strip().splitlines()[-1]); print('$w', d['value'], {k: round(v,2) for k,v in d['phase_ms_per_step'].items() if v})"
+  grep sweeps gpurun_out/exp_$w.err | sort | uniq -c
 done
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/pytest_gpu.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"chol|trinv" --csv --log-file gpurun_out/l_c4.csv python bench.py --workload c4 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/c4n.log 2>&1; echo "exit $?"
