@@ -808,7 +808,7 @@ bool persistent() {
 template <int S, int BK>
 cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int64_t L_M, const int8_t* R,
                                 int64_t R_rows, int64_t K_pad, int64_t row0, int64_t rows, int64_t N_real, int splits,
-                                const OzParams& base, bool multicast, cudaStream_t st) {
+                                const OzParams& base, bool multicast, cudaStream_t st, bool persist) {
   constexpr int kS = S;
   constexpr size_t kSmemBytes = Dig<S, BK>::smem;
   constexpr CUtensorMapSwizzle kSwK = BK == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
@@ -867,7 +867,7 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   attr[0].val.clusterDim.z = 1;
   cfgl.attrs = attr;
   cfgl.numAttrs = 1;
-  if (persistent()) {  // one resident cluster per slot, looping over the tile groups
+  if (persist) {  // one resident cluster per slot, looping over the tile groups
     int nclusters = 0;
     auto kfn = L_mn ? ozaki_gemm_kernel<true, S, BK> : ozaki_gemm_kernel<false, S, BK>;
     if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &cfgl) != cudaSuccess || nclusters <= 0) {
@@ -893,17 +893,18 @@ int stage_bk() {
 
 cudaError_t launch_digit_gemm(int S, const int8_t* L, int64_t L_rows, bool L_mn, int64_t L_M, const int8_t* R,
                               int64_t R_rows, int64_t K_pad, int64_t row0, int64_t rows, int64_t N_real, int splits,
-                              const OzParams& base, bool multicast, cudaStream_t st) {
+                              const OzParams& base, bool multicast, cudaStream_t st, int persist = -1) {
   const bool b32 = stage_bk() == 32;
+  const bool pers = persist < 0 ? persistent() : persist == 1;
   if (S == 4)
     return b32 ? launch_digit_gemm_s<4, 32>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
-                                            multicast, st)
+                                            multicast, st, pers)
                : launch_digit_gemm_s<4, 64>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
-                                            multicast, st);
+                                            multicast, st, pers);
   return b32 ? launch_digit_gemm_s<7, 32>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
-                                          multicast, st)
+                                          multicast, st, pers)
              : launch_digit_gemm_s<7, 64>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
-                                          multicast, st);
+                                          multicast, st, pers);
 }
 
 // Column exponents (many CTAs per column) + digits of the thin operand R

@@ -503,8 +503,10 @@ Status pass_tn_raw(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Y, int64_t
   if (oz && oz->on && oz->tn) {
     Timed t(c, "pass_tn");
     const bool pre = oz->thin_src == Y && oz->thin_cols == cols && !oz->a.shared;
-    oz->thin_src = nullptr;
     RF_CUDA(ozaki_tn(oz->a, Y, ldy, cols, Z, a->n, oz->work.p, c->stream, pre));
+    // Y's column-scaled digits stay in the work buffer (the lift may reuse them)
+    oz->thin_src = oz->a.shared ? nullptr : Y;
+    oz->thin_cols = cols;
     return {};
   }
   return gemm(c, true, a->n, cols, a->m, static_cast<const double*>(a->dev), a->lda, Y, ldy, Z, a->n, nullptr,
@@ -643,6 +645,8 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
     Timed tc(c, "chol");
     RF_CUDA(chol_inv(G1, cols, R1, R1i, cwork, info, infod, st));
   }
+  // (an INT8 digit-path TRSM from X's digits measured 4.1 ms against 2.9 ms on DMMA at config 3: K = l is too
+  // short for the digit GEMM's per-tile fetch and epilogue)
   RF_TRY(gemm(c, false, m, cols, cols, X, ldx, R1i, cols, Q1, ldq1, nullptr, "trsm", false, /*tri_b=*/true));
   RF_TRY(gram(Q1, ldq1, G2));
   if (dist) RF_TRY(allreduce(c, G2, cc));
@@ -745,7 +749,7 @@ struct RangeOut {
 // R2ibuf (ell x ell) receive the basis; Bt (n x ell, ld n) receives
 // B^T = A^T Q (summed over ranks). power_range, rangefinder.cpp:63-80.
 Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, int64_t q, bool reorth,
-                  double* Qbuf, int64_t ldq, double* R2ibuf, double* Bt, RangeOut* out) {
+                  double* Qbuf, int64_t ldq, double* R2ibuf, double* Bt, RangeOut* out, OzPasses* ozp = nullptr) {
   cudaStream_t st = c->stream;
   const int64_t m = a->m, n = a->n;
   DBuf y, z, w, tmp, ssq, scal;
@@ -753,7 +757,8 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
   RF_TRY(z.alloc(sizeof(double) * n * ell, st));
   RF_TRY(w.alloc(sizeof(double) * n * ell, st));
   RF_TRY(tmp.alloc(sizeof(double) * n * ell, st));
-  OzPasses oz;
+  OzPasses oz_local;
+  OzPasses& oz = ozp ? *ozp : oz_local;  // the caller may keep the digit buffers past the range finder (rsvd's lift)
   RF_TRY(oz.init(c, a, ell));
   const int64_t slots = pass1_slots(c, a, ell, oz);
   RF_TRY(ssq.alloc(sizeof(double) * std::max<int64_t>(1, slots), st));

@@ -88,7 +88,6 @@ cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell,
 // layout ozaki_tn reads), then G = R^T R (ell x ell).
 cudaError_t ozaki_slice_thin(const OzakiA& a, const double* R, int64_t ldr, int64_t ell, void* work, cudaStream_t st);
 cudaError_t ozaki_gram_thin(const OzakiA& a, int64_t ell, void* work, double* G, int64_t ldg, cudaStream_t st);
-
 // ---- small dense kernels (small_f64.cu) ----------------------------------
 // Upper Cholesky R^T R = G (G c x c, symmetric, upper triangle consulted,
 // ld = c) and R^{-1}, both c x c column-major with zeros below the diagonal.
