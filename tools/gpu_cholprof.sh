@@ -1,5 +1,8 @@
 set -x
 mkdir -p gpurun_out
-export M=20000 N=4000 K=200 P=20
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"chol|trinv" --csv --log-file gpurun_out/chol_launches.csv python tools/prof_small.py > gpurun_out/chol_l.log 2>&1; echo "exit $?"
-timeout 600 python -m pytest tests/test_gpu_rsvd.py tests/test_gpu_ozaki.py -x -q > gpurun_out/pytest_part.log 2>&1; echo "pytest exit $?"; tail -2 gpurun_out/pytest_part.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/pytest_gpu.log
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"chol|trinv" --csv --log-file gpurun_out/chol_launches.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/chol_l.log 2>&1; echo "exit $?"
+for w in c3 c1 c2; do
+  timeout 500 python bench.py --workload $w --no-e2e --no-cpu-baseline --steps 3 > gpurun_out/exp_$w.json 2>gpurun_out/exp_$w.err; echo "$w exit $?"
+  python -c "import json; d=json.loads(open('gpurun_out/exp_$w.json').read().strip().splitlines()[-1]); print('$w', d['value'], {k: round(v,2) for k,v in d['phase_ms_per_step'].items() if v})"
+done
