@@ -1033,13 +1033,18 @@ cudaError_t ozaki_prepare_rows(const void* A, bool f32, int64_t lda, int64_t r0,
              : prepare_rows_t(static_cast<const double*>(A), lda, r0, r1, a, ssq_part, slice_rows, st);
 }
 
-cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext) {
+cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext, bool decide) {
   cudaError_t e = cudaMemsetAsync(a->ext, 0x80, 2 * sizeof(int), st);  // very negative
   if (e != cudaSuccess) return e;
   const int64_t nblk = (a->m + 255) / 256;
   colexp_kernel<<<static_cast<unsigned>((a->n_pad + 31) / 32), dim3(32, 32), 0, st>>>(a->colpart, nblk, a->n,
                                                                                       a->n_pad, a->colexp, a->ext);
   count_launch();
+  if (!decide) {  // the second digit set is already allocated: nothing to decide on the host, no sync
+    a->shared = false;
+    a->shared_ok = false;
+    return cudaGetLastError();
+  }
   if ((e = cudaMemcpyAsync(h_ext, a->ext, 2 * sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
   const bool any = h_ext[0] > -100000;  // some non-zero column

@@ -429,7 +429,9 @@ struct OzPasses {
   // serves A^T Q when the column scales allow it (ozaki.cu kSharedSpread),
   // else A^T Q stays on DMMA.
   Status columns(rfgpu_ctx* c, const rfgpu_matrix* m) {
-    RF_CUDA(ozaki_col_exponents(&a, c->stream, c->h_info));
+    const char* fs = std::getenv("RFGPU_OZAKI_SHARED");
+    const bool decide = !a.cs || (fs && fs[0] == '1');  // host decision only for the memory fallback / forced mode
+    RF_CUDA(ozaki_col_exponents(&a, c->stream, c->h_info, decide));
     if (!a.shared && !a.cs) {
       if (cplanes.alloc(ozaki_set_bytes(m->m, m->n, a.digits), c->stream).ok()) {
         a.cs = cplanes.as<int8_t>();
@@ -440,7 +442,7 @@ struct OzPasses {
         if (std::getenv("RFGPU_DEBUG")) std::fprintf(stderr, "[rfgpu] column-scaled digits do not fit: DMMA A^T Q\n");
       }
     }
-    if (std::getenv("RFGPU_DEBUG"))
+    if (std::getenv("RFGPU_DEBUG") && decide)
       std::fprintf(stderr, "[rfgpu] digit sets: %s (column exponents %d..%d)\n", a.shared ? "shared" : "two",
                    -c->h_info[1], c->h_info[0]);
     return {};

@@ -71,8 +71,9 @@ cudaError_t ozaki_prepare_rows(const void* A, bool f32, int64_t lda, int64_t r0,
                                double* ssq_part, bool slice_rows, cudaStream_t st);
 // After every row block's stats: column exponents and whether one shared
 // digit set could serve A^T Q too (shared_ok; shared is set only when forced
-// by RFGPU_OZAKI_SHARED=1). Synchronises the stream; h_ext: 2 pinned ints.
-cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext);
+// by RFGPU_OZAKI_SHARED=1). With decide, synchronises the stream to read the
+// exponent range (h_ext: 2 pinned ints); without, only launches the kernel.
+cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext, bool decide = true);
 // One read of A writing the row-scaled (rows) and / or column-scaled (cols) digits.
 cudaError_t ozaki_slice_sets(const void* A, bool f32, int64_t lda, const OzakiA& a, bool rows, bool cols,
                              cudaStream_t st);
