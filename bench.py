@@ -396,6 +396,17 @@ def main():
             e1.synchronize()
             e2e_s = max_over_ranks(e0.elapsed_time(e1) / args.steps) / 1e3
             kk = rank_out.value
+            if os.environ.get("RFGPU_BENCH_E2E_PHASES"):  # diagnostics: per-phase GPU time of one e2e call
+                ctx.profile(True)
+                ctx.profile_reset()
+                t0 = time.perf_counter()
+                e2e_step()
+                torch.cuda.synchronize()
+                wall = time.perf_counter() - t0
+                names = ("pass_nn", "pass_tn", "ozaki_slice", "orth", "small_svd", "lift", "gram", "trsm", "chol")
+                print(json.dumps({"e2e_wall_s": wall, "phases_ms": {nm: ctx.profile_read(nm)[1] for nm in names}}),
+                      file=sys.stderr, flush=True)
+                ctx.profile(False)
             e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(8 * (mloc * n + n * ell)),
                    "d2h_bytes_per_step": int(8 * (mloc * kk + n * kk + kk))}
             del Ah, Uh, Vh

@@ -49,6 +49,7 @@ constexpr int OBN = 64;        // tile columns per accumulator group
 // K bytes per pipeline stage: BK = 64 (64B-swizzled K-major rows, 2 stages
 // of 86 KB for 7 digits) or 32 (32B swizzle, 5 stages of 43 KB: more bytes in
 // flight per SM at the same shared-memory footprint).
+constexpr int BKQ = 64;  // K bytes per block in kb_split_fixed
 constexpr int64_t kSplitK = 16384;  // int32 safety: S * K * 128^2 < 2^31
 // K per split of the A^T Q pass (<= kSplitK, a multiple of 256): RFGPU_OZAKI_TNK overrides.
 int64_t tn_split_k() {
@@ -161,25 +162,34 @@ __global__ void rowexp_kernel(const uint32_t* __restrict__ rowhi, int64_t r0, in
     rowexp[i] = hi_exp(rowhi[i]);
 }
 
-// Column exponents from the per-block column maxima; ext[0] = max and ext[1] =
-// -min exponent over the non-zero columns (both pre-set very negative).
-// Block (32, 32): 32 columns, the row blocks strided over threadIdx.y (each
-// warp reads 128 contiguous bytes per row block), then a shared-memory max.
-__global__ void __launch_bounds__(1024) colexp_kernel(const uint32_t* __restrict__ colpart, int64_t nblk, int64_t n,
-                                                      int64_t n_pad, int* __restrict__ colexp, int* __restrict__ ext) {
+// Column exponents of the column-scaled digit set, per row chunk (the A^T Q
+// K-splits: chunk c = rows [c chunk_rows, (c+1) chunk_rows), 256-row blocks
+// per chunk = bpc): colexp[c][j] from the per-block column maxima colpart.
+// Chunks [c0, c1) only (the streamed upload computes them panel by panel).
+// ext[0] = max and ext[1] = -min exponent over the non-zero columns of those
+// chunks (both pre-set very negative), for the shared-set fallback test.
+// Block (32, 32): 32 columns, the chunks strided over threadIdx.y (each warp
+// reads 128 contiguous bytes per row block).
+__global__ void __launch_bounds__(1024) colexp_kernel(const uint32_t* __restrict__ colpart, int64_t nblk, int64_t bpc,
+                                                      int64_t c0, int64_t c1, int64_t n, int64_t n_pad,
+                                                      int* __restrict__ colexp, int* __restrict__ ext) {
   __shared__ uint32_t red[32][33];
   const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
-  uint32_t mx = 0;
-  if (j < n)
-    for (int64_t b = threadIdx.y; b < nblk; b += 32) mx = max(mx, colpart[b * n_pad + j]);
-  red[threadIdx.y][threadIdx.x] = mx;
+  uint32_t gmx = 0;
+  for (int64_t ch = c0 + threadIdx.y; ch < c1; ch += 32) {
+    uint32_t mx = 0;
+    if (j < n)
+      for (int64_t b = ch * bpc; b < min(nblk, (ch + 1) * bpc); ++b) mx = max(mx, colpart[b * n_pad + j]);
+    if (j < n_pad) colexp[ch * n_pad + j] = hi_exp(mx);
+    gmx = max(gmx, mx);
+  }
+  red[threadIdx.y][threadIdx.x] = gmx;
   __syncthreads();
   if (threadIdx.y == 0) {
-    for (int y = 1; y < 32; ++y) mx = max(mx, red[y][threadIdx.x]);
-    if (j < n_pad) colexp[j] = hi_exp(mx);
+    for (int y = 1; y < 32; ++y) gmx = max(gmx, red[y][threadIdx.x]);
     int emax = INT_MIN, nmin = INT_MIN;
-    if (mx != 0) {
-      emax = hi_exp(mx);
+    if (gmx != 0) {
+      emax = hi_exp(gmx);
       nmin = -emax;
     }
     emax = __reduce_max_sync(0xffffffffu, emax);
@@ -230,8 +240,9 @@ __device__ __forceinline__ void transpose4(const uint32_t* p, uint32_t* w) {
 template <class T, int S>
 __global__ void __launch_bounds__(256) slice_a_kernel(const T* __restrict__ A, int64_t m, int64_t n, int64_t lda,
                                                       int64_t r0, int64_t r1, const int* __restrict__ rowexp,
-                                                      const int* __restrict__ colexp, int8_t* __restrict__ rs,
-                                                      int8_t* __restrict__ cs, int64_t m_pad, int64_t n_pad) {
+                                                      const int* __restrict__ colexp, int64_t chunk_rows,
+                                                      int8_t* __restrict__ rs, int8_t* __restrict__ cs, int64_t m_pad,
+                                                      int64_t n_pad) {
   const int64_t quads = (r1 - r0 + 3) / 4;
   const int64_t total = quads * n_pad;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
@@ -239,7 +250,7 @@ __global__ void __launch_bounds__(256) slice_a_kernel(const T* __restrict__ A, i
     const int64_t j = e / quads, i0 = r0 + (e - j * quads) * 4;
     uint32_t wr[S] = {}, wc[S] = {};
     if (j < n) {
-      const int fj = cs ? colexp[j] : 0;
+      const int fj = cs ? colexp[(i0 / chunk_rows) * n_pad + j] : 0;  // 4-row quads never straddle a chunk
       double v[4];
       int er[4];
       if (i0 + 3 < m && sizeof(T) == 8 && ((j * lda + i0) & 1) == 0) {
@@ -316,13 +327,14 @@ constexpr int kSliceTRows = 128, kSliceTCols = 64;
 
 template <class T, int S>
 __global__ void __launch_bounds__(256) slice_at_kernel(const T* __restrict__ A, int64_t m, int64_t n, int64_t lda,
-                                                       const int* __restrict__ rowexp, const int* __restrict__ colexp,
-                                                       int8_t* __restrict__ rs, int8_t* __restrict__ cs,
-                                                       int64_t m_pad, int64_t n_pad) {
+                                                       const int* __restrict__ rowexp, const int* __restrict__ colexp_all,
+                                                       int64_t chunk_rows, int64_t row_start, int8_t* __restrict__ rs,
+                                                       int8_t* __restrict__ cs, int64_t m_pad, int64_t n_pad) {
   extern __shared__ uint32_t W[];  // [S][kSliceTCols][33]
   const int64_t ntc = n_pad / kSliceTCols;
   const int64_t jt = blockIdx.x % ntc, it = blockIdx.x / ntc;
-  const int64_t i0 = it * kSliceTRows, j0 = jt * kSliceTCols;
+  const int64_t i0 = row_start + it * kSliceTRows, j0 = jt * kSliceTCols;
+  const int* __restrict__ colexp = colexp_all + (i0 / chunk_rows) * n_pad;  // a tile never straddles a chunk
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ib = i0 + 4 * lane;
   int er[4] = {0, 0, 0, 0};
@@ -484,6 +496,8 @@ struct OzParams {
   int cl;             // cluster size along N tiles: the A tile is TMA-multicast to all of them
   int64_t ngroups;    // tile groups (all tiles / cl); the grid may be smaller (persistent)
   int last_w;         // width of the last n-tile (multiple of 16, <= OBN): l's padding is not multiplied
+  int64_t rex_stride;      // rowexp is [split][rex_stride] (per K-chunk output-row exponents; 0: one vector)
+  int64_t kb_split_fixed;  // K blocks per split when it must match the chunks (0: even split)
 };
 
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
@@ -695,7 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t lrow = tc.lrow0 + q * 32 + lane;
       const int64_t orow = p.c_row0 + (lrow - p.row0);
-      const int rex = (p.rowexp && tc.nk > 0) ? p.rowexp[lrow] : 0;
+      const int rex = (p.rowexp && tc.nk > 0) ? p.rowexp[tc.split * p.rex_stride + lrow] : 0;
       const bool row_ok = orow < p.M_real + p.c_row0 && lrow - p.row0 < p.M_real;
       for (int c = 0; c < tc.w; c += 16) {
         uint32_t r[kS][16];
@@ -835,8 +849,13 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   p.L_rows = L_rows;
   p.R_rows = R_rows;
   p.kb_total = K_pad / BK;
+  if (base.kb_split_fixed > 0) {  // chunk-aligned splits (given in 64-byte K blocks)
+    p.kb_per_split = base.kb_split_fixed * 64 / BK;
+    splits = static_cast<int>((p.kb_total + p.kb_per_split - 1) / p.kb_per_split);
+  } else {
+    p.kb_per_split = (p.kb_total + splits - 1) / splits;
+  }
   p.splits = splits;
-  p.kb_per_split = (p.kb_total + splits - 1) / splits;
   p.ntn = ntn;
   p.last_w = last_w;
   p.mtn = static_cast<int>((rows + OBM - 1) / OBM);
@@ -928,14 +947,17 @@ cudaError_t slice_thin(int S, const double* R, int64_t K, int64_t N, int64_t ldr
 
 template <class T>
 void slice_a(int S, const T* A, int64_t m, int64_t n, int64_t lda, int64_t r0, int64_t r1, const int* rowexp,
-             const int* colexp, int8_t* rs, int8_t* cs, int64_t m_pad, int64_t n_pad, cudaStream_t st) {
+             const int* colexp, int64_t chunk_rows, int8_t* rs, int8_t* cs, int64_t m_pad, int64_t n_pad,
+             cudaStream_t st) {
   const int64_t items = (r1 - r0 + 3) / 4 * n_pad;
   if (items <= 0) return;
   const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((items + 255) / 256, 148 * 32));
   if (S == 4)
-    slice_a_kernel<T, 4><<<blocks, 256, 0, st>>>(A, m, n, lda, r0, r1, rowexp, colexp, rs, cs, m_pad, n_pad);
+    slice_a_kernel<T, 4><<<blocks, 256, 0, st>>>(A, m, n, lda, r0, r1, rowexp, colexp, chunk_rows, rs, cs, m_pad,
+                                                 n_pad);
   else
-    slice_a_kernel<T, 7><<<blocks, 256, 0, st>>>(A, m, n, lda, r0, r1, rowexp, colexp, rs, cs, m_pad, n_pad);
+    slice_a_kernel<T, 7><<<blocks, 256, 0, st>>>(A, m, n, lda, r0, r1, rowexp, colexp, chunk_rows, rs, cs, m_pad,
+                                                 n_pad);
 }
 
 }  // namespace
@@ -954,6 +976,8 @@ OzakiA ozaki_layout(int64_t m, int64_t n, int digits) {
   a.digits = digits;
   a.m_pad = roundup(std::max<int64_t>(m, 1), 256);
   a.n_pad = roundup(std::max<int64_t>(n, 1), OBM);
+  a.chunk_rows = tn_split_k();  // the A^T Q K-splits: a multiple of 256
+  a.nchunks = (a.m_pad + a.chunk_rows - 1) / a.chunk_rows;
   return a;
 }
 
@@ -962,6 +986,8 @@ size_t ozaki_set_bytes(int64_t m, int64_t n, int digits) {
   return static_cast<size_t>(digits) * a.m_pad * a.n_pad;
 }
 
+int64_t ozaki_chunk_rows() { return tn_split_k(); }
+
 bool ozaki_cs_rowmajor() {
   const char* e = std::getenv("RFGPU_OZAKI_TNMN");  // experiments: 0 keeps the column-major cs (K-major A^T Q)
   return !(e && e[0] == '0');
@@ -969,7 +995,7 @@ bool ozaki_cs_rowmajor() {
 
 size_t ozaki_a_bytes(int64_t m, int64_t n, int digits) {
   const OzakiA a = ozaki_layout(m, n, digits);
-  return ozaki_set_bytes(m, n, digits) + sizeof(int) * (2 * a.m_pad + a.n_pad + 8) +
+  return ozaki_set_bytes(m, n, digits) + sizeof(int) * (2 * a.m_pad + a.nchunks * a.n_pad + 8) +
          sizeof(uint32_t) * (a.m_pad / 256) * a.n_pad + 1024;
 }
 
@@ -991,7 +1017,7 @@ void ozaki_bind(void* work, int64_t m, int64_t n, int digits, OzakiA* out) {
   out->cs = nullptr;  // bound by the caller once ozaki_decide says the column-scaled set is needed
   out->rowexp = reinterpret_cast<int*>(base + planes);
   out->colexp = out->rowexp + out->m_pad;
-  out->ext = out->colexp + out->n_pad;
+  out->ext = out->colexp + out->nchunks * out->n_pad;
   out->rowhi = reinterpret_cast<uint32_t*>(out->ext + 8);
   out->colpart = out->rowhi + out->m_pad;
 }
@@ -1021,7 +1047,8 @@ cudaError_t prepare_rows_t(const T* A, int64_t lda, int64_t r0, int64_t r1, cons
     count_launch(2);
   }
   if (slice_rows) {
-    slice_a<T>(a.digits, A, a.m, a.n, lda, r0, s1, a.rowexp, nullptr, a.rs, nullptr, a.m_pad, a.n_pad, st);
+    slice_a<T>(a.digits, A, a.m, a.n, lda, r0, s1, a.rowexp, nullptr, a.chunk_rows, a.rs, nullptr, a.m_pad, a.n_pad,
+               st);
     count_launch();
   }
   return cudaGetLastError();
@@ -1033,13 +1060,21 @@ cudaError_t ozaki_prepare_rows(const void* A, bool f32, int64_t lda, int64_t r0,
              : prepare_rows_t(static_cast<const double*>(A), lda, r0, r1, a, ssq_part, slice_rows, st);
 }
 
+namespace {
+cudaError_t chunk_colexp(const OzakiA& a, int64_t c0, int64_t c1, cudaStream_t st) {
+  if (c1 <= c0) return cudaSuccess;
+  const int64_t nblk = (a.m + 255) / 256;
+  colexp_kernel<<<static_cast<unsigned>((a.n_pad + 31) / 32), dim3(32, 32), 0, st>>>(
+      a.colpart, nblk, a.chunk_rows / 256, c0, c1, a.n, a.n_pad, a.colexp, a.ext);
+  count_launch();
+  return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext, bool decide) {
   cudaError_t e = cudaMemsetAsync(a->ext, 0x80, 2 * sizeof(int), st);  // very negative
   if (e != cudaSuccess) return e;
-  const int64_t nblk = (a->m + 255) / 256;
-  colexp_kernel<<<static_cast<unsigned>((a->n_pad + 31) / 32), dim3(32, 32), 0, st>>>(a->colpart, nblk, a->n,
-                                                                                      a->n_pad, a->colexp, a->ext);
-  count_launch();
+  if ((e = chunk_colexp(*a, 0, a->nchunks, st)) != cudaSuccess) return e;
   if (!decide) {  // the second digit set is already allocated: nothing to decide on the host, no sync
     a->shared = false;
     a->shared_ok = false;
@@ -1057,7 +1092,8 @@ cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext, bool dec
 }
 
 template <class T>
-cudaError_t slice_sets_t(const T* A, int64_t lda, const OzakiA& a, bool rows, bool cols, cudaStream_t st) {
+cudaError_t slice_sets_t(const T* A, int64_t lda, const OzakiA& a, bool rows, bool cols, int64_t r0, int64_t r1,
+                         cudaStream_t st) {
   if (cols && a.cs_rowmajor) {
     const size_t smem = sizeof(uint32_t) * a.digits * kSliceTCols * 33;
     static bool cfg = false;
@@ -1069,17 +1105,18 @@ cudaError_t slice_sets_t(const T* A, int64_t lda, const OzakiA& a, bool rows, bo
       }
       cfg = true;
     }
-    const unsigned grid = static_cast<unsigned>((a.m_pad / kSliceTRows) * (a.n_pad / kSliceTCols));
+    if (r1 <= r0) return cudaSuccess;
+    const unsigned grid = static_cast<unsigned>(((r1 - r0) / kSliceTRows) * (a.n_pad / kSliceTCols));
     if (a.digits == 4)
-      slice_at_kernel<T, 4><<<grid, 256, smem, st>>>(A, a.m, a.n, lda, a.rowexp, a.colexp, rows ? a.rs : nullptr, a.cs,
-                                                     a.m_pad, a.n_pad);
+      slice_at_kernel<T, 4><<<grid, 256, smem, st>>>(A, a.m, a.n, lda, a.rowexp, a.colexp, a.chunk_rows, r0,
+                                                     rows ? a.rs : nullptr, a.cs, a.m_pad, a.n_pad);
     else
-      slice_at_kernel<T, 7><<<grid, 256, smem, st>>>(A, a.m, a.n, lda, a.rowexp, a.colexp, rows ? a.rs : nullptr, a.cs,
-                                                     a.m_pad, a.n_pad);
+      slice_at_kernel<T, 7><<<grid, 256, smem, st>>>(A, a.m, a.n, lda, a.rowexp, a.colexp, a.chunk_rows, r0,
+                                                     rows ? a.rs : nullptr, a.cs, a.m_pad, a.n_pad);
     count_launch();
     return cudaGetLastError();
   }
-  slice_a<T>(a.digits, A, a.m, a.n, lda, 0, a.m_pad, a.rowexp, a.colexp, rows ? a.rs : nullptr,
+  slice_a<T>(a.digits, A, a.m, a.n, lda, r0, r1, a.rowexp, a.colexp, a.chunk_rows, rows ? a.rs : nullptr,
              cols ? a.cs : nullptr, a.m_pad, a.n_pad, st);
   count_launch();
   return cudaGetLastError();
@@ -1088,8 +1125,21 @@ cudaError_t slice_sets_t(const T* A, int64_t lda, const OzakiA& a, bool rows, bo
 cudaError_t ozaki_slice_sets(const void* A, bool f32, int64_t lda, const OzakiA& a, bool rows, bool cols,
                              cudaStream_t st) {
   if (!rows && !cols) return cudaSuccess;
-  return f32 ? slice_sets_t(static_cast<const float*>(A), lda, a, rows, cols, st)
-             : slice_sets_t(static_cast<const double*>(A), lda, a, rows, cols, st);
+  return f32 ? slice_sets_t(static_cast<const float*>(A), lda, a, rows, cols, 0, a.m_pad, st)
+             : slice_sets_t(static_cast<const double*>(A), lda, a, rows, cols, 0, a.m_pad, st);
+}
+
+// Rows [r0, r1) of an uploaded panel (r0, r1 multiples of chunk_rows, or r1 =
+// m): the column exponents of the chunks these rows complete, then their
+// column-scaled digits (cs must be bound). Lets the streamed upload slice cs
+// panel by panel instead of reading all of A again after the last panel.
+cudaError_t ozaki_slice_cols_rows(const void* A, bool f32, int64_t lda, const OzakiA& a, int64_t r0, int64_t r1,
+                                  cudaStream_t st) {
+  const int64_t s1 = r1 >= a.m ? a.m_pad : r1;
+  cudaError_t e = chunk_colexp(a, r0 / a.chunk_rows, (s1 + a.chunk_rows - 1) / a.chunk_rows, st);
+  if (e != cudaSuccess) return e;
+  return f32 ? slice_sets_t(static_cast<const float*>(A), lda, a, false, true, r0, s1, st)
+             : slice_sets_t(static_cast<const double*>(A), lda, a, false, true, r0, s1, st);
 }
 
 size_t ozaki_nn_work_bytes(const OzakiA& a, int64_t rows, int64_t ell) {
@@ -1159,7 +1209,9 @@ cudaError_t ozaki_tn(const OzakiA& a, const double* Q, int64_t ldq, int64_t ell,
   p.C = splits > 1 ? ws : Z;
   p.ldc = ldz;
   p.c_row0 = 0;
-  p.rowexp = a.shared ? nullptr : a.colexp;  // output row j of A^T Q = column j of A
+  p.rowexp = a.shared ? nullptr : a.colexp;  // output row j of A^T Q = column j of A (per K-split chunk)
+  p.rex_stride = a.shared ? 0 : a.n_pad;
+  p.kb_split_fixed = a.chunk_rows / BKQ;  // K-splits = the column-exponent chunks
   p.colexp = colexp;
   p.cshift = a.shared ? a.emax : 0;
   p.ws_mode = splits > 1 ? 1 : 0;

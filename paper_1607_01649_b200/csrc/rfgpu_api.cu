@@ -382,7 +382,10 @@ int64_t sumsq_slots(rfgpu_ctx* c, int64_t M, int64_t N, int64_t K) {
 // the only compute not hidden under the copy.
 std::vector<std::pair<int64_t, int64_t>> upload_panels(int64_t m) {
   int64_t np = m >= (int64_t{1} << 19) ? 16 : (m >= (int64_t{1} << 16) ? 4 : 1);
-  const int64_t step = ((m + np - 1) / np + 255) / 256 * 256;
+  // panel boundaries on the digit path's column-exponent chunks, so that each
+  // panel's column-scaled digits can be written as soon as it lands
+  const int64_t q = ozaki_chunk_rows();
+  const int64_t step = ((m + np - 1) / np + q - 1) / q * q;
   std::vector<std::pair<int64_t, int64_t>> out;
   for (int64_t r = 0; r < m; r += step) out.emplace_back(r, std::min(m, r + step));
   if (out.empty()) out.emplace_back(0, 0);
@@ -478,6 +481,8 @@ Status pass1_rows(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
     } else {
       Timed t(c, "ozaki_slice");
       RF_CUDA(ozaki_prepare_rows(A, false, a->lda, r0, r1, oz.a, ssq, true, c->stream));
+      if (oz.tn && oz.a.cs && !oz.a.shared)  // this panel's column-scaled digits (per-chunk exponents)
+        RF_CUDA(ozaki_slice_cols_rows(A, false, a->lda, oz.a, r0, r1, c->stream));
     }
     Timed t(c, "pass_nn");
     RF_CUDA(ozaki_nn(oz.a, r0, r1, G, a->n, ell, Y, ldy, oz.work.p, c->stream));
@@ -553,10 +558,12 @@ Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, 
     s = pass1_rows(c, a, G, ell, Y, ldy, ssq + off, r0, r0 + rows, oz, false);
     off += oz.on ? ozaki_ssq_slots(rows, a->n) : sumsq_slots(c, rows, ell, n);
   }
-  if (s.ok() && oz.on) {  // all rows landed: column exponents, and the A^T Q digits unless shared
+  if (s.ok() && oz.on) {  // all rows landed: the A^T Q digits unless sliced per panel already
     Timed t(c, "ozaki_slice");
+    const bool sliced = oz.tn && oz.a.cs && !oz.a.shared;
     s = oz.columns(c, a);
-    if (s.ok() && ozaki_slice_sets(A, false, lda, oz.a, false, oz.tn && !oz.a.shared, st) != cudaSuccess)
+    if (s.ok() && !sliced &&
+        ozaki_slice_sets(A, false, lda, oz.a, false, oz.tn && !oz.a.shared, st) != cudaSuccess)
       s = make_err(RFGPU_ECUDA, "pass 1: slicing failed");
   }
   a->src = nullptr;  // issued: every later consumer is ordered after the waits above

@@ -46,7 +46,7 @@ struct OzakiA {
   int8_t* cs;   // digits of A(i,j) 2^-colexp[j] (A^T Q when !shared; caller-bound): [digits][m_pad][n_pad]
                 // (row-major, read M-major) when cs_rowmajor, else [digits][n_pad][m_pad] (read K-major)
   int* rowexp;  // m_pad: |A(i,:)| < 2^rowexp[i]
-  int* colexp;  // n_pad: |A(:,j)| < 2^colexp[j]
+  int* colexp;  // [nchunks][n_pad]: |A(rows of chunk c, j)| < 2^colexp[c][j]
   int* ext;     // 2 (+pad): max column exponent, -min column exponent (non-zero columns)
   uint32_t* rowhi;    // m_pad row maxima (high words of |A(i,:)|)
   uint32_t* colpart;  // (m_pad / 256) x n_pad per-block column maxima (high words)
@@ -56,7 +56,9 @@ struct OzakiA {
   bool shared_ok;  // the column scales allow it (ozaki_col_exponents)
   int emax;     // max column exponent (shared mode's thin-operand shift)
   bool cs_rowmajor;
+  int64_t chunk_rows, nchunks;  // colexp is [nchunks][n_pad]: column exponents per row chunk (= A^T Q K-split)
 };
+int64_t ozaki_chunk_rows();  // rows per column-exponent chunk (the A^T Q split; a multiple of 256)
 bool ozaki_cs_rowmajor();  // layout of the column-scaled set (RFGPU_OZAKI_TNMN=0: column-major)
 bool ozaki_enabled(int64_t m, int64_t n);  // RFGPU_OZAKI=0/1 overrides the size rule
 OzakiA ozaki_layout(int64_t m, int64_t n, int digits);  // shapes only (no buffers)
@@ -74,6 +76,10 @@ cudaError_t ozaki_prepare_rows(const void* A, bool f32, int64_t lda, int64_t r0,
 // by RFGPU_OZAKI_SHARED=1). With decide, synchronises the stream to read the
 // exponent range (h_ext: 2 pinned ints); without, only launches the kernel.
 cudaError_t ozaki_col_exponents(OzakiA* a, cudaStream_t st, int* h_ext, bool decide = true);
+// Column exponents of the chunks completed by rows [r0, r1) and those rows'
+// column-scaled digits (streamed upload; r0, r1 chunk-aligned or r1 = m).
+cudaError_t ozaki_slice_cols_rows(const void* A, bool f32, int64_t lda, const OzakiA& a, int64_t r0, int64_t r1,
+                                  cudaStream_t st);
 // One read of A writing the row-scaled (rows) and / or column-scaled (cols) digits.
 cudaError_t ozaki_slice_sets(const void* A, bool f32, int64_t lda, const OzakiA& a, bool rows, bool cols,
                              cudaStream_t st);
