@@ -589,6 +589,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
 struct BJParams {
   const double* X;  // mr x c input
   int mr, c, nb;
+  int cross_only;   // later block rounds visit only the cross pairs
   double* U;
   double* S;
   double* V;
@@ -606,6 +607,7 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
   const BJParams& p = (static_cast<int>(blockIdx.x) / P == 0) ? p0 : p1;
   const int q = static_cast<int>(cluster.block_rank());
   const int mr = p.mr, c = p.c, nb = p.nb, W = nb * kBJB;  // W columns incl. zero padding
+  const bool bj_cross_only = p.cross_only != 0;
   const int LX = mr | 1, LV = c | 1;
   extern __shared__ double sm[];
   double* Xs = sm;                    // [2 kBJB][LX]
@@ -639,9 +641,20 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
         Vs[t * LV + i] = p.Vg[static_cast<int64_t>(gcol(t)) * c + i];
       }
       __syncthreads();
-      for (int ir = 0; ir < 2 * kBJB - 1; ++ir) {
+      // The first block round of a sweep runs a full inner sweep over the 2B
+      // columns (every intra-block pair); later ones only the B x B cross
+      // pairs (B rounds: column w of the first block with column (w + s) mod B
+      // of the second), so each column pair is visited once per sweep.
+      const bool full = r == 0 || !bj_cross_only;
+      const int nir = full ? 2 * kBJB - 1 : kBJB;
+      for (int ir = 0; ir < nir; ++ir) {
         int u, v;
-        pair_of(ir, warp, 2 * kBJB, &u, &v);
+        if (full) {
+          pair_of(ir, warp, 2 * kBJB, &u, &v);
+        } else {
+          u = warp;
+          v = kBJB + (warp + ir) % kBJB;
+        }
         double* xu = Xs + u * LX;
         double* xv = Xs + v * LX;
         double app = 0.0, aqq = 0.0, apq = 0.0;
@@ -1045,7 +1058,9 @@ cudaError_t bjacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64
                            cudaStream_t st) {
   BJParams ps[2];
   for (int i = 0; i < count; ++i) {
-    ps[i] = BJParams{pr[i].X, static_cast<int>(mr), static_cast<int>(c), B.nb, pr[i].U, pr[i].S, pr[i].V,
+    const char* co = std::getenv("RFGPU_JACOBI_CROSS");
+    ps[i] = BJParams{pr[i].X, static_cast<int>(mr), static_cast<int>(c), B.nb, (co && co[0] == '0') ? 0 : 1,
+                     pr[i].U, pr[i].S, pr[i].V,
                      pr[i].work, pr[i].work + static_cast<size_t>(B.nb) * B.B * mr, pr[i].info, pr[i].sweeps};
   }
   if (count == 1) ps[1] = ps[0];
