@@ -411,6 +411,100 @@ __global__ void trinv_upper_kernel(const double* __restrict__ R, int64_t ldr, in
   }
 }
 
+// Blocked R^{-1} (k > 64): 32 x 32 diagonal blocks D_I = R_II^{-1} first (one
+// CTA each, warp-parallel back substitution per column with precomputed
+// reciprocal pivots), then one CTA per block column J:
+//   X_JJ = D_J,  X_IJ = -D_I sum_{K=I+1..J} R_IK X_KJ  for I = J-1 .. 0,
+// the X_KJ blocks of the column held in shared memory. Every dependency chain
+// is 32 steps long instead of k (the per-column trinv_upper_kernel reads R
+// from global memory in a k-step chain).
+constexpr int kTB = 32;
+
+__global__ void __launch_bounds__(256) trinv_diag_kernel(const double* __restrict__ R, int64_t ldr, int k,
+                                                         double* __restrict__ Dinv) {
+  __shared__ double A[kTB][kTB + 1];  // A[col][row]
+  __shared__ double rd[kTB];
+  const int I = blockIdx.x, i0 = I * kTB, bw = min(kTB, k - i0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < kTB * kTB; e += blockDim.x) {
+    const int c = e / kTB, r = e % kTB;
+    A[c][r] = (c < bw && r <= c) ? R[static_cast<int64_t>(i0 + c) * ldr + i0 + r] : 0.0;
+  }
+  __syncthreads();
+  if (tid < kTB) rd[tid] = tid < bw ? 1.0 / A[tid][tid] : 0.0;
+  __syncthreads();
+  for (int j = warp; j < kTB; j += 8) {
+    double x = (lane == j && j < bw) ? 1.0 : 0.0;
+    if (j < bw)
+      for (int i = j; i >= 0; --i) {
+        const double xi = __shfl_sync(0xffffffffu, x, i) * rd[i];
+        if (lane == i) x = xi;
+        else if (lane < i) x = fma(-xi, A[i][lane], x);
+      }
+    Dinv[(static_cast<int64_t>(I) * kTB + j) * kTB + lane] = (lane <= j && j < bw) ? x : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) trinv_blockcol_kernel(const double* __restrict__ R, int64_t ldr, int k,
+                                                             const double* __restrict__ Dinv,
+                                                             double* __restrict__ Rinv) {
+  extern __shared__ double X[];       // [J + 1][kTB][kTB + 1]: X_KJ blocks, [c][r]
+  __shared__ double Rt[kTB][kTB + 1];  // R_IK, [c][r]
+  __shared__ double S[kTB][kTB + 1];   // partial sum, [c][r]
+  const int J = blockIdx.x, j0 = J * kTB;
+  const int tid = threadIdx.x;
+  const int c = tid & 31, r0 = (tid >> 5) * 4;  // this thread's outputs: rows r0..r0+3 of column c
+  auto xb = [&](int K) { return X + static_cast<size_t>(K) * kTB * (kTB + 1); };
+  {
+    const double* d = Dinv + static_cast<int64_t>(J) * kTB * kTB;
+    double* x = xb(J);
+    for (int e = tid; e < kTB * kTB; e += blockDim.x) x[(e / kTB) * (kTB + 1) + e % kTB] = d[e];
+  }
+  __syncthreads();
+  for (int I = J - 1; I >= 0; --I) {
+    const int i0 = I * kTB;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int K = I + 1; K <= J; ++K) {
+      const int kk0 = K * kTB, kw = min(kTB, k - kk0);
+      __syncthreads();  // Rt reuse
+      for (int e = tid; e < kTB * kTB; e += blockDim.x) {
+        const int cc = e / kTB, rr = e % kTB;
+        Rt[cc][rr] = cc < kw ? R[static_cast<int64_t>(kk0 + cc) * ldr + i0 + rr] : 0.0;
+      }
+      __syncthreads();
+      const double* x = xb(K);
+#pragma unroll 4
+      for (int t = 0; t < kTB; ++t) {
+        const double b = x[c * (kTB + 1) + t];  // X_KJ(t, c)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = fma(Rt[t][r0 + u], b, acc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) S[c][r0 + u] = acc[u];
+    __syncthreads();
+    // X_IJ = -D_I S
+    const double* d = Dinv + static_cast<int64_t>(I) * kTB * kTB;  // [col][row]
+    double o[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int t = 0; t < kTB; ++t) {
+      const double b = S[c][t];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o[u] = fma(d[t * kTB + r0 + u], b, o[u]);
+    }
+    double* xi = xb(I);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xi[c * (kTB + 1) + r0 + u] = -o[u];
+    __syncthreads();
+  }
+  // column block J of R^{-1}: rows 0 .. j0 + kTB from the X blocks, zeros below
+  const int jw = min(kTB, k - j0);
+  for (int e = tid; e < jw * k; e += blockDim.x) {
+    const int cc = e / k, rr = e % k;
+    const int K = rr / kTB;
+    Rinv[static_cast<int64_t>(j0 + cc) * k + rr] = K <= J ? xb(K)[cc * (kTB + 1) + rr % kTB] : 0.0;
+  }
+}
+
 // Z (ke x n): Z(:, perm[j]) = e_j for j < ke, = T(:, j - ke) otherwise.
 __global__ void assemble_z_kernel(const int64_t* __restrict__ perm, int ke, int64_t n,
                                   const double* __restrict__ T, double* __restrict__ Z) {
@@ -469,6 +563,25 @@ cudaError_t cpqr_rank(double* W, int64_t ld, int m, int64_t n, int kmax, double 
 cudaError_t trinv_upper(const double* R, int64_t ldr, int k, double* Rinv, cudaStream_t st) {
   if (k <= 0) return cudaSuccess;
   if (k > 352) return cudaErrorInvalidValue;
+  const int nb = (k + kTB - 1) / kTB;
+  const size_t smem = sizeof(double) * nb * kTB * (kTB + 1);
+  if (k > 64 && smem <= 200 * 1024) {
+    static bool cfg = false;
+    if (!cfg) {
+      cudaError_t e = cudaFuncSetAttribute(trinv_blockcol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) return e;
+      cfg = true;
+    }
+    double* dinv = nullptr;
+    cudaError_t e = cudaMallocAsync(&dinv, sizeof(double) * nb * kTB * kTB, st);
+    if (e != cudaSuccess) return e;
+    trinv_diag_kernel<<<nb, 256, 0, st>>>(R, ldr, k, dinv);
+    trinv_blockcol_kernel<<<nb, 256, smem, st>>>(R, ldr, k, dinv, Rinv);
+    count_launch(2);
+    e = cudaGetLastError();
+    cudaFreeAsync(dinv, st);
+    return e;
+  }
   const int warps = 8;
   trinv_upper_kernel<11><<<(k + warps - 1) / warps, warps * 32, 0, st>>>(R, ldr, k, Rinv);
   count_launch();

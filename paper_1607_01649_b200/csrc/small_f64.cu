@@ -890,27 +890,27 @@ __global__ void __launch_bounds__(256) cholb_diag(double* __restrict__ R, int c,
   }
   __syncthreads();
   const double floor = stat[0], trace = stat[1];
-  // factor the diagonal block with warp 0 alone (warp-synchronous steps):
-  // lane r owns row r of each trailing column
-  if (warp == 0) {
-    for (int j = 0; j < b; ++j) {
-      const double d = A[j][j];
-      if (d <= floor || !(d > 0.0)) {  // every lane sees the same pivot
-        if (lane == 0) s_fail = k0 + j + 1;
-        break;
-      }
-      if (lane == 0) s_min = fmin(s_min, trace > 0.0 ? d / trace : 0.0);
-      const double cjj = sqrt(d);
-      __syncwarp();
-      if (lane == j) A[j][j] = cjj;
-      if (lane > j && lane < b) A[lane][j] /= cjj;  // row j of R: column `lane`
-      __syncwarp();
-      for (int col = j + 1; col < b; ++col) {
-        const double rc = A[col][j];
-        if (lane > j && lane <= col) A[col][lane] = fma(-A[lane][j], rc, A[col][lane]);
-      }
-      __syncwarp();
+  // factor the diagonal block: every thread reads the pivot, row j is scaled
+  // by warp 0, the trailing columns are updated by the 8 warps (column col by
+  // warp col % 8, lane = row), two barriers per step
+  for (int j = 0; j < b; ++j) {
+    const double d = A[j][j];
+    if (d <= floor || !(d > 0.0)) {  // every thread sees the same pivot
+      if (tid == 0) s_fail = k0 + j + 1;
+      break;
     }
+    const double cjj = sqrt(d);
+    if (warp == 0) {
+      if (lane == 0) s_min = fmin(s_min, trace > 0.0 ? d / trace : 0.0);
+      if (lane > j && lane < b) A[lane][j] /= cjj;  // row j of R: column `lane`
+    }
+    __syncthreads();
+    if (tid == 0) A[j][j] = cjj;
+    for (int col = j + 1 + warp; col < b; col += 8) {
+      const double rc = A[col][j];
+      if (lane > j && lane <= col) A[col][lane] = fma(-A[lane][j], rc, A[col][lane]);
+    }
+    __syncthreads();
   }
   __syncthreads();
   if (s_fail) {
@@ -922,10 +922,13 @@ __global__ void __launch_bounds__(256) cholb_diag(double* __restrict__ R, int c,
   }
   // R_kk^{-1} (upper), one warp per column j: back substitution with x over
   // the lanes (lane r holds x_r), one shuffle per step
+  __shared__ double rdg[kCB];
+  if (tid < b) rdg[tid] = 1.0 / A[tid][tid];
+  __syncthreads();
   for (int j = warp; j < b; j += 8) {
     double x = (lane == j) ? 1.0 : 0.0;
     for (int i = j; i >= 0; --i) {
-      const double xi = __shfl_sync(0xffffffffu, x, i) / A[i][i];
+      const double xi = __shfl_sync(0xffffffffu, x, i) * rdg[i];
       if (lane == i) x = xi;
       else if (lane < i) x = fma(-xi, A[i][lane], x);
     }
