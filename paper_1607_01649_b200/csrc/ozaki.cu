@@ -497,6 +497,7 @@ struct OzParams {
   int64_t ngroups;    // tile groups (all tiles / cl); the grid may be smaller (persistent)
   int last_w;         // width of the last n-tile (multiple of 16, <= OBN): l's padding is not multiplied
   int64_t rex_stride;      // rowexp is [split][rex_stride] (per K-chunk output-row exponents; 0: one vector)
+  int tma3;                // 1: one 3-D TMA copy per operand and stage (no multicast)
   int64_t kb_split_fixed;  // K blocks per split when it must match the chunks (0: even split)
 };
 
@@ -505,6 +506,15 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
           smem_u32(dst)),
       "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// 3-D box (all digit planes of a tile in one copy): coordinates {c0, c1, plane}.
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 
@@ -579,6 +589,9 @@ template <bool L_MN, int S, int BK>
 __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmL,
                                                                   const __grid_constant__ CUtensorMap tmR,
                                                                   const __grid_constant__ CUtensorMap tmR2,
+                                                                  const __grid_constant__ CUtensorMap tmL3,
+                                                                  const __grid_constant__ CUtensorMap tmR3,
+                                                                  const __grid_constant__ CUtensorMap tmR23,
                                                                   const OzParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -630,6 +643,13 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
         mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(ASZ + kS * tc.w * BK));
         const CUtensorMap* tr = tc.w == OBN ? &tmR : &tmR2;  // the narrow last tile: box of w rows
         const int kx = static_cast<int>((tc.kb0 + kb) * BK);
+        if (p.tma3) {  // all digit planes of each operand tile in one 3-D copy (2 TMA issues per stage)
+          const int lc0 = L_MN ? static_cast<int>(tc.lrow0) : kx;
+          const int lc1 = L_MN ? static_cast<int>((tc.kb0 + kb) * BK) : static_cast<int>(tc.lrow0);
+          tma3d(sA + st * ASZ, &tmL3, &full[st], lc0, lc1, 0);
+          tma3d(sB + st * BSZ, tc.w == OBN ? &tmR3 : &tmR23, &full[st], kx, static_cast<int>(tc.ncol0), 0);
+          continue;
+        }
 #pragma unroll
         for (int s = 0; s < kS; ++s) {
           // A planes round-robin over the cluster, multicast to all of it
@@ -807,6 +827,22 @@ bool digit_tmap(CUtensorMap* tm, const int8_t* base, int64_t rows, int64_t inner
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D map over the digit planes: dims {inner, rows per plane, planes}; box
+// {box_inner, box_rows, planes} lands in shared memory plane after plane.
+bool digit_tmap3(CUtensorMap* tm, const int8_t* base, int64_t planes, int64_t rows, int64_t inner, int box_inner,
+                 int box_rows, CUtensorMapSwizzle sw) {
+  auto fn = tmap_encoder();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(planes)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(inner * rows)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_rows),
+                       static_cast<cuuint32_t>(planes)};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // multicast: share each A tile across the CTAs of its N tiles (cluster).
 // Measured at config 3: it pays for the split-K A^T Q pass (31.1 vs 39.1 ms)
 // and costs the NN pass (30.3 vs 25.3 ms: four CTAs in lock step through a
@@ -845,6 +881,15 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   if (last_w > OBN || (nw && nw[0] == '0')) last_w = OBN;
   CUtensorMap tr2 = tr;
   if (last_w < OBN && !digit_tmap(&tr2, R, kS * R_rows, K_pad, BK, last_w, kSwK)) return cudaErrorInvalidValue;
+  CUtensorMap tl3 = tl, tr3 = tr, tr23 = tr2;
+  const char* t3e = std::getenv("RFGPU_OZAKI_TMA3");
+  bool tma3 = !(t3e && t3e[0] == '0');
+  if (tma3) {
+    tma3 = (L_mn ? digit_tmap3(&tl3, L, kS, L_rows, L_M, OBM, BK, CU_TENSOR_MAP_SWIZZLE_128B)
+                 : digit_tmap3(&tl3, L, kS, L_rows, K_pad, BK, OBM, kSwK)) &&
+           digit_tmap3(&tr3, R, kS, R_rows, K_pad, BK, OBN, kSwK) &&
+           (last_w == OBN || digit_tmap3(&tr23, R, kS, R_rows, K_pad, BK, last_w, kSwK));
+  }
   OzParams p = base;
   p.L_rows = L_rows;
   p.R_rows = R_rows;
@@ -874,6 +919,7 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
         break;
       }
   p.ngroups = grid / p.cl;
+  p.tma3 = (tma3 && p.cl == 1) ? 1 : 0;
   cudaLaunchConfig_t cfgl{};
   cfgl.gridDim = dim3(static_cast<unsigned>(grid));
   cfgl.blockDim = dim3(kThreads);
@@ -895,8 +941,8 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
     }
     if (nclusters < p.ngroups) cfgl.gridDim = dim3(static_cast<unsigned>(nclusters * p.cl));
   }
-  cudaError_t e = L_mn ? cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<true, S, BK>, tl, tr, tr2, p)
-                       : cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<false, S, BK>, tl, tr, tr2, p);
+  cudaError_t e = L_mn ? cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<true, S, BK>, tl, tr, tr2, tl3, tr3, tr23, p)
+                       : cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<false, S, BK>, tl, tr, tr2, tl3, tr3, tr23, p);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
