@@ -343,7 +343,7 @@ def main():
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     launches = ctx.launch_count() // args.steps
     prof = {nm: ctx.profile_read(nm) for nm in ("pass_nn", "pass_tn", "ozaki_slice", "sketch_nn", "sketch_tn", "orth", "small_svd",
-                                                "jacobi", "gram", "chol", "trsm", "lift", "col_id", "cpqr", "trsm_id",
+                                                "jacobi", "gram", "chol", "trsm", "lift", "stats", "slicer", "col_id", "cpqr", "trsm_id",
                                                 "single_pass_core", "gemm_nn", "gemm_tn", "allreduce")}
     ctx.profile(False)
     pass_names = ("sketch_nn", "sketch_tn") if kind == "single_pass" else ("pass_nn", "pass_tn")

@@ -454,8 +454,12 @@ struct OzPasses {
   // row-scaled when `rows` (A X) or shared, column-scaled when not shared.
   Status prepare(rfgpu_ctx* c, const rfgpu_matrix* m, double* ssq, bool rows = true) {
     Timed t(c, "ozaki_slice");
-    RF_CUDA(ozaki_prepare_rows(m->dev, m->f32, m->lda, 0, m->m, a, ssq, false, c->stream));
+    {
+      Timed ts(c, "stats");
+      RF_CUDA(ozaki_prepare_rows(m->dev, m->f32, m->lda, 0, m->m, a, ssq, false, c->stream));
+    }
     RF_TRY(columns(c, m));
+    Timed tsl(c, "slicer");
     RF_CUDA(ozaki_slice_sets(m->dev, m->f32, m->lda, a, rows || a.shared, tn && !a.shared, c->stream));
     return {};
   }
