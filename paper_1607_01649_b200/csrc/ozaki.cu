@@ -1060,7 +1060,7 @@ void ozaki_bind(void* work, int64_t m, int64_t n, int digits, OzakiA* out) {
   const size_t planes = ozaki_set_bytes(m, n, digits);
   int8_t* base = static_cast<int8_t*>(work);
   out->rs = base;
-  out->cs = nullptr;  // bound by the caller once ozaki_decide says the column-scaled set is needed
+  out->cs = nullptr;  // the caller binds the column-scaled set (OzPasses::init / columns)
   out->rowexp = reinterpret_cast<int*>(base + planes);
   out->colexp = out->rowexp + out->m_pad;
   out->ext = out->colexp + out->nchunks * out->n_pad;
