@@ -608,20 +608,29 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
   const int q = static_cast<int>(cluster.block_rank());
   const int mr = p.mr, c = p.c, nb = p.nb, W = nb * kBJB;  // W columns incl. zero padding
   const bool bj_cross_only = p.cross_only != 0;
-  const int LX = mr | 1, LV = c | 1;
+  const int LX = mr + (mr & 1), LV = c + (c & 1);  // even: every column 16-byte aligned for the bulk copies
   extern __shared__ double sm[];
   double* Xs = sm;                    // [2 kBJB][LX]
   double* Vs = Xs + 2 * kBJB * LX;    // [2 kBJB][LV]
   __shared__ int s_tot[3];            // rotations per sweep (CTA 0's copy is the cluster total), by sweep % 3
   __shared__ int s_rot;
+  __shared__ __align__(8) uint64_t s_bar;  // block loads: transaction bytes of the bulk copies
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+  // working copies with even leading dimensions LX / LV (padding rows zero)
   for (int j = q; j < W; j += P) {
-    for (int i = tid; i < mr; i += kBJThreads) p.Xg[static_cast<int64_t>(j) * mr + i] = j < c ? p.X[static_cast<int64_t>(j) * mr + i] : 0.0;
-    for (int i = tid; i < c; i += kBJThreads) p.Vg[static_cast<int64_t>(j) * c + i] = (i == j) ? 1.0 : 0.0;
+    for (int i = tid; i < LX; i += kBJThreads)
+      p.Xg[static_cast<int64_t>(j) * LX + i] = (j < c && i < mr) ? p.X[static_cast<int64_t>(j) * mr + i] : 0.0;
+    for (int i = tid; i < LV; i += kBJThreads) p.Vg[static_cast<int64_t>(j) * LV + i] = (i == j && j < c) ? 1.0 : 0.0;
   }
-  if (tid == 0) s_tot[0] = s_tot[1] = s_tot[2] = 0;
+  if (tid == 0) {
+    s_tot[0] = s_tot[1] = s_tot[2] = 0;
+    mbar_init(&s_bar, 1);
+    mbar_fence_init();
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> the bulk copies' reads
   cluster.sync();
+  uint32_t bar_phase = 0;
 
   int sweep = 0;
   bool conv = c <= 1;
@@ -632,15 +641,16 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
       int bi, bj;
       pair_of(r, q, nb, &bi, &bj);
       auto gcol = [&](int t) { return t < kBJB ? bi * kBJB + t : bj * kBJB + t - kBJB; };
-      for (int e = tid; e < 2 * kBJB * mr; e += kBJThreads) {
-        const int t = e / mr, i = e - t * mr;
-        Xs[t * LX + i] = p.Xg[static_cast<int64_t>(gcol(t)) * mr + i];
+      // both blocks (X and V columns) into shared memory: one bulk copy per column on the TMA engine
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&s_bar, static_cast<uint32_t>(sizeof(double) * 2 * kBJB * (LX + LV)));
+        for (int t = 0; t < 2 * kBJB; ++t) {
+          bulk_g2s(Xs + t * LX, p.Xg + static_cast<int64_t>(gcol(t)) * LX, sizeof(double) * LX, &s_bar);
+          bulk_g2s(Vs + t * LV, p.Vg + static_cast<int64_t>(gcol(t)) * LV, sizeof(double) * LV, &s_bar);
+        }
       }
-      for (int e = tid; e < 2 * kBJB * c; e += kBJThreads) {
-        const int t = e / c, i = e - t * c;
-        Vs[t * LV + i] = p.Vg[static_cast<int64_t>(gcol(t)) * c + i];
-      }
-      __syncthreads();
+      mbar_wait(&s_bar, bar_phase);
+      bar_phase ^= 1;
       // The first block round of a sweep runs a full inner sweep over the 2B
       // columns (every intra-block pair); later ones only the B x B cross
       // pairs (B rounds: column w of the first block with column (w + s) mod B
@@ -687,13 +697,23 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
         }
         __syncthreads();
       }
-      for (int e = tid; e < 2 * kBJB * mr; e += kBJThreads) {
-        const int t = e / mr, i = e - t * mr;
-        p.Xg[static_cast<int64_t>(gcol(t)) * mr + i] = Xs[t * LX + i];
-      }
-      for (int e = tid; e < 2 * kBJB * c; e += kBJThreads) {
-        const int t = e / c, i = e - t * c;
-        p.Vg[static_cast<int64_t>(gcol(t)) * c + i] = Vs[t * LV + i];
+      // write both blocks back with bulk shared->global copies (all rotations are done: the
+      // barrier at the end of the last inner round)
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int t = 0; t < 2 * kBJB; ++t) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                           p.Xg + static_cast<int64_t>(gcol(t)) * LX),
+                       "r"(smem_u32(Xs + t * LX)), "r"(static_cast<uint32_t>(sizeof(double) * LX))
+                       : "memory");
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                           p.Vg + static_cast<int64_t>(gcol(t)) * LV),
+                       "r"(smem_u32(Vs + t * LV)), "r"(static_cast<uint32_t>(sizeof(double) * LV))
+                       : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       cluster.sync();  // block round done everywhere: the working copies are consistent
     }
@@ -708,7 +728,7 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
     double* nrm = Xs;                             // [W] (shared memory is free now)
     int* perm = reinterpret_cast<int*>(Xs + W);   // [c]
     for (int j = warp; j < c; j += kBJThreads / 32) {
-      const double* x = p.Xg + static_cast<int64_t>(j) * mr;
+      const double* x = p.Xg + static_cast<int64_t>(j) * LX;
       double s2 = 0.0;
       for (int i = lane; i < mr; i += 32) s2 = fma(x[i], x[i], s2);
       s2 = warp_sum(s2);
@@ -733,9 +753,9 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
       const bool ok = sv > 0.0 && sv > smax * 1e-250;
       if (!ok) zero_cols = 1;
       if (tid == 0) p.S[j] = ok ? sv : 0.0;
-      const double* x = p.Xg + static_cast<int64_t>(src) * mr;
+      const double* x = p.Xg + static_cast<int64_t>(src) * LX;
       for (int i = tid; i < mr; i += kBJThreads) p.U[static_cast<int64_t>(j) * mr + i] = ok ? x[i] / sv : 0.0;
-      const double* vv = p.Vg + static_cast<int64_t>(src) * c;
+      const double* vv = p.Vg + static_cast<int64_t>(src) * LV;
       for (int i = tid; i < c; i += kBJThreads) p.V[static_cast<int64_t>(j) * c + i] = vv[i];
     }
     if (tid == 0) {
@@ -763,8 +783,8 @@ BJLayout bj_layout(int64_t mr, int64_t c) {
     L.B = B;
     L.nb = static_cast<int>(blocks + (blocks & 1));
     L.P = L.nb / 2;
-    L.smem = sizeof(double) * 2 * B * ((mr | 1) + (c | 1)) + 256;
-    L.work = sizeof(double) * static_cast<size_t>(L.nb) * B * (mr + c);
+    L.smem = sizeof(double) * 2 * B * ((mr + (mr & 1)) + (c + (c & 1))) + 256;
+    L.work = sizeof(double) * static_cast<size_t>(L.nb) * B * ((mr + (mr & 1)) + (c + (c & 1)));
     L.ok = L.P <= 16 && L.smem <= 220 * 1024;
     if (L.ok) return L;
   }
@@ -1064,7 +1084,8 @@ cudaError_t bjacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64
     const char* co = std::getenv("RFGPU_JACOBI_CROSS");
     ps[i] = BJParams{pr[i].X, static_cast<int>(mr), static_cast<int>(c), B.nb, (co && co[0] == '0') ? 0 : 1,
                      pr[i].U, pr[i].S, pr[i].V,
-                     pr[i].work, pr[i].work + static_cast<size_t>(B.nb) * B.B * mr, pr[i].info, pr[i].sweeps};
+                     pr[i].work, pr[i].work + static_cast<size_t>(B.nb) * B.B * (mr + (mr & 1)), pr[i].info,
+                     pr[i].sweeps};
   }
   if (count == 1) ps[1] = ps[0];
   static bool cfg_done = false;
