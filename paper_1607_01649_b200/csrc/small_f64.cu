@@ -677,7 +677,8 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
         app = warp_sum(app);
         aqq = warp_sum(aqq);
         apq = warp_sum(apq);
-        if (app != 0.0 && aqq != 0.0 && !(fabs(apq) <= 1e-15 * sqrt(app * aqq))) {
+        // skip rule |apq| <= 1e-15 sqrt(app aqq) (dense.cpp:631), squared: no sqrt on the round's chain
+        if (app != 0.0 && aqq != 0.0 && !(apq * apq <= 1e-30 * (app * aqq))) {
           const double zeta = (aqq - app) / (2.0 * apq);
           const double t = (zeta < 0.0 ? -1.0 : 1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = rsqrt(1.0 + t * t), sn = cs * t;
