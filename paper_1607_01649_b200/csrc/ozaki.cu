@@ -337,29 +337,35 @@ __global__ void __launch_bounds__(256) slice_at_kernel(const T* __restrict__ A, 
   const int* __restrict__ colexp = colexp_all + (i0 / chunk_rows) * n_pad;  // a tile never straddles a chunk
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ib = i0 + 4 * lane;
+  const int64_t plane = m_pad * n_pad;  // bytes per digit plane (both sets)
   int er[4] = {0, 0, 0, 0};
   if (rs)
 #pragma unroll
     for (int b = 0; b < 4; ++b) er[b] = ib + b < m ? rowexp[ib + b] : 0;
-  // 4 rows of column j0 + cc (zeros outside A); the next column's loads are
+  // running pointers (columns j0 + cc, cc = warp, warp + 8, ...): no 64-bit
+  // index products inside the loop
+  const bool vec = sizeof(T) == 8 && ib + 3 < m && (lda & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+  const T* colp = A + (j0 + warp) * lda + ib;
+  const int64_t col_step = 8 * lda;
+  int8_t* rsp = rs ? rs + (j0 + warp) * m_pad + ib : nullptr;
+  // 4 rows of one column (zeros outside A); the next column's loads are
   // issued before the current one is processed (two columns in flight per warp)
-  auto load4 = [&](int cc, double* v) {
-    const int64_t j = j0 + cc;
-    if (j < n && ib + 3 < m && sizeof(T) == 8 && ((j * lda + ib) & 1) == 0) {
-      const double2 p0 = *reinterpret_cast<const double2*>(A + j * lda + ib);
-      const double2 p1 = *reinterpret_cast<const double2*>(A + j * lda + ib + 2);
+  auto load4 = [&](const T* cp, int64_t j, double* v) {
+    if (j < n && vec) {
+      const double2 p0 = reinterpret_cast<const double2*>(cp)[0];
+      const double2 p1 = reinterpret_cast<const double2*>(cp)[1];
       v[0] = p0.x, v[1] = p0.y, v[2] = p1.x, v[3] = p1.y;
     } else {
 #pragma unroll
-      for (int b = 0; b < 4; ++b) v[b] = (j < n && ib + b < m) ? static_cast<double>(A[j * lda + ib + b]) : 0.0;
+      for (int b = 0; b < 4; ++b) v[b] = (j < n && ib + b < m) ? static_cast<double>(cp[b]) : 0.0;
     }
   };
   double vn[4];
-  load4(warp, vn);
-  for (int cc = warp; cc < kSliceTCols; cc += 8) {
+  load4(colp, j0 + warp, vn);
+  for (int cc = warp; cc < kSliceTCols; cc += 8, colp += col_step) {
     const int64_t j = j0 + cc;
     double v[4] = {vn[0], vn[1], vn[2], vn[3]};
-    if (cc + 8 < kSliceTCols) load4(cc + 8, vn);
+    if (cc + 8 < kSliceTCols) load4(colp + col_step, j + 8, vn);
     uint32_t wr[S], wc[S];
 #pragma unroll
     for (int q = 0; q < S; ++q) wr[q] = wc[q] = 0u;
@@ -391,25 +397,28 @@ __global__ void __launch_bounds__(256) slice_at_kernel(const T* __restrict__ A, 
         for (int q = 0; q < S; ++q) wr[q] = t[S - 1 - q];
       }
     }
-    if (rs)
+    if (rs) {
+      int8_t* d = rsp;
 #pragma unroll
-      for (int q = 0; q < S; ++q)
-        *reinterpret_cast<uint32_t*>(rs + static_cast<int64_t>(q) * n_pad * m_pad + j * m_pad + ib) = wr[q];
+      for (int q = 0; q < S; ++q, d += plane) *reinterpret_cast<uint32_t*>(d) = wr[q];
+      rsp += 8 * m_pad;
+    }
 #pragma unroll
     for (int q = 0; q < S; ++q) W[(q * kSliceTCols + cc) * 33 + lane] = wc[q];
   }
   __syncthreads();
   const int cq = threadIdx.x & 15;  // column quad: columns 4 cq .. 4 cq + 3 of the tile
   for (int rg = threadIdx.x >> 4; rg < kSliceTRows / 4; rg += 16) {
+    int8_t* dst = cs + (i0 + 4 * rg) * n_pad + j0 + 4 * cq;
 #pragma unroll
-    for (int q = 0; q < S; ++q) {
+    for (int q = 0; q < S; ++q, dst += plane) {
       uint32_t in[4], out[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) in[c] = W[(q * kSliceTCols + 4 * cq + c) * 33 + rg];
       transpose4(in, out);  // out[u]: row 4 rg + u, columns 4 cq .. 4 cq + 3
-      int8_t* dst = cs + static_cast<int64_t>(q) * m_pad * n_pad + (i0 + 4 * rg) * n_pad + j0 + 4 * cq;
+      int8_t* d = dst;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) *reinterpret_cast<uint32_t*>(dst + u * n_pad) = out[u];
+      for (int u = 0; u < 4; ++u, d += n_pad) *reinterpret_cast<uint32_t*>(d) = out[u];
     }
   }
 }
