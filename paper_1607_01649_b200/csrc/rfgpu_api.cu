@@ -515,7 +515,7 @@ Status pass_tn_raw(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Y, int64_t
     Timed t(c, "pass_tn");
     const bool pre = oz->thin_src == Y && oz->thin_cols == cols && !oz->a.shared;
     RF_CUDA(ozaki_tn(oz->a, Y, ldy, cols, Z, a->n, oz->work.p, c->stream, pre));
-    // Y's column-scaled digits stay in the work buffer (the lift may reuse them)
+    // Y's column-scaled digits stay in the work buffer
     oz->thin_src = oz->a.shared ? nullptr : Y;
     oz->thin_cols = cols;
     return {};
@@ -762,7 +762,7 @@ struct RangeOut {
 // R2ibuf (ell x ell) receive the basis; Bt (n x ell, ld n) receives
 // B^T = A^T Q (summed over ranks). power_range, rangefinder.cpp:63-80.
 Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, int64_t q, bool reorth,
-                  double* Qbuf, int64_t ldq, double* R2ibuf, double* Bt, RangeOut* out, OzPasses* ozp = nullptr) {
+                  double* Qbuf, int64_t ldq, double* R2ibuf, double* Bt, RangeOut* out) {
   cudaStream_t st = c->stream;
   const int64_t m = a->m, n = a->n;
   DBuf y, z, w, tmp, ssq, scal;
@@ -770,8 +770,7 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
   RF_TRY(z.alloc(sizeof(double) * n * ell, st));
   RF_TRY(w.alloc(sizeof(double) * n * ell, st));
   RF_TRY(tmp.alloc(sizeof(double) * n * ell, st));
-  OzPasses oz_local;
-  OzPasses& oz = ozp ? *ozp : oz_local;  // the caller may keep the digit buffers past the range finder (rsvd's lift)
+  OzPasses oz;
   RF_TRY(oz.init(c, a, ell));
   const int64_t slots = pass1_slots(c, a, ell, oz);
   RF_TRY(ssq.alloc(sizeof(double) * std::max<int64_t>(1, slots), st));
