@@ -515,9 +515,7 @@ Status pass_tn_raw(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Y, int64_t
     Timed t(c, "pass_tn");
     const bool pre = oz->thin_src == Y && oz->thin_cols == cols && !oz->a.shared;
     RF_CUDA(ozaki_tn(oz->a, Y, ldy, cols, Z, a->n, oz->work.p, c->stream, pre));
-    // Y's column-scaled digits stay in the work buffer
-    oz->thin_src = oz->a.shared ? nullptr : Y;
-    oz->thin_cols = cols;
+    oz->thin_src = nullptr;  // only orth's Gram hands digits to the pass right after it
     return {};
   }
   return gemm(c, true, a->n, cols, a->m, static_cast<const double*>(a->dev), a->lda, Y, ldy, Z, a->n, nullptr,
