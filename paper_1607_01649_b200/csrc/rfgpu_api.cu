@@ -855,7 +855,8 @@ Status check_sample(const rfgpu_matrix* a, int64_t k, int64_t ell, const char* w
 
 // rsvd on device buffers; U (ldu x ell), D (ell), V (n x ell). lowrank.cpp:74-96.
 Status rsvd_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t k, int64_t ell, int64_t q, bool keep_over,
-                 bool reorth, double* U, int64_t ldu, double* D, double* V, int64_t* rank_out) {
+                 bool reorth, double* U, int64_t ldu, double* D, double* V, int64_t* rank_out, double* Uhost = nullptr,
+                 int64_t ldh = 0) {
   cudaStream_t st = c->stream;
   const int64_t m = a->m, n = a->n;
   const int64_t ldq = even(m);
@@ -884,7 +885,46 @@ Status rsvd_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t k
     RF_TRY(gemm(c, false, r, keep, r, b.R2inv, r, Ub.d(), r, Ub2.d(), r));
     ub = Ub2.d();
   }
-  RF_TRY(gemm(c, false, m, keep, r, b.Q, b.ldq, ub, r, U, ldu, nullptr, "lift"));
+  if (Uhost && c->copy_stream && m >= 65536) {
+    // Lift in row panels and read each one back on the copy stream while the next is computed. All the
+    // GEMMs are queued before the first copy so a pageable destination (whose copy blocks the host)
+    // cannot serialise them.
+    constexpr int kPanels = 8;
+    const int64_t step = (m + kPanels * 128 - 1) / (kPanels * 128) * 128;  // keeps every panel base 16-byte aligned
+    cudaEvent_t ev[kPanels];
+    int np = 0;
+    for (int64_t r0 = 0; r0 < m; r0 += step, ++np) {
+      const int64_t rows = std::min(step, m - r0);
+      RF_TRY(gemm(c, false, rows, keep, r, b.Q + r0, b.ldq, ub, r, U + r0, ldu, nullptr, "lift"));
+      RF_CUDA(cudaEventCreateWithFlags(&ev[np], cudaEventDisableTiming));
+      RF_CUDA(cudaEventRecord(ev[np], st));
+    }
+    cudaError_t e = cudaSuccess;
+    for (int p = 0; p < np; ++p) {
+      const int64_t r0 = p * step, rows = std::min(step, m - r0);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c->copy_stream, ev[p], 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(Uhost + r0, sizeof(double) * ldh, U + r0, sizeof(double) * ldu, sizeof(double) * rows,
+                              keep, cudaMemcpyDeviceToHost, c->copy_stream);
+      cudaEventDestroy(ev[p]);
+    }
+    if (e == cudaSuccess) {
+      cudaEvent_t done;
+      e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+      if (e == cudaSuccess) {
+        e = cudaEventRecord(done, c->copy_stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, done, 0);
+        cudaEventDestroy(done);
+      }
+    }
+    RF_CUDA(e);
+  } else {
+    RF_TRY(gemm(c, false, m, keep, r, b.Q, b.ldq, ub, r, U, ldu, nullptr, "lift"));
+    if (Uhost) {
+      RF_CUDA(cudaMemcpy2DAsync(Uhost, sizeof(double) * ldh, U, sizeof(double) * ldu, sizeof(double) * m, keep,
+                                cudaMemcpyDeviceToHost, st));
+    }
+  }
   RF_CUDA(cudaMemcpyAsync(V, Vb.d(), sizeof(double) * n * keep, cudaMemcpyDeviceToDevice, st));
   RF_CUDA(cudaMemcpyAsync(D, Dd.d(), sizeof(double) * keep, cudaMemcpyDeviceToDevice, st));
   *rank_out = keep;
@@ -1668,12 +1708,12 @@ int rfgpu_rsvd_host(rfgpu_ctx* c, const double* a, int64_t m, int64_t n, int64_t
     RF_TRY(V.alloc(sizeof(double) * n * ell, st));
     RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
     int64_t r = 0;
-    Status cs = rsvd_core(c, &h, gd.d(), k, ell, q, keep_over != 0, reorth != 0, U.d(), ldu, D.d(), V.d(), &r);
+    Status cs = rsvd_core(c, &h, gd.d(), k, ell, q, keep_over != 0, reorth != 0, U.d(), ldu, D.d(), V.d(), &r,
+                          Uh, ldu);
     if (!cs.ok()) {
-      cudaStreamSynchronize(c->copy_stream);  // never leave a copy from the caller's buffer in flight
+      cudaStreamSynchronize(c->copy_stream);  // never leave a copy from or into the caller's buffers in flight
       return cs;
     }
-    RF_TRY(copy_out(c, Uh, ldu, U.d(), ldu, m, r));
     RF_TRY(copy_out(c, Dh, std::max<int64_t>(1, r), D.d(), std::max<int64_t>(1, r), r, 1));
     RF_TRY(copy_out(c, Vh, n, V.d(), n, n, r));
     RF_CUDA(cudaStreamSynchronize(st));
