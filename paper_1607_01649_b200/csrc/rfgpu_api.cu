@@ -893,13 +893,21 @@ Status rsvd_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t k
     const int64_t step = (m + kPanels * 128 - 1) / (kPanels * 128) * 128;  // keeps every panel base 16-byte aligned
     cudaEvent_t ev[kPanels];
     int np = 0;
-    for (int64_t r0 = 0; r0 < m; r0 += step, ++np) {
-      const int64_t rows = std::min(step, m - r0);
-      RF_TRY(gemm(c, false, rows, keep, r, b.Q + r0, b.ldq, ub, r, U + r0, ldu, nullptr, "lift"));
-      RF_CUDA(cudaEventCreateWithFlags(&ev[np], cudaEventDisableTiming));
-      RF_CUDA(cudaEventRecord(ev[np], st));
-    }
+    Status gs;
     cudaError_t e = cudaSuccess;
+    for (int64_t r0 = 0; r0 < m && gs.ok() && e == cudaSuccess; r0 += step) {
+      const int64_t rows = std::min(step, m - r0);
+      gs = gemm(c, false, rows, keep, r, b.Q + r0, b.ldq, ub, r, U + r0, ldu, nullptr, "lift");
+      if (gs.ok()) e = cudaEventCreateWithFlags(&ev[np], cudaEventDisableTiming);
+      if (gs.ok() && e == cudaSuccess) {
+        ++np;
+        e = cudaEventRecord(ev[np - 1], st);
+      }
+    }
+    if (!gs.ok()) {
+      for (int p = 0; p < np; ++p) cudaEventDestroy(ev[p]);
+      return gs;
+    }
     for (int p = 0; p < np; ++p) {
       const int64_t r0 = p * step, rows = std::min(step, m - r0);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(c->copy_stream, ev[p], 0);
