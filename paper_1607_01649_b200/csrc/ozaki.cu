@@ -423,9 +423,9 @@ __global__ void __launch_bounds__(256) slice_at_kernel(const T* __restrict__ A, 
   }
 }
 
-// slice_at_kernel for FP64 A with even lda and a 16-byte aligned base (the
-// usual case): the loads go through cp.async instead of registers, so each
-// lane has all 8 of its columns (8 x 32 B) in flight at once and a CTA 64 KB
+// slice_at_kernel for A whose columns start 16-byte aligned (the device
+// layout): the loads go through cp.async instead of registers, so each lane
+// has all 8 of its columns (8 x 32 B, FP32: 8 x 16 B) in flight at once and a CTA 64 KB
 // (the register-prefetch version above keeps 2 columns per warp in flight and
 // reaches ~5.2 TB/s on 94 GB). Lane l loads rows 4l..4l+3 of its warp's
 // columns into the tile's shared copy, one commit group per column, and
@@ -433,8 +433,8 @@ __global__ void __launch_bounds__(256) slice_at_kernel(const T* __restrict__ A, 
 // column, its column-scaled words overwrite that column's 1 KB of the copy
 // (word q * 33 + ((lane + cc) & 31): the skew keeps the transpose reads below
 // at most 2-way bank conflicted).
-template <int S>
-__global__ void __launch_bounds__(256) slice_at_async_kernel(const double* __restrict__ A, int64_t m, int64_t n,
+template <class T, int S>
+__global__ void __launch_bounds__(256) slice_at_async_kernel(const T* __restrict__ A, int64_t m, int64_t n,
                                                              int64_t lda, const int* __restrict__ rowexp,
                                                              const int* __restrict__ colexp_all, int64_t chunk_rows,
                                                              int64_t row_start, int8_t* __restrict__ rs,
@@ -447,21 +447,23 @@ __global__ void __launch_bounds__(256) slice_at_async_kernel(const double* __res
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ib = i0 + 4 * lane;
   const int64_t plane = m_pad * n_pad;
-  // bytes of this lane's 4 rows that exist (the rest is zero-filled)
-  const int valid = ib >= m ? 0 : (ib + 4 <= m ? 32 : static_cast<int>(m - ib) * 8);
+  // bytes of this lane's 4 rows that exist (the rest is zero-filled): 32 (FP64) or 16 (FP32)
+  constexpr int kLane = 4 * static_cast<int>(sizeof(T));
+  const int valid = ib >= m ? 0 : (ib + 4 <= m ? kLane : static_cast<int>(m - ib) * static_cast<int>(sizeof(T)));
   const int v0 = valid >= 16 ? 16 : valid, v1 = valid >= 16 ? valid - 16 : 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int cc = warp + 8 * i;
     const int64_t j = j0 + cc;
     const bool in = j < n;
-    const double* src = in ? A + j * lda + ib : A;
-    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(Ws + cc * 256 + 8 * lane));
+    const T* src = in ? A + j * lda + ib : A;
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(Ws + cc * 256 + (kLane / 4) * lane));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(in ? v0 : 0)
                  : "memory");
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst + 16), "l"(in && v0 == 16 ? src + 2 : src),
-                 "r"(in ? v1 : 0)
-                 : "memory");
+    if (kLane == 32)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst + 16),
+                   "l"(in && v0 == 16 ? src + 16 / sizeof(T) : src), "r"(in ? v1 : 0)
+                   : "memory");
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
   int er[4] = {0, 0, 0, 0};
@@ -484,9 +486,15 @@ __global__ void __launch_bounds__(256) slice_at_async_kernel(const double* __res
       default: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
     }
     uint32_t* col = Ws + cc * 256;
-    const double2 p0 = reinterpret_cast<const double2*>(col + 8 * lane)[0];
-    const double2 p1 = reinterpret_cast<const double2*>(col + 8 * lane)[1];
-    const double v[4] = {p0.x, p0.y, p1.x, p1.y};
+    double v[4];
+    if constexpr (sizeof(T) == 8) {
+      const double2 p0 = reinterpret_cast<const double2*>(col + 8 * lane)[0];
+      const double2 p1 = reinterpret_cast<const double2*>(col + 8 * lane)[1];
+      v[0] = p0.x, v[1] = p0.y, v[2] = p1.x, v[3] = p1.y;
+    } else {
+      const float4 p = reinterpret_cast<const float4*>(col + 4 * lane)[0];
+      v[0] = p.x, v[1] = p.y, v[2] = p.z, v[3] = p.w;
+    }
     __syncwarp();  // every lane has read the column before its words overwrite it
     uint32_t wr[S], wc[S];
 #pragma unroll
@@ -1292,22 +1300,21 @@ cudaError_t slice_sets_t(const T* A, int64_t lda, const OzakiA& a, bool rows, bo
       const char* v = std::getenv("RFGPU_OZAKI_SLICE_ASYNC");  // experiments: 0 = register-prefetch slicer
       return !(v && v[0] == '0');
     }();
-    if (sizeof(T) == 8 && async_ok && (lda & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
+    if (async_ok && (lda * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
       constexpr size_t smem_async = sizeof(uint32_t) * kSliceTCols * 256;
       static bool cfg_async = false;
       if (!cfg_async) {
-        for (auto fn : {slice_at_async_kernel<7>, slice_at_async_kernel<4>}) {
+        for (auto fn : {slice_at_async_kernel<T, 7>, slice_at_async_kernel<T, 4>}) {
           cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_async);
           if (e != cudaSuccess) return e;
         }
         cfg_async = true;
       }
-      const double* Ad = reinterpret_cast<const double*>(A);
       if (a.digits == 4)
-        slice_at_async_kernel<4><<<grid, 256, smem_async, st>>>(Ad, a.m, a.n, lda, a.rowexp, a.colexp, a.chunk_rows,
+        slice_at_async_kernel<T, 4><<<grid, 256, smem_async, st>>>(A, a.m, a.n, lda, a.rowexp, a.colexp, a.chunk_rows,
                                                                 r0, rows ? a.rs : nullptr, a.cs, a.m_pad, a.n_pad);
       else
-        slice_at_async_kernel<7><<<grid, 256, smem_async, st>>>(Ad, a.m, a.n, lda, a.rowexp, a.colexp, a.chunk_rows,
+        slice_at_async_kernel<T, 7><<<grid, 256, smem_async, st>>>(A, a.m, a.n, lda, a.rowexp, a.colexp, a.chunk_rows,
                                                                 r0, rows ? a.rs : nullptr, a.cs, a.m_pad, a.n_pad);
       count_launch();
       return cudaGetLastError();
