@@ -58,7 +58,10 @@ int64_t tn_split_k() {
   k = std::max<int64_t>(256, std::min<int64_t>(kSplitK, k));
   return k / 256 * 256;
 }
-constexpr int kThreads = 192;
+// warp 0 TMA producer, warp 1 MMA issuer, warps 2..9 epilogue (two warps per
+// TMEM lane quarter, alternating 16-column chunks)
+constexpr int kThreads = 320;
+constexpr int kEpiWarps = kThreads / 32 - 2;
 // One digit set may serve both passes when the non-zero columns' exponents
 // span at most this many bits (ozaki_col_exponents): A^T Q on the row-scaled
 // digits then loses at most kSharedSpread + 2 bits against column-scaled
@@ -758,7 +761,7 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
       mbar_init(&empty[s], cl);  // every CTA of the cluster must release the (shared) A stage
     }
     mbar_init(done, 1);
-    mbar_init(tfree, 4);  // the four epilogue warps
+    mbar_init(tfree, kEpiWarps);
     mbar_fence_init();
   }
   if (warp == 1) {
@@ -864,7 +867,9 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
                    : "memory");
     }
   } else if (warp >= 2) {
-    const int q = warp & 3;  // TMEM lane quarter of this warp
+    const int q = warp & 3;              // TMEM lane quarter of this warp
+    const int half = (warp - 2) >> 2;    // its 16-column chunks: half, half + 2, ...
+    constexpr int kHalves = kEpiWarps / 4;
     uint32_t tt = 0;
     for (int64_t g = cid; g < p.ngroups; g += ncl, ++tt) {
       const TileCoord tc = tile_coord(p, g * cl + crank);
@@ -874,7 +879,11 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
       const int64_t orow = p.c_row0 + (lrow - p.row0);
       const int rex = (p.rowexp && tc.nk > 0) ? p.rowexp[tc.split * p.rex_stride + lrow] : 0;
       const bool row_ok = orow < p.M_real + p.c_row0 && lrow - p.row0 < p.M_real;
-      for (int c = 0; c < tc.w; c += 16) {
+      if (half * 16 >= tc.w) {  // no chunk for this warp in a narrow tile
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tfree);
+      }
+      for (int c = half * 16; c < tc.w; c += 16 * kHalves) {
         uint32_t r[kS][16];
         if (tc.nk > 0) {
 #pragma unroll
@@ -889,20 +898,30 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         }
-        if (c + 16 == tc.w) {  // every TMEM column of this tile is in registers: release it
+        if (c + 16 * kHalves >= tc.w) {  // this warp's last chunk is in registers: release its share of TMEM
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(tfree);
         }
+        // sum_g acc_g 2^-(12+8g) = 2^-36 (hi + 2^-24 lo), hi = sum_{g<4} acc_g 256^(3-g) and
+        // lo = sum_{g>=4} acc_g 256^(6-g) exact in int64 (|acc_g| < 2^31): two conversions, not seven
         double acc[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = 0.0;
         if (tc.nk > 0) {
 #pragma unroll
-          for (int gg = kS - 1; gg >= 0; --gg) {
-            const double sc = ldexp(1.0, -12 - 8 * gg);
+          for (int j = 0; j < 16; ++j) {
+            int64_t hi = static_cast<int32_t>(r[0][j]);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] = fma(static_cast<double>(static_cast<int32_t>(r[gg][j])), sc, acc[j]);
+            for (int gg = 1; gg < 4 && gg < kS; ++gg) hi = hi * 256 + static_cast<int32_t>(r[gg][j]);
+            double d = static_cast<double>(hi);
+            if constexpr (kS > 4) {
+              int64_t lo = static_cast<int32_t>(r[4][j]);
+#pragma unroll
+              for (int gg = 5; gg < kS; ++gg) lo = lo * 256 + static_cast<int32_t>(r[gg][j]);
+              d = fma(static_cast<double>(lo), 0x1p-24, d);
+            }
+            acc[j] = d;
           }
         }
         if (row_ok) {
@@ -910,7 +929,7 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
           for (int j = 0; j < 16; ++j) {
             const int64_t col = tc.ncol0 + c + j;
             if (col < p.N_real) {
-              const double v = ldexp(acc[j], rex + p.colexp[col] + p.cshift);
+              const double v = ldexp(acc[j], rex + p.colexp[col] + p.cshift - 36);
               if (p.ws_mode)
                 p.C[(static_cast<int64_t>(tc.split) * p.N_real + col) * p.M_real + (lrow - p.row0)] = v;
               else
