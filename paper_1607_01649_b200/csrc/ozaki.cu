@@ -641,7 +641,8 @@ struct OzParams {
   int ws_mode;        // 1: C is [split][N_real][M_real]
   int cl;             // cluster size along N tiles: the A tile is TMA-multicast to all of them
   int64_t ngroups;    // tile groups (all tiles / cl); the grid may be smaller (persistent)
-  int last_w;         // width of the last n-tile (multiple of 16, <= OBN): l's padding is not multiplied
+  int w_big, n_big;   // the first n_big n-tiles are w_big wide, the rest w_small (multiples of 16, <= OBN):
+  int w_small;        // l's padding is not multiplied, and the tiles sharing an A tile stay close in speed
   int64_t rex_stride;      // rowexp is [split][rex_stride] (per K-chunk output-row exponents; 0: one vector)
   int tma3;                // 1: one 3-D TMA copy per operand and stage (no multicast)
   int64_t kb_split_fixed;  // K blocks per split when it must match the chunks (0: even split)
@@ -712,7 +713,7 @@ __device__ __forceinline__ uint64_t umma_desc_mn(const void* p) {
 struct TileCoord {
   int64_t lrow0, ncol0, kb0;
   int nk, split;
-  int w;  // tile width: OBN, or p.last_w for the last n-tile (l not a multiple of 64)
+  int w;  // tile width: p.w_big or p.w_small
 };
 
 __device__ __forceinline__ TileCoord tile_coord(const OzParams& p, int64_t tile) {
@@ -723,8 +724,9 @@ __device__ __forceinline__ TileCoord tile_coord(const OzParams& p, int64_t tile)
   const int mt = static_cast<int>(rest % p.mtn);
   t.split = static_cast<int>(rest / p.mtn);
   t.lrow0 = p.row0 + static_cast<int64_t>(mt) * OBM;
-  t.ncol0 = static_cast<int64_t>(nt) * OBN;
-  t.w = nt == p.ntn - 1 ? p.last_w : OBN;
+  t.w = nt < p.n_big ? p.w_big : p.w_small;
+  t.ncol0 = nt < p.n_big ? static_cast<int64_t>(nt) * p.w_big
+                         : static_cast<int64_t>(p.n_big) * p.w_big + static_cast<int64_t>(nt - p.n_big) * p.w_small;
   t.kb0 = t.split * p.kb_per_split;
   const int64_t kb1 = min(p.kb_total, t.kb0 + p.kb_per_split);
   t.nk = static_cast<int>(kb1 - t.kb0);
@@ -787,13 +789,13 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
         const uint32_t ph = (it / kStages) & 1;
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(ASZ + kS * tc.w * BK));
-        const CUtensorMap* tr = tc.w == OBN ? &tmR : &tmR2;  // the narrow last tile: box of w rows
+        const CUtensorMap* tr = tc.w == p.w_big ? &tmR : &tmR2;  // box of w rows
         const int kx = static_cast<int>((tc.kb0 + kb) * BK);
         if (p.tma3) {  // all digit planes of each operand tile in one 3-D copy (2 TMA issues per stage)
           const int lc0 = L_MN ? static_cast<int>(tc.lrow0) : kx;
           const int lc1 = L_MN ? static_cast<int>((tc.kb0 + kb) * BK) : static_cast<int>(tc.lrow0);
           tma3d(sA + st * ASZ, &tmL3, &full[st], lc0, lc1, 0);
-          tma3d(sB + st * BSZ, tc.w == OBN ? &tmR3 : &tmR23, &full[st], kx, static_cast<int>(tc.ncol0), 0);
+          tma3d(sB + st * BSZ, tc.w == p.w_big ? &tmR3 : &tmR23, &full[st], kx, static_cast<int>(tc.ncol0), 0);
           continue;
         }
 #pragma unroll
@@ -1035,22 +1037,37 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   CUtensorMap tl, tr;
   const bool okl = L_mn ? digit_tmap(&tl, L, kS * L_rows, L_M, OBM, BK, CU_TENSOR_MAP_SWIZZLE_128B)
                         : digit_tmap(&tl, L, kS * L_rows, K_pad, BK, OBM, kSwK);
-  if (!okl || !digit_tmap(&tr, R, kS * R_rows, K_pad, BK, OBN, kSwK)) return cudaErrorInvalidValue;
-  // the last n-tile spans only roundup(N_real - 64 (ntn - 1), 16) columns
+  if (!okl) return cudaErrorInvalidValue;
+  // n-tile widths: roundup(N_real, 16) split over the ntn tiles as evenly as 16-column units allow
+  // (l = 220: 64 64 48 48); RFGPU_OZAKI_NARROW=0 pads every tile to 64, =1 keeps 64 ... 64 + a narrow last
   const int ntn = static_cast<int>(R_rows / OBN);
-  int last_w = static_cast<int>(roundup(std::max<int64_t>(1, N_real - static_cast<int64_t>(ntn - 1) * OBN), 16));
-  const char* nw = std::getenv("RFGPU_OZAKI_NARROW");  // experiments: 0 pads the last tile to 64 columns
-  if (last_w > OBN || (nw && nw[0] == '0')) last_w = OBN;
-  CUtensorMap tr2 = tr;
-  if (last_w < OBN && !digit_tmap(&tr2, R, kS * R_rows, K_pad, BK, last_w, kSwK)) return cudaErrorInvalidValue;
+  const int units = static_cast<int>(std::min<int64_t>(4 * ntn, std::max<int64_t>(1, (N_real + 15) / 16)));
+  int w_big, n_big, w_small;
+  const char* nw = std::getenv("RFGPU_OZAKI_NARROW");
+  if (nw && nw[0] == '0') {
+    w_big = w_small = OBN, n_big = ntn;
+  } else if (nw && nw[0] == '1') {
+    w_big = OBN, n_big = ntn - 1, w_small = 16 * (units - 4 * (ntn - 1));
+  } else {
+    const int q = units / ntn, r = units % ntn;
+    w_small = 16 * q;
+    w_big = r ? 16 * (q + 1) : 16 * q;
+    n_big = r ? r : ntn;
+  }
+  if (w_small <= 0) w_small = w_big;
+  CUtensorMap tr2;
+  if (!digit_tmap(&tr, R, kS * R_rows, K_pad, BK, w_big, kSwK)) return cudaErrorInvalidValue;
+  tr2 = tr;
+  if (w_small != w_big && !digit_tmap(&tr2, R, kS * R_rows, K_pad, BK, w_small, kSwK)) return cudaErrorInvalidValue;
   CUtensorMap tl3 = tl, tr3 = tr, tr23 = tr2;
   const char* t3e = std::getenv("RFGPU_OZAKI_TMA3");
   bool tma3 = !(t3e && t3e[0] == '0');
   if (tma3) {
     tma3 = (L_mn ? digit_tmap3(&tl3, L, kS, L_rows, L_M, OBM, BK, CU_TENSOR_MAP_SWIZZLE_128B)
                  : digit_tmap3(&tl3, L, kS, L_rows, K_pad, BK, OBM, kSwK)) &&
-           digit_tmap3(&tr3, R, kS, R_rows, K_pad, BK, OBN, kSwK) &&
-           (last_w == OBN || digit_tmap3(&tr23, R, kS, R_rows, K_pad, BK, last_w, kSwK));
+           digit_tmap3(&tr3, R, kS, R_rows, K_pad, BK, w_big, kSwK) &&
+           (w_small == w_big || digit_tmap3(&tr23, R, kS, R_rows, K_pad, BK, w_small, kSwK));
+    if (w_small == w_big) tr23 = tr3;
   }
   OzParams p = base;
   p.L_rows = L_rows;
@@ -1064,7 +1081,9 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   }
   p.splits = splits;
   p.ntn = ntn;
-  p.last_w = last_w;
+  p.w_big = w_big;
+  p.n_big = n_big;
+  p.w_small = w_small;
   p.mtn = static_cast<int>((rows + OBM - 1) / OBM);
   p.row0 = row0;
   p.M_real = rows;
