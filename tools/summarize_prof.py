@@ -22,7 +22,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OURS = ("gemm_f64", "jacobi_svd", "chol_inv", "trinv_upper", "cpqr", "reduce_splits", "symmetrize", "sumsq",
         "sum_array", "transpose", "gather_", "lsq_scale", "gs_", "add_inplace", "sylvester", "f32_to_f64",
         "scale_", "copy_", "fill_", "ozaki_gemm", "stats_kernel", "slice_a_kernel", "slice_r_kernel", "colexp_kernel",
-        "col_exp_kernel", "rowexp_kernel", "reduce_ws_kernel", "chol_kernel", "trinv_smem", "slice_at_kernel",
+        "col_exp_kernel", "rowexp_kernel", "reduce_ws_kernel", "chol_kernel", "trinv_smem", "slice_at_kernel", "slice_at_async",
         "colexp_fix", "cholb_", "rfgpu")
 
 
