@@ -87,6 +87,24 @@ def test_power_range_matches_oracle(ctx, port):
         assert abs(got.residual_frob - want.residual_frob) <= 1e-6 * np.linalg.norm(a)
 
 
+@pytest.mark.parametrize("ell", [1, 2, 3, 33, 97, 220, 235, 236, 237])
+def test_power_range_all_sketch_widths(ctx, port, ell):
+    """CholeskyQR2 at every sketch-width class: the single-CTA Cholesky (odd
+    and even widths, one and several rows per lane, up to the largest width
+    whose packed triangle fits in shared memory, 236) and the blocked one just
+    above it. Q must be orthonormal and span the oracle's."""
+    p = min(5, ell - 1)
+    k = ell - p
+    sig = 0.97 ** np.arange(300, dtype=np.float64)
+    a = planted(port, 1200, 300, sig, seed=ell)
+    want = port.power_range(a, k, p, 0, 3, reorth=True)
+    got = rf.power_range(a, k, p, 0, 3, reorthonormalize=True, ctx=ctx)
+    assert got.Q.shape == want.Q.shape == (1200, ell)
+    assert np.abs(got.Q.T @ got.Q - np.eye(ell)).max() < 1e-12
+    s = np.linalg.svd(want.Q.T @ got.Q, compute_uv=False)
+    assert np.abs(s - 1).max() < 1e-8
+
+
 def test_basic_range_tracks_residual(ctx):
     # test_rangefinder.cpp:43-71
     sig = geometric(12, 0.5)
