@@ -26,6 +26,7 @@ workload on all host cores and extrapolates linearly in m.
 from __future__ import annotations
 
 import argparse
+import datetime
 import ctypes as C
 import json
 import os
@@ -124,19 +125,39 @@ def gen_shard(torch, dist, w, row0, row1, dev):
 
 # ------------------------------------------------------------------ clocks ---
 class ClockSampler:
-    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+    """nvidia-smi clocks / power / throttle reasons every 200 ms. Started before
+    the warm-up (nvidia-smi's own start-up takes driver locks that stall the
+    host-synchronising steps of the first timed iterations on a fresh box);
+    mark() opens the timed window and stop() keeps the samples taken inside it
+    (the last warm-up sample too when the window is shorter than one period)."""
+    FIELDS = ["timestamp", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
 
     def __init__(self, device):
         self.path = tempfile.mktemp(suffix=".csv")
         self.proc = None
+        self.t0 = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(device), "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits",
                  "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+
+    def settle(self, timeout=5.0):
+        """Wait for the first sample (nvidia-smi initialised) before anything is timed."""
+        end = time.time() + timeout
+        while self.proc is not None and time.time() < end:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    return
+            except OSError:
+                pass
+            time.sleep(0.05)
+
+    def mark(self):
+        self.t0 = datetime.datetime.now()
 
     def stop(self):
         if self.proc is None:
@@ -146,22 +167,24 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, mx, reasons, pw = [], [], set(), []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for line in open(self.path):
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 7:
+            if len(parts) < 8:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-                pw.append(float(parts[2]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f")
+                rows.append((ts, float(parts[1]), float(parts[2]), float(parts[3]), parts[4:8]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
         os.unlink(self.path)
+        if self.t0 is not None:
+            inside = [r for r in rows if r[0] >= self.t0]
+            before = [r for r in rows if r[0] < self.t0]
+            rows = inside if len(inside) >= 2 else before[-1:] + inside
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = {nm for r in rows for nm, v in zip(names, r[4]) if v.lower().startswith("active")}
+        sm, mx, pw = [r[1] for r in rows], [r[2] for r in rows], [r[3] for r in rows]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
 
@@ -322,6 +345,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    sampler = ClockSampler(local)
+    sampler.settle()
     for _ in range(max(3, args.warmup)):
         step()
     ctx.synchronize()
@@ -330,7 +355,7 @@ def main():
     ctx.profile(True)
     ctx.profile_reset()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local)
+    sampler.mark()
     ev0.record(stream)
     for _ in range(args.steps):
         step()
