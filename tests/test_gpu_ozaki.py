@@ -145,15 +145,18 @@ def test_streamed_panels_on_digit_gemm(ctx, ozaki, monkeypatch):
     assert np.max(np.abs(host.D - dev.D) / dev.D) < 1e-12
 
 
+@pytest.mark.parametrize("m", [1500, 1501])
 @pytest.mark.parametrize("f32", [False, True])
-def test_single_pass_device_on_digit_gemm(ctx, port, ozaki, f32):
+def test_single_pass_device_on_digit_gemm(ctx, port, ozaki, f32, m):
     """rfgpu_single_pass_svd_device with both sketches on the digit path:
     FP64 data (7 digits) within 1e-8 of the restated oracle, FP32 data (4
     digits, 10 products) within the FP32 bar 1e-4 of the oracle run on the
-    same rounded data."""
+    same rounded data. m = 1501 gives columns that do not start 16-byte
+    aligned, so A is sliced by the register-prefetch slicer instead of the
+    cp.async one."""
     import ctypes as C
     import torch
-    m, n, k, p = 1500, 1200, 60, 10
+    n, k, p = 1200, 60, 10
     ell = k + p
     a = planted(port, m, n, np.exp(-np.arange(1, 201) / 10.0), seed=1, noise=1e-4)
     if f32:
