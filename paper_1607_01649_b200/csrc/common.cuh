@@ -1,5 +1,6 @@
 // Shared device helpers for the rfgpu kernels (sm_100a only).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -8,6 +9,21 @@
 #endif
 
 namespace rfgpu {
+
+// Kernel attributes (dynamic shared memory, cluster sizes) belong to one
+// device's context: a per-call-site bit per device records which devices a
+// cudaFuncSetAttribute block has already run on (one process may drive
+// several GPUs through several contexts).
+inline bool attr_pending(const std::atomic<uint64_t>& mask) {
+  int d = 0;
+  cudaGetDevice(&d);
+  return ((mask.load(std::memory_order_acquire) >> (d & 63)) & 1u) == 0;
+}
+inline void attr_done(std::atomic<uint64_t>& mask) {
+  int d = 0;
+  cudaGetDevice(&d);
+  mask.fetch_or(uint64_t(1) << (d & 63), std::memory_order_release);
+}
 
 // 16-byte async global->shared copy with zero fill of the (16 - src_bytes)
 // tail; src_bytes == 0 writes zeros without touching global memory.

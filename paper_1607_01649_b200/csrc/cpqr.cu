@@ -566,11 +566,11 @@ cudaError_t trinv_upper(const double* R, int64_t ldr, int k, double* Rinv, cudaS
   const int nb = (k + kTB - 1) / kTB;
   const size_t smem = sizeof(double) * nb * kTB * (kTB + 1);
   if (k > 64 && smem <= 200 * 1024) {
-    static bool cfg = false;
-    if (!cfg) {
+    static std::atomic<uint64_t> cfg{0};
+    if (attr_pending(cfg)) {
       cudaError_t e = cudaFuncSetAttribute(trinv_blockcol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
-      cfg = true;
+      attr_done(cfg);
     }
     double* dinv = nullptr;
     cudaError_t e = cudaMallocAsync(&dinv, sizeof(double) * nb * kTB * kTB, st);

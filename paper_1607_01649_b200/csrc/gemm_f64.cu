@@ -562,11 +562,11 @@ template <bool TRANS, int NT, bool V16>
 cudaError_t launch_one(const GemmParams& g, int64_t grid, cudaStream_t st) {
   auto kern = gemm_f64_kernel<TRANS, NT, V16>;
   constexpr size_t smem = smem_bytes<TRANS, NT>();
-  static bool configured = false;  // per-instantiation, per-process (device 0 properties apply to all B200s)
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  if (attr_pending(configured)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    configured = true;
+    attr_done(configured);
   }
   kern<<<static_cast<unsigned>(grid), NTHREADS, smem, st>>>(g);
   count_launch();
@@ -578,11 +578,11 @@ cudaError_t launch_tma(const GemmParams& g, const CUtensorMap& ta, const CUtenso
                        cudaStream_t st) {
   auto kern = gemm_f64_tma_kernel<TRANS, NT>;
   constexpr size_t smem = smem_bytes_ws<TRANS, NT>();
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  if (attr_pending(configured)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    configured = true;
+    attr_done(configured);
   }
   kern<<<static_cast<unsigned>(grid), WS_THREADS, smem, st>>>(g, ta, tb);
   count_launch();

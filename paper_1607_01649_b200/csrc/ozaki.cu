@@ -1026,13 +1026,13 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   constexpr int kS = S;
   constexpr size_t kSmemBytes = Dig<S, BK>::smem;
   constexpr CUtensorMapSwizzle kSwK = BK == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
-  static bool cfg = false;
-  if (!cfg) {
+  static std::atomic<uint64_t> cfg{0};
+  if (attr_pending(cfg)) {
     for (auto fn : {ozaki_gemm_kernel<true, S, BK>, ozaki_gemm_kernel<false, S, BK>}) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
       if (e != cudaSuccess) return e;
     }
-    cfg = true;
+    attr_done(cfg);
   }
   CUtensorMap tl, tr;
   const bool okl = L_mn ? digit_tmap(&tl, L, kS * L_rows, L_M, OBM, BK, CU_TENSOR_MAP_SWIZZLE_128B)
@@ -1323,14 +1323,14 @@ cudaError_t slice_sets_t(const T* A, int64_t lda, const OzakiA& a, bool rows, bo
                          cudaStream_t st) {
   if (cols && a.cs_rowmajor) {
     const size_t smem = sizeof(uint32_t) * a.digits * kSliceTCols * 33;
-    static bool cfg = false;
-    if (!cfg) {
+    static std::atomic<uint64_t> cfg{0};
+    if (attr_pending(cfg)) {
       for (auto fn : {slice_at_kernel<T, 7>, slice_at_kernel<T, 4>}) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(sizeof(uint32_t) * 7 * kSliceTCols * 33));
         if (e != cudaSuccess) return e;
       }
-      cfg = true;
+      attr_done(cfg);
     }
     if (r1 <= r0) return cudaSuccess;
     const unsigned grid = static_cast<unsigned>(((r1 - r0) / kSliceTRows) * (a.n_pad / kSliceTCols));
@@ -1340,13 +1340,13 @@ cudaError_t slice_sets_t(const T* A, int64_t lda, const OzakiA& a, bool rows, bo
     }();
     if (async_ok && (lda * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
       constexpr size_t smem_async = sizeof(uint32_t) * kSliceTCols * 256;
-      static bool cfg_async = false;
-      if (!cfg_async) {
+      static std::atomic<uint64_t> cfg_async{0};
+      if (attr_pending(cfg_async)) {
         for (auto fn : {slice_at_async_kernel<T, 7>, slice_at_async_kernel<T, 4>}) {
           cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_async);
           if (e != cudaSuccess) return e;
         }
-        cfg_async = true;
+        attr_done(cfg_async);
       }
       if (a.digits == 4)
         slice_at_async_kernel<T, 4><<<grid, 256, smem_async, st>>>(A, a.m, a.n, lda, a.rowexp, a.colexp, a.chunk_rows,

@@ -1050,13 +1050,13 @@ cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double
   const size_t smem = chol_smem_bytes(c);
   const int ci = static_cast<int>(c);
   if (smem <= 224 * 1024 && c <= 256) {
-    static bool cfg = false;
-    if (!cfg) {
+    static std::atomic<uint64_t> cfg{0};
+    if (attr_pending(cfg)) {
       for (const void* fn : {reinterpret_cast<const void*>(chol_kernel), reinterpret_cast<const void*>(trinv_smem_kernel<8>)}) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
         if (e != cudaSuccess) return e;
       }
-      cfg = true;
+      attr_done(cfg);
     }
     double* rdiag = work;  // c doubles
     chol_kernel<<<1, kSmallThreads, smem, st>>>(G, ci, R, rdiag, info, info_d);
@@ -1089,8 +1089,8 @@ cudaError_t bjacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64
                      pr[i].sweeps};
   }
   if (count == 1) ps[1] = ps[0];
-  static bool cfg_done = false;
-  if (!cfg_done) {
+  static std::atomic<uint64_t> cfg_done{0};
+  if (attr_pending(cfg_done)) {
     for (const void* fn : {reinterpret_cast<const void*>(bjacobi_kernel<8>), reinterpret_cast<const void*>(bjacobi_kernel<12>),
                            reinterpret_cast<const void*>(bjacobi_kernel<16>)}) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -1098,7 +1098,7 @@ cudaError_t bjacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
-    cfg_done = true;
+    attr_done(cfg_done);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(B.P * count);
