@@ -80,7 +80,7 @@ def ncu_full(rnd, wl):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
-    out, best = [], None
+    out, best, passes = [], None, []
     for r in rows[2:]:
         d = {"kernel": short(r[hdr.index("Kernel Name")])}
         for m in METRICS:
@@ -94,6 +94,10 @@ def ncu_full(rnd, wl):
             t = float(r[hdr.index("dram__bytes_read.sum")].replace(",", "")) * (1e9 if "Gbyte" in units[hdr.index("dram__bytes_read.sum")] else 1)
             wb = float(r[hdr.index("dram__bytes_write.sum")].replace(",", "")) * (1e9 if "Gbyte" in units[hdr.index("dram__bytes_write.sum")] else 1)
             dur = float(r[hdr.index("gpu__time_duration.sum")].replace(",", ""))
+            tu = units[hdr.index("gpu__time_duration.sum")]
+            dur_ms = dur * {"ms": 1.0, "msecond": 1.0, "us": 1e-3, "usecond": 1e-3, "ns": 1e-6, "nsecond": 1e-6}.get(tu, 1.0)
+            grid = r[hdr.index("launch__grid_size")] if "launch__grid_size" in hdr else ""
+            passes.append((dur_ms, t + wb, d["kernel"], grid))
             if best is None or dur > best[0]:
                 best = (dur, t + wb, d["kernel"])
         except (ValueError, IndexError):
@@ -109,9 +113,14 @@ def ncu_full(rnd, wl):
                 cur = {}
         except Exception:
             cur = {}
-        cur[wl] = {"kernel": best[2], "traffic_bytes": best[1],
+        # the passes over A (M-major digit GEMM launches: A X and A^T Q); bench.py's roofline.achieved is an
+        # average over the step's passes, so the traffic figure is the mean over the captured pass launches
+        pl = [x for x in passes if "ozaki_gemm_kernel<1" in x[2]] or passes
+        cur[wl] = {"kernel": best[2], "traffic_bytes": sum(x[1] for x in pl) / len(pl),
+                   "per_launch": [{"grid": x[3], "ms": x[0], "dram_bytes": x[1]} for x in pl],
                    "source": f"ncu --set full, profiles/{rnd}_ncu_top_kernels_{wl}.jsonl",
-                   "note": "dram__bytes_read.sum + dram__bytes_write.sum of the longest captured pass launch"}
+                   "note": "mean of dram__bytes_read.sum + dram__bytes_write.sum over the captured pass launches "
+                           "(A X and A^T Q)"}
         json.dump(cur, open(path, "w"), indent=1)
     for d in out:
         print(d)
