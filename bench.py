@@ -369,7 +369,7 @@ def main():
     launches = ctx.launch_count() // args.steps
     prof = {nm: ctx.profile_read(nm) for nm in ("pass_nn", "pass_tn", "ozaki_slice", "sketch_nn", "sketch_tn", "orth", "small_svd",
                                                 "jacobi", "gram", "chol", "trsm", "lift", "stats", "slicer", "col_id", "cpqr", "trsm_id",
-                                                "single_pass_core", "gemm_nn", "gemm_tn", "allreduce")}
+                                                "single_pass_core", "gemm_nn", "gemm_tn", "allreduce", "sp_total", "sp_alloc")}
     ctx.profile(False)
     pass_names = ("sketch_nn", "sketch_tn") if kind == "single_pass" else ("pass_nn", "pass_tn")
     if kind == "single_pass" and prof["sketch_nn"][0] == 0:  # the dual sketch ran on the digit path

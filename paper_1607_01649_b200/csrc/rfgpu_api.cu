@@ -2155,21 +2155,29 @@ int rfgpu_single_pass_svd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const doub
     // row-sharded A: gr is the FULL m_global x ell Gr; this rank uses its rows
     const int64_t m = a->m, n = a->n, ldgr = a->m_global;
     gr += a->row0;
+    Timed tt(c, "sp_total");
+    // The digit planes are allocated first and held to the end of the call,
+    // as in rsvd: released before the core, their pool block was carved up by
+    // the core's temporaries and the next call's 34 GB request (config 4)
+    // grew the pool again (22-118 ms per call outside every kernel).
+    OzPasses oz;  // both sketches on the INT8 tensor cores at pass sizes (FP32 data: 4 digits)
     DBuf yc, yr, scratch, conv;
-    RF_TRY(yc.alloc(sizeof(double) * m * ell, s));
-    RF_TRY(yr.alloc(sizeof(double) * n * ell, s));
-    RF_TRY(scratch.alloc(sizeof(double) * m * ell, s));
     bool on_digits = false;
     {
-      OzPasses oz;  // both sketches on the INT8 tensor cores at pass sizes (FP32 data: 4 digits)
-      RF_TRY(oz.init(c, a, ell));
+      {
+        Timed ta(c, "sp_alloc");
+        RF_TRY(oz.init(c, a, ell));
+        RF_TRY(yc.alloc(sizeof(double) * m * ell, s));
+        RF_TRY(yr.alloc(sizeof(double) * n * ell, s));
+        RF_TRY(scratch.alloc(sizeof(double) * m * ell, s));
+      }
       if (oz.on) {
         RF_TRY(oz.prepare(c, a, nullptr, true));
         RF_TRY(pass_nn(c, a, gc, ell, yc.d(), m, &oz));                       // Yc = A Gc
         RF_TRY(pass_tn_raw(c, a, gr, ldgr, ell, yr.d(), &oz));                // Yr = A^T Gr
         on_digits = true;
       }
-    }  // digit planes released before the core
+    }
     if (!on_digits) {
       Timed t(c, "dual_sketch");
       if (!a->f32) {
