@@ -4,13 +4,14 @@
 Workload (BASELINE.json configs[2], the 1/2/4/8-GPU tall-matrix config the
 metric is quoted on): A = U_r diag(s) V_r^T + 1e-8 N, m = 1,048,576,
 n = 4096, r = 1024, s_j = j^-1.5, U_r / V_r orthonormal Q factors of seeded
-Gaussians, N i.i.d. Gaussian; rsvd(A, k=200, p=20, q=1, reorthonormalize=true)
-with G = gaussian(1, "range.G", n, 220) from the reference generator. A is
-row-sharded over the ranks (strong scaling: the matrix is fixed, N GPUs share
-its rows); the only collectives are NCCL allreduces of the n x l products and
-the l x l Grams. Synthetic data generated on the device (seeded torch RNG per
-64Ki-row chunk, so every N sees the same A); A (34.4 GB) is larger than L2, so
-no flush is needed between steps.
+Gaussians (the reference recipe planted_matrix, diagnostics.cpp:124-136, built
+row block by row block by paper_1607_01649_b200/planted.py from the
+reference's own Gaussian stream), N = gaussian(1, "noise.N", m, n);
+rsvd(A, k=200, p=20, q=1, reorthonormalize=true) with G = gaussian(1,
+"range.G", n, 220) from the reference generator. A is row-sharded over the
+ranks (strong scaling: the matrix is fixed, N GPUs share its rows); the only
+collectives are allreduces of the n x l products and the l x l Grams. A (34.4
+GB) is larger than L2, so no flush is needed between steps.
 
 `value` = device-resident time per rsvd call (A, G already in HBM; CUDA
 events on the library's stream; max over ranks). `e2e` = the same call made
@@ -19,9 +20,16 @@ drop-in rsvd(const DenseMatrix&) makes): A streamed from pinned memory in row
 panels overlapped with the first pass, and the D2H of U, D, V, all inside the
 timed region.
 
+After the timed region the run checks its own output (`parity`): the
+singular values against the golden values of the full-size oracle run
+(tests/golden/config_golden.json, from tools/parity_c3_full.py) and against
+the same call with the passes forced onto FP64 DMMA (RFGPU_OZAKI=0).
+
 --impl reference runs the reference's own CPU implementation (oracle/_ref,
-compiled from /root/reference/proj/src) on a bounded row sample of the same
-workload on all host cores and extrapolates linearly in m.
+compiled from /root/reference/proj/src) on all host cores on row samples of
+the workload at two row counts; only the part that grows with m is
+extrapolated (t(m) = a + b m fitted to the two measured points), at 16
+threads and at the reference's default of 8 (dense.cpp:69-94).
 """
 from __future__ import annotations
 
@@ -63,18 +71,8 @@ OZAKI_PRODUCTS_F32 = 10  # FP32 data: 4 digits, s + t <= 3
 
 
 def spectrum(kind, r):
-    j = np.arange(1, r + 1, dtype=np.float64)
-    if kind == "pow1.5":
-        return j ** -1.5
-    if kind == "exp20":
-        return np.exp(-j / 20.0)
-    if kind == "pow2":
-        return 1.0 / j ** 2
-    if kind == "exp100":
-        return np.exp(-j / 100.0)
-    if kind == "decade6":
-        return 10.0 ** (-6.0 * (j - 1) / (r - 1))
-    raise ValueError(kind)
+    from paper_1607_01649_b200.planted import spectrum as sp
+    return sp(kind, r)
 
 
 def env_int(name, default):
@@ -86,41 +84,17 @@ def env_int(name, default):
 
 # ----------------------------------------------------------------- GPU data ---
 def gen_shard(torch, dist, w, row0, row1, dev):
-    """A^T for rows [row0, row1) as an (n, rows) float64 tensor (= A col-major, lda = rows)."""
-    m, n, r = w["m"], w["n"], w["r"]
-    sig = torch.tensor(spectrum(w["spectrum"], r), device=dev, dtype=torch.float64)
-    g = torch.Generator(device=dev)
-    g.manual_seed(SEED * 7919 + 2)
-    V, _ = torch.linalg.qr(torch.randn(n, r, generator=g, device=dev, dtype=torch.float64))
-    rows = row1 - row0
-    U = torch.empty(rows, r, device=dev, dtype=torch.float64)
-    for c0 in range((row0 // CHUNK) * CHUNK, row1, CHUNK):
-        g.manual_seed(SEED * 1000003 + c0 // CHUNK)
-        blk = torch.randn(CHUNK, r, generator=g, device=dev, dtype=torch.float64)
-        a0, a1 = max(c0, row0), min(c0 + CHUNK, row1)
-        U[a0 - row0:a1 - row0] = blk[a0 - c0:a1 - c0]
-        del blk
-    for _ in range(2):  # CholeskyQR2 of the distributed Gaussian -> orthonormal Q factor
-        gram = U.T @ U
-        if dist is not None:
-            dist.all_reduce(gram)
-        R = torch.linalg.cholesky(gram, upper=True)
-        U = torch.linalg.solve_triangular(R, U, upper=True, left=False)
-    At = (V * sig) @ U.T  # n x rows
-    del U, V
-    if w["noise"]:
-        nch = max(1024, min(CHUNK, (1 << 28) // n))  # noise rows per draw (<= 2 GiB)
-        for c0 in range((row0 // nch) * nch, row1, nch):
-            g.manual_seed(SEED * 2000003 + c0 // nch)
-            blk = torch.randn(n, nch, generator=g, device=dev, dtype=torch.float64)
-            a0, a1 = max(c0, row0), min(c0 + nch, row1)
-            At[:, a0 - row0:a1 - row0].add_(blk[:, a0 - c0:a1 - c0], alpha=w["noise"])
-            del blk
+    """A^T for rows [row0, row1) as an (n, rows) tensor (= A col-major, lda = rows): the
+    reference recipe planted_matrix(m, n, s, 1) + noise * gaussian(1, "noise.N", m, n)."""
+    from paper_1607_01649_b200.planted import planted_matrix
+    ar = (lambda t: dist.all_reduce(t)) if dist is not None else None
+    at = planted_matrix(w["m"], w["n"], spectrum(w["spectrum"], w["r"]), SEED, noise=w["noise"], row0=row0,
+                        row1=row1, device=dev, allreduce=ar)
     if w.get("f32"):
-        At32 = At.float()
-        del At
-        return At32.contiguous()
-    return At.contiguous()
+        at32 = at.float().contiguous()
+        del at
+        return at32
+    return at.contiguous()
 
 
 # ------------------------------------------------------------------ clocks ---
@@ -212,33 +186,128 @@ def run_reference_rsvd(w, a_sample, threads):
     return time.perf_counter() - t0
 
 
-def sample_rows_for(w, budget_rows):
-    return max(w["n"], min(w["m"], budget_rows))
+FIT_ROWS = (8192, 24576)
+
+
+def reference_fit(w, sample_fn, threads_list, rows=FIT_ROWS):
+    """Time the reference rsvd at two row counts per thread count and fit t(m) = a + b m: the part of
+    the call that does not grow with m (svd_dense of the l x n B, the n x l orth) stays a, only b m is
+    extrapolated to the workload's m (the passes and the m x l orths are linear in m)."""
+    points, fits = [], {}
+    for th in threads_list:
+        ts = []
+        for r in rows:
+            t = run_reference_rsvd(w, sample_fn(r), th)
+            points.append({"rows": r, "threads": th, "s": t})
+            ts.append(t)
+        b = (ts[1] - ts[0]) / (rows[1] - rows[0])
+        a0 = ts[0] - b * rows[0]
+        fits[th] = {"a_s": a0, "b_s_per_row": b, "extrapolated_s": a0 + b * w["m"]}
+    return points, fits
 
 
 def reference_arm(args, w, rank, world):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    rows = sample_rows_for(w, args.ref_rows)
-    a = cpu_sample_matrix(w, rows)
-    scale = w["m"] / rows
-    for _ in range(args.warmup):
-        run_reference_rsvd(w, a, threads)
-    times = [run_reference_rsvd(w, a, threads) * scale for _ in range(args.steps)]
+    default_threads = min(8, threads)  # the reference's default: min(hw, 8) (dense.cpp:69-94)
+    samples = {}
+
+    def sample(rows):
+        if rows not in samples:
+            samples[rows] = cpu_sample_matrix(w, rows)
+        return samples[rows]
+
+    if w["m"] <= FIT_ROWS[1]:  # small config: timed at full size, nothing extrapolated
+        a = cpu_sample_matrix(w, w["m"])
+        for _ in range(args.warmup):
+            run_reference_rsvd(w, a, threads)
+        times = [run_reference_rsvd(w, a, threads) for _ in range(args.steps)]
+        points, fits, how = [], {}, f"reference rsvd at full size ({w['m']}x{w['n']}), {threads} threads"
+    else:
+        points, fits = reference_fit(w, sample, sorted({threads, default_threads}, reverse=True))
+        b = fits[threads]["b_s_per_row"]
+        r0 = FIT_ROWS[0]
+        for _ in range(args.warmup):
+            run_reference_rsvd(w, sample(r0), threads)
+        # every step: one measured sample at r0 rows + the fitted per-row cost of the remaining rows
+        times = [run_reference_rsvd(w, sample(r0), threads) + b * (w["m"] - r0) for _ in range(args.steps)]
+        how = (f"reference rsvd(A_sample, k={w['k']}, p={w['p']}, q={w['q']}, reorth=true) on row samples of the "
+               f"workload; each step = measured {r0}x{w['n']} call + fitted b*(m - {r0}) with t(m) = a + b m fitted "
+               f"to {FIT_ROWS[0]} and {FIT_ROWS[1]} rows (only the m-linear part extrapolated)")
     val = statistics.mean(times)
-    sample = (f"reference rsvd(A_sample, k={w['k']}, p={w['p']}, q={w['q']}, reorth=true) on a {rows}x{w['n']} "
-              f"row sample (1/{scale:g} of config rows), time scaled x{scale:g} (linear in m)")
     line = {
         "metric": "rsvd_time_to_rank_k", "value": val, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (planted spectrum, seeded)", "impl": "reference",
         "config": config_of(w, world, args),
-        "cpu_baseline": {"value": val, "unit": "s", "cores": threads, "kind": "reference", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": "s", "cores": threads, "kind": "reference", "sample": how,
+                         "points": points, "fit": {str(k): v for k, v in fits.items()},
+                         "default_threads": default_threads,
+                         "default_threads_value": fits.get(default_threads, {}).get("extrapolated_s")},
         "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+GOLDEN = os.path.join(ROOT, "tests", "golden", "config_golden.json")
+
+
+def check_parity(args, w, kind, step, ctx, rank_out, Ud, Dd, Vd, Js, mloc, n):
+    """The timed call's result against (1) the golden singular values / pivots of the full-size CPU oracle
+    run on the same A (tests/golden/config_golden.json, tools/parity_c3_full.py) and (2) the same call with
+    the passes forced onto FP64 DMMA (RFGPU_OZAKI=0; an independent product kernel). Outside the timed
+    region."""
+    import torch
+    ctx.synchronize()
+    kk = rank_out.value
+    tol = 1e-4 if w.get("f32") else 1e-10
+    res = {"tolerance_sigma_rel": tol}
+    if kind == "cur":
+        got_js = np.array(Js[:kk], copy=True)
+    else:
+        got_d = Dd[:kk].cpu().numpy().copy()
+        got_u, got_v = Ud[: mloc * kk].view(kk, mloc).clone(), Vd[: n * kk].view(kk, n).clone()
+    ok = True
+    gold = {}
+    if os.path.exists(GOLDEN):
+        gold = json.load(open(GOLDEN)).get(args.workload, {})
+    if gold.get("D") is not None and kind != "cur":
+        gd = np.asarray(gold["D"])
+        e = float(np.max(np.abs(got_d[: len(gd)] - gd) / gd)) if len(gd) == kk else float("inf")
+        res.update(golden_sigma_max_rel=e, golden_source=gold.get("source"))
+        ok &= e <= tol
+    if gold.get("Js") is not None and kind == "cur":
+        res.update(golden_pivots_equal=bool(np.array_equal(got_js, np.asarray(gold["Js"]))),
+                   golden_source=gold.get("source"))
+        ok &= res["golden_pivots_equal"]
+    prev = os.environ.get("RFGPU_OZAKI")
+    os.environ["RFGPU_OZAKI"] = "0"
+    try:
+        step()
+        ctx.synchronize()
+    finally:
+        if prev is None:
+            os.environ.pop("RFGPU_OZAKI", None)
+        else:
+            os.environ["RFGPU_OZAKI"] = prev
+    if kind == "cur":
+        res["dmma_pivots_equal"] = bool(np.array_equal(got_js, np.asarray(Js[: rank_out.value])))
+        ok &= res["dmma_pivots_equal"]
+    else:
+        d = Dd[:kk].cpu().numpy()
+        u, v = Ud[: mloc * kk].view(kk, mloc), Vd[: n * kk].view(kk, n)
+
+        def aligned(x, ref):  # rows of x / ref are singular vectors
+            s = torch.sign(torch.sum(x * ref, dim=1, keepdim=True))
+            s[s == 0] = 1
+            return float(torch.max(torch.abs(x * s - ref)))
+        res.update(dmma_sigma_max_rel=float(np.max(np.abs(got_d - d) / d)) if rank_out.value == kk else float("inf"),
+                   dmma_U_max_abs=aligned(got_u, u), dmma_V_max_abs=aligned(got_v, v))
+        ok &= res["dmma_sigma_max_rel"] <= tol
+    res["ok"] = bool(ok)
+    return res
 
 
 def config_of(w, world, args):
@@ -247,7 +316,8 @@ def config_of(w, world, args):
             "single_pass": f"single-pass SVD, fp32 A (fp64 arithmetic) m={w['m']} n={w['n']} k={w['k']} p={w['p']}"}
     return {"workload": f"{args.workload}: " + desc[w["kind"]], "m": w["m"], "n": w["n"], "k": w["k"], "p": w["p"], "q": w["q"],
             "rank_planted": w["r"], "noise": w["noise"], "seed": SEED, "parallelism": f"row-shard x{world}",
-            "l2": "A (8*m*n bytes) larger than L2; no flush needed"}
+            "l2": ("A (8*m*n bytes) larger than L2; no flush needed" if 8 * w["m"] * w["n"] > 126e6 else
+                   "A fits in L2 and stays warm between steps (no flush)")}
 
 
 # --------------------------------------------------------------------- main ---
@@ -260,7 +330,6 @@ def main():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-rows", type=int, default=8192, help="row sample for the CPU reference")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
@@ -392,6 +461,9 @@ def main():
         except Exception:
             traffic = None
 
+    # ---- self-check of the timed result (outside the timed region) ----------
+    parity = check_parity(args, w, kind, step, ctx, rank_out, Ud, Dd, Vd, Js if kind == "cur" else None, mloc, n)
+
     # ---- e2e through the host-buffer C ABI (upload + rsvd + D2H) -----------
     e2e = None
     if not args.no_e2e and kind == "rsvd":
@@ -438,17 +510,23 @@ def main():
         except Exception as ex:  # report, never hide
             e2e = {"value": None, "unit": "s", "error": f"{type(ex).__name__}: {ex}"}
 
-    # ---- CPU baseline (reference, bounded sample), rank 0 at N=1 ------------
+    # ---- CPU baseline (reference, bounded samples of this A), rank 0 at N=1 -
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and kind == "rsvd":
-        rows = sample_rows_for(w, args.ref_rows)
-        a_s = np.asfortranarray(At[:, :rows].T.cpu().numpy())
         threads = os.cpu_count() or 1
-        t = run_reference_rsvd(w, a_s, threads)
-        scale = m / rows
-        cpu = {"value": t * scale, "unit": "s", "cores": threads, "kind": "reference",
-               "sample": f"reference rsvd (reorth=true) on the first {rows} rows of this A ({rows}x{n}); "
-                         f"{t:.2f} s measured, scaled x{scale:g} (linear in m)"}
+        if m <= FIT_ROWS[1]:
+            t = run_reference_rsvd(w, np.asfortranarray(At.T.cpu().numpy()), threads)
+            cpu = {"value": t, "unit": "s", "cores": threads, "kind": "reference",
+                   "sample": f"reference rsvd (reorth=true) on this A ({m}x{n}), full size"}
+        else:
+            points, fits = reference_fit(w, lambda r: np.asfortranarray(At[:, :r].T.cpu().numpy()),
+                                         [threads, min(8, threads)] if threads > 8 else [threads])
+            cpu = {"value": fits[threads]["extrapolated_s"], "unit": "s", "cores": threads, "kind": "reference",
+                   "sample": (f"reference rsvd (reorth=true) on the first {FIT_ROWS[0]} and {FIT_ROWS[1]} rows of "
+                              f"this A; t(m) = a + b m fitted per thread count, b m extrapolated to m = {m}"),
+                   "points": points, "fit": {str(k): v for k, v in fits.items()},
+                   "default_threads": min(8, threads),
+                   "default_threads_value": fits[min(8, threads)]["extrapolated_s"]}
 
     if rank == 0:
         line = {
@@ -480,7 +558,7 @@ def main():
                           "peak_source": "FP64 DMMA microbenchmark profiles/r01_fp_peaks.txt (no FP64 entry in "
                                          "MEASURED_PEAKS.json)"}),
             "phase_ms_per_step": {nm: v[1] / args.steps for nm, v in prof.items()},
-            "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu, "parity": parity,
         }
         print(json.dumps(line), flush=True)
     A.free()

@@ -145,6 +145,10 @@ namespace b200 {
 void set_device(int device);
 // Number of rfgpu kernels launched by the drop-in so far (telemetry).
 std::int64_t kernel_launches();
+// Returns the drop-in's cached device memory (the A buffer kept between
+// calls, the context's memory pools) to the driver; the next call
+// re-allocates.
+void release_memory();
 }  // namespace b200
 
 }  // namespace randfact

@@ -71,7 +71,23 @@ int rfgpu_ctx_create(int device, rfgpu_ctx** out);
 int rfgpu_nccl_unique_id(void* id, size_t id_bytes);
 int rfgpu_ctx_create_dist(int device, int rank, int world, const void* nccl_id, size_t id_bytes,
                           rfgpu_ctx** out);
+/* Host-staged reduction backend: the sums over ranks (the same points where
+ * the NCCL context allreduces) go through sum(user, buf, count), which must
+ * replace buf[0..count) (pinned host memory) by its elementwise sum over all
+ * ranks and return 0 (non-zero fails the call with RFGPU_ECUDA). For hosts
+ * without NCCL and for several ranks sharing one GPU (NCCL cannot place two
+ * ranks on one device): the test suite runs the row-sharded schedule this way
+ * with a torch.distributed gloo callback. No reference counterpart (the
+ * reference is single-process). */
+typedef int (*rfgpu_host_sum_fn)(void* user, double* buf, int64_t count);
+int rfgpu_ctx_create_hostsum(int device, int rank, int world, rfgpu_host_sum_fn sum, void* user, rfgpu_ctx** out);
 int rfgpu_ctx_destroy(rfgpu_ctx* ctx);
+/* Returns every cached device block of the context to the driver: the
+ * stream-ordered pools (trimmed to zero) and the host-call A buffer. The next
+ * call re-allocates. */
+int rfgpu_ctx_release_memory(rfgpu_ctx* ctx);
+/* Device bytes the context currently holds (pool reservations + A cache). */
+int64_t rfgpu_ctx_pool_bytes(rfgpu_ctx* ctx);
 int rfgpu_ctx_rank(const rfgpu_ctx* ctx);
 int rfgpu_ctx_world(const rfgpu_ctx* ctx);
 /* Blocks until all work issued on the context's stream is done. */

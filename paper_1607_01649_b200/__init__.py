@@ -87,7 +87,10 @@ _SIGS = {
     "rfgpu_ctx_create": (_int, [_int, C.POINTER(_vp)]),
     "rfgpu_nccl_unique_id": (_int, [_vp, C.c_size_t]),
     "rfgpu_ctx_create_dist": (_int, [_int, _int, _int, _vp, C.c_size_t, C.POINTER(_vp)]),
+    "rfgpu_ctx_create_hostsum": (_int, [_int, _int, _int, _vp, _vp, C.POINTER(_vp)]),
     "rfgpu_ctx_destroy": (_int, [_vp]),
+    "rfgpu_ctx_release_memory": (_int, [_vp]),
+    "rfgpu_ctx_pool_bytes": (_i64, [_vp]),
     "rfgpu_ctx_rank": (_int, [_vp]),
     "rfgpu_ctx_world": (_int, [_vp]),
     "rfgpu_ctx_synchronize": (_int, [_vp]),
@@ -221,9 +224,26 @@ class Context:
     """One GPU (and, for world > 1, one NCCL communicator). Not re-entrant:
     the C layer serialises calls on the same context."""
 
-    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+    HOST_SUM = C.CFUNCTYPE(C.c_int, C.c_void_p, _pd, C.c_int64)
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 host_sum=None):
+        """host_sum: optional callable(np.ndarray) -> None that sums the float64
+        buffer over all ranks in place (the host-staged reduction backend,
+        rfgpu_ctx_create_hostsum); otherwise world > 1 uses NCCL with nccl_id."""
         self._h = _vp()
-        if world == 1:
+        self._cb = None
+        if host_sum is not None:
+            def _sum(_user, buf, count):
+                try:
+                    host_sum(np.ctypeslib.as_array(buf, shape=(count,)))
+                    return 0
+                except BaseException:  # never unwind through the C library
+                    return 1
+            self._cb = Context.HOST_SUM(_sum)
+            _check(lib().rfgpu_ctx_create_hostsum(device, rank, world, C.cast(self._cb, _vp), None,
+                                                  C.byref(self._h)))
+        elif world == 1:
             _check(lib().rfgpu_ctx_create(device, C.byref(self._h)))
         else:
             buf = C.create_string_buffer(nccl_id, 128)
@@ -260,6 +280,13 @@ class Context:
 
     def launch_count(self) -> int:
         return int(lib().rfgpu_launch_count(self._h))
+
+    def release_memory(self):
+        """Return the context's cached device memory (pools, host-call A buffer) to the driver."""
+        _check(lib().rfgpu_ctx_release_memory(self._h))
+
+    def pool_bytes(self) -> int:
+        return int(lib().rfgpu_ctx_pool_bytes(self._h))
 
     def matrix(self, a, f32: bool = False) -> "DeviceMatrix":
         return DeviceMatrix.upload(self, a, f32=f32)
@@ -570,16 +597,20 @@ class MatrixStream:
         return 1 if self.next_col >= self.a.shape[1] else 0
 
 
-def single_pass_svd(stream: MatrixStream, k: int, p: int, seed: int, ctx: Context | None = None) -> SvdFactors:
+def single_pass_svd(stream: MatrixStream, k: int, p: int, seed: int, ctx: Context | None = None,
+                    m_global: int | None = None) -> SvdFactors:
     """randfact::single_pass_svd(stream, k, p, seed): one traversal of the stream;
     every block is pushed to the device once (Yc += A_blk Gc_blk, Yr_blk = A_blk^T Gr)
-    and the core is solved on the device."""
+    and the core is solved on the device. On a multi-rank context the stream
+    holds this rank's rows of A and m_global is the row count of the whole A
+    (Gr is drawn for all of it; each rank uses its rows)."""
     m, n = stream.rows(), stream.cols()
-    _check_sample(k, p, m, n, "single_pass_svd")
+    mg = m if m_global is None else m_global
+    _check_sample(k, p, mg, n, "single_pass_svd")
     ctx = ctx or default_context()
     ell = k + p
     gc = gaussian(seed, "spsvd.Gc", n, ell)
-    gr = gaussian(seed, "spsvd.Gr", m, ell)
+    gr = gaussian(seed, "spsvd.Gr", mg, ell)
     h = _vp()
     _check(lib().rfgpu_single_pass_begin(ctx.handle, m, n, ell, _dp(_flat(gc)), _dp(_flat(gr)), C.byref(h)))
     try:

@@ -573,7 +573,7 @@ cudaError_t trinv_upper(const double* R, int64_t ldr, int k, double* Rinv, cudaS
       attr_done(cfg);
     }
     double* dinv = nullptr;
-    cudaError_t e = cudaMallocAsync(&dinv, sizeof(double) * nb * kTB * kTB, st);
+    cudaError_t e = ws_alloc(reinterpret_cast<void**>(&dinv), sizeof(double) * nb * kTB * kTB, st);
     if (e != cudaSuccess) return e;
     trinv_diag_kernel<<<nb, 256, 0, st>>>(R, ldr, k, dinv);
     trinv_blockcol_kernel<<<nb, 256, smem, st>>>(R, ldr, k, dinv, Rinv);

@@ -238,6 +238,17 @@ struct rfgpu_ctx {
   cudaStream_t copy_stream = nullptr;
   void* a_cache = nullptr;
   size_t a_cache_bytes = 0;
+  // Stream-ordered memory pools owned by this context (ws_alloc): small
+  // temporaries and large blocks (digit planes) apart, freed memory kept
+  // cached between calls, everything returned on rfgpu_ctx_release_memory /
+  // destroy. Other allocators in the process never see these blocks.
+  cudaMemPool_t pool_small = nullptr, pool_large = nullptr;
+  // Host-staged reduction backend (rfgpu_ctx_create_hostsum): the sums over
+  // ranks go through the caller's host callback instead of NCCL.
+  rfgpu_host_sum_fn host_sum = nullptr;
+  void* host_user = nullptr;
+  double* h_stage = nullptr;
+  size_t h_stage_n = 0;
 
   cudaEvent_t get_event() {
     if (!event_pool.empty()) {
@@ -301,7 +312,29 @@ void drain_profile(rfgpu_ctx* c) {
   c->pending.clear();
 }
 
-// Stream-ordered device buffer from the default memory pool.
+// The pools of the context whose C-ABI call is running on this thread.
+thread_local rfgpu_ctx* t_ctx = nullptr;
+constexpr size_t kSmallBlock = size_t{256} << 20;
+
+// Locks the context for one C-ABI call and installs its pools for ws_alloc.
+struct CtxCall {
+  std::lock_guard<std::mutex> lk;
+  rfgpu_ctx* prev;
+  explicit CtxCall(rfgpu_ctx* c) : lk(c->mu), prev(t_ctx) { t_ctx = c; }
+  ~CtxCall() { t_ctx = prev; }
+};
+
+}  // namespace
+
+cudaError_t rfgpu::ws_alloc(void** p, size_t bytes, cudaStream_t st) {
+  rfgpu_ctx* c = t_ctx;
+  if (c && c->pool_small) return cudaMallocFromPoolAsync(p, bytes, bytes < kSmallBlock ? c->pool_small : c->pool_large, st);
+  return cudaMallocAsync(p, bytes, st);
+}
+
+namespace {
+
+// Stream-ordered device buffer from the context's memory pools.
 struct DBuf {
   void* p = nullptr;
   cudaStream_t s = nullptr;
@@ -314,7 +347,7 @@ struct DBuf {
   Status alloc(size_t bytes, cudaStream_t st) {
     s = st;
     if (bytes == 0) bytes = 16;
-    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    cudaError_t e = rfgpu::ws_alloc(&p, bytes, st);
     if (e != cudaSuccess) {
       p = nullptr;
       cudaGetLastError();
@@ -331,9 +364,31 @@ struct DBuf {
 
 inline int64_t even(int64_t x) { return x + (x & 1); }
 
+// Host-staged sum over ranks (rfgpu_ctx_create_hostsum): the stream is
+// drained, the buffer goes through pinned host memory to the caller's
+// callback and back; stream order covers the copy back.
+cudaError_t host_allreduce(rfgpu_ctx* c, double* buf, int64_t count, cudaStream_t st) {
+  if (c->h_stage_n < static_cast<size_t>(count)) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    c->h_stage = nullptr;
+    c->h_stage_n = 0;
+    e = cudaMallocHost(&c->h_stage, sizeof(double) * count);
+    if (e != cudaSuccess) return e;
+    c->h_stage_n = static_cast<size_t>(count);
+  }
+  cudaError_t e = cudaMemcpyAsync(c->h_stage, buf, sizeof(double) * count, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return e;
+  if (c->host_sum(c->host_user, c->h_stage, count) != 0) return cudaErrorUnknown;
+  return cudaMemcpyAsync(buf, c->h_stage, sizeof(double) * count, cudaMemcpyHostToDevice, st);
+}
+
 cudaError_t nccl_allreduce_cb(void* vctx, double* buf, int64_t count, cudaStream_t st) {
   rfgpu_ctx* c = static_cast<rfgpu_ctx*>(vctx);
   if (c->world <= 1 || count <= 0) return cudaSuccess;
+  if (c->host_sum) return host_allreduce(c, buf, count, st);
   int r = g_nccl.allReduce(buf, buf, static_cast<size_t>(count), kNcclDouble, kNcclSum, c->comm, st);
   return r == 0 ? cudaSuccess : cudaErrorUnknown;
 }
@@ -350,6 +405,11 @@ DeviceAllreduce allreduce_of(rfgpu_ctx* c) {
 Status allreduce(rfgpu_ctx* c, double* buf, int64_t count) {
   if (c->world <= 1 || count <= 0) return {};
   Timed t(c, "allreduce");
+  if (c->host_sum) {
+    cudaError_t e = host_allreduce(c, buf, count, c->stream);
+    if (e != cudaSuccess) return make_err(RFGPU_ECUDA, std::string("host-staged allreduce failed: ") + cudaGetErrorString(e));
+    return {};
+  }
   int r = g_nccl.allReduce(buf, buf, static_cast<size_t>(count), kNcclDouble, kNcclSum, c->comm, c->stream);
   if (r != 0) return make_err(RFGPU_ECUDA, std::string("NCCL allreduce: ") + g_nccl.getErrorString(r));
   return {};
@@ -1369,13 +1429,38 @@ int rfgpu_nccl_unique_id(void* id, size_t id_bytes) {
   return RFGPU_OK;
 }
 
-int rfgpu_ctx_create_dist(int device, int rank, int world, const void* nccl_id, size_t id_bytes, rfgpu_ctx** out) {
+}  // extern "C"
+
+namespace {
+
+void ctx_free(rfgpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  drain_profile(c);
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->comm) g_nccl.commDestroy(c->comm);
+  if (c->h_info) cudaFreeHost(c->h_info);
+  if (c->h_d) cudaFreeHost(c->h_d);
+  if (c->h_i64) cudaFreeHost(c->h_i64);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
+  if (c->a_cache) cudaFree(c->a_cache);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  // every block of the context's pools goes back to the driver
+  if (c->pool_small) cudaMemPoolDestroy(c->pool_small);
+  if (c->pool_large) cudaMemPoolDestroy(c->pool_large);
+  delete c;
+}
+
+// Device checks, stream, pinned scratch and the context's two memory pools.
+int ctx_create_common(int device, int rank, int world, rfgpu_ctx** out) {
   if (!out) return finish(make_err(RFGPU_EPARAM, "ctx_create: null output"));
+  *out = nullptr;
   if (world < 1 || rank < 0 || rank >= world) return finish(make_err(RFGPU_EPARAM, "ctx_create: bad rank/world"));
-  auto c = std::make_unique<rfgpu_ctx>();
-  c->device = device;
-  c->rank = rank;
-  c->world = world;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -1388,50 +1473,102 @@ int rfgpu_ctx_create_dist(int device, int rank, int world, const void* nccl_id, 
   if (prop.major != 10) {
     return finish(make_err(RFGPU_ECUDA, std::string("rfgpu is built for sm_100a (B200); device is ") + prop.name));
   }
+  auto c = new rfgpu_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
   c->num_sms = prop.multiProcessorCount;
-  cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
-  cudaMallocHost(&c->h_info, 64);
-  cudaMallocHost(&c->h_d, 64);
-  cudaMallocHost(&c->h_i64, 64);
-  // keep freed pool memory cached (stream-ordered temporaries are reused)
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  bool ok = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMallocHost(&c->h_info, 64) == cudaSuccess && cudaMallocHost(&c->h_d, 64) == cudaSuccess &&
+            cudaMallocHost(&c->h_i64, 64) == cudaSuccess;
+  // freed pool memory stays cached (stream-ordered temporaries are reused call after call)
+  cudaMemPoolProps pp{};
+  pp.allocType = cudaMemAllocationTypePinned;
+  pp.location.type = cudaMemLocationTypeDevice;
+  pp.location.id = device;
+  uint64_t thr = UINT64_MAX;
+  for (cudaMemPool_t* pool : {&c->pool_small, &c->pool_large}) {
+    ok = ok && cudaMemPoolCreate(pool, &pp) == cudaSuccess &&
+         cudaMemPoolSetAttribute(*pool, cudaMemPoolAttrReleaseThreshold, &thr) == cudaSuccess;
   }
+  if (!ok) {
+    cudaGetLastError();
+    ctx_free(c);
+    return finish(make_err(RFGPU_ECUDA, "ctx_create: stream / pinned memory / memory pool creation failed"));
+  }
+  c->launch_base = launch_counter();
+  *out = c;
+  return RFGPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rfgpu_ctx_create_dist(int device, int rank, int world, const void* nccl_id, size_t id_bytes, rfgpu_ctx** out) {
+  if (world > 1 && (!nccl_id || id_bytes < 128))
+    return finish(make_err(RFGPU_EPARAM, "ctx_create_dist: nccl id required"));
+  rfgpu_ctx* c = nullptr;
+  int st = ctx_create_common(device, rank, world, &c);
+  if (st != RFGPU_OK) return st;
   if (world > 1) {
     std::lock_guard<std::mutex> lk(g_nccl_mu);
     std::string why;
-    if (!nccl_id || id_bytes < 128) return finish(make_err(RFGPU_EPARAM, "ctx_create_dist: nccl id required"));
-    if (!g_nccl.load(&why)) return finish(make_err(RFGPU_ECUDA, why));
+    if (!g_nccl.load(&why)) {
+      ctx_free(c);
+      return finish(make_err(RFGPU_ECUDA, why));
+    }
     char idb[128];
     std::memcpy(idb, nccl_id, 128);
     int r = g_nccl.commInitRank(&c->comm, world, idb, rank);
-    if (r != 0) return finish(make_err(RFGPU_ECUDA, std::string("ncclCommInitRank: ") + g_nccl.getErrorString(r)));
+    if (r != 0) {
+      c->comm = nullptr;
+      ctx_free(c);
+      return finish(make_err(RFGPU_ECUDA, std::string("ncclCommInitRank: ") + g_nccl.getErrorString(r)));
+    }
   }
-  c->launch_base = launch_counter();
-  *out = c.release();
+  *out = c;
+  return RFGPU_OK;
+}
+
+int rfgpu_ctx_create_hostsum(int device, int rank, int world, rfgpu_host_sum_fn sum, void* user, rfgpu_ctx** out) {
+  if (world > 1 && !sum) return finish(make_err(RFGPU_EPARAM, "ctx_create_hostsum: sum callback required"));
+  rfgpu_ctx* c = nullptr;
+  int st = ctx_create_common(device, rank, world, &c);
+  if (st != RFGPU_OK) return st;
+  c->host_sum = sum;
+  c->host_user = user;
+  *out = c;
   return RFGPU_OK;
 }
 
 int rfgpu_ctx_destroy(rfgpu_ctx* c) {
-  if (!c) return RFGPU_OK;
+  ctx_free(c);
+  return RFGPU_OK;
+}
+
+int rfgpu_ctx_release_memory(rfgpu_ctx* c) {
+  if (!c) return finish(make_err(RFGPU_EPARAM, "ctx_release_memory: null context"));
+  CtxCall lk(c);
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  drain_profile(c);
-  for (auto e : c->event_pool) cudaEventDestroy(e);
-  if (c->comm) g_nccl.commDestroy(c->comm);
-  cudaFreeHost(c->h_info);
-  cudaFreeHost(c->h_d);
-  cudaFreeHost(c->h_i64);
-  if (c->copy_stream) {
-    cudaStreamSynchronize(c->copy_stream);
-    cudaStreamDestroy(c->copy_stream);
-  }
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   if (c->a_cache) cudaFree(c->a_cache);
-  cudaStreamDestroy(c->stream);
-  delete c;
+  c->a_cache = nullptr;
+  c->a_cache_bytes = 0;
+  for (cudaMemPool_t pool : {c->pool_small, c->pool_large})
+    if (pool) cudaMemPoolTrimTo(pool, 0);
   return RFGPU_OK;
+}
+
+int64_t rfgpu_ctx_pool_bytes(rfgpu_ctx* c) {
+  if (!c) return -1;
+  uint64_t tot = 0;
+  for (cudaMemPool_t pool : {c->pool_small, c->pool_large}) {
+    uint64_t v = 0;
+    if (pool && cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &v) == cudaSuccess) tot += v;
+  }
+  return static_cast<int64_t>(tot + c->a_cache_bytes);
 }
 
 int rfgpu_ctx_rank(const rfgpu_ctx* c) { return c ? c->rank : -1; }
@@ -1445,13 +1582,13 @@ int rfgpu_ctx_synchronize(rfgpu_ctx* c) {
 }
 
 int rfgpu_profile_enable(rfgpu_ctx* c, int on) {
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   c->profile = on != 0;
   return RFGPU_OK;
 }
 
 int rfgpu_profile_reset(rfgpu_ctx* c) {
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   drain_profile(c);
   c->prof.clear();
   c->launch_base = launch_counter();
@@ -1459,7 +1596,7 @@ int rfgpu_profile_reset(rfgpu_ctx* c) {
 }
 
 int rfgpu_profile_read(rfgpu_ctx* c, const char* name, int64_t* launches, double* total_ms) {
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   drain_profile(c);
   auto it = c->prof.find(name);
   *launches = it == c->prof.end() ? 0 : it->second.first;
@@ -1474,7 +1611,7 @@ static int matrix_make(rfgpu_ctx* c, const void* host, const void* dev, bool f32
   if (!c || !out) return finish(make_err(RFGPU_EPARAM, "matrix: null argument"));
   if (m < 0 || n < 0) return finish(make_err(RFGPU_EPARAM, "DenseMatrix: negative dimension"));
   if (lda < std::max<int64_t>(1, m)) return finish(make_err(RFGPU_EPARAM, "matrix: lda < m"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   cudaSetDevice(c->device);
   auto h = std::make_unique<rfgpu_matrix>();
   h->ctx = c;
@@ -1552,7 +1689,7 @@ static Status copy_out(rfgpu_ctx* c, double* host, int64_t ldh, const double* de
 
 int rfgpu_multiply(rfgpu_ctx* c, const rfgpu_matrix* a, int trans, const double* x, int64_t ncols, double* out) {
   if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "multiply: bad handle"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status s = [&]() -> Status {
     RF_TRY(ensure_device(c));
     cudaStream_t st = c->stream;
@@ -1588,7 +1725,7 @@ int rfgpu_multiply(rfgpu_ctx* c, const rfgpu_matrix* a, int trans, const double*
 int rfgpu_range_finder(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t ell, int64_t q, int reorth,
                        double* Qh, double* Bh, double* resid, int64_t* ell_out) {
   if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "range_finder: bad handle"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status s = [&]() -> Status {
     if (q < 0) return make_err(RFGPU_EPARAM, "power_range: q must be non-negative");
     if (ell < 1 || ell > std::min(a->m_global, a->n))
@@ -1628,7 +1765,7 @@ int rfgpu_range_finder(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int
 int rfgpu_rsvd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g_dev, int64_t k, int64_t ell, int64_t q,
                       int keep_over, int reorth, double* U, double* D, double* V, int64_t* rank_out) {
   if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "rsvd: bad handle"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status s = [&]() -> Status {
     RF_TRY(check_sample(a, k, ell, "power_range"));
     if (q < 0) return make_err(RFGPU_EPARAM, "power_range: q must be non-negative");
@@ -1644,7 +1781,7 @@ int rfgpu_rsvd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g_dev, 
 int rfgpu_rsvd(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t k, int64_t ell, int64_t q, int keep_over,
                int reorth, double* Uh, double* Dh, double* Vh, int64_t* rank_out) {
   if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "rsvd: bad handle"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status s = [&]() -> Status {
     RF_TRY(check_sample(a, k, ell, "power_range"));
     if (q < 0) return make_err(RFGPU_EPARAM, "power_range: q must be non-negative");
@@ -1679,7 +1816,7 @@ int rfgpu_rsvd_host(rfgpu_ctx* c, const double* a, int64_t m, int64_t n, int64_t
   if (!c) return finish(make_err(RFGPU_EPARAM, "rsvd: null context"));
   if (m < 0 || n < 0) return finish(make_err(RFGPU_EPARAM, "DenseMatrix: negative dimension"));
   if (lda < std::max<int64_t>(1, m) || (!a && m * n > 0)) return finish(make_err(RFGPU_EPARAM, "rsvd: bad host matrix"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status s = [&]() -> Status {
     RF_TRY(ensure_device(c));
     rfgpu_matrix h;
@@ -1733,7 +1870,7 @@ int rfgpu_rsvd_host(rfgpu_ctx* c, const double* a, int64_t m, int64_t n, int64_t
 
 int rfgpu_row_sketch_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t ell, double* Y) {
   if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "row_sketch: bad handle"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status s = [&]() -> Status {
     if (ell < 1) return make_err(RFGPU_EPARAM, "row_sketch: ell must be at least 1");
     RF_TRY(ensure_device(c));
@@ -1771,7 +1908,7 @@ int rfgpu_row_sketch(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64
 int rfgpu_col_id_device(rfgpu_ctx* c, const double* Y, int64_t m, int64_t n, int64_t k, int64_t* Js, double* Z,
                         int64_t* rank_out, int* truncated) {
   if (!c) return finish(make_err(RFGPU_EPARAM, "col_id: null context"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status s = [&]() -> Status {
     if (k < 1) return make_err(RFGPU_EPARAM, "id_deterministic: k must be at least 1");
     if (k > std::min(m, n)) return make_err(RFGPU_EPARAM, "id_deterministic: k exceeds min(m, n)");
@@ -1807,7 +1944,7 @@ int rfgpu_col_id(rfgpu_ctx* c, const double* Yh, int64_t m, int64_t n, int64_t k
 int rfgpu_randomized_id(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t k, int64_t ell, int64_t q,
                         int64_t* Is, double* Xh, int64_t* rank_out, int* truncated) {
   if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "randomized_id: bad handle"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status s = [&]() -> Status {
     RF_TRY(check_sample(a, k, ell, "randomized_id"));
     if (q < 0) return make_err(RFGPU_EPARAM, "randomized_id: q must be non-negative");
@@ -1860,7 +1997,7 @@ int rfgpu_randomized_cur(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, i
                          int64_t* Js, int64_t* Is, double* Uh, double* cond_c, double* cond_r, int* warning,
                          int64_t* kc_out, int64_t* kr_out) {
   if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "randomized_cur: bad handle"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status s = [&]() -> Status {
     RF_TRY(check_sample(a, k, ell, "randomized_cur"));
     if (q < 0) return make_err(RFGPU_EPARAM, "randomized_cur: q must be non-negative");
@@ -1959,7 +2096,7 @@ int rfgpu_randomized_cur(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, i
 int rfgpu_dual_sketch_f32(rfgpu_ctx* c, const rfgpu_matrix* a, const float* gc, const float* gr, int64_t ell,
                           float* yc, float* yr) {
   if (!c || !a || !a->f32) return finish(make_err(RFGPU_EPARAM, "dual_sketch_f32: needs an fp32 handle"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status st = [&]() -> Status {
     RF_TRY(ensure_device(c));
     cudaStream_t s = c->stream;
@@ -2049,7 +2186,7 @@ int rfgpu_single_pass_begin(rfgpu_ctx* c, int64_t m, int64_t n, int64_t ell, con
                             rfgpu_single_pass** out) {
   if (!c || !out) return finish(make_err(RFGPU_EPARAM, "single_pass: null argument"));
   if (m < 1 || n < 1 || ell < 1) return finish(make_err(RFGPU_EPARAM, "single_pass_svd: bad dimensions"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   // Row-sharded stream (world > 1): every rank streams the column blocks of
   // ITS rows (m = local rows) and passes the FULL m_global x ell Gr.
   rfgpu_matrix shape;
@@ -2089,7 +2226,7 @@ int rfgpu_single_pass_begin(rfgpu_ctx* c, int64_t m, int64_t n, int64_t ell, con
 int rfgpu_single_pass_push(rfgpu_single_pass* s, int64_t col0, const double* blk, int64_t b) {
   if (!s) return finish(make_err(RFGPU_EPARAM, "single_pass: null state"));
   rfgpu_ctx* c = s->ctx;
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status st = [&]() -> Status {
     if (col0 != s->next_col || b < 0 || col0 + b > s->n)
       return make_err(RFGPU_ESTREAM, "single_pass: blocks must arrive once, in column order");
@@ -2113,7 +2250,7 @@ int rfgpu_single_pass_finish(rfgpu_single_pass* s, int64_t k, double* Uh, double
   rfgpu_ctx* c = s->ctx;
   Status st;
   {
-    std::lock_guard<std::mutex> lk(c->mu);
+    CtxCall lk(c);
     st = [&]() -> Status {
       if (s->next_col != s->n) return make_err(RFGPU_ESTREAM, "single_pass: stream not fully consumed");
       RF_TRY(ensure_device(c));
@@ -2147,7 +2284,7 @@ int rfgpu_single_pass_abort(rfgpu_single_pass* s) {
 int rfgpu_single_pass_svd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* gc, const double* gr, int64_t k,
                                  int64_t ell, double* U, double* D, double* V, int64_t* rank_out) {
   if (!c || !a) return finish(make_err(RFGPU_EPARAM, "single_pass_svd: bad handle"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status st = [&]() -> Status {
     RF_TRY(check_sample(a, k, ell, "single_pass_svd"));
     RF_TRY(ensure_device(c));
@@ -2213,7 +2350,7 @@ int rfgpu_single_pass_svd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const doub
 int rfgpu_svd(rfgpu_ctx* c, const double* Mh, int64_t rows, int64_t cols, double* Uh, double* Sh, double* Vh,
               int* sweeps) {
   if (!c) return finish(make_err(RFGPU_EPARAM, "svd: null context"));
-  std::lock_guard<std::mutex> lk(c->mu);
+  CtxCall lk(c);
   Status st = [&]() -> Status {
     if (rows < cols) return make_err(RFGPU_EPARAM, "svd: device path expects rows >= cols (transpose wide input)");
     if (cols < 1 || cols > 2048) return make_err(RFGPU_EPARAM, "svd: 1 <= cols <= 2048");

@@ -153,6 +153,13 @@ cudaError_t cpqr_rank(double* W, int64_t ld, int m, int64_t n, int kmax, double 
 cudaError_t trinv_upper(const double* R, int64_t ldr, int k, double* Rinv, cudaStream_t st);
 cudaError_t assemble_z(const int64_t* perm, int ke, int64_t n, const double* T, double* Z, cudaStream_t st);
 
+// Stream-ordered device allocation from the calling context's memory pools
+// (installed for the duration of every C-ABI call: temporaries under 256 MiB
+// from a small-block pool, larger ones from a large-block pool, so small
+// temporaries never carve up the blocks the digit planes reuse call after
+// call); the device's default pool outside a call.
+cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st);
+
 // *dst += *src (one thread; keeps scalar bookkeeping on the device).
 cudaError_t add_scalar(double* dst, const double* src, cudaStream_t st);
 

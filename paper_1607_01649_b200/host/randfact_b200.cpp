@@ -307,6 +307,10 @@ void set_device(int device) {
   g_device = device;
 }
 std::int64_t kernel_launches() { return g_ctx ? rfgpu_launch_count(g_ctx) : 0; }
+void release_memory() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_ctx) check(rfgpu_ctx_release_memory(g_ctx));
+}
 }  // namespace b200
 
 }  // namespace randfact
