@@ -139,6 +139,13 @@ IdFactors id_deterministic(const DenseMatrix& a, idx k, IdSide side);
 IdFactors randomized_id(const DenseMatrix& a, idx k, idx p, idx q, std::uint64_t seed);
 CurFactors randomized_cur(const DenseMatrix& a, idx k, idx p, idx q, std::uint64_t seed);
 
+// Matrix files (matrix_io.hpp:9-20): .mtx/.mm Matrix Market (array or
+// coordinate; real, integer or pattern; general or symmetric) and .csv, by
+// extension. ParseError on malformed input, ParameterError on an unknown
+// extension; write_matrix commits atomically and refuses non-finite entries.
+DenseMatrix read_matrix(const std::string& path);
+void write_matrix(const std::string& path, const DenseMatrix& a);
+
 namespace b200 {
 // Device used by the drop-in (default: $RANDFACT_B200_DEVICE, else
 // $LOCAL_RANK, else 0). Must be called before the first offloaded call.

@@ -201,6 +201,24 @@ int rfgpu_dual_sketch_f32(rfgpu_ctx* ctx, const rfgpu_matrix* a32, const float* 
 int rfgpu_svd(rfgpu_ctx* ctx, const double* M, int64_t rows, int64_t cols, double* U, double* S, double* V,
               int* sweeps);
 
+/* randfact::frob_residual (proj/src/rangefinder.cpp:45-54; the residual of
+ * finish_with_projection): *resid = sqrt(max(0, a_frob^2 - ||B||_F^2)),
+ * ||B||_F summed on the device over the count entries of B (host buffer).
+ * RFGPU_ENUMERICAL when ||B||_F > a_frob (1 + 1e-8) (basis orthonormality was
+ * lost upstream); RFGPU_EPARAM when a_frob is negative or NaN. */
+int rfgpu_frob_residual(rfgpu_ctx* ctx, double a_frob, const double* B, int64_t count, double* resid);
+
+/* Error of a low-rank factorization A ~ L R recomputed on the device, for the
+ * randfact/1 reports (the CLI's error block, proj/src/cli.cpp:191-206):
+ * *frob_abs = ||A - L R||_F (L m x k, R k x n, host, column-major; the
+ * product is formed in 256-column blocks and subtracted in a fused
+ * sum-of-squares pass); probe_norms[i] = ||(A - L R) g_i|| for the nprobes
+ * columns g_i of probes (n x nprobes host; the CLI passes
+ * gaussian(seed ^ 0x9e3779b9, "specnorm", n, 10), the reference's probe
+ * stream, diagnostics.cpp:75-96). k may be 0 (L R = 0). */
+int rfgpu_lowrank_error(rfgpu_ctx* ctx, const rfgpu_matrix* a, const double* L, const double* R, int64_t k,
+                        const double* probes, int64_t nprobes, double* frob_abs, double* probe_norms);
+
 /* ---- single pass (randfact::single_pass_svd, proj/src/lowrank.cpp:160-220)
  * Streaming form (MatrixStream, proj/include/randfact/stream.hpp:13-41):
  * begin with Gc = gaussian(seed, "spsvd.Gc", n, ell) and

@@ -280,6 +280,22 @@ class Oracle:
         rr = r.value
         return Svd(U[: m * rr].reshape((m, rr), order="F"), D[:rr].copy(), V[: n * rr].reshape((n, rr), order="F"))
 
+    def read_matrix(self, path: str):
+        """reference read_matrix (matrix_io.cpp) -> (status, message, array or None) (reference only)."""
+        rows, cols, data = _i64(), _i64(), C.POINTER(C.c_double)()
+        st = self._fn("read_matrix")(path.encode(), C.byref(rows), C.byref(cols), C.byref(data))
+        if st != 0:
+            return st, self._err().decode(), None
+        m, n = rows.value, cols.value
+        arr = np.ctypeslib.as_array(data, shape=(max(1, m * n),))[: m * n].copy().reshape((m, n), order="F")
+        self.lib.rfref_free(data)
+        return 0, "", arr
+
+    def write_matrix(self, path: str, a) -> tuple[int, str]:
+        a = fmat(a)
+        st = self._fn("write_matrix")(path.encode(), _dp(_flat(a)), _i64(a.shape[0]), _i64(a.shape[1]))
+        return st, (self._err().decode() if st else "")
+
     def dual_sketch(self, a, gc, gr, block=32):
         """(Yc = A Gc, Yr = A^T Gr) accumulated in MatrixStream block order (port only)."""
         a, gc, gr = fmat(a), fmat(gc), fmat(gr)

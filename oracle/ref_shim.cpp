@@ -19,6 +19,7 @@
 #include "randfact/dense.hpp"
 #include "randfact/diagnostics.hpp"
 #include "randfact/lowrank.hpp"
+#include "randfact/matrix_io.hpp"
 #include "randfact/rangefinder.hpp"
 #include "randfact/rng.hpp"
 #include "randfact/sketch.hpp"
@@ -238,5 +239,23 @@ int rfref_single_pass_svd(const double* a, int64_t m, int64_t n, int64_t k, int6
 int rfref_frob_residual(double a_frob, const double* b, int64_t m, int64_t n, double* out) {
     return guard([&] { *out = rf::frob_residual(a_frob, wrap(b, m, n)); });
 }
+
+// matrix_io.cpp:224-233: the reference reader (rows/cols out; data into a
+// buffer the caller frees with rfref_free)
+int rfref_read_matrix(const char* path, int64_t* rows, int64_t* cols, double** data) {
+    return guard([&] {
+        rf::DenseMatrix a = rf::read_matrix(path);
+        *rows = a.rows;
+        *cols = a.cols;
+        *data = new double[a.data.size() ? a.data.size() : 1];
+        put(a, *data);
+    });
+}
+
+int rfref_write_matrix(const char* path, const double* a, int64_t m, int64_t n) {
+    return guard([&] { rf::write_matrix(path, wrap(a, m, n)); });
+}
+
+void rfref_free(double* p) { delete[] p; }
 
 }  // extern "C"

@@ -33,7 +33,7 @@ __all__ = [
     "StreamContractError", "DeviceError", "Context", "DeviceMatrix", "SvdFactors", "RangeBasis", "IdFactors",
     "CurFactors", "gaussian", "basic_range", "power_range", "rsvd", "randomized_id", "randomized_cur",
     "id_deterministic", "single_pass_svd", "MatrixStream", "library_path", "default_context", "row_sketch",
-    "multiply", "svd_dense",
+    "multiply", "svd_dense", "frob_residual",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -121,6 +121,8 @@ _SIGS = {
     "rfgpu_single_pass_abort": (_int, [_vp]),
     "rfgpu_single_pass_svd_device": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _pi]),
     "rfgpu_svd": (_int, [_vp, _pd, _i64, _i64, _pd, _pd, _pd, C.POINTER(_int)]),
+    "rfgpu_frob_residual": (_int, [_vp, C.c_double, _pd, _i64, _pd]),
+    "rfgpu_lowrank_error": (_int, [_vp, _vp, _pd, _pd, _i64, _pd, _i64, _pd, _pd]),
     "rfgpu_randomized_id": (_int, [_vp, _vp, _pd, _i64, _i64, _i64, _pi, _pd, _pi, C.POINTER(_int)]),
     "rfgpu_randomized_cur": (_int, [_vp, _vp, _pd, _i64, _i64, _i64, _pi, _pi, _pd, _pd, _pd, C.POINTER(_int), _pi,
                                      _pi]),
@@ -484,6 +486,17 @@ def svd_dense(a, ctx: Context | None = None) -> SvdFactors:
     _check(lib().rfgpu_svd(ctx.handle, _dp(_flat(x)), r, c, _dp(U), _dp(S), _dp(V), C.byref(sw)))
     U, V = U.reshape((r, c), order="F"), V.reshape((c, c), order="F")
     return SvdFactors(V, S, U) if wide else SvdFactors(U, S, V)
+
+
+def frob_residual(a_frob: float, b, ctx: Context | None = None) -> float:
+    """randfact::frob_residual(a_frob, B) (rangefinder.cpp:45-54): ||B||_F summed on the device."""
+    if not (a_frob >= 0.0):
+        raise ParameterError("frob_residual: norm must be non-negative")
+    b = _fmat(b)
+    ctx = ctx or default_context()
+    out = C.c_double()
+    _check(lib().rfgpu_frob_residual(ctx.handle, float(a_frob), _dp(_flat(b)), b.size, C.byref(out)))
+    return out.value
 
 
 def id_deterministic(a, k: int, side: str = "Col", ctx: Context | None = None) -> IdFactors:

@@ -114,6 +114,27 @@ __global__ void f32_to_f64_kernel(const float* __restrict__ x, int64_t rows, int
   }
 }
 
+// part[blockIdx.x] = sum over this block's share of (A - S)^2 for a rows x cols block (column-major both).
+__global__ void diff_sumsq_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ S, int64_t lds,
+                                  int64_t rows, int64_t cols, double* __restrict__ part) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  const int64_t total = rows * cols, stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total; e += stride) {
+    const int64_t j = e / rows, i = e - j * rows;
+    const double d = A[j * lda + i] - S[j * lds + i];
+    acc = fma(d, d, acc);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+  }
+}
+
 __global__ void f64_to_f32_kernel(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -799,7 +820,7 @@ Status small_svd_of_bt(rfgpu_ctx* c, const double* Bt, int64_t n, int64_t ell, d
     const size_t jwb = jacobi_work_bytes(n, ell);
     if (jwb) RF_TRY(jw.alloc(jwb, st));
     Timed tj(c, "jacobi");
-    RF_CUDA(jacobi_svd(Bt, n, ell, Vb, D, Ub, jw.d(), info, info + 1, st));
+    RF_CUDA(jacobi_svd(Bt, n, ell, Vb, D, Ub, jw.d(), info, info + 1, st, /*sorted=*/true));
   }
   RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));
@@ -1033,7 +1054,7 @@ Status svd_tall_dev(rfgpu_ctx* c, const double* M, int64_t rows, int64_t cols, i
       const size_t jwb = jacobi_work_bytes(r, cols);
       if (jwb) RF_TRY(jw.alloc(jwb, st));
       Timed tj(c, "jacobi");
-      RF_CUDA(jacobi_svd(rq.d(), r, cols, ur.d(), S, Vm, jw.d(), info, info + 1, st));
+      RF_CUDA(jacobi_svd(rq.d(), r, cols, ur.d(), S, Vm, jw.d(), info, info + 1, st, /*sorted=*/true));
     }
     RF_CUDA(cudaMemsetAsync(Um, 0, sizeof(double) * rows * cols, st));
     if (r > 0) RF_TRY(gemm(c, false, rows, cols, r, b.Q, b.ldq, ur.d(), r, Um, rows));
@@ -1064,7 +1085,7 @@ Status svd_tall_dev(rfgpu_ctx* c, const double* M, int64_t rows, int64_t cols, i
     const size_t jwb = jacobi_work_bytes(rows, cols);
     if (jwb) RF_TRY(jw.alloc(jwb, st));
     Timed tj(c, "jacobi");
-    RF_CUDA(jacobi_svd(src, rows, cols, Um, S, Vm, jw.d(), info, info + 1, st));
+    RF_CUDA(jacobi_svd(src, rows, cols, Um, S, Vm, jw.d(), info, info + 1, st, /*sorted=*/true));
   }
   RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));
@@ -2346,6 +2367,88 @@ int rfgpu_single_pass_svd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const doub
   return finish(st);
 }
 
+
+// frob_residual (rangefinder.cpp:45-54): sqrt(max(0, a_frob^2 - ||B||_F^2)) with ||B||_F summed on the
+// device; NumericalError when ||B||_F > a_frob (1 + 1e-8) (basis orthonormality lost upstream).
+int rfgpu_frob_residual(rfgpu_ctx* c, double a_frob, const double* Bh, int64_t count, double* resid) {
+  if (!c) return finish(make_err(RFGPU_EPARAM, "frob_residual: null context"));
+  if (!(a_frob >= 0.0)) return finish(make_err(RFGPU_EPARAM, "frob_residual: norm must be non-negative"));
+  if (count < 0 || (count > 0 && !Bh)) return finish(make_err(RFGPU_EPARAM, "frob_residual: bad matrix"));
+  CtxCall lk(c);
+  Status st = [&]() -> Status {
+    RF_TRY(ensure_device(c));
+    DBuf b;
+    RF_TRY(b.alloc(sizeof(double) * std::max<int64_t>(1, count), c->stream));
+    if (count > 0) RF_CUDA(cudaMemcpyAsync(b.d(), Bh, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
+    return frob_residual_dev(c, a_frob * a_frob, b.d(), count, resid);
+  }();
+  return finish(st);
+}
+
+// ||A - L R||_F and the CLI's spectral probes ||(A - L R) g_i|| (cli.cpp:191-206 error block) for a
+// device-resident A: L R is formed 256 columns at a time on the FP64 tensor pipe and subtracted in a
+// fused sum-of-squares pass, so no m x n temporary exists.
+int rfgpu_lowrank_error(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Lh, const double* Rh, int64_t k,
+                        const double* probes, int64_t nprobes, double* frob_abs, double* probe_norms) {
+  if (!c || !a || a->f32) return finish(make_err(RFGPU_EPARAM, "lowrank_error: bad handle"));
+  if (k < 0 || nprobes < 0 || (nprobes > 0 && (!probes || !probe_norms)))
+    return finish(make_err(RFGPU_EPARAM, "lowrank_error: bad arguments"));
+  CtxCall lk(c);
+  Status st = [&]() -> Status {
+    RF_TRY(ensure_device(c));
+    cudaStream_t s = c->stream;
+    const int64_t m = a->m, n = a->n;
+    const double* A = static_cast<const double*>(a->dev);
+    constexpr int64_t W = 256;
+    constexpr int kBlocks = 592;
+    const int64_t nblk = (n + W - 1) / W;
+    DBuf L, R, S, part, tot;
+    RF_TRY(L.alloc(sizeof(double) * std::max<int64_t>(1, m * k), s));
+    RF_TRY(R.alloc(sizeof(double) * std::max<int64_t>(1, k * n), s));
+    RF_TRY(S.alloc(sizeof(double) * std::max<int64_t>(1, m * std::min(W, n)), s));
+    RF_TRY(part.alloc(sizeof(double) * kBlocks * std::max<int64_t>(nblk, nprobes), s));
+    RF_TRY(tot.alloc(sizeof(double) * 16, s));
+    if (m * k > 0) RF_CUDA(cudaMemcpyAsync(L.d(), Lh, sizeof(double) * m * k, cudaMemcpyHostToDevice, s));
+    if (k * n > 0) RF_CUDA(cudaMemcpyAsync(R.d(), Rh, sizeof(double) * k * n, cudaMemcpyHostToDevice, s));
+    RF_CUDA(cudaMemsetAsync(S.d(), 0, sizeof(double) * std::max<int64_t>(1, m * std::min(W, n)), s));
+    for (int64_t b = 0; b < nblk; ++b) {
+      const int64_t c0 = b * W, w = std::min(W, n - c0);
+      if (k > 0) RF_TRY(gemm(c, false, m, w, k, L.d(), m, R.d() + c0 * k, k, S.d(), m, nullptr, "lowrank_error"));
+      diff_sumsq_kernel<<<kBlocks, 256, 0, s>>>(A + c0 * a->lda, a->lda, S.d(), m, m, w, part.d() + b * kBlocks);
+      count_launch();
+      RF_CUDA(cudaGetLastError());
+    }
+    RF_CUDA(sum_array(part.d(), kBlocks * nblk, tot.d(), s));
+    RF_CUDA(cudaMemcpyAsync(c->h_d, tot.d(), sizeof(double), cudaMemcpyDeviceToHost, s));
+    RF_CUDA(cudaStreamSynchronize(s));
+    *frob_abs = std::sqrt(c->h_d[0]);
+    if (nprobes > 0) {
+      DBuf G, Y, T, Wm;
+      RF_TRY(G.alloc(sizeof(double) * n * nprobes, s));
+      RF_TRY(Y.alloc(sizeof(double) * m * nprobes, s));
+      RF_TRY(T.alloc(sizeof(double) * std::max<int64_t>(1, k * nprobes), s));
+      RF_TRY(Wm.alloc(sizeof(double) * m * nprobes, s));
+      RF_CUDA(cudaMemcpyAsync(G.d(), probes, sizeof(double) * n * nprobes, cudaMemcpyHostToDevice, s));
+      RF_TRY(gemm(c, false, m, nprobes, n, A, a->lda, G.d(), n, Y.d(), m));          // A g
+      RF_CUDA(cudaMemsetAsync(Wm.d(), 0, sizeof(double) * m * nprobes, s));
+      if (k > 0) {
+        RF_TRY(gemm(c, false, k, nprobes, n, R.d(), k, G.d(), n, T.d(), k));         // R g
+        RF_TRY(gemm(c, false, m, nprobes, k, L.d(), m, T.d(), k, Wm.d(), m));        // L (R g)
+      }
+      for (int64_t j = 0; j < nprobes; ++j) {
+        diff_sumsq_kernel<<<kBlocks, 256, 0, s>>>(Y.d() + j * m, m, Wm.d() + j * m, m, m, 1, part.d() + j * kBlocks);
+        count_launch();
+        RF_CUDA(cudaGetLastError());
+        RF_CUDA(sum_array(part.d() + j * kBlocks, kBlocks, tot.d() + j % 16, s));
+        RF_CUDA(cudaMemcpyAsync(c->h_d, tot.d() + j % 16, sizeof(double), cudaMemcpyDeviceToHost, s));
+        RF_CUDA(cudaStreamSynchronize(s));
+        probe_norms[j] = std::sqrt(c->h_d[0]);
+      }
+    }
+    return {};
+  }();
+  return finish(st);
+}
 
 int rfgpu_svd(rfgpu_ctx* c, const double* Mh, int64_t rows, int64_t cols, double* Uh, double* Sh, double* Vh,
               int* sweeps) {

@@ -110,8 +110,14 @@ size_t chol_inv_work_bytes(int64_t c);
 // 1e-15, <= 60 sweeps, columns with S <= smax*1e-250 zeroed). U mr x c,
 // V c x c. info[0] = 0 ok, 1 no convergence, 2 zero singular values present
 // (those U columns are left zero; the caller completes them).
+// sorted = true forces the per-column kernel, which re-orders the columns by
+// norm before every sweep exactly as the reference does (dense.cpp:597-618):
+// required for graded / ill-conditioned X (a spectrum spanning many decades),
+// where unsorted cyclic sweeps can exceed the sweep cap; the block kernel
+// (cluster-wide, no per-sweep ordering) serves the well-conditioned l x l
+// factors of CholeskyQR2.
 cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double* S, double* V, double* work,
-                       int* info, int* sweeps_out, cudaStream_t st);
+                       int* info, int* sweeps_out, cudaStream_t st, bool sorted = false);
 size_t jacobi_work_bytes(int64_t mr, int64_t c);
 // Two independent same-shape problems in one launch (one cluster each).
 struct JacobiProblem {

@@ -1120,10 +1120,11 @@ cudaError_t bjacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64
   return cudaGetLastError();
 }
 
-cudaError_t jacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64_t c, cudaStream_t st) {
+cudaError_t jacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64_t c, cudaStream_t st,
+                          bool sorted = false) {
   if (c <= 0 || mr <= 0) return cudaSuccess;
   const BJLayout B = bj_layout(mr, c);
-  if (B.ok) return bjacobi_launch(pr, count, mr, c, B, st);
+  if (B.ok && !sorted) return bjacobi_launch(pr, count, mr, c, B, st);
   const JacobiLayout L = jacobi_layout(mr, c);
   JacobiParams ps[2];
   for (int i = 0; i < count; ++i) {
@@ -1167,30 +1168,24 @@ cudaError_t jacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64_
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e;
-  if (L.smem) {
-    static size_t c1 = 0;
-    if (L.bytes > c1) {
-      e = cudaFuncSetAttribute(jacobi_svd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(L.bytes));
-      if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(jacobi_svd_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-      c1 = L.bytes;
+  // kernel attributes once per device, at the device's opt-in shared-memory maximum (the layout never
+  // asks for more), so every context on every device launches with them set
+  static std::atomic<uint64_t> attr_cfg{0};
+  if (attr_pending(attr_cfg)) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    for (const void* fn : {reinterpret_cast<const void*>(jacobi_svd_kernel<true>),
+                           reinterpret_cast<const void*>(jacobi_svd_kernel<false>)}) {
+      cudaError_t ea = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+      if (ea == cudaSuccess) ea = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (ea != cudaSuccess) return ea;
     }
-    e = cudaLaunchKernelEx(&cfg, jacobi_svd_kernel<true>, ps[0], ps[1]);
-    count_launch();
-  } else {
-    static size_t c2 = 0;
-    if (L.bytes > c2) {
-      e = cudaFuncSetAttribute(jacobi_svd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(L.bytes));
-      if (e != cudaSuccess) return e;
-      c2 = L.bytes;
-    }
-    e = cudaLaunchKernelEx(&cfg, jacobi_svd_kernel<false>, ps[0], ps[1]);
-    count_launch();
+    attr_done(attr_cfg);
   }
+  cudaError_t e = L.smem ? cudaLaunchKernelEx(&cfg, jacobi_svd_kernel<true>, ps[0], ps[1])
+                         : cudaLaunchKernelEx(&cfg, jacobi_svd_kernel<false>, ps[0], ps[1]);
+  count_launch();
   if (e != cudaSuccess) return e;
 #ifdef RFGPU_JACOBI_TRACE
   {
@@ -1208,9 +1203,9 @@ cudaError_t jacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64_
 }  // namespace
 
 cudaError_t jacobi_svd(const double* X, int64_t mr, int64_t c, double* U, double* S, double* V, double* work,
-                       int* info, int* sweeps_out, cudaStream_t st) {
+                       int* info, int* sweeps_out, cudaStream_t st, bool sorted) {
   const JacobiProblem p{X, U, S, V, work, info, sweeps_out};
-  return jacobi_launch(&p, 1, mr, c, st);
+  return jacobi_launch(&p, 1, mr, c, st, sorted);
 }
 
 cudaError_t jacobi_svd_pair(const JacobiProblem& a, const JacobiProblem& b, int64_t mr, int64_t c, cudaStream_t st) {

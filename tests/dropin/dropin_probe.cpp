@@ -7,6 +7,8 @@
 //   dropin_probe cpu                       -> expects randfact::Error without a GPU
 //   dropin_probe rsvd A.bin m n k p q reorth out.bin
 //   dropin_probe cur  A.bin m n k p out.bin
+//   dropin_probe io   FILE out.bin          -> randfact::read_matrix (matrix_io.hpp) from the drop-in
+//   dropin_probe iow  A.bin m n FILE        -> randfact::write_matrix
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -15,6 +17,7 @@
 #include "randfact/common.hpp"
 #include "randfact/dense.hpp"
 #include "randfact/lowrank.hpp"
+#include "randfact/matrix_io.hpp"
 #include "randfact/rangefinder.hpp"
 #include "randfact/sketch.hpp"
 
@@ -77,6 +80,33 @@ int main(int argc, char** argv) {
     for (idx i : c.Is) out.push_back(static_cast<double>(i));
     write_vec(argv[7], out);
     std::printf("kc %zu kr %zu condC %.6g condR %.6g\n", c.Js.size(), c.Is.size(), c.cond_C, c.cond_R);
+    return 0;
+  }
+  if (argc >= 4 && std::string(argv[1]) == "io") {
+    try {
+      DenseMatrix a = read_matrix(argv[2]);
+      write_vec(argv[3], a.data);
+      std::printf("OK %lld %lld\n", static_cast<long long>(a.rows), static_cast<long long>(a.cols));
+    } catch (const ParseError& e) {
+      std::printf("PARSE_ERROR %s\n", e.what());
+    } catch (const ParameterError& e) {
+      std::printf("PARAM_ERROR %s\n", e.what());
+    } catch (const Error& e) {
+      std::printf("ERROR %s\n", e.what());
+    }
+    return 0;
+  }
+  if (argc >= 6 && std::string(argv[1]) == "iow") {
+    const idx m = std::atoll(argv[3]), n = std::atoll(argv[4]);
+    DenseMatrix a = read_matrix_bin(argv[2], m, n);
+    try {
+      write_matrix(argv[5], a);
+      std::printf("OK\n");
+    } catch (const NumericalError& e) {
+      std::printf("NUMERICAL_ERROR %s\n", e.what());
+    } catch (const ParameterError& e) {
+      std::printf("PARAM_ERROR %s\n", e.what());
+    }
     return 0;
   }
   std::fprintf(stderr, "usage: dropin_probe cpu | rsvd ... | cur ...\n");
