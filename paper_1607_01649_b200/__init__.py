@@ -24,6 +24,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -235,6 +236,7 @@ class Context:
         rfgpu_ctx_create_hostsum); otherwise world > 1 uses NCCL with nccl_id."""
         self._h = _vp()
         self._cb = None
+        self._mats = weakref.WeakSet()  # device matrices of this context: freed before the context
         if host_sum is not None:
             def _sum(_user, buf, count):
                 try:
@@ -295,6 +297,8 @@ class Context:
 
     def close(self):
         if self._h:
+            for mat in list(self._mats):  # a handle must never outlive its context
+                mat.free()
             lib().rfgpu_ctx_destroy(self._h)
             self._h = _vp()
 
@@ -321,6 +325,7 @@ class DeviceMatrix:
     def __init__(self, ctx: Context, handle, m: int, n: int, f32: bool, keep=None):
         self.ctx, self._h, self.f32 = ctx, handle, f32
         self._keep = keep
+        ctx._mats.add(self)
         ml, nn, mg, r0 = _i64(), _i64(), _i64(), _i64()
         _check(lib().rfgpu_matrix_shape(handle, C.byref(ml), C.byref(nn), C.byref(mg), C.byref(r0)))
         self.m, self.n, self.m_global, self.row0 = ml.value, nn.value, mg.value, r0.value

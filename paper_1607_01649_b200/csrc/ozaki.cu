@@ -1093,12 +1093,15 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   p.cl = 1;
   const char* mc_env = std::getenv("RFGPU_OZAKI_MC");  // experiments: 0 never, 1 always, unset: caller's choice
   if (mc_env) multicast = mc_env[0] == '1';
-  if (multicast)
+  if (multicast) {
+    const char* mcs = std::getenv("RFGPU_OZAKI_MCSIZE");  // experiments: the largest cluster <= this dividing ntn
+    const int cmax = mcs ? std::max(2, std::atoi(mcs)) : 8;
     for (int c : {8, 7, 6, 5, 4, 3, 2})
-      if (p.ntn % c == 0) {
+      if (c <= cmax && p.ntn % c == 0) {
         p.cl = c;
         break;
       }
+  }
   p.ngroups = grid / p.cl;
   p.tma3 = (tma3 && p.cl == 1) ? 1 : 0;
   cudaLaunchConfig_t cfgl{};

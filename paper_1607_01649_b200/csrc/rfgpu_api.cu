@@ -114,6 +114,15 @@ __global__ void f32_to_f64_kernel(const float* __restrict__ x, int64_t rows, int
   }
 }
 
+// Speculative orth: the CholeskyQR2 gate (both factorizations succeeded and min pivot / trace(G) >= gate),
+// else bit 0 of *flags. Jacobi: info 1 (no convergence) sets bit 1.
+__global__ void orth_gate_kernel(const int* info, const double* info_d, double gate, int* flags) {
+  if (info[0] != 0 || info[1] != 0 || !(info_d[0] >= gate)) atomicOr(flags, 1);
+}
+__global__ void jacobi_gate_kernel(const int* info, int* flags) {
+  if (info[0] == 1) atomicOr(flags + 1, 1);
+}
+
 // part[blockIdx.x] = sum over this block's share of (A - S)^2 for a rows x cols block (column-major both).
 __global__ void diff_sumsq_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ S, int64_t lds,
                                   int64_t rows, int64_t cols, double* __restrict__ part) {
@@ -257,6 +266,12 @@ struct rfgpu_ctx {
   // device buffer for A, so repeated drop-in calls neither re-allocate nor
   // serialise the upload in front of the first pass
   cudaStream_t copy_stream = nullptr;
+  // pinned staging ring for pageable host buffers (host copy threads fill a
+  // slot, the copy engine moves it; a slot is refilled once its copy is done)
+  std::vector<void*> stage_slots;
+  std::vector<cudaEvent_t> stage_done;
+  size_t stage_bytes = 0;
+  size_t stage_next = 0;
   void* a_cache = nullptr;
   size_t a_cache_bytes = 0;
   // Stream-ordered memory pools owned by this context (ws_alloc): small
@@ -266,6 +281,14 @@ struct rfgpu_ctx {
   cudaMemPool_t pool_small = nullptr, pool_large = nullptr;
   // Host-staged reduction backend (rfgpu_ctx_create_hostsum): the sums over
   // ranks go through the caller's host callback instead of NCCL.
+  // Speculative CholeskyQR2 (rsvd / range finder): every orth assumes the
+  // fast path and records a failed gate on the device (spec_flags); the call
+  // reads the flags once at its end and re-runs without speculation when one
+  // is set. No host round trip inside the call (so it can be graph-captured).
+  bool spec = false;
+  int* spec_flags = nullptr;   // device: [0] orth gate failures, [1] Jacobi non-convergence
+  double* spec_vals = nullptr; // device: [0] ||A||_F^2, [1] ||B||_F^2
+  void* h_spec = nullptr;      // pinned copy of both (64 bytes)
   rfgpu_host_sum_fn host_sum = nullptr;
   void* host_user = nullptr;
   double* h_stage = nullptr;
@@ -393,6 +416,10 @@ cudaError_t host_allreduce(rfgpu_ctx* c, double* buf, int64_t count, cudaStream_
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return e;
     if (c->h_stage) cudaFreeHost(c->h_stage);
+  for (void* sl : c->stage_slots) cudaFreeHost(sl);
+  for (cudaEvent_t e : c->stage_done) cudaEventDestroy(e);
+  if (c->h_spec) cudaFreeHost(c->h_spec);
+  if (c->spec_flags) cudaFree(c->spec_flags);
     c->h_stage = nullptr;
     c->h_stage_n = 0;
     e = cudaMallocHost(&c->h_stage, sizeof(double) * count);
@@ -603,6 +630,123 @@ Status pass_tn_raw(rfgpu_ctx* c, const rfgpu_matrix* a, const double* Y, int64_t
               "pass_tn");
 }
 
+// ---- pageable host buffers: pinned staging ring ----------------------------------------
+// A DMA from pageable memory is staged by the driver synchronously and slowly;
+// instead, host threads copy column blocks of the caller's buffer into pinned
+// slots (kStageSlots x kStageBytes, allocated once per context) and the copy
+// engine moves each slot while the next is being filled.
+constexpr int kStageSlots = 4;
+constexpr size_t kStageBytes = size_t{128} << 20;
+
+bool host_is_pageable(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
+
+Status stage_ring(rfgpu_ctx* c) {
+  if (!c->stage_slots.empty()) return {};
+  for (int i = 0; i < kStageSlots; ++i) {
+    void* p = nullptr;
+    cudaEvent_t e;
+    RF_CUDA(cudaMallocHost(&p, kStageBytes));
+    c->stage_slots.push_back(p);
+    RF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->stage_done.push_back(e);
+  }
+  c->stage_bytes = kStageBytes;
+  return {};
+}
+
+// Parallel strided copy of `cols` columns of `rows` doubles (ld_src -> ld_dst) on the host.
+void host_copy_cols(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows, int64_t cols) {
+  const int64_t bytes = rows * cols * 8;
+  const int nt = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), bytes >> 22)));
+  auto part = [&](int t) {
+    if (cols >= nt) {
+      for (int64_t j = cols * t / nt; j < cols * (t + 1) / nt; ++j)
+        std::memcpy(dst + j * ldd, src + j * lds, sizeof(double) * rows);
+    } else {  // few columns: split the rows
+      const int64_t r0 = rows * t / nt, r1 = rows * (t + 1) / nt;
+      for (int64_t j = 0; j < cols; ++j) std::memcpy(dst + j * ldd + r0, src + j * lds + r0, sizeof(double) * (r1 - r0));
+    }
+  };
+  if (nt == 1) {
+    part(0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(part, t);
+  part(0);
+  for (auto& x : th) x.join();
+}
+
+// H2D of rows x cols (column-major, ld lds) from pageable host memory into the
+// device (ld ldd) on stream cs through the staging ring. Returns once every
+// block is issued (host copies done, DMAs queued).
+Status staged_h2d(rfgpu_ctx* c, double* dev, int64_t ldd, const double* host, int64_t lds, int64_t rows, int64_t cols,
+                  cudaStream_t cs) {
+  if (rows <= 0 || cols <= 0) return {};
+  RF_TRY(stage_ring(c));
+  const int64_t rstep = static_cast<size_t>(rows) * 8 <= c->stage_bytes ? rows : static_cast<int64_t>(c->stage_bytes / 8);
+  for (int64_t r0 = 0; r0 < rows; r0 += rstep) {
+    const int64_t rr = std::min(rstep, rows - r0);
+    const int64_t cstep = std::max<int64_t>(1, static_cast<int64_t>(c->stage_bytes / (sizeof(double) * rr)));
+    for (int64_t c0 = 0; c0 < cols; c0 += cstep) {
+      const int64_t cc = std::min(cstep, cols - c0);
+      const size_t sl = c->stage_next++ % c->stage_slots.size();
+      RF_CUDA(cudaEventSynchronize(c->stage_done[sl]));  // the slot's previous copy has landed
+      double* buf = static_cast<double*>(c->stage_slots[sl]);
+      host_copy_cols(buf, rr, host + c0 * lds + r0, lds, rr, cc);
+      RF_CUDA(cudaMemcpy2DAsync(dev + c0 * ldd + r0, sizeof(double) * ldd, buf, sizeof(double) * rr, sizeof(double) * rr,
+                                cc, cudaMemcpyHostToDevice, cs));
+      RF_CUDA(cudaEventRecord(c->stage_done[sl], cs));
+    }
+  }
+  return {};
+}
+
+// D2H into pageable host memory through the ring (blocks until the data is in `host`).
+Status staged_d2h(rfgpu_ctx* c, double* host, int64_t ldh, const double* dev, int64_t ldd, int64_t rows, int64_t cols,
+                  cudaStream_t cs) {
+  if (rows <= 0 || cols <= 0) return {};
+  RF_TRY(stage_ring(c));
+  const int64_t rstep = static_cast<size_t>(rows) * 8 <= c->stage_bytes ? rows : static_cast<int64_t>(c->stage_bytes / 8);
+  struct Pending {
+    size_t slot;
+    int64_t r0, rr, c0, cc;
+  };
+  std::vector<Pending> q;
+  auto drain = [&](size_t keep) -> Status {
+    while (q.size() > keep) {
+      const Pending pd = q.front();
+      q.erase(q.begin());
+      RF_CUDA(cudaEventSynchronize(c->stage_done[pd.slot]));
+      host_copy_cols(host + pd.c0 * ldh + pd.r0, ldh, static_cast<double*>(c->stage_slots[pd.slot]), pd.rr, pd.rr, pd.cc);
+    }
+    return {};
+  };
+  for (int64_t r0 = 0; r0 < rows; r0 += rstep) {
+    const int64_t rr = std::min(rstep, rows - r0);
+    const int64_t cstep = std::max<int64_t>(1, static_cast<int64_t>(c->stage_bytes / (sizeof(double) * rr)));
+    for (int64_t c0 = 0; c0 < cols; c0 += cstep) {
+      const int64_t cc = std::min(cstep, cols - c0);
+      RF_TRY(drain(c->stage_slots.size() - 1));  // the next slot in turn is free
+      const size_t sl = c->stage_next++ % c->stage_slots.size();
+      RF_CUDA(cudaEventSynchronize(c->stage_done[sl]));
+      RF_CUDA(cudaMemcpy2DAsync(c->stage_slots[sl], sizeof(double) * rr, dev + c0 * ldd + r0, sizeof(double) * ldd,
+                                sizeof(double) * rr, cc, cudaMemcpyDeviceToHost, cs));
+      RF_CUDA(cudaEventRecord(c->stage_done[sl], cs));
+      q.push_back({sl, r0, rr, c0, cc});
+    }
+  }
+  return drain(0);
+}
+
 // Y = A G with ||A||_F^2 partials fused (pass 1). For a handle whose rows are
 // still on the host, panel i+1's H2D copy runs on the copy stream while panel
 // i's product runs on the compute stream.
@@ -613,13 +757,18 @@ Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, 
   if (!a->src) return pass1_rows(c, a, G, ell, Y, ldy, ssq, 0, m, oz, true);
   cudaStream_t st = c->stream, cs = c->copy_stream;
   const auto panels = upload_panels(m);
+  const bool pageable = host_is_pageable(a->src);
   std::vector<cudaEvent_t> ev(panels.size());
   for (auto& e : ev) RF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   auto copy = [&](size_t i) -> Status {
     const int64_t r0 = panels[i].first, rows = panels[i].second - r0;
-    if (rows > 0 && n > 0)
-      RF_CUDA(cudaMemcpy2DAsync(const_cast<double*>(A) + r0, sizeof(double) * lda, a->src + r0,
-                                sizeof(double) * a->src_ld, sizeof(double) * rows, n, cudaMemcpyHostToDevice, cs));
+    if (rows > 0 && n > 0) {
+      if (pageable)  // host threads through the pinned ring; returns once issued
+        RF_TRY(staged_h2d(c, const_cast<double*>(A) + r0, lda, a->src + r0, a->src_ld, rows, n, cs));
+      else
+        RF_CUDA(cudaMemcpy2DAsync(const_cast<double*>(A) + r0, sizeof(double) * lda, a->src + r0,
+                                  sizeof(double) * a->src_ld, sizeof(double) * rows, n, cudaMemcpyHostToDevice, cs));
+    }
     RF_CUDA(cudaEventRecord(ev[i], cs));
     return {};
   };
@@ -628,11 +777,11 @@ Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, 
   RF_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   RF_CUDA(cudaEventRecord(ready, st));
   RF_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+  // panel i's product is queued before panel i+1 is copied: with a pageable
+  // source the host is busy staging panel i+1 while the GPU works on panel i
   Status s = copy(0);
   int64_t off = 0;
   for (size_t i = 0; i < panels.size() && s.ok(); ++i) {
-    if (i + 1 < panels.size()) s = copy(i + 1);
-    if (!s.ok()) break;
     const int64_t r0 = panels[i].first, rows = panels[i].second - r0;
     if (cudaStreamWaitEvent(st, ev[i], 0) != cudaSuccess) {
       s = make_err(RFGPU_ECUDA, "pass 1: stream wait failed");
@@ -640,6 +789,7 @@ Status pass1(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t ell, 
     }
     s = pass1_rows(c, a, G, ell, Y, ldy, ssq + off, r0, r0 + rows, oz, false);
     off += oz.on ? ozaki_ssq_slots(rows, a->n) : sumsq_slots(c, rows, ell, n);
+    if (s.ok() && i + 1 < panels.size()) s = copy(i + 1);
   }
   if (s.ok() && oz.on) {  // all rows landed: the A^T Q digits unless sliced per panel already
     Timed t(c, "ozaki_slice");
@@ -746,10 +896,18 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
     Timed tc(c, "chol");
     RF_CUDA(chol_inv(G2, cols, R2, R2i, cwork, info + 1, infod + 1, st));
   }
-  RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-  RF_CUDA(cudaMemcpyAsync(c->h_d, infod, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  RF_CUDA(cudaStreamSynchronize(st));
-  const bool fast = c->h_info[0] == 0 && c->h_info[1] == 0 && c->h_d[0] >= kCholGate;
+  bool fast;
+  if (c->spec) {  // decided at the end of the call (spec_flags)
+    rfgpu::orth_gate_kernel<<<1, 1, 0, st>>>(info, infod, kCholGate, c->spec_flags);
+    count_launch();
+    RF_CUDA(cudaGetLastError());
+    fast = true;
+  } else {
+    RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    RF_CUDA(cudaMemcpyAsync(c->h_d, infod, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RF_CUDA(cudaStreamSynchronize(st));
+    fast = c->h_info[0] == 0 && c->h_info[1] == 0 && c->h_d[0] >= kCholGate;
+  }
   if (fast) {
     out->fast = true;
     out->r = cols;
@@ -822,6 +980,12 @@ Status small_svd_of_bt(rfgpu_ctx* c, const double* Bt, int64_t n, int64_t ell, d
     Timed tj(c, "jacobi");
     RF_CUDA(jacobi_svd(Bt, n, ell, Vb, D, Ub, jw.d(), info, info + 1, st, /*sorted=*/true));
   }
+  if (c->spec) {  // convergence checked at the end of the call
+    rfgpu::jacobi_gate_kernel<<<1, 1, 0, st>>>(info, c->spec_flags);
+    count_launch();
+    RF_CUDA(cudaGetLastError());
+    return {};
+  }
   RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));
   if (std::getenv("RFGPU_DEBUG"))
@@ -889,6 +1053,11 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
   }
   // projection: B^T = A^T Q (finish_with_projection, rangefinder.cpp:24-30)
   if (Qb.r > 0) RF_TRY(pass_tn(c, a, Qb, Bt, tmp.d(), &oz));
+  if (c->spec) {  // read once at the end of the call (spec_finish)
+    RF_CUDA(cudaMemcpyAsync(c->spec_vals, scal.d(), sizeof(double), cudaMemcpyDeviceToDevice, st));
+    out->a_frob2 = -1.0;
+    return {};
+  }
   RF_CUDA(cudaMemcpyAsync(c->h_d, scal.d(), sizeof(double), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaStreamSynchronize(st));
   out->a_frob2 = c->h_d[0];
@@ -904,9 +1073,20 @@ Status materialize_q(rfgpu_ctx* c, int64_t m, const Basis& b, double* Qo, int64_
   return {};
 }
 
+constexpr int kSpecRetry = 100;  // internal: a speculative call must be re-run without speculation
+
 // frob_residual (rangefinder.cpp:45-54) from ||A||_F^2 and B^T on the device.
 Status frob_residual_dev(rfgpu_ctx* c, double a_frob2, const double* Bt, int64_t count, double* resid) {
   cudaStream_t st = c->stream;
+  if (c->spec) {  // ||B||_F^2 into spec_vals[1]; compared with ||A||_F^2 in spec_finish
+    DBuf part;
+    RF_TRY(part.alloc(sizeof(double) * 1024, st));
+    if (count > 0)
+      RF_CUDA(sumsq(Bt, count, part.d(), c->spec_vals + 1, st));
+    else
+      RF_CUDA(cudaMemsetAsync(c->spec_vals + 1, 0, sizeof(double), st));
+    return {};
+  }
   DBuf part, out;
   RF_TRY(part.alloc(sizeof(double) * 1024, st));
   RF_TRY(out.alloc(sizeof(double), st));
@@ -925,6 +1105,44 @@ Status frob_residual_dev(rfgpu_ctx* c, double a_frob2, const double* Bt, int64_t
   const double diff = a_frob * a_frob - bn * bn;
   if (resid) *resid = std::sqrt(std::max(0.0, diff));
   return {};
+}
+
+// End of a speculative call: the one host round trip. kSpecRetry when an orth
+// gate or a Jacobi failed (the caller re-runs without speculation), else the
+// frob_residual check and value.
+Status spec_finish(rfgpu_ctx* c, double* resid) {
+  cudaStream_t st = c->stream;
+  RF_CUDA(cudaMemcpyAsync(c->h_spec, c->spec_flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  RF_CUDA(cudaMemcpyAsync(static_cast<char*>(c->h_spec) + 16, c->spec_vals, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                          st));
+  RF_CUDA(cudaStreamSynchronize(st));
+  const int* fl = static_cast<const int*>(c->h_spec);
+  const double* v = reinterpret_cast<const double*>(static_cast<const char*>(c->h_spec) + 16);
+  if (fl[0] || fl[1]) {
+    if (std::getenv("RFGPU_DEBUG"))
+      std::fprintf(stderr, "[rfgpu] speculation failed (orth gate %d, jacobi %d): re-running\n", fl[0], fl[1]);
+    return make_err(kSpecRetry, "speculative CholeskyQR2 rejected");
+  }
+  const double a_frob = std::sqrt(v[0]), bn = std::sqrt(v[1]);
+  if (bn > a_frob * (1.0 + 1e-8))
+    return make_err(RFGPU_ENUMERICAL,
+                    "frob_residual: projection exceeds the total norm; basis orthonormality was lost upstream");
+  if (resid) *resid = std::sqrt(std::max(0.0, a_frob * a_frob - bn * bn));
+  return {};
+}
+
+// Runs body() speculatively (no host round trip inside; RFGPU_SPECULATE=0
+// disables) and again without speculation if the speculation failed.
+template <class F>
+Status with_speculation(rfgpu_ctx* c, F&& body) {
+  const char* e = std::getenv("RFGPU_SPECULATE");
+  if (e && e[0] == '0') return body();
+  RF_CUDA(cudaMemsetAsync(c->spec_flags, 0, 2 * sizeof(int), c->stream));
+  c->spec = true;
+  Status s = body();
+  c->spec = false;
+  if (s.code == kSpecRetry) s = body();
+  return s;
 }
 
 Status check_sample(const rfgpu_matrix* a, int64_t k, int64_t ell, const char* where) {
@@ -966,7 +1184,16 @@ Status rsvd_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t k
     RF_TRY(gemm(c, false, r, keep, r, b.R2inv, r, Ub.d(), r, Ub2.d(), r));
     ub = Ub2.d();
   }
-  if (Uhost && c->copy_stream && m >= 65536) {
+  if (Uhost && c->copy_stream && host_is_pageable(Uhost)) {
+    // pageable destination: lift, then read U back through the pinned ring (copy stream, host copy threads)
+    RF_TRY(gemm(c, false, m, keep, r, b.Q, b.ldq, ub, r, U, ldu, nullptr, "lift"));
+    cudaEvent_t lifted;
+    RF_CUDA(cudaEventCreateWithFlags(&lifted, cudaEventDisableTiming));
+    RF_CUDA(cudaEventRecord(lifted, st));
+    RF_CUDA(cudaStreamWaitEvent(c->copy_stream, lifted, 0));
+    cudaEventDestroy(lifted);
+    RF_TRY(staged_d2h(c, Uhost, ldh, U, ldu, m, keep, c->copy_stream));
+  } else if (Uhost && c->copy_stream && m >= 65536) {
     // Lift in row panels and read each one back on the copy stream while the next is computed. All the
     // GEMMs are queued before the first copy so a pageable destination (whose copy blocks the host)
     // cannot serialise them.
@@ -1016,6 +1243,7 @@ Status rsvd_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t k
   }
   RF_CUDA(cudaMemcpyAsync(V, Vb.d(), sizeof(double) * n * keep, cudaMemcpyDeviceToDevice, st));
   RF_CUDA(cudaMemcpyAsync(D, Dd.d(), sizeof(double) * keep, cudaMemcpyDeviceToDevice, st));
+  if (c->spec) RF_TRY(spec_finish(c, nullptr));
   *rank_out = keep;
   return {};
 }
@@ -1465,6 +1693,10 @@ void ctx_free(rfgpu_ctx* c) {
   if (c->h_d) cudaFreeHost(c->h_d);
   if (c->h_i64) cudaFreeHost(c->h_i64);
   if (c->h_stage) cudaFreeHost(c->h_stage);
+  for (void* sl : c->stage_slots) cudaFreeHost(sl);
+  for (cudaEvent_t e : c->stage_done) cudaEventDestroy(e);
+  if (c->h_spec) cudaFreeHost(c->h_spec);
+  if (c->spec_flags) cudaFree(c->spec_flags);
   if (c->copy_stream) {
     cudaStreamSynchronize(c->copy_stream);
     cudaStreamDestroy(c->copy_stream);
@@ -1501,7 +1733,9 @@ int ctx_create_common(int device, int rank, int world, rfgpu_ctx** out) {
   c->num_sms = prop.multiProcessorCount;
   bool ok = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaMallocHost(&c->h_info, 64) == cudaSuccess && cudaMallocHost(&c->h_d, 64) == cudaSuccess &&
-            cudaMallocHost(&c->h_i64, 64) == cudaSuccess;
+            cudaMallocHost(&c->h_i64, 64) == cudaSuccess && cudaMallocHost(&c->h_spec, 64) == cudaSuccess &&
+            cudaMalloc(&c->spec_flags, 64) == cudaSuccess;
+  if (ok) c->spec_vals = reinterpret_cast<double*>(c->spec_flags + 4);
   // freed pool memory stays cached (stream-ordered temporaries are reused call after call)
   cudaMemPoolProps pp{};
   pp.allocType = cudaMemAllocationTypePinned;
@@ -1763,10 +1997,14 @@ int rfgpu_range_finder(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int
     RF_TRY(Bd.alloc(sizeof(double) * n * ell, st));
     RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
     RangeOut ro;
-    RF_TRY(range_core(c, a, gd.d(), ell, q, reorth != 0, Q.d(), ldq, R2i.d(), Bt.d(), &ro));
-    const int64_t r = ro.basis.r;
     double res = 0.0;
-    RF_TRY(frob_residual_dev(c, ro.a_frob2, Bt.d(), n * r, &res));
+    RF_TRY(with_speculation(c, [&]() -> Status {
+      RF_TRY(range_core(c, a, gd.d(), ell, q, reorth != 0, Q.d(), ldq, R2i.d(), Bt.d(), &ro));
+      RF_TRY(frob_residual_dev(c, ro.a_frob2, Bt.d(), n * ro.basis.r, &res));
+      if (c->spec) RF_TRY(spec_finish(c, &res));
+      return {};
+    }));
+    const int64_t r = ro.basis.r;
     if (resid) *resid = res;
     if (ell_out) *ell_out = r;
     if (Qh) {
@@ -1792,7 +2030,9 @@ int rfgpu_rsvd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g_dev, 
     if (q < 0) return make_err(RFGPU_EPARAM, "power_range: q must be non-negative");
     RF_TRY(ensure_device(c));
     int64_t r = 0;
-    RF_TRY(rsvd_core(c, a, g_dev, k, ell, q, keep_over != 0, reorth != 0, U, std::max<int64_t>(1, a->m), D, V, &r));
+    RF_TRY(with_speculation(c, [&] {
+      return rsvd_core(c, a, g_dev, k, ell, q, keep_over != 0, reorth != 0, U, std::max<int64_t>(1, a->m), D, V, &r);
+    }));
     if (rank_out) *rank_out = r;
     return {};
   }();
@@ -1816,7 +2056,9 @@ int rfgpu_rsvd(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t k, 
     RF_TRY(V.alloc(sizeof(double) * n * ell, st));
     RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
     int64_t r = 0;
-    RF_TRY(rsvd_core(c, a, gd.d(), k, ell, q, keep_over != 0, reorth != 0, U.d(), ldu, D.d(), V.d(), &r));
+    RF_TRY(with_speculation(c, [&] {
+      return rsvd_core(c, a, gd.d(), k, ell, q, keep_over != 0, reorth != 0, U.d(), ldu, D.d(), V.d(), &r);
+    }));
     RF_TRY(copy_out(c, Uh, ldu, U.d(), ldu, m, r));
     RF_TRY(copy_out(c, Dh, std::max<int64_t>(1, r), D.d(), std::max<int64_t>(1, r), r, 1));
     RF_TRY(copy_out(c, Vh, n, V.d(), n, n, r));
@@ -1874,8 +2116,9 @@ int rfgpu_rsvd_host(rfgpu_ctx* c, const double* a, int64_t m, int64_t n, int64_t
     RF_TRY(V.alloc(sizeof(double) * n * ell, st));
     RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
     int64_t r = 0;
-    Status cs = rsvd_core(c, &h, gd.d(), k, ell, q, keep_over != 0, reorth != 0, U.d(), ldu, D.d(), V.d(), &r,
-                          Uh, ldu);
+    Status cs = with_speculation(c, [&] {
+      return rsvd_core(c, &h, gd.d(), k, ell, q, keep_over != 0, reorth != 0, U.d(), ldu, D.d(), V.d(), &r, Uh, ldu);
+    });
     if (!cs.ok()) {
       cudaStreamSynchronize(c->copy_stream);  // never leave a copy from or into the caller's buffers in flight
       return cs;
