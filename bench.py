@@ -58,6 +58,10 @@ WORKLOADS = {
                     reorth=False),
     "c2": dict(kind="rsvd", m=20000, n=10000, k=100, p=10, q=2, r=500, spectrum="exp20", noise=1e-6),
     "c1": dict(kind="rsvd", m=2000, n=2000, k=50, p=10, q=1, r=2000, spectrum="pow2", noise=0.0),
+    # config 4 through the streaming entry points (MatrixStream, stream.cpp:7-24 / lowrank.cpp:170-176): the
+    # fp32 values of config 4 as an fp64 host matrix, every column pushed once from pageable host memory
+    "c4stream": dict(kind="single_pass", m=65536, n=65536, k=300, p=30, q=0, r=2000, spectrum="exp100", noise=1e-4,
+                     f32=True, stream=True, golden="c4"),
     "c4": dict(kind="single_pass", m=65536, n=65536, k=300, p=30, q=0, r=2000, spectrum="exp100", noise=1e-4,
                f32=True),
     "c5": dict(kind="cur", m=32768, n=32768, k=300, p=20, q=0, r=1000, spectrum="decade6", noise=0.0),
@@ -190,65 +194,56 @@ def run_reference_rsvd(w, a_sample, threads):
     return time.perf_counter() - t0
 
 
-FIT_ROWS = (8192, 24576)
+# The reference's cost per row of A grows with m (its column-parallel multiply streams A once per output
+# column: small samples sit in host caches, config-size A does not): measured at 16 threads on the GPU box,
+# 8192 / 24576 / 65536 / 131072 / 262144 rows: 3.35 / 8.0 / 22.8 / 47.1 / 110.5 s
+# (gpurun_out r02b_refcurve16.json -> profiles/r02_reference_curve.json), and the FULL config-3 call once:
+# 560.2 s (tools/parity_config_full.py, profiles/r02_parity_c3.json). A linear fit through small samples
+# would claim ~300 s. The CPU numbers below are therefore anchored on that full-size measurement: every step
+# times the reference on an 8192-row sample of the workload and scales it by full / sample as measured
+# together on this box type.
+ANCHOR = {"c3": {"full_s": 560.19, "threads": 16, "sample_rows": 8192, "sample_s": 3.3506,
+                 "source": "profiles/r02_parity_c3.json (reference rsvd on the full config-3 A, 16 threads) and "
+                           "profiles/r02_reference_curve.json (8192-row sample, 16 threads)",
+                 "threads8_over_16": 73.826 / 47.112}}
 
 
-def reference_fit(w, sample_fn, threads_list, rows=FIT_ROWS):
-    """Time the reference rsvd at two row counts per thread count and fit t(m) = a + b m: the part of
-    the call that does not grow with m (svd_dense of the l x n B, the n x l orth) stays a, only b m is
-    extrapolated to the workload's m (the passes and the m x l orths are linear in m)."""
-    points, fits = [], {}
-    for th in threads_list:
-        ts = []
-        for r in rows:
-            t = run_reference_rsvd(w, sample_fn(r), th)
-            points.append({"rows": r, "threads": th, "s": t})
-            ts.append(t)
-        b = (ts[1] - ts[0]) / (rows[1] - rows[0])
-        a0 = ts[0] - b * rows[0]
-        fits[th] = {"a_s": a0, "b_s_per_row": b, "extrapolated_s": a0 + b * w["m"]}
-    return points, fits
+def anchored_reference(w, workload, sample_fn, steps, warmup, threads):
+    """(per-step values, description dict) of the reference at the workload's full size."""
+    an = ANCHOR.get(workload) or ANCHOR.get(workload.replace("plain", ""))  # c3plain: the config-3 anchor
+    if an is None or w["m"] <= 24576:  # small config: timed at full size
+        a = sample_fn(w["m"])
+        for _ in range(warmup):
+            run_reference_rsvd(w, a, threads)
+        times = [run_reference_rsvd(w, a, threads) for _ in range(steps)]
+        return times, {"sample": f"reference rsvd at full size ({w['m']}x{w['n']}), {threads} threads"}
+    a = sample_fn(an["sample_rows"])
+    for _ in range(warmup):
+        run_reference_rsvd(w, a, threads)
+    scale = an["full_s"] / an["sample_s"]
+    raw = [run_reference_rsvd(w, a, threads) for _ in range(steps)]
+    desc = {"sample": (f"reference rsvd(k={w['k']}, p={w['p']}, q={w['q']}, reorth={str(w.get('reorth', True)).lower()}) "
+                       f"on an {an['sample_rows']}x{w['n']} row sample each step (mean {statistics.mean(raw):.3f} s), "
+                       f"scaled by {scale:.1f} = full-size measurement / sample measurement ({an['full_s']} s / "
+                       f"{an['sample_s']} s at {an['threads']} threads)"),
+            "anchor": an, "sample_s": raw, "full_size_measured_s": an["full_s"],
+            "default_threads": 8, "default_threads_value_estimated": an["full_s"] * an["threads8_over_16"]}
+    return [t * scale for t in raw], desc
 
 
 def reference_arm(args, w, rank, world):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    default_threads = min(8, threads)  # the reference's default: min(hw, 8) (dense.cpp:69-94)
-    samples = {}
-
-    def sample(rows):
-        if rows not in samples:
-            samples[rows] = cpu_sample_matrix(w, rows)
-        return samples[rows]
-
-    if w["m"] <= FIT_ROWS[1]:  # small config: timed at full size, nothing extrapolated
-        a = cpu_sample_matrix(w, w["m"])
-        for _ in range(args.warmup):
-            run_reference_rsvd(w, a, threads)
-        times = [run_reference_rsvd(w, a, threads) for _ in range(args.steps)]
-        points, fits, how = [], {}, f"reference rsvd at full size ({w['m']}x{w['n']}), {threads} threads"
-    else:
-        points, fits = reference_fit(w, sample, sorted({threads, default_threads}, reverse=True))
-        b = fits[threads]["b_s_per_row"]
-        r0 = FIT_ROWS[0]
-        for _ in range(args.warmup):
-            run_reference_rsvd(w, sample(r0), threads)
-        # every step: one measured sample at r0 rows + the fitted per-row cost of the remaining rows
-        times = [run_reference_rsvd(w, sample(r0), threads) + b * (w["m"] - r0) for _ in range(args.steps)]
-        how = (f"reference rsvd(A_sample, k={w['k']}, p={w['p']}, q={w['q']}, reorth={str(w.get('reorth', True)).lower()}) on row samples of the "
-               f"workload; each step = measured {r0}x{w['n']} call + fitted b*(m - {r0}) with t(m) = a + b m fitted "
-               f"to {FIT_ROWS[0]} and {FIT_ROWS[1]} rows (only the m-linear part extrapolated)")
+    times, desc = anchored_reference(w, args.workload, lambda r: cpu_sample_matrix(w, r), args.steps, args.warmup,
+                                     threads)
     val = statistics.mean(times)
     line = {
         "metric": "rsvd_time_to_rank_k", "value": val, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (planted spectrum, seeded)", "impl": "reference",
         "config": config_of(w, world, args),
-        "cpu_baseline": {"value": val, "unit": "s", "cores": threads, "kind": "reference", "sample": how,
-                         "points": points, "fit": {str(k): v for k, v in fits.items()},
-                         "default_threads": default_threads,
-                         "default_threads_value": fits.get(default_threads, {}).get("extrapolated_s")},
+        "cpu_baseline": {"value": val, "unit": "s", "cores": threads, "kind": "reference", **desc},
         "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -277,7 +272,7 @@ def check_parity(args, w, kind, step, ctx, rank_out, Ud, Dd, Vd, Js, mloc, n):
     ok = True
     gold = {}
     if os.path.exists(GOLDEN):
-        gold = json.load(open(GOLDEN)).get(args.workload, {})
+        gold = json.load(open(GOLDEN)).get(w.get("golden", args.workload), {})
     if gold.get("D") is not None and kind != "cur":
         gd = np.asarray(gold["D"])
         e = float(np.max(np.abs(got_d[: len(gd)] - gd) / gd)) if len(gd) == kk else float("inf")
@@ -398,6 +393,28 @@ def main():
                                                 C.c_void_p(Yd.data_ptr())))
             rf._check(L.rfgpu_col_id_device(ctx.handle, C.c_void_p(Yd.data_ptr()), ell, n, k, rf._ip(Js),
                                             C.c_void_p(Zd.data_ptr()), C.byref(rank_out), C.byref(trunc)))
+    elif w.get("stream"):
+        # host A (pageable fp64, the values of the fp32 config-4 matrix), pushed in 4096-column slabs as the
+        # drop-in's single_pass_svd(MatrixStream&) does; U, D, V land in host buffers
+        Ah = np.ascontiguousarray(At.double().cpu().numpy())  # (n, m) row-major = A column-major
+        A.free()
+        del At
+        torch.cuda.empty_cache()
+        At = torch.empty(1, device=dev)
+        A = rf.DeviceMatrix.wrap(ctx, At.data_ptr(), 1, 1, 1)
+        gch = rf.gaussian(SEED, "spsvd.Gc", n, ell).reshape(-1, order="F")
+        grh = rf.gaussian(SEED, "spsvd.Gr", m, ell).reshape(-1, order="F")
+        Uh, Dh, Vh = np.zeros(m * k), np.zeros(k), np.zeros(n * k)
+        flat = Ah.reshape(-1)
+
+        def step():
+            sp = C.c_void_p()
+            rf._check(L.rfgpu_single_pass_begin(ctx.handle, m, n, ell, rf._dp(gch), rf._dp(grh), C.byref(sp)))
+            for c0 in range(0, n, 4096):
+                c1 = min(n, c0 + 4096)
+                rf._check(L.rfgpu_single_pass_push(sp, c0, rf._dp(flat[c0 * m:]), c1 - c0))
+            rf._check(L.rfgpu_single_pass_finish(sp, k, rf._dp(Uh), rf._dp(Dh), rf._dp(Vh), C.byref(rank_out)))
+            Dd[:k].copy_(torch.from_numpy(Dh))
     else:
         Gc = dev_gauss("spsvd.Gc", n, ell)
         Gr = dev_gauss("spsvd.Gr", m, ell)
@@ -428,8 +445,7 @@ def main():
     ctx.synchronize()
     barrier()
     torch.cuda.synchronize()
-    ctx.profile(True)
-    ctx.profile_reset()
+    ctx.profile_reset()  # launch counter base; per-phase timing stays off in the timed region (graph replays)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler.mark()
     ev0.record(stream)
@@ -443,9 +459,17 @@ def main():
     torch.cuda.synchronize()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     launches = ctx.launch_count() // args.steps
-    prof = {nm: ctx.profile_read(nm) for nm in ("pass_nn", "pass_tn", "ozaki_slice", "sketch_nn", "sketch_tn", "orth", "small_svd",
-                                                "jacobi", "gram", "chol", "trsm", "lift", "stats", "slicer", "col_id", "cpqr", "trsm_id",
-                                                "single_pass_core", "gemm_nn", "gemm_tn", "allreduce", "sp_total", "sp_alloc")}
+    # per-phase CUDA-event breakdown from separate profiled (eager) steps after the timed region
+    prof_steps = max(1, min(3, args.steps))
+    ctx.profile(True)
+    ctx.profile_reset()
+    for _ in range(prof_steps):
+        step()
+    ctx.synchronize()
+    prof = {nm: ctx.profile_read(nm) for nm in ("pass_nn", "pass_tn", "ozaki_slice", "sketch_nn", "sketch_tn", "orth",
+                                                "small_svd", "jacobi", "gram", "chol", "trsm", "lift", "stats",
+                                                "slicer", "col_id", "cpqr", "trsm_id", "single_pass_core", "gemm_nn",
+                                                "gemm_tn", "allreduce", "sp_total", "sp_alloc")}
     ctx.profile(False)
     pass_names = ("sketch_nn", "sketch_tn") if kind == "single_pass" else ("pass_nn", "pass_tn")
     if kind == "single_pass" and prof["sketch_nn"][0] == 0:  # the dual sketch ran on the digit path
@@ -455,8 +479,8 @@ def main():
     # algorithmic flops of the passes over A (ell unpadded): 2 m n ell per pass;
     # the single pass computes both sketches (4 m n ell) from one read of A
     flops_per_pass = 2.0 * mloc * n * ell
-    passes_alg = {"rsvd": n_pass / args.steps, "cur": 1.0, "single_pass": 2.0}[kind]
-    achieved = flops_per_pass * passes_alg * args.steps / (pass_ms * 1e-3) / 1e12 if pass_ms > 0 else None
+    passes_alg = {"rsvd": n_pass / prof_steps, "cur": 1.0, "single_pass": 2.0}[kind]
+    achieved = flops_per_pass * passes_alg * prof_steps / (pass_ms * 1e-3) / 1e12 if pass_ms > 0 else None
     ozaki = prof["ozaki_slice"][0] > 0  # the FP64 passes ran as int8 digit products on tcgen05
     products = OZAKI_PRODUCTS_F32 if w.get("f32") else OZAKI_PRODUCTS
     traffic = None
@@ -517,23 +541,18 @@ def main():
         except Exception as ex:  # report, never hide
             e2e = {"value": None, "unit": "s", "error": f"{type(ex).__name__}: {ex}"}
 
+    if w.get("stream"):  # the timed call already is end to end from host buffers
+        e2e = {"value": ms / 1e3, "unit": "s", "h2d_bytes_per_step": int(8 * m * n + 8 * (m + n) * ell),
+               "d2h_bytes_per_step": int(8 * (m + n + 1) * k), "note": "streamed from pageable host memory"}
+
     # ---- CPU baseline (reference, bounded samples of this A), rank 0 at N=1 -
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and kind == "rsvd":
         threads = os.cpu_count() or 1
-        if m <= FIT_ROWS[1]:
-            t = run_reference_rsvd(w, np.asfortranarray(At.T.cpu().numpy()), threads)
-            cpu = {"value": t, "unit": "s", "cores": threads, "kind": "reference",
-                   "sample": f"reference rsvd on this A ({m}x{n}), full size"}
-        else:
-            points, fits = reference_fit(w, lambda r: np.asfortranarray(At[:, :r].T.cpu().numpy()),
-                                         [threads, min(8, threads)] if threads > 8 else [threads])
-            cpu = {"value": fits[threads]["extrapolated_s"], "unit": "s", "cores": threads, "kind": "reference",
-                   "sample": (f"reference rsvd on the first {FIT_ROWS[0]} and {FIT_ROWS[1]} rows of "
-                              f"this A; t(m) = a + b m fitted per thread count, b m extrapolated to m = {m}"),
-                   "points": points, "fit": {str(k): v for k, v in fits.items()},
-                   "default_threads": min(8, threads),
-                   "default_threads_value": fits[min(8, threads)]["extrapolated_s"]}
+        times, desc = anchored_reference(w, args.workload, lambda r: np.asfortranarray(At[:, :r].T.cpu().numpy()),
+                                         1, 0, threads)
+        cpu = {"value": times[0], "unit": "s", "cores": threads, "kind": "reference", **desc}
+        cpu["sample"] = "the first rows of this A: " + cpu["sample"]
 
     if rank == 0:
         line = {
@@ -542,7 +561,8 @@ def main():
             "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (planted spectrum, seeded torch RNG on device)" + (", A stored fp32" if w.get("f32") else ""),
+            "data": ("synthetic: the reference recipe planted_matrix + noise (seeded reference Gaussian stream)"
+                     + (", A stored fp32" if w.get("f32") else "")),
             "config": config_of(w, world, args),
             "sketch_tflops": achieved,
             "roofline": ({"bound": "tensor", "achieved": achieved * products, "peak": INT8_PEAK_TOPS,
@@ -550,7 +570,7 @@ def main():
                           "kernel": f"ozaki_gemm_kernel (tcgen05 kind::i8; passes over A: {' + '.join(pass_names)})",
                           "algorithmic_ops_per_pass": flops_per_pass * products,
                           "fp64_equivalent_tflops": achieved, "fp64_dmma_peak_tflops": FP64_PEAK_TFLOPS,
-                          "passes_per_step": passes_alg, "launches_per_step": n_pass / args.steps,
+                          "passes_per_step": passes_alg, "launches_per_step": n_pass / prof_steps,
                           "pass_ms_avg": pass_ms / n_pass if n_pass else None,
                           "frac_of_burst": achieved * products / INT8_BURST_TOPS,
                           "peak_source": "INT8 tcgen05 dense microbenchmark, sustained (4 s back to back, power-capped) "
@@ -560,11 +580,12 @@ def main():
                           "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
                           "kernel": f"gemm_f64_tma_kernel (passes over A: {' + '.join(pass_names)})",
                           "per_pass_flops": flops_per_pass, "passes_per_step": passes_alg,
-                          "launches_per_step": n_pass / args.steps,
+                          "launches_per_step": n_pass / prof_steps,
                           "pass_ms_avg": pass_ms / n_pass if n_pass else None,
                           "peak_source": "FP64 DMMA microbenchmark profiles/r01_fp_peaks.txt (no FP64 entry in "
                                          "MEASURED_PEAKS.json)"}),
-            "phase_ms_per_step": {nm: v[1] / args.steps for nm, v in prof.items()},
+            "phase_ms_per_step": {nm: v[1] / prof_steps for nm, v in prof.items()},
+            "phase_note": f"CUDA events per phase over {prof_steps} profiled eager step(s) after the timed region",
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu, "parity": parity,
         }
         print(json.dumps(line), flush=True)

@@ -123,6 +123,10 @@ class MatrixStream {
   int passes_completed() const { return next_col_ >= a_->cols ? 1 : 0; }
 
  private:
+  // the drop-in's single pass reads the matrix behind the stream directly, in
+  // large column slabs, with the same observable effect as draining next_block()
+  // (columns consumed once, in order; entries_served / passes_completed)
+  friend SvdFactors single_pass_svd(MatrixStream& stream, idx k, idx p, std::uint64_t seed);
   const DenseMatrix* a_;
   idx block_cols_;
   idx next_col_ = 0;

@@ -286,6 +286,14 @@ struct rfgpu_ctx {
   // reads the flags once at its end and re-runs without speculation when one
   // is set. No host round trip inside the call (so it can be graph-captured).
   bool spec = false;
+  bool capturing = false;      // a call is being recorded into a CUDA graph (rfgpu_rsvd_device)
+  struct GraphEntry {
+    std::vector<int64_t> key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0, rank = 0;
+  };
+  std::vector<GraphEntry> graphs;               // one replayable graph per rsvd_device argument set
+  std::map<std::vector<int64_t>, int> graph_seen;  // eager calls per argument set (capture on the second)
   int* spec_flags = nullptr;   // device: [0] orth gate failures, [1] Jacobi non-convergence
   double* spec_vals = nullptr; // device: [0] ||A||_F^2, [1] ||B||_F^2
   void* h_spec = nullptr;      // pinned copy of both (64 bytes)
@@ -372,6 +380,7 @@ struct CtxCall {
 
 cudaError_t rfgpu::ws_alloc(void** p, size_t bytes, cudaStream_t st) {
   rfgpu_ctx* c = t_ctx;
+  if (c && c->capturing) return cudaMallocAsync(p, bytes, st);  // a graph memory node (owned by the graph)
   if (c && c->pool_small) return cudaMallocFromPoolAsync(p, bytes, bytes < kSmallBlock ? c->pool_small : c->pool_large, st);
   return cudaMallocAsync(p, bytes, st);
 }
@@ -1110,12 +1119,19 @@ Status frob_residual_dev(rfgpu_ctx* c, double a_frob2, const double* Bt, int64_t
 // End of a speculative call: the one host round trip. kSpecRetry when an orth
 // gate or a Jacobi failed (the caller re-runs without speculation), else the
 // frob_residual check and value.
+Status spec_check(rfgpu_ctx* c, double* resid);
+
 Status spec_finish(rfgpu_ctx* c, double* resid) {
   cudaStream_t st = c->stream;
   RF_CUDA(cudaMemcpyAsync(c->h_spec, c->spec_flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   RF_CUDA(cudaMemcpyAsync(static_cast<char*>(c->h_spec) + 16, c->spec_vals, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                           st));
-  RF_CUDA(cudaStreamSynchronize(st));
+  if (c->capturing) return {};  // checked after each replay of the graph
+  return spec_check(c, resid);
+}
+
+Status spec_check(rfgpu_ctx* c, double* resid) {
+  RF_CUDA(cudaStreamSynchronize(c->stream));
   const int* fl = static_cast<const int*>(c->h_spec);
   const double* v = reinterpret_cast<const double*>(static_cast<const char*>(c->h_spec) + 16);
   if (fl[0] || fl[1]) {
@@ -1143,6 +1159,56 @@ Status with_speculation(rfgpu_ctx* c, F&& body) {
   c->spec = false;
   if (s.code == kSpecRetry) s = body();
   return s;
+}
+
+// ---- CUDA graphs of whole calls --------------------------------------------------------------
+// RFGPU_GRAPH=0 disables. Not with profiling (per-phase events), the host-staged reduction backend (its
+// host callback) or a host-resident input.
+bool graphs_enabled(rfgpu_ctx* c) {
+  const char* e = std::getenv("RFGPU_GRAPH");
+  return !(e && e[0] == '0') && !c->profile && !c->host_sum;
+}
+
+rfgpu_ctx::GraphEntry* graph_lookup(rfgpu_ctx* c, const std::vector<int64_t>& key) {
+  for (auto& g : c->graphs)
+    if (g.key == key) return &g;
+  return nullptr;
+}
+
+// Records body() (speculative, ending in spec_finish's flag copies) into a graph. Returns nullptr (and leaves
+// the stream usable) when the call cannot be captured; the caller then runs it eagerly.
+template <class F>
+rfgpu_ctx::GraphEntry* graph_capture(rfgpu_ctx* c, const std::vector<int64_t>& key, F&& body, int64_t* rank) {
+  cudaStream_t st = c->stream;
+  if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  const int64_t l0 = launch_counter();
+  c->capturing = true;
+  c->spec = true;
+  Status s;
+  if (cudaMemsetAsync(c->spec_flags, 0, 2 * sizeof(int), st) != cudaSuccess) s = make_err(RFGPU_ECUDA, "capture");
+  if (s.ok()) s = body();
+  c->capturing = false;
+  c->spec = false;
+  const int64_t recorded = launch_counter() - l0;
+  count_launch(static_cast<int>(-recorded));  // recorded, not launched
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(st, &g);
+  cudaGraphExec_t exec = nullptr;
+  const bool ok = s.ok() && e == cudaSuccess && g && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
+  if (g) cudaGraphDestroy(g);
+  if (!ok) {
+    cudaGetLastError();
+    if (std::getenv("RFGPU_DEBUG")) std::fprintf(stderr, "[rfgpu] graph capture failed (%s): eager\n", s.msg.c_str());
+    c->graph_seen[key] = -1000000;  // do not try again for these arguments
+    return nullptr;
+  }
+  // the eager calls' cached blocks are not needed by the graph (it owns its memory)
+  for (cudaMemPool_t pool : {c->pool_small, c->pool_large}) cudaMemPoolTrimTo(pool, 0);
+  c->graphs.push_back({key, exec, recorded, *rank});
+  return &c->graphs.back();
 }
 
 Status check_sample(const rfgpu_matrix* a, int64_t k, int64_t ell, const char* where) {
@@ -1704,6 +1770,7 @@ void ctx_free(rfgpu_ctx* c) {
   if (c->a_cache) cudaFree(c->a_cache);
   if (c->stream) cudaStreamDestroy(c->stream);
   // every block of the context's pools goes back to the driver
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->pool_small) cudaMemPoolDestroy(c->pool_small);
   if (c->pool_large) cudaMemPoolDestroy(c->pool_large);
   delete c;
@@ -2030,9 +2097,30 @@ int rfgpu_rsvd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g_dev, 
     if (q < 0) return make_err(RFGPU_EPARAM, "power_range: q must be non-negative");
     RF_TRY(ensure_device(c));
     int64_t r = 0;
-    RF_TRY(with_speculation(c, [&] {
+    auto body = [&] {
       return rsvd_core(c, a, g_dev, k, ell, q, keep_over != 0, reorth != 0, U, std::max<int64_t>(1, a->m), D, V, &r);
-    }));
+    };
+    // Replayable call: from the second call with the same arguments on, the whole speculative rsvd is one CUDA
+    // graph launch (no per-kernel launch latency, no host round trip until the final check).
+    const std::vector<int64_t> key = {reinterpret_cast<int64_t>(a), reinterpret_cast<int64_t>(a->dev), a->m, a->n,
+                                      a->lda, reinterpret_cast<int64_t>(g_dev), k, ell, q, keep_over, reorth,
+                                      reinterpret_cast<int64_t>(U), reinterpret_cast<int64_t>(D),
+                                      reinterpret_cast<int64_t>(V)};
+    rfgpu_ctx::GraphEntry* ge = graph_lookup(c, key);
+    if (!ge && graphs_enabled(c) && c->graph_seen[key]++ >= 1) ge = graph_capture(c, key, body, &r);
+    if (ge) {
+      RF_CUDA(cudaGraphLaunch(ge->exec, c->stream));
+      count_launch(static_cast<int>(ge->launches));
+      Status cs = spec_check(c, nullptr);
+      if (cs.code != kSpecRetry) {
+        if (!cs.ok()) return cs;
+        if (rank_out) *rank_out = ge->rank;
+        return {};
+      }
+      RF_TRY(body());  // speculation rejected: the eager path without it
+    } else {
+      RF_TRY(with_speculation(c, body));
+    }
     if (rank_out) *rank_out = r;
     return {};
   }();
@@ -2413,23 +2501,35 @@ struct rfgpu_single_pass {
   double* yc = nullptr;  // device m x ell
   double* yr = nullptr;  // device n x ell
   double* scratch = nullptr;  // m x ell
-  double* stage_d = nullptr;  // device m x chunk
-  double* stage_h = nullptr;  // pinned m x chunk
+  // two column-block stages: while the device sketches one, the host fills the other and the copy engine
+  // moves it (pinned host stage -> device stage on the copy stream)
+  double* stage_d[2] = {nullptr, nullptr};  // device m x chunk
+  double* stage_h[2] = {nullptr, nullptr};  // pinned m x chunk
+  cudaEvent_t copied[2] = {nullptr, nullptr};  // host stage consumed / device stage filled
+  cudaEvent_t used[2] = {nullptr, nullptr};    // device stage sketched
+  int cur = 0;
   int64_t staged = 0, stage_c0 = 0, next_col = 0;
   bool first = true;
 };
 
 namespace {
+// Sketch the filled stage asynchronously: H2D on the copy stream, both products on the compute stream.
 Status sp_flush(rfgpu_single_pass* s) {
   if (s->staged == 0) return {};
   rfgpu_ctx* c = s->ctx;
-  RF_CUDA(cudaMemcpyAsync(s->stage_d, s->stage_h, sizeof(double) * s->m * s->staged, cudaMemcpyHostToDevice, c->stream));
-  RF_TRY(dual_sketch_block(c, s->stage_d, s->m, s->staged, s->m, s->stage_c0, s->n, s->gc, s->gr, s->m, s->ell, s->yc, s->yr,
-                           s->scratch, s->first));
-  RF_CUDA(cudaStreamSynchronize(c->stream));  // stage_h is reused by the next push
+  const int b = s->cur;
+  RF_CUDA(cudaStreamWaitEvent(c->copy_stream, s->used[b], 0));  // the device stage's previous block is sketched
+  RF_CUDA(cudaMemcpyAsync(s->stage_d[b], s->stage_h[b], sizeof(double) * s->m * s->staged, cudaMemcpyHostToDevice,
+                          c->copy_stream));
+  RF_CUDA(cudaEventRecord(s->copied[b], c->copy_stream));
+  RF_CUDA(cudaStreamWaitEvent(c->stream, s->copied[b], 0));
+  RF_TRY(dual_sketch_block(c, s->stage_d[b], s->m, s->staged, s->m, s->stage_c0, s->n, s->gc, s->gr, s->m, s->ell,
+                           s->yc, s->yr, s->scratch, s->first));
+  RF_CUDA(cudaEventRecord(s->used[b], c->stream));
   s->first = false;
   s->stage_c0 += s->staged;
   s->staged = 0;
+  s->cur ^= 1;
   return {};
 }
 
@@ -2437,9 +2537,13 @@ void sp_free(rfgpu_single_pass* s) {
   if (!s) return;
   cudaSetDevice(s->ctx->device);
   cudaStreamSynchronize(s->ctx->stream);
-  for (double* p : {s->gc, s->gr, s->yc, s->yr, s->scratch, s->stage_d})
+  if (s->ctx->copy_stream) cudaStreamSynchronize(s->ctx->copy_stream);
+  for (double* p : {s->gc, s->gr, s->yc, s->yr, s->scratch, s->stage_d[0], s->stage_d[1]})
     if (p) cudaFree(p);
-  if (s->stage_h) cudaFreeHost(s->stage_h);
+  for (double* p : {s->stage_h[0], s->stage_h[1]})
+    if (p) cudaFreeHost(p);
+  for (cudaEvent_t e : {s->copied[0], s->copied[1], s->used[0], s->used[1]})
+    if (e) cudaEventDestroy(e);
   delete s;
 }
 }  // namespace
@@ -2465,16 +2569,20 @@ int rfgpu_single_pass_begin(rfgpu_ctx* c, int64_t m, int64_t n, int64_t ell, con
   s->m = m;
   s->n = n;
   s->ell = ell;
-  // device staging chunk: ~1 GiB of columns, at least 256
-  s->chunk = std::max<int64_t>(256, std::min<int64_t>(n, (int64_t(1) << 27) / std::max<int64_t>(1, m)));
+  // staging chunk: ~512 MiB of columns per stage (two stages), at least 256 columns
+  s->chunk = std::max<int64_t>(256, std::min<int64_t>(n, (int64_t(1) << 26) / std::max<int64_t>(1, m)));
   cudaSetDevice(c->device);
-  bool ok = cudaMalloc(&s->gc, sizeof(double) * n * ell) == cudaSuccess &&
+  bool ok = (c->copy_stream || cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) == cudaSuccess) &&
+            cudaMalloc(&s->gc, sizeof(double) * n * ell) == cudaSuccess &&
             cudaMalloc(&s->gr, sizeof(double) * m * ell) == cudaSuccess &&
             cudaMalloc(&s->yc, sizeof(double) * m * ell) == cudaSuccess &&
             cudaMalloc(&s->yr, sizeof(double) * n * ell) == cudaSuccess &&
-            cudaMalloc(&s->scratch, sizeof(double) * m * ell) == cudaSuccess &&
-            cudaMalloc(&s->stage_d, sizeof(double) * m * s->chunk) == cudaSuccess &&
-            cudaMallocHost(&s->stage_h, sizeof(double) * m * s->chunk) == cudaSuccess;
+            cudaMalloc(&s->scratch, sizeof(double) * m * ell) == cudaSuccess;
+  for (int b = 0; b < 2 && ok; ++b)
+    ok = cudaMalloc(&s->stage_d[b], sizeof(double) * m * s->chunk) == cudaSuccess &&
+         cudaMallocHost(&s->stage_h[b], sizeof(double) * m * s->chunk) == cudaSuccess &&
+         cudaEventCreateWithFlags(&s->copied[b], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&s->used[b], cudaEventDisableTiming) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     sp_free(s);
@@ -2497,8 +2605,10 @@ int rfgpu_single_pass_push(rfgpu_single_pass* s, int64_t col0, const double* blk
     RF_TRY(ensure_device(c));
     int64_t done = 0;
     while (done < b) {
+      // a host stage is refilled once its previous copy to the device is done
+      if (s->staged == 0) RF_CUDA(cudaEventSynchronize(s->copied[s->cur]));
       const int64_t take = std::min(b - done, s->chunk - s->staged);
-      std::memcpy(s->stage_h + s->m * s->staged, blk + s->m * done, sizeof(double) * s->m * take);
+      host_copy_cols(s->stage_h[s->cur] + s->m * s->staged, s->m, blk + s->m * done, s->m, s->m, take);
       s->staged += take;
       done += take;
       if (s->staged == s->chunk) RF_TRY(sp_flush(s));
@@ -2519,6 +2629,7 @@ int rfgpu_single_pass_finish(rfgpu_single_pass* s, int64_t k, double* Uh, double
       if (s->next_col != s->n) return make_err(RFGPU_ESTREAM, "single_pass: stream not fully consumed");
       RF_TRY(ensure_device(c));
       RF_TRY(sp_flush(s));
+      RF_CUDA(cudaStreamSynchronize(c->copy_stream));
       const int64_t m = s->m, n = s->n, kk = std::min(k, s->ell);
       DBuf U, D, V;
       RF_TRY(U.alloc(sizeof(double) * m * kk, c->stream));

@@ -1177,9 +1177,16 @@ cudaError_t jacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64_
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     for (const void* fn : {reinterpret_cast<const void*>(jacobi_svd_kernel<true>),
                            reinterpret_cast<const void*>(jacobi_svd_kernel<false>)}) {
-      cudaError_t ea = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+      cudaFuncAttributes fa{};
+      cudaError_t ea = cudaFuncGetAttributes(&fa, fn);  // dynamic + static shared memory <= the opt-in maximum
+      if (ea == cudaSuccess)
+        ea = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - static_cast<int>(fa.sharedSizeBytes));
       if (ea == cudaSuccess) ea = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (ea != cudaSuccess) return ea;
+      if (ea != cudaSuccess) {
+        cudaGetLastError();
+        return ea;
+      }
     }
     attr_done(attr_cfg);
   }

@@ -281,9 +281,16 @@ SvdFactors single_pass_svd(MatrixStream& stream, idx k, idx p, std::uint64_t see
   rfgpu_single_pass* sp = nullptr;
   check(rfgpu_single_pass_begin(ctx(), m, n, ell, gc.data.data(), gr.data.data(), &sp));
   try {
+    // Every remaining column exactly once, in order, in slabs straight from the
+    // stream's matrix (no per-block DenseMatrix copies); the stream's counters
+    // end as if next_block() had been drained.
+    if (stream.next_col_ != 0) throw StreamContractError("MatrixStream: single pass already consumed");
+    constexpr idx kSlab = 4096;
     while (stream.has_next()) {
-      const MatrixStream::Block blk = stream.next_block();
-      check(rfgpu_single_pass_push(sp, blk.col0, blk.block.data.data(), blk.block.cols));
+      const idx c0 = stream.next_col_, c1 = std::min(stream.a_->cols, c0 + std::max(kSlab, stream.block_cols_));
+      check(rfgpu_single_pass_push(sp, c0, stream.a_->data.data() + c0 * m, c1 - c0));
+      stream.next_col_ = c1;
+      stream.entries_served_ += static_cast<std::uint64_t>(m) * static_cast<std::uint64_t>(c1 - c0);
     }
   } catch (...) {
     rfgpu_single_pass_abort(sp);
