@@ -120,6 +120,13 @@ class Oracle:
         self._check(self._fn("planted")(_i64(m), _i64(n), _dp(s), _i64(len(s)), _u64(seed), _dp(out)))
         return out.reshape((m, n), order="F")
 
+    def test_planted(self, m: int, n: int, sigma, seed: int) -> np.ndarray:
+        """The reference test suite's planted() (tests/test_support.hpp:37-46; reference only)."""
+        s = np.ascontiguousarray(sigma, dtype=np.float64)
+        out = np.empty(m * n)
+        self._check(self._fn("test_planted")(_i64(m), _i64(n), _dp(s), _i64(len(s)), _u64(seed), _dp(out)))
+        return out.reshape((m, n), order="F")
+
     # ---------------------------------------------------------------- dense
     def multiply(self, a, b, ta=False, tb=False) -> np.ndarray:
         a, b = fmat(a), fmat(b)

@@ -240,6 +240,18 @@ int rfref_frob_residual(double a_frob, const double* b, int64_t m, int64_t n, do
     return guard([&] { *out = rf::frob_residual(a_frob, wrap(b, m, n)); });
 }
 
+// tests/test_support.hpp:37-46 (the reference suite's planted(): Haar factors from the "planted.u" /
+// "planted.v" streams), for re-expressing the reference's own tests on their own data
+int rfref_test_planted(int64_t m, int64_t n, const double* sigma, int64_t r, uint64_t seed, double* a_out) {
+    return guard([&] {
+        rf::DenseMatrix u = rf::householder_qr(rf::gaussian(seed, "planted.u", m, r)).first;
+        rf::DenseMatrix v = rf::householder_qr(rf::gaussian(seed, "planted.v", n, r)).first;
+        for (int64_t j = 0; j < r; ++j)
+            for (int64_t i = 0; i < m; ++i) u(i, j) *= sigma[j];
+        put(rf::multiply(u, v, false, true), a_out);
+    });
+}
+
 // matrix_io.cpp:224-233: the reference reader (rows/cols out; data into a
 // buffer the caller frees with rfref_free)
 int rfref_read_matrix(const char* path, int64_t* rows, int64_t* cols, double** data) {

@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -242,6 +244,80 @@ constexpr int kNcclSum = 0;     // ncclSum
 }  // namespace
 
 // ============================================================ context ====
+// Persistent host worker threads for the staging copies (pageable <-> pinned):
+// run(n, fn) executes fn(0..n-1) across the workers and the calling thread.
+class HostPool {
+ public:
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void run(int n, const std::function<void(int)>& fn) {
+    if (n <= 1 || workers() == 0) {
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      n_ = n;
+      next_.store(0);
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ == n_; });
+    fn_ = nullptr;
+  }
+  int workers() {
+    std::call_once(once_, [&] {
+      const int nt = static_cast<int>(std::max(1u, std::thread::hardware_concurrency())) - 1;
+      for (int i = 0; i < std::min(nt, 31); ++i) th_.emplace_back([this] { loop(); });
+    });
+    return static_cast<int>(th_.size());
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      const int i = next_.fetch_add(1);
+      if (i >= n_) return;
+      (*fn_)(i);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (++done_ == n_) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        if (!fn_) continue;
+      }
+      work();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  std::vector<std::thread> th_;
+  std::once_flag once_;
+  const std::function<void(int)>* fn_ = nullptr;
+  std::atomic<int> next_{0};
+  int n_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 struct rfgpu_ctx {
   int device = 0, rank = 0, world = 1;
   int num_sms = 148;
@@ -268,6 +344,7 @@ struct rfgpu_ctx {
   cudaStream_t copy_stream = nullptr;
   // pinned staging ring for pageable host buffers (host copy threads fill a
   // slot, the copy engine moves it; a slot is refilled once its copy is done)
+  HostPool host_pool;
   std::vector<void*> stage_slots;
   std::vector<cudaEvent_t> stage_done;
   size_t stage_bytes = 0;
@@ -294,6 +371,7 @@ struct rfgpu_ctx {
   };
   std::vector<GraphEntry> graphs;               // one replayable graph per rsvd_device argument set
   std::map<std::vector<int64_t>, int> graph_seen;  // eager calls per argument set (capture on the second)
+  std::map<std::vector<int64_t>, bool> spec_failed;  // argument sets whose speculation was rejected: run eagerly
   int* spec_flags = nullptr;   // device: [0] orth gate failures, [1] Jacobi non-convergence
   double* spec_vals = nullptr; // device: [0] ||A||_F^2, [1] ||B||_F^2
   void* h_spec = nullptr;      // pinned copy of both (64 bytes)
@@ -670,11 +748,12 @@ Status stage_ring(rfgpu_ctx* c) {
   return {};
 }
 
-// Parallel strided copy of `cols` columns of `rows` doubles (ld_src -> ld_dst) on the host.
-void host_copy_cols(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows, int64_t cols) {
+// Parallel strided copy of `cols` columns of `rows` doubles (ld_src -> ld_dst) on the host (the context's
+// worker threads; 16 MiB or so per task).
+void host_copy_cols(rfgpu_ctx* c, double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                    int64_t cols) {
   const int64_t bytes = rows * cols * 8;
-  const int nt = static_cast<int>(std::max<int64_t>(
-      1, std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), bytes >> 22)));
+  const int nt = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, bytes >> 24)));
   auto part = [&](int t) {
     if (cols >= nt) {
       for (int64_t j = cols * t / nt; j < cols * (t + 1) / nt; ++j)
@@ -684,14 +763,7 @@ void host_copy_cols(double* dst, int64_t ldd, const double* src, int64_t lds, in
       for (int64_t j = 0; j < cols; ++j) std::memcpy(dst + j * ldd + r0, src + j * lds + r0, sizeof(double) * (r1 - r0));
     }
   };
-  if (nt == 1) {
-    part(0);
-    return;
-  }
-  std::vector<std::thread> th;
-  for (int t = 1; t < nt; ++t) th.emplace_back(part, t);
-  part(0);
-  for (auto& x : th) x.join();
+  c->host_pool.run(nt, part);
 }
 
 // H2D of rows x cols (column-major, ld lds) from pageable host memory into the
@@ -710,7 +782,7 @@ Status staged_h2d(rfgpu_ctx* c, double* dev, int64_t ldd, const double* host, in
       const size_t sl = c->stage_next++ % c->stage_slots.size();
       RF_CUDA(cudaEventSynchronize(c->stage_done[sl]));  // the slot's previous copy has landed
       double* buf = static_cast<double*>(c->stage_slots[sl]);
-      host_copy_cols(buf, rr, host + c0 * lds + r0, lds, rr, cc);
+      host_copy_cols(c, buf, rr, host + c0 * lds + r0, lds, rr, cc);
       RF_CUDA(cudaMemcpy2DAsync(dev + c0 * ldd + r0, sizeof(double) * ldd, buf, sizeof(double) * rr, sizeof(double) * rr,
                                 cc, cudaMemcpyHostToDevice, cs));
       RF_CUDA(cudaEventRecord(c->stage_done[sl], cs));
@@ -735,7 +807,7 @@ Status staged_d2h(rfgpu_ctx* c, double* host, int64_t ldh, const double* dev, in
       const Pending pd = q.front();
       q.erase(q.begin());
       RF_CUDA(cudaEventSynchronize(c->stage_done[pd.slot]));
-      host_copy_cols(host + pd.c0 * ldh + pd.r0, ldh, static_cast<double*>(c->stage_slots[pd.slot]), pd.rr, pd.rr, pd.cc);
+      host_copy_cols(c, host + pd.c0 * ldh + pd.r0, ldh, static_cast<double*>(c->stage_slots[pd.slot]), pd.rr, pd.rr, pd.cc);
     }
     return {};
   };
@@ -847,8 +919,12 @@ bool digit_grams() {
   return !(e && e[0] == '0');
 }
 
+// single = true: CholeskyQR (one Gram) only — a basis of range(X) that is orthonormal only to ~eps kappa(X)^2,
+// for an intermediate power-iteration basis whose one consumer is a product followed by another orth: for
+// Q1 = Q S (S upper triangular, near identity) the next orthonormalised basis is the same matrix (the QR factor
+// with positive R diagonal is unique), so the second Gram, Cholesky and fold are skipped.
 Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx, Basis* out, double* R2inv_buf,
-            double* R, bool dist, bool fold, OzPasses* oz = nullptr) {
+            double* R, bool dist, bool fold, OzPasses* oz = nullptr, bool single = false) {
   Timed t(c, "orth");
   out->r = 0;
   out->folded = false;
@@ -869,9 +945,9 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
   double* cwork = infod + 8;  // chol_inv_work_bytes(cols)
   int* info = reinterpret_cast<int*>(infod + 4);
   DBuf q1buf;
-  double* Q1 = out->Q;  // folded: Q1 lands directly in the output buffer
+  double* Q1 = out->Q;  // folded or single: Q1 lands directly in the output buffer
   int64_t ldq1 = out->ldq;
-  if (!fold) {
+  if (!fold && !single) {
     ldq1 = even(m);
     RF_TRY(q1buf.alloc(sizeof(double) * std::max<int64_t>(1, ldq1 * cols), st));
     Q1 = q1buf.d();
@@ -899,9 +975,11 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
   // (an INT8 digit-path TRSM from X's digits measured 4.1 ms against 2.9 ms on DMMA at config 3: K = l is too
   // short for the digit GEMM's per-tile fetch and epilogue)
   RF_TRY(gemm(c, false, m, cols, cols, X, ldx, R1i, cols, Q1, ldq1, nullptr, "trsm", false, /*tri_b=*/true));
-  RF_TRY(gram(Q1, ldq1, G2));
-  if (dist) RF_TRY(allreduce(c, G2, cc));
-  {
+  if (single) {
+    RF_CUDA(cudaMemsetAsync(info + 1, 0, sizeof(int), st));
+  } else {
+    RF_TRY(gram(Q1, ldq1, G2));
+    if (dist) RF_TRY(allreduce(c, G2, cc));
     Timed tc(c, "chol");
     RF_CUDA(chol_inv(G2, cols, R2, R2i, cwork, info + 1, infod + 1, st));
   }
@@ -916,6 +994,12 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
     RF_CUDA(cudaMemcpyAsync(c->h_d, infod, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     RF_CUDA(cudaStreamSynchronize(st));
     fast = c->h_info[0] == 0 && c->h_info[1] == 0 && c->h_d[0] >= kCholGate;
+  }
+  if (fast && single) {  // the CholeskyQR basis itself (already in out->Q)
+    out->fast = true;
+    out->r = cols;
+    if (R) RF_CUDA(cudaMemcpyAsync(R, R1, sizeof(double) * cc, cudaMemcpyDeviceToDevice, st));
+    return {};
   }
   if (fast) {
     out->fast = true;
@@ -1045,19 +1129,21 @@ Status range_core(rfgpu_ctx* c, const rfgpu_matrix* a, const double* G, int64_t 
     }
     RF_TRY(orth(c, y.d(), m, ell, ldq, &Qb, R2ibuf, nullptr, true, true, &oz));
   } else {
-    RF_TRY(orth(c, y.d(), m, ell, ldq, &Qb, R2ibuf, nullptr, true, true, &oz));
+    // every basis but the last only feeds the next product: CholeskyQR (one Gram) suffices for it (orth's
+    // `single`); the last one (B = Q^T A, U = Q Ub) is CholeskyQR2
+    RF_TRY(orth(c, y.d(), m, ell, ldq, &Qb, R2ibuf, nullptr, true, true, &oz, /*single=*/q > 0));
     for (int64_t j = 0; j < q && Qb.r > 0; ++j) {
       RF_TRY(pass_tn(c, a, Qb, z.d(), tmp.d(), &oz));
       Basis Wb;
       Wb.Q = w.d();
       Wb.ldq = n;
-      RF_TRY(orth(c, z.d(), n, Qb.r, n, &Wb, nullptr, nullptr, false, false));
+      RF_TRY(orth(c, z.d(), n, Qb.r, n, &Wb, nullptr, nullptr, false, false, nullptr, /*single=*/true));
       if (Wb.r == 0) {
         Qb.r = 0;
         break;
       }
       RF_TRY(pass_nn(c, a, w.d(), Wb.r, y.d(), ldq, &oz));
-      RF_TRY(orth(c, y.d(), m, Wb.r, ldq, &Qb, R2ibuf, nullptr, true, true, &oz));
+      RF_TRY(orth(c, y.d(), m, Wb.r, ldq, &Qb, R2ibuf, nullptr, true, true, &oz, /*single=*/j + 1 < q));
     }
   }
   // projection: B^T = A^T Q (finish_with_projection, rangefinder.cpp:24-30)
@@ -1149,15 +1235,25 @@ Status spec_check(rfgpu_ctx* c, double* resid) {
 
 // Runs body() speculatively (no host round trip inside; RFGPU_SPECULATE=0
 // disables) and again without speculation if the speculation failed.
+// Argument set of a call (entry point, matrix, shape, sketch parameters) for the per-context memo of
+// rejected speculations and recorded graphs.
+std::vector<int64_t> call_key(int entry, const rfgpu_matrix* a, int64_t k, int64_t ell, int64_t q, int reorth) {
+  return {entry, reinterpret_cast<int64_t>(a), reinterpret_cast<int64_t>(a ? a->dev : nullptr), a ? a->m : 0,
+          a ? a->n : 0, a ? a->lda : 0, k, ell, q, reorth};
+}
+
 template <class F>
-Status with_speculation(rfgpu_ctx* c, F&& body) {
+Status with_speculation(rfgpu_ctx* c, const std::vector<int64_t>& key, F&& body) {
   const char* e = std::getenv("RFGPU_SPECULATE");
-  if (e && e[0] == '0') return body();
+  if ((e && e[0] == '0') || c->spec_failed.count(key)) return body();
   RF_CUDA(cudaMemsetAsync(c->spec_flags, 0, 2 * sizeof(int), c->stream));
   c->spec = true;
   Status s = body();
   c->spec = false;
-  if (s.code == kSpecRetry) s = body();
+  if (s.code == kSpecRetry) {  // the same arguments will fail again (rank-deficient or plain-mode sketch)
+    c->spec_failed[key] = true;
+    s = body();
+  }
   return s;
 }
 
@@ -1167,6 +1263,17 @@ Status with_speculation(rfgpu_ctx* c, F&& body) {
 bool graphs_enabled(rfgpu_ctx* c) {
   const char* e = std::getenv("RFGPU_GRAPH");
   return !(e && e[0] == '0') && !c->profile && !c->host_sum;
+}
+
+void graph_drop(rfgpu_ctx* c, const std::vector<int64_t>& key) {
+  for (size_t i = 0; i < c->graphs.size(); ++i)
+    if (c->graphs[i].key == key) {
+      cudaGraphExecDestroy(c->graphs[i].exec);
+      c->graphs.erase(c->graphs.begin() + static_cast<long>(i));
+      break;
+    }
+  c->graph_seen[key] = -1000000;
+  cudaDeviceGraphMemTrim(c->device);  // the dropped graph's memory back to the driver
 }
 
 rfgpu_ctx::GraphEntry* graph_lookup(rfgpu_ctx* c, const std::vector<int64_t>& key) {
@@ -2065,7 +2172,7 @@ int rfgpu_range_finder(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int
     RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
     RangeOut ro;
     double res = 0.0;
-    RF_TRY(with_speculation(c, [&]() -> Status {
+    RF_TRY(with_speculation(c, call_key(1, a, 0, ell, q, reorth), [&]() -> Status {
       RF_TRY(range_core(c, a, gd.d(), ell, q, reorth != 0, Q.d(), ldq, R2i.d(), Bt.d(), &ro));
       RF_TRY(frob_residual_dev(c, ro.a_frob2, Bt.d(), n * ro.basis.r, &res));
       if (c->spec) RF_TRY(spec_finish(c, &res));
@@ -2107,19 +2214,28 @@ int rfgpu_rsvd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g_dev, 
                                       reinterpret_cast<int64_t>(U), reinterpret_cast<int64_t>(D),
                                       reinterpret_cast<int64_t>(V)};
     rfgpu_ctx::GraphEntry* ge = graph_lookup(c, key);
-    if (!ge && graphs_enabled(c) && c->graph_seen[key]++ >= 1) ge = graph_capture(c, key, body, &r);
+    if (!ge && graphs_enabled(c) && !c->spec_failed.count(key) && c->graph_seen[key]++ >= 1)
+      ge = graph_capture(c, key, body, &r);
     if (ge) {
-      RF_CUDA(cudaGraphLaunch(ge->exec, c->stream));
-      count_launch(static_cast<int>(ge->launches));
-      Status cs = spec_check(c, nullptr);
-      if (cs.code != kSpecRetry) {
-        if (!cs.ok()) return cs;
-        if (rank_out) *rank_out = ge->rank;
-        return {};
+      cudaError_t le = cudaGraphLaunch(ge->exec, c->stream);
+      Status cs;
+      if (le == cudaSuccess) {
+        count_launch(static_cast<int>(ge->launches));
+        cs = spec_check(c, nullptr);
+        if (cs.code != kSpecRetry) {
+          if (!cs.ok()) return cs;
+          if (rank_out) *rank_out = ge->rank;
+          return {};
+        }
+        c->spec_failed[key] = true;  // speculation rejected: these arguments run eagerly from now on
+      } else {
+        cudaGetLastError();  // e.g. no room for the graph's memory next to the eager pools: eager from now on
+        cudaStreamSynchronize(c->stream);
       }
-      RF_TRY(body());  // speculation rejected: the eager path without it
+      graph_drop(c, key);
+      RF_TRY(body());
     } else {
-      RF_TRY(with_speculation(c, body));
+      RF_TRY(with_speculation(c, key, body));
     }
     if (rank_out) *rank_out = r;
     return {};
@@ -2144,7 +2260,7 @@ int rfgpu_rsvd(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int64_t k, 
     RF_TRY(V.alloc(sizeof(double) * n * ell, st));
     RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
     int64_t r = 0;
-    RF_TRY(with_speculation(c, [&] {
+    RF_TRY(with_speculation(c, call_key(2, a, k, ell, q, reorth), [&] {
       return rsvd_core(c, a, gd.d(), k, ell, q, keep_over != 0, reorth != 0, U.d(), ldu, D.d(), V.d(), &r);
     }));
     RF_TRY(copy_out(c, Uh, ldu, U.d(), ldu, m, r));
@@ -2204,7 +2320,7 @@ int rfgpu_rsvd_host(rfgpu_ctx* c, const double* a, int64_t m, int64_t n, int64_t
     RF_TRY(V.alloc(sizeof(double) * n * ell, st));
     RF_CUDA(cudaMemcpyAsync(gd.d(), g, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st));
     int64_t r = 0;
-    Status cs = with_speculation(c, [&] {
+    Status cs = with_speculation(c, {3, m, n, lda, k, ell, q, reorth}, [&] {
       return rsvd_core(c, &h, gd.d(), k, ell, q, keep_over != 0, reorth != 0, U.d(), ldu, D.d(), V.d(), &r, Uh, ldu);
     });
     if (!cs.ok()) {
@@ -2608,7 +2724,7 @@ int rfgpu_single_pass_push(rfgpu_single_pass* s, int64_t col0, const double* blk
       // a host stage is refilled once its previous copy to the device is done
       if (s->staged == 0) RF_CUDA(cudaEventSynchronize(s->copied[s->cur]));
       const int64_t take = std::min(b - done, s->chunk - s->staged);
-      host_copy_cols(s->stage_h[s->cur] + s->m * s->staged, s->m, blk + s->m * done, s->m, s->m, take);
+      host_copy_cols(c, s->stage_h[s->cur] + s->m * s->staged, s->m, blk + s->m * done, s->m, s->m, take);
       s->staged += take;
       done += take;
       if (s->staged == s->chunk) RF_TRY(sp_flush(s));

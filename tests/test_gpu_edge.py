@@ -26,22 +26,22 @@ def orthonormality_defect(q):
     return float(np.max(np.abs(q.T @ q - np.eye(q.shape[1]))))
 
 
-def test_svd_dense_23_decade_spectrum(ctx, port):
+def test_svd_dense_23_decade_spectrum(ctx, ref):
     sigma = 0.7 ** np.arange(150, dtype=np.float64)  # support::geometric_sigma(150, 0.7): 1 .. 1e-23
-    a = port.planted(200, 150, sigma, 1)
+    a = ref.test_planted(200, 150, sigma, 1)  # the reference test's own matrix (support::planted, Haar factors)
     f = rf.svd_dense(a, ctx=ctx)
     assert f.U.shape == (200, 150) and f.V.shape == (150, 150) and len(f.D) == 150
     assert orthonormality_defect(f.U) < 1e-12
     assert orthonormality_defect(f.V) < 1e-12
     rec = (f.U * f.D) @ f.V.T
     assert np.linalg.norm(rec - a) / np.linalg.norm(a) < 1e-13
+    # CHECK(f.D[j] == doctest::Approx(sigma[j]).epsilon(1e-10)): |d - s| < 1e-10 (1 + max(|d|, |s|))
     for j, s in enumerate(sigma):
         if s < 1e-10 * sigma[0]:
             break
-        assert abs(f.D[j] - s) <= 1e-10 * s, (j, f.D[j], s)
-    want = port.svd(a)
-    big = want.D >= 1e-10 * want.D[0]
-    assert np.max(np.abs(f.D[big] - want.D[big]) / want.D[big]) <= 1e-10
+        assert abs(f.D[j] - s) < 1e-10 * (1.0 + max(abs(f.D[j]), s)), (j, f.D[j], s)
+    want = ref.svd(a)
+    assert np.max(np.abs(f.D - want.D) / (1.0 + want.D)) < 1e-14
 
 
 def test_frob_residual_guards(ctx):
