@@ -450,7 +450,10 @@ constexpr size_t kSmallBlock = size_t{256} << 20;
 struct CtxCall {
   std::lock_guard<std::mutex> lk;
   rfgpu_ctx* prev;
-  explicit CtxCall(rfgpu_ctx* c) : lk(c->mu), prev(t_ctx) { t_ctx = c; }
+  explicit CtxCall(rfgpu_ctx* c) : lk(c->mu), prev(t_ctx) {
+    t_ctx = c;
+    cudaGetLastError();  // a runtime error left on this thread by other code must not be reported as ours
+  }
   ~CtxCall() { t_ctx = prev; }
 };
 
@@ -516,7 +519,9 @@ cudaError_t host_allreduce(rfgpu_ctx* c, double* buf, int64_t count, cudaStream_
   cudaError_t e = cudaMemcpyAsync(c->h_stage, buf, sizeof(double) * count, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return e;
-  if (c->host_sum(c->host_user, c->h_stage, count) != 0) return cudaErrorUnknown;
+  const int rc = c->host_sum(c->host_user, c->h_stage, count);
+  cudaGetLastError();  // the callback is foreign code: a runtime error it left behind is not ours
+  if (rc != 0) return cudaErrorUnknown;
   return cudaMemcpyAsync(buf, c->h_stage, sizeof(double) * count, cudaMemcpyHostToDevice, st);
 }
 
