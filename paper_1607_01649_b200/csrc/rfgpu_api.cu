@@ -1251,7 +1251,19 @@ template <class F>
 Status with_speculation(rfgpu_ctx* c, const std::vector<int64_t>& key, F&& body) {
   const char* e = std::getenv("RFGPU_SPECULATE");
   if ((e && e[0] == '0') || c->spec_failed.count(key)) return body();
-  RF_CUDA(cudaMemsetAsync(c->spec_flags, 0, 2 * sizeof(int), c->stream));
+  {
+    cudaError_t me = cudaMemsetAsync(c->spec_flags, 0, 2 * sizeof(int), c->stream);
+    if (me != cudaSuccess && std::getenv("RFGPU_DEBUG")) {
+      cudaPointerAttributes at{};
+      cudaError_t pe = cudaPointerGetAttributes(&at, c->spec_flags);
+      int dev = -1;
+      cudaGetDevice(&dev);
+      std::fprintf(stderr, "[rfgpu] spec memset failed: %s ptr=%p (attr %s type %d dev %d) cur dev %d ctx dev %d stream %p\n",
+                   cudaGetErrorString(me), static_cast<void*>(c->spec_flags), cudaGetErrorString(pe),
+                   static_cast<int>(at.type), at.device, dev, c->device, static_cast<void*>(c->stream));
+    }
+    RF_CUDA(me);
+  }
   c->spec = true;
   Status s = body();
   c->spec = false;
