@@ -1801,8 +1801,17 @@ Status ensure_device(rfgpu_ctx* c) {
   return {};
 }
 
+void dbg_ptr(const char* where, const void* p) {
+  if (!std::getenv("RFGPU_DEBUG_PTR")) return;
+  cudaPointerAttributes at{};
+  cudaError_t pe = cudaPointerGetAttributes(&at, p);
+  std::fprintf(stderr, "[rfgpu] %s: %p attr %s type %d dev %d\n", where, p, cudaGetErrorString(pe),
+               static_cast<int>(at.type), at.device);
+}
+
 // Global row count and this rank's row offset for a row-sharded A.
 Status global_rows(rfgpu_ctx* c, rfgpu_matrix* h) {
+  dbg_ptr("global_rows entry spec_flags", c->spec_flags);
   h->m_global = h->m;
   h->row0 = 0;
   if (c->world <= 1) return {};
@@ -1812,6 +1821,7 @@ Status global_rows(rfgpu_ctx* c, rfgpu_matrix* h) {
   v[c->rank] = static_cast<double>(h->m);
   RF_CUDA(cudaMemcpyAsync(b.d(), v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, c->stream));
   RF_TRY(allreduce(c, b.d(), c->world));
+  dbg_ptr("global_rows after allreduce spec_flags", c->spec_flags);
   RF_CUDA(cudaMemcpyAsync(v.data(), b.d(), sizeof(double) * c->world, cudaMemcpyDeviceToHost, c->stream));
   RF_CUDA(cudaStreamSynchronize(c->stream));
   int64_t tot = 0, off = 0;
@@ -1944,6 +1954,7 @@ int ctx_create_common(int device, int rank, int world, rfgpu_ctx** out) {
   }
   c->launch_base = launch_counter();
   *out = c;
+  dbg_ptr("ctx_create spec_flags", c->spec_flags);
   return RFGPU_OK;
 }
 
