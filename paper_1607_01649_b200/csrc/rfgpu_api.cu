@@ -506,10 +506,6 @@ cudaError_t host_allreduce(rfgpu_ctx* c, double* buf, int64_t count, cudaStream_
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return e;
     if (c->h_stage) cudaFreeHost(c->h_stage);
-  for (void* sl : c->stage_slots) cudaFreeHost(sl);
-  for (cudaEvent_t e : c->stage_done) cudaEventDestroy(e);
-  if (c->h_spec) cudaFreeHost(c->h_spec);
-  if (c->spec_flags) cudaFree(c->spec_flags);
     c->h_stage = nullptr;
     c->h_stage_n = 0;
     e = cudaMallocHost(&c->h_stage, sizeof(double) * count);
@@ -1251,19 +1247,7 @@ template <class F>
 Status with_speculation(rfgpu_ctx* c, const std::vector<int64_t>& key, F&& body) {
   const char* e = std::getenv("RFGPU_SPECULATE");
   if ((e && e[0] == '0') || c->spec_failed.count(key)) return body();
-  {
-    cudaError_t me = cudaMemsetAsync(c->spec_flags, 0, 2 * sizeof(int), c->stream);
-    if (me != cudaSuccess && std::getenv("RFGPU_DEBUG")) {
-      cudaPointerAttributes at{};
-      cudaError_t pe = cudaPointerGetAttributes(&at, c->spec_flags);
-      int dev = -1;
-      cudaGetDevice(&dev);
-      std::fprintf(stderr, "[rfgpu] spec memset failed: %s ptr=%p (attr %s type %d dev %d) cur dev %d ctx dev %d stream %p\n",
-                   cudaGetErrorString(me), static_cast<void*>(c->spec_flags), cudaGetErrorString(pe),
-                   static_cast<int>(at.type), at.device, dev, c->device, static_cast<void*>(c->stream));
-    }
-    RF_CUDA(me);
-  }
+  RF_CUDA(cudaMemsetAsync(c->spec_flags, 0, 2 * sizeof(int), c->stream));
   c->spec = true;
   Status s = body();
   c->spec = false;
@@ -1801,17 +1785,8 @@ Status ensure_device(rfgpu_ctx* c) {
   return {};
 }
 
-void dbg_ptr(const char* where, const void* p) {
-  if (!std::getenv("RFGPU_DEBUG_PTR")) return;
-  cudaPointerAttributes at{};
-  cudaError_t pe = cudaPointerGetAttributes(&at, p);
-  std::fprintf(stderr, "[rfgpu] %s: %p attr %s type %d dev %d\n", where, p, cudaGetErrorString(pe),
-               static_cast<int>(at.type), at.device);
-}
-
 // Global row count and this rank's row offset for a row-sharded A.
 Status global_rows(rfgpu_ctx* c, rfgpu_matrix* h) {
-  dbg_ptr("global_rows entry spec_flags", c->spec_flags);
   h->m_global = h->m;
   h->row0 = 0;
   if (c->world <= 1) return {};
@@ -1821,7 +1796,6 @@ Status global_rows(rfgpu_ctx* c, rfgpu_matrix* h) {
   v[c->rank] = static_cast<double>(h->m);
   RF_CUDA(cudaMemcpyAsync(b.d(), v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, c->stream));
   RF_TRY(allreduce(c, b.d(), c->world));
-  dbg_ptr("global_rows after allreduce spec_flags", c->spec_flags);
   RF_CUDA(cudaMemcpyAsync(v.data(), b.d(), sizeof(double) * c->world, cudaMemcpyDeviceToHost, c->stream));
   RF_CUDA(cudaStreamSynchronize(c->stream));
   int64_t tot = 0, off = 0;
@@ -1954,7 +1928,6 @@ int ctx_create_common(int device, int rank, int world, rfgpu_ctx** out) {
   }
   c->launch_base = launch_counter();
   *out = c;
-  dbg_ptr("ctx_create spec_flags", c->spec_flags);
   return RFGPU_OK;
 }
 
