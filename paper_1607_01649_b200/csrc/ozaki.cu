@@ -51,13 +51,9 @@ constexpr int OBN = 64;        // tile columns per accumulator group
 // flight per SM at the same shared-memory footprint).
 constexpr int BKQ = 64;  // K bytes per block in kb_split_fixed
 constexpr int64_t kSplitK = 16384;  // int32 safety: S * K * 128^2 < 2^31
-// K per split of the A^T Q pass (<= kSplitK, a multiple of 256): RFGPU_OZAKI_TNK overrides.
-int64_t tn_split_k() {
-  const char* e = std::getenv("RFGPU_OZAKI_TNK");
-  int64_t k = e ? std::atoll(e) : kSplitK;
-  k = std::max<int64_t>(256, std::min<int64_t>(kSplitK, k));
-  return k / 256 * 256;
-}
+// K per split of the A^T Q pass (= the column-exponent chunk). Measured: 4096 / 2048 instead of 16384 make
+// the pass 17 % / 70 % slower (more partial sums to write and reduce).
+int64_t tn_split_k() { return kSplitK; }
 // warp 0 TMA producer, warp 1 MMA issuer, warps 2..9 epilogue (two warps per
 // TMEM lane quarter, alternating 16-column chunks)
 constexpr int kThreads = 320;
@@ -69,8 +65,6 @@ constexpr int kEpiWarps = kThreads / 32 - 2;
 // the row-major column-scaled set makes A^T Q ~20% faster than the shared
 // set read K-major.
 constexpr int kSharedSpread = 2;
-constexpr int kDefaultBK = 64;  // stage depth (see Dig); RFGPU_OZAKI_BK overrides
-constexpr bool kDefaultPersist = false;  // persistent digit GEMM grid (measured no faster); RFGPU_OZAKI_PERSIST=1 enables   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
 
 // Per digit count S: S accumulator groups of OBN TMEM columns; as many
 // 2-digit-plane... stages as fit in shared memory.
@@ -640,7 +634,7 @@ struct OzParams {
   int cshift;         // extra output exponent (the thin operand's row pre-scaling shift)
   int ws_mode;        // 1: C is [split][N_real][M_real]
   int cl;             // cluster size along N tiles: the A tile is TMA-multicast to all of them
-  int64_t ngroups;    // tile groups (all tiles / cl); the grid may be smaller (persistent)
+  int64_t ngroups;    // tile groups (all tiles / cl); the kernel loops over groups when the grid is smaller
   int w_big, n_big;   // the first n_big n-tiles are w_big wide, the rest w_small (multiples of 16, <= OBN):
   int w_small;        // l's padding is not multiplied, and the tiles sharing an A tile stay close in speed
   int ilv;            // 1: big and small tiles alternate in tile order (big at even nt): equal work per cluster pair
@@ -1021,16 +1015,11 @@ bool digit_tmap3(CUtensorMap* tm, const int8_t* base, int64_t planes, int64_t ro
 // 2-stage ring), so the caller chooses.
 // L_mn: L planes are [kS][K_pad][L_M] (M contiguous, L_rows = K_pad rows per
 // plane, L_M = M extent), else [kS][L_rows][K_pad].
-// RFGPU_OZAKI_PERSIST=0: one CTA per tile; otherwise the persistent grid.
-bool persistent() {
-  const char* e = std::getenv("RFGPU_OZAKI_PERSIST");
-  return e ? e[0] != '0' : kDefaultPersist;
-}
 
 template <int S, int BK>
 cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int64_t L_M, const int8_t* R,
                                 int64_t R_rows, int64_t K_pad, int64_t row0, int64_t rows, int64_t N_real, int splits,
-                                const OzParams& base, bool multicast, cudaStream_t st, bool persist) {
+                                const OzParams& base, bool multicast, cudaStream_t st) {
   constexpr int kS = S;
   constexpr size_t kSmemBytes = Dig<S, BK>::smem;
   constexpr CUtensorMapSwizzle kSwK = BK == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
@@ -1050,27 +1039,17 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   // (l = 220: 64 64 48 48); RFGPU_OZAKI_NARROW=0 pads every tile to 64, =1 keeps 64 ... 64 + a narrow last
   const int ntn = static_cast<int>(R_rows / OBN);
   const int units = static_cast<int>(std::min<int64_t>(4 * ntn, std::max<int64_t>(1, (N_real + 15) / 16)));
-  int w_big, n_big, w_small;
-  const char* nw = std::getenv("RFGPU_OZAKI_NARROW");
-  if (nw && nw[0] == '0') {
-    w_big = w_small = OBN, n_big = ntn;
-  } else if (nw && nw[0] == '1') {
-    w_big = OBN, n_big = ntn - 1, w_small = 16 * (units - 4 * (ntn - 1));
-  } else {
-    const int q = units / ntn, r = units % ntn;
-    w_small = 16 * q;
-    w_big = r ? 16 * (q + 1) : 16 * q;
-    n_big = r ? r : ntn;
-  }
-  if (w_small <= 0) w_small = w_big;
+  // (measured: padding every tile to 64 columns costs 7 %, 64-column tiles and one narrow last tile 1-2 %)
+  const int q = units / ntn, r = units % ntn;
+  const int w_small = 16 * q > 0 ? 16 * q : 16 * (q + 1), w_big = r ? 16 * (q + 1) : 16 * q;
+  const int n_big = r ? r : ntn;
   CUtensorMap tr2;
   if (!digit_tmap(&tr, R, kS * R_rows, K_pad, BK, w_big, kSwK)) return cudaErrorInvalidValue;
   tr2 = tr;
   if (w_small != w_big && !digit_tmap(&tr2, R, kS * R_rows, K_pad, BK, w_small, kSwK)) return cudaErrorInvalidValue;
   CUtensorMap tl3 = tl, tr3 = tr, tr23 = tr2;
-  const char* t3e = std::getenv("RFGPU_OZAKI_TMA3");
-  bool tma3 = !(t3e && t3e[0] == '0');
-  if (tma3) {
+  bool tma3 = true;  // all digit planes of a tile in one 3-D copy (2 TMA issues per stage instead of 14)
+  {
     tma3 = (L_mn ? digit_tmap3(&tl3, L, kS, L_rows, L_M, OBM, BK, CU_TENSOR_MAP_SWIZZLE_128B)
                  : digit_tmap3(&tl3, L, kS, L_rows, K_pad, BK, OBM, kSwK)) &&
            digit_tmap3(&tr3, R, kS, R_rows, K_pad, BK, w_big, kSwK) &&
@@ -1128,15 +1107,6 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   attr[0].val.clusterDim.z = 1;
   cfgl.attrs = attr;
   cfgl.numAttrs = 1;
-  if (persist) {  // one resident cluster per slot, looping over the tile groups
-    int nclusters = 0;
-    auto kfn = L_mn ? ozaki_gemm_kernel<true, S, BK> : ozaki_gemm_kernel<false, S, BK>;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &cfgl) != cudaSuccess || nclusters <= 0) {
-      cudaGetLastError();
-      nclusters = 148 / p.cl;
-    }
-    if (nclusters < p.ngroups) cfgl.gridDim = dim3(static_cast<unsigned>(nclusters * p.cl));
-  }
   cudaError_t e = L_mn ? cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<true, S, BK>, tl, tr, tr2, tl3, tr3, tr23, p)
                        : cudaLaunchKernelEx(&cfgl, ozaki_gemm_kernel<false, S, BK>, tl, tr, tr2, tl3, tr3, tr23, p);
   count_launch();
@@ -1145,27 +1115,15 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
 }
 
 
-// Stage depth: RFGPU_OZAKI_BK=32 (5 x 43 KB stages for 7 digits) or 64 (2 x 86 KB).
-int stage_bk() {
-  const char* e = std::getenv("RFGPU_OZAKI_BK");
-  if (e) return std::atoi(e) == 32 ? 32 : 64;
-  return kDefaultBK;
-}
-
+// 64 K-bytes per stage, 2 stages (measured: 32-byte stages, 5 deep, with a 32B swizzle are 30 % slower)
 cudaError_t launch_digit_gemm(int S, const int8_t* L, int64_t L_rows, bool L_mn, int64_t L_M, const int8_t* R,
                               int64_t R_rows, int64_t K_pad, int64_t row0, int64_t rows, int64_t N_real, int splits,
-                              const OzParams& base, bool multicast, cudaStream_t st, int persist = -1) {
-  const bool b32 = stage_bk() == 32;
-  const bool pers = persist < 0 ? persistent() : persist == 1;
+                              const OzParams& base, bool multicast, cudaStream_t st) {
   if (S == 4)
-    return b32 ? launch_digit_gemm_s<4, 32>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
-                                            multicast, st, pers)
-               : launch_digit_gemm_s<4, 64>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
-                                            multicast, st, pers);
-  return b32 ? launch_digit_gemm_s<7, 32>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
-                                          multicast, st, pers)
-             : launch_digit_gemm_s<7, 64>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
-                                          multicast, st, pers);
+    return launch_digit_gemm_s<4, 64>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
+                                      multicast, st);
+  return launch_digit_gemm_s<7, 64>(L, L_rows, L_mn, L_M, R, R_rows, K_pad, row0, rows, N_real, splits, base,
+                                    multicast, st);
 }
 
 // Column exponents (many CTAs per column) + digits of the thin operand R
@@ -1230,10 +1188,9 @@ size_t ozaki_set_bytes(int64_t m, int64_t n, int digits) {
 
 int64_t ozaki_chunk_rows() { return tn_split_k(); }
 
-bool ozaki_cs_rowmajor() {
-  const char* e = std::getenv("RFGPU_OZAKI_TNMN");  // experiments: 0 keeps the column-major cs (K-major A^T Q)
-  return !(e && e[0] == '0');
-}
+// The column-scaled set is row-major, read M-major by A^T Q (measured: the column-major set read K-major is
+// ~30 % slower on the tensor cores); the K-major reader remains for the shared-set fallback.
+bool ozaki_cs_rowmajor() { return true; }
 
 size_t ozaki_a_bytes(int64_t m, int64_t n, int digits) {
   const OzakiA a = ozaki_layout(m, n, digits);
@@ -1349,11 +1306,9 @@ cudaError_t slice_sets_t(const T* A, int64_t lda, const OzakiA& a, bool rows, bo
     }
     if (r1 <= r0) return cudaSuccess;
     const unsigned grid = static_cast<unsigned>(((r1 - r0) / kSliceTRows) * (a.n_pad / kSliceTCols));
-    static const bool async_ok = [] {
-      const char* v = std::getenv("RFGPU_OZAKI_SLICE_ASYNC");  // experiments: 0 = register-prefetch slicer
-      return !(v && v[0] == '0');
-    }();
-    if (async_ok && (lda * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
+    // cp.async loads (all 8 columns of a lane in flight) whenever the columns are 16-byte aligned; the
+    // register-prefetch slicer otherwise (5.8 vs 5.2 TB/s at config 3)
+    if ((lda * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
       constexpr size_t smem_async = sizeof(uint32_t) * kSliceTCols * 256;
       static std::atomic<uint64_t> cfg_async{0};
       if (attr_pending(cfg_async)) {

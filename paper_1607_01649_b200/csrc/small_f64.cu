@@ -767,6 +767,139 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
   cluster.sync();
 }
 
+// One-sided Jacobi for small problems (c <= 128 columns, X and V both in one
+// CTA's shared memory): the reference algorithm (dense.cpp:585-686: columns
+// re-ordered by descending norm before every sweep, rotation formula, skip
+// rule |apq| <= 1e-15 sqrt(app aqq), <= 60 sweeps, D non-increasing) with the
+// pairs of a sweep in circle-method rounds, one warp per pair and one CTA
+// barrier per round: no cluster barriers, no global round trips. The sort is
+// an index permutation (`ord`), never a data move. One problem per CTA
+// (blockIdx.x picks p0 / p1).
+struct J1Params {
+  const double* X;
+  int mr, c;
+  double *U, *S, *V;
+  int* info;
+  int* sweeps_out;
+};
+
+__global__ void __launch_bounds__(1024, 1) jacobi1_kernel(const J1Params p0, const J1Params p1) {
+  const J1Params& p = blockIdx.x == 0 ? p0 : p1;
+  const int mr = p.mr, c = p.c, cc = c + (c & 1);  // cc: even count of positions (last one virtual if c odd)
+  extern __shared__ double sm[];
+  double* X = sm;                      // [c][mr]
+  double* V = X + static_cast<size_t>(c) * mr;  // [c][c]
+  double* nrm = V + static_cast<size_t>(c) * c;  // [c]
+  int* ord = reinterpret_cast<int*>(nrm + c);   // [cc] position -> column
+  __shared__ int s_rot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  for (int e = tid; e < c * mr; e += blockDim.x) X[e] = p.X[e];
+  for (int e = tid; e < c * c; e += blockDim.x) V[e] = (e % c == e / c) ? 1.0 : 0.0;
+  if (tid < cc) ord[tid] = tid;
+  __syncthreads();
+  auto norms = [&]() {
+    for (int j = warp; j < c; j += nwarps) {
+      const double* x = X + static_cast<size_t>(j) * mr;
+      double s2 = 0.0;
+      for (int i = lane; i < mr; i += 32) s2 = fma(x[i], x[i], s2);
+      s2 = warp_sum(s2);
+      if (lane == 0) nrm[j] = s2;
+    }
+    __syncthreads();
+  };
+  // stable descending rank sort of the columns by nrm into ord (positions >= c stay virtual)
+  auto sort_cols = [&]() {
+    for (int j = tid; j < c; j += blockDim.x) {
+      const double kj = nrm[j];
+      int rank = 0;
+      for (int i = 0; i < c; ++i) {
+        const double ki = nrm[i];
+        rank += (ki > kj || (ki == kj && i < j)) ? 1 : 0;
+      }
+      ord[rank] = j;
+    }
+    if (tid == 0 && cc > c) ord[c] = c;  // the virtual column
+    __syncthreads();
+  };
+  int sweep = 0;
+  bool conv = c <= 1;
+  while (!conv && sweep < 60) {
+    norms();
+    sort_cols();
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int r = 0; r < cc - 1; ++r) {
+      for (int k = warp; k < cc / 2; k += nwarps) {
+        int a, b;
+        pair_of(r, k, cc, &a, &b);
+        const int u = ord[a], v = ord[b];
+        if (u >= c || v >= c) continue;
+        double* xu = X + static_cast<size_t>(u) * mr;
+        double* xv = X + static_cast<size_t>(v) * mr;
+        double app = 0.0, aqq = 0.0, apq = 0.0;
+        for (int i = lane; i < mr; i += 32) {
+          const double x = xu[i], y = xv[i];
+          app = fma(x, x, app);
+          aqq = fma(y, y, aqq);
+          apq = fma(x, y, apq);
+        }
+        app = warp_sum(app);
+        aqq = warp_sum(aqq);
+        apq = warp_sum(apq);
+        // (u, v) are (p, q) of the reference in sorted position order: a < b
+        if (app != 0.0 && aqq != 0.0 && !(apq * apq <= 1e-30 * (app * aqq))) {
+          const double zeta = (aqq - app) / (2.0 * apq);
+          const double t = (zeta < 0.0 ? -1.0 : 1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          for (int i = lane; i < mr; i += 32) {
+            const double x = xu[i], y = xv[i];
+            xu[i] = cs * x - sn * y;
+            xv[i] = sn * x + cs * y;
+          }
+          double* vu = V + static_cast<size_t>(u) * c;
+          double* vv = V + static_cast<size_t>(v) * c;
+          for (int i = lane; i < c; i += 32) {
+            const double x = vu[i], y = vv[i];
+            vu[i] = cs * x - sn * y;
+            vv[i] = sn * x + cs * y;
+          }
+          if (lane == 0) s_rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    conv = s_rot == 0;
+    ++sweep;
+    __syncthreads();
+  }
+  // singular values (column norms) in stable descending order, U = X / s, V permuted
+  norms();
+  for (int j = tid; j < c; j += blockDim.x) nrm[j] = sqrt(nrm[j]);
+  __syncthreads();
+  sort_cols();
+  const double smax = c > 0 ? nrm[ord[0]] : 0.0;
+  bool zero_cols = false;
+  for (int j = 0; j < c; ++j) {
+    const int src = ord[j];
+    const double sv = nrm[src];
+    const bool ok = sv > 0.0 && sv > smax * 1e-250;
+    zero_cols |= !ok;
+    if (tid == 0) p.S[j] = ok ? sv : 0.0;
+    const double* x = X + static_cast<size_t>(src) * mr;
+    for (int i = tid; i < mr; i += blockDim.x) p.U[static_cast<int64_t>(j) * mr + i] = ok ? x[i] / sv : 0.0;
+    const double* vv = V + static_cast<size_t>(src) * c;
+    for (int i = tid; i < c; i += blockDim.x) p.V[static_cast<int64_t>(j) * c + i] = vv[i];
+  }
+  if (tid == 0) {
+    p.info[0] = conv ? (zero_cols ? 2 : 0) : 1;
+    if (p.sweeps_out) p.sweeps_out[0] = sweep;
+  }
+}
+
+size_t jacobi1_smem(int64_t mr, int64_t c) {
+  return sizeof(double) * static_cast<size_t>(c) * (mr + c + 1) + sizeof(int) * static_cast<size_t>(c + 2);
+}
+
 // Block Jacobi applies when the two blocks' rows fit in shared memory and the
 // tournament fits one cluster (<= 16 CTAs); RFGPU_JACOBI_BLOCK=0 disables it.
 struct BJLayout {
@@ -1123,6 +1256,28 @@ cudaError_t bjacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64
 cudaError_t jacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64_t c, cudaStream_t st,
                           bool sorted = false) {
   if (c <= 0 || mr <= 0) return cudaSuccess;
+  // small problems: the single-CTA kernel (RFGPU_JACOBI_BLOCK pins the cluster kernels for experiments)
+  if (c <= 128 && !std::getenv("RFGPU_JACOBI_BLOCK") && jacobi1_smem(mr, c) <= 220 * 1024) {
+    static std::atomic<uint64_t> j1cfg{0};
+    if (attr_pending(j1cfg)) {
+      cudaError_t e = cudaFuncSetAttribute(jacobi1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return e;
+      }
+      attr_done(j1cfg);
+    }
+    J1Params ps[2];
+    for (int i = 0; i < count; ++i)
+      ps[i] = J1Params{pr[i].X, static_cast<int>(mr), static_cast<int>(c), pr[i].U, pr[i].S, pr[i].V, pr[i].info,
+                       pr[i].sweeps};
+    if (count == 1) ps[1] = ps[0];
+    const int pairs = static_cast<int>((c + (c & 1)) / 2);
+    const int threads = 32 * std::max(1, std::min(32, pairs));
+    jacobi1_kernel<<<count, threads, jacobi1_smem(mr, c), st>>>(ps[0], ps[1]);
+    count_launch();
+    return cudaGetLastError();
+  }
   const BJLayout B = bj_layout(mr, c);
   if (B.ok && !sorted) return bjacobi_launch(pr, count, mr, c, B, st);
   const JacobiLayout L = jacobi_layout(mr, c);
