@@ -24,15 +24,15 @@ __global__ void copy_col_kernel(const double* __restrict__ x, int64_t m, double*
     v[i] = x[i];
 }
 
-// partial[chunk][c] = sum over the chunk's rows of Q(i, c) * v(i), c < *r.
+// partial[chunk][c] = sum over the chunk's rows of Q(i, c) * v(i), *base <= c < *r.
 __global__ void dots_partial_kernel(const double* __restrict__ Q, int64_t ldq, int64_t m,
-                                    const int64_t* __restrict__ r_dev, const double* __restrict__ v,
-                                    double* __restrict__ partial, int64_t cmax) {
-  const int64_t r = *r_dev;
+                                    const int64_t* __restrict__ r_dev, const int64_t* __restrict__ base,
+                                    const double* __restrict__ v, double* __restrict__ partial, int64_t cmax) {
+  const int64_t r = *r_dev, c0 = *base;
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRowsPerChunk;
   const int64_t row1 = min(m, row0 + kRowsPerChunk);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int64_t c = warp; c < r; c += nw) {
+  for (int64_t c = c0 + warp; c < r; c += nw) {
     const double* q = Q + c * ldq;
     double s = 0.0;
     for (int64_t i = row0 + lane; i < row1; i += 32) s = fma(q[i], v[i], s);
@@ -42,9 +42,10 @@ __global__ void dots_partial_kernel(const double* __restrict__ Q, int64_t ldq, i
 }
 
 __global__ void dots_reduce_kernel(const double* __restrict__ partial, int chunks, int64_t cmax,
-                                   const int64_t* __restrict__ r_dev, double* __restrict__ dots) {
+                                   const int64_t* __restrict__ r_dev, const int64_t* __restrict__ base,
+                                   double* __restrict__ dots) {
   const int64_t r = *r_dev;
-  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < r;
+  for (int64_t c = *base + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < r;
        c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double s = 0.0;
     for (int k = 0; k < chunks; ++k) s += partial[k * cmax + c];
@@ -52,15 +53,15 @@ __global__ void dots_reduce_kernel(const double* __restrict__ partial, int chunk
   }
 }
 
-// v(i) -= sum_c dots(c) Q(i, c)
+// v(i) -= sum_c dots(c) Q(i, c), *base <= c < *r
 __global__ void update_kernel(const double* __restrict__ Q, int64_t ldq, int64_t m,
-                              const int64_t* __restrict__ r_dev, const double* __restrict__ dots,
-                              double* __restrict__ v) {
-  const int64_t r = *r_dev;
+                              const int64_t* __restrict__ r_dev, const int64_t* __restrict__ base,
+                              const double* __restrict__ dots, double* __restrict__ v) {
+  const int64_t r = *r_dev, c0 = *base;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double acc = v[i];
-    for (int64_t c = 0; c < r; ++c) acc -= dots[c] * Q[c * ldq + i];
+    for (int64_t c = c0; c < r; ++c) acc -= dots[c] * Q[c * ldq + i];
     v[i] = acc;
   }
 }
@@ -85,13 +86,46 @@ __global__ void store_col_kernel(const double* __restrict__ v, int64_t m, const 
     Q[col * ldq + i] = v[i] / nrm;
 }
 
+__global__ void snapshot_kernel(const int64_t* __restrict__ r_dev, int64_t* __restrict__ base) { *base = *r_dev; }
+
+// W(:, 0:b) -= T(:, 0:b) (both ld m)
+__global__ void sub_kernel(double* __restrict__ W, const double* __restrict__ T, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    W[i] -= T[i];
+}
+
+__global__ void copy_cols_kernel(const double* __restrict__ X, int64_t ldx, int64_t m, int64_t b,
+                                 double* __restrict__ W) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < m * b;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / m, i = e - j * m;
+    W[e] = X[j * ldx + i];
+  }
+}
+
 inline int grid_for(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(1184, (n + 255) / 256))); }
 
 }  // namespace
 
+// Blocked: columns in blocks of kBlock. Each block is first orthogonalised
+// twice against every column kept so far with two FP64 tensor-core GEMMs per
+// pass (C = Q^T W, W -= Q C; Q is zero beyond the kept count, so the GEMMs
+// need no host-side count), then column by column against the block's own
+// kept columns (CGS2, drop rule). In exact arithmetic every residual equals
+// the reference's (the kept columns of earlier blocks are orthogonal to the
+// block's), so the same columns are kept; rounding-level differences only.
+constexpr int64_t kBlock = 32;
+
+GemmPlan block_plan_tn(int64_t m, int64_t c) { return plan_gemm(c, kBlock, m, 148); }
+GemmPlan block_plan_nn(int64_t m, int64_t c) { return plan_gemm(m, kBlock, c, 148); }
+
 size_t gs_orth_work_doubles(int64_t m, int64_t c) {
   const int64_t chunks = (m + kRowsPerChunk - 1) / kRowsPerChunk;
-  return static_cast<size_t>(m) + chunks * c + c + 1024 + 8;
+  const size_t ws = std::max(gemm_workspace_bytes(c, kBlock, block_plan_tn(m, c)),
+                             gemm_workspace_bytes(m, kBlock, block_plan_nn(m, c)));
+  return static_cast<size_t>(m) + chunks * c + c + 1024 + 8 + 2 * static_cast<size_t>(m) * kBlock + c * kBlock +
+         (ws + 7) / 8 + 8;
 }
 
 cudaError_t gs_orth(const double* X, int64_t m, int64_t c, int64_t ldx, double* Q, int64_t ldq, int64_t* r_dev,
@@ -101,9 +135,20 @@ cudaError_t gs_orth(const double* X, int64_t m, int64_t c, int64_t ldx, double* 
   double* partial = v + m;
   double* dots = partial + static_cast<int64_t>(chunks) * c;
   double* sq_part = dots + c;      // 1024 partials for sumsq
-  double* scal = sq_part + 1024;   // [0] ||v||^2, [1] ||X||^2, [2..3] flag
+  double* scal = sq_part + 1024;   // [0] ||v||^2, [1] ||X||^2, [2..3] flag, [4] scratch, [5] r0 (int64)
+  int64_t* r0_dev = reinterpret_cast<int64_t*>(scal + 5);
+  double* W = scal + 8;            // m x kBlock
+  double* T = W + m * kBlock;      // m x kBlock
+  double* Cb = T + m * kBlock;     // c x kBlock
+  double* gws = Cb + c * kBlock;
+  const GemmPlan ptn = block_plan_tn(m, c), pnn = block_plan_nn(m, c);
+  const size_t gws_bytes = std::max(gemm_workspace_bytes(c, kBlock, ptn), gemm_workspace_bytes(m, kBlock, pnn));
   cudaError_t e = cudaMemsetAsync(r_dev, 0, sizeof(int64_t), st);
   if (e != cudaSuccess) return e;
+  for (int64_t j = 0; j < c; ++j) {  // Q beyond the kept count must read as zero for the block GEMMs
+    e = cudaMemsetAsync(Q + j * ldq, 0, sizeof(double) * m, st);
+    if (e != cudaSuccess) return e;
+  }
   // ||X||_F^2 (column by column to honour ldx), accumulated in fixed order
   e = cudaMemsetAsync(scal + 1, 0, sizeof(double), st);
   if (e != cudaSuccess) return e;
@@ -117,33 +162,53 @@ cudaError_t gs_orth(const double* X, int64_t m, int64_t c, int64_t ldx, double* 
     e = ar.fn(ar.ctx, scal + 1, 1, st);
     if (e != cudaSuccess) return e;
   }
-  for (int64_t j = 0; j < c; ++j) {
-    copy_col_kernel<<<grid_for(m), 256, 0, st>>>(X + j * ldx, m, v);
-    count_launch();
-    for (int pass = 0; pass < 2; ++pass) {
-      dots_partial_kernel<<<chunks, 256, 0, st>>>(Q, ldq, m, r_dev, v, partial, c);
-    count_launch();
-      dots_reduce_kernel<<<1, 256, 0, st>>>(partial, chunks, c, r_dev, dots);
-    count_launch();
+  for (int64_t j0 = 0; j0 < c; j0 += kBlock) {
+    const int64_t b = std::min(kBlock, c - j0);
+    copy_cols_kernel<<<grid_for(m * b), 256, 0, st>>>(X + j0 * ldx, ldx, m, b, W);
+    snapshot_kernel<<<1, 1, 0, st>>>(r_dev, r0_dev);
+    count_launch(2);
+    if (j0 > 0) {  // twice against the columns kept by earlier blocks
+      for (int pass = 0; pass < 2; ++pass) {
+        e = gemm_f64(true, c, b, m, Q, ldq, W, m, Cb, c, gws, gws_bytes, nullptr, block_plan_tn(m, c), st);
+        if (e != cudaSuccess) return e;
+        if (ar.fn) {
+          e = ar.fn(ar.ctx, Cb, c * b, st);
+          if (e != cudaSuccess) return e;
+        }
+        e = gemm_f64(false, m, b, c, Q, ldq, Cb, c, T, m, gws, gws_bytes, nullptr, block_plan_nn(m, c), st);
+        if (e != cudaSuccess) return e;
+        sub_kernel<<<grid_for(m * b), 256, 0, st>>>(W, T, m * b);
+        count_launch();
+      }
+    }
+    for (int64_t t = 0; t < b; ++t) {  // then within the block, column by column (CGS2, drop rule)
+      copy_col_kernel<<<grid_for(m), 256, 0, st>>>(W + t * m, m, v);
+      count_launch();
+      if (t > 0) {
+        for (int pass = 0; pass < 2; ++pass) {
+          dots_partial_kernel<<<chunks, 256, 0, st>>>(Q, ldq, m, r_dev, r0_dev, v, partial, c);
+          dots_reduce_kernel<<<1, 256, 0, st>>>(partial, chunks, c, r_dev, r0_dev, dots);
+          count_launch(2);
+          if (ar.fn) {
+            e = ar.fn(ar.ctx, dots, c, st);  // zero-padded beyond r on every rank
+            if (e != cudaSuccess) return e;
+          }
+          update_kernel<<<grid_for(m), 256, 0, st>>>(Q, ldq, m, r_dev, r0_dev, dots, v);
+          count_launch();
+        }
+      }
+      e = sumsq(v, m, sq_part, scal, st);
+      if (e != cudaSuccess) return e;
       if (ar.fn) {
-        e = ar.fn(ar.ctx, dots, c, st);  // zero-padded beyond r on every rank
+        e = ar.fn(ar.ctx, scal, 1, st);
         if (e != cudaSuccess) return e;
       }
-      update_kernel<<<grid_for(m), 256, 0, st>>>(Q, ldq, m, r_dev, dots, v);
-    count_launch();
-    }
-    e = sumsq(v, m, sq_part, scal, st);
-    if (e != cudaSuccess) return e;
-    if (ar.fn) {
-      e = ar.fn(ar.ctx, scal, 1, st);
+      accept_kernel<<<1, 1, 0, st>>>(scal, r_dev, scal + 2);
+      store_col_kernel<<<grid_for(m), 256, 0, st>>>(v, m, scal + 2, Q, ldq);
+      count_launch(2);
+      e = cudaGetLastError();
       if (e != cudaSuccess) return e;
     }
-    accept_kernel<<<1, 1, 0, st>>>(scal, r_dev, scal + 2);
-    count_launch();
-    store_col_kernel<<<grid_for(m), 256, 0, st>>>(v, m, scal + 2, Q, ldq);
-    count_launch();
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }

@@ -2214,7 +2214,7 @@ int rfgpu_rsvd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g_dev, 
                                       a->lda, reinterpret_cast<int64_t>(g_dev), k, ell, q, keep_over, reorth,
                                       reinterpret_cast<int64_t>(U), reinterpret_cast<int64_t>(D),
                                       reinterpret_cast<int64_t>(V)};
-    rfgpu_ctx::GraphEntry* ge = graph_lookup(c, key);
+    rfgpu_ctx::GraphEntry* ge = graphs_enabled(c) ? graph_lookup(c, key) : nullptr;  // profiling: eager phases
     if (!ge && graphs_enabled(c) && !c->spec_failed.count(key) && c->graph_seen[key]++ >= 1)
       ge = graph_capture(c, key, body, &r);
     if (ge) {
