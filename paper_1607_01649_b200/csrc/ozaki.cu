@@ -637,7 +637,6 @@ struct OzParams {
   int64_t ngroups;    // tile groups (all tiles / cl); the kernel loops over groups when the grid is smaller
   int w_big, n_big;   // the first n_big n-tiles are w_big wide, the rest w_small (multiples of 16, <= OBN):
   int w_small;        // l's padding is not multiplied, and the tiles sharing an A tile stay close in speed
-  int ilv;            // 1: big and small tiles alternate in tile order (big at even nt): equal work per cluster pair
   int64_t rex_stride;      // rowexp is [split][rex_stride] (per K-chunk output-row exponents; 0: one vector)
   int tma3;                // 1: one 3-D TMA copy per operand and stage (no multicast)
   int64_t kb_split_fixed;  // K blocks per split when it must match the chunks (0: even split)
@@ -719,16 +718,9 @@ __device__ __forceinline__ TileCoord tile_coord(const OzParams& p, int64_t tile)
   const int mt = static_cast<int>(rest % p.mtn);
   t.split = static_cast<int>(rest / p.mtn);
   t.lrow0 = p.row0 + static_cast<int64_t>(mt) * OBM;
-  if (p.ilv) {  // big tiles at even nt, small at odd; columns still big-first
-    const bool big = (nt & 1) == 0;
-    t.w = big ? p.w_big : p.w_small;
-    t.ncol0 = big ? static_cast<int64_t>(nt >> 1) * p.w_big
-                  : static_cast<int64_t>(p.n_big) * p.w_big + static_cast<int64_t>(nt >> 1) * p.w_small;
-  } else {
-    t.w = nt < p.n_big ? p.w_big : p.w_small;
-    t.ncol0 = nt < p.n_big ? static_cast<int64_t>(nt) * p.w_big
-                           : static_cast<int64_t>(p.n_big) * p.w_big + static_cast<int64_t>(nt - p.n_big) * p.w_small;
-  }
+  t.w = nt < p.n_big ? p.w_big : p.w_small;
+  t.ncol0 = nt < p.n_big ? static_cast<int64_t>(nt) * p.w_big
+                         : static_cast<int64_t>(p.n_big) * p.w_big + static_cast<int64_t>(nt - p.n_big) * p.w_small;
   t.kb0 = t.split * p.kb_per_split;
   const int64_t kb1 = min(p.kb_total, t.kb0 + p.kb_per_split);
   t.nk = static_cast<int>(kb1 - t.kb0);
@@ -1071,10 +1063,6 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   p.w_big = w_big;
   p.n_big = n_big;
   p.w_small = w_small;
-  {
-    const char* il = std::getenv("RFGPU_OZAKI_ILV");  // experiments
-    p.ilv = (il && il[0] == '1' && w_small != w_big && 2 * n_big == ntn) ? 1 : 0;
-  }
   p.mtn = static_cast<int>((rows + OBM - 1) / OBM);
   p.row0 = row0;
   p.M_real = rows;
@@ -1082,17 +1070,14 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   const int64_t grid = static_cast<int64_t>(p.ntn) * p.mtn * splits;
   if (grid <= 0) return cudaSuccess;
   p.cl = 1;
-  const char* mc_env = std::getenv("RFGPU_OZAKI_MC");  // experiments: 0 never, 1 always, unset: caller's choice
-  if (mc_env) multicast = mc_env[0] == '1';
-  if (multicast) {
-    const char* mcs = std::getenv("RFGPU_OZAKI_MCSIZE");  // experiments: the largest cluster <= this dividing ntn
-    const int cmax = mcs ? std::max(2, std::atoi(mcs)) : 8;
+  // multicast of the A tile over the n-tiles of a cluster: the digit Grams (short K) use it; the passes do
+  // not (measured at config 3: clusters of 4 cost 25-30 %, of 2 with equal-work pairs 0-13 %)
+  if (multicast)
     for (int c : {8, 7, 6, 5, 4, 3, 2})
-      if (c <= cmax && p.ntn % c == 0) {
+      if (p.ntn % c == 0) {
         p.cl = c;
         break;
       }
-  }
   p.ngroups = grid / p.cl;
   p.tma3 = (tma3 && p.cl == 1) ? 1 : 0;
   cudaLaunchConfig_t cfgl{};
