@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
   cluster.sync();
 }
 
-// One-sided Jacobi for small problems (c <= 128 columns, X and V both in one
+// One-sided Jacobi for narrow problems (c < 32 columns, X and V both in one
 // CTA's shared memory): the reference algorithm (dense.cpp:585-686: columns
 // re-ordered by descending norm before every sweep, rotation formula, skip
 // rule |apq| <= 1e-15 sqrt(app aqq), <= 60 sweeps, D non-increasing) with the
@@ -1256,8 +1256,10 @@ cudaError_t bjacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64
 cudaError_t jacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64_t c, cudaStream_t st,
                           bool sorted = false) {
   if (c <= 0 || mr <= 0) return cudaSuccess;
-  // small problems: the single-CTA kernel (RFGPU_JACOBI_BLOCK pins the cluster kernels for experiments)
-  if (c <= 128 && !std::getenv("RFGPU_JACOBI_BLOCK") && jacobi1_smem(mr, c) <= 220 * 1024) {
+  // narrow problems (c < 32, below the block kernel's range): the single-CTA kernel. (Measured for
+  // 32 <= c <= 128 too, but there the cluster block kernel is faster: l = 60 0.81 vs 0.62 ms, l = 110 3.4 vs
+  // 1.2 ms — a round's rotation chain costs the same, and the block kernel's CTAs are smaller.)
+  if (c < 32 && jacobi1_smem(mr, c) <= 220 * 1024) {
     static std::atomic<uint64_t> j1cfg{0};
     if (attr_pending(j1cfg)) {
       cudaError_t e = cudaFuncSetAttribute(jacobi1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
