@@ -345,6 +345,8 @@ struct rfgpu_ctx {
   // pinned staging ring for pageable host buffers (host copy threads fill a
   // slot, the copy engine moves it; a slot is refilled once its copy is done)
   HostPool host_pool;
+  double* sp_stage_h[2] = {nullptr, nullptr};  // pinned stages of the streamed single pass, kept between calls
+  size_t sp_stage_bytes = 0;
   std::vector<void*> stage_slots;
   std::vector<cudaEvent_t> stage_done;
   size_t stage_bytes = 0;
@@ -1869,6 +1871,8 @@ void ctx_free(rfgpu_ctx* c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (void* sl : c->stage_slots) cudaFreeHost(sl);
   for (cudaEvent_t e : c->stage_done) cudaEventDestroy(e);
+  for (double* h : c->sp_stage_h)
+    if (h) cudaFreeHost(h);
   if (c->h_spec) cudaFreeHost(c->h_spec);
   if (c->spec_flags) cudaFree(c->spec_flags);
   if (c->copy_stream) {
@@ -1986,6 +1990,15 @@ int rfgpu_ctx_release_memory(rfgpu_ctx* c) {
   if (c->a_cache) cudaFree(c->a_cache);
   c->a_cache = nullptr;
   c->a_cache_bytes = 0;
+  for (double*& h : c->sp_stage_h) {  // pinned host stages too
+    if (h) cudaFreeHost(h);
+    h = nullptr;
+  }
+  c->sp_stage_bytes = 0;
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  c->graphs.clear();
+  c->graph_seen.clear();
+  cudaDeviceGraphMemTrim(c->device);
   for (cudaMemPool_t pool : {c->pool_small, c->pool_large})
     if (pool) cudaMemPoolTrimTo(pool, 0);
   return RFGPU_OK;
@@ -2653,12 +2666,10 @@ Status sp_flush(rfgpu_single_pass* s) {
 void sp_free(rfgpu_single_pass* s) {
   if (!s) return;
   cudaSetDevice(s->ctx->device);
-  cudaStreamSynchronize(s->ctx->stream);
   if (s->ctx->copy_stream) cudaStreamSynchronize(s->ctx->copy_stream);
   for (double* p : {s->gc, s->gr, s->yc, s->yr, s->scratch, s->stage_d[0], s->stage_d[1]})
-    if (p) cudaFree(p);
-  for (double* p : {s->stage_h[0], s->stage_h[1]})
-    if (p) cudaFreeHost(p);
+    if (p) cudaFreeAsync(p, s->ctx->stream);
+  cudaStreamSynchronize(s->ctx->stream);  // the pinned stages (the context's) may be refilled by the next call
   for (cudaEvent_t e : {s->copied[0], s->copied[1], s->used[0], s->used[1]})
     if (e) cudaEventDestroy(e);
   delete s;
@@ -2689,25 +2700,50 @@ int rfgpu_single_pass_begin(rfgpu_ctx* c, int64_t m, int64_t n, int64_t ell, con
   // staging chunk: ~512 MiB of columns per stage (two stages), at least 256 columns
   s->chunk = std::max<int64_t>(256, std::min<int64_t>(n, (int64_t(1) << 26) / std::max<int64_t>(1, m)));
   cudaSetDevice(c->device);
-  bool ok = (c->copy_stream || cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) == cudaSuccess) &&
-            cudaMalloc(&s->gc, sizeof(double) * n * ell) == cudaSuccess &&
-            cudaMalloc(&s->gr, sizeof(double) * m * ell) == cudaSuccess &&
-            cudaMalloc(&s->yc, sizeof(double) * m * ell) == cudaSuccess &&
-            cudaMalloc(&s->yr, sizeof(double) * n * ell) == cudaSuccess &&
-            cudaMalloc(&s->scratch, sizeof(double) * m * ell) == cudaSuccess;
-  for (int b = 0; b < 2 && ok; ++b)
-    ok = cudaMalloc(&s->stage_d[b], sizeof(double) * m * s->chunk) == cudaSuccess &&
-         cudaMallocHost(&s->stage_h[b], sizeof(double) * m * s->chunk) == cudaSuccess &&
-         cudaEventCreateWithFlags(&s->copied[b], cudaEventDisableTiming) == cudaSuccess &&
+  // device buffers from the context's pools (stream-ordered); the pinned stages are kept on the context, so
+  // repeated streamed calls do not page-lock 1 GiB each time
+  const size_t stage_bytes = sizeof(double) * m * s->chunk;
+  bool ok = c->copy_stream || cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
+  cudaStream_t st = c->stream;
+  auto dalloc = [&](double** p, size_t bytes) {
+    ok = ok && ws_alloc(reinterpret_cast<void**>(p), bytes, st) == cudaSuccess;
+  };
+  dalloc(&s->gc, sizeof(double) * n * ell);
+  dalloc(&s->gr, sizeof(double) * m * ell);
+  dalloc(&s->yc, sizeof(double) * m * ell);
+  dalloc(&s->yr, sizeof(double) * n * ell);
+  dalloc(&s->scratch, sizeof(double) * m * ell);
+  dalloc(&s->stage_d[0], stage_bytes);
+  dalloc(&s->stage_d[1], stage_bytes);
+  if (ok && c->sp_stage_bytes < stage_bytes) {
+    cudaStreamSynchronize(st);
+    for (double*& h : c->sp_stage_h) {
+      if (h) cudaFreeHost(h);
+      h = nullptr;
+    }
+    c->sp_stage_bytes = 0;
+    ok = cudaMallocHost(&c->sp_stage_h[0], stage_bytes) == cudaSuccess &&
+         cudaMallocHost(&c->sp_stage_h[1], stage_bytes) == cudaSuccess;
+    if (ok) c->sp_stage_bytes = stage_bytes;
+  }
+  for (int b = 0; b < 2 && ok; ++b) {
+    s->stage_h[b] = c->sp_stage_h[b];
+    ok = cudaEventCreateWithFlags(&s->copied[b], cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&s->used[b], cudaEventDisableTiming) == cudaSuccess;
+  }
   if (!ok) {
     cudaGetLastError();
     sp_free(s);
     return finish(make_err(RFGPU_ENOMEM, "single_pass: device allocation failed"));
   }
-  cudaMemcpy(s->gc, gc, sizeof(double) * n * ell, cudaMemcpyHostToDevice);
-  cudaMemcpy2D(s->gr, sizeof(double) * m, gr + shape.row0, sizeof(double) * shape.m_global, sizeof(double) * m, ell,
-               cudaMemcpyHostToDevice);
+  cudaError_t ce = cudaMemcpyAsync(s->gc, gc, sizeof(double) * n * ell, cudaMemcpyHostToDevice, st);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpy2DAsync(s->gr, sizeof(double) * m, gr + shape.row0, sizeof(double) * shape.m_global,
+                           sizeof(double) * m, ell, cudaMemcpyHostToDevice, st);
+  if (ce != cudaSuccess) {
+    sp_free(s);
+    return finish(make_err(RFGPU_ECUDA, std::string("single_pass: ") + cudaGetErrorString(ce)));
+  }
   *out = s;
   return RFGPU_OK;
 }
