@@ -503,6 +503,7 @@ def main():
     # pinned buffers is reported beside it.
     e2e = None
     if not args.no_e2e and kind == "rsvd":
+        ctx.release_memory()  # the device-resident call's graph and cached pools: the host call needs the room
         try:
             Gh = rf.gaussian(SEED, "range.G", n, ell)
             gflat = np.asfortranarray(Gh).reshape(-1, order="F")

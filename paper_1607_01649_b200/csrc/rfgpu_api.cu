@@ -590,6 +590,20 @@ std::vector<std::pair<int64_t, int64_t>> upload_panels(int64_t m) {
   return out;
 }
 
+// Drops every recorded graph of the context (their memory goes back to the driver) and the eager pools'
+// cached blocks; true if anything was released. Used when a large allocation fails.
+bool release_graph_memory(rfgpu_ctx* c) {
+  if (c->graphs.empty()) return false;
+  cudaStreamSynchronize(c->stream);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  c->graphs.clear();
+  c->graph_seen.clear();
+  cudaDeviceGraphMemTrim(c->device);
+  for (cudaMemPool_t pool : {c->pool_small, c->pool_large}) cudaMemPoolTrimTo(pool, 0);
+  cudaGetLastError();
+  return true;
+}
+
 // FP64 passes on the INT8 tensor cores (ozaki.cu) for one call: the digit
 // planes of A are built once (inside pass 1) and serve every later pass.
 struct OzPasses {
@@ -614,7 +628,9 @@ struct OzPasses {
     const size_t base = (ozaki_a_bytes(m->m, m->n, digits) + 4095) / 4096 * 4096;
     const size_t set = ozaki_set_bytes(m->m, m->n, digits);
     const size_t wbytes = std::max(ozaki_nn_work_bytes(lay, m->m, ell), ozaki_tn_work_bytes(lay, ell));
-    const bool both = planes.alloc(base + set, c->stream).ok();
+    bool both = planes.alloc(base + set, c->stream).ok();
+    if (!both && !c->capturing && release_graph_memory(c))  // recorded graphs hold their own copies: free them
+      both = planes.alloc(base + set, c->stream).ok();
     if ((!both && !planes.alloc(base, c->stream).ok()) || !work.alloc(wbytes, c->stream).ok()) {
       on = false;
       if (std::getenv("RFGPU_DEBUG")) std::fprintf(stderr, "[rfgpu] digit planes do not fit: DMMA passes\n");
@@ -756,7 +772,7 @@ Status stage_ring(rfgpu_ctx* c) {
 void host_copy_cols(rfgpu_ctx* c, double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
                     int64_t cols) {
   const int64_t bytes = rows * cols * 8;
-  const int nt = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, bytes >> 24)));
+  const int nt = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, bytes >> 23)));  // 8 MiB tasks
   auto part = [&](int t) {
     if (cols >= nt) {
       for (int64_t j = cols * t / nt; j < cols * (t + 1) / nt; ++j)
