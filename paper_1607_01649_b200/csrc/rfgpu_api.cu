@@ -755,15 +755,19 @@ bool host_is_pageable(const void* p) {
 
 Status stage_ring(rfgpu_ctx* c) {
   if (!c->stage_slots.empty()) return {};
-  for (int i = 0; i < kStageSlots; ++i) {
+  const char* es = std::getenv("RFGPU_STAGE_SLOTS");  // experiments
+  const char* eb = std::getenv("RFGPU_STAGE_MB");
+  const int slots = es ? std::max(2, std::atoi(es)) : kStageSlots;
+  const size_t bytes = eb ? (static_cast<size_t>(std::max(16, std::atoi(eb))) << 20) : kStageBytes;
+  for (int i = 0; i < slots; ++i) {
     void* p = nullptr;
     cudaEvent_t e;
-    RF_CUDA(cudaMallocHost(&p, kStageBytes));
+    RF_CUDA(cudaMallocHost(&p, bytes));
     c->stage_slots.push_back(p);
     RF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->stage_done.push_back(e);
   }
-  c->stage_bytes = kStageBytes;
+  c->stage_bytes = bytes;
   return {};
 }
 
