@@ -8,6 +8,7 @@
 // device memory so no host round trip happens per column; only the final
 // count is read back by the orchestrator.
 #include <algorithm>
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "rfgpu_internal.h"
@@ -15,6 +16,8 @@
 namespace rfgpu {
 
 namespace {
+
+namespace cg = cooperative_groups;
 
 constexpr int kRowsPerChunk = 4096;
 
@@ -104,6 +107,87 @@ __global__ void copy_cols_kernel(const double* __restrict__ X, int64_t ldx, int6
   }
 }
 
+// The in-block part of the blocked Gram-Schmidt for one block of b columns W (m x b, already orthogonalised
+// against every earlier block), in ONE cooperative launch: column after column, two passes of projection
+// against the block's kept columns, then the drop rule and normalisation. Each CTA owns a contiguous row
+// range; the sums over rows are per-CTA partials reduced by every CTA in the same fixed order (identical
+// results everywhere, no extra barrier), with a grid barrier between writing and reading partials (three
+// per column) and alternating partial buffers. The kept count lives on the device (*r_dev, base *r0_dev).
+__global__ void __launch_bounds__(256) gs_block_kernel(double* __restrict__ W, int64_t m, int b,
+                                                       double* __restrict__ Q, int64_t ldq,
+                                                       int64_t* __restrict__ r_dev, const int64_t* __restrict__ r0_dev,
+                                                       const double* __restrict__ xnorm2, double* __restrict__ part,
+                                                       int cmax) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[8][33];
+  __shared__ double dots[64];
+  const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t rows_per = (m + G - 1) / G;
+  const int64_t i0 = min(m, static_cast<int64_t>(blockIdx.x) * rows_per), i1 = min(m, i0 + rows_per);
+  const int64_t r0 = *r0_dev;
+  int64_t r = r0;
+  const double drop = 1e-13 * sqrt(*xnorm2);
+  int buf = 0;
+  // CTA partial sums of up to 32 values at once: vals[j] for j < nv, written to part[buf][cta][j]
+  auto cta_partials = [&](const double* vals, int nv) {
+    for (int j = 0; j < nv; ++j) {
+      double s2 = warp_sum(vals[j]);
+      if (lane == 0) red[warp][j] = s2;
+    }
+    __syncthreads();
+    if (tid < nv) {
+      double s2 = 0.0;
+      for (int w = 0; w < 8; ++w) s2 += red[w][tid];
+      part[(static_cast<int64_t>(buf) * G + blockIdx.x) * cmax + tid] = s2;
+    }
+    __syncthreads();
+  };
+  auto reduce_all = [&](int nv) {  // dots[j] = sum over CTAs, fixed order (every CTA the same bits)
+    for (int j = tid; j < nv; j += blockDim.x) {
+      double s2 = 0.0;
+      for (int g = 0; g < G; ++g) s2 += part[(static_cast<int64_t>(buf) * G + g) * cmax + j];
+      dots[j] = s2;
+    }
+    __syncthreads();
+    buf ^= 1;
+  };
+  for (int t = 0; t < b; ++t) {
+    double* v = W + static_cast<int64_t>(t) * m;
+    const int nk = static_cast<int>(r - r0);  // the block's kept columns so far (< 32)
+    for (int pass = 0; pass < 2 && nk > 0; ++pass) {
+      double acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+      for (int64_t i = i0 + tid; i < i1; i += blockDim.x) {
+        const double vi = v[i];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nk) acc[j] = fma(Q[(r0 + j) * ldq + i], vi, acc[j]);
+      }
+      cta_partials(acc, nk);
+      grid.sync();
+      reduce_all(nk);
+      for (int64_t i = i0 + tid; i < i1; i += blockDim.x) {
+        double x = v[i];
+        for (int j = 0; j < nk; ++j) x -= dots[j] * Q[(r0 + j) * ldq + i];
+        v[i] = x;
+      }
+    }
+    double sq[1] = {0.0};
+    for (int64_t i = i0 + tid; i < i1; i += blockDim.x) sq[0] = fma(v[i], v[i], sq[0]);
+    cta_partials(sq, 1);
+    grid.sync();
+    reduce_all(1);
+    const double nrm = sqrt(dots[0]);
+    if (nrm > drop && nrm > 0.0) {
+      for (int64_t i = i0 + tid; i < i1; i += blockDim.x) Q[r * ldq + i] = v[i] / nrm;
+      ++r;
+    }
+    __syncthreads();  // dots[] is rewritten by the next column
+  }
+  if (blockIdx.x == 0 && tid == 0) *r_dev = r;
+}
+
 inline int grid_for(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(1184, (n + 255) / 256))); }
 
 }  // namespace
@@ -180,6 +264,25 @@ cudaError_t gs_orth(const double* X, int64_t m, int64_t c, int64_t ldx, double* 
         sub_kernel<<<grid_for(m * b), 256, 0, st>>>(W, T, m * b);
         count_launch();
       }
+    }
+    if (!ar.fn) {  // one cooperative launch for the block's columns
+      static int coop_blocks = 0;
+      if (coop_blocks == 0) {
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_block_kernel, 256, 0);
+        coop_blocks = std::max(1, std::min(2, per_sm)) * sms;
+      }
+      int G = static_cast<int>(std::min<int64_t>(coop_blocks, std::max<int64_t>(1, (m + 1023) / 1024)));
+      int bb = static_cast<int>(b), cm = 32;
+      const double* xn = scal + 1;
+      double* gpart = T;  // m x kBlock scratch, free here: 2 x G x 32 partials
+      void* args[] = {&W, const_cast<int64_t*>(&m), &bb, &Q, &ldq, &r_dev, &r0_dev, &xn, &gpart, &cm};
+      e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gs_block_kernel), dim3(G), dim3(256), args, 0, st);
+      count_launch();
+      if (e != cudaSuccess) return e;
+      continue;
     }
     for (int64_t t = 0; t < b; ++t) {  // then within the block, column by column (CGS2, drop rule)
       copy_col_kernel<<<grid_for(m), 256, 0, st>>>(W + t * m, m, v);
