@@ -1281,11 +1281,11 @@ Status with_speculation(rfgpu_ctx* c, const std::vector<int64_t>& key, F&& body)
 }
 
 // ---- CUDA graphs of whole calls --------------------------------------------------------------
-// RFGPU_GRAPH=0 disables. Not with profiling (per-phase events), the host-staged reduction backend (its
-// host callback) or a host-resident input.
+// RFGPU_GRAPH=0 disables. Not with profiling (per-phase events), multi-rank contexts or a host-resident input.
 bool graphs_enabled(rfgpu_ctx* c) {
   const char* e = std::getenv("RFGPU_GRAPH");
-  return !(e && e[0] == '0') && !c->profile && !c->host_sum;
+  // single GPU only: multi-rank calls keep their collectives outside graphs (not exercised on one-GPU boxes)
+  return !(e && e[0] == '0') && !c->profile && !c->host_sum && c->world == 1;
 }
 
 void graph_drop(rfgpu_ctx* c, const std::vector<int64_t>& key) {
