@@ -7,6 +7,7 @@
 //   dropin_probe cpu                       -> expects randfact::Error without a GPU
 //   dropin_probe rsvd A.bin m n k p q reorth out.bin
 //   dropin_probe cur  A.bin m n k p out.bin
+//   dropin_probe spsvd A.bin m n k p b out.bin -> single_pass_svd(MatrixStream(A, b)) + stream telemetry
 //   dropin_probe io   FILE out.bin          -> randfact::read_matrix (matrix_io.hpp) from the drop-in
 //   dropin_probe iow  A.bin m n FILE        -> randfact::write_matrix
 #include <cstdio>
@@ -18,6 +19,7 @@
 #include "randfact/dense.hpp"
 #include "randfact/lowrank.hpp"
 #include "randfact/matrix_io.hpp"
+#include "randfact/stream.hpp"
 #include "randfact/rangefinder.hpp"
 #include "randfact/sketch.hpp"
 
@@ -80,6 +82,23 @@ int main(int argc, char** argv) {
     for (idx i : c.Is) out.push_back(static_cast<double>(i));
     write_vec(argv[7], out);
     std::printf("kc %zu kr %zu condC %.6g condR %.6g\n", c.Js.size(), c.Is.size(), c.cond_C, c.cond_R);
+    return 0;
+  }
+  if (argc >= 9 && std::string(argv[1]) == "spsvd") {
+    const idx m = std::atoll(argv[3]), n = std::atoll(argv[4]);
+    DenseMatrix a = read_matrix_bin(argv[2], m, n);
+    MatrixStream stream(a, std::atoll(argv[7]));
+    SvdFactors f = single_pass_svd(stream, std::atoll(argv[5]), std::atoll(argv[6]), 1);
+    write_vec(argv[8], f.D);
+    std::printf("rank %zu entries_served %llu passes_completed %d has_next %d\n", f.D.size(),
+                static_cast<unsigned long long>(stream.entries_served()), stream.passes_completed(),
+                stream.has_next() ? 1 : 0);
+    try {
+      single_pass_svd(stream, std::atoll(argv[5]), std::atoll(argv[6]), 1);
+      std::printf("SECOND_PASS_ALLOWED\n");
+    } catch (const StreamContractError&) {
+      std::printf("STREAM_CONTRACT_OK\n");
+    }
     return 0;
   }
   if (argc >= 4 && std::string(argv[1]) == "io") {

@@ -57,3 +57,23 @@ def test_probe_cur_matches_oracle(port):
         got = np.fromfile(out).astype(np.int64)
     want = port.randomized_cur(a, 30, 10, 0, 1)
     assert np.array_equal(got[:30], want.Js) and np.array_equal(got[30:], want.Is)
+
+
+@needs_probe
+@pytest.mark.gpu
+def test_probe_single_pass_stream_telemetry(port):
+    """single_pass_svd(MatrixStream&) through the drop-in (which reads the stream's matrix in slabs): the
+    stream ends exactly as if drained block by block (acceptance #8, acceptance.cpp:296-316), a second
+    pass raises StreamContractError, and the singular values match the oracle's single pass."""
+    m, n, k, p, b = 700, 520, 12, 12, 32
+    a = port.planted(m, n, np.exp(-np.arange(1, 301) / 12.0), 3) + 1e-9 * port.gaussian(3, "noise.N", m, n)
+    with tempfile.TemporaryDirectory() as d:
+        ain, out = os.path.join(d, "a.bin"), os.path.join(d, "o.bin")
+        np.asfortranarray(a).reshape(-1, order="F").tofile(ain)
+        r = run("spsvd", ain, m, n, k, p, b, out)
+        assert r.returncode == 0, r.stdout + r.stderr
+        got = np.fromfile(out)
+    assert f"rank {k} entries_served {m * n} passes_completed 1 has_next 0" in r.stdout
+    assert "STREAM_CONTRACT_OK" in r.stdout
+    want = port.single_pass_svd(a, k, p, 1, block=b)
+    assert np.max(np.abs(got - want.D) / want.D) <= 1e-8
