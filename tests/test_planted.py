@@ -37,3 +37,43 @@ def test_planted_row_blocks_match_whole(ref):
 def test_spectra():
     assert pl.spectrum("decade6", 1000)[-1] == pytest.approx(1e-6)
     assert pl.spectrum("pow2", 3)[2] == pytest.approx(1 / 9)
+
+
+def _planted_worker(rank, world, port, out):
+    import os
+    import sys
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1607_01649_b200 import planted as p
+    m, n = 777, 160
+    r0, r1 = m * rank // world, m * (rank + 1) // world
+    at = p.planted_matrix(m, n, p.spectrum("pow1.5", 90), 2, noise=1e-8, row0=r0, row1=r1,
+                          allreduce=lambda t: dist.all_reduce(t))
+    out.put((rank, r0, r1, at.numpy().copy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_planted_row_sharded_world2_matches_whole():
+    """bench.py's multi-rank generator: every rank builds only its rows (distributed CholeskyQR2 of the
+    reference Gaussian), and together they are the whole planted matrix."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_planted_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    parts = sorted([q.get(timeout=240) for _ in range(2)])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    got = np.hstack([at for _, _, _, at in parts]).T  # (m, n)
+    whole = pl.planted_matrix(777, 160, pl.spectrum("pow1.5", 90), 2, noise=1e-8).numpy().T
+    assert np.max(np.abs(got - whole)) <= 1e-14 * np.max(np.abs(whole))
