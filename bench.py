@@ -198,14 +198,17 @@ def run_reference_rsvd(w, a_sample, threads):
 # column: small samples sit in host caches, config-size A does not): measured at 16 threads on the GPU box,
 # 8192 / 24576 / 65536 / 131072 / 262144 rows: 3.35 / 8.0 / 22.8 / 47.1 / 110.5 s
 # (gpurun_out r02b_refcurve16.json -> profiles/r02_reference_curve.json), and the FULL config-3 call once:
-# 560.2 s (tools/parity_config_full.py, profiles/r02_parity_c3.json). A linear fit through small samples
+# 560.2 s (tools/parity_config_full.py, profiles/r02_parity_c3.json); at the reference's default 8 threads
+# 709.4 s (tools/ref_full_time.py, profiles/r02_reference_c3_8threads.json). A linear fit through small samples
 # would claim ~300 s. The CPU numbers below are therefore anchored on that full-size measurement: every step
 # times the reference on an 8192-row sample of the workload and scales it by full / sample as measured
 # together on this box type.
 ANCHOR = {"c3": {"full_s": 560.19, "threads": 16, "sample_rows": 8192, "sample_s": 3.3506,
                  "source": "profiles/r02_parity_c3.json (reference rsvd on the full config-3 A, 16 threads) and "
                            "profiles/r02_reference_curve.json (8192-row sample, 16 threads)",
-                 "threads8_over_16": 73.826 / 47.112}}
+                 "full_s_8_threads": 709.41,
+                 "source_8_threads": "profiles/r02_reference_c3_8threads.json (the reference's default thread count, "
+                                     "min(hw, 8), dense.cpp:69-94; full config-3 A)"}}
 
 
 def anchored_reference(w, workload, sample_fn, steps, warmup, threads):
@@ -227,7 +230,7 @@ def anchored_reference(w, workload, sample_fn, steps, warmup, threads):
                        f"scaled by {scale:.1f} = full-size measurement / sample measurement ({an['full_s']} s / "
                        f"{an['sample_s']} s at {an['threads']} threads)"),
             "anchor": an, "sample_s": raw, "full_size_measured_s": an["full_s"],
-            "default_threads": 8, "default_threads_value_estimated": an["full_s"] * an["threads8_over_16"]}
+            "default_threads": 8, "default_threads_value_measured": an["full_s_8_threads"]}
     return [t * scale for t in raw], desc
 
 
