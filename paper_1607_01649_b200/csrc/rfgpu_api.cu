@@ -28,6 +28,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "rfgpu.h"
 #include "rfgpu_internal.h"
 
@@ -410,11 +412,21 @@ struct rfgpu_matrix {
 namespace {
 
 // Scoped CUDA-event timer on the context stream.
+// Every phase is also an NVTX range (RFGPU_NVTX=1) for timeline tools (ncu's --nvtx filters, Nsight).
+bool nvtx_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("RFGPU_NVTX");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 struct Timed {
   rfgpu_ctx* c;
   std::string name;
   cudaEvent_t a = nullptr;
   Timed(rfgpu_ctx* ctx, const char* nm) : c(ctx), name(nm) {
+    if (nvtx_on()) nvtxRangePushA(nm);
     if (c->profile) {
       a = c->get_event();
       cudaEventRecord(a, c->stream);
@@ -426,6 +438,7 @@ struct Timed {
       cudaEventRecord(b, c->stream);
       c->pending.push_back({name, a, b});
     }
+    if (nvtx_on()) nvtxRangePop();
   }
 };
 
