@@ -199,7 +199,7 @@ inline int grid_for(int64_t n) { return static_cast<int>(std::max<int64_t>(1, st
 // kept columns (CGS2, drop rule). In exact arithmetic every residual equals
 // the reference's (the kept columns of earlier blocks are orthogonal to the
 // block's), so the same columns are kept; rounding-level differences only.
-constexpr int64_t kBlock = 32;
+constexpr int64_t kBlock = 16;  // the in-block traffic grows with the block width (c b), the GEMMs' with c^2
 
 GemmPlan block_plan_tn(int64_t m, int64_t c) { return plan_gemm(c, kBlock, m, 148); }
 GemmPlan block_plan_nn(int64_t m, int64_t c) { return plan_gemm(m, kBlock, c, 148); }
@@ -236,11 +236,16 @@ cudaError_t gs_orth(const double* X, int64_t m, int64_t c, int64_t ldx, double* 
   // ||X||_F^2 (column by column to honour ldx), accumulated in fixed order
   e = cudaMemsetAsync(scal + 1, 0, sizeof(double), st);
   if (e != cudaSuccess) return e;
-  for (int64_t j = 0; j < c; ++j) {
-    e = sumsq(X + j * ldx, m, sq_part, scal + 4, st);
+  if (ldx == m) {  // contiguous: one fixed-order reduction
+    e = sumsq(X, m * c, sq_part, scal + 1, st);
     if (e != cudaSuccess) return e;
-    e = add_scalar(scal + 1, scal + 4, st);
-    if (e != cudaSuccess) return e;
+  } else {
+    for (int64_t j = 0; j < c; ++j) {
+      e = sumsq(X + j * ldx, m, sq_part, scal + 4, st);
+      if (e != cudaSuccess) return e;
+      e = add_scalar(scal + 1, scal + 4, st);
+      if (e != cudaSuccess) return e;
+    }
   }
   if (ar.fn) {
     e = ar.fn(ar.ctx, scal + 1, 1, st);
