@@ -640,6 +640,7 @@ struct OzParams {
   int64_t rex_stride;      // rowexp is [split][rex_stride] (per K-chunk output-row exponents; 0: one vector)
   int tma3;                // 1: one 3-D TMA copy per operand and stage (no multicast)
   int64_t kb_split_fixed;  // K blocks per split when it must match the chunks (0: even split)
+  int exp_chunk;           // EXPERIMENT switch (RFGPU_OZAKI_CHUNK)
 };
 
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
@@ -821,6 +822,7 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
     uint32_t it = 0, tt = 0;
     for (int64_t g = cid; g < p.ngroups; g += ncl, ++tt) {
       const TileCoord tc = tile_coord(p, g * cl + crank);
+      const int maxc = 256 / tc.w;       // thin digits one MMA can cover (N <= 256)
       mbar_wait(tfree, (tt & 1) ^ 1);  // the epilogue has drained the previous tile
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int kb = 0; kb < tc.nk; ++kb, ++it) {
@@ -832,9 +834,14 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
         for (int kk = 0; kk < BK / 32; ++kk) {
 #pragma unroll
           for (int s = 0; s < kS; ++s) {
-#pragma unroll
-            for (int t0 = 0; t0 < kS - s; t0 += 4) {
-              const int cnt = (kS - s - t0) < 4 ? (kS - s - t0) : 4;
+            // the kS - s thin digits of this A digit in the fewest MMAs of N <= 256 columns, split evenly
+            // (7 digits of 64 columns: 4 + 3, not 4 + 2 + 1): an MMA narrower than 128 columns runs at half
+            // rate (profiles/r01_i8_mix.txt), so single-digit leftovers are avoided where possible
+            const int nch = (kS - s + maxc - 1) / maxc;
+            const int cbase = (kS - s) / nch, crem = (kS - s) % nch;
+            for (int ch = 0, t0 = 0; ch < nch; ++ch) {
+              int cnt = cbase + (ch < crem ? 1 : 0);
+              if (p.exp_chunk == 0) cnt = (kS - s - t0) < 4 ? (kS - s - t0) : 4;  // EXPERIMENT: round-1 chunks
               // M-major: K advances by 32 K-rows = 4 swizzle atoms
               const uint64_t da = L_MN ? umma_desc_mn<BK>(sA + st * ASZ + s * OBM * BK + kk * 32 * OBM)
                                        : umma_desc<BK>(sA + st * ASZ + s * OBM * BK + kk * 32);
@@ -845,6 +852,7 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
                   "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                   "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (s + t0) * tc.w),
                   "l"(da), "l"(db), "r"(idesc_n(tc.w * cnt)), "r"(accum));
+              t0 += cnt;
             }
           }
         }
@@ -1081,6 +1089,10 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
         break;
       }
   p.ngroups = grid / p.cl;
+  {
+    const char* e = std::getenv("RFGPU_OZAKI_CHUNK");
+    p.exp_chunk = (e && e[0] == '0') ? 0 : 1;
+  }
   p.tma3 = (tma3 && p.cl == 1) ? 1 : 0;
   cudaLaunchConfig_t cfgl{};
   cfgl.gridDim = dim3(static_cast<unsigned>(grid));

@@ -1301,6 +1301,20 @@ bool graphs_enabled(rfgpu_ctx* c) {
   return !(e && e[0] == '0') && !c->profile && !c->host_sum && c->world == 1;
 }
 
+// The RFGPU_* switches decide which kernels a call records (digit path or DMMA, Gram kernel, Jacobi variant):
+// their values are part of a graph's key, so a call made under different switches never replays a graph
+// recorded under the old ones (bench.py's DMMA self-check re-runs the same call with RFGPU_OZAKI=0).
+int64_t env_signature() {
+  uint64_t h = 1469598103934665603ull;
+  for (const char* name : {"RFGPU_OZAKI", "RFGPU_OZAKI_SHARED", "RFGPU_OZAKI_CHUNK", "RFGPU_DIGIT_GRAM",
+                           "RFGPU_JACOBI_BLOCK", "RFGPU_JACOBI_RPW", "RFGPU_JACOBI_ROWS", "RFGPU_JACOBI_CROSS"}) {
+    const char* v = std::getenv(name);
+    for (const char* p = v ? v : "\x01"; *p; ++p) h = (h ^ static_cast<unsigned char>(*p)) * 1099511628211ull;
+    h = (h ^ 0xffu) * 1099511628211ull;
+  }
+  return static_cast<int64_t>(h);
+}
+
 void graph_drop(rfgpu_ctx* c, const std::vector<int64_t>& key) {
   for (size_t i = 0; i < c->graphs.size(); ++i)
     if (c->graphs[i].key == key) {
@@ -2259,7 +2273,7 @@ int rfgpu_rsvd_device(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g_dev, 
     const std::vector<int64_t> key = {reinterpret_cast<int64_t>(a), reinterpret_cast<int64_t>(a->dev), a->m, a->n,
                                       a->lda, reinterpret_cast<int64_t>(g_dev), k, ell, q, keep_over, reorth,
                                       reinterpret_cast<int64_t>(U), reinterpret_cast<int64_t>(D),
-                                      reinterpret_cast<int64_t>(V)};
+                                      reinterpret_cast<int64_t>(V), env_signature()};
     rfgpu_ctx::GraphEntry* ge = graphs_enabled(c) ? graph_lookup(c, key) : nullptr;  // profiling: eager phases
     if (!ge && graphs_enabled(c) && !c->spec_failed.count(key) && c->graph_seen[key]++ >= 1)
       ge = graph_capture(c, key, body, &r);
