@@ -35,9 +35,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdlib>
-#include <cstring>
 #include <mutex>
-#include <type_traits>
 
 #include "common.cuh"
 #include "rfgpu_internal.h"
@@ -76,7 +74,7 @@ struct Dig {
   static constexpr int fit = static_cast<int>((225 * 1024 - 2048) / stage_bytes);
   static constexpr int stages = fit > 8 ? 8 : fit;
   static constexpr int tmem_cols = S * OBN <= 256 ? 256 : 512;
-  static constexpr size_t smem = stages * stage_bytes + 1024 + 1024;  // alignment slack + barriers
+  static constexpr size_t smem = stages * stage_bytes + 1024 + 256;
 };
 
 __host__ __device__ inline int64_t roundup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -642,9 +640,6 @@ struct OzParams {
   int64_t rex_stride;      // rowexp is [split][rex_stride] (per K-chunk output-row exponents; 0: one vector)
   int tma3;                // 1: one 3-D TMA copy per operand and stage (no multicast)
   int64_t kb_split_fixed;  // K blocks per split when it must match the chunks (0: even split)
-  int fine;                // 1: plane-granular ring (one full / empty barrier pair per digit plane and stage)
-  int exp_chunk;           // EXPERIMENT switch (RFGPU_OZAKI_CHUNK)
-  int exp_mode;            // EXPERIMENT (RFGPU_OZAKI_EXP): 1 no MMAs (TMA only), 2 no TMA (MMA only), 3 no B loads
 };
 
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
@@ -751,12 +746,6 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
   uint64_t* done = empty + kStages;
   uint64_t* tfree = done + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tfree + 1);
-  // plane-granular ring (p.fine): per stage and digit plane, full / empty barriers of the A plane and of the
-  // thin operand's plane
-  uint64_t* fA = reinterpret_cast<uint64_t*>(tslot + 2);
-  uint64_t* eA = fA + kStages * kS;
-  uint64_t* fB = eA + kStages * kS;
-  uint64_t* eB = fB + kStages * kS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cl = p.cl;
   const int crank = static_cast<int>(blockIdx.x % cl);  // rank in the cluster (consecutive n-tiles)
@@ -767,7 +756,6 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], cl);  // every CTA of the cluster must release the (shared) A stage
     }
-    for (int i = 0; i < 4 * kStages * kS; ++i) mbar_init(&fA[i], 1);
     mbar_init(done, 1);
     mbar_init(tfree, kEpiWarps);
     mbar_fence_init();
@@ -793,42 +781,14 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
       for (int kb = 0; kb < tc.nk; ++kb, ++it) {
         const int st = static_cast<int>(it % kStages);
         const uint32_t ph = (it / kStages) & 1;
-        if (p.fine) {
-          // Plane-granular ring: the MMA warp walks the A digits s = 0 .. kS-1 of a stage in order and releases
-          // A plane s and thin plane kS-1-s (last used by A digit s) right after digit s, so their slots are
-          // refilled for the k-block two ahead while the rest of this stage still computes: ~1.5-1.9 stages of
-          // lookahead instead of 1 (the whole-stage ring stalls on every refill: a pass without its MMAs takes
-          // 11.7 ms, without its loads 16.2 ms, with both 19.5 ms).
-          const CUtensorMap* trp = tc.w == p.w_big ? &tmR : &tmR2;
-          const int kxp = static_cast<int>((tc.kb0 + kb) * BK);
-#pragma unroll
-          for (int s = 0; s < kS; ++s) {
-            const int t = kS - 1 - s;
-            mbar_wait(&eA[st * kS + s], ph ^ 1);
-            mbar_arrive_expect_tx(&fA[st * kS + s], static_cast<uint32_t>(OBM * BK));
-            const int lc0 = L_MN ? static_cast<int>(tc.lrow0) : kxp;
-            const int lc1 = L_MN ? static_cast<int>(s * p.L_rows + (tc.kb0 + kb) * BK)
-                                 : static_cast<int>(s * p.L_rows + tc.lrow0);
-            tma2d(sA + st * ASZ + s * OBM * BK, &tmL, &fA[st * kS + s], lc0, lc1);
-            mbar_wait(&eB[st * kS + t], ph ^ 1);
-            mbar_arrive_expect_tx(&fB[st * kS + t], static_cast<uint32_t>(tc.w * BK));
-            tma2d(sB + st * BSZ + t * tc.w * BK, trp, &fB[st * kS + t], kxp, static_cast<int>(t * p.R_rows + tc.ncol0));
-          }
-          continue;
-        }
         mbar_wait(&empty[st], ph ^ 1);
-        if (p.exp_mode == 2) {  // EXPERIMENT: no loads at all
-          mbar_arrive(&full[st]);
-          continue;
-        }
-        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(p.exp_mode == 3 ? ASZ : ASZ + kS * tc.w * BK));
+        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(ASZ + kS * tc.w * BK));
         const CUtensorMap* tr = tc.w == p.w_big ? &tmR : &tmR2;  // box of w rows
         const int kx = static_cast<int>((tc.kb0 + kb) * BK);
         if (p.tma3) {  // all digit planes of each operand tile in one 3-D copy (2 TMA issues per stage)
           const int lc0 = L_MN ? static_cast<int>(tc.lrow0) : kx;
           const int lc1 = L_MN ? static_cast<int>((tc.kb0 + kb) * BK) : static_cast<int>(tc.lrow0);
           tma3d(sA + st * ASZ, &tmL3, &full[st], lc0, lc1, 0);
-          if (p.exp_mode != 3)
           tma3d(sB + st * BSZ, tc.w == p.w_big ? &tmR3 : &tmR23, &full[st], kx, static_cast<int>(tc.ncol0), 0);
           continue;
         }
@@ -866,66 +826,29 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const __grid_co
       for (int kb = 0; kb < tc.nk; ++kb, ++it) {
         const int st = static_cast<int>(it % kStages);
         const uint32_t ph = (it / kStages) & 1;
-        if (p.fine) {
-#pragma unroll
-          for (int t = 0; t < kS; ++t) mbar_wait(&fB[st * kS + t], ph);  // A digit 0 meets every thin digit
-        } else {
-          mbar_wait(&full[st], ph);
-        }
+        mbar_wait(&full[st], ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        // The kS - s thin digits of A digit s go out in the fewest MMAs of N <= 256 columns, split evenly
-        // (7 digits of 64 columns: 4 + 3, 6: 3 + 3, 5: 3 + 2; 48-column tiles take up to 5 digits per MMA; an
-        // MMA narrower than 128 columns runs at half rate, profiles/r01_i8_mix.txt; measured neutral against
-        // 4 + rest: the passes are not bound by the MMA issue rate). The split is a compile-time table per
-        // tile-width class (runtime divisions on the issuing thread cost more than the MMAs they schedule:
-        // measured 2.2x slower).
-        auto issue = [&](auto maxc_c) {
-          constexpr int MAXC = decltype(maxc_c)::value;
+#pragma unroll
+        for (int kk = 0; kk < BK / 32; ++kk) {
 #pragma unroll
           for (int s = 0; s < kS; ++s) {
-            if (p.fine) {
-              mbar_wait(&fA[st * kS + s], ph);
-              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            }
 #pragma unroll
-            for (int kk = 0; kk < BK / 32; ++kk) {
-              const int nch = (kS - s + MAXC - 1) / MAXC;
-              const int cbase = (kS - s) / nch, crem = (kS - s) % nch;
-#pragma unroll
-              for (int ch = 0; ch < nch; ++ch) {
-                const int cnt = cbase + (ch < crem ? 1 : 0);
-                const int t0 = ch * cbase + (ch < crem ? ch : crem);
-                // M-major: K advances by 32 K-rows = 4 swizzle atoms
-                const uint64_t da = L_MN ? umma_desc_mn<BK>(sA + st * ASZ + s * OBM * BK + kk * 32 * OBM)
-                                         : umma_desc<BK>(sA + st * ASZ + s * OBM * BK + kk * 32);
-                const uint64_t db = umma_desc<BK>(sB + st * BSZ + t0 * tc.w * BK + kk * 32);
-                // groups s + t0 .. s + t0 + cnt - 1; every group is first written by s = 0
-                const uint32_t accum = (kb == 0 && kk == 0 && s == 0) ? 0u : 1u;
-                asm volatile(
-                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (s + t0) * tc.w),
-                    "l"(da), "l"(db), "r"(idesc_n(tc.w * cnt)), "r"(accum));
-              }
-            }
-            if (p.fine) {  // A plane s and thin plane kS-1-s are done with: release their slots
-              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                               smem_u32(&eA[st * kS + s]))
-                           : "memory");
-              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                               smem_u32(&eB[st * kS + (kS - 1 - s)]))
-                           : "memory");
+            for (int t0 = 0; t0 < kS - s; t0 += 4) {
+              const int cnt = (kS - s - t0) < 4 ? (kS - s - t0) : 4;
+              // M-major: K advances by 32 K-rows = 4 swizzle atoms
+              const uint64_t da = L_MN ? umma_desc_mn<BK>(sA + st * ASZ + s * OBM * BK + kk * 32 * OBM)
+                                       : umma_desc<BK>(sA + st * ASZ + s * OBM * BK + kk * 32);
+              const uint64_t db = umma_desc<BK>(sB + st * BSZ + t0 * tc.w * BK + kk * 32);
+              // groups s + t0 .. s + t0 + cnt - 1; every group is first written by s = 0
+              const uint32_t accum = (kb == 0 && kk == 0 && s == 0) ? 0u : 1u;
+              asm volatile(
+                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (s + t0) * tc.w),
+                  "l"(da), "l"(db), "r"(idesc_n(tc.w * cnt)), "r"(accum));
             }
           }
-        };
-        if (p.exp_mode == 1) {  // EXPERIMENT: no MMAs
-        } else if (tc.w > 48)
-          issue(std::integral_constant<int, 4>{});
-        else if (tc.w > 32)
-          issue(std::integral_constant<int, 5>{});
-        else
-          issue(std::integral_constant<int, kS>{});
-        if (p.fine) {
-        } else if (cl == 1)
+        }
+        if (cl == 1)
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                            smem_u32(&empty[st]))
                        : "memory");
@@ -1158,14 +1081,6 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
         break;
       }
   p.ngroups = grid / p.cl;
-  {
-    const char* e = std::getenv("RFGPU_OZAKI_CHUNK");
-    p.exp_chunk = (e && e[0] == '0') ? 0 : 1;
-    const char* f = std::getenv("RFGPU_OZAKI_FINE");
-    p.fine = (p.cl == 1 && !(f && f[0] == '0')) ? 1 : 0;
-    const char* x = std::getenv("RFGPU_OZAKI_EXP");
-    p.exp_mode = x ? std::atoi(x) : 0;
-  }
   p.tma3 = (tma3 && p.cl == 1) ? 1 : 0;
   cudaLaunchConfig_t cfgl{};
   cfgl.gridDim = dim3(static_cast<unsigned>(grid));
@@ -1175,13 +1090,6 @@ cudaError_t launch_digit_gemm_s(const int8_t* L, int64_t L_rows, bool L_mn, int6
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(p.cl);
-  {  // EXPERIMENT (RFGPU_OZAKI_COSCHED=c): launch the c n-tile CTAs sharing an A tile as one cluster (co-scheduled,
-     // otherwise independent: no multicast, no shared barriers) so that they read the tile at about the same time
-    const char* e = std::getenv("RFGPU_OZAKI_COSCHED");
-    const int c = e ? std::atoi(e) : 0;
-    const bool tn_only = e && std::strchr(e, 't');
-    if (c > 1 && p.cl == 1 && p.ntn % c == 0 && (!tn_only || !L_mn)) attr[0].val.clusterDim.x = static_cast<unsigned>(c);
-  }
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfgl.attrs = attr;

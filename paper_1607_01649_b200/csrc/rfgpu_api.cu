@@ -1306,7 +1306,7 @@ bool graphs_enabled(rfgpu_ctx* c) {
 // recorded under the old ones (bench.py's DMMA self-check re-runs the same call with RFGPU_OZAKI=0).
 int64_t env_signature() {
   uint64_t h = 1469598103934665603ull;
-  for (const char* name : {"RFGPU_OZAKI", "RFGPU_OZAKI_SHARED", "RFGPU_OZAKI_CHUNK", "RFGPU_DIGIT_GRAM",
+  for (const char* name : {"RFGPU_OZAKI", "RFGPU_OZAKI_SHARED", "RFGPU_DIGIT_GRAM",
                            "RFGPU_JACOBI_BLOCK", "RFGPU_JACOBI_RPW", "RFGPU_JACOBI_ROWS", "RFGPU_JACOBI_CROSS"}) {
     const char* v = std::getenv(name);
     for (const char* p = v ? v : "\x01"; *p; ++p) h = (h ^ static_cast<unsigned char>(*p)) * 1099511628211ull;

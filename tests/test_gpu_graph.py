@@ -81,3 +81,49 @@ def test_graph_falls_back_when_speculation_fails(port):
     for r, d, _ in got:
         assert r == len(want.D) == 15
         assert np.max(np.abs(d - want.D) / want.D) <= 1e-9
+
+
+def test_graph_is_keyed_by_the_path_switches(port):
+    """A graph recorded on the digit path must not be replayed when the same call is made with
+    RFGPU_OZAKI=0 (bench.py's DMMA self-check does exactly that): the replies differ in the last bits,
+    and the DMMA reply equals the eager DMMA call bit for bit."""
+    import torch
+    m, n = 3000, 700
+    a = port.planted(m, n, 1.0 / np.arange(1, 401) ** 1.5, 1) + 1e-9 * port.gaussian(1, "noise.N", m, n)
+    at = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()
+    ctx = rf.Context(0)
+    # same context, same buffers: 4 calls on the digits (graph recorded and replayed), then the DMMA call
+    ell = 40
+    A = rf.DeviceMatrix.wrap(ctx, at.data_ptr(), m, n, m, keep=at)
+    g = torch.from_numpy(rf.gaussian(1, "range.G", n, ell).reshape(-1, order="F")).cuda()
+    U = torch.zeros(m * ell, dtype=torch.float64, device="cuda")
+    D = torch.zeros(ell, dtype=torch.float64, device="cuda")
+    V = torch.zeros(n * ell, dtype=torch.float64, device="cuda")
+    r = rf._i64()
+
+    def call():
+        rf._check(rf.lib().rfgpu_rsvd_device(ctx.handle, A.handle, rf._vp(g.data_ptr()), 30, ell, 1, 0, 1,
+                                             rf._vp(U.data_ptr()), rf._vp(D.data_ptr()), rf._vp(V.data_ptr()),
+                                             rf.C.byref(r)))
+        ctx.synchronize()
+        return D.cpu().numpy()[:30].copy()
+
+    old = os.environ.get("RFGPU_OZAKI")
+    try:
+        os.environ["RFGPU_OZAKI"] = "1"
+        digits = [call() for _ in range(4)][-1]
+        os.environ["RFGPU_OZAKI"] = "0"
+        dmma = call()
+    finally:
+        if old is None:
+            os.environ.pop("RFGPU_OZAKI", None)
+        else:
+            os.environ["RFGPU_OZAKI"] = old
+    A.free()
+    ctx.close()
+    ctx2 = rf.Context(0)
+    want = device_rsvd(ctx2, at, m, n, 30, 10, 1, True, 1, {"RFGPU_OZAKI": "0", "RFGPU_GRAPH": "0"})[0][1]
+    ctx2.close()
+    assert np.array_equal(dmma, want)
+    assert not np.array_equal(dmma, digits)
+    assert np.max(np.abs(dmma - digits) / dmma) <= 1e-12
