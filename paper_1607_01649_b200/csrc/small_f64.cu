@@ -951,10 +951,7 @@ JacobiLayout jacobi_layout(int64_t mr, int64_t c) {
   // Row groups per pair: enough warps to keep ~8 rows each. More groups make
   // the rows/warp loop shorter but the serial per-pair reduction over groups
   // longer; both sit on every round's critical path.
-  static const int rpw = [] {
-    const char* e = std::getenv("RFGPU_JACOBI_RPW");
-    return e ? std::max(1, std::atoi(e)) : 8;
-  }();
+  constexpr int rpw = 8;  // (measured best at l = 60 ... 330)
   auto groups = [&](int64_t rows) { return std::max<int64_t>(1, std::min<int64_t>(32 / G, (rows + rpw - 1) / rpw)); };
   auto extra = [&](int P, bool bcast) {
     const int64_t H = groups((mr + P - 1) / P);
@@ -967,10 +964,7 @@ JacobiLayout jacobi_layout(int64_t mr, int64_t c) {
   constexpr size_t kMax = 224 * 1024;
   // Smallest cluster that leaves at most `target` rows of X per CTA: the
   // per-round shared-memory traffic of a CTA is proportional to its rows.
-  static const int target = [] {
-    const char* e = std::getenv("RFGPU_JACOBI_ROWS");
-    return e ? std::max(1, std::atoi(e)) : 32;
-  }();
+  constexpr int target = 32;
   int P0 = 1;
   while (P0 < 16 && (mr + P0 - 1) / P0 > target) P0 *= 2;
   for (bool bcast : {true, false}) {
@@ -1215,8 +1209,7 @@ cudaError_t bjacobi_launch(const JacobiProblem* pr, int count, int64_t mr, int64
                            cudaStream_t st) {
   BJParams ps[2];
   for (int i = 0; i < count; ++i) {
-    const char* co = std::getenv("RFGPU_JACOBI_CROSS");
-    ps[i] = BJParams{pr[i].X, static_cast<int>(mr), static_cast<int>(c), B.nb, (co && co[0] == '0') ? 0 : 1,
+    ps[i] = BJParams{pr[i].X, static_cast<int>(mr), static_cast<int>(c), B.nb, /*cross_only=*/1,
                      pr[i].U, pr[i].S, pr[i].V,
                      pr[i].work, pr[i].work + static_cast<size_t>(B.nb) * B.B * (mr + (mr & 1)), pr[i].info,
                      pr[i].sweeps};
