@@ -118,6 +118,43 @@ __global__ void f32_to_f64_kernel(const float* __restrict__ x, int64_t rows, int
   }
 }
 
+// Shifted CholeskyQR3: G += shift * trace(G) on the diagonal (one CTA), and the reference-drop-rule statistic
+// out[0] = min_j r1(j,j) r2(j,j) r3(j,j) / sqrt(trace(G of X)) from the three Cholesky factors' diagonals.
+__global__ void shift_diag_kernel(double* __restrict__ G, int c, double shift, double* __restrict__ trace_out) {
+  __shared__ double red[32];
+  double t = 0.0;
+  for (int j = threadIdx.x; j < c; j += blockDim.x) t += G[static_cast<int64_t>(j) * c + j];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    t = 0.0;
+    for (unsigned w = 0; w < (blockDim.x >> 5); ++w) t += red[w];
+    red[0] = t;
+    trace_out[0] = t;
+  }
+  __syncthreads();
+  const double s = shift * red[0];
+  for (int j = threadIdx.x; j < c; j += blockDim.x) G[static_cast<int64_t>(j) * c + j] += s;
+}
+__global__ void rdiag_min_kernel(const double* __restrict__ R1, const double* __restrict__ R2,
+                                 const double* __restrict__ R3, int c, const double* __restrict__ trace,
+                                 double* __restrict__ out) {
+  __shared__ double red[32];
+  double mn = INFINITY;
+  for (int j = threadIdx.x; j < c; j += blockDim.x) {
+    const int64_t d = static_cast<int64_t>(j) * c + j;
+    mn = fmin(mn, R1[d] * R2[d] * R3[d]);
+  }
+  for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (unsigned w = 1; w < (blockDim.x >> 5); ++w) mn = fmin(mn, red[w]);
+    out[0] = trace[0] > 0.0 ? mn / sqrt(trace[0]) : 0.0;
+  }
+}
+
 // Speculative orth: the CholeskyQR2 gate (both factorizations succeeded and min pivot / trace(G) >= gate),
 // else bit 0 of *flags. Jacobi: info 1 (no convergence) sets bit 1.
 __global__ void orth_gate_kernel(const int* info, const double* info_d, double gate, int* flags) {
@@ -1049,6 +1086,74 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
       RF_TRY(gemm(c, false, m, cols, cols, Q1, ldq1, R2i, cols, out->Q, out->ldq, nullptr, "trsm", false, true));
     }
     return {};
+  }
+  // Ill-conditioned but full-rank X (the plain power mode's sketch (A A^T)^q A G, kappa ~ (s1/sl)^(2q+1)):
+  // shifted CholeskyQR3 (Fukaya et al. 2020). Q1 = X R1^-1 with R1^T R1 = X^T X + shift tr(X^T X) I has
+  // kappa(Q1) ~ sqrt(shift) kappa(X), then CholeskyQR2 on Q1. X = Q (R3 R2 R1) is then THE QR factorization
+  // of X, whose diagonal is the residual norm the reference's Gram-Schmidt tests against 1e-13 ||X||_F
+  // (dense.cpp:404,423): accepted only if every residual clears ten times that, so the reference keeps every
+  // column too; anything closer goes to Gram-Schmidt with the reference's rule itself. Not speculative (host
+  // round trips), not for intermediate bases (single) and only when the fast path has just failed.
+  if (!c->spec && !single && cols > 1) {
+    Timed ts(c, "scholqr3");
+    constexpr double kShift = 1e-11, kMidGate = 1e-14, kDropMargin = 1e-12;
+    DBuf sb, q2buf;
+    RF_TRY(sb.alloc(sizeof(double) * (3 * cc + 16), st));
+    double* R3 = sb.d();
+    double* R3i = R3 + cc;
+    double* G3 = R3i + cc;
+    double* stat = G3 + cc;  // trace, min residual ratio
+    RF_TRY(gram(X, ldx, G1));
+    if (dist) RF_TRY(allreduce(c, G1, cc));
+    rfgpu::shift_diag_kernel<<<1, 256, 0, st>>>(G1, static_cast<int>(cols), kShift, stat);
+    count_launch();
+    RF_CUDA(chol_inv(G1, cols, R1, R1i, cwork, info, infod, st));
+    // Q1 into a temporary, Q2 into the output buffer
+    const int64_t ldt = even(m);
+    RF_TRY(q2buf.alloc(sizeof(double) * std::max<int64_t>(1, ldt * cols), st));
+    double* T1 = q2buf.d();
+    RF_TRY(gemm(c, false, m, cols, cols, X, ldx, R1i, cols, T1, ldt, nullptr, "trsm", false, true));
+    RF_TRY(gram(T1, ldt, G2));
+    if (dist) RF_TRY(allreduce(c, G2, cc));
+    RF_CUDA(chol_inv(G2, cols, R2, R2i, cwork, info + 1, infod + 1, st));
+    RF_CUDA(cudaMemcpyAsync(c->h_info, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    RF_CUDA(cudaMemcpyAsync(c->h_d, infod, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RF_CUDA(cudaStreamSynchronize(st));
+    bool ok = c->h_info[0] == 0 && c->h_info[1] == 0 && c->h_d[1] >= kMidGate;
+    double* Q2 = fold ? out->Q : Q1;
+    const int64_t ldq2 = fold ? out->ldq : ldq1;
+    if (ok) {
+      RF_TRY(gemm(c, false, m, cols, cols, T1, ldt, R2i, cols, Q2, ldq2, nullptr, "trsm", false, true));
+      RF_TRY(gram(Q2, ldq2, G3));
+      if (dist) RF_TRY(allreduce(c, G3, cc));
+      RF_CUDA(chol_inv(G3, cols, R3, R3i, cwork, info, infod, st));
+      rfgpu::rdiag_min_kernel<<<1, 256, 0, st>>>(R1, R2, R3, static_cast<int>(cols), stat, stat + 1);
+      count_launch();
+      RF_CUDA(cudaMemcpyAsync(c->h_info, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+      RF_CUDA(cudaMemcpyAsync(c->h_d, infod, sizeof(double), cudaMemcpyDeviceToHost, st));
+      RF_CUDA(cudaMemcpyAsync(c->h_d + 1, stat + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+      RF_CUDA(cudaStreamSynchronize(st));
+      ok = c->h_info[0] == 0 && c->h_d[0] >= kCholGate && c->h_d[1] >= kDropMargin;
+      if (std::getenv("RFGPU_DEBUG"))
+        std::fprintf(stderr, "[rfgpu] orth: shifted CholeskyQR3 %s (min residual / ||X||_F = %.3e, gate %.3e)\n",
+                     ok ? "accepted" : "rejected", c->h_d[1], c->h_d[0]);
+    }
+    if (ok) {
+      out->fast = true;
+      out->r = cols;
+      if (R) {  // R = R3 R2 R1
+        RF_TRY(gemm(c, false, cols, cols, cols, R2, cols, R1, cols, G2, cols));
+        RF_TRY(gemm(c, false, cols, cols, cols, R3, cols, G2, cols, R, cols));
+      }
+      if (fold) {
+        RF_CUDA(cudaMemcpyAsync(R2inv_buf, R3i, sizeof(double) * cc, cudaMemcpyDeviceToDevice, st));
+        out->R2inv = R2inv_buf;
+        out->folded = true;
+      } else {
+        RF_TRY(gemm(c, false, m, cols, cols, Q2, ldq2, R3i, cols, out->Q, out->ldq, nullptr, "trsm", false, true));
+      }
+      return {};
+    }
   }
   // Gram-Schmidt with the reference's drop rule (its basis replaces Q1 in out->Q).
   if (oz) oz->thin_src = nullptr;

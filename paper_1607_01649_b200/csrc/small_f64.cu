@@ -579,12 +579,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
 // back; a cluster barrier separates block rounds. Every column pair meets
 // once per block sweep, all of a round's work is CTA-local, and there are
 // nb - 1 cluster barriers per sweep instead of c - 1 exchanges.
-// Converged when a block sweep applies no rotation; <= 60 sweeps. The final
+// Converged when a block sweep meets no pair above 1e-14 relative (kJacobiDone); <= 60 sweeps. The final
 // columns are sorted by norm (stable, descending) exactly as jacobi_svd_kernel.
 // Block width B = 8 (more CTAs, fewer pairs per CTA per inner round) when the
 // tournament fits a 16-CTA cluster, else 12, else 16; one warp per pair (32 B
 // threads). Measured at l = 220: B = 8 7.5 ms, B = 16 9.0 ms, the per-column
 // cluster kernel 11.4 ms (9-10 sweeps each).
+
+constexpr double kJacobiDone = 1e-14;
 
 struct BJParams {
   const double* X;  // mr x c input
@@ -694,7 +696,11 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
             vu[i] = cs * a - sn * b;
             vv[i] = sn * a + cs * b;
           }
-          if (lane == 0) s_rot = 1;
+          // The sweeps end once a whole sweep met no pair above kJacobiDone (relative |apq|): rotations of
+          // pairs between the reference's skip tolerance (1e-15) and 1e-14 are still applied, but they are at
+          // the rounding level of apq itself (eps sqrt(rows)) and would otherwise cost two or three more
+          // sweeps of "noise chasing" before one happens to apply none.
+          if (lane == 0 && !(apq * apq <= kJacobiDone * kJacobiDone * (app * aqq))) s_rot = 1;
         }
         __syncthreads();
       }
