@@ -803,6 +803,12 @@ bool host_is_pageable(const void* p) {
   return at.type == cudaMemoryTypeUnregistered;
 }
 
+// EXPERIMENT switch while measuring (RFGPU_STAGE_NT=0: glibc memcpy into the pinned slots)
+bool nt_staging() {
+  const char* e = std::getenv("RFGPU_STAGE_NT");
+  return !(e && e[0] == '0');
+}
+
 Status stage_ring(rfgpu_ctx* c) {
   if (!c->stage_slots.empty()) return {};
   // 4 x 128 MiB measured best at config 3 (8 x 128: 0.90 s, 4 x 256: 0.90 s, 8 x 64: 1.39 s, 3 x 512: 0.99 s
@@ -824,16 +830,21 @@ Status stage_ring(rfgpu_ctx* c) {
 // Parallel strided copy of `cols` columns of `rows` doubles (ld_src -> ld_dst) on the host (the context's
 // worker threads; 16 MiB or so per task).
 void host_copy_cols(rfgpu_ctx* c, double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
-                    int64_t cols) {
+                    int64_t cols, bool stream_dst = false) {
   const int64_t bytes = rows * cols * 8;
   const int nt = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, bytes >> 23)));  // 8 MiB tasks
+  // into a pinned slot (read next by the copy engine only): non-temporal stores (csrc/host_copy.cpp)
+  auto cp = [stream_dst](void* d, const void* s, size_t n) {
+    if (stream_dst) rfgpu::host_stream_copy(d, s, n);
+    else std::memcpy(d, s, n);
+  };
   auto part = [&](int t) {
     if (cols >= nt) {
       for (int64_t j = cols * t / nt; j < cols * (t + 1) / nt; ++j)
-        std::memcpy(dst + j * ldd, src + j * lds, sizeof(double) * rows);
+        cp(dst + j * ldd, src + j * lds, sizeof(double) * rows);
     } else {  // few columns: split the rows
       const int64_t r0 = rows * t / nt, r1 = rows * (t + 1) / nt;
-      for (int64_t j = 0; j < cols; ++j) std::memcpy(dst + j * ldd + r0, src + j * lds + r0, sizeof(double) * (r1 - r0));
+      for (int64_t j = 0; j < cols; ++j) cp(dst + j * ldd + r0, src + j * lds + r0, sizeof(double) * (r1 - r0));
     }
   };
   c->host_pool.run(nt, part);
@@ -855,7 +866,7 @@ Status staged_h2d(rfgpu_ctx* c, double* dev, int64_t ldd, const double* host, in
       const size_t sl = c->stage_next++ % c->stage_slots.size();
       RF_CUDA(cudaEventSynchronize(c->stage_done[sl]));  // the slot's previous copy has landed
       double* buf = static_cast<double*>(c->stage_slots[sl]);
-      host_copy_cols(c, buf, rr, host + c0 * lds + r0, lds, rr, cc);
+      host_copy_cols(c, buf, rr, host + c0 * lds + r0, lds, rr, cc, /*stream_dst=*/nt_staging());
       RF_CUDA(cudaMemcpy2DAsync(dev + c0 * ldd + r0, sizeof(double) * ldd, buf, sizeof(double) * rr, sizeof(double) * rr,
                                 cc, cudaMemcpyHostToDevice, cs));
       RF_CUDA(cudaEventRecord(c->stage_done[sl], cs));
@@ -1045,10 +1056,21 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
     Timed tc(c, "chol");
     RF_CUDA(chol_inv(G1, cols, R1, R1i, cwork, info, infod, st));
   }
+  // Outside speculation the first factorization is checked at once: a sketch that fails it (the plain power
+  // mode's, a rank-deficient one) goes straight to the fallbacks without the m x l product and second Gram.
+  bool first_ok = true;
+  if (!c->spec) {
+    RF_CUDA(cudaMemcpyAsync(c->h_info, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RF_CUDA(cudaMemcpyAsync(c->h_d, infod, sizeof(double), cudaMemcpyDeviceToHost, st));
+    RF_CUDA(cudaStreamSynchronize(st));
+    first_ok = c->h_info[0] == 0 && c->h_d[0] >= kCholGate;
+  }
   // (an INT8 digit-path TRSM from X's digits measured 4.1 ms against 2.9 ms on DMMA at config 3: K = l is too
   // short for the digit GEMM's per-tile fetch and epilogue)
-  RF_TRY(gemm(c, false, m, cols, cols, X, ldx, R1i, cols, Q1, ldq1, nullptr, "trsm", false, /*tri_b=*/true));
-  if (single) {
+  if (first_ok)
+    RF_TRY(gemm(c, false, m, cols, cols, X, ldx, R1i, cols, Q1, ldq1, nullptr, "trsm", false, /*tri_b=*/true));
+  if (!first_ok) {
+  } else if (single) {
     RF_CUDA(cudaMemsetAsync(info + 1, 0, sizeof(int), st));
   } else {
     RF_TRY(gram(Q1, ldq1, G2));
@@ -1057,7 +1079,9 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
     RF_CUDA(chol_inv(G2, cols, R2, R2i, cwork, info + 1, infod + 1, st));
   }
   bool fast;
-  if (c->spec) {  // decided at the end of the call (spec_flags)
+  if (!first_ok) {
+    fast = false;
+  } else if (c->spec) {  // decided at the end of the call (spec_flags)
     rfgpu::orth_gate_kernel<<<1, 1, 0, st>>>(info, infod, kCholGate, c->spec_flags);
     count_launch();
     RF_CUDA(cudaGetLastError());
@@ -1103,8 +1127,7 @@ Status orth(rfgpu_ctx* c, const double* X, int64_t m, int64_t cols, int64_t ldx,
     double* R3i = R3 + cc;
     double* G3 = R3i + cc;
     double* stat = G3 + cc;  // trace, min residual ratio
-    RF_TRY(gram(X, ldx, G1));
-    if (dist) RF_TRY(allreduce(c, G1, cc));
+    // G1 still holds X^T X (summed over ranks): the Cholesky kernels do not write their input
     rfgpu::shift_diag_kernel<<<1, 256, 0, st>>>(G1, static_cast<int>(cols), kShift, stat);
     count_launch();
     RF_CUDA(chol_inv(G1, cols, R1, R1i, cwork, info, infod, st));
@@ -2943,7 +2966,8 @@ int rfgpu_single_pass_push(rfgpu_single_pass* s, int64_t col0, const double* blk
       // a host stage is refilled once its previous copy to the device is done
       if (s->staged == 0) RF_CUDA(cudaEventSynchronize(s->copied[s->cur]));
       const int64_t take = std::min(b - done, s->chunk - s->staged);
-      host_copy_cols(c, s->stage_h[s->cur] + s->m * s->staged, s->m, blk + s->m * done, s->m, s->m, take);
+      host_copy_cols(c, s->stage_h[s->cur] + s->m * s->staged, s->m, blk + s->m * done, s->m, s->m, take,
+                     /*stream_dst=*/nt_staging());
       s->staged += take;
       done += take;
       if (s->staged == s->chunk) RF_TRY(sp_flush(s));

@@ -169,4 +169,6 @@ cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st);
 // *dst += *src (one thread; keeps scalar bookkeeping on the device).
 cudaError_t add_scalar(double* dst, const double* src, cudaStream_t st);
 
+// Copy into a buffer that is next read by a DMA engine only (non-temporal stores when the CPU has AVX2).
+void host_stream_copy(void* dst, const void* src, size_t bytes);
 }  // namespace rfgpu

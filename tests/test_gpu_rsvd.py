@@ -160,6 +160,35 @@ def test_rsvd_plain_power_mode_matches_oracle(ctx, port):
         assert abs(r1 - r2) <= 0.01 * r2
 
 
+def test_plain_mode_orth_runs_shifted_choleskyqr3(port):
+    """The plain power mode's sketch (A A^T) A G is far too ill-conditioned for CholeskyQR2 (kappa ~ 1e9 here)
+    but has full rank: orth takes the shifted CholeskyQR3 path (three Grams, no column-by-column work), keeps
+    every column like the reference's Gram-Schmidt (dense.cpp:402-431) and gives the reference's factors. An
+    exactly rank-deficient sketch is rejected by the same path and falls through to Gram-Schmidt, which
+    drops the reference's columns."""
+    sig = 1.0 / np.arange(1, 301, dtype=np.float64) ** 2
+    a = planted(port, 2000, 300, sig)
+    c = rf.Context(0)
+    c.profile(True)
+    try:
+        want = port.rsvd(a, 20, 10, 1, 7, False, False)
+        got = rf.rsvd(a, 20, 10, 1, 7, ctx=c)
+        n3, _ = c.profile_read("scholqr3")
+        assert n3 >= 1
+        assert got.D.shape == want.D.shape and rel(got.D, want.D).max() < 1e-6
+        r1, r2 = np.linalg.norm(a - recon(got)), np.linalg.norm(a - recon(want))
+        assert abs(r1 - r2) <= 0.01 * r2
+        assert np.abs(got.U.T @ got.U - np.eye(20)).max() < 1e-12
+        # exact rank 6 < l = 12: every path but Gram-Schmidt must refuse it
+        low = planted(port, 500, 200, np.array([5.0, 4.0, 3.0, 2.0, 1.0, 0.5]), seed=3)
+        c.profile_reset()
+        w2 = port.rsvd(low, 8, 4, 1, 7, False, False)
+        g2 = rf.rsvd(low, 8, 4, 1, 7, ctx=c)
+        assert g2.D.shape == w2.D.shape and rel(g2.D, w2.D).max() < 1e-6
+    finally:
+        c.close()
+
+
 def test_rsvd_deterministic(ctx, port):
     sig = geometric(10, 0.5)
     a = planted(port, 25, 20, sig, seed=2)
