@@ -803,11 +803,11 @@ bool host_is_pageable(const void* p) {
   return at.type == cudaMemoryTypeUnregistered;
 }
 
-// EXPERIMENT switch while measuring (RFGPU_STAGE_NT=0: glibc memcpy into the pinned slots)
-bool nt_staging() {
-  const char* e = std::getenv("RFGPU_STAGE_NT");
-  return !(e && e[0] == '0');
-}
+// Copies into the pinned slots use non-temporal stores (csrc/host_copy.cpp). Measured on the GPU box's host
+// (tools/microbench/hostcopy_nt.cu, 16 threads, 512 KB column chunks): glibc memcpy 48.6 GB/s alone and 36.9
+// GB/s while the copy engine reads the previous slot, non-temporal 68.8 / 45.8 GB/s; config 3 from pageable
+// memory 0.902 -> 0.887 s. The staging copy, not PCIe (55 GB/s), stays the bound of the pageable call.
+constexpr bool nt_staging() { return true; }
 
 Status stage_ring(rfgpu_ctx* c) {
   if (!c->stage_slots.empty()) return {};
