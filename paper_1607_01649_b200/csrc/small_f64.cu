@@ -1192,7 +1192,9 @@ cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double
       attr_done(cfg);
     }
     double* rdiag = work;  // c doubles
-    chol_kernel<<<1, kSmallThreads, smem, st>>>(G, ci, R, rdiag, info, info_d);
+    // one barrier per column step: fewer threads make it cheaper when the trailing update is small anyway
+    const int chol_threads = ci <= 64 ? 256 : ci <= 128 ? 512 : kSmallThreads;
+    chol_kernel<<<1, chol_threads, smem, st>>>(G, ci, R, rdiag, info, info_d);
     trinv_smem_kernel<8><<<(ci + 31) / 32, kSmallThreads, sizeof(double) * c * (c + 1) / 2, st>>>(R, ci, rdiag, Rinv);
     count_launch(2);
     return cudaGetLastError();
