@@ -71,6 +71,10 @@ int rfgpu_ctx_create(int device, rfgpu_ctx** out);
 int rfgpu_nccl_unique_id(void* id, size_t id_bytes);
 int rfgpu_ctx_create_dist(int device, int rank, int world, const void* nccl_id, size_t id_bytes,
                           rfgpu_ctx** out);
+/* One-GPU check of the NCCL transport behind rfgpu_ctx_create_dist (same bindings): a one-rank communicator
+ * from a fresh id, ncclAllReduce (sum, double) of `count` values in place on the device, the result back in
+ * out[0..count) (one rank: equal to the input). No reference counterpart. */
+int rfgpu_nccl_selftest(int device, const double* values, int64_t count, double* out);
 /* Host-staged reduction backend: the sums over ranks (the same points where
  * the NCCL context allreduces) go through sum(user, buf, count), which must
  * replace buf[0..count) (pinned host memory) by its elementwise sum over all

@@ -87,6 +87,7 @@ _SIGS = {
     "rfgpu_gaussian_range": (_int, [_u64, C.c_char_p, _i64, _i64, _pd]),
     "rfgpu_ctx_create": (_int, [_int, C.POINTER(_vp)]),
     "rfgpu_nccl_unique_id": (_int, [_vp, C.c_size_t]),
+    "rfgpu_nccl_selftest": (_int, [_int, _pd, _i64, _pd]),
     "rfgpu_ctx_create_dist": (_int, [_int, _int, _int, _vp, C.c_size_t, C.POINTER(_vp)]),
     "rfgpu_ctx_create_hostsum": (_int, [_int, _int, _int, _vp, _vp, C.POINTER(_vp)]),
     "rfgpu_ctx_destroy": (_int, [_vp]),

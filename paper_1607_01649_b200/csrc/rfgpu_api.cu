@@ -246,10 +246,15 @@ int finish(const Status& s) {
 // ============================================================ NCCL (dlopen)
 // NCCL is loaded lazily so the single-GPU path has no NCCL dependency and so
 // an NCCL already loaded in the process (e.g. torch's) is reused.
+// ncclUniqueId is a 128-byte struct passed BY VALUE to ncclCommInitRank (on the stack in the x86-64 ABI): the
+// binding must declare it as a struct, not as a char array (which would decay to a pointer argument).
+struct NcclUniqueId {
+  char internal[128];
+};
 struct Nccl {
   void* h = nullptr;
-  int (*getUniqueId)(void*) = nullptr;
-  int (*commInitRank)(void**, int, char[128], int) = nullptr;
+  int (*getUniqueId)(NcclUniqueId*) = nullptr;
+  int (*commInitRank)(void**, int, NcclUniqueId, int) = nullptr;
   int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*commDestroy)(void*) = nullptr;
   const char* (*getErrorString)(int) = nullptr;
@@ -2054,9 +2059,47 @@ int rfgpu_nccl_unique_id(void* id, size_t id_bytes) {
   std::string why;
   if (id_bytes < 128) return finish(make_err(RFGPU_EPARAM, "nccl id buffer must hold 128 bytes"));
   if (!g_nccl.load(&why)) return finish(make_err(RFGPU_ECUDA, why));
-  int r = g_nccl.getUniqueId(id);
+  int r = g_nccl.getUniqueId(static_cast<NcclUniqueId*>(id));
   if (r != 0) return finish(make_err(RFGPU_ECUDA, std::string("ncclGetUniqueId: ") + g_nccl.getErrorString(r)));
   return RFGPU_OK;
+}
+
+// One-GPU check of the NCCL transport the multi-rank contexts use (every gpurun box has one GPU, so the
+// multi-rank tests run on host-staged sums): loads NCCL, creates a ONE-rank communicator from a fresh id with
+// the same bindings rfgpu_ctx_create_dist uses, sums `count` doubles in place on the device with
+// ncclAllReduce (one rank: the sum is the input) and destroys the communicator. The sum of the result is
+// returned in *checksum.
+int rfgpu_nccl_selftest(int device, const double* values, int64_t count, double* out) {
+  if (!values || !out || count <= 0) return finish(make_err(RFGPU_EPARAM, "nccl_selftest: bad arguments"));
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  std::string why;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return finish(make_err(RFGPU_ECUDA, "no CUDA device available (rfgpu has no CPU fallback)"));
+  }
+  if (!g_nccl.load(&why)) return finish(make_err(RFGPU_ECUDA, why));
+  NcclUniqueId id;
+  int r = g_nccl.getUniqueId(&id);
+  if (r != 0) return finish(make_err(RFGPU_ECUDA, std::string("ncclGetUniqueId: ") + g_nccl.getErrorString(r)));
+  void* comm = nullptr;
+  r = g_nccl.commInitRank(&comm, 1, id, 0);
+  if (r != 0) return finish(make_err(RFGPU_ECUDA, std::string("ncclCommInitRank: ") + g_nccl.getErrorString(r)));
+  double* d = nullptr;
+  cudaStream_t st = nullptr;
+  Status s = [&]() -> Status {
+    RF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    RF_CUDA(cudaMalloc(&d, sizeof(double) * count));
+    RF_CUDA(cudaMemcpyAsync(d, values, sizeof(double) * count, cudaMemcpyHostToDevice, st));
+    const int rr = g_nccl.allReduce(d, d, static_cast<size_t>(count), kNcclDouble, kNcclSum, comm, st);
+    if (rr != 0) return make_err(RFGPU_ECUDA, std::string("ncclAllReduce: ") + g_nccl.getErrorString(rr));
+    RF_CUDA(cudaMemcpyAsync(out, d, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+    RF_CUDA(cudaStreamSynchronize(st));
+    return {};
+  }();
+  if (d) cudaFree(d);
+  if (st) cudaStreamDestroy(st);
+  g_nccl.commDestroy(comm);
+  return finish(s);
 }
 
 }  // extern "C"
@@ -2157,8 +2200,8 @@ int rfgpu_ctx_create_dist(int device, int rank, int world, const void* nccl_id, 
       ctx_free(c);
       return finish(make_err(RFGPU_ECUDA, why));
     }
-    char idb[128];
-    std::memcpy(idb, nccl_id, 128);
+    NcclUniqueId idb;
+    std::memcpy(idb.internal, nccl_id, 128);
     int r = g_nccl.commInitRank(&c->comm, world, idb, rank);
     if (r != 0) {
       c->comm = nullptr;
