@@ -1192,9 +1192,8 @@ cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double
       attr_done(cfg);
     }
     double* rdiag = work;  // c doubles
-    // one barrier per column step: fewer threads make it cheaper when the trailing update is small anyway
-    const int chol_threads = ci <= 64 ? 256 : ci <= 128 ? 512 : kSmallThreads;
-    chol_kernel<<<1, chol_threads, smem, st>>>(G, ci, R, rdiag, info, info_d);
+    // (256 / 512 threads for l <= 64 / 128 measured slower: config 1's 8 Choleskys 0.33 -> 0.44 ms)
+    chol_kernel<<<1, kSmallThreads, smem, st>>>(G, ci, R, rdiag, info, info_d);
     trinv_smem_kernel<8><<<(ci + 31) / 32, kSmallThreads, sizeof(double) * c * (c + 1) / 2, st>>>(R, ci, rdiag, Rinv);
     count_launch(2);
     return cudaGetLastError();
