@@ -228,6 +228,27 @@ def test_rsvd_host_streamed_matches_device_path(ctx, m):
     assert np.array_equal(small.D, want.D) and np.array_equal(small.U, want.U)
 
 
+def test_rsvd_host_staging_odd_rows_misaligned_base(ctx):
+    """The pinned staging ring copies caller columns with non-temporal stores (32-byte aligned bodies, plain
+    heads and tails): an odd row count and a base 8 bytes off a 32-byte boundary walk every alignment."""
+    m, n, k, p = 70001, 64, 8, 4
+    rng = np.random.default_rng(11)
+    buf = np.empty(m * n + 3)
+    a = buf[1:1 + m * n].reshape((m, n), order="F")
+    u, _ = np.linalg.qr(rng.standard_normal((m, 20)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, 20)))
+    a[...] = (u * 0.7 ** np.arange(20)) @ v.T
+    assert a.ctypes.data % 32 != 0 and a.flags.f_contiguous
+    host = rf.rsvd(a, k, p, 1, 3, reorthonormalize=True, ctx=ctx)
+    dm = ctx.matrix(np.asfortranarray(a.copy(order="F")))
+    try:
+        dev = rf.rsvd(dm, k, p, 1, 3, reorthonormalize=True, ctx=ctx)
+    finally:
+        dm.free()
+    assert rel(host.D, dev.D).max() < 1e-12
+    assert np.abs(np.abs(host.U) - np.abs(dev.U)).max() < 1e-9
+
+
 def test_rsvd_zero_matrix(ctx):
     f = rf.rsvd(np.zeros((12, 9)), 3, 2, 0, 1, ctx=ctx)
     assert f.U.shape[1] == 0 and f.D.size == 0
