@@ -1,5 +1,7 @@
-"""Config-3 passes (A X and A^T Q on the INT8 digit path, m=1048576, n=4096, l=220) timed alone under the
-current RFGPU_* environment: mean ms over 5 calls each, TOPS of the 28 digit products (l unpadded)."""
+"""Config-3 passes (A X and A^T Q on the INT8 digit path, m=1048576, n=4096, l=220) timed alone: mean ms over 5
+calls each, TOPS of the 28 digit products (l unpadded). This is the harness behind
+profiles/r02_pass_experiments.txt: each experiment there was a temporary RFGPU_OZAKI_* switch in csrc/ozaki.cu
+(printed in the line's prefix), run against the default in the same gpurun call and removed afterwards."""
 import os
 import sys
 
