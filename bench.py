@@ -22,7 +22,7 @@ timed region.
 
 After the timed region the run checks its own output (`parity`): the
 singular values against the golden values of the full-size oracle run
-(tests/golden/config_golden.json, from tools/parity_c3_full.py) and against
+(tests/golden/config_golden.json, from tests/fullsize/parity_config_full.py) and against
 the same call with the passes forced onto FP64 DMMA (RFGPU_OZAKI=0).
 
 --impl reference runs the reference's own CPU implementation (oracle/_ref,
@@ -207,8 +207,8 @@ def run_reference_rsvd(w, a_sample, threads):
 # column: small samples sit in host caches, config-size A does not): measured at 16 threads on the GPU box,
 # 8192 / 24576 / 65536 / 131072 / 262144 rows: 3.35 / 8.0 / 22.8 / 47.1 / 110.5 s
 # (gpurun_out r02b_refcurve16.json -> profiles/r02_reference_curve.json), and the FULL config-3 call once:
-# 560.2 s (tools/parity_config_full.py, profiles/r02_parity_c3.json); at the reference's default 8 threads
-# 709.4 s (tools/ref_full_time.py, profiles/r02_reference_c3_8threads.json). A linear fit through small samples
+# 560.2 s (tests/fullsize/parity_config_full.py, profiles/r02_parity_c3.json); at the reference's default 8 threads
+# 709.4 s (tests/fullsize/ref_full_time.py, profiles/r02_reference_c3_8threads.json). A linear fit through small samples
 # would claim ~300 s. The CPU numbers below are therefore anchored on that full-size measurement: every step
 # times the reference on an 8192-row sample of the workload and scales it by full / sample as measured
 # together on this box type.
@@ -267,7 +267,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden", "config_golden.json")
 
 def check_parity(args, w, kind, step, ctx, rank_out, Ud, Dd, Vd, Js, mloc, n):
     """The timed call's result against (1) the golden singular values / pivots of the full-size CPU oracle
-    run on the same A (tests/golden/config_golden.json, tools/parity_c3_full.py) and (2) the same call with
+    run on the same A (tests/golden/config_golden.json, tests/fullsize/parity_config_full.py) and (2) the same call with
     the passes forced onto FP64 DMMA (RFGPU_OZAKI=0; an independent product kernel). Outside the timed
     region."""
     import torch

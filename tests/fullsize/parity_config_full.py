@@ -14,7 +14,7 @@ Writes profiles/r02_parity_<workload>.json (deviations, timings) and merges
 the oracle's singular values / pivots into tests/golden/config_golden.json,
 which bench.py's self-check reads.
 
-usage: python tools/parity_config_full.py c3 [c5 c2 c4 ...]
+usage: python tests/fullsize/parity_config_full.py c3 [c5 c2 c4 ...]
 """
 from __future__ import annotations
 
@@ -25,7 +25,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import bench  # noqa: E402  (workload table and generator)
@@ -69,7 +69,7 @@ def run(workload, threads):
     port = get("port")
     ref.set_threads(threads)
     port.set_threads(threads)
-    gold = {"source": f"tools/parity_config_full.py {workload}: compiled reference (oracle/_ref) on the bench's A, "
+    gold = {"source": f"tests/fullsize/parity_config_full.py {workload}: compiled reference (oracle/_ref) on the bench's A, "
                       f"{threads} host threads"}
     if w["kind"] == "rsvd":
         got = rf.rsvd(A, k, p, q, 1, reorthonormalize=True)

@@ -1,11 +1,11 @@
 """Reference rsvd (compiled reference, oracle/_ref) wall time on row samples of the config-3 workload, for
-the CPU-baseline extrapolation: python tools/probe_ref_timing.py ROWS[,ROWS..] THREADS[,THREADS..] OUT.json"""
+the CPU-baseline extrapolation: python tests/fullsize/probe_ref_timing.py ROWS[,ROWS..] THREADS[,THREADS..] OUT.json"""
 import json
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import bench  # noqa: E402
 from oracle.oracle import get  # noqa: E402
 

@@ -1,5 +1,5 @@
 """Wall time of the compiled reference rsvd on the FULL config-3 matrix (the bench's A, generated on the device
-and copied to host memory) at a given host thread count: python tools/ref_full_time.py THREADS OUT.json"""
+and copied to host memory) at a given host thread count: python tests/fullsize/ref_full_time.py THREADS OUT.json"""
 import json
 import os
 import sys
@@ -8,7 +8,7 @@ import time
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import bench  # noqa: E402
 from oracle.oracle import get  # noqa: E402
 

@@ -17,9 +17,9 @@ for what in "${@:-tests bench}"; do
       timeout 1800 python -m pytest tests -m gpu -q -p no:randomly > gpurun_out/round2_pytest.log 2>&1
       echo "pytest rc=$?" >> gpurun_out/round2_pytest.log ;;
     parity)
-      timeout 3600 python tools/parity_config_full.py c3 c5 c2 c4 > gpurun_out/round2_parity.log 2>&1
+      timeout 3600 python tests/fullsize/parity_config_full.py c3 c5 c2 c4 > gpurun_out/round2_parity.log 2>&1
       cp profiles/r02_parity_*.json tests/golden/config_golden.json gpurun_out/ 2>/dev/null
-      timeout 2400 python tools/ref_full_time.py 8 gpurun_out/r02_reference_c3_8threads.json ;;
+      timeout 2400 python tests/fullsize/ref_full_time.py 8 gpurun_out/r02_reference_c3_8threads.json ;;
     bench)
       timeout 1200 python bench.py --steps 5 --warmup 3 > gpurun_out/round2_bench_c3.json 2> gpurun_out/round2_bench_c3.err
       for wl in c1 c2 c3plain c4 c4stream c5; do
@@ -30,6 +30,6 @@ for what in "${@:-tests bench}"; do
       bash tools/gpu_prof_r02.sh ;;
     host)
       /usr/local/cuda/bin/nvcc -O3 -o /tmp/hostcopy tools/microbench/hostcopy.cu && /tmp/hostcopy > gpurun_out/round2_hostcopy.txt 2>&1
-      timeout 900 python tools/probe_ref_timing.py 32768,65536,131072,262144 16 gpurun_out/round2_refcurve16.json ;;
+      timeout 900 python tests/fullsize/probe_ref_timing.py 32768,65536,131072,262144 16 gpurun_out/round2_refcurve16.json ;;
   esac
 done
