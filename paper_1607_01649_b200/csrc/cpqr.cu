@@ -562,9 +562,11 @@ cudaError_t cpqr_rank(double* W, int64_t ld, int m, int64_t n, int kmax, double 
 
 cudaError_t trinv_upper(const double* R, int64_t ldr, int k, double* Rinv, cudaStream_t st) {
   if (k <= 0) return cudaSuccess;
-  if (k > 352) return cudaErrorInvalidValue;
   const int nb = (k + kTB - 1) / kTB;
   const size_t smem = sizeof(double) * nb * kTB * (kTB + 1);
+  // the blocked kernel holds one block column in shared memory (k <= 736); the per-column kernel keeps a
+  // column in 11 registers per lane (k <= 352)
+  if (k > 352 && smem > 200 * 1024) return cudaErrorInvalidValue;
   if (k > 64 && smem <= 200 * 1024) {
     static std::atomic<uint64_t> cfg{0};
     if (attr_pending(cfg)) {

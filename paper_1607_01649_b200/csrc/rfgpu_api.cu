@@ -1521,6 +1521,9 @@ Status check_sample(const rfgpu_matrix* a, int64_t k, int64_t ell, const char* w
   if (k < 1) return make_err(RFGPU_EPARAM, std::string(where) + ": k must be at least 1");
   if (ell < k) return make_err(RFGPU_EPARAM, std::string(where) + ": p must be non-negative");
   if (ell > std::min(a->m_global, a->n)) return make_err(RFGPU_EPARAM, std::string(where) + ": k + p exceeds min(m, n)");
+  // the l x l factorizations (Cholesky / triangular inverse of the Gram matrices) hold a block column in one
+  // CTA's shared memory: l <= 736 (no such bound in the reference; reported as a parameter error, not a crash)
+  if (ell > 736) return make_err(RFGPU_EPARAM, std::string(where) + ": k + p above 736 is not supported on the device");
   return {};
 }
 
@@ -2421,6 +2424,7 @@ int rfgpu_range_finder(rfgpu_ctx* c, const rfgpu_matrix* a, const double* g, int
     if (q < 0) return make_err(RFGPU_EPARAM, "power_range: q must be non-negative");
     if (ell < 1 || ell > std::min(a->m_global, a->n))
       return make_err(RFGPU_EPARAM, "power_range: k + p exceeds min(m, n)");
+    if (ell > 736) return make_err(RFGPU_EPARAM, "power_range: k + p above 736 is not supported on the device");
     RF_TRY(ensure_device(c));
     cudaStream_t st = c->stream;
     const int64_t m = a->m, n = a->n, ldq = even(m);
@@ -3212,7 +3216,7 @@ int rfgpu_svd(rfgpu_ctx* c, const double* Mh, int64_t rows, int64_t cols, double
   CtxCall lk(c);
   Status st = [&]() -> Status {
     if (rows < cols) return make_err(RFGPU_EPARAM, "svd: device path expects rows >= cols (transpose wide input)");
-    if (cols < 1 || cols > 2048) return make_err(RFGPU_EPARAM, "svd: 1 <= cols <= 2048");
+    if (cols < 1 || cols > 736) return make_err(RFGPU_EPARAM, "svd: 1 <= cols <= 736 on the device");
     RF_TRY(ensure_device(c));
     cudaStream_t s = c->stream;
     DBuf M, U, S, V;

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "rfgpu_internal.h"
@@ -28,6 +29,7 @@ namespace rfgpu {
 namespace {
 
 constexpr int kSmallThreads = 1024;
+constexpr int kMaxSmallFactor = 736;  // the blocked triangular inverse's block column in shared memory (cpqr.cu)
 
 // ------------------------------------------------------------ chol_inv ---
 // One CTA, the packed upper triangle P (column-packed: (i, j) at
@@ -587,6 +589,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
 // cluster kernel 11.4 ms (9-10 sweeps each).
 
 constexpr double kJacobiDone = 1e-14;
+constexpr int kBJRegs = 14;    // register-resident cross rounds: rows and columns up to 32 * 14 = 448 ...
+constexpr int kBJRegsMin = 4;  // ... and from 97 (4 entries per lane) on
 
 struct BJParams {
   const double* X;  // mr x c input
@@ -660,7 +664,92 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
       // pairs (B rounds: column w of the first block with column (w + s) mod B
       // of the second), so each column pair is visited once per sweep.
       const bool full = r == 0 || !bj_cross_only;
-      const int nir = full ? 2 * kBJB - 1 : kBJB;
+      // Cross rounds with the warp's own column in REGISTERS: in the B cross rounds of a block round warp w
+      // always holds column w of the first block, so its X and V entries (rows lane, lane + 32, ...) are
+      // loaded once, rotated in registers and written back once; only the partner column goes through
+      // shared memory every round. The inner rounds are bound by shared-memory bandwidth (measured at
+      // l = 330: 24.2 of the 29.6 us of a block round, 317 KB per round through 128 B/clk): this cuts a
+      // round's traffic from 6 mr + 4 c to 2 mr + 2 c doubles per pair. Same operations in the same order:
+      // bitwise the shared-memory path, which tall inputs (rows or columns above 32 kBJRegs) and small ones
+      // (below 32 kBJRegsMin: l = 60 measured 0.80 ms in shared memory, 0.93 ms in registers) keep.
+      const int kneed = (max(mr, c) + 31) / 32;  // entries per lane of a column
+      auto cross_in_registers = [&](auto k_c) {
+        constexpr int K = decltype(k_c)::value;
+        const int u = warp;
+        double* xus = Xs + u * LX;
+        double* vus = Vs + u * LV;
+        double xu[K], vu[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int i = lane + 32 * k;
+          xu[k] = i < mr ? xus[i] : 0.0;
+          vu[k] = i < c ? vus[i] : 0.0;
+        }
+        for (int ir = 0; ir < kBJB; ++ir) {
+          const int v = kBJB + (warp + ir) % kBJB;
+          double* xv = Xs + v * LX;
+          double xvr[K];
+          double app = 0.0, aqq = 0.0, apq = 0.0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int i = lane + 32 * k;
+            if (i < mr) {
+              const double a = xu[k], b = xv[i];
+              xvr[k] = b;
+              app = fma(a, a, app);
+              aqq = fma(b, b, aqq);
+              apq = fma(a, b, apq);
+            } else {
+              xvr[k] = 0.0;
+            }
+          }
+          app = warp_sum(app);
+          aqq = warp_sum(aqq);
+          apq = warp_sum(apq);
+          if (app != 0.0 && aqq != 0.0 && !(apq * apq <= 1e-30 * (app * aqq))) {
+            const double zeta = (aqq - app) / (2.0 * apq);
+            const double t = (zeta < 0.0 ? -1.0 : 1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double cs = rsqrt(1.0 + t * t), sn = cs * t;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              const int i = lane + 32 * k;
+              if (i < mr) {
+                const double a = xu[k], b = xvr[k];
+                xu[k] = cs * a - sn * b;
+                xv[i] = sn * a + cs * b;
+              }
+            }
+            double* vv = Vs + v * LV;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              const int i = lane + 32 * k;
+              if (i < c) {
+                const double a = vu[k], b = vv[i];
+                vu[k] = cs * a - sn * b;
+                vv[i] = sn * a + cs * b;
+              }
+            }
+            if (lane == 0 && !(apq * apq <= kJacobiDone * kJacobiDone * (app * aqq))) s_rot = 1;
+          }
+          __syncthreads();
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int i = lane + 32 * k;
+          if (i < mr) xus[i] = xu[k];
+          if (i < c) vus[i] = vu[k];
+        }
+        __syncthreads();
+      };
+      const bool in_regs = !full && kneed <= kBJRegs && kneed >= kBJRegsMin;
+      if (in_regs) {
+        if (kneed <= 5) cross_in_registers(std::integral_constant<int, 5>{});
+        else if (kneed <= 7) cross_in_registers(std::integral_constant<int, 7>{});
+        else if (kneed <= 9) cross_in_registers(std::integral_constant<int, 9>{});
+        else if (kneed <= 11) cross_in_registers(std::integral_constant<int, 11>{});
+        else cross_in_registers(std::integral_constant<int, kBJRegs>{});
+      }
+      const int nir = in_regs ? 0 : (full ? 2 * kBJB - 1 : kBJB);
       for (int ir = 0; ir < nir; ++ir) {
         int u, v;
         if (full) {
@@ -1181,7 +1270,7 @@ cudaError_t chol_blocked(const double* G, int c, double* R, double* work, int* i
 cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double* work, int* info,
                      double* info_d, cudaStream_t st) {
   if (c <= 0) return cudaSuccess;
-  if (c > 352) return cudaErrorInvalidValue;
+  if (c > kMaxSmallFactor) return cudaErrorInvalidValue;  // callers check (rfgpu_max_sketch_width)
   const size_t smem = chol_smem_bytes(c);
   const int ci = static_cast<int>(c);
   if (smem <= 224 * 1024 && c <= 256) {

@@ -86,3 +86,26 @@ def test_dual_sketch_f32_entry_point(ctx):
     want_r = a64.T @ gr.astype(np.float64)
     assert np.max(np.abs(yc.reshape((m, ell), order="F") - want_c)) <= 1e-6 * np.max(np.abs(want_c))
     assert np.max(np.abs(yr.reshape((n, ell), order="F") - want_r)) <= 1e-6 * np.max(np.abs(want_r))
+
+
+def test_wide_sketches_beyond_352(port):
+    """l = k + p above 352 (the single-CTA triangular inverse's range) runs on the blocked l x l kernels up
+    to 736; above that the call is refused with the reference's parameter error class, not a CUDA failure."""
+    ctx = rf.Context(0)
+    try:
+        ell = 400
+        rng = np.random.default_rng(ell)
+        u, _ = np.linalg.qr(rng.standard_normal((2 * ell, ell)))
+        v, _ = np.linalg.qr(rng.standard_normal((ell, ell)))
+        a = np.asfortranarray((u * np.arange(1, ell + 1) ** -1.0) @ v.T)
+        f = rf.svd_dense(a, ctx=ctx)
+        s = np.linalg.svd(a, compute_uv=False)
+        assert np.max(np.abs(f.D - s) / s) < 1e-12
+        big = port.planted(3000, 1500, 1.0 / np.arange(1, 801) ** 1.2, 1)
+        got = rf.rsvd(big, 380, 20, 1, 7, reorthonormalize=True, ctx=ctx)
+        want = port.rsvd(big, 380, 20, 1, 7, False, True)
+        assert got.D.shape == want.D.shape and np.max(np.abs(got.D - want.D) / want.D) < 1e-10
+        with pytest.raises(rf.ParameterError):
+            rf.rsvd(port.planted(900, 800, 1.0 / np.arange(1, 801), 1), 730, 10, 0, 1, ctx=ctx)
+    finally:
+        ctx.close()
