@@ -125,6 +125,102 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   }
 }
 
+// The same factorization with the matrix in REGISTERS (c <= 128): the per-step update of chol_kernel moves
+// three doubles through shared memory per entry (c^3 / 2 in all: at l = 110 that is 5 MB through 128 B/clk,
+// as long as the arithmetic), so here the 32 x 32 thread grid owns the entries 2-D cyclically (thread (ti, tj):
+// rows ti + 32 a, columns tj + 32 b) and only the pivot row goes through shared memory (the contiguous
+// double-buffered copy, published by the threads that own row j + 1). Same operations on every entry in the
+// same order as chol_kernel: bitwise the same R, rdiag and gate statistics.
+template <int T>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    chol_reg_kernel(const double* __restrict__ G, int c, double* __restrict__ R, double* __restrict__ rdiag, int* info,
+                    double* info_d) {
+  extern __shared__ double sm[];
+  double* rowb = sm;          // [2][c] pivot rows (unscaled)
+  double* piv = sm + 2 * c;   // [c] pivots
+  const int tid = threadIdx.x, ti = tid & 31, tj = tid >> 5;
+  __shared__ double s_floor, s_trace, s_minratio;
+  double e[T][T];
+#pragma unroll
+  for (int b = 0; b < T; ++b)
+#pragma unroll
+    for (int a = 0; a < T; ++a) {
+      const int i = ti + 32 * a, col = tj + 32 * b;
+      e[a][b] = (i <= col && col < c) ? G[static_cast<int64_t>(col) * c + i] : 0.0;
+      if (i == 0 && col < c) rowb[col] = e[a][b];  // row 0
+    }
+  if (tj == 0) {
+    double mx = 0.0, tr = 0.0;
+    for (int j = ti; j < c; j += 32) {
+      const double g = G[static_cast<int64_t>(j) * c + j];
+      mx = fmax(mx, fabs(g));
+      tr += g;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    }
+    if (ti == 0) {
+      s_floor = 1e-14 * mx;
+      s_trace = tr;
+      s_minratio = INFINITY;
+    }
+  }
+  __syncthreads();
+  const double floor = s_floor, trace = s_trace;
+  int fail = 0;
+  for (int j = 0; j < c; ++j) {
+    const double* rj = rowb + (j & 1) * c;
+    double* rn = rowb + ((j + 1) & 1) * c;
+    const double d = rj[j];
+    if (d <= floor || !(d > 0.0)) {  // every thread sees the same pivot
+      fail = j + 1;
+      break;
+    }
+    if (tid == 0) {
+      s_minratio = fmin(s_minratio, trace > 0.0 ? d / trace : 0.0);
+      piv[j] = d;
+    }
+    const double inv_d = 1.0 / d;
+#pragma unroll
+    for (int b = 0; b < T; ++b) {
+      const int col = tj + 32 * b;
+      if (col > j && col < c) {
+        const double f = rj[col] * inv_d;
+#pragma unroll
+        for (int a = 0; a < T; ++a) {
+          const int i = ti + 32 * a;
+          if (i > j && i <= col) {
+            const double v = fma(-rj[i], f, e[a][b]);
+            e[a][b] = v;
+            if (i == j + 1) rn[col] = v;  // the next pivot row
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    info[0] = fail;
+    info_d[0] = s_minratio;
+  }
+  if (fail) return;
+  double* rs = rowb;  // sqrt of the pivots (the row buffers are free now)
+  for (int j = tid; j < c; j += blockDim.x) {
+    const double r = sqrt(piv[j]);
+    rs[j] = r;
+    rdiag[j] = 1.0 / r;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < T; ++b)
+#pragma unroll
+    for (int a = 0; a < T; ++a) {
+      const int i = ti + 32 * a, col = tj + 32 * b;
+      if (i < c && col < c) R[static_cast<int64_t>(col) * c + i] = i < col ? e[a][b] / rs[i] : (i == col ? rs[i] : 0.0);
+    }
+}
+
 // R^{-1} of the upper-triangular c x c R (c <= 236): each CTA stages the packed
 // upper triangle in shared memory, one warp per column j: back substitution
 // R x = e_j in axpy form, x over the lanes' registers (S slots), the pivots
@@ -1284,7 +1380,17 @@ cudaError_t chol_inv(const double* G, int64_t c, double* R, double* Rinv, double
     }
     double* rdiag = work;  // c doubles
     // (256 / 512 threads for l <= 64 / 128 measured slower: config 1's 8 Choleskys 0.33 -> 0.44 ms)
-    chol_kernel<<<1, kSmallThreads, smem, st>>>(G, ci, R, rdiag, info, info_d);
+    const size_t rsm = sizeof(double) * 3 * c;
+    if (ci <= 32)
+      chol_reg_kernel<1><<<1, kSmallThreads, rsm, st>>>(G, ci, R, rdiag, info, info_d);
+    else if (ci <= 64)
+      chol_reg_kernel<2><<<1, kSmallThreads, rsm, st>>>(G, ci, R, rdiag, info, info_d);
+    else if (ci <= 96)
+      chol_reg_kernel<3><<<1, kSmallThreads, rsm, st>>>(G, ci, R, rdiag, info, info_d);
+    else if (ci <= 128)
+      chol_reg_kernel<4><<<1, kSmallThreads, rsm, st>>>(G, ci, R, rdiag, info, info_d);
+    else
+      chol_kernel<<<1, kSmallThreads, smem, st>>>(G, ci, R, rdiag, info, info_d);
     trinv_smem_kernel<8><<<(ci + 31) / 32, kSmallThreads, sizeof(double) * c * (c + 1) / 2, st>>>(R, ci, rdiag, Rinv);
     count_launch(2);
     return cudaGetLastError();
