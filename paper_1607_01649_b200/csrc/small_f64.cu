@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) jacobi_svd_kernel(const Jaco
 
 constexpr double kJacobiDone = 1e-14;
 constexpr int kBJRegs = 14;    // register-resident cross rounds: rows and columns up to 32 * 14 = 448 ...
-constexpr int kBJRegsMin = 4;  // ... and from 97 (4 entries per lane) on
+constexpr int kBJRegsMin = 1;  // ... and every smaller size (the register count is a template argument: exact fit)
 
 struct BJParams {
   const double* X;  // mr x c input
@@ -766,8 +766,9 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
       // shared memory every round. The inner rounds are bound by shared-memory bandwidth (measured at
       // l = 330: 24.2 of the 29.6 us of a block round, 317 KB per round through 128 B/clk): this cuts a
       // round's traffic from 6 mr + 4 c to 2 mr + 2 c doubles per pair. Same operations in the same order:
-      // bitwise the shared-memory path, which tall inputs (rows or columns above 32 kBJRegs) and small ones
-      // (below 32 kBJRegsMin: l = 60 measured 0.80 ms in shared memory, 0.93 ms in registers) keep.
+      // bitwise the shared-memory path, which tall inputs (rows or columns above 32 kBJRegs) keep. The register
+      // count per lane is a template argument (2 .. 14): with 14 for every size l = 60 ran 0.93 ms against 0.80
+      // ms in shared memory, with the exact count 0.63 ms.
       const int kneed = (max(mr, c) + 31) / 32;  // entries per lane of a column
       auto cross_in_registers = [&](auto k_c) {
         constexpr int K = decltype(k_c)::value;
@@ -839,7 +840,9 @@ __global__ void __launch_bounds__(32 * kBJB, 1) bjacobi_kernel(const BJParams p0
       };
       const bool in_regs = !full && kneed <= kBJRegs && kneed >= kBJRegsMin;
       if (in_regs) {
-        if (kneed <= 5) cross_in_registers(std::integral_constant<int, 5>{});
+        if (kneed <= 2) cross_in_registers(std::integral_constant<int, 2>{});
+        else if (kneed <= 3) cross_in_registers(std::integral_constant<int, 3>{});
+        else if (kneed <= 5) cross_in_registers(std::integral_constant<int, 5>{});
         else if (kneed <= 7) cross_in_registers(std::integral_constant<int, 7>{});
         else if (kneed <= 9) cross_in_registers(std::integral_constant<int, 9>{});
         else if (kneed <= 11) cross_in_registers(std::integral_constant<int, 11>{});
