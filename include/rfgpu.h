@@ -133,7 +133,9 @@ int rfgpu_multiply(rfgpu_ctx* ctx, const rfgpu_matrix* a, int trans, const doubl
  * Outputs: Q (m_local x ell_out, caller allocates m_local*ell), B (ell_out x n,
  * caller allocates ell*n), *resid = ||A - Q B||_F by down-dating
  * (frob_residual, :45-54), *ell_out = kept columns (orth may drop). Any of
- * Q/B/resid may be NULL. */
+ * Q/B/resid may be NULL.
+ * Device-path limit (all sketching entry points): ell = k + p <= 736, else
+ * RFGPU_EPARAM (the reference has no such bound). */
 int rfgpu_range_finder(rfgpu_ctx* ctx, const rfgpu_matrix* a, const double* g, int64_t ell, int64_t q, int reorth,
                        double* Q, double* B, double* resid, int64_t* ell_out);
 
