@@ -56,3 +56,21 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(rf.DeviceError):
         rf.Context(0)
+
+
+def test_staging_copy_non_temporal_paths():
+    """csrc/host_copy.cpp: the pinned ring's staging copy (AVX-512 / AVX2 non-temporal stores with plain heads
+    and tails, memcpy below 4 KB) at every destination alignment and odd lengths. CPU only."""
+    import ctypes as C
+    lib = rf.lib()
+    fn = getattr(lib, "_ZN5rfgpu16host_stream_copyEPvPKvm")
+    fn.restype = None
+    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    rng = np.random.default_rng(3)
+    src = rng.integers(0, 256, size=(1 << 20) + 64, dtype=np.uint8)
+    for off in (0, 1, 8, 31, 33, 63):
+        for n in (0, 1, 100, 4095, 4096, 4097, 70001, 1 << 20):
+            dst = np.zeros(n + off + 64, dtype=np.uint8)
+            fn(dst.ctypes.data + off, src.ctypes.data + 5, n)
+            assert np.array_equal(dst[off:off + n], src[5:5 + n])
+            assert not dst[:off].any() and not dst[off + n:].any()
