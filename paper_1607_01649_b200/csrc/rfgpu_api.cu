@@ -810,10 +810,11 @@ bool host_is_pageable(const void* p) {
 
 // Copies into the pinned slots use non-temporal stores (csrc/host_copy.cpp). Measured on the GPU box's host
 // (tools/microbench/hostcopy_nt.cu, 16 threads, 512 KB column chunks): glibc memcpy 48.6 GB/s alone and 36.9
-// GB/s while the copy engine reads the previous slot, non-temporal 68.8 / 45.8 GB/s (AVX2), 76.2 / 48.8 GB/s
-// (AVX-512); config 3 from pageable memory 0.902 -> 0.887 s with AVX2. The staging copy and the DMA slow each
-// other down (the DMA alone reaches 55 GB/s, 48-49 GB/s beside the copy): that contention, not PCIe, bounds
-// the pageable call.
+// GB/s while the copy engine reads the previous slot, non-temporal 68.8 / 45.8 GB/s; config 3 from pageable
+// memory 0.902 -> 0.887 s. (64-byte AVX-512 stores: 48.8 GB/s in the microbenchmark, but the call itself
+// 0.881 / 0.946 s against 0.886 / 0.890 s with AVX2 on one box: not kept.) The staging copy and the DMA slow
+// each other down (the DMA alone reaches 55 GB/s, 48-49 GB/s beside the copy): that contention, not PCIe,
+// bounds the pageable call.
 constexpr bool nt_staging() { return true; }
 
 Status stage_ring(rfgpu_ctx* c) {
